@@ -1,0 +1,158 @@
+/*
+ * psb200.h -- C ABI of libpsb200.so, the sm_100a implementation of the
+ * ProxSkip / PDHGSkip TV hot path (arXiv 2411.00688).
+ *
+ * The reference (`imgskip`, pure Python) has no FFI: its drop-in surface is
+ * the duck-typed Python API listed in SURVEY.md 8(b).  Each entry point below
+ * names the reference function it replaces (paths relative to
+ * /root/reference/pkg/src/imgskip).  The Python package
+ * `paper_2411_00688_b200` binds these symbols with ctypes and re-exposes the
+ * reference's names and signatures (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every function returns PSB_OK (0) or a PSB_ERR_* status; the message is
+ *     available from psb_last_error() (thread-local).
+ *   - device buffers are plain device pointers; sizes are element counts;
+ *     `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - layouts follow the reference: image (H, W) row-major; dual field
+ *     (2, H, W) with channel 0 = row (vertical) differences (tensor.py:80-106,
+ *     operators.py:44-57); sinogram (n_angles, n_bins) (tensor.py:109-127).
+ *     A batch of problems is the same layout repeated with a per-problem
+ *     stride ("pstride", in elements).
+ *   - FGP dual state: each problem owns three dual "slots" of (2, H, W)
+ *     (q_pstride >= 6*H*W); the warm start q_warm (tv.py:25-50) lives in
+ *     slot 0 between prox calls, inner iteration `it` reads slots it%3 and
+ *     (it+2)%3 and writes slot (it+1)%3, and the finalize step moves the last
+ *     iterate back to slot 0.
+ *   - dtype codes: PSB_F32 (production) or PSB_F64 (bit-exact debug path:
+ *     every op rounded separately, matching numpy).
+ */
+#ifndef PSB200_H_
+#define PSB200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSB_ABI_VERSION 1
+
+#define PSB_OK 0
+#define PSB_ERR_VALUE 1    /* maps to ValueError */
+#define PSB_ERR_CUDA 2     /* maps to RuntimeError */
+#define PSB_ERR_DIVERGED 3 /* maps to DivergenceError (errors.py:4-11) */
+
+#define PSB_F32 0
+#define PSB_F64 1
+
+int psb_abi_version(void);
+const char* psb_last_error(void);
+int psb_device_sm_count(int* out);
+
+/* ---- finite differences: operators.py:44-57 (grad_forward), :60-71 (divergence) */
+int psb_grad2d(int dtype, const void* u, void* g, int64_t n, int H, int W, void* stream);
+int psb_div2d(int dtype, const void* q, void* d, int64_t n, int H, int W, void* stream);
+
+/* ---- pointwise proxes: proximal.py:10-21 (project_ball), :39-41 (project_nonneg) */
+int psb_project_ball2d(int dtype, const void* q, void* out, int64_t n, int64_t HW, double radius,
+                       void* stream);
+int psb_project_nonneg(int dtype, const void* u, void* out, int64_t count, void* stream);
+
+/* ---- generic elementwise building block for the drivers' vector algebra
+ * (skip.py:66-74, solvers.py:139-206 with user-supplied closures):
+ * out = (a*x) + (b*y), each product rounded separately; a == 1 skips the
+ * first product, y == NULL drops the second term. */
+int psb_lincomb(int dtype, double a, const void* x, double b, const void* y, void* out,
+                int64_t count, void* stream);
+
+/* ---- FGP TV prox, tv.py:53-89 -------------------------------------------
+ * psb_fgp2d_iter: ONE inner iteration (tv.py:75-80) for every problem in
+ *   `active` (device int32[n_active]; NULL = problems 0..n_active-1):
+ *     y   = q_it + beta_prev * (q_it - q_{it-1})        (recomputed, not stored)
+ *     q'  = P_w(y + step * grad(clamp(x + div y)))        -> slot (it+1)%3
+ *   At it == 0 the warm start is re-projected onto the new ball first when the
+ *   problem's reproject flag is set (tv.py:68-69).  `weights` (device double,
+ *   one per ACTIVE-LIST POSITION) overrides `weight` when non-NULL; likewise
+ *   `reproject` (device uint8 per active-list position) overrides
+ *   `reproject_all`.
+ * psb_fgp2d_finalize: u = clamp(x + div q_n) (tv.py:89) and q_n -> slot 0.
+ * psb_tv_prox2d: the whole prox (re-projection, n_inner iterations with the
+ *   Beck-Teboulle beta table computed in double on the host, finalize).
+ *   accelerated = 0 runs the plain projected-gradient branch (tv.py:82-84). */
+int psb_fgp2d_iter(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
+                   const int32_t* active, int n_active, double weight, const double* weights,
+                   int reproject_all, const uint8_t* reproject, int H, int W, int it,
+                   double beta_prev, double step, int nonneg, void* stream);
+int psb_fgp2d_finalize(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
+                       const int32_t* active, int n_active, int H, int W, int n_inner, int nonneg,
+                       void* u, int64_t u_pstride, void* stream);
+int psb_tv_prox2d(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
+                  const int32_t* active, int n_active, double weight, const double* weights,
+                  int reproject_all, const uint8_t* reproject, int H, int W, int n_inner,
+                  int accelerated, int nonneg, double step, void* u, int64_t u_pstride,
+                  void* stream);
+
+/* ---- reductions (fp64 accumulation, deterministic two-pass) ---------------
+ * per-problem results are written to the DEVICE array out[n].
+ * psb_sumsq: sum((a-b)^2) (b may be NULL) -- tensor.py:28-30, 42-51 building block
+ * psb_dot:   sum(a*b)                      -- tensor.py:17-25
+ * psb_tv2d:  isotropic TV, tv.py:19-22
+ * psb_count_nonfinite: number of non-finite entries (solvers.py:111-113) */
+int psb_sumsq(int dtype, const void* a, const void* b, int64_t n, int64_t len, double* out,
+              void* stream);
+int psb_dot(int dtype, const void* a, const void* b, int64_t n, int64_t len, double* out,
+            void* stream);
+int psb_tv2d(int dtype, const void* u, int64_t n, int H, int W, double* out, void* stream);
+int psb_count_nonfinite(int dtype, const void* a, int64_t count, double* out, void* stream);
+
+/* ---- ProxSkip outer step, skip.py:46-79 -------------------------------------
+ * State x, h (dtype_outer) and prox input z (dtype_fgp), all (n, H, W).
+ * `g_or_b`: when ident != 0 it is b and the gradient x - b of the identity
+ * fidelity (problems.py:121, operators.py:297-307) is fused; otherwise it is
+ * the precomputed gradient g = A^T(Ax - b).
+ * psb_proxskip_pre: for every problem i: if coins[i]:
+ *      z = (x - gamma g) + hcoef h            (hcoef = gamma - gamma/p)
+ *   else (skipped, h unchanged):
+ *      x = (x - gamma g) + gamma h
+ *   coins: device uint8[n] (NULL = all fire, e.g. PGD).
+ * psb_proxskip_post (coin-fired problems in `active`): fused FGP finalize
+ *   u = clamp(z + div q_n), q_n -> slot 0, then
+ *      xhat = (x - gamma g) + gamma h ; h += pg * (u - xhat) ; x = u   (pg = p/gamma)
+ * Non-finite iterates record min(bad_iter[i], k) (device int32[n]) so the
+ * host can raise DivergenceError(k) (solvers.py:111-113). */
+int psb_proxskip_pre(int dtype_outer, int dtype_fgp, void* x, const void* g_or_b, int ident,
+                     const void* h, void* z, int64_t n, int64_t HW, const uint8_t* coins,
+                     double gamma, double hcoef, int32_t* bad_iter, int k, void* stream);
+int psb_proxskip_post(int dtype_outer, int dtype_fgp, void* x, const void* g_or_b, int ident,
+                      void* h, const void* z, void* q, int64_t q_pstride, const int32_t* active,
+                      int n_active, int H, int W, int n_inner, int nonneg, double gamma, double pg,
+                      int32_t* bad_iter, int k, void* stream);
+
+/* ---- fused run drivers (the native runtime) ---------------------------------
+ * psb_proxskip_denoise_run: K outer ProxSkip iterations of the implicit TV
+ *   denoising problem (identity fidelity; problems.py:117-132 + skip.py:46-79)
+ *   for n independent problems.  coins_host: host uint8[K * n] (row k =
+ *   iteration k, the per-problem Philox streams drawn by the caller,
+ *   skip.py:27-28).  last_weight_host: host double[n], NaN = never called
+ *   (TvProxState.last_weight = None).  On return last_weight_host is updated
+ *   and prox_count_host[n] (host int64) holds the prox calls per problem.
+ *   use_graph != 0 captures the launch sequence into one CUDA graph.
+ *   elapsed_host (nullable, host double[K]) receives the device time in
+ *   seconds from the run start to the end of each outer iteration
+ *   (IterationLog.elapsed_s, solvers.py:84-86), from CUDA events.
+ *   fgp_time_host (nullable, host double[K]) receives the device time of the
+ *   FGP inner-iteration burst of each outer iteration (0 when no coin fired),
+ *   for the benchmark's roofline accounting. */
+int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
+                             void* z, void* q, int64_t n, int H, int W, const uint8_t* coins_host,
+                             int K, double gamma, double p, double alpha, int n_inner,
+                             int accelerated, int nonneg, double* last_weight_host,
+                             int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
+                             double* elapsed_host, double* fgp_time_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSB200_H_ */

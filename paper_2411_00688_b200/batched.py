@@ -1,0 +1,120 @@
+"""Batched ProxSkip TV denoising (BASELINE config 4).
+
+The reference has no batch API: config 4 is 4096 independent
+``build_tv_recon(identity_map, b_i, alpha, inner_budget=50)`` +
+``run_proxskip(..., SkipConfig(p, seed_i), K)`` problems.  Here they live in
+one set of device buffers -- x, h, b, z: (N, H, W); dual slots (N, 3, 2, H, W)
+-- and advance together: every outer iteration launches one fused pre kernel
+over all N problems, the FGP inner iterations over the compacted list of
+coin-fired problems only (each problem keeps its own Philox coin stream), and
+one post kernel over that list.  Per-problem semantics (coins, warm starts,
+last_weight re-projection, inner-iteration counters) equal N separate
+reference runs; tests/test_gpu_parity.py checks sampled problems against the
+oracle.  Multi-GPU: problems are sharded across ranks with no collective
+(``shard_indices``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _arrays as AR
+from . import _lib as L
+from .errors import DivergenceError
+from .skip import INT32_MAX, SkipConfig
+from .tv import PRECISIONS
+
+
+def shard_indices(n_total, rank, world):
+    """Contiguous block of problem indices owned by ``rank`` (weak-free, no exchange)."""
+    per = (n_total + world - 1) // world
+    lo = min(n_total, rank * per)
+    return np.arange(lo, min(n_total, lo + per))
+
+
+def coin_table(p, seeds, iters):
+    """(iters, N) uint8: column i is SkipConfig(p, seeds[i]).coins(iters)."""
+    return np.ascontiguousarray(np.stack([SkipConfig(p, int(s)).coins(iters) for s in seeds], axis=1))
+
+
+class BatchedTvDenoise:
+    """N independent 0.5||u - b_i||^2 + alpha TV(u) problems on one GPU."""
+
+    def __init__(self, b, alpha, inner_budget=50, *, precision="fp32", accelerated=True,
+                 nonneg=False):
+        if alpha <= 0:
+            raise ValueError("alpha must be positive")
+        if inner_budget < 1:
+            raise ValueError("inner_budget must be >= 1")
+        dto, dtf = PRECISIONS[precision]
+        self.b = AR.to_dev(b, dto)
+        if self.b.dim() != 3:
+            raise ValueError(f"expected (N, H, W) data, got {tuple(self.b.shape)}")
+        self.n, self.H, self.W = self.b.shape
+        self.alpha = alpha
+        self.inner_iters = inner_budget
+        self.accelerated = accelerated
+        self.nonneg = nonneg
+        self.dto, self.dtf = dto, dtf
+        self.x = torch.zeros_like(self.b)
+        self.h = torch.zeros_like(self.b)
+        self.z = torch.empty((self.n, self.H, self.W), dtype=dtf, device="cuda")
+        self.slots = torch.zeros((self.n, 3, 2, self.H, self.W), dtype=dtf, device="cuda")
+        self.last_weight = np.full(self.n, np.nan)
+        self.prox_count = np.zeros(self.n, dtype=np.int64)
+        self.bad = torch.full((self.n,), INT32_MAX, dtype=torch.int32, device="cuda")
+        self.elapsed = None
+
+    def reset(self, x0=None, h0=None):
+        """Cold start: zero warm starts and counters (harness.py:283-286 semantics)."""
+        if x0 is None:
+            self.x.zero_()
+        else:
+            self.x.copy_(AR.to_dev(x0, self.dto))
+        if h0 is None:
+            self.h.zero_()
+        else:
+            self.h.copy_(AR.to_dev(h0, self.dto))
+        self.slots.zero_()
+        self.last_weight[:] = np.nan
+        self.prox_count[:] = 0
+        self.bad.fill_(INT32_MAX)
+
+    @property
+    def total_inner_iterations(self):
+        return self.prox_count * self.inner_iters
+
+    def run_proxskip(self, coins, gamma=1.0, p=0.1, *, use_graph=False, record_elapsed=False,
+                     fgp_time=None):
+        """K outer iterations; ``coins`` is the (K, N) table of ``coin_table``."""
+        coins = np.ascontiguousarray(coins, dtype=np.uint8)
+        K = coins.shape[0]
+        if coins.shape[1] != self.n:
+            raise ValueError("coin table does not match the batch")
+        self.elapsed = np.zeros(max(K, 1)) if record_elapsed else None
+        L.call("psb_proxskip_denoise_run", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
+               L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), L.ptr(self.slots), self.n, self.H,
+               self.W, coins.ctypes.data_as(L.C.c_void_p), K, float(gamma), float(p),
+               float(self.alpha), self.inner_iters, int(self.accelerated), int(self.nonneg),
+               self.last_weight.ctypes.data_as(L.C.c_void_p),
+               self.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(self.bad), int(bool(use_graph)),
+               self.elapsed.ctypes.data_as(L.C.c_void_p) if record_elapsed else None,
+               fgp_time.ctypes.data_as(L.C.c_void_p) if fgp_time is not None else None,
+               L.stream())
+        return self.x
+
+    def check_finite(self):
+        bad = self.bad.cpu().numpy()
+        hit = np.nonzero(bad != INT32_MAX)[0]
+        if hit.size:
+            raise DivergenceError(int(bad[hit].min()), f"proxskip[problem {int(hit[0])}]")
+
+
+def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.0,
+                         precision="fp32", use_graph=False):
+    """Config-4 entry point: returns (x, prox_counts) as the input currency."""
+    solver = BatchedTvDenoise(b, alpha, inner_budget, precision=precision)
+    solver.run_proxskip(coin_table(p, seeds, iters), gamma, p, use_graph=use_graph)
+    solver.check_finite()
+    return AR.like(solver.x, b), solver.prox_count.copy()

@@ -1,0 +1,129 @@
+// Shared device/host helpers for libpsb200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+#include <cmath>
+#include <algorithm>
+
+#include "../../include/psb200.h"
+
+namespace psb {
+
+// ---- error reporting (psb_last_error) ---------------------------------------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+
+#define PSB_CUDA(call)                                                             \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return ::psb::fail(PSB_ERR_CUDA, std::string(#call) + ": " +                 \
+                                           cudaGetErrorString(e_));                \
+  } while (0)
+
+#define PSB_LAUNCHED(name)                                                         \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return ::psb::fail(PSB_ERR_CUDA, std::string(name) + " launch: " +           \
+                                           cudaGetErrorString(e_));                \
+  } while (0)
+
+#define PSB_REQUIRE(cond, msg)                                                     \
+  do {                                                                             \
+    if (!(cond)) return ::psb::fail(PSB_ERR_VALUE, msg);                           \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// ---- arithmetic -------------------------------------------------------------
+// The double instantiation must round every operation separately, exactly like
+// numpy (SURVEY 8(c+)): use the _rn intrinsics, which ptxas never contracts
+// into FMA.  The float instantiation is the production path and may contract.
+template <class T> struct Ar;
+
+template <> struct Ar<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
+  // proximal.py:19-21: r * q / max(r, |q|), |q| = sqrt(a*a + b*b), no FMA.
+  static __device__ __forceinline__ double ball_scale(double a, double b, double r) {
+    double m = __dsqrt_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)));
+    return __ddiv_rn(r, fmax(r, m));
+  }
+  static __device__ __forceinline__ double ball_scale3(double a, double b, double c, double r) {
+    double m = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
+    return __ddiv_rn(r, fmax(r, m));
+  }
+};
+
+template <> struct Ar<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
+  // Same projection with one MUFU: scale = 1 inside the ball, r/|q| outside.
+  static __device__ __forceinline__ float ball_scale(float a, float b, float r) {
+    float m2 = fmaf(a, a, b * b);
+    return m2 > r * r ? r * rsqrtf(m2) : 1.0f;
+  }
+  static __device__ __forceinline__ float ball_scale3(float a, float b, float c, float r) {
+    float m2 = fmaf(a, a, fmaf(b, b, c * c));
+    return m2 > r * r ? r * rsqrtf(m2) : 1.0f;
+  }
+};
+
+// ---- vector loads -----------------------------------------------------------
+template <class T, int V> struct Vec { T v[V]; };
+
+template <class T, int V>
+__device__ __forceinline__ void ldv(T (&d)[V], const T* p) {
+  if constexpr (sizeof(T) * V == 16) {
+    float4 r = __ldg(reinterpret_cast<const float4*>(p));
+    const T* s = reinterpret_cast<const T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+  } else if constexpr (sizeof(T) * V == 8) {
+    float2 r = __ldg(reinterpret_cast<const float2*>(p));
+    const T* s = reinterpret_cast<const T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = __ldg(p + i);
+  }
+}
+
+// Vector store (the kernels never re-read what they write in the same launch,
+// so all loads above may use the read-only path).
+template <class T, int V>
+__device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
+  if constexpr (sizeof(T) * V == 16) {
+    float4 r;
+    T* d = reinterpret_cast<T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+    *reinterpret_cast<float4*>(p) = r;
+  } else if constexpr (sizeof(T) * V == 8) {
+    float2 r;
+    T* d = reinterpret_cast<T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+    *reinterpret_cast<float2*>(p) = r;
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) p[i] = s[i];
+  }
+}
+
+template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
+
+}  // namespace psb

@@ -1,0 +1,211 @@
+// Native run driver for ProxSkip TV denoising (BASELINE configs 1 and 4).
+//
+// The Bernoulli coins of every problem and iteration are known before the run
+// (drawn on the host from the reference's Philox streams, skip.py:27-28), so
+// the driver resolves the control flow up front: it compacts the coin table
+// into per-iteration active lists, uploads them once, and enqueues
+//     pre(all problems) -> n_inner x fgp2d_iter(active) -> post(active)
+// per outer iteration without any host synchronisation.  With use_graph the
+// whole launch sequence is captured into one CUDA graph first (a 256^2 FGP
+// iteration is only a few microseconds of GPU work, so launch cost matters).
+#include <climits>
+
+#include "common.cuh"
+
+namespace psb {
+
+int fgp2d_iter(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
+               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
+               int H, int W, int it, double beta, double step, int nonneg, cudaStream_t st);
+int proxskip_pre(int dto, int dtf, void* x, const void* gb, int ident, const void* h, void* z,
+                 int64_t n, int64_t HW, const uint8_t* coins, double gamma, double hcoef,
+                 int32_t* bad, int k, cudaStream_t st);
+int proxskip_post(int dto, int dtf, void* x, const void* gb, int ident, void* h, const void* z,
+                  void* q, int64_t qps, const int32_t* active, int n_active, int H, int W,
+                  int n_inner, int nonneg, double gamma, double pg, int32_t* bad, int k,
+                  cudaStream_t st);
+void fista_betas(int n, double* out);
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void* z, void* q,
+                         int64_t n, int H, int W, const uint8_t* coins_host, int K, double gamma,
+                         double p, double alpha, int n_inner, int accelerated, int nonneg,
+                         double* last_weight, int64_t* prox_count, int32_t* bad, int use_graph,
+                         double* elapsed, double* fgp_time, cudaStream_t user_stream) {
+  PSB_REQUIRE(gamma > 0, "run_proxskip: gamma must be positive");
+  PSB_REQUIRE(p > 0 && p <= 1, "SkipConfig: p must be in (0, 1]");
+  PSB_REQUIRE(alpha > 0, "build_tv_recon: alpha must be positive");
+  PSB_REQUIRE(n_inner >= 1, "TvProxState: inner_iters must be >= 1");
+  PSB_REQUIRE(H >= 2 && W >= 2, "grad_forward: need a 2-D grid with both sides >= 2");
+  PSB_REQUIRE(n >= 1 && n <= 65535, "proxskip run: batch size out of range");
+  if (K <= 0) return PSB_OK;
+  const int64_t HW = (int64_t)H * W;
+  const int64_t qps = 6 * HW;
+  // skip.py:64,70,74 -- scalars formed in double exactly as the reference does
+  const double hcoef = gamma - gamma / p;
+  const double weight = (gamma / p) * alpha;  // prox_g(u, gamma/p) -> tv_prox(u, step*alpha)
+  const double pg = p / gamma;
+
+  // Active lists + per-entry reprojection flags (tv.py:68-69 fires only on the
+  // first call of this run whose weight differs from the stored last_weight).
+  std::vector<int32_t> act;
+  std::vector<uint8_t> rep;
+  std::vector<int64_t> off(K + 1, 0);
+  std::vector<uint8_t> seen(n, 0);
+  act.reserve((size_t)(K * n * p * 1.2) + 16);
+  for (int k = 0; k < K; ++k) {
+    for (int64_t i = 0; i < n; ++i) {
+      if (!coins_host[(int64_t)k * n + i]) continue;
+      act.push_back((int32_t)i);
+      const double lw = last_weight[i];
+      uint8_t r = 0;
+      if (!seen[i]) {
+        r = (!std::isnan(lw) && lw != weight) ? 1 : 0;
+        seen[i] = 1;
+      }
+      rep.push_back(r);
+      prox_count[i] += 1;
+    }
+    off[k + 1] = (int64_t)act.size();
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (seen[i]) last_weight[i] = weight;
+
+  std::vector<double> beta(n_inner, 0.0);
+  if (accelerated) fista_betas(n_inner, beta.data());
+
+  DevBuf d_coins, d_act, d_rep;
+  PSB_CUDA(cudaMalloc(&d_coins.p, (size_t)K * n));
+  PSB_CUDA(cudaMemcpy(d_coins.p, coins_host, (size_t)K * n, cudaMemcpyHostToDevice));
+  if (!act.empty()) {
+    PSB_CUDA(cudaMalloc(&d_act.p, act.size() * sizeof(int32_t)));
+    PSB_CUDA(cudaMalloc(&d_rep.p, rep.size()));
+    PSB_CUDA(cudaMemcpy(d_act.p, act.data(), act.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    PSB_CUDA(cudaMemcpy(d_rep.p, rep.data(), rep.size(), cudaMemcpyHostToDevice));
+  }
+  const uint8_t* coins_d = static_cast<const uint8_t*>(d_coins.p);
+  const int32_t* act_d = static_cast<const int32_t*>(d_act.p);
+  const uint8_t* rep_d = static_cast<const uint8_t*>(d_rep.p);
+
+  // Graph capture needs a capturable (non-legacy) stream: run on a private
+  // stream ordered after / before the caller's stream with events.
+  cudaStream_t st = user_stream;
+  cudaStream_t priv = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  if (use_graph) {
+    PSB_CUDA(cudaStreamCreateWithFlags(&priv, cudaStreamNonBlocking));
+    PSB_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    PSB_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    PSB_CUDA(cudaEventRecord(ev_in, user_stream));
+    PSB_CUDA(cudaStreamWaitEvent(priv, ev_in, 0));
+    st = priv;
+    PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  }
+
+  std::vector<cudaEvent_t> evs;
+  if (elapsed) {
+    evs.resize(K + 1, nullptr);
+    for (auto& e : evs) PSB_CUDA(cudaEventCreate(&e));
+    PSB_CUDA(cudaEventRecord(evs[0], st));
+  }
+  // optional per-iteration timing of the FGP burst (bench roofline)
+  std::vector<cudaEvent_t> fev;
+  if (fgp_time) {
+    fev.resize(2 * (size_t)K, nullptr);
+    for (auto& e : fev) PSB_CUDA(cudaEventCreate(&e));
+  }
+  int rc = PSB_OK;
+  for (int k = 0; k < K && rc == PSB_OK; ++k) {
+    if (elapsed && k > 0) cudaEventRecord(evs[k], st);
+    rc = proxskip_pre(dto, dtf, x, b, 1, h, z, n, HW, coins_d + (int64_t)k * n, gamma, hcoef, bad,
+                      k, st);
+    const int na = (int)(off[k + 1] - off[k]);
+    if (rc || na == 0) continue;
+    if (fgp_time) cudaEventRecord(fev[2 * k], st);
+    for (int it = 0; it < n_inner && rc == PSB_OK; ++it) {
+      const double bprev = (accelerated && it > 0) ? beta[it - 1] : 0.0;
+      rc = fgp2d_iter(dtf, z, HW, q, qps, act_d + off[k], na, weight, nullptr, 0, rep_d + off[k],
+                      H, W, it, bprev, 0.125, nonneg, st);
+    }
+    if (fgp_time) cudaEventRecord(fev[2 * k + 1], st);
+    if (rc == PSB_OK)
+      rc = proxskip_post(dto, dtf, x, b, 1, h, z, q, qps, act_d + off[k], na, H, W, n_inner,
+                         nonneg, gamma, pg, bad, k, st);
+  }
+
+  if (elapsed && rc == PSB_OK) cudaEventRecord(evs[K], st);
+  if (use_graph) {
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (rc == PSB_OK && e != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exec = nullptr;
+    if (rc == PSB_OK) {
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) rc = fail(PSB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    if (rc == PSB_OK) {
+      e = cudaGraphLaunch(exec, st);
+      if (e != cudaSuccess) rc = fail(PSB_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+    }
+    cudaEventRecord(ev_out, st);
+    cudaStreamWaitEvent(user_stream, ev_out, 0);
+    // The device buffers above are freed by DevBuf below; cudaFree waits for
+    // the whole device, so no launch can outlive them.
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_out);
+    cudaStreamDestroy(priv);
+  }
+  if (fgp_time) {
+    cudaError_t e = cudaStreamSynchronize(use_graph ? user_stream : st);
+    if (rc == PSB_OK && e != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("run: ") + cudaGetErrorString(e));
+    for (int k = 0; k < K; ++k) {
+      float ms = 0.f;
+      fgp_time[k] = 0.0;
+      if (rc == PSB_OK && off[k + 1] > off[k] &&
+          cudaEventElapsedTime(&ms, fev[2 * k], fev[2 * k + 1]) == cudaSuccess)
+        fgp_time[k] = ms * 1e-3;
+    }
+    for (auto e : fev) cudaEventDestroy(e);
+  }
+  if (elapsed) {
+    cudaError_t e = cudaStreamSynchronize(use_graph ? user_stream : st);
+    if (rc == PSB_OK && e != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("run: ") + cudaGetErrorString(e));
+    for (int k = 0; k < K && rc == PSB_OK; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, evs[0], evs[k + 1]);
+      elapsed[k] = ms * 1e-3;
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+  return rc;
+}
+
+}  // namespace psb
+
+extern "C" int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void* b,
+                                        void* h, void* z, void* q, int64_t n, int H, int W,
+                                        const uint8_t* coins_host, int K, double gamma, double p,
+                                        double alpha, int n_inner, int accelerated, int nonneg,
+                                        double* last_weight_host, int64_t* prox_count_host,
+                                        int32_t* bad_iter, int use_graph, double* elapsed_host,
+                                        double* fgp_time_host, void* stream) {
+  return psb::proxskip_denoise_run(dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
+                                   gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
+                                   prox_count_host, bad_iter, use_graph, elapsed_host,
+                                   fgp_time_host, psb::as_stream(stream));
+}

@@ -1,0 +1,383 @@
+// FGP / accelerated dual projected gradient for the 2-D TV prox (tv.py:53-89).
+//
+// One launch = one inner iteration for a batch of problems.  Each warp owns a
+// band of 32*V columns and marches down a strip of rows, keeping the previous
+// row's dual y and primal u in registers (2.5-D register blocking): per pixel
+// the kernel reads x (1), q_k (2), q_{k-1} (2) and writes q_{k+1} (2) -- the
+// 28 B/pixel-iteration algorithmic minimum of SURVEY 8(d) for fp32 -- and
+// recomputes y_k = q_k + beta (q_k - q_{k-1}) instead of storing it.  Column
+// neighbours come from warp shuffles; the two band-edge columns come from one
+// predicated scalar load per row by lanes 0 and 31.  Strip-edge rows are
+// re-read (L2 hits).
+#include "common.cuh"
+
+namespace psb {
+
+namespace {
+
+template <class T, int V>
+struct FgpArgs {
+  const T* x;
+  int64_t xps;
+  T* q;
+  int64_t qps;
+  const int32_t* active;
+  const double* wts;
+  double w_all;
+  const uint8_t* rep;
+  int rep_all;
+  int H, W, it;
+  T beta;
+  T step;
+  int nonneg;
+  int rs;      // rows per strip
+  int nbands;  // column bands of 32*V
+  int nitems;  // nbands * nstrips
+};
+
+// Load y = q_k + beta (q_k - q_m) at V consecutive pixels (both channels),
+// re-projecting q_k first when `rp` (only at it == 0, where beta == 0).
+template <class T, int V>
+__device__ __forceinline__ void load_y(const T* qk, const T* qm, int64_t off, int64_t HW, bool mom,
+                                       bool rp, T beta, T w, T (&yy)[V], T (&yx)[V]) {
+  using A = Ar<T>;
+  ldv<T, V>(yy, qk + off);
+  ldv<T, V>(yx, qk + HW + off);
+  if (rp) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      T s = A::ball_scale(yy[v], yx[v], w);
+      yy[v] = A::mul(yy[v], s);
+      yx[v] = A::mul(yx[v], s);
+    }
+  }
+  if (mom) {
+    T my[V], mx[V];
+    ldv<T, V>(my, qm + off);
+    ldv<T, V>(mx, qm + HW + off);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      yy[v] = A::add(yy[v], A::mul(beta, A::sub(yy[v], my[v])));
+      yx[v] = A::add(yx[v], A::mul(beta, A::sub(yx[v], mx[v])));
+    }
+  }
+}
+
+// divergence at one pixel in the reference's accumulation order
+// (operators.py:66-70): ((0 + [i<H-1] yy) - [i>0] yy_up) + [c<W-1] yx - [c>0] yx_left
+template <class T>
+__device__ __forceinline__ T div_at(int i, int c, int H, int W, T yy, T yy_up, T yx, T yx_left) {
+  using A = Ar<T>;
+  T d = T(0);
+  if (i < H - 1) d = A::add(d, yy);
+  if (i > 0) d = A::sub(d, yy_up);
+  if (c < W - 1) d = A::add(d, yx);
+  if (c > 0) d = A::sub(d, yx_left);
+  return d;
+}
+
+template <class T>
+__device__ __forceinline__ T clampu(T v, int nonneg) {
+  return nonneg ? (v > T(0) ? v : T(0)) : v;  // np.maximum(v, 0); NaN -> 0 differs only for NaN
+}
+
+template <class T, int V>
+__global__ void __launch_bounds__(128) fgp2d_iter_kernel(FgpArgs<T, V> a) {
+  using A = Ar<T>;
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= a.nitems) return;  // whole warp exits together
+  const int band = item % a.nbands;
+  const int strip = item / a.nbands;
+  const int p = a.active ? a.active[blockIdx.y] : (int)blockIdx.y;
+  const int H = a.H, W = a.W;
+  const int64_t HW = (int64_t)H * W;
+
+  const T* __restrict__ xp = a.x + (int64_t)p * a.xps;
+  T* qbase = a.q + (int64_t)p * a.qps;
+  const T* qk = qbase + (int64_t)(a.it % 3) * 2 * HW;
+  const T* qm = qbase + (int64_t)((a.it + 2) % 3) * 2 * HW;
+  T* qo = qbase + (int64_t)((a.it + 1) % 3) * 2 * HW;
+  const T w = (T)(a.wts ? a.wts[blockIdx.y] : a.w_all);
+  const bool rp = a.it == 0 && (a.rep ? a.rep[blockIdx.y] != 0 : a.rep_all != 0);
+  const bool mom = a.beta != T(0);
+  const T beta = a.beta, step = a.step;
+
+  const int c0 = band * 32 * V;
+  const int cl = c0 + lane * V;
+  const bool lin = cl < W;  // V divides W, so the whole vector is in range
+  // band-edge halo column: lane 0 -> c0-1 (needs y_x), lane 31 -> c0+32V (needs y, x)
+  const int hc = lane == 0 ? c0 - 1 : c0 + 32 * V;
+  const bool hval = (lane == 0 && c0 > 0) || (lane == 31 && hc < W);
+
+  const int r0 = strip * a.rs;
+  const int r1 = min(H, r0 + a.rs);
+
+  T yyu[V], yy[V], yx[V], u[V];
+  T hyyu = T(0), hyy = T(0), hyx = T(0), hu = T(0);
+
+#pragma unroll
+  for (int v = 0; v < V; ++v) yyu[v] = yy[v] = yx[v] = u[v] = T(0);
+
+  auto load_row = [&](int r, T(&ty)[V], T(&tx)[V], T(&tu)[V], T& ty1, T& tx1, T& tu1) {
+    const int64_t ro = (int64_t)r * W;
+    if (lin) {
+      load_y<T, V>(qk, qm, ro + cl, HW, mom, rp, beta, w, ty, tx);
+      ldv<T, V>(tu, xp + ro + cl);
+    }
+    if (hval) {
+      T a1[1], b1[1];
+      load_y<T, 1>(qk, qm, ro + hc, HW, mom, rp, beta, w, a1, b1);
+      ty1 = a1[0];
+      tx1 = b1[0];
+      tu1 = __ldg(xp + ro + hc);
+    }
+  };
+
+  // u(i) = clamp(x(i) + div y) for the lane's V columns and (lane 31) the halo
+  auto prim_row = [&](int r, const T(&ty)[V], const T(&tyu)[V], const T(&tx)[V], T(&tu)[V],
+                      T ty1, T tyu1, T tx1, T& tu1) {
+    T left = __shfl_up_sync(0xffffffffu, tx[V - 1], 1);
+    if (lane == 0) left = tx1;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const T xl = v > 0 ? tx[v - 1] : left;
+      tu[v] = clampu(A::add(tu[v], div_at<T>(r, cl + v, H, W, ty[v], tyu[v], tx[v], xl)), a.nonneg);
+    }
+    if (lane == 31) tu1 = clampu(A::add(tu1, div_at<T>(r, hc, H, W, ty1, tyu1, tx1, tx[V - 1])), a.nonneg);
+  };
+
+  // prologue: y_y at row r0-1, then row r0 and u(r0)
+  if (r0 > 0) {
+    T tx[V], tu[V], tx1 = T(0), tu1 = T(0);
+    load_row(r0 - 1, yyu, tx, tu, hyyu, tx1, tu1);
+  }
+  {
+    T hx1 = T(0);
+    load_row(r0, yy, yx, u, hyy, hyx, hx1);
+    hu = hx1;
+    prim_row(r0, yy, yyu, yx, u, hyy, hyyu, hyx, hu);
+  }
+
+  for (int i = r0; i < r1; ++i) {
+    const bool nxt = i + 1 < H;
+    T nyy[V], nyx[V], nu[V];
+    T nhyy = T(0), nhyx = T(0), nhu = T(0);
+#pragma unroll
+    for (int v = 0; v < V; ++v) nyy[v] = nyx[v] = nu[v] = T(0);
+    if (nxt) {
+      load_row(i + 1, nyy, nyx, nu, nhyy, nhyx, nhu);
+      prim_row(i + 1, nyy, yy, nyx, nu, nhyy, hyy, nhyx, nhu);
+    }
+    T right = __shfl_down_sync(0xffffffffu, u[0], 1);
+    if (lane == 31) right = hu;
+    T oy[V], ox[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = cl + v;
+      const T ur = v < V - 1 ? u[v + 1] : right;
+      const T gy = nxt ? A::sub(nu[v], u[v]) : T(0);
+      const T gx = c < W - 1 ? A::sub(ur, u[v]) : T(0);
+      const T ay = A::add(yy[v], A::mul(step, gy));
+      const T ax = A::add(yx[v], A::mul(step, gx));
+      const T s = A::ball_scale(ay, ax, w);
+      oy[v] = A::mul(ay, s);
+      ox[v] = A::mul(ax, s);
+    }
+    if (lin) {
+      const int64_t o = (int64_t)i * W + cl;
+      stv<T, V>(qo + o, oy);
+      stv<T, V>(qo + HW + o, ox);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      yyu[v] = yy[v];
+      yy[v] = nyy[v];
+      yx[v] = nyx[v];
+      u[v] = nu[v];
+    }
+    hyyu = hyy;
+    hyy = nhyy;
+    hyx = nhyx;
+    hu = nhu;
+  }
+}
+
+// u = clamp(x + div q_n) and q_n -> slot 0 (tv.py:86-89)
+template <class T>
+__global__ void fgp2d_finalize_kernel(const T* __restrict__ x, int64_t xps, T* q, int64_t qps,
+                                      const int32_t* __restrict__ active, int H, int W, int n_inner,
+                                      int nonneg, T* __restrict__ u, int64_t ups) {
+  using A = Ar<T>;
+  const int p = active ? active[blockIdx.y] : (int)blockIdx.y;
+  const int64_t HW = (int64_t)H * W;
+  const int slot = n_inner % 3;
+  T* qb = q + (int64_t)p * qps;
+  const T* qn = qb + (int64_t)slot * 2 * HW;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < HW;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / W), c = (int)(idx % W);
+    const T yy = qn[idx], yx = qn[HW + idx];
+    const T yyu = i > 0 ? qn[idx - W] : T(0);
+    const T yxl = c > 0 ? qn[HW + idx - 1] : T(0);
+    const T d = div_at<T>(i, c, H, W, yy, yyu, yx, yxl);
+    u[(int64_t)p * ups + idx] = clampu(A::add(x[(int64_t)p * xps + idx], d), nonneg);
+    if (slot != 0) {
+      qb[idx] = yy;
+      qb[HW + idx] = yx;
+    }
+  }
+}
+
+template <class T, int V>
+int launch_iter(const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active, int n_active,
+                double weight, const double* wts, int rep_all, const uint8_t* rep, int H, int W,
+                int it, double beta, double step, int nonneg, cudaStream_t st) {
+  FgpArgs<T, V> a;
+  a.x = static_cast<const T*>(x);
+  a.xps = xps;
+  a.q = static_cast<T*>(q);
+  a.qps = qps;
+  a.active = active;
+  a.wts = wts;
+  a.w_all = weight;
+  a.rep = rep;
+  a.rep_all = rep_all;
+  a.H = H;
+  a.W = W;
+  a.it = it;
+  a.beta = (T)beta;
+  a.step = (T)step;
+  a.nonneg = nonneg;
+  a.nbands = (W + 32 * V - 1) / (32 * V);
+  // Strip height: long strips amortise the two re-read halo rows; short ones
+  // expose enough warps when the batch is small (single 256^2 / 512^2 solves).
+  const int64_t warps_per_row = (int64_t)a.nbands * n_active;
+  const int64_t target = 4LL * sm_count() * 16;  // ~16 warps per SM, 4 waves
+  int rs = 32;
+  while (rs > 4 && warps_per_row * ((H + rs - 1) / rs) < target) rs >>= 1;
+  a.rs = rs;
+  a.nitems = a.nbands * ((H + rs - 1) / rs);
+  dim3 block(128);
+  dim3 grid((a.nitems + 3) / 4, n_active);
+  fgp2d_iter_kernel<T, V><<<grid, block, 0, st>>>(a);
+  PSB_LAUNCHED("fgp2d_iter");
+  return PSB_OK;
+}
+
+template <class T>
+int dispatch_iter(const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
+                  int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
+                  int H, int W, int it, double beta, double step, int nonneg, cudaStream_t st) {
+  constexpr int VMAX = 16 / sizeof(T);
+  const bool aligned = (W % VMAX == 0) && (xps % VMAX == 0) && (qps % VMAX == 0) &&
+                       (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(q) % 16 == 0);
+  if (aligned)
+    return launch_iter<T, VMAX>(x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W,
+                                it, beta, step, nonneg, st);
+  return launch_iter<T, 1>(x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W, it,
+                           beta, step, nonneg, st);
+}
+
+}  // namespace
+
+int fgp2d_iter(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
+               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
+               int H, int W, int it, double beta, double step, int nonneg, cudaStream_t st) {
+  PSB_REQUIRE(H >= 2 && W >= 2, "fgp2d: need a 2-D grid with both sides >= 2");
+  PSB_REQUIRE(n_active >= 0 && n_active <= 65535, "fgp2d: n_active out of range");
+  PSB_REQUIRE(qps >= 6LL * H * W, "fgp2d: q_pstride must hold three (2,H,W) slots");
+  PSB_REQUIRE(wts != nullptr || weight > 0, "tv_prox: weight must be positive");
+  if (n_active == 0) return PSB_OK;
+  if (dtype == PSB_F32)
+    return dispatch_iter<float>(x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W,
+                                it, beta, step, nonneg, st);
+  if (dtype == PSB_F64)
+    return dispatch_iter<double>(x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W,
+                                 it, beta, step, nonneg, st);
+  return fail(PSB_ERR_VALUE, "fgp2d: unknown dtype");
+}
+
+int fgp2d_finalize(int dtype, const void* x, int64_t xps, void* q, int64_t qps,
+                   const int32_t* active, int n_active, int H, int W, int n_inner, int nonneg,
+                   void* u, int64_t ups, cudaStream_t st) {
+  PSB_REQUIRE(H >= 2 && W >= 2, "fgp2d: need a 2-D grid with both sides >= 2");
+  PSB_REQUIRE(n_active >= 0 && n_active <= 65535, "fgp2d: n_active out of range");
+  if (n_active == 0) return PSB_OK;
+  const int64_t HW = (int64_t)H * W;
+  dim3 block(256);
+  dim3 grid((unsigned)std::min<int64_t>((HW + 255) / 256, 1024), n_active);
+  if (dtype == PSB_F32)
+    fgp2d_finalize_kernel<float><<<grid, block, 0, st>>>(
+        static_cast<const float*>(x), xps, static_cast<float*>(q), qps, active, H, W, n_inner,
+        nonneg, static_cast<float*>(u), ups);
+  else if (dtype == PSB_F64)
+    fgp2d_finalize_kernel<double><<<grid, block, 0, st>>>(
+        static_cast<const double*>(x), xps, static_cast<double*>(q), qps, active, H, W, n_inner,
+        nonneg, static_cast<double*>(u), ups);
+  else
+    return fail(PSB_ERR_VALUE, "fgp2d: unknown dtype");
+  PSB_LAUNCHED("fgp2d_finalize");
+  return PSB_OK;
+}
+
+// Beck-Teboulle momentum table, t_0 = 1, in double with the reference's
+// operation order (tv.py:77-80).
+void fista_betas(int n, double* out) {
+  double t = 1.0;
+  for (int i = 0; i < n; ++i) {
+    const double t1 = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    out[i] = (t - 1.0) / t1;
+    t = t1;
+  }
+}
+
+int tv_prox2d(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
+              int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
+              int H, int W, int n_inner, int accelerated, int nonneg, double step, void* u,
+              int64_t ups, cudaStream_t st) {
+  PSB_REQUIRE(n_inner >= 1, "TvProxState: inner_iters must be >= 1");
+  std::vector<double> beta(n_inner, 0.0);
+  if (accelerated) fista_betas(n_inner, beta.data());
+  for (int it = 0; it < n_inner; ++it) {
+    // y_it = q_it + beta_{it-1} (q_it - q_{it-1}); beta_{-1} := 0 (y_0 = q_0)
+    const double b = (accelerated && it > 0) ? beta[it - 1] : 0.0;
+    int rc = fgp2d_iter(dtype, x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W, it,
+                        b, step, nonneg, st);
+    if (rc) return rc;
+  }
+  return fgp2d_finalize(dtype, x, xps, q, qps, active, n_active, H, W, n_inner, nonneg, u, ups, st);
+}
+
+}  // namespace psb
+
+extern "C" {
+
+int psb_fgp2d_iter(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
+                   const int32_t* active, int n_active, double weight, const double* weights,
+                   int reproject_all, const uint8_t* reproject, int H, int W, int it,
+                   double beta_prev, double step, int nonneg, void* stream) {
+  return psb::fgp2d_iter(dtype, x, x_pstride, q, q_pstride, active, n_active, weight, weights,
+                         reproject_all, reproject, H, W, it, beta_prev, step, nonneg,
+                         psb::as_stream(stream));
+}
+
+int psb_fgp2d_finalize(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
+                       const int32_t* active, int n_active, int H, int W, int n_inner, int nonneg,
+                       void* u, int64_t u_pstride, void* stream) {
+  return psb::fgp2d_finalize(dtype, x, x_pstride, q, q_pstride, active, n_active, H, W, n_inner,
+                             nonneg, u, u_pstride, psb::as_stream(stream));
+}
+
+int psb_tv_prox2d(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
+                  const int32_t* active, int n_active, double weight, const double* weights,
+                  int reproject_all, const uint8_t* reproject, int H, int W, int n_inner,
+                  int accelerated, int nonneg, double step, void* u, int64_t u_pstride,
+                  void* stream) {
+  return psb::tv_prox2d(dtype, x, x_pstride, q, q_pstride, active, n_active, weight, weights,
+                        reproject_all, reproject, H, W, n_inner, accelerated, nonneg, step, u,
+                        u_pstride, psb::as_stream(stream));
+}
+
+}  // extern "C"

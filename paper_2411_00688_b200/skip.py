@@ -1,0 +1,228 @@
+"""ProxSkip and PDHGSkip-2 on the device (skip.py of the reference).
+
+Coins: one ``Generator(Philox(seed)).random()`` draw per iteration, compared
+with p (skip.py:27-28, 67, 136).  The whole coin sequence is drawn on the host
+up front -- bit-identical to the reference's stream -- so the GPU never
+generates randomness and the fused drivers know the skip pattern in advance.
+
+Fast path: a problem assembled by ``problems.build_tv_recon`` with an
+identity fidelity (BASELINE configs 1/4) and a passive IterationLog runs the
+whole outer loop inside the native driver (psb_proxskip_denoise_run: fused
+pre/FGP/post kernels, optionally one CUDA graph).  Every other case runs the
+same kernels step by step from Python and observes each iteration exactly
+like the reference.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _arrays as AR
+from . import _lib as L
+from . import tensor as T
+from .errors import DivergenceError
+from .operators import apply_adjoint, apply_forward
+from .solvers import IterationLog, RunRecord, _check_finite, _check_step_rule, _dev, _ensure_log
+
+INT32_MAX = 2 ** 31 - 1
+
+
+@dataclass
+class SkipConfig:
+    """Skip probability + seed of the per-run Bernoulli stream (skip.py:16-28)."""
+
+    p: float
+    seed: int = 0
+
+    def __post_init__(self):
+        if not 0.0 < self.p <= 1.0:
+            raise ValueError(f"SkipConfig: p must be in (0, 1], got {self.p}")
+
+    def stream(self):
+        return np.random.Generator(np.random.Philox(self.seed))
+
+    def coins(self, iters):
+        """theta_k = stream().random() < p for k < iters (host, uint8)."""
+        return (self.stream().random(iters) < self.p).astype(np.uint8)
+
+
+def optimal_probability(mu, L_):
+    """sqrt(mu / L) (skip.py:31-35)."""
+    if mu <= 0 or L_ <= 0 or mu > L_:
+        raise ValueError(f"optimal_probability: need 0 < mu <= L, got mu={mu}, L={L_}")
+    return float(np.sqrt(mu / L_))
+
+
+def _finish_passive(log, coins, elapsed, base_inner, inner_iters):
+    """Fill the records of a passive log after a fused run."""
+    counts = np.cumsum(coins.astype(np.int64))
+    for k in range(len(coins)):
+        inner = base_inner + inner_iters * int(counts[k]) if log.inner_counter is not None else 0
+        log.records.append(RunRecord(k + 1, float(elapsed[k]), int(counts[k]), inner, None, None,
+                                     bool(coins[k])))
+
+
+def run_proxskip(problem, x0, h0, gamma, skip, iters, log=None, *, use_graph=None):
+    """ProxSkip (skip.py:46-79).  Returns (x_final, IterationLog)."""
+    if gamma <= 0:
+        raise ValueError("run_proxskip: gamma must be positive")
+    log = _ensure_log(log)
+    fused = getattr(problem, "_fused", None)
+    if fused is not None and fused.get("kind") == "denoise" and log.passive:
+        return _proxskip_denoise_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph)
+    log.start(AR.is_host(x0))
+    p = skip.p
+    coins = skip.coins(iters)
+    dt = getattr(problem, "outer_dtype", torch.float64)
+    x = AR.to_dev(x0, dt).clone()
+    h = AR.to_dev(h0, dt).clone() if h0 is not None else torch.zeros_like(x)
+    hc = gamma - gamma / p
+    pg = p / gamma
+    prox_count = 0
+    step = fused is not None and fused.get("kind") == "denoise"
+    for k in range(iters):
+        theta = bool(coins[k])
+        if step:
+            x, h = _denoise_step(problem, fused, x, h, gamma, p, hc, pg, theta, k)
+        else:
+            g = _dev(problem.smooth.grad(x), x)
+            t = T.lincomb(1.0, x, -gamma, g)
+            xhat = T.lincomb(1.0, t, gamma, h)
+            if theta:
+                xn = _dev(problem.prox_g(T.lincomb(1.0, t, hc, h), gamma / p), x)
+            else:
+                xn = xhat
+            h = T.lincomb(1.0, h, pg, T.lincomb(1.0, xn, -1.0, xhat))
+            x = xn
+        prox_count += theta
+        _check_finite(x, k, "proxskip")
+        if log.observe(k + 1, x, prox_count, theta):
+            break
+    return AR.like(x, x0), log
+
+
+# -- fused identity-fidelity path (configs 1 / 4) ------------------------------
+
+_ONE = {}
+
+
+def _coin_dev(theta):
+    key = (torch.cuda.current_device(), bool(theta))
+    if key not in _ONE:
+        _ONE[key] = torch.tensor([1 if theta else 0], dtype=torch.uint8, device="cuda")
+    return _ONE[key]
+
+
+def _denoise_step(problem, fused, x, h, gamma, p, hc, pg, theta, k):
+    """One outer iteration with the same kernels the native driver uses."""
+    st = problem.tv_state
+    b = fused["b_dev"]
+    H, W = st.shape
+    HW = H * W
+    dto, dtf = L.dcode(x.dtype), L.dcode(st.dtype)
+    z = fused.setdefault("z", torch.empty((H, W), dtype=st.dtype, device="cuda"))
+    bad = fused.setdefault("bad", torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda"))
+    L.call("psb_proxskip_pre", dto, dtf, L.ptr(x), L.ptr(b), 1, L.ptr(h), L.ptr(z), 1, HW,
+           L.ptr(_coin_dev(theta)), gamma, hc, L.ptr(bad), k, L.stream())
+    if theta:
+        weight = (gamma / p) * problem.alpha  # prox_g(z, gamma/p) -> tv_prox(z, step*alpha)
+        rep = int(st.last_weight is not None and st.last_weight != weight)
+        from .tv import INNER_STEP
+        betas = fused.setdefault("betas", _betas(st.inner_iters))
+        for it in range(st.inner_iters):
+            bprev = betas[it - 1] if (st.accelerated and it > 0) else 0.0
+            L.call("psb_fgp2d_iter", dtf, L.ptr(z), HW, L.ptr(st.slots), 6 * HW, None, 1, weight,
+                   None, rep, None, H, W, it, bprev, INNER_STEP, int(st.nonneg), L.stream())
+        L.call("psb_proxskip_post", dto, dtf, L.ptr(x), L.ptr(b), 1, L.ptr(h), L.ptr(z),
+               L.ptr(st.slots), 6 * HW, None, 1, H, W, st.inner_iters, int(st.nonneg), gamma, pg,
+               L.ptr(bad), k, L.stream())
+        st.last_weight = weight
+        st.total_inner_iterations += st.inner_iters
+    return x, h
+
+
+def _betas(n):
+    out, t = [], 1.0
+    for _ in range(n):
+        t1 = (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
+        out.append((t - 1.0) / t1)
+        t = t1
+    return out
+
+
+def _proxskip_denoise_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph):
+    log.start(AR.is_host(x0))
+    st = problem.tv_state
+    H, W = st.shape
+    dt = problem.outer_dtype
+    x = AR.to_dev(x0, dt).clone()
+    h = AR.to_dev(h0, dt).clone() if h0 is not None else torch.zeros_like(x)
+    z = torch.empty((H, W), dtype=st.dtype, device="cuda")
+    coins = skip.coins(iters)
+    lw = np.array([np.nan if st.last_weight is None else st.last_weight], dtype=np.float64)
+    pc = np.zeros(1, dtype=np.int64)
+    bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
+    elapsed = np.zeros(max(iters, 1), dtype=np.float64)
+    if use_graph is None:
+        use_graph = H * W <= 1024 * 1024
+    base_inner = st.total_inner_iterations
+    L.call("psb_proxskip_denoise_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
+           L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), 1, H, W,
+           coins.ctypes.data_as(L.C.c_void_p), iters, float(gamma), float(skip.p),
+           float(problem.alpha), st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)),
+           lw.ctypes.data_as(L.C.c_void_p), pc.ctypes.data_as(L.C.c_void_p), L.ptr(bad),
+           int(bool(use_graph)), elapsed.ctypes.data_as(L.C.c_void_p), None, L.stream())
+    k_bad = int(bad.item())
+    if k_bad != INT32_MAX:
+        raise DivergenceError(k_bad, "proxskip")
+    st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
+    st.total_inner_iterations += st.inner_iters * int(pc[0])
+    _finish_passive(log, coins[:iters], elapsed, base_inner, st.inner_iters)
+    return AR.like(x, x0), log
+
+
+# -- PDHGSkip-2 (skip.py:117-150) ----------------------------------------------
+
+def run_pdhgskip2(problem, x0, y0, h0, sigma, tau, skip, iters, log=None):
+    """PDHG with a ProxSkip control variate on the primal prox (Alg. 6)."""
+    _check_step_rule(sigma, tau, problem.norm_K_sq)
+    fused = getattr(problem, "_fused", None)
+    if fused is not None:
+        return _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, "pdhgskip2")
+    log = _ensure_log(log)
+    log.start(AR.is_host(x0))
+    p = skip.p
+    coins = skip.coins(iters)
+    K = problem.K
+    x = AR.to_dev(x0, torch.float64).clone()
+    y = AR.to_dev(y0, torch.float64).clone()
+    h = AR.to_dev(h0, torch.float64).clone() if h0 is not None else torch.zeros_like(x)
+    hc = sigma - sigma / p
+    ps = p / sigma
+    prox_count = 0
+    for k in range(iters):
+        kty = apply_adjoint(K, y)
+        theta = bool(coins[k])
+        t = T.lincomb(1.0, x, -sigma, kty)
+        xhat = T.lincomb(1.0, t, sigma, h)
+        if theta:
+            xn = _dev(problem.prox_g(T.lincomb(1.0, t, hc, h), sigma / p), x)
+            prox_count += 1
+        else:
+            xn = xhat
+        xbar = T.lincomb(2.0, xn, -1.0, x)
+        y = _dev(problem.prox_fstar(T.lincomb(1.0, y, tau, apply_forward(K, xbar)), tau), y)
+        h = T.lincomb(1.0, h, ps, T.lincomb(1.0, xn, -1.0, xhat))
+        x = xn
+        _check_finite(x, k, "pdhgskip2")
+        if log.observe(k + 1, x, prox_count, theta):
+            break
+    return AR.like(x, x0), log
+
+
+def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo):
+    raise NotImplementedError("fused PDHG path not built yet")

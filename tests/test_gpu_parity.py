@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden vectors.
+
+fp64 device path: bit-identical to the oracle (every op rounded separately).
+fp32 / mixed production path: rel-L2(u) <= 1e-4 and rel objective <= 1e-5
+(BASELINE north_star tolerance) -- tighter where the inputs allow.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2411_00688_b200 as psb  # noqa: E402
+from paper_2411_00688_b200 import phantoms  # noqa: E402
+from oracle import imgskip_cpu as oc  # noqa: E402
+
+U_TOL = 1e-4
+OBJ_TOL = 1e-5
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+# -- operators --------------------------------------------------------------
+
+def test_grad_div_ball_bitwise(golden):
+    g = golden
+    np.testing.assert_array_equal(psb.grad_forward(g["op_u"]), g["op_grad"])
+    np.testing.assert_array_equal(psb.divergence(g["op_q"]), g["op_div"])
+    np.testing.assert_array_equal(psb.divergence(g["op_qint"]), g["op_divint"])
+    np.testing.assert_array_equal(psb.project_ball(3.0 * g["op_q"], 0.7), g["op_ball"])
+    assert psb.tv_value(g["op_u"]) == pytest.approx(float(g["op_tv"]), rel=1e-14)
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (3, 5), (37, 130), (256, 256)])
+def test_grad_div_adjoint(shape):
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal(shape)
+    q = rng.standard_normal((2,) + shape)
+    np.testing.assert_array_equal(psb.grad_forward(u), oc.fd_grad(u))
+    np.testing.assert_array_equal(psb.divergence(q), oc.fd_div(q))
+    lhs = np.sum(psb.grad_forward(u) * q)
+    rhs = -np.sum(u * psb.divergence(q))
+    assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(u) * np.linalg.norm(q)
+
+
+def test_reductions():
+    rng = np.random.default_rng(2)
+    a, b = rng.standard_normal((64, 48)), rng.standard_normal((64, 48))
+    assert psb.dot(a, b) == pytest.approx(oc.inner(a, b), rel=1e-13)
+    assert psb.norm2(a) == pytest.approx(oc.l2(a), rel=1e-14)
+    assert psb.rel_error(a, b) == pytest.approx(oc.relerr(a, b), rel=1e-13)
+    assert psb.tv_value(a) == pytest.approx(oc.tv_total(a), rel=1e-13)
+    with pytest.raises(ZeroDivisionError):
+        psb.rel_error(a, np.zeros_like(a))
+
+
+# -- TV prox ------------------------------------------------------------------
+
+def test_tv_prox_fp64_bitwise_golden(golden):
+    g = golden
+    x = g["tv_x"]
+    st = psb.TvProxState.cold(x.shape, 7, dtype=torch.float64)
+    np.testing.assert_array_equal(psb.tv_prox(x, 0.3, st), g["tv_u1"])
+    np.testing.assert_array_equal(st.q_warm, g["tv_q1"])
+    np.testing.assert_array_equal(psb.tv_prox(x, 0.3, st), g["tv_u2"])
+    np.testing.assert_array_equal(psb.tv_prox(x, 0.05, st), g["tv_u3"])  # re-projection
+    np.testing.assert_array_equal(st.q_warm, g["tv_q3"])
+    assert st.total_inner_iterations == int(g["tv_count"])
+    st = psb.TvProxState.cold(x.shape, 11, nonneg=True, dtype=torch.float64)
+    np.testing.assert_array_equal(psb.tv_prox(x - 0.5, 0.2, st), g["tv_nn"])
+    st = psb.TvProxState.cold(x.shape, 9, accelerated=False, dtype=torch.float64)
+    np.testing.assert_array_equal(psb.tv_prox(x, 0.3, st), g["tv_plain"])
+
+
+# shapes exercising: V=1 path (odd W), several 32*V bands with halo columns,
+# partial bands, strips, tiny grids
+@pytest.mark.parametrize("shape", [(2, 2), (5, 7), (12, 9), (33, 64), (70, 130), (130, 260),
+                                   (256, 256), (97, 516)])
+@pytest.mark.parametrize("inner", [1, 2, 5])
+def test_tv_prox_fp64_bitwise_vs_oracle(shape, inner):
+    rng = np.random.default_rng(hash(shape) % 1000 + inner)
+    x = rng.standard_normal(shape)
+    st = psb.TvProxState.cold(shape, inner, dtype=torch.float64)
+    so = oc.FgpState.zeros(shape, inner)
+    for w in (0.3, 0.3, 0.1):  # warm start, then weight change -> re-projection
+        np.testing.assert_array_equal(psb.tv_prox(x, w, st), oc.fgp_prox(x, w, so))
+        np.testing.assert_array_equal(st.q_warm, so.q)
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (256, 256), (130, 260), (512, 512)])
+def test_tv_prox_fp32_tolerance(shape):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(shape)
+    st = psb.TvProxState.cold(shape, 50)
+    so = oc.FgpState.zeros(shape, 50)
+    for _ in range(2):
+        u = psb.tv_prox(x, 0.5, st)
+        uo = oc.fgp_prox(x, 0.5, so)
+        assert rel(u, uo) < 1e-5
+
+
+def test_tv_prox_properties_device():
+    # test_tv.py:100-116 semantics on the device
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((8, 8)) - 0.5
+    st = psb.TvProxState.cold((8, 8), 50, nonneg=True)
+    assert psb.tv_prox(x, 0.2, st).min() >= 0.0
+    st = psb.TvProxState.cold((6, 6), 20)
+    y = rng.standard_normal((6, 6))
+    psb.tv_prox(y, 0.5, st)
+    psb.tv_prox(y, 0.05, st)
+    mag = np.sqrt(st.q_warm[0] ** 2 + st.q_warm[1] ** 2)
+    assert mag.max() <= 0.05 * (1 + 1e-6)
+    with pytest.raises(ValueError):
+        psb.tv_prox(y, 0.0, st)
+    st = psb.TvProxState.cold((8, 8), 4000, dtype=torch.float64)
+    x8 = rng.standard_normal((8, 8))
+    psb.tv_prox(x8, 0.25, st)
+    assert abs(psb.dual_gap_rof(x8, st.q_warm, 0.25)) < 1e-8
+
+
+# -- ProxSkip / PGD -------------------------------------------------------------
+
+def _traj_log():
+    xs, flags = [], []
+    return xs, flags, psb.IterationLog(callback=lambda r, x: (xs.append(x.copy()),
+                                                             flags.append(r.prox_applied)))
+
+
+def test_proxskip_fp64_trajectory_bitwise_golden(golden):
+    g = golden
+    b = g["dn_b"]
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=7, precision="fp64")
+    xs, fl, log = _traj_log()
+    psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0, psb.SkipConfig(0.3, 5), 25,
+                     log)
+    np.testing.assert_array_equal(np.stack(xs), g["dn_ps_traj"])
+    np.testing.assert_array_equal(np.array(fl), g["dn_ps_flags"])
+    assert prob.tv_state.total_inner_iterations == int(g["dn_ps_inner"])
+    assert psb.objective_tv(xs[-1], prob) == pytest.approx(float(g["dn_ps_obj"]), rel=1e-13)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_proxskip_fused_driver_fp64_bitwise(golden, graph):
+    g = golden
+    b = g["dn_b"]
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=7, precision="fp64")
+    x, log = psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0,
+                              psb.SkipConfig(0.3, 5), 25, use_graph=graph)
+    np.testing.assert_array_equal(x, g["dn_ps_traj"][-1])
+    assert [r.prox_applied for r in log.records] == list(g["dn_ps_flags"])
+    assert log.records[-1].prox_count == int(g["dn_ps_flags"].sum())
+    assert prob.tv_state.total_inner_iterations == int(g["dn_ps_inner"])
+    assert all(r2.elapsed_s >= r1.elapsed_s for r1, r2 in zip(log.records, log.records[1:]))
+
+
+def test_pgd_bitwise_golden(golden):
+    b = golden["dn_b"]
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=7, precision="fp64")
+    xs, _, log = _traj_log()
+    psb.run_pgd(prob.prox_problem, np.zeros_like(b), 1.0, 6, log)
+    np.testing.assert_array_equal(np.stack(xs), golden["dn_pgd_traj"])
+
+
+def test_proxskip_p1_is_pgd_bitwise():
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal((20, 24))
+    xs_a, _, la = _traj_log()
+    xs_b, _, lb = _traj_log()
+    pa = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.2, inner_budget=5, precision="fp64")
+    pb = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.2, inner_budget=5, precision="fp64")
+    psb.run_pgd(pa.prox_problem, np.zeros_like(b), 0.9, 30, la)
+    psb.run_proxskip(pb.prox_problem, np.zeros_like(b), None, 0.9, psb.SkipConfig(1.0, 0), 30, lb)
+    for a, c in zip(xs_a, xs_b):
+        np.testing.assert_array_equal(a, c)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("mixed", 1e-6)])
+def test_config1_full_size_parity(precision, tol):
+    """BASELINE config 1 at full size: 256^2, alpha 0.1, FGP-100, p=0.1, 500 outer."""
+    truth, b = phantoms.config1_data(seed=0)
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=100,
+                              precision=precision)
+    x, log = psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0,
+                              psb.SkipConfig(0.1, 0), 500)
+    xr, _, n_prox, inner = _oracle_config1()
+    assert log.records[-1].prox_count == n_prox
+    assert prob.tv_state.total_inner_iterations == inner
+    assert rel(x, xr) < min(tol, U_TOL)
+    pr = oc.make_recon(oc.identity_op(b.shape), b, 0.1, inner=100)
+    o_dev, o_ref = psb.objective_tv(x, prob), oc.tv_objective(xr, pr)
+    assert abs(o_dev - o_ref) / abs(o_ref) < OBJ_TOL
+
+
+_C1 = {}
+
+
+def _oracle_config1():
+    if not _C1:
+        _, b = phantoms.config1_data(seed=0)
+        _C1["r"] = oc.proxskip_denoise(b, 0.1, 0.1, 0, 500, 100)
+    return _C1["r"]
+
+
+def test_divergence_error_iteration():
+    b = np.ones((16, 16))
+    b[3, 4] = np.nan
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=3)
+    with pytest.raises(psb.DivergenceError) as ei:
+        psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0, psb.SkipConfig(0.5, 1), 10)
+    assert ei.value.iteration == 0 and ei.value.algorithm == "proxskip"
+
+
+# -- batched (config 4 path) ----------------------------------------------------
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_batched_matches_per_problem_oracle(precision):
+    n, N, K, inner = 48, 6, 40, 10
+    idx = np.arange(N) * 683  # spread of seeds incl. 0
+    b = np.stack([phantoms.config4_problem(int(i), n=n)[1] for i in idx])
+    x, counts = psb.run_proxskip_batched(b, 0.1, 0.1, idx, K, inner, precision=precision)
+    for j, i in enumerate(idx):
+        xr, _, n_prox, _ = oc.proxskip_denoise(b[j], 0.1, 0.1, int(i), K, inner)
+        assert counts[j] == n_prox
+        if precision == "fp64":
+            np.testing.assert_array_equal(x[j], xr)
+        else:
+            assert rel(x[j], xr) < 1e-5
+
+
+def test_batched_graph_equals_stream():
+    n, N, K = 32, 5, 20
+    idx = np.arange(N)
+    b = np.stack([phantoms.config4_problem(int(i), n=n)[1] for i in idx])
+    xa, ca = psb.run_proxskip_batched(b, 0.1, 0.3, idx, K, 8, precision="fp32", use_graph=False)
+    xb, cb = psb.run_proxskip_batched(b, 0.1, 0.3, idx, K, 8, precision="fp32", use_graph=True)
+    np.testing.assert_array_equal(xa, xb)
+    np.testing.assert_array_equal(ca, cb)
