@@ -112,11 +112,14 @@ int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void
     PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   }
 
+  // inside a capture an event record must be an explicit (external) graph node
+  // to be usable for timing afterwards
+  const unsigned rec_flags = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
   std::vector<cudaEvent_t> evs;
   if (elapsed) {
     evs.resize(K + 1, nullptr);
     for (auto& e : evs) PSB_CUDA(cudaEventCreate(&e));
-    PSB_CUDA(cudaEventRecord(evs[0], st));
+    PSB_CUDA(cudaEventRecordWithFlags(evs[0], st, rec_flags));
   }
   // optional per-iteration timing of the FGP burst (bench roofline)
   std::vector<cudaEvent_t> fev;
@@ -126,24 +129,24 @@ int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void
   }
   int rc = PSB_OK;
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
-    if (elapsed && k > 0) cudaEventRecord(evs[k], st);
+    if (elapsed && k > 0) cudaEventRecordWithFlags(evs[k], st, rec_flags);
     rc = proxskip_pre(dto, dtf, x, b, 1, h, z, n, HW, coins_d + (int64_t)k * n, gamma, hcoef, bad,
                       k, st);
     const int na = (int)(off[k + 1] - off[k]);
     if (rc || na == 0) continue;
-    if (fgp_time) cudaEventRecord(fev[2 * k], st);
+    if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
     for (int it = 0; it < n_inner && rc == PSB_OK; ++it) {
       const double bprev = (accelerated && it > 0) ? beta[it - 1] : 0.0;
       rc = fgp2d_iter(dtf, z, HW, q, qps, act_d + off[k], na, weight, nullptr, 0, rep_d + off[k],
                       H, W, it, bprev, 0.125, nonneg, st);
     }
-    if (fgp_time) cudaEventRecord(fev[2 * k + 1], st);
+    if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
     if (rc == PSB_OK)
       rc = proxskip_post(dto, dtf, x, b, 1, h, z, q, qps, act_d + off[k], na, H, W, n_inner,
                          nonneg, gamma, pg, bad, k, st);
   }
 
-  if (elapsed && rc == PSB_OK) cudaEventRecord(evs[K], st);
+  if (elapsed && rc == PSB_OK) cudaEventRecordWithFlags(evs[K], st, rec_flags);
   if (use_graph) {
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &graph);
@@ -175,9 +178,12 @@ int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void
     for (int k = 0; k < K; ++k) {
       float ms = 0.f;
       fgp_time[k] = 0.0;
-      if (rc == PSB_OK && off[k + 1] > off[k] &&
-          cudaEventElapsedTime(&ms, fev[2 * k], fev[2 * k + 1]) == cudaSuccess)
-        fgp_time[k] = ms * 1e-3;
+      if (rc == PSB_OK && off[k + 1] > off[k]) {
+        if (cudaEventElapsedTime(&ms, fev[2 * k], fev[2 * k + 1]) == cudaSuccess)
+          fgp_time[k] = ms * 1e-3;
+        else
+          fgp_time[k] = std::nan(""), (void)cudaGetLastError();
+      }
     }
     for (auto e : fev) cudaEventDestroy(e);
   }
@@ -187,8 +193,10 @@ int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void
       rc = fail(PSB_ERR_CUDA, std::string("run: ") + cudaGetErrorString(e));
     for (int k = 0; k < K && rc == PSB_OK; ++k) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, evs[0], evs[k + 1]);
-      elapsed[k] = ms * 1e-3;
+      if (cudaEventElapsedTime(&ms, evs[0], evs[k + 1]) == cudaSuccess)
+        elapsed[k] = ms * 1e-3;
+      else
+        elapsed[k] = std::nan(""), (void)cudaGetLastError();
     }
     for (auto e : evs) cudaEventDestroy(e);
   }
