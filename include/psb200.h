@@ -93,6 +93,20 @@ int psb_tv_prox2d(int dtype, const void* x, int64_t x_pstride, void* q, int64_t 
                   int accelerated, int nonneg, double step, void* u, int64_t u_pstride,
                   void* stream);
 
+/* ---- periodic blur, operators.py:109-184 -----------------------------------
+ * psb_blur2d: blur_forward (adjoint = 0) / blur_adjoint (adjoint = 1) of n
+ *   images with the reference's 2-D tap order (bit-exact in fp64).
+ *   taps2d: HOST double[ksize*ksize], row-major, odd ksize <= 15.
+ * psb_blur_grad2d: the fidelity gradient g = A^T (A u - b) (problems.py:121).
+ *   separable != 0: one fused kernel with the 1-D factor taps1d (HOST
+ *   double[ksize], w = taps1d taps1d^T); separable == 0: the direct order via
+ *   `scratch` (device, H*W elements). */
+int psb_blur2d(int dtype, const void* u, void* out, int64_t n, int H, int W, const double* taps2d,
+               int ksize, int adjoint, void* stream);
+int psb_blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
+                    const double* taps2d, const double* taps1d, int ksize, int separable,
+                    void* scratch, void* stream);
+
 /* ---- reductions (fp64 accumulation, deterministic two-pass) ---------------
  * per-problem results are written to the DEVICE array out[n].
  * psb_sumsq: sum((a-b)^2) (b may be NULL) -- tensor.py:28-30, 42-51 building block
@@ -150,6 +164,19 @@ int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void
                              int accelerated, int nonneg, double* last_weight_host,
                              int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
                              double* elapsed_host, double* fgp_time_host, void* stream);
+
+/* psb_proxskip_deblur_run: the same native driver for the implicit TV
+ *   deblurring problem (BASELINE config 2): A = periodic blur, one problem,
+ *   the gradient A^T(Ax - b) recomputed every outer iteration into `g`
+ *   (device, H*W of dtype_outer) by psb_blur_grad2d (`scratch` is needed only
+ *   when separable == 0). */
+int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
+                            void* z, void* q, void* g, void* scratch, int H, int W,
+                            const double* taps2d, const double* taps1d, int ksize, int separable,
+                            const uint8_t* coins_host, int K, double gamma, double p, double alpha,
+                            int n_inner, int accelerated, int nonneg, double* last_weight_host,
+                            int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
+                            double* elapsed_host, double* fgp_time_host, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,209 @@
+// Periodic convolution blur and its fidelity gradient (operators.py:109-184,
+// problems.py:121 -- BASELINE config 2).
+//
+// Two evaluation orders:
+//  * direct  : the reference's 2-D tap loop (a outer, b inner, accumulator
+//              starting at 0, every op rounded) -- bit-identical to
+//              blur_forward/blur_adjoint in the fp64 instantiation;
+//  * separable: Gaussian kernels are outer products w = w1 w1^T, so the
+//              production path does 2k instead of k^2 MACs per pixel, and the
+//              fidelity gradient g = A^T (A u - b) is ONE fused kernel: a CTA
+//              stages its u tile plus a 2R halo (periodic wrap) in shared
+//              memory, forms r = A u - b on the tile plus an R halo, and then
+//              applies the flipped (correlation) pass to produce g -- u, b
+//              read once, g written once (12 B/px fp32, 24 B/px fp64).
+#include "common.cuh"
+
+namespace psb {
+
+namespace {
+
+constexpr int KMAX = 15;
+
+struct Taps {
+  int k;
+  double w2[KMAX * KMAX];
+  double w1[KMAX];
+};
+
+__device__ __forceinline__ int wrap(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+// operators.py:149-158 / 161-172 in the reference order.
+template <class T>
+__global__ void blur_direct_kernel(const T* __restrict__ u, T* __restrict__ out, int64_t n, int H,
+                                   int W, Taps t, int adjoint) {
+  using A = Ar<T>;
+  const int c = t.k / 2;
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * HW;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx / HW;
+    const int i = (int)((idx % HW) / W), j = (int)(idx % W);
+    const T* up = u + p * HW;
+    T acc = T(0);
+    for (int a = 0; a < t.k; ++a) {
+      const int ii = adjoint ? wrap(i + a - c, H) : wrap(i - a + c, H);
+      for (int b = 0; b < t.k; ++b) {
+        const T w = (T)t.w2[a * t.k + b];
+        if (w == T(0)) continue;
+        const int jj = adjoint ? wrap(j + b - c, W) : wrap(j - b + c, W);
+        acc = A::add(acc, A::mul(w, up[(int64_t)ii * W + jj]));
+      }
+    }
+    out[idx] = acc;
+  }
+}
+
+// Fused g = A^T (A u - b) (or r = A u - b only when `fwd_only`), separable.
+template <class T, int TS>
+__global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict__ u,
+                                                            const T* __restrict__ bdat,
+                                                            T* __restrict__ g, int H, int W,
+                                                            Taps t) {
+  extern __shared__ unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  const int R = t.k / 2;
+  const int NU = TS + 4 * R;  // u tile side (2R halo each side)
+  const int NR = TS + 2 * R;  // r tile side
+  T* su = sm;                 // NU x NU
+  T* sh = su + NU * NU;       // NU rows x NR cols  (row pass of A)
+  T* sr = sh + NU * NR;       // NR x NR            (r = A u - b)
+  T* sh2 = sr + NR * NR;      // NR rows x TS cols  (row pass of A^T)
+#define w1(q) ((T)t.w1[q])  // kernel-parameter (constant bank) reads
+
+  const int i0 = blockIdx.y * TS, j0 = blockIdx.x * TS;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < NU * NU; e += nt) {
+    const int a = e / NU, b = e % NU;
+    su[e] = u[(int64_t)wrap(i0 - 2 * R + a, H) * W + wrap(j0 - 2 * R + b, W)];
+  }
+  __syncthreads();
+  // forward A: out(i,j) = sum_a sum_b w1[a] w1[b] u(i-a+c, j-b+c)
+  for (int e = tid; e < NU * NR; e += nt) {
+    const int a = e / NR, jc = e % NR;  // jc: r-tile column; u column jc + R + (c - b)
+    T acc = T(0);
+    for (int q = 0; q < t.k; ++q) acc += w1(q) * su[a * NU + jc + R + (R - q)];
+    sh[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < NR * NR; e += nt) {
+    const int ic = e / NR, jc = e % NR;
+    T acc = T(0);
+    for (int q = 0; q < t.k; ++q) acc += w1(q) * sh[(ic + R + (R - q)) * NR + jc];
+    const int gi = wrap(i0 - R + ic, H), gj = wrap(j0 - R + jc, W);
+    sr[e] = acc - bdat[(int64_t)gi * W + gj];
+  }
+  __syncthreads();
+  // adjoint A^T: out(i,j) = sum_a sum_b w1[a] w1[b] r(i+a-c, j+b-c)
+  for (int e = tid; e < NR * TS; e += nt) {
+    const int ic = e / TS, jt = e % TS;
+    T acc = T(0);
+    for (int q = 0; q < t.k; ++q) acc += w1(q) * sr[ic * NR + jt + q];
+    sh2[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < TS * TS; e += nt) {
+    const int it = e / TS, jt = e % TS;
+    const int gi = i0 + it, gj = j0 + jt;
+    if (gi >= H || gj >= W) continue;
+    T acc = T(0);
+    for (int q = 0; q < t.k; ++q) acc += w1(q) * sh2[(it + q) * TS + jt];
+    g[(int64_t)gi * W + gj] = acc;
+  }
+#undef w1
+}
+
+template <class T, int TS>
+size_t sep_smem(int k) {
+  const int R = k / 2, NU = TS + 4 * R, NR = TS + 2 * R;
+  return sizeof(T) * (size_t)(NU * NU + NU * NR + NR * NR + NR * TS);
+}
+
+int make_taps(const double* taps2d, const double* taps1d, int k, Taps& t) {
+  PSB_REQUIRE(k >= 1 && k <= KMAX && (k % 2) == 1, "blur: kernel size must be odd and <= 15");
+  t.k = k;
+  for (int i = 0; i < k * k; ++i) t.w2[i] = taps2d ? taps2d[i] : 0.0;
+  for (int i = 0; i < k; ++i) t.w1[i] = taps1d ? taps1d[i] : 0.0;
+  return PSB_OK;
+}
+
+template <class T>
+int launch_sep(const void* u, const void* b, void* g, int H, int W, const Taps& t, cudaStream_t st) {
+  constexpr int TS = 32;
+  const size_t sm = sep_smem<T, TS>(t.k);
+  PSB_CUDA(cudaFuncSetAttribute(blur_grad_sep_kernel<T, TS>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  dim3 grid((W + TS - 1) / TS, (H + TS - 1) / TS);
+  blur_grad_sep_kernel<T, TS><<<grid, 256, sm, st>>>((const T*)u, (const T*)b, (T*)g, H, W, t);
+  PSB_LAUNCHED("blur_grad_sep");
+  return PSB_OK;
+}
+
+}  // namespace
+
+int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
+                const double* taps2d, const double* taps1d, int k, int separable, void* scratch,
+                cudaStream_t st);
+
+}  // namespace psb
+
+extern "C" {
+
+int psb_blur2d(int dtype, const void* u, void* out, int64_t n, int H, int W, const double* taps2d,
+               int ksize, int adjoint, void* stream) {
+  psb::Taps t;
+  int rc = psb::make_taps(taps2d, nullptr, ksize, t);
+  if (rc) return rc;
+  PSB_REQUIRE(ksize <= H && ksize <= W, "blur: kernel size exceeds image");
+  const int64_t cnt = n * (int64_t)H * W;
+  if (cnt == 0) return PSB_OK;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, 64LL * psb::sm_count())));
+  auto st = psb::as_stream(stream);
+  if (dtype == PSB_F32)
+    psb::blur_direct_kernel<float><<<grid, 256, 0, st>>>((const float*)u, (float*)out, n, H, W, t, adjoint);
+  else if (dtype == PSB_F64)
+    psb::blur_direct_kernel<double><<<grid, 256, 0, st>>>((const double*)u, (double*)out, n, H, W, t, adjoint);
+  else
+    return psb::fail(PSB_ERR_VALUE, "blur: unknown dtype");
+  PSB_LAUNCHED("blur_direct");
+  return PSB_OK;
+}
+
+int psb_blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
+                    const double* taps2d, const double* taps1d, int ksize, int separable,
+                    void* scratch, void* stream) {
+  return psb::blur_grad2d(dtype, u, b, g, H, W, taps2d, taps1d, ksize, separable, scratch,
+                          psb::as_stream(stream));
+}
+
+}  // extern "C"
+
+namespace psb {
+
+// g = A^T (A u - b).  separable: one fused kernel.  direct: the reference
+// order (forward into `scratch`, subtract b, adjoint), bit-exact in fp64.
+int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
+                const double* taps2d, const double* taps1d, int k, int separable, void* scratch,
+                cudaStream_t st) {
+  Taps t;
+  int rc = make_taps(taps2d, taps1d, k, t);
+  if (rc) return rc;
+  PSB_REQUIRE(k <= H && k <= W, "blur: kernel size exceeds image");
+  if (separable) {
+    PSB_REQUIRE(taps1d != nullptr, "blur: separable mode needs 1-D taps");
+    if (dtype == PSB_F32) return launch_sep<float>(u, b, g, H, W, t, st);
+    if (dtype == PSB_F64) return launch_sep<double>(u, b, g, H, W, t, st);
+    return fail(PSB_ERR_VALUE, "blur: unknown dtype");
+  }
+  PSB_REQUIRE(scratch != nullptr, "blur: direct mode needs an (H, W) scratch buffer");
+  rc = psb_blur2d(dtype, u, scratch, 1, H, W, taps2d, k, 0, st);
+  if (rc) return rc;
+  rc = psb_lincomb(dtype, 1.0, scratch, -1.0, b, scratch, (int64_t)H * W, st);
+  if (rc) return rc;
+  return psb_blur2d(dtype, scratch, g, 1, H, W, taps2d, k, 1, st);
+}
+
+}  // namespace psb

@@ -25,6 +25,22 @@ int proxskip_post(int dto, int dtf, void* x, const void* gb, int ident, void* h,
                   int n_inner, int nonneg, double gamma, double pg, int32_t* bad, int k,
                   cudaStream_t st);
 void fista_betas(int n, double* out);
+int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
+                const double* taps2d, const double* taps1d, int k, int separable, void* scratch,
+                cudaStream_t st);
+
+// Fidelity A of the implicit splitting.  kind 0: identity (g = x - b fused
+// into the outer kernels); kind 1: periodic blur (g = A^T(Ax - b) by the
+// fused separable kernel, or the bit-exact direct path, into `g`).
+struct Fidelity {
+  int kind = 0;
+  const double* taps2d = nullptr;
+  const double* taps1d = nullptr;
+  int ksize = 0;
+  int separable = 1;
+  void* g = nullptr;
+  void* scratch = nullptr;
+};
 
 namespace {
 
@@ -37,11 +53,12 @@ struct DevBuf {
 
 }  // namespace
 
-int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void* z, void* q,
-                         int64_t n, int H, int W, const uint8_t* coins_host, int K, double gamma,
-                         double p, double alpha, int n_inner, int accelerated, int nonneg,
-                         double* last_weight, int64_t* prox_count, int32_t* bad, int use_graph,
-                         double* elapsed, double* fgp_time, cudaStream_t user_stream) {
+int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* b, void* h, void* z,
+                    void* q, int64_t n, int H, int W, const uint8_t* coins_host, int K,
+                    double gamma, double p, double alpha, int n_inner, int accelerated, int nonneg,
+                    double* last_weight, int64_t* prox_count, int32_t* bad, int use_graph,
+                    double* elapsed, double* fgp_time, cudaStream_t user_stream) {
+  PSB_REQUIRE(fid.kind == 0 || n == 1, "proxskip run: a blur fidelity runs one problem at a time");
   PSB_REQUIRE(gamma > 0, "run_proxskip: gamma must be positive");
   PSB_REQUIRE(p > 0 && p <= 1, "SkipConfig: p must be in (0, 1]");
   PSB_REQUIRE(alpha > 0, "build_tv_recon: alpha must be positive");
@@ -130,8 +147,14 @@ int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void
   int rc = PSB_OK;
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
     if (elapsed && k > 0) cudaEventRecordWithFlags(evs[k], st, rec_flags);
-    rc = proxskip_pre(dto, dtf, x, b, 1, h, z, n, HW, coins_d + (int64_t)k * n, gamma, hcoef, bad,
-                      k, st);
+    const int ident = fid.kind == 0;
+    if (!ident) {
+      rc = blur_grad2d(dto, x, b, fid.g, H, W, fid.taps2d, fid.taps1d, fid.ksize, fid.separable,
+                       fid.scratch, st);
+      if (rc) break;
+    }
+    rc = proxskip_pre(dto, dtf, x, ident ? b : fid.g, ident, h, z, n, HW, coins_d + (int64_t)k * n,
+                      gamma, hcoef, bad, k, st);
     const int na = (int)(off[k + 1] - off[k]);
     if (rc || na == 0) continue;
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
@@ -142,8 +165,8 @@ int proxskip_denoise_run(int dto, int dtf, void* x, const void* b, void* h, void
     }
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
     if (rc == PSB_OK)
-      rc = proxskip_post(dto, dtf, x, b, 1, h, z, q, qps, act_d + off[k], na, H, W, n_inner,
-                         nonneg, gamma, pg, bad, k, st);
+      rc = proxskip_post(dto, dtf, x, ident ? b : fid.g, ident, h, z, q, qps, act_d + off[k], na,
+                         H, W, n_inner, nonneg, gamma, pg, bad, k, st);
   }
 
   if (elapsed && rc == PSB_OK) cudaEventRecordWithFlags(evs[K], st, rec_flags);
@@ -212,8 +235,31 @@ extern "C" int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x,
                                         double* last_weight_host, int64_t* prox_count_host,
                                         int32_t* bad_iter, int use_graph, double* elapsed_host,
                                         double* fgp_time_host, void* stream) {
-  return psb::proxskip_denoise_run(dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
-                                   gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
-                                   prox_count_host, bad_iter, use_graph, elapsed_host,
-                                   fgp_time_host, psb::as_stream(stream));
+  psb::Fidelity fid;
+  return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
+                              gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
+                              prox_count_host, bad_iter, use_graph, elapsed_host, fgp_time_host,
+                              psb::as_stream(stream));
+}
+
+extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void* b,
+                                       void* h, void* z, void* q, void* g, void* scratch, int H,
+                                       int W, const double* taps2d, const double* taps1d,
+                                       int ksize, int separable, const uint8_t* coins_host, int K,
+                                       double gamma, double p, double alpha, int n_inner,
+                                       int accelerated, int nonneg, double* last_weight_host,
+                                       int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
+                                       double* elapsed_host, double* fgp_time_host, void* stream) {
+  psb::Fidelity fid;
+  fid.kind = 1;
+  fid.taps2d = taps2d;
+  fid.taps1d = taps1d;
+  fid.ksize = ksize;
+  fid.separable = separable;
+  fid.g = g;
+  fid.scratch = scratch;
+  return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, 1, H, W, coins_host, K,
+                              gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
+                              prox_count_host, bad_iter, use_graph, elapsed_host, fgp_time_host,
+                              psb::as_stream(stream));
 }

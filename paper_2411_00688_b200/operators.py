@@ -91,6 +91,100 @@ def grad_map(shape, norm_sq_estimate=None):
         norm_sq_estimate=norm_sq_estimate, kind="grad")
 
 
+# -- periodic blur (operators.py:109-184) ---------------------------------------
+
+@dataclass
+class BlurKernel:
+    """Odd square kernel, nonnegative weights summing to 1 (operators.py:109-128).
+
+    ``factor`` is the 1-D factor when the kernel is separable (w = f f^T, as
+    for Gaussians); the production gradient kernel then runs 2k instead of
+    k^2 MACs per pixel.
+    """
+
+    weights: np.ndarray
+    factor: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        self.weights = np.asarray(self.weights, dtype=np.float64)
+        s = self.weights.shape
+        if len(s) != 2 or s[0] != s[1] or s[0] % 2 == 0:
+            raise ValueError(f"BlurKernel: weights must be odd and square, got {s}")
+        if np.any(self.weights < 0):
+            raise ValueError("BlurKernel: negative weights")
+        total = float(self.weights.sum())
+        if abs(total - 1.0) > 1e-12:
+            raise ValueError(f"BlurKernel: weights sum to {total}, expected 1")
+        if self.factor is None:
+            f = np.sqrt(np.diag(self.weights))
+            if np.max(np.abs(np.outer(f, f) - self.weights)) <= 1e-15:
+                self.factor = f
+        if s[0] > 15:
+            raise ValueError("BlurKernel: kernels up to 15x15 are supported on the device")
+
+    @property
+    def size(self):
+        return self.weights.shape[0]
+
+
+def gaussian_kernel(size, sigma):
+    """Normalised truncated Gaussian (operators.py:131-137); exact 1-D factor kept."""
+    if size % 2 == 0 or size < 1:
+        raise ValueError(f"gaussian_kernel: size must be odd, got {size}")
+    ax = np.arange(size) - size // 2
+    g = np.exp(-(ax[:, None] ** 2 + ax[None, :] ** 2) / (2.0 * sigma ** 2))
+    e = np.exp(-(ax ** 2) / (2.0 * sigma ** 2))
+    return BlurKernel(g / g.sum(), factor=e / e.sum())
+
+
+def _taps(kernel):
+    w2 = np.ascontiguousarray(kernel.weights, dtype=np.float64)
+    return w2, w2.ctypes.data_as(L.C.c_void_p)
+
+
+def _blur_dev(t, kernel, adjoint):
+    if t.dim() != 2:
+        raise ValueError(f"blur: expected 2-D image, got shape {tuple(t.shape)}")
+    if kernel.size > min(t.shape):
+        raise ValueError(f"blur: kernel size {kernel.size} exceeds image {tuple(t.shape)}")
+    out = torch.empty_like(t)
+    w2, wp = _taps(kernel)
+    L.call("psb_blur2d", L.dcode(t.dtype), L.ptr(t), L.ptr(out), 1, t.shape[0], t.shape[1], wp,
+           kernel.size, int(adjoint), L.stream())
+    return out
+
+
+def blur_forward(u, kernel):
+    """Circular 2-D convolution (operators.py:149-158), reference tap order."""
+    return _wrap(lambda t: _blur_dev(t, kernel, False))(u)
+
+
+def blur_adjoint(r, kernel):
+    """Circular correlation, the adjoint (operators.py:161-172)."""
+    return _wrap(lambda t: _blur_dev(t, kernel, True))(r)
+
+
+def blur_grad_dev(u, b, kernel, separable=True, out=None):
+    """g = A^T (A u - b) in one fused kernel (separable) or the exact tap order."""
+    H, W = u.shape
+    g = torch.empty_like(u) if out is None else out
+    w2, wp = _taps(kernel)
+    sep = separable and kernel.factor is not None
+    f = np.ascontiguousarray(kernel.factor if sep else np.zeros(1), dtype=np.float64)
+    scratch = None if sep else torch.empty_like(u)
+    L.call("psb_blur_grad2d", L.dcode(u.dtype), L.ptr(u), L.ptr(b), L.ptr(g), H, W, wp,
+           f.ctypes.data_as(L.C.c_void_p), kernel.size, int(sep), L.ptr(scratch), L.stream())
+    return g
+
+
+def blur_map(kernel, shape):
+    """LinearMap of the periodic blur (operators.py:175-184); |A| = A."""
+    fwd = _wrap(lambda t: _blur_dev(t, kernel, False))
+    adj = _wrap(lambda t: _blur_dev(t, kernel, True))
+    return LinearMap(tuple(shape), tuple(shape), fwd, adj, abs_forward=fwd, abs_adjoint=adj,
+                     kind="blur", params=kernel)
+
+
 # -- identity (operators.py:297-307) ------------------------------------------
 
 def identity_map(shape):

@@ -72,8 +72,8 @@ def run_proxskip(problem, x0, h0, gamma, skip, iters, log=None, *, use_graph=Non
         raise ValueError("run_proxskip: gamma must be positive")
     log = _ensure_log(log)
     fused = getattr(problem, "_fused", None)
-    if fused is not None and fused.get("kind") == "denoise" and log.passive:
-        return _proxskip_denoise_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph)
+    if fused is not None and fused.get("kind") in ("denoise", "deblur") and log.passive:
+        return _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph)
     log.start(AR.is_host(x0))
     p = skip.p
     coins = skip.coins(iters)
@@ -154,7 +154,10 @@ def _betas(n):
     return out
 
 
-def _proxskip_denoise_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph):
+def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph,
+                       fgp_time=None):
+    """Whole run inside the native driver (psb_proxskip_denoise_run /
+    psb_proxskip_deblur_run): no host round trip per iteration."""
     log.start(AR.is_host(x0))
     st = problem.tv_state
     H, W = st.shape
@@ -170,12 +173,26 @@ def _proxskip_denoise_fused(problem, fused, x0, h0, gamma, skip, iters, log, use
     if use_graph is None:
         use_graph = H * W <= 1024 * 1024
     base_inner = st.total_inner_iterations
-    L.call("psb_proxskip_denoise_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
-           L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), 1, H, W,
-           coins.ctypes.data_as(L.C.c_void_p), iters, float(gamma), float(skip.p),
-           float(problem.alpha), st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)),
-           lw.ctypes.data_as(L.C.c_void_p), pc.ctypes.data_as(L.C.c_void_p), L.ptr(bad),
-           int(bool(use_graph)), elapsed.ctypes.data_as(L.C.c_void_p), None, L.stream())
+    vp = L.C.c_void_p
+    ft = fgp_time.ctypes.data_as(vp) if fgp_time is not None else None
+    common_tail = (coins.ctypes.data_as(vp), iters, float(gamma), float(skip.p),
+                   float(problem.alpha), st.inner_iters, int(bool(st.accelerated)),
+                   int(bool(st.nonneg)), lw.ctypes.data_as(vp), pc.ctypes.data_as(vp), L.ptr(bad),
+                   int(bool(use_graph)), elapsed.ctypes.data_as(vp), ft, L.stream())
+    if fused["kind"] == "denoise":
+        L.call("psb_proxskip_denoise_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
+               L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), 1, H, W, *common_tail)
+    else:
+        ker = fused["kernel"]
+        sep = bool(fused["separable"] and ker.factor is not None)
+        w2 = np.ascontiguousarray(ker.weights, dtype=np.float64)
+        w1 = np.ascontiguousarray(ker.factor if sep else np.zeros(1), dtype=np.float64)
+        g = torch.empty_like(x)
+        scratch = None if sep else torch.empty_like(x)
+        L.call("psb_proxskip_deblur_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
+               L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), L.ptr(g),
+               L.ptr(scratch), H, W, w2.ctypes.data_as(vp), w1.ctypes.data_as(vp), ker.size,
+               int(sep), *common_tail)
     k_bad = int(bad.item())
     if k_bad != INT32_MAX:
         raise DivergenceError(k_bad, "proxskip")
