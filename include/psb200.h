@@ -165,6 +165,49 @@ int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void
                              int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
                              double* elapsed_host, double* fgp_time_host, void* stream);
 
+/* ---- parallel-beam projector, operators.py:189-292 (matrix-free) ------------
+ * Geometry of RadonGeometry (operators.py:189-215) plus the sample lattice of
+ * radon_system_matrix (operators.py:224-229): `tables` is a DEVICE double
+ * array [offsets (n_bins) | steps (n_steps) | cos(angles) | sin(angles)]
+ * computed on the host with numpy exactly as the reference does, so sample
+ * positions are bit-identical.  step_spacing = 2*half_span/(n_steps-1). */
+typedef struct psb_radon_geom {
+  int n;
+  int n_angles;
+  int n_bins;
+  int n_steps;
+  double center;
+  double half_span;
+  double step_spacing;
+  double bin_spacing;
+  const double* tables;
+} psb_radon_geom;
+
+/* psb_radon_fwd: sino = A img (CSR SpMV of operators.py:273-277, ray-driven)
+ * psb_radon_adj: img = A^T sino (operators.py:279-283, pixel-driven gather,
+ *   the exact transpose of psb_radon_fwd's weights) */
+int psb_radon_fwd(int dtype, const psb_radon_geom* geom, const void* img, void* sino, void* stream);
+int psb_radon_adj(int dtype, const psb_radon_geom* geom, const void* sino, void* img, void* stream);
+
+/* ---- PDHG / PDHGSkip-2 on K = [A; D] (explicit splitting, BASELINE config 3)
+ * y is the reference's flat dual [y_A (n_angles*n_bins) | y_D (2*n*n)]
+ * (problems.py:136-146); b the sinogram.  One step =
+ *   primal (fused A^T y_A - div y_D, prox_g = max(., 0) when nonneg, the
+ *   ProxSkip control variate when h != NULL, xbar = 2x' - x),
+ *   dual fidelity ((y_A + tau A xbar) - tau b)/(1 + tau),
+ *   dual TV P_alpha(y_D + tau grad xbar).
+ * h == NULL: plain PDHG (solvers.py:187-209); else PDHGSkip-2 (skip.py:117-150)
+ * with coin = this iteration's Bernoulli draw, hcoef = sigma - sigma/p,
+ * ps = p/sigma.  psb_pdhg_run loops K steps (coins_host: host uint8[K]; skip=0
+ * runs PDHG), optionally as one CUDA graph. */
+int psb_pdhg_step(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
+                  const void* b, int32_t* bad_iter, int k, int coin, double sigma, double tau,
+                  double hcoef, double ps, double alpha, int nonneg, void* stream);
+int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
+                 const void* b, const uint8_t* coins_host, int K, double sigma, double tau,
+                 double p, double alpha, int nonneg, int skip, int32_t* bad_iter, int use_graph,
+                 double* elapsed_host, void* stream);
+
 /* psb_proxskip_deblur_run: the same native driver for the implicit TV
  *   deblurring problem (BASELINE config 2): A = periodic blur, one problem,
  *   the gradient A^T(Ax - b) recomputed every outer iteration into `g`

@@ -356,8 +356,10 @@ class Recon:
 
 
 def make_recon(A: Op, b, alpha, nonneg=False, splitting="implicit", inner=100,
-               accelerated=True):
-    """build_tv_recon (problems.py:101-159)."""
+               accelerated=True, K_nsq=None):
+    """build_tv_recon (problems.py:101-159).  ``K_nsq`` (test convenience)
+    seeds the cached ||K||^2 of the explicit splitting instead of running the
+    power method, exactly like setting LinearMap.norm_sq_estimate."""
     if alpha <= 0:
         raise ValueError("make_recon: alpha must be positive")
     b = np.asarray(b, np.float64)
@@ -384,6 +386,8 @@ def make_recon(A: Op, b, alpha, nonneg=False, splitting="implicit", inner=100,
         pr.prox_fstar = pfs
         pr.prox_g = (lambda u, s: clamp_nonneg(u)) if nonneg else (
             lambda u, s: np.array(u, dtype=np.float64))
+        if K_nsq is not None:
+            K.nsq = K_nsq
         pr.K_nsq = K.norm_sq()
     else:
         raise ValueError(f"make_recon: unknown splitting {splitting!r}")

@@ -11,9 +11,9 @@ library raises.
 from . import _lib  # noqa: F401  (fails loudly when libpsb200.so is missing)
 from .batched import BatchedTvDenoise, coin_table, run_proxskip_batched, shard_indices
 from .errors import DivergenceError, ReferenceRejectedError
-from .operators import (BlurKernel, LinearMap, blur_adjoint, blur_forward, blur_map, block_stack,
-                        divergence, gaussian_kernel, grad_forward, grad_map, identity_map,
-                        power_method)
+from .operators import (BlurKernel, LinearMap, RadonGeometry, blur_adjoint, blur_forward, blur_map,
+                        block_stack, divergence, gaussian_kernel, grad_forward, grad_map,
+                        identity_map, power_method, radon_map)
 from .problems import (GRAD_NORM_SQ, TvReconstructionProblem, build_tv_recon,
                        build_tv_saddle_implicit, objective_tv)
 from .proximal import project_ball, project_nonneg, prox_zero

@@ -23,6 +23,18 @@ F32, F64 = 0, 1
 
 _vp, _i32, _i64, _dbl = C.c_void_p, C.c_int, C.c_int64, C.c_double
 
+
+class RadonGeom(C.Structure):
+    """Mirror of psb_radon_geom (include/psb200.h)."""
+
+    _fields_ = [("n", C.c_int), ("n_angles", C.c_int), ("n_bins", C.c_int),
+                ("n_steps", C.c_int), ("center", C.c_double), ("half_span", C.c_double),
+                ("step_spacing", C.c_double), ("bin_spacing", C.c_double),
+                ("tables", C.c_void_p)]
+
+
+_geo = C.POINTER(RadonGeom)
+
 # name -> argtypes, mirroring include/psb200.h one for one.
 SIGNATURES = {
     "psb_abi_version": [],
@@ -50,6 +62,12 @@ SIGNATURES = {
     "psb_proxskip_denoise_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp,
                                  _i32, _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32,
                                  _vp, _vp, _vp],
+    "psb_radon_fwd": [_i32, _geo, _vp, _vp, _vp],
+    "psb_radon_adj": [_i32, _geo, _vp, _vp, _vp],
+    "psb_pdhg_step": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _dbl, _dbl, _dbl, _dbl,
+                      _dbl, _i32, _vp],
+    "psb_pdhg_run": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl, _dbl, _dbl, _dbl, _i32,
+                     _i32, _vp, _i32, _vp, _vp],
     "psb_blur2d": [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _i32, _i32, _vp],
     "psb_blur_grad2d": [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _vp],
     "psb_proxskip_deblur_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp,

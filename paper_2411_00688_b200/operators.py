@@ -185,6 +185,84 @@ def blur_map(kernel, shape):
                      kind="blur", params=kernel)
 
 
+# -- parallel-beam Radon transform (operators.py:189-292) ---------------------
+
+@dataclass
+class RadonGeometry:
+    """Parallel-beam geometry on a square image (operators.py:189-215)."""
+
+    image_side: int
+    n_angles: int
+    n_bins: int
+    bin_spacing: float = 1.0
+    angles: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        if self.image_side < 2 or self.n_angles < 1:
+            raise ValueError("RadonGeometry: need image_side >= 2 and n_angles >= 1")
+        if self.n_bins < self.image_side:
+            raise ValueError(f"RadonGeometry: n_bins {self.n_bins} < image_side {self.image_side}")
+        if self.angles is None:
+            self.angles = np.arange(self.n_angles) * (np.pi / self.n_angles)
+        else:
+            self.angles = np.asarray(self.angles, dtype=np.float64)
+            if np.any(np.diff(self.angles) <= 0):
+                raise ValueError("RadonGeometry: angles must be strictly increasing")
+        self._dev = None
+
+    def device(self):
+        """(ctypes psb_radon_geom, device tables) -- the ray-sample lattice of
+        radon_system_matrix (operators.py:224-229) computed with numpy as the
+        reference does, so device sample positions are bit-identical."""
+        if self._dev is None:
+            n = self.image_side
+            center = (n - 1) / 2.0
+            half_span = n / np.sqrt(2.0)
+            n_steps = int(np.ceil(2.0 * half_span)) + 1
+            steps = np.linspace(-half_span, half_span, n_steps)
+            offsets = (np.arange(self.n_bins) - (self.n_bins - 1) / 2.0) * self.bin_spacing
+            # per-angle scalar cos/sin exactly as the reference loop evaluates them
+            cs = np.array([np.cos(t) for t in self.angles])
+            sn = np.array([np.sin(t) for t in self.angles])
+            tab = np.concatenate([offsets, steps, cs, sn])
+            tdev = AR.to_dev(tab, torch.float64)
+            g = L.RadonGeom(n, len(self.angles), self.n_bins, n_steps, center, half_span,
+                            2.0 * half_span / (n_steps - 1), float(self.bin_spacing),
+                            tdev.data_ptr())
+            self._dev = (g, tdev)
+        return self._dev
+
+    @property
+    def sinogram_shape(self):
+        return (len(self.angles), self.n_bins)
+
+
+def _radon_dev(geom, t, adjoint):
+    g, _ = geom.device()
+    n = geom.image_side
+    if adjoint:
+        if tuple(t.shape) != geom.sinogram_shape:
+            raise ValueError(f"radon adjoint: expected {geom.sinogram_shape}, got {tuple(t.shape)}")
+        out = torch.empty((n, n), dtype=t.dtype, device="cuda")
+        L.call("psb_radon_adj", L.dcode(t.dtype), L.C.byref(g), L.ptr(t), L.ptr(out), L.stream())
+    else:
+        if tuple(t.shape) != (n, n):
+            raise ValueError(f"radon forward: expected {(n, n)}, got {tuple(t.shape)}")
+        out = torch.empty(geom.sinogram_shape, dtype=t.dtype, device="cuda")
+        L.call("psb_radon_fwd", L.dcode(t.dtype), L.C.byref(g), L.ptr(t), L.ptr(out), L.stream())
+    return out
+
+
+def radon_map(geom):
+    """Matrix-free projector pair with the reference's ray-driven bilinear
+    weights (operators.py:266-292); |A| = A (weights are nonnegative)."""
+    n = geom.image_side
+    fwd = _wrap(lambda t: _radon_dev(geom, t, False))
+    adj = _wrap(lambda t: _radon_dev(geom, t, True))
+    return LinearMap((n, n), geom.sinogram_shape, fwd, adj, abs_forward=fwd, abs_adjoint=adj,
+                     kind="radon", params=geom)
+
+
 # -- identity (operators.py:297-307) ------------------------------------------
 
 def identity_map(shape):

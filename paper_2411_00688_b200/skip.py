@@ -241,5 +241,48 @@ def run_pdhgskip2(problem, x0, y0, h0, sigma, tau, skip, iters, log=None):
     return AR.like(x, x0), log
 
 
-def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo):
-    raise NotImplementedError("fused PDHG path not built yet")
+def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, use_graph=True):
+    """PDHG (skip is None) / PDHGSkip-2 on K = [A; D] with the fused kernels of
+    csrc/radon.cu.  Passive logs run the whole loop natively (psb_pdhg_run);
+    observing logs step it from here with the same kernels."""
+    f = problem._fused
+    dt = f["dtype"]
+    log = _ensure_log(log)
+    log.start(AR.is_host(x0))
+    g, _ = f["geom"].device()
+    x = AR.to_dev(x0, dt).clone()
+    y = AR.to_dev(y0, dt).clone().reshape(-1)
+    is_skip = skip is not None
+    h = None
+    if is_skip:
+        h = AR.to_dev(h0, dt).clone() if h0 is not None else torch.zeros_like(x)
+    xbar = torch.empty_like(x)
+    bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
+    p = skip.p if is_skip else 1.0
+    coins = skip.coins(iters) if is_skip else np.ones(iters, dtype=np.uint8)
+    if log.passive:
+        elapsed = np.zeros(max(iters, 1))
+        L.call("psb_pdhg_run", L.dcode(dt), L.C.byref(g), L.ptr(x), L.ptr(y), L.ptr(h), L.ptr(xbar),
+               L.ptr(f["b_dev"]), coins.ctypes.data_as(L.C.c_void_p), iters, float(sigma),
+               float(tau), float(p), float(f["alpha"]), int(bool(f["nonneg"])), int(is_skip),
+               L.ptr(bad), int(bool(use_graph)), elapsed.ctypes.data_as(L.C.c_void_p), L.stream())
+        k_bad = int(bad.item())
+        if k_bad != INT32_MAX:
+            raise DivergenceError(k_bad, algo)
+        _finish_passive(log, coins[:iters], elapsed, 0, 0)
+    else:
+        hc = sigma - sigma / p if is_skip else 0.0
+        ps = p / sigma if is_skip else 0.0
+        n_prox = 0
+        for k in range(iters):
+            th = int(coins[k])
+            L.call("psb_pdhg_step", L.dcode(dt), L.C.byref(g), L.ptr(x), L.ptr(y), L.ptr(h),
+                   L.ptr(xbar), L.ptr(f["b_dev"]), L.ptr(bad), k, th, float(sigma), float(tau),
+                   float(hc), float(ps), float(f["alpha"]), int(bool(f["nonneg"])), L.stream())
+            n_prox += th
+            if int(bad.item()) != INT32_MAX:
+                raise DivergenceError(k, algo)
+            if log.observe(k + 1, x, n_prox, bool(th)):
+                break
+    log.y_final = y
+    return AR.like(x, x0), log
