@@ -208,6 +208,24 @@ int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* 
                  double p, double alpha, int nonneg, int skip, int32_t* bad_iter, int use_graph,
                  double* elapsed_host, void* stream);
 
+/* ---- 3-D TV prox + ProxSkip for BASELINE config 5 -----
+ * Volume (D, H, W) with dual channels (z, y, x), dual step 1/12 (pass it as
+ * `step`), the 2-D reference algorithm otherwise.  Slots as in 2-D, each of
+ * (3, D, H, W).  z-slab decomposition: this call owns planes [z0, z0+D) of a
+ * volume of depth Dg; halo_below_* are plane z0-1 of q_it / q_{it-1} (3, H, W)
+ * (NULL when z0 == 0), halo_above_* plane z0+D of q_it / q_{it-1} and of x
+ * (NULL when z0+D == Dg).  zchunk <= 0 picks the z-chunk per CTA.
+ * psb_proxskip_post3d: identity-fidelity ProxSkip post fused with the 3-D
+ * finalize; halo_below_qn = plane z0-1 of the final dual iterate. */
+int psb_fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z0, int Dg, int it,
+                   double beta_prev, double step, double weight, int reproject, int nonneg,
+                   const void* halo_below_qk, const void* halo_below_qm, const void* halo_above_qk,
+                   const void* halo_above_qm, const void* halo_above_x, int zchunk, void* stream);
+int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
+                        const void* z, void* q, const void* halo_below_qn, int D, int H, int W,
+                        int z0, int Dg, int n_inner, int nonneg, double gamma, double pg,
+                        int32_t* bad_iter, int k, void* stream);
+
 /* psb_proxskip_deblur_run: the same native driver for the implicit TV
  *   deblurring problem (BASELINE config 2): A = periodic blur, one problem,
  *   the gradient A^T(Ax - b) recomputed every outer iteration into `g`
