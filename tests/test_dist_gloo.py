@@ -1,0 +1,191 @@
+"""Multi-rank paths on CPU with the gloo backend (world_size 2 and 3).
+
+* config 4 (batched): problem sharding covers every problem exactly once and
+  needs no collective on the data path;
+* config 5 (z-slabs): ``DistExchange`` -- the exact halo exchange the GPU
+  run uses over NCCL -- drives a slab-decomposed FGP whose per-slab compute is
+  the CPU oracle; the result must equal the whole-volume oracle bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import tv3d_cpu as o3
+from oracle.imgskip_cpu import fista_betas
+
+from paper_2411_00688_b200.volume3d import DistExchange, slab_bounds
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_iter(x, qk, qm, beta, w, step=o3.STEP_3D):
+    """One accelerated FGP inner iteration on a full volume (tv.py:75-80 in 3-D)."""
+    y = qk if beta == 0.0 else qk + beta * (qk - qm)
+    return o3.ball_project3(y + step * o3.fd_grad3(x + o3.fd_div3(y)), w)
+
+
+class OracleSlab:
+    """CPU stand-in for Slab3D with the same exchange interface; compute by
+    embedding the slab + halos into a zero volume and running the oracle."""
+
+    def __init__(self, x_full, z0, z1, n_inner):
+        self.Dg, self.H, self.W = x_full.shape
+        self.z0, self.z1 = z0, z1
+        self.x = torch.from_numpy(x_full[z0:z1].copy())
+        self.q = torch.zeros((3, 3, z1 - z0, self.H, self.W), dtype=torch.float64)
+        self.has_below, self.has_above = z0 > 0, z1 < self.Dg
+        plane = (self.H, self.W)
+        self.hb = torch.zeros((6,) + plane, dtype=torch.float64) if self.has_below else None
+        self.ha = torch.zeros((6,) + plane, dtype=torch.float64) if self.has_above else None
+        self.hx = torch.zeros(plane, dtype=torch.float64) if self.has_above else None
+        self.hqn = torch.zeros((3,) + plane, dtype=torch.float64) if self.has_below else None
+        self.inner = n_inner
+
+    def edge_planes(self, it):
+        qk, qm = self.q[it % 3], self.q[(it + 2) % 3]
+        bot = torch.cat([qk[:, 0], qm[:, 0]]) if self.has_below else None
+        top = torch.cat([qk[:, -1], qm[:, -1]]) if self.has_above else None
+        return bot, top
+
+    def set_halos(self, below, above):
+        if self.has_below:
+            self.hb.copy_(below)
+        if self.has_above:
+            self.ha.copy_(above)
+
+    def prox_input_bottom(self):
+        return self.x[0] if self.has_below else None
+
+    def set_prox_input_above(self, plane):
+        if self.has_above:
+            self.hx.copy_(plane)
+
+    def final_dual_top(self):
+        return self.q[self.inner % 3][:, -1] if self.has_above else None
+
+    def set_final_dual_below(self, plane):
+        if self.has_below:
+            self.hqn.copy_(plane)
+
+    def step(self, it, beta, w):
+        X = np.zeros((self.Dg, self.H, self.W))
+        QK = np.zeros((3, self.Dg, self.H, self.W))
+        QM = np.zeros_like(QK)
+        X[self.z0:self.z1] = self.x.numpy()
+        QK[:, self.z0:self.z1] = self.q[it % 3].numpy()
+        QM[:, self.z0:self.z1] = self.q[(it + 2) % 3].numpy()
+        if self.has_below:
+            QK[:, self.z0 - 1] = self.hb[0:3].numpy()
+            QM[:, self.z0 - 1] = self.hb[3:6].numpy()
+        if self.has_above:
+            QK[:, self.z1] = self.ha[0:3].numpy()
+            QM[:, self.z1] = self.ha[3:6].numpy()
+            X[self.z1] = self.hx.numpy()
+        out = _oracle_iter(X, QK, QM, beta, w)
+        self.q[(it + 1) % 3] = torch.from_numpy(out[:, self.z0:self.z1].copy())
+
+    def finalize(self):
+        """u = x + div q_n on the slab (the z-term below needs the halo)."""
+        Q = np.zeros((3, self.Dg, self.H, self.W))
+        Q[:, self.z0:self.z1] = self.q[self.inner % 3].numpy()
+        if self.has_below:
+            Q[:, self.z0 - 1] = self.hqn.numpy()
+        return self.x.numpy() + o3.fd_div3(Q)[self.z0:self.z1]
+
+
+def _worker(rank, world, port, shape, n_inner, w, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x_full = np.random.default_rng(7).standard_normal(shape)
+        z0, z1 = slab_bounds(shape[0], rank, world)
+        slab = OracleSlab(x_full, z0, z1, n_inner)
+        ex = DistExchange()
+        betas = fista_betas(n_inner)
+        ex.prox_input([slab])
+        for it in range(n_inner):
+            ex.halos([slab], it)
+            slab.step(it, betas[it - 1] if it > 0 else 0.0, w)
+        ex.final_dual([slab])
+        u = slab.finalize()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (z0, z1, u, slab.q[n_inner % 3].numpy()))
+        if rank == 0:
+            out_q.put(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_exchange_matches_whole_volume(world):
+    shape, n_inner, w = (11, 6, 9), 6, 0.3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, n_inner, w, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x_full = np.random.default_rng(7).standard_normal(shape)
+    st = o3.Fgp3State.zeros(shape, n_inner)
+    u_ref = o3.fgp_prox3(x_full, w, st)
+    for z0, z1, u, qn in gathered:
+        np.testing.assert_array_equal(u, u_ref[z0:z1])
+        np.testing.assert_array_equal(qn, st.q[:, z0:z1])
+
+
+def _shard_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_00688_b200.batched import shard_indices
+        mine = shard_indices(4096, rank, world)
+        n = torch.tensor([len(mine)], dtype=torch.int64)
+        dist.all_reduce(n)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine.tolist())
+        if rank == 0:
+            out_q.put((int(n.item()), gathered))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_problem_sharding_two_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    total, parts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert total == 4096
+    assert sorted(parts[0] + parts[1]) == list(range(4096))
+    assert not set(parts[0]) & set(parts[1])
+
+
+def test_slab_bounds():
+    for Dg, world in [(1024, 8), (23, 5), (7, 7)]:
+        b = [slab_bounds(Dg, r, world) for r in range(world)]
+        assert b[0][0] == 0 and b[-1][1] == Dg
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))

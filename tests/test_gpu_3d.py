@@ -1,0 +1,77 @@
+"""GPU parity for the 3-D path (BASELINE config 5): the 3-D FGP kernel against
+the oracle restatement (oracle/tv3d_cpu.py, itself pinned to the reference's
+2-D prox), and the z-slab decomposition against the whole volume."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2411_00688_b200 as psb  # noqa: E402,F401
+from paper_2411_00688_b200 import phantoms, volume3d as v3  # noqa: E402
+from oracle import tv3d_cpu as o3  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def test_plane_constant_volume_equals_reference_2d(golden):
+    x2 = golden["tv_x"]
+    vol = np.broadcast_to(x2, (4,) + x2.shape).copy()
+    st = v3.TvProxState3D(vol.shape, 7, dtype=torch.float64, step=0.125)
+    u = v3.tv_prox3d(vol, 0.3, st)
+    for z in range(4):
+        np.testing.assert_array_equal(u[z], golden["tv_u1"])
+    np.testing.assert_array_equal(st.q_warm[0], 0.0)
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 2), (3, 5, 7), (9, 13, 37), (17, 8, 70)])
+@pytest.mark.parametrize("inner", [1, 3])
+def test_tv_prox3d_fp64_bitwise(shape, inner):
+    rng = np.random.default_rng(sum(shape) + inner)
+    x = rng.standard_normal(shape)
+    st = v3.TvProxState3D(shape, inner, dtype=torch.float64)
+    so = o3.Fgp3State.zeros(shape, inner)
+    for w in (0.2, 0.2, 0.05):
+        np.testing.assert_array_equal(v3.tv_prox3d(x, w, st), o3.fgp_prox3(x, w, so))
+        np.testing.assert_array_equal(st.q_warm, so.q)
+
+
+def test_tv_prox3d_fp32_tolerance():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((40, 48, 64))
+    st = v3.TvProxState3D(x.shape, 20)
+    so = o3.Fgp3State.zeros(x.shape, 20)
+    for _ in range(2):
+        assert rel(v3.tv_prox3d(x, 0.3, st), o3.fgp_prox3(x, 0.3, so)) < 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("n_slabs", [2, 3, 5])
+def test_slab_decomposition_is_exact(precision, n_slabs):
+    vol = phantoms.random_ellipsoids((23, 20, 36), 6, np.random.default_rng(1))
+    b = phantoms.add_noise(vol, 0.1, 1)
+    x1, s1 = v3.proxskip_denoise3d(b, 0.08, 0.3, 4, 20, 5, n_slabs=1, precision=precision)
+    xn, sn = v3.proxskip_denoise3d(b, 0.08, 0.3, 4, 20, 5, n_slabs=n_slabs, precision=precision)
+    np.testing.assert_array_equal(x1, xn)
+    assert s1[0].prox_count == sn[-1].prox_count
+
+
+def test_config5_reduced_size_vs_oracle():
+    """Config 5 inputs at 48^3 (50 ellipsoids, noise 0.1, alpha 0.08, p 0.1,
+    FGP-20, step 1/12, 200 outer) against the 3-D oracle; fp32 device path,
+    2 emulated slabs."""
+    n = 48
+    vol = phantoms.random_ellipsoids((n, n, n), 50, np.random.default_rng(0)).astype(np.float64)
+    b = phantoms.add_noise(vol, 0.1, 0)
+    x, slabs = v3.proxskip_denoise3d(b, 0.08, 0.1, 0, 200, 20, n_slabs=2, precision="fp32")
+    xr, _, n_prox, _ = o3.proxskip_denoise3(b, 0.08, 0.1, 0, 200, 20)
+    assert slabs[0].prox_count == n_prox
+    assert rel(x, xr) < 1e-4
+    obj = lambda u: 0.5 * np.sum((u - b) ** 2) + 0.08 * o3.tv_total3(u)
+    assert abs(obj(x) - obj(xr)) / obj(xr) < 1e-5
