@@ -226,6 +226,11 @@ int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, 
                         int z0, int Dg, int n_inner, int nonneg, double gamma, double pg,
                         int32_t* bad_iter, int k, void* stream);
 
+/* psb_cluster_max_active: how many 16-CTA clusters of the cluster-resident
+ * 256x256 ProxSkip kernel (csrc/fgp_cluster.cu, used by
+ * psb_proxskip_denoise_run for 256x256 fp32-FGP problems) fit on the device. */
+int psb_cluster_max_active(int* out);
+
 /* psb_proxskip_deblur_run: the same native driver for the implicit TV
  *   deblurring problem (BASELINE config 2): A = periodic blur, one problem,
  *   the gradient A^T(Ax - b) recomputed every outer iteration into `g`

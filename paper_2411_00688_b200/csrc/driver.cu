@@ -28,6 +28,15 @@ void fista_betas(int n, double* out);
 int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
                 const double* taps2d, const double* taps1d, int k, int separable, void* scratch,
                 cudaStream_t st);
+bool cluster_shape_ok(int H, int W);
+int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
+                      const int32_t* active, int n_active, const int32_t* pend,
+                      const int32_t* kfirst, const uint8_t* rep, int n_inner, int accelerated,
+                      int nonneg, double weight, double gamma, double hc, double pg, double step,
+                      const float* betas, int32_t* bad, int k, cudaStream_t st);
+int skip_flush(int dto, void* x, const void* b, const void* h, const int32_t* pend,
+               const int32_t* kfirst, int64_t n, int64_t HW, double gamma, int32_t* bad,
+               cudaStream_t st);
 
 // Fidelity A of the implicit splitting.  kind 0: identity (g = x - b fused
 // into the outer kernels); kind 1: periodic blur (g = A^T(Ax - b) by the
@@ -101,7 +110,47 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   std::vector<double> beta(n_inner, 0.0);
   if (accelerated) fista_betas(n_inner, beta.data());
 
-  DevBuf d_coins, d_act, d_rep;
+  // Cluster-resident path (csrc/fgp_cluster.cu): 256 x 256 identity-fidelity
+  // problems with an fp32 FGP.  Skipped iterations are deferred per problem
+  // and executed in registers at the next prox call / the final flush.
+  const char* no_cluster = std::getenv("PSB_NO_CLUSTER");
+  const bool use_cluster = fid.kind == 0 && dtf == PSB_F32 && cluster_shape_ok(H, W) &&
+                           !(no_cluster && no_cluster[0] == '1');
+  std::vector<int32_t> pend, kfirst, fl_pend(n, 0), fl_kfirst(n, 0);
+  std::vector<float> beta_f(n_inner, 0.f);
+  if (use_cluster) {
+    std::vector<int32_t> last(n, -1);  // last outer iteration whose x is materialised
+    pend.resize(act.size());
+    kfirst.resize(act.size());
+    for (int k = 0; k < K; ++k)
+      for (int64_t e = off[k]; e < off[k + 1]; ++e) {
+        const int32_t i = act[e];
+        pend[e] = k - last[i] - 1;
+        kfirst[e] = last[i] + 1;
+        last[i] = k;
+      }
+    for (int64_t i = 0; i < n; ++i) {
+      fl_pend[i] = K - 1 - last[i];
+      fl_kfirst[i] = last[i] + 1;
+    }
+    for (int i = 0; i < n_inner; ++i) beta_f[i] = (float)beta[i];
+  }
+
+  DevBuf d_coins, d_act, d_rep, d_pend, d_kfirst, d_flp, d_flk, d_beta;
+  if (use_cluster) {
+    if (!act.empty()) {
+      PSB_CUDA(cudaMalloc(&d_pend.p, pend.size() * sizeof(int32_t)));
+      PSB_CUDA(cudaMalloc(&d_kfirst.p, kfirst.size() * sizeof(int32_t)));
+      PSB_CUDA(cudaMemcpy(d_pend.p, pend.data(), pend.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      PSB_CUDA(cudaMemcpy(d_kfirst.p, kfirst.data(), kfirst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    PSB_CUDA(cudaMalloc(&d_flp.p, n * sizeof(int32_t)));
+    PSB_CUDA(cudaMalloc(&d_flk.p, n * sizeof(int32_t)));
+    PSB_CUDA(cudaMalloc(&d_beta.p, n_inner * sizeof(float)));
+    PSB_CUDA(cudaMemcpy(d_flp.p, fl_pend.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    PSB_CUDA(cudaMemcpy(d_flk.p, fl_kfirst.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    PSB_CUDA(cudaMemcpy(d_beta.p, beta_f.data(), n_inner * sizeof(float), cudaMemcpyHostToDevice));
+  }
   PSB_CUDA(cudaMalloc(&d_coins.p, (size_t)K * n));
   PSB_CUDA(cudaMemcpy(d_coins.p, coins_host, (size_t)K * n, cudaMemcpyHostToDevice));
   if (!act.empty()) {
@@ -147,6 +196,18 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   int rc = PSB_OK;
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
     if (elapsed && k > 0) cudaEventRecordWithFlags(evs[k], st, rec_flags);
+    if (use_cluster) {
+      const int na = (int)(off[k + 1] - off[k]);
+      if (na == 0) continue;
+      if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
+      rc = cluster_prox_step(dto, x, b, h, q, qps, act_d + off[k], na,
+                             static_cast<const int32_t*>(d_pend.p) + off[k],
+                             static_cast<const int32_t*>(d_kfirst.p) + off[k], rep_d + off[k],
+                             n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
+                             static_cast<const float*>(d_beta.p), bad, k, st);
+      if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
+      continue;
+    }
     const int ident = fid.kind == 0;
     if (!ident) {
       rc = blur_grad2d(dto, x, b, fid.g, H, W, fid.taps2d, fid.taps1d, fid.ksize, fid.separable,
@@ -169,6 +230,9 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                          H, W, n_inner, nonneg, gamma, pg, bad, k, st);
   }
 
+  if (use_cluster && rc == PSB_OK)  // remaining deferred skip iterations
+    rc = skip_flush(dto, x, b, h, static_cast<const int32_t*>(d_flp.p),
+                    static_cast<const int32_t*>(d_flk.p), n, HW, gamma, bad, st);
   if (elapsed && rc == PSB_OK) cudaEventRecordWithFlags(evs[K], st, rec_flags);
   if (use_graph) {
     cudaGraph_t graph = nullptr;

@@ -1,0 +1,116 @@
+"""The cluster-resident 256x256 ProxSkip path (csrc/fgp_cluster.cu) against the
+streaming kernels and the CPU oracle."""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2411_00688_b200 as psb  # noqa: E402
+from paper_2411_00688_b200 import phantoms  # noqa: E402
+from oracle import imgskip_cpu as oc  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def _batch(idx):
+    return np.stack([phantoms.config4_problem(int(i))[1] for i in idx])
+
+
+def _run(b, idx, K, inner, p, stream_only, precision="fp32", graph=False):
+    old = os.environ.get("PSB_NO_CLUSTER")
+    os.environ["PSB_NO_CLUSTER"] = "1" if stream_only else "0"
+    try:
+        return psb.run_proxskip_batched(b, 0.1, p, idx, K, inner, precision=precision,
+                                        use_graph=graph)
+    finally:
+        if old is None:
+            os.environ.pop("PSB_NO_CLUSTER")
+        else:
+            os.environ["PSB_NO_CLUSTER"] = old
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_cluster_matches_streaming_and_oracle(graph):
+    idx = np.array([0, 5, 4095, 77, 1234])
+    b = _batch(idx)
+    K, inner, p = 40, 12, 0.25
+    xc, cc = _run(b, idx, K, inner, p, stream_only=False, graph=graph)
+    xs, cs = _run(b, idx, K, inner, p, stream_only=True)
+    np.testing.assert_array_equal(cc, cs)
+    for j, i in enumerate(idx):
+        assert rel(xc[j], xs[j]) < 2e-6
+        xr, _, n_prox, _ = oc.proxskip_denoise(b[j], 0.1, p, int(i), K, inner)
+        assert cc[j] == n_prox
+        assert rel(xc[j], xr) < 1e-5
+
+
+def test_cluster_warm_restart_reprojection_and_state():
+    """Two runs on the same solver: the second uses a different p, so the prox
+    weight changes and the warm start is re-projected (tv.py:68-69); x and h
+    carry over; deferred skips span the run boundary via the flush."""
+    idx = np.arange(3)
+    b = _batch(idx)
+    K1, K2, inner = 25, 30, 10
+    solvers = {}
+    for mode in ("cluster", "stream"):
+        os.environ["PSB_NO_CLUSTER"] = "1" if mode == "stream" else "0"
+        s = psb.BatchedTvDenoise(b, 0.1, inner, precision="fp32")
+        s.run_proxskip(psb.coin_table(0.3, idx, K1), 1.0, 0.3)
+        s.run_proxskip(psb.coin_table(0.15, idx + 100, K2), 1.0, 0.15)
+        s.check_finite()
+        solvers[mode] = s
+    os.environ.pop("PSB_NO_CLUSTER")
+    a, c = solvers["cluster"], solvers["stream"]
+    for j in range(3):
+        assert rel(a.x[j].cpu().numpy(), c.x[j].cpu().numpy()) < 2e-6
+        assert rel(a.h[j].cpu().numpy(), c.h[j].cpu().numpy()) < 1e-4
+        assert rel(a.slots[j, 0].cpu().numpy(), c.slots[j, 0].cpu().numpy()) < 1e-5
+    np.testing.assert_array_equal(a.prox_count, c.prox_count)
+    # oracle: the same two-run sequence with one FgpState per problem
+    for j, i in enumerate(idx):
+        pr = oc.make_recon(oc.identity_op(b[j].shape), b[j].astype(np.float64), 0.1, inner=inner)
+        x, h, _, _ = oc.proxskip(pr.grad, pr.prox, np.zeros((256, 256)), None, 1.0, 0.3, int(i), K1)
+        x, h, _, _ = oc.proxskip(pr.grad, pr.prox, x, h, 1.0, 0.15, int(i) + 100, K2)
+        assert rel(a.x[j].cpu().numpy(), x) < 1e-5
+
+
+def test_cluster_mixed_precision_single_problem_matches_oracle():
+    truth, b = phantoms.config1_data(seed=2)
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=30, precision="mixed")
+    x, log = psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0, psb.SkipConfig(0.2, 2),
+                              60)
+    xr, _, n_prox, inner = oc.proxskip_denoise(b, 0.1, 0.2, 2, 60, 30)
+    assert log.records[-1].prox_count == n_prox
+    assert prob.tv_state.total_inner_iterations == inner
+    assert rel(x, xr) < 1e-6
+
+
+def test_cluster_divergence_reports_iteration():
+    idx = np.arange(2)
+    b = _batch(idx).astype(np.float32)
+    b[1, 10, 10] = np.inf
+    coins = psb.coin_table(0.3, idx, 20)
+    s = psb.BatchedTvDenoise(b, 0.1, 5)
+    s.run_proxskip(coins, 1.0, 0.3)
+    with pytest.raises(psb.DivergenceError) as ei:
+        s.check_finite()
+    # problem 1's first iterate is already non-finite (iteration 0)
+    assert ei.value.iteration == 0
+
+
+def test_cluster_occupancy_query():
+    import ctypes
+    from paper_2411_00688_b200 import _lib as L
+    n = ctypes.c_int(0)
+    L.call("psb_cluster_max_active", ctypes.byref(n))
+    assert n.value >= 1
+    print("max active 16-CTA clusters:", n.value)
