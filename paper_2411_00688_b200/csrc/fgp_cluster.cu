@@ -9,7 +9,7 @@
 //           thread-block cluster (16 SMs, 512 threads each, 8 pixels per
 //           thread); row halos cross CTA boundaries through distributed
 //           shared memory, column halos through warp shuffles and shared
-//           memory; two cluster barriers per inner iteration
+//           memory; one cluster barrier per inner iteration
 //   post  : finalize u = clamp(z + div q_n) (tv.py:89), control variate
 //           h <- h + (p/g)(u - xhat), x <- u, q_n -> warm-start slot 0
 //           (skip.py:68-75)
@@ -69,6 +69,21 @@ __device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
   return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
 }
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Exchange pattern per inner iteration (ONE cluster barrier): at the end of
+// iteration t every CTA publishes its first row of q (both channels) and its
+// last row of q (row channel) into a parity-(t&1) buffer and arrives; at the
+// start of t+1 it waits, reads its neighbours' rows over DSMEM and rebuilds
+// the halo y rows itself (momentum from the previously received rows).  The
+// bottom row group also recomputes u for the first row of the CTA below, so
+// no u ever crosses a CTA boundary.  Row groups inside a CTA and warp edges
+// exchange through shared memory with __syncthreads.
 template <class TO>
 __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO> a) {
   using A = Ar<TO>;
@@ -81,12 +96,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const int j = tid % CW, rg = tid / CW;
   const int lane = tid & 31, wc = j >> 5;
   const int row0 = cr * (CRG * CRPT) + rg * CRPT;
+  const bool rg_top = rg == 0, rg_bot = rg == CRG - 1;
+  const bool has_up = cr > 0, has_dn = cr < CCL - 1;
   constexpr int64_t HW = (int64_t)CH * CW;
 
-  __shared__ float s_bot_yy[CRG][CW];
-  __shared__ float s_top_u[CRG][CW];
-  __shared__ float s_edge_yx[CRG][CWARPS_ROW][CRPT];
-  __shared__ float s_edge_u[CRG][CWARPS_ROW][CRPT];
+  __shared__ float pub_top[2][2][CW];  // [parity][channel][col]: first row of q
+  __shared__ float pub_bot[2][CW];     // [parity][col]: last row of q, row channel
+  __shared__ float s_rg_yy[CW];        // row group 0's last-row y_y (for group 1's div)
+  __shared__ float s_rg_u[CW];         // row group 1's first-row u (for group 0's grad)
+  __shared__ float s_edge_yx[CRG][CWARPS_ROW][CRPT + 1];
+  __shared__ float s_edge_u[CRG][CWARPS_ROW][CRPT + 1];
 
   TO* xp = a.x + (int64_t)p * HW;
   const TO* bp = a.b + (int64_t)p * HW;
@@ -97,97 +116,123 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool rp = a.rep ? a.rep[entry] != 0 : false;
   const TO g = a.gamma;
   const float w = a.weight;
+  const bool nonneg = a.nonneg != 0;
 
   float z[CRPT], qky[CRPT], qkx[CRPT], qmy[CRPT], qmx[CRPT];
-  bool ok = true;
   int kbad = 0x7fffffff;
-  // ---- prologue: deferred skips, prox input, warm start --------------------
-#pragma unroll
-  for (int t = 0; t < CRPT; ++t) {
-    const int64_t o = (int64_t)(row0 + t) * CW + j;
+  auto prox_input = [&](int64_t o, bool track) {
     TO xo = xp[o];
     const TO bo = bp[o], ho = hp[o];
     for (int s = 0; s < m; ++s) {
       xo = skip_update(xo, bo, ho, g);
-      if (!finite(xo)) kbad = min(kbad, kf + s);
+      if (track && !finite(xo)) kbad = min(kbad, kf + s);
     }
-    z[t] = (float)A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(a.hc, ho));
+    return (float)A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(a.hc, ho));
+  };
+  // ---- prologue: deferred skips, prox input, warm start --------------------
+#pragma unroll
+  for (int t = 0; t < CRPT; ++t) {
+    const int64_t o = (int64_t)(row0 + t) * CW + j;
+    z[t] = prox_input(o, true);
     float vy = q0[o], vx = q0[HW + o];
     if (rp) {
       const float sc = F::ball_scale(vy, vx, w);
       vy *= sc;
       vx *= sc;
     }
-    qky[t] = vy;
-    qkx[t] = vx;
-    qmy[t] = vy;
-    qmx[t] = vx;
+    qky[t] = qmy[t] = vy;
+    qkx[t] = qmx[t] = vx;
   }
+  // the bottom row group also owns the CTA-below's first row for u
+  float z_ex = 0.f;
+  if (rg_bot && has_dn) z_ex = prox_input((int64_t)(row0 + CRPT) * CW + j, false);
+  if (rg_top) {
+    pub_top[1][0][j] = qky[0];
+    pub_top[1][1][j] = qkx[0];
+  }
+  if (rg_bot) pub_bot[1][j] = qky[CRPT - 1];
+  cluster_arrive();
 
-  auto halo_div = [&](const float(&yy)[CRPT], const float(&yx)[CRPT], float(&d)[CRPT]) {
-    // publish the values neighbours need, then read theirs
-    s_bot_yy[rg][j] = yy[CRPT - 1];
+  float up_k = 0.f, up_m = 0.f;                          // row above, row channel
+  float dn_ky = 0.f, dn_kx = 0.f, dn_my = 0.f, dn_mx = 0.f;  // row below, both channels
+
+  for (int it = 0; it < a.n_inner; ++it) {
+    const float beta = (a.accelerated && it > 0) ? a.betas[it - 1] : 0.f;
+    const int par = (it - 1) & 1;
+    float yy[CRPT], yx[CRPT];
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      yy[t] = beta != 0.f ? qky[t] + beta * (qky[t] - qmy[t]) : qky[t];
+      yx[t] = beta != 0.f ? qkx[t] + beta * (qkx[t] - qmx[t]) : qkx[t];
+    }
+    cluster_wait();
+    float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
+    if (rg_top && has_up) {
+      const float v = cluster.map_shared_rank(&pub_bot[par][0], cr - 1)[j];
+      up_m = it == 0 ? v : up_k;
+      up_k = v;
+      y_up = beta != 0.f ? up_k + beta * (up_k - up_m) : up_k;
+    }
+    if (rg_bot && has_dn) {
+      const float* rt = cluster.map_shared_rank(&pub_top[par][0][0], cr + 1);
+      const float vy = rt[j], vx = rt[CW + j];
+      dn_my = it == 0 ? vy : dn_ky;
+      dn_mx = it == 0 ? vx : dn_kx;
+      dn_ky = vy;
+      dn_kx = vx;
+      ex_y = beta != 0.f ? dn_ky + beta * (dn_ky - dn_my) : dn_ky;
+      ex_x = beta != 0.f ? dn_kx + beta * (dn_kx - dn_mx) : dn_kx;
+    }
+    if (rg_top) s_rg_yy[j] = yy[CRPT - 1];
     if (lane == 31) {
 #pragma unroll
       for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = yx[t];
+      s_edge_yx[rg][wc][CRPT] = ex_x;
     }
-    cluster.sync();
-    float yy_up = 0.f;
-    if (rg > 0)
-      yy_up = s_bot_yy[rg - 1][j];
-    else if (cr > 0)
-      yy_up = cluster.map_shared_rank(&s_bot_yy[CRG - 1][0], cr - 1)[j];
+    __syncthreads();
+    const float yy_above = rg_top ? y_up : s_rg_yy[j];
+    float u[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float left = __shfl_up_sync(0xffffffffu, yx[t], 1);
       if (lane == 0) left = wc > 0 ? s_edge_yx[rg][wc - 1][t] : 0.f;
       const int r = row0 + t;
-      float dd = 0.f;  // operators.py:66-70 order
-      if (r < CH - 1) dd += yy[t];
-      if (r > 0) dd -= (t > 0 ? yy[t - 1] : yy_up);
-      if (j < CW - 1) dd += yx[t];
-      if (j > 0) dd -= left;
-      d[t] = dd;
+      float d = 0.f;  // operators.py:66-70 order
+      if (r < CH - 1) d += yy[t];
+      if (r > 0) d -= (t > 0 ? yy[t - 1] : yy_above);
+      if (j < CW - 1) d += yx[t];
+      if (j > 0) d -= left;
+      const float v = z[t] + d;
+      u[t] = nonneg ? fmaxf(v, 0.f) : v;
     }
-  };
-
-  for (int it = 0; it < a.n_inner; ++it) {
-    float yy[CRPT], yx[CRPT];
-    const float beta = (a.accelerated && it > 0) ? a.betas[it - 1] : 0.f;
-#pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      if (beta != 0.f) {
-        yy[t] = qky[t] + beta * (qky[t] - qmy[t]);
-        yx[t] = qkx[t] + beta * (qkx[t] - qmx[t]);
-      } else {
-        yy[t] = qky[t];
-        yx[t] = qkx[t];
+    float u_ex = 0.f;
+    {
+      float left = __shfl_up_sync(0xffffffffu, ex_x, 1);
+      if (lane == 0) left = wc > 0 ? s_edge_yx[rg][wc - 1][CRPT] : 0.f;
+      if (rg_bot && has_dn) {
+        const int r = row0 + CRPT;
+        float d = 0.f;
+        if (r < CH - 1) d += ex_y;
+        d -= yy[CRPT - 1];
+        if (j < CW - 1) d += ex_x;
+        if (j > 0) d -= left;
+        const float v = z_ex + d;
+        u_ex = nonneg ? fmaxf(v, 0.f) : v;
       }
     }
-    float u[CRPT];
-    halo_div(yy, yx, u);
-#pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      float v = z[t] + u[t];
-      u[t] = a.nonneg ? fmaxf(v, 0.f) : v;
-    }
-    s_top_u[rg][j] = u[0];
+    if (rg_bot) s_rg_u[j] = u[0];
     if (lane == 0) {
 #pragma unroll
       for (int t = 0; t < CRPT; ++t) s_edge_u[rg][wc][t] = u[t];
     }
-    cluster.sync();
-    float u_dn = 0.f;
-    if (rg < CRG - 1)
-      u_dn = s_top_u[rg + 1][j];
-    else if (cr < CCL - 1)
-      u_dn = cluster.map_shared_rank(&s_top_u[0][0], cr + 1)[j];
+    __syncthreads();
+    const float u_below = rg_top ? s_rg_u[j] : u_ex;
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float right = __shfl_down_sync(0xffffffffu, u[t], 1);
       if (lane == 31) right = wc < CWARPS_ROW - 1 ? s_edge_u[rg][wc + 1][t] : 0.f;
       const int r = row0 + t;
-      const float below = t < CRPT - 1 ? u[t + 1] : u_dn;
+      const float below = t < CRPT - 1 ? u[t + 1] : u_below;
       const float gy = r < CH - 1 ? below - u[t] : 0.f;
       const float gx = j < CW - 1 ? right - u[t] : 0.f;
       const float ay = yy[t] + a.step * gy;
@@ -198,16 +243,41 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       qky[t] = ay * sc;
       qkx[t] = ax * sc;
     }
+    const int pw = it & 1;
+    if (rg_top) {
+      pub_top[pw][0][j] = qky[0];
+      pub_top[pw][1][j] = qkx[0];
+    }
+    if (rg_bot) pub_bot[pw][j] = qky[CRPT - 1];
+    cluster_arrive();
   }
 
-  // ---- epilogue: finalize + ProxSkip post ------------------------------------
-  float d[CRPT];
-  halo_div(qky, qkx, d);
+  // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
+  cluster_wait();
+  float yy_above = 0.f;
+  if (rg_top && has_up)
+    yy_above = cluster.map_shared_rank(&pub_bot[(a.n_inner - 1) & 1][0], cr - 1)[j];
+  if (rg_top) s_rg_yy[j] = qky[CRPT - 1];
+  if (lane == 31) {
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = qkx[t];
+  }
+  __syncthreads();
+  if (!rg_top) yy_above = s_rg_yy[j];
+  bool ok = true;
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
-    const int64_t o = (int64_t)(row0 + t) * CW + j;
-    float uf = z[t] + d[t];
-    if (a.nonneg) uf = fmaxf(uf, 0.f);
+    float left = __shfl_up_sync(0xffffffffu, qkx[t], 1);
+    if (lane == 0) left = wc > 0 ? s_edge_yx[rg][wc - 1][t] : 0.f;
+    const int r = row0 + t;
+    float d = 0.f;
+    if (r < CH - 1) d += qky[t];
+    if (r > 0) d -= (t > 0 ? qky[t - 1] : yy_above);
+    if (j < CW - 1) d += qkx[t];
+    if (j > 0) d -= left;
+    float uf = z[t] + d;
+    if (nonneg) uf = fmaxf(uf, 0.f);
+    const int64_t o = (int64_t)r * CW + j;
     TO xo = xp[o];
     const TO bo = bp[o], ho = hp[o];
     for (int s = 0; s < m; ++s) xo = skip_update(xo, bo, ho, g);
@@ -221,7 +291,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   }
   if (!ok) kbad = min(kbad, a.k);
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
-  cluster.sync();  // keep this CTA's shared memory alive for its neighbours' last reads
+  cluster_arrive();  // keep shared memory alive until every neighbour has read it
+  cluster_wait();
 }
 
 // Apply each problem's remaining deferred skips (end of a run).
