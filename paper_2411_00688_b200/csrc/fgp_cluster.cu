@@ -140,6 +140,12 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       vy *= sc;
       vx *= sc;
     }
+    // The reference's divergence ignores q_y on the last row and q_x on the
+    // last column (operators.py:66-70) and the gradient is 0 there, so those
+    // entries stay 0 from a cold start; zeroing them here lets the inner loop
+    // drop every boundary test (zero padding instead of masks).
+    if (row0 + t == CH - 1) vy = 0.f;
+    if (j == CW - 1) vx = 0.f;
     qky[t] = qmy[t] = vy;
     qkx[t] = qmx[t] = vx;
   }
@@ -155,15 +161,21 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
 
   float up_k = 0.f, up_m = 0.f;                          // row above, row channel
   float dn_ky = 0.f, dn_kx = 0.f, dn_my = 0.f, dn_mx = 0.f;  // row below, both channels
+  const bool last_row_thread = rg_bot && !has_dn;  // owns global row H-1 (t = CRPT-1)
+  const bool right_edge = lane == 31 && wc == CWARPS_ROW - 1;  // global column W-1
+  const bool left_fetch = lane == 0 && wc > 0;
+  const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
 
-  for (int it = 0; it < a.n_inner; ++it) {
+  // One inner iteration; reads (QK, QM), writes the new iterate into QM.
+  auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
+                   int it) {
     const float beta = (a.accelerated && it > 0) ? a.betas[it - 1] : 0.f;
     const int par = (it - 1) & 1;
     float yy[CRPT], yx[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
-      yy[t] = beta != 0.f ? qky[t] + beta * (qky[t] - qmy[t]) : qky[t];
-      yx[t] = beta != 0.f ? qkx[t] + beta * (qkx[t] - qmx[t]) : qkx[t];
+      yy[t] = QKy[t] + beta * (QKy[t] - QMy[t]);
+      yx[t] = QKx[t] + beta * (QKx[t] - QMx[t]);
     }
     cluster_wait();
     float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
@@ -171,7 +183,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       const float v = cluster.map_shared_rank(&pub_bot[par][0], cr - 1)[j];
       up_m = it == 0 ? v : up_k;
       up_k = v;
-      y_up = beta != 0.f ? up_k + beta * (up_k - up_m) : up_k;
+      y_up = up_k + beta * (up_k - up_m);
     }
     if (rg_bot && has_dn) {
       const float* rt = cluster.map_shared_rank(&pub_top[par][0][0], cr + 1);
@@ -180,8 +192,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       dn_mx = it == 0 ? vx : dn_kx;
       dn_ky = vy;
       dn_kx = vx;
-      ex_y = beta != 0.f ? dn_ky + beta * (dn_ky - dn_my) : dn_ky;
-      ex_x = beta != 0.f ? dn_kx + beta * (dn_kx - dn_mx) : dn_kx;
+      ex_y = dn_ky + beta * (dn_ky - dn_my);
+      ex_x = dn_kx + beta * (dn_kx - dn_mx);
     }
     if (rg_top) s_rg_yy[j] = yy[CRPT - 1];
     if (lane == 31) {
@@ -195,30 +207,19 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float left = __shfl_up_sync(0xffffffffu, yx[t], 1);
-      if (lane == 0) left = wc > 0 ? s_edge_yx[rg][wc - 1][t] : 0.f;
-      const int r = row0 + t;
-      float d = 0.f;  // operators.py:66-70 order
-      if (r < CH - 1) d += yy[t];
-      if (r > 0) d -= (t > 0 ? yy[t - 1] : yy_above);
-      if (j < CW - 1) d += yx[t];
-      if (j > 0) d -= left;
+      if (lane == 0) left = left_fetch ? s_edge_yx[rg][wc - 1][t] : 0.f;
+      // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded
+      const float d = ((yy[t] - (t > 0 ? yy[t - 1] : yy_above)) + yx[t]) - left;
       const float v = z[t] + d;
       u[t] = nonneg ? fmaxf(v, 0.f) : v;
     }
-    float u_ex = 0.f;
+    float u_ex;
     {
       float left = __shfl_up_sync(0xffffffffu, ex_x, 1);
-      if (lane == 0) left = wc > 0 ? s_edge_yx[rg][wc - 1][CRPT] : 0.f;
-      if (rg_bot && has_dn) {
-        const int r = row0 + CRPT;
-        float d = 0.f;
-        if (r < CH - 1) d += ex_y;
-        d -= yy[CRPT - 1];
-        if (j < CW - 1) d += ex_x;
-        if (j > 0) d -= left;
-        const float v = z_ex + d;
-        u_ex = nonneg ? fmaxf(v, 0.f) : v;
-      }
+      if (lane == 0) left = left_fetch ? s_edge_yx[rg][wc - 1][CRPT] : 0.f;
+      const float d = ((ex_y - yy[CRPT - 1]) + ex_x) - left;
+      const float v = z_ex + d;
+      u_ex = nonneg ? fmaxf(v, 0.f) : v;
     }
     if (rg_bot) s_rg_u[j] = u[0];
     if (lane == 0) {
@@ -226,30 +227,42 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       for (int t = 0; t < CRPT; ++t) s_edge_u[rg][wc][t] = u[t];
     }
     __syncthreads();
-    const float u_below = rg_top ? s_rg_u[j] : u_ex;
+    // the global last row has no row below: gy = 0 (below := u)
+    const float u_below = rg_top ? s_rg_u[j] : (last_row_thread ? u[CRPT - 1] : u_ex);
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float right = __shfl_down_sync(0xffffffffu, u[t], 1);
-      if (lane == 31) right = wc < CWARPS_ROW - 1 ? s_edge_u[rg][wc + 1][t] : 0.f;
-      const int r = row0 + t;
+      if (lane == 31) right = right_fetch ? s_edge_u[rg][wc + 1][t] : u[t];  // W-1: gx = 0
       const float below = t < CRPT - 1 ? u[t + 1] : u_below;
-      const float gy = r < CH - 1 ? below - u[t] : 0.f;
-      const float gx = j < CW - 1 ? right - u[t] : 0.f;
-      const float ay = yy[t] + a.step * gy;
-      const float ax = yx[t] + a.step * gx;
-      const float sc = F::ball_scale(ay, ax, w);
-      qmy[t] = qky[t];
-      qmx[t] = qkx[t];
-      qky[t] = ay * sc;
-      qkx[t] = ax * sc;
+      const float ay = yy[t] + a.step * (below - u[t]);
+      const float ax = yx[t] + a.step * (right - u[t]);
+      const float m2 = fmaf(ay, ay, ax * ax);
+      const float sc = fminf(1.f, w * rsqrtf(m2));  // w / max(w, |a|)
+      QMy[t] = ay * sc;
+      QMx[t] = ax * sc;
     }
+    (void)right_edge;
     const int pw = it & 1;
     if (rg_top) {
-      pub_top[pw][0][j] = qky[0];
-      pub_top[pw][1][j] = qkx[0];
+      pub_top[pw][0][j] = QMy[0];
+      pub_top[pw][1][j] = QMx[0];
     }
-    if (rg_bot) pub_bot[pw][j] = qky[CRPT - 1];
+    if (rg_bot) pub_bot[pw][j] = QMy[CRPT - 1];
     cluster_arrive();
+  };
+
+  int it = 0;
+  for (; it + 1 < a.n_inner; it += 2) {
+    inner(qky, qkx, qmy, qmx, it);      // new iterate in qm*
+    inner(qmy, qmx, qky, qkx, it + 1);  // new iterate in qk*
+  }
+  if (it < a.n_inner) {
+    inner(qky, qkx, qmy, qmx, it);
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      qky[t] = qmy[t];
+      qkx[t] = qmx[t];
+    }
   }
 
   // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
