@@ -38,6 +38,16 @@ INNER = 50
 RUN_LEN = 300
 BYTES_FGP_MOM = 28   # fp32 per pixel-iteration: x + q_k(2) + q_{k-1}(2) read, q_{k+1}(2) write
 BYTES_FGP_FIRST = 20  # first inner iteration (beta = 0): no q_{k-1} read
+CLUSTER = os.environ.get("PSB_NO_CLUSTER", "0") != "1"
+if CLUSTER:
+    KERNEL = ("fgp_cluster_kernel<float>: the whole coin-fired prox step (pre + 50 FGP iterations "
+              "+ post) per 16-CTA cluster, FGP state in registers; the 28 B/px-iter of the "
+              "streaming formulation stay on-chip, so frac > 1 is expected")
+    # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch / (launch px) -- see profiles/
+    TRAFFIC = None
+else:
+    KERNEL = "fgp2d_iter_kernel<float,4> (streaming, one launch per inner iteration)"
+    TRAFFIC = None
 METRIC = "ProxSkip TV outer iter/s (config 4: 4096 x 256^2 batch, FGP-50, p=0.1)"
 WORKLOAD = "config4: batched ProxSkip TV denoising, 4096 x 256x256, alpha=0.1, p=0.1, FGP-50"
 
@@ -233,8 +243,12 @@ def run_gpu(args):
     timed = coins[args.warmup:]
     active = timed.sum(axis=1)                       # coin-fired problems per step
     fgp_bytes = active * HW * (BYTES_FGP_FIRST + (INNER - 1) * BYTES_FGP_MOM)
-    fgp_launch = int(np.count_nonzero(active)) * INNER
-    launches = args.steps + int(np.count_nonzero(active)) * (INNER + 1)
+    n_fired_steps = int(np.count_nonzero(active))
+    if CLUSTER:
+        # one fused cluster launch per step with a coin-fired problem + the final skip flush
+        launches = n_fired_steps + 1
+    else:
+        launches = args.steps + n_fired_steps * (INNER + 1)
     stats = np.array([t_local, fgp_t.sum(), float(fgp_bytes.sum()), float(active.sum())])
     if world > 1:
         import torch.distributed as dist
@@ -287,9 +301,11 @@ def run_gpu(args):
         "fgp_inner_iter_per_s": inner_rate,
         "fgp_mpx_iter_per_s": inner_rate * HW / 1e6,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": "fgp2d_iter_kernel<float,4>",
-                     "bytes_per_unit": "28 B/pixel-iteration (20 B at the first inner iteration)",
+                     "frac": achieved / peak, "traffic": TRAFFIC,
+                     "kernel": KERNEL,
+                     "bytes_per_unit": "28 B/pixel-iteration (20 B at the first inner iteration), "
+                                       "SURVEY 8(d); x per launch = coin-fired problems x 65536 px "
+                                       "x 50 inner iterations",
                      "peak_source": peak_kind},
         "cpu_baseline": cpu,
         "e2e": {"value": n_e2e / t_e2e, "unit": "outer-iter/s (4096-problem batch)",

@@ -235,13 +235,245 @@ __global__ void proxskip_post3d_kernel(TO* __restrict__ x, const TO* __restrict_
   if (!ok && bad) atomicMin(bad, kiter);
 }
 
+// ---- register z-march (v2) -------------------------------------------------
+// CTA = (MTY + 2) warps; warp w owns image row i0 - 1 + w of a band of 32*V
+// columns and marches along z keeping y(k), u(k) of its row in registers.
+// Warps 1..MTY produce output; warp 0 (row i0-1) only supplies y_y for warp
+// 1's divergence and warp MTY+1 (row i0+MTY) only supplies u for warp MTY's
+// y-gradient.  Rows meet in shared memory (2 __syncthreads per plane), columns
+// through shuffles plus one predicated halo column per warp edge, planes
+// through registers.  HBM: x + q_k(3) + q_{k-1}(3) read, q_{k+1}(3) written
+// once per voxel-iteration (40 B fp32), row/column halos re-read from L2.
+constexpr int MTY = 16;
+
+template <class T, int V>
+struct Row3 {
+  T y[3][V];  // z, y, x channels of the momentum point y
+  T h[3];     // halo column (lane 0: c0-1, lane 31: c0+32V)
+  T u[V];
+  T hu;
+};
+
+template <class T, int V>
+__device__ __forceinline__ void load_plane_row(const Fgp3Args<T>& a, int kl, int i, int cl, bool lin,
+                                               int hc, bool hval, bool mom, bool rp,
+                                               Row3<T, V>& R, T (&xv)[V], T& hx) {
+  using A = Ar<T>;
+  const T* qk;
+  const T* qm;
+  int64_t cs, po;
+  plane_src(a, kl, qk, qm, cs, po);
+  const int64_t HW = (int64_t)a.H * a.W;
+  const T* xs = (kl < a.D) ? a.x + (int64_t)kl * HW : a.ha_x;
+  auto one = [&](int64_t o, T& v0, T& v1, T& v2) {
+    if (rp) {
+      const T s = A::ball_scale3(v0, v1, v2, a.w);
+      v0 = A::mul(v0, s);
+      v1 = A::mul(v1, s);
+      v2 = A::mul(v2, s);
+    }
+    (void)o;
+  };
+  if (lin) {
+    const int64_t o = po + (int64_t)i * a.W + cl;
+    T k0[V], k1[V], k2[V];
+    ldv<T, V>(k0, qk + o);
+    ldv<T, V>(k1, qk + cs + o);
+    ldv<T, V>(k2, qk + 2 * cs + o);
+    if (xs) ldv<T, V>(xv, xs + (int64_t)i * a.W + cl);
+    if (mom) {
+      T m0[V], m1[V], m2[V];
+      ldv<T, V>(m0, qm + o);
+      ldv<T, V>(m1, qm + cs + o);
+      ldv<T, V>(m2, qm + 2 * cs + o);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        R.y[0][v] = A::add(k0[v], A::mul(a.beta, A::sub(k0[v], m0[v])));
+        R.y[1][v] = A::add(k1[v], A::mul(a.beta, A::sub(k1[v], m1[v])));
+        R.y[2][v] = A::add(k2[v], A::mul(a.beta, A::sub(k2[v], m2[v])));
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        T v0 = k0[v], v1 = k1[v], v2 = k2[v];
+        one(0, v0, v1, v2);
+        R.y[0][v] = v0;
+        R.y[1][v] = v1;
+        R.y[2][v] = v2;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) R.y[0][v] = R.y[1][v] = R.y[2][v] = xv[v] = T(0);
+  }
+  R.h[0] = R.h[1] = R.h[2] = T(0);
+  hx = T(0);
+  if (hval) {
+    const int64_t o = po + (int64_t)i * a.W + hc;
+    T v0 = qk[o], v1 = qk[cs + o], v2 = qk[2 * cs + o];
+    if (mom) {
+      v0 = A::add(v0, A::mul(a.beta, A::sub(v0, qm[o])));
+      v1 = A::add(v1, A::mul(a.beta, A::sub(v1, qm[cs + o])));
+      v2 = A::add(v2, A::mul(a.beta, A::sub(v2, qm[2 * cs + o])));
+    } else {
+      one(0, v0, v1, v2);
+    }
+    R.h[0] = v0;
+    R.h[1] = v1;
+    R.h[2] = v2;
+    if (xs) hx = xs[(int64_t)i * a.W + hc];
+  }
+}
+
+template <class T, int V>
+__global__ void __launch_bounds__((MTY + 2) * 32) fgp3d_march_kernel(Fgp3Args<T> a) {
+  using A = Ar<T>;
+  constexpr int BW = 32 * V;
+  __shared__ T s_yy[MTY + 2][BW + 1];
+  __shared__ T s_u[2][MTY + 2][BW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * BW;
+  const int i = blockIdx.y * MTY - 1 + w;
+  const int ks = blockIdx.z * a.zchunk;
+  const int ke = min(a.D, ks + a.zchunk);
+  if (ks >= ke) return;
+  const int H = a.H, W = a.W;
+  const bool row_ok = i >= 0 && i < H;
+  const int cl = c0 + lane * V;
+  const bool lin = row_ok && cl < W;
+  const int hc = lane == 0 ? c0 - 1 : c0 + BW;
+  const bool hval = row_ok && ((lane == 0 && c0 > 0) || (lane == 31 && hc < W));
+  const bool mom = a.beta != T(0);
+  const bool rp = a.rep && a.it == 0;
+  const bool out_row = w >= 1 && w <= MTY && row_ok;
+  const int64_t HW = (int64_t)H * W, N3 = (int64_t)a.D * HW;
+  T* qo = a.q + (int64_t)((a.it + 1) % 3) * 3 * N3;
+
+  // u(plane) of this row from its y (cur), y_z of the plane below (yzp, hyzp),
+  // y_y of the row above (s_yy[w-1]) and the left neighbour's y_x.
+  auto prim = [&](int kg, Row3<T, V>& R, const T (&yzp)[V], T hyzp, const T (&xv)[V], T hx) {
+    T left = __shfl_up_sync(0xffffffffu, R.y[2][V - 1], 1);
+    if (lane == 0) left = R.h[2];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = cl + v;
+      T d = T(0);
+      if (kg < a.Dg - 1) d = A::add(d, R.y[0][v]);
+      if (kg > 0) d = A::sub(d, yzp[v]);
+      if (i < H - 1) d = A::add(d, R.y[1][v]);
+      if (i > 0) d = A::sub(d, w > 0 ? s_yy[w - 1][lane * V + v] : T(0));
+      if (c < W - 1) d = A::add(d, R.y[2][v]);
+      if (c > 0) d = A::sub(d, v > 0 ? R.y[2][v - 1] : left);
+      T u = A::add(xv[v], d);
+      R.u[v] = a.nonneg ? (u > T(0) ? u : T(0)) : u;
+    }
+    if (lane == 31) {  // halo column c0 + BW
+      const int c = hc;
+      T d = T(0);
+      if (kg < a.Dg - 1) d = A::add(d, R.h[0]);
+      if (kg > 0) d = A::sub(d, hyzp);
+      if (i < H - 1) d = A::add(d, R.h[1]);
+      if (i > 0) d = A::sub(d, w > 0 ? s_yy[w - 1][BW] : T(0));
+      if (c < W - 1) d = A::add(d, R.h[2]);
+      if (c > 0) d = A::sub(d, R.y[2][V - 1]);
+      T u = A::add(hx, d);
+      R.hu = a.nonneg ? (u > T(0) ? u : T(0)) : u;
+    }
+  };
+  auto publish_yy = [&](const Row3<T, V>& R) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) s_yy[w][lane * V + v] = R.y[1][v];
+    if (lane == 31) s_yy[w][BW] = R.h[1];
+  };
+  auto publish_u = [&](const Row3<T, V>& R, int par) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) s_u[par][w][lane * V + v] = R.u[v];
+  };
+
+  Row3<T, V> C, N;
+  T yzp[V], hyzp = T(0), xv[V], hx;
+#pragma unroll
+  for (int v = 0; v < V; ++v) yzp[v] = T(0);
+  // prologue: y_z of plane ks-1, then plane ks and u(ks)
+  if (a.z0 + ks > 0) {
+    T xd[V], hxd;
+    load_plane_row<T, V>(a, ks - 1, i, cl, lin, hc, hval, mom, rp, N, xd, hxd);
+#pragma unroll
+    for (int v = 0; v < V; ++v) yzp[v] = N.y[0][v];
+    hyzp = N.h[0];
+  }
+  load_plane_row<T, V>(a, ks, i, cl, lin, hc, hval, mom, rp, C, xv, hx);
+  publish_yy(C);
+  __syncthreads();
+  prim(a.z0 + ks, C, yzp, hyzp, xv, hx);
+  publish_u(C, ks & 1);
+  __syncthreads();
+
+  for (int k = ks; k < ke; ++k) {
+    const int kg = a.z0 + k;
+    const bool nxt = kg + 1 < a.Dg;
+    if (nxt) {
+      load_plane_row<T, V>(a, k + 1, i, cl, lin, hc, hval, mom, rp, N, xv, hx);
+      publish_yy(N);
+    }
+    __syncthreads();
+    if (nxt) {
+      T yzc[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) yzc[v] = C.y[0][v];
+      prim(kg + 1, N, yzc, C.h[0], xv, hx);
+      publish_u(N, (k + 1) & 1);
+    }
+    __syncthreads();
+    if (out_row) {
+      T right = __shfl_down_sync(0xffffffffu, C.u[0], 1);
+      if (lane == 31) right = C.hu;
+      T oz[V], oy[V], ox[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int c = cl + v;
+        const T uc = C.u[v];
+        const T gz = nxt ? A::sub(N.u[v], uc) : T(0);
+        const T gy = i < H - 1 ? A::sub(s_u[k & 1][w + 1][lane * V + v], uc) : T(0);
+        const T ur = v < V - 1 ? C.u[v + 1] : right;
+        const T gx = c < W - 1 ? A::sub(ur, uc) : T(0);
+        const T az = A::add(C.y[0][v], A::mul(a.step, gz));
+        const T ay = A::add(C.y[1][v], A::mul(a.step, gy));
+        const T ax = A::add(C.y[2][v], A::mul(a.step, gx));
+        const T sc = A::ball_scale3(az, ay, ax, a.w);
+        oz[v] = A::mul(az, sc);
+        oy[v] = A::mul(ay, sc);
+        ox[v] = A::mul(ax, sc);
+      }
+      if (lin) {
+        const int64_t o = (int64_t)k * HW + (int64_t)i * W + cl;
+        stv<T, V>(qo + o, oz);
+        stv<T, V>(qo + N3 + o, oy);
+        stv<T, V>(qo + 2 * N3 + o, ox);
+      }
+    } else {
+      // keep the shuffle participation uniform across the warp
+      (void)__shfl_down_sync(0xffffffffu, C.u[0], 1);
+    }
+    C = N;
+  }
+}
+
 template <class T>
 int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
-  dim3 block(TX, TY);
+  constexpr int VMAX = 16 / sizeof(T);
   const int zc = a.zchunk;
-  dim3 grid((a.W + TX - 1) / TX, (a.H + TY - 1) / TY, (a.D + zc - 1) / zc);
-  fgp3d_iter_kernel<T><<<grid, block, 0, st>>>(a);
-  PSB_LAUNCHED("fgp3d_iter");
+  const int nz = (a.D + zc - 1) / zc;
+  const bool vec = (a.W % VMAX == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.q) % 16 == 0);
+  if (vec) {
+    dim3 grid((a.W + 32 * VMAX - 1) / (32 * VMAX), (a.H + MTY - 1) / MTY, nz);
+    fgp3d_march_kernel<T, VMAX><<<grid, (MTY + 2) * 32, 0, st>>>(a);
+  } else {
+    dim3 grid((a.W + 31) / 32, (a.H + MTY - 1) / MTY, nz);
+    fgp3d_march_kernel<T, 1><<<grid, (MTY + 2) * 32, 0, st>>>(a);
+  }
+  PSB_LAUNCHED("fgp3d_march");
   return PSB_OK;
 }
 
@@ -258,8 +490,8 @@ int fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z0, i
   PSB_REQUIRE(z0 + D == Dg || (ha_qk && ha_qm && ha_x), "fgp3d: slab below the top needs the halo above");
   if (zchunk <= 0) {
     // enough CTAs for ~4 waves; long chunks amortise the two halo planes
-    const int64_t tiles = (int64_t)((W + TX - 1) / TX) * ((H + TY - 1) / TY);
-    const int64_t want = 4LL * sm_count() * 6;
+    const int64_t tiles = (int64_t)((W + 127) / 128) * ((H + MTY - 1) / MTY);
+    const int64_t want = 4LL * sm_count();
     int nz = (int)std::max<int64_t>(1, std::min<int64_t>(D, (want + tiles - 1) / tiles));
     zchunk = std::max(8, (D + nz - 1) / nz);
   }
