@@ -3,14 +3,10 @@
 // proximal.py:10-21) on a (D, H, W) volume with dual channels (z, y, x),
 // Neumann zeros on the last plane of each axis and dual step 1/12.
 //
-// One launch = one inner iteration.  2.5-D blocking: a CTA owns a TY x TX
-// column tile and marches along z over a chunk of planes.  Per plane it
-// stages y = q_k + beta (q_k - q_{k-1}) for the tile plus a one-voxel halo in
-// shared memory, forms u = clamp(x + div y) on the tile plus the +1 row/col
-// halo, and writes q_{k+1} for the previous plane; the y and u planes rotate
-// through shared memory so every voxel's q_k / q_{k-1} / x is read from HBM
-// once (40 B/voxel-iteration fp32: x + q_k(3) + q_{k-1}(3) read, q_{k+1}(3)
-// write).
+// One launch = one inner iteration (fgp3d_march_kernel below): warps march
+// along z over a chunk of planes keeping their row's y and u in registers;
+// every voxel's q_k / q_{k-1} / x is read from HBM once (40 B/voxel-iteration
+// fp32: x + q_k(3) + q_{k-1}(3) read, q_{k+1}(3) written).
 //
 // z-slab decomposition (BASELINE config 5 on N GPUs): a rank owns planes
 // [z0, z0 + D) of a volume of depth Dg.  Plane z0-1 (below) and plane z0+D
@@ -22,9 +18,6 @@
 namespace psb {
 
 namespace {
-
-constexpr int TY = 8, TX = 32;
-constexpr int RY = TY + 2, RX = TX + 2;  // y region: rows i0-1..i0+TY, cols j0-1..j0+TX
 
 template <class T>
 struct Fgp3Args {
@@ -64,129 +57,6 @@ __device__ __forceinline__ void plane_src(const Fgp3Args<T>& a, int kl, const T*
     qm = a.ha_qm;
     cstride = HW;
     poff = 0;
-  }
-}
-
-template <class T>
-__device__ __forceinline__ void load_yplane(const Fgp3Args<T>& a, int kl, int i0, int j0,
-                                            T (*sy)[RY][RX]) {
-  using A = Ar<T>;
-  const T* qk;
-  const T* qm;
-  int64_t cs, po;
-  plane_src(a, kl, qk, qm, cs, po);
-  const bool mom = a.beta != T(0);
-  const bool rp = a.rep && a.it == 0;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-  for (int e = tid; e < RY * RX; e += nt) {
-    const int ry = e / RX, rx = e % RX;
-    const int r = i0 - 1 + ry, c = j0 - 1 + rx;
-    T v0 = T(0), v1 = T(0), v2 = T(0);
-    if (r >= 0 && r < a.H && c >= 0 && c < a.W && qk != nullptr) {
-      const int64_t o = po + (int64_t)r * a.W + c;
-      v0 = qk[o];
-      v1 = qk[cs + o];
-      v2 = qk[2 * cs + o];
-      if (rp) {
-        const T s = A::ball_scale3(v0, v1, v2, a.w);
-        v0 = A::mul(v0, s);
-        v1 = A::mul(v1, s);
-        v2 = A::mul(v2, s);
-      }
-      if (mom) {
-        v0 = A::add(v0, A::mul(a.beta, A::sub(v0, qm[o])));
-        v1 = A::add(v1, A::mul(a.beta, A::sub(v1, qm[cs + o])));
-        v2 = A::add(v2, A::mul(a.beta, A::sub(v2, qm[2 * cs + o])));
-      }
-    }
-    sy[0][ry][rx] = v0;
-    sy[1][ry][rx] = v1;
-    sy[2][ry][rx] = v2;
-  }
-}
-
-// u(kl) = clamp(x + div y) on rows i0..i0+TY, cols j0..j0+TX; `yc` = y(kl), `yp` = y(kl-1)
-template <class T>
-__device__ __forceinline__ void prim_plane(const Fgp3Args<T>& a, int kl, int i0, int j0,
-                                           T (*yc)[RY][RX], T (*yp)[RY][RX],
-                                           T (*su)[TX + 1]) {
-  using A = Ar<T>;
-  const int kg = a.z0 + kl;
-  const int64_t HW = (int64_t)a.H * a.W;
-  const T* xs = (kl < a.D) ? a.x + (int64_t)kl * HW : a.ha_x;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-  for (int e = tid; e < (TY + 1) * (TX + 1); e += nt) {
-    const int uy = e / (TX + 1), ux = e % (TX + 1);
-    const int ry = uy + 1, rx = ux + 1;
-    const int r = i0 + uy, c = j0 + ux;
-    T u = T(0);
-    if (r < a.H && c < a.W) {
-      T d = T(0);
-      if (kg < a.Dg - 1) d = A::add(d, yc[0][ry][rx]);
-      if (kg > 0) d = A::sub(d, yp[0][ry][rx]);
-      if (r < a.H - 1) d = A::add(d, yc[1][ry][rx]);
-      if (r > 0) d = A::sub(d, yc[1][ry - 1][rx]);
-      if (c < a.W - 1) d = A::add(d, yc[2][ry][rx]);
-      if (c > 0) d = A::sub(d, yc[2][ry][rx - 1]);
-      u = A::add(xs[(int64_t)r * a.W + c], d);
-      if (a.nonneg) u = u > T(0) ? u : T(0);
-    }
-    su[uy][ux] = u;
-  }
-}
-
-template <class T>
-__global__ void __launch_bounds__(TX * TY) fgp3d_iter_kernel(Fgp3Args<T> a) {
-  using A = Ar<T>;
-  __shared__ T sy[3][3][RY][RX];      // three rotating y planes (prev, cur, next)
-  __shared__ T su[2][TY + 1][TX + 1];  // u planes (cur, next)
-  const int i0 = blockIdx.y * TY, j0 = blockIdx.x * TX;
-  const int ks = blockIdx.z * a.zchunk;
-  const int ke = min(a.D, ks + a.zchunk);
-  if (ks >= ke) return;
-  const int64_t HW = (int64_t)a.H * a.W, N3 = (int64_t)a.D * HW;
-  T* qo = a.q + (int64_t)((a.it + 1) % 3) * 3 * N3;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int r = i0 + ty, c = j0 + tx;
-
-  int P = 0, Cc = 1, Nn = 2, UC = 0, UN = 1;
-  // prologue: y(ks - 1) (only its z channel is used), y(ks), u(ks)
-  if (a.z0 + ks > 0) load_yplane(a, ks - 1, i0, j0, sy[P]);
-  load_yplane(a, ks, i0, j0, sy[Cc]);
-  __syncthreads();
-  prim_plane(a, ks, i0, j0, sy[Cc], sy[P], su[UC]);
-  __syncthreads();
-  for (int k = ks; k < ke; ++k) {
-    const int kg = a.z0 + k;
-    const bool nxt = kg + 1 < a.Dg;
-    if (nxt) {
-      load_yplane(a, k + 1, i0, j0, sy[Nn]);
-      __syncthreads();
-      prim_plane(a, k + 1, i0, j0, sy[Nn], sy[Cc], su[UN]);
-      __syncthreads();
-    }
-    if (r < a.H && c < a.W) {
-      const int ry = ty + 1, rx = tx + 1;
-      const T uc = su[UC][ty][tx];
-      const T gz = nxt ? A::sub(su[UN][ty][tx], uc) : T(0);
-      const T gy = r < a.H - 1 ? A::sub(su[UC][ty + 1][tx], uc) : T(0);
-      const T gx = c < a.W - 1 ? A::sub(su[UC][ty][tx + 1], uc) : T(0);
-      const T az = A::add(sy[Cc][0][ry][rx], A::mul(a.step, gz));
-      const T ay = A::add(sy[Cc][1][ry][rx], A::mul(a.step, gy));
-      const T ax = A::add(sy[Cc][2][ry][rx], A::mul(a.step, gx));
-      const T s = A::ball_scale3(az, ay, ax, a.w);
-      const int64_t o = (int64_t)k * HW + (int64_t)r * a.W + c;
-      qo[o] = A::mul(az, s);
-      qo[N3 + o] = A::mul(ay, s);
-      qo[2 * N3 + o] = A::mul(ax, s);
-    }
-    __syncthreads();
-    const int t = P;
-    P = Cc;
-    Cc = Nn;
-    Nn = t;
-    UC ^= 1;
-    UN ^= 1;
   }
 }
 

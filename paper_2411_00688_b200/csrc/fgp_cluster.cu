@@ -6,7 +6,7 @@
 //           prox input z = (x - g(x - b)) + hc h            (skip.py:66-70)
 //   FGP   : all n_inner accelerated iterations (tv.py:75-80) with the
 //           problem's x, q_k, q_{k-1} resident in REGISTERS of a 16-CTA
-//           thread-block cluster (16 SMs, 512 threads each, 8 pixels per
+//           thread-block cluster (16 SMs, 1024 threads each, 4 pixels per
 //           thread); row halos cross CTA boundaries through distributed
 //           shared memory, column halos through warp shuffles and shared
 //           memory; one cluster barrier per inner iteration
@@ -34,11 +34,11 @@ namespace psb {
 namespace {
 
 constexpr int CW = 256;           // image width  (columns = threads per row group)
-constexpr int CRG = 2;            // row groups per CTA
-constexpr int CRPT = 8;           // rows per thread
+constexpr int CRG = 4;            // row groups per CTA
+constexpr int CRPT = 4;           // rows per thread
 constexpr int CCL = 16;           // CTAs per cluster
 constexpr int CH = CCL * CRG * CRPT;  // image height = 256
-constexpr int CTHREADS = CW * CRG;    // 512
+constexpr int CTHREADS = CW * CRG;    // 1024
 constexpr int CWARPS_ROW = CW / 32;   // 8 warps across a row group
 
 template <class TO>
@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
 
   __shared__ float pub_top[2][2][CW];  // [parity][channel][col]: first row of q
   __shared__ float pub_bot[2][CW];     // [parity][col]: last row of q, row channel
-  __shared__ float s_rg_yy[CW];        // row group 0's last-row y_y (for group 1's div)
-  __shared__ float s_rg_u[CW];         // row group 1's first-row u (for group 0's grad)
+  __shared__ float s_rg_yy[CRG][CW];   // each row group's last-row y_y (for the group below)
+  __shared__ float s_rg_u[CRG][CW];    // each row group's first-row u (for the group above)
   __shared__ float s_edge_yx[CRG][CWARPS_ROW][CRPT + 1];
   __shared__ float s_edge_u[CRG][CWARPS_ROW][CRPT + 1];
 
@@ -195,14 +195,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       ex_y = dn_ky + beta * (dn_ky - dn_my);
       ex_x = dn_kx + beta * (dn_kx - dn_mx);
     }
-    if (rg_top) s_rg_yy[j] = yy[CRPT - 1];
+    s_rg_yy[rg][j] = yy[CRPT - 1];
     if (lane == 31) {
 #pragma unroll
       for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = yx[t];
       s_edge_yx[rg][wc][CRPT] = ex_x;
     }
     __syncthreads();
-    const float yy_above = rg_top ? y_up : s_rg_yy[j];
+    const float yy_above = rg_top ? y_up : s_rg_yy[rg - 1][j];
     float u[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
@@ -221,14 +221,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       const float v = z_ex + d;
       u_ex = nonneg ? fmaxf(v, 0.f) : v;
     }
-    if (rg_bot) s_rg_u[j] = u[0];
+    s_rg_u[rg][j] = u[0];
     if (lane == 0) {
 #pragma unroll
       for (int t = 0; t < CRPT; ++t) s_edge_u[rg][wc][t] = u[t];
     }
     __syncthreads();
     // the global last row has no row below: gy = 0 (below := u)
-    const float u_below = rg_top ? s_rg_u[j] : (last_row_thread ? u[CRPT - 1] : u_ex);
+    const float u_below = !rg_bot ? s_rg_u[rg + 1][j] : (last_row_thread ? u[CRPT - 1] : u_ex);
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float right = __shfl_down_sync(0xffffffffu, u[t], 1);
@@ -270,13 +270,13 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   float yy_above = 0.f;
   if (rg_top && has_up)
     yy_above = cluster.map_shared_rank(&pub_bot[(a.n_inner - 1) & 1][0], cr - 1)[j];
-  if (rg_top) s_rg_yy[j] = qky[CRPT - 1];
+  s_rg_yy[rg][j] = qky[CRPT - 1];
   if (lane == 31) {
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = qkx[t];
   }
   __syncthreads();
-  if (!rg_top) yy_above = s_rg_yy[j];
+  if (!rg_top) yy_above = s_rg_yy[rg - 1][j];
   bool ok = true;
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
