@@ -124,75 +124,114 @@ struct Row3 {
   T hu;
 };
 
+// ---- cp.async staging: each lane copies its own row segment of the 7 plane
+// arrays (q_k 3 ch, q_{k-1} 3 ch, x) into a 2-stage shared-memory ring one
+// plane ahead of the compute, so DRAM latency overlaps a whole plane step.
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+template <int B>
+__device__ __forceinline__ void cp_async_small(void* dst, const void* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = pred ? B : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(B), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 template <class T, int V>
-__device__ __forceinline__ void load_plane_row(const Fgp3Args<T>& a, int kl, int i, int cl, bool lin,
-                                               int hc, bool hval, bool mom, bool rp,
-                                               Row3<T, V>& R, T (&xv)[V], T& hx) {
-  using A = Ar<T>;
+__device__ __forceinline__ void copy_vec(T* dst, const T* src, bool pred) {
+  if constexpr (sizeof(T) * V == 16) {
+    cp_async_16(dst, src, pred);
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) cp_async_small<sizeof(T)>(dst + v, src + v, pred);
+  }
+}
+
+// stage layout per warp: [7][32*V] (arrays: k0 k1 k2 m0 m1 m2 x) + halo [7][2]
+template <class T, int V>
+__device__ __forceinline__ void issue_plane(const Fgp3Args<T>& a, int kl, int i, int cl, bool lin,
+                                            int hc, bool hval, bool mom, int lane, T* st, T* hs) {
   const T* qk;
   const T* qm;
   int64_t cs, po;
   plane_src(a, kl, qk, qm, cs, po);
   const int64_t HW = (int64_t)a.H * a.W;
-  const T* xs = (kl < a.D) ? a.x + (int64_t)kl * HW : a.ha_x;
-  auto one = [&](int64_t o, T& v0, T& v1, T& v2) {
+  const T* xs = (kl < 0) ? nullptr : (kl < a.D ? a.x + (int64_t)kl * HW : a.ha_x);
+  constexpr int BW = 32 * V;
+  const T* dummy = a.x;
+  const int64_t o = po + (int64_t)i * a.W + cl;
+  const bool lq = lin && qk != nullptr;
+  const bool lm = lq && mom;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    copy_vec<T, V>(st + c * BW + lane * V, lq ? qk + c * cs + o : dummy, lq);
+    copy_vec<T, V>(st + (3 + c) * BW + lane * V, lm ? qm + c * cs + o : dummy, lm);
+  }
+  const bool lx = lin && xs != nullptr;
+  copy_vec<T, V>(st + 6 * BW + lane * V, lx ? xs + (int64_t)i * a.W + cl : dummy, lx);
+  if (lane == 0 || lane == 31) {
+    const int hs_i = lane == 0 ? 0 : 1;
+    const int64_t oh = po + (int64_t)i * a.W + hc;
+    const bool hq = hval && qk != nullptr, hm = hq && mom, hx = hval && xs != nullptr;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      cp_async_small<sizeof(T)>(hs + c * 2 + hs_i, hq ? qk + c * cs + oh : dummy, hq);
+      cp_async_small<sizeof(T)>(hs + (3 + c) * 2 + hs_i, hm ? qm + c * cs + oh : dummy, hm);
+    }
+    cp_async_small<sizeof(T)>(hs + 6 * 2 + hs_i, hx ? xs + (int64_t)i * a.W + hc : dummy, hx);
+  }
+}
+
+template <class T, int V>
+__device__ __forceinline__ void read_plane(const Fgp3Args<T>& a, bool mom, bool rp, int lane,
+                                           const T* st, const T* hs, Row3<T, V>& R, T (&xv)[V],
+                                           T& hx) {
+  using A = Ar<T>;
+  constexpr int BW = 32 * V;
+  T k[3][V], m[3][V];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      k[c][v] = st[c * BW + lane * V + v];
+      m[c][v] = st[(3 + c) * BW + lane * V + v];
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) xv[v] = st[6 * BW + lane * V + v];
+  auto y_of = [&](T& v0, T& v1, T& v2, T n0, T n1, T n2) {
     if (rp) {
       const T s = A::ball_scale3(v0, v1, v2, a.w);
       v0 = A::mul(v0, s);
       v1 = A::mul(v1, s);
       v2 = A::mul(v2, s);
     }
-    (void)o;
+    if (mom) {
+      v0 = A::add(v0, A::mul(a.beta, A::sub(v0, n0)));
+      v1 = A::add(v1, A::mul(a.beta, A::sub(v1, n1)));
+      v2 = A::add(v2, A::mul(a.beta, A::sub(v2, n2)));
+    }
   };
-  if (lin) {
-    const int64_t o = po + (int64_t)i * a.W + cl;
-    T k0[V], k1[V], k2[V];
-    ldv<T, V>(k0, qk + o);
-    ldv<T, V>(k1, qk + cs + o);
-    ldv<T, V>(k2, qk + 2 * cs + o);
-    if (xs) ldv<T, V>(xv, xs + (int64_t)i * a.W + cl);
-    if (mom) {
-      T m0[V], m1[V], m2[V];
-      ldv<T, V>(m0, qm + o);
-      ldv<T, V>(m1, qm + cs + o);
-      ldv<T, V>(m2, qm + 2 * cs + o);
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        R.y[0][v] = A::add(k0[v], A::mul(a.beta, A::sub(k0[v], m0[v])));
-        R.y[1][v] = A::add(k1[v], A::mul(a.beta, A::sub(k1[v], m1[v])));
-        R.y[2][v] = A::add(k2[v], A::mul(a.beta, A::sub(k2[v], m2[v])));
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        T v0 = k0[v], v1 = k1[v], v2 = k2[v];
-        one(0, v0, v1, v2);
-        R.y[0][v] = v0;
-        R.y[1][v] = v1;
-        R.y[2][v] = v2;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int v = 0; v < V; ++v) R.y[0][v] = R.y[1][v] = R.y[2][v] = xv[v] = T(0);
+  for (int v = 0; v < V; ++v) {
+    T v0 = k[0][v], v1 = k[1][v], v2 = k[2][v];
+    y_of(v0, v1, v2, m[0][v], m[1][v], m[2][v]);
+    R.y[0][v] = v0;
+    R.y[1][v] = v1;
+    R.y[2][v] = v2;
   }
-  R.h[0] = R.h[1] = R.h[2] = T(0);
-  hx = T(0);
-  if (hval) {
-    const int64_t o = po + (int64_t)i * a.W + hc;
-    T v0 = qk[o], v1 = qk[cs + o], v2 = qk[2 * cs + o];
-    if (mom) {
-      v0 = A::add(v0, A::mul(a.beta, A::sub(v0, qm[o])));
-      v1 = A::add(v1, A::mul(a.beta, A::sub(v1, qm[cs + o])));
-      v2 = A::add(v2, A::mul(a.beta, A::sub(v2, qm[2 * cs + o])));
-    } else {
-      one(0, v0, v1, v2);
-    }
-    R.h[0] = v0;
-    R.h[1] = v1;
-    R.h[2] = v2;
-    if (xs) hx = xs[(int64_t)i * a.W + hc];
-  }
+  const int hi = lane == 31 ? 1 : 0;
+  T h0 = hs[0 * 2 + hi], h1 = hs[1 * 2 + hi], h2 = hs[2 * 2 + hi];
+  y_of(h0, h1, h2, hs[3 * 2 + hi], hs[4 * 2 + hi], hs[5 * 2 + hi]);
+  R.h[0] = h0;
+  R.h[1] = h1;
+  R.h[2] = h2;
+  hx = hs[6 * 2 + hi];
 }
 
 template <class T, int V>
@@ -260,19 +299,38 @@ __global__ void __launch_bounds__((MTY + 2) * 32) fgp3d_march_kernel(Fgp3Args<T>
     for (int v = 0; v < V; ++v) s_u[par][w][lane * V + v] = R.u[v];
   };
 
+  extern __shared__ unsigned char dyn_smem[];
+  T* stage0 = reinterpret_cast<T*>(dyn_smem);
+  constexpr int SW = 7 * BW;  // per-warp stage floats
+  T* hs_all = stage0 + (size_t)2 * (MTY + 2) * SW;
+  auto st_ptr = [&](int sidx) { return stage0 + (size_t)(sidx * (MTY + 2) + w) * SW; };
+  auto hs_ptr = [&](int sidx) { return hs_all + (size_t)(sidx * (MTY + 2) + w) * 14; };
+
   Row3<T, V> C, N;
   T yzp[V], hyzp = T(0), xv[V], hx;
 #pragma unroll
   for (int v = 0; v < V; ++v) yzp[v] = T(0);
-  // prologue: y_z of plane ks-1, then plane ks and u(ks)
+  // prologue: y_z of plane ks-1 (synchronously), then planes ks and ks+1 in flight
   if (a.z0 + ks > 0) {
     T xd[V], hxd;
-    load_plane_row<T, V>(a, ks - 1, i, cl, lin, hc, hval, mom, rp, N, xd, hxd);
+    issue_plane<T, V>(a, ks - 1, i, cl, lin, hc, hval, mom, lane, st_ptr(0), hs_ptr(0));
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    read_plane<T, V>(a, mom, rp, lane, st_ptr(0), hs_ptr(0), N, xd, hxd);
 #pragma unroll
     for (int v = 0; v < V; ++v) yzp[v] = N.y[0][v];
     hyzp = N.h[0];
+    __syncwarp();
   }
-  load_plane_row<T, V>(a, ks, i, cl, lin, hc, hval, mom, rp, C, xv, hx);
+  issue_plane<T, V>(a, ks, i, cl, lin, hc, hval, mom, lane, st_ptr(0), hs_ptr(0));
+  cp_async_commit();
+  if (a.z0 + ks + 1 < a.Dg)
+    issue_plane<T, V>(a, ks + 1, i, cl, lin, hc, hval, mom, lane, st_ptr(1), hs_ptr(1));
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncwarp();
+  read_plane<T, V>(a, mom, rp, lane, st_ptr(0), hs_ptr(0), C, xv, hx);
   publish_yy(C);
   __syncthreads();
   prim(a.z0 + ks, C, yzp, hyzp, xv, hx);
@@ -283,7 +341,15 @@ __global__ void __launch_bounds__((MTY + 2) * 32) fgp3d_march_kernel(Fgp3Args<T>
     const int kg = a.z0 + k;
     const bool nxt = kg + 1 < a.Dg;
     if (nxt) {
-      load_plane_row<T, V>(a, k + 1, i, cl, lin, hc, hval, mom, rp, N, xv, hx);
+      // plane k+1 was issued one step ago into stage (k+1-ks)&1; put plane k+2
+      // into the stage plane k used, then wait for plane k+1 only
+      const int sn = (k + 1 - ks) & 1;
+      if (kg + 2 < a.Dg)
+        issue_plane<T, V>(a, k + 2, i, cl, lin, hc, hval, mom, lane, st_ptr(sn ^ 1), hs_ptr(sn ^ 1));
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      read_plane<T, V>(a, mom, rp, lane, st_ptr(sn), hs_ptr(sn), N, xv, hx);
       publish_yy(N);
     }
     __syncthreads();
@@ -329,6 +395,11 @@ __global__ void __launch_bounds__((MTY + 2) * 32) fgp3d_march_kernel(Fgp3Args<T>
   }
 }
 
+template <class T, int V>
+size_t march_smem() {
+  return sizeof(T) * ((size_t)2 * (MTY + 2) * 7 * 32 * V + (size_t)2 * (MTY + 2) * 14);
+}
+
 template <class T>
 int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   constexpr int VMAX = 16 / sizeof(T);
@@ -337,11 +408,17 @@ int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   const bool vec = (a.W % VMAX == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(a.q) % 16 == 0);
   if (vec) {
+    const size_t sm = march_smem<T, VMAX>();
+    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, VMAX>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 grid((a.W + 32 * VMAX - 1) / (32 * VMAX), (a.H + MTY - 1) / MTY, nz);
-    fgp3d_march_kernel<T, VMAX><<<grid, (MTY + 2) * 32, 0, st>>>(a);
+    fgp3d_march_kernel<T, VMAX><<<grid, (MTY + 2) * 32, sm, st>>>(a);
   } else {
+    const size_t sm = march_smem<T, 1>();
+    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, 1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 grid((a.W + 31) / 32, (a.H + MTY - 1) / MTY, nz);
-    fgp3d_march_kernel<T, 1><<<grid, (MTY + 2) * 32, 0, st>>>(a);
+    fgp3d_march_kernel<T, 1><<<grid, (MTY + 2) * 32, sm, st>>>(a);
   }
   PSB_LAUNCHED("fgp3d_march");
   return PSB_OK;
