@@ -143,6 +143,16 @@ int psb_proxskip_post(int dtype_outer, int dtype_fgp, void* x, const void* g_or_
                       int n_active, int H, int W, int n_inner, int nonneg, double gamma, double pg,
                       int32_t* bad_iter, int k, void* stream);
 
+/* psb_skip_chain: `pend` deferred skipped ProxSkip iterations of the identity
+ * fidelity (skip.py:68, h unchanged), executed in registers in the reference's
+ * op order -- bit-identical to `pend` separate passes.  z != NULL: write the
+ * prox input z = (x_m - gamma (x_m - b)) + hcoef h and leave x in memory
+ * (the post kernel recomputes x_m); z == NULL: store x_m (end-of-run flush).
+ * Non-finite x_m at step s records kfirst + s in bad_iter[0]. */
+int psb_skip_chain(int dtype_outer, int dtype_fgp, void* x, const void* b, const void* h, void* z,
+                   int64_t count, int pend, double gamma, double hcoef, int32_t* bad_iter,
+                   int kfirst, void* stream);
+
 /* ---- fused run drivers (the native runtime) ---------------------------------
  * psb_proxskip_denoise_run: K outer ProxSkip iterations of the implicit TV
  *   denoising problem (identity fidelity; problems.py:117-132 + skip.py:46-79)
@@ -216,7 +226,8 @@ int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* 
  * (NULL when z0 == 0), halo_above_* plane z0+D of q_it / q_{it-1} and of x
  * (NULL when z0+D == Dg).  zchunk <= 0 picks the z-chunk per CTA.
  * psb_proxskip_post3d: identity-fidelity ProxSkip post fused with the 3-D
- * finalize; halo_below_qn = plane z0-1 of the final dual iterate. */
+ * finalize; halo_below_qn = plane z0-1 of the final dual iterate; `pend`
+ * deferred skip iterations are applied to x (in registers) before x-hat. */
 int psb_fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z0, int Dg, int it,
                    double beta_prev, double step, double weight, int reproject, int nonneg,
                    const void* halo_below_qk, const void* halo_below_qm, const void* halo_above_qk,
@@ -224,7 +235,7 @@ int psb_fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z
 int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
                         const void* z, void* q, const void* halo_below_qn, int D, int H, int W,
                         int z0, int Dg, int n_inner, int nonneg, double gamma, double pg,
-                        int32_t* bad_iter, int k, void* stream);
+                        int pend, int32_t* bad_iter, int k, void* stream);
 
 /* psb_cluster_max_active: how many 16-CTA clusters of the cluster-resident
  * 256x256 ProxSkip kernel (csrc/fgp_cluster.cu, used by

@@ -66,7 +66,8 @@ SIGNATURES = {
     "psb_fgp3d_iter": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32,
                        _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
     "psb_proxskip_post3d": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
-                            _i32, _i32, _i32, _dbl, _dbl, _vp, _i32, _vp],
+                            _i32, _i32, _i32, _dbl, _dbl, _i32, _vp, _i32, _vp],
+    "psb_skip_chain": [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _dbl, _dbl, _vp, _i32, _vp],
     "psb_radon_fwd": [_i32, _geo, _vp, _vp, _vp],
     "psb_radon_adj": [_i32, _geo, _vp, _vp, _vp],
     "psb_pdhg_step": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _dbl, _dbl, _dbl, _dbl,

@@ -68,7 +68,7 @@ __global__ void proxskip_post3d_kernel(TO* __restrict__ x, const TO* __restrict_
                                        TO* __restrict__ h, const TF* __restrict__ z, TF* q,
                                        const TF* __restrict__ hb_qn, int D, int H, int W, int z0,
                                        int Dg, int n_inner, int nonneg, TO gamma, TO pg,
-                                       int32_t* bad, int kiter) {
+                                       int pend, int32_t* bad, int kiter) {
   using A = Ar<TO>;
   using F = Ar<TF>;
   const int64_t HW = (int64_t)H * W, N3 = (int64_t)D * HW;
@@ -95,8 +95,12 @@ __global__ void proxskip_post3d_kernel(TO* __restrict__ x, const TO* __restrict_
       q[N3 + i] = vy;
       q[2 * N3 + i] = vx;
     }
-    const TO xo = x[i], ho = h[i];
-    const TO xhat = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, b[i]))), A::mul(gamma, ho));
+    TO xo = x[i];
+    const TO ho = h[i], bo = b[i];
+    // the `pend` deferred skip iterations since x was last stored (skip.py:68)
+    for (int s = 0; s < pend; ++s)
+      xo = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(gamma, ho));
+    const TO xhat = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(gamma, ho));
     const TO xn = (TO)uf;
     h[i] = A::add(ho, A::mul(pg, A::sub(xn, xhat)));
     x[i] = xn;
@@ -459,22 +463,24 @@ int fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z0, i
 
 int proxskip_post3d(int dto, int dtf, void* x, const void* b, void* h, const void* z, void* q,
                     const void* hb_qn, int D, int H, int W, int z0, int Dg, int n_inner,
-                    int nonneg, double gamma, double pg, int32_t* bad, int k, cudaStream_t st) {
+                    int nonneg, double gamma, double pg, int pend, int32_t* bad, int k,
+                    cudaStream_t st) {
   PSB_REQUIRE(z0 == 0 || hb_qn, "proxskip3d: slab above plane 0 needs the halo below");
+  PSB_REQUIRE(pend >= 0, "proxskip3d: negative deferred-skip count");
   const int64_t N3 = (int64_t)D * H * W;
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((N3 + 255) / 256, 16LL * sm_count())));
   if (dto == PSB_F32 && dtf == PSB_F32)
     proxskip_post3d_kernel<float, float><<<grid, 256, 0, st>>>(
         (float*)x, (const float*)b, (float*)h, (const float*)z, (float*)q, (const float*)hb_qn, D,
-        H, W, z0, Dg, n_inner, nonneg, (float)gamma, (float)pg, bad, k);
+        H, W, z0, Dg, n_inner, nonneg, (float)gamma, (float)pg, pend, bad, k);
   else if (dto == PSB_F64 && dtf == PSB_F64)
     proxskip_post3d_kernel<double, double><<<grid, 256, 0, st>>>(
         (double*)x, (const double*)b, (double*)h, (const double*)z, (double*)q,
-        (const double*)hb_qn, D, H, W, z0, Dg, n_inner, nonneg, gamma, pg, bad, k);
+        (const double*)hb_qn, D, H, W, z0, Dg, n_inner, nonneg, gamma, pg, pend, bad, k);
   else if (dto == PSB_F64 && dtf == PSB_F32)
     proxskip_post3d_kernel<double, float><<<grid, 256, 0, st>>>(
         (double*)x, (const double*)b, (double*)h, (const float*)z, (float*)q, (const float*)hb_qn,
-        D, H, W, z0, Dg, n_inner, nonneg, gamma, pg, bad, k);
+        D, H, W, z0, Dg, n_inner, nonneg, gamma, pg, pend, bad, k);
   else
     return fail(PSB_ERR_VALUE, "proxskip3d: unsupported dtype pair");
   PSB_LAUNCHED("proxskip_post3d");
@@ -497,9 +503,10 @@ int psb_fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z
 int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
                         const void* z, void* q, const void* halo_below_qn, int D, int H, int W,
                         int z0, int Dg, int n_inner, int nonneg, double gamma, double pg,
-                        int32_t* bad_iter, int k, void* stream) {
+                        int pend, int32_t* bad_iter, int k, void* stream) {
   return psb::proxskip_post3d(dtype_outer, dtype_fgp, x, b, h, z, q, halo_below_qn, D, H, W, z0,
-                              Dg, n_inner, nonneg, gamma, pg, bad_iter, k, psb::as_stream(stream));
+                              Dg, n_inner, nonneg, gamma, pg, pend, bad_iter, k,
+                              psb::as_stream(stream));
 }
 
 }  // extern "C"

@@ -120,7 +120,57 @@ void launch_post(void* x, const void* gb, int ident, void* h, const void* z, voi
         (TO)gamma, (TO)pg, bad, k);
 }
 
+// Deferred skip iterations of the identity-fidelity ProxSkip (skip.py:68 with
+// h unchanged, repeated `pend` times in registers, bit-identical to `pend`
+// separate passes).  z != NULL: write the prox input z = (x_m - g(x_m - b)) +
+// hc h without storing x_m (the post kernel recomputes it); z == NULL: store
+// x_m (flush).
+template <class TO, class TF>
+__global__ void skip_chain_kernel(TO* __restrict__ x, const TO* __restrict__ b,
+                                  const TO* __restrict__ h, TF* __restrict__ z, int64_t count,
+                                  int pend, TO gamma, TO hcoef, int32_t* bad, int kfirst) {
+  using A = Ar<TO>;
+  int kbad = 0x7fffffff;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    TO xo = x[i];
+    const TO bo = b[i], ho = h[i];
+    for (int s = 0; s < pend; ++s) {
+      xo = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(gamma, ho));
+      if (!finite(xo)) kbad = min(kbad, kfirst + s);
+    }
+    if (z)
+      z[i] = (TF)A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(hcoef, ho));
+    else
+      x[i] = xo;
+  }
+  if (kbad != 0x7fffffff && bad) atomicMin(bad, kbad);
+}
+
 }  // namespace
+
+int skip_chain(int dto, int dtf, void* x, const void* b, const void* h, void* z, int64_t count,
+               int pend, double gamma, double hcoef, int32_t* bad, int kfirst, cudaStream_t st) {
+  PSB_REQUIRE(pend >= 0, "skip chain: negative count");
+  if (count == 0 || (pend == 0 && z == nullptr)) return PSB_OK;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 16LL * sm_count())));
+  if (dto == PSB_F32 && dtf == PSB_F32)
+    skip_chain_kernel<float, float><<<grid, 256, 0, st>>>((float*)x, (const float*)b, (const float*)h,
+                                                         (float*)z, count, pend, (float)gamma,
+                                                         (float)hcoef, bad, kfirst);
+  else if (dto == PSB_F64 && dtf == PSB_F32)
+    skip_chain_kernel<double, float><<<grid, 256, 0, st>>>((double*)x, (const double*)b,
+                                                          (const double*)h, (float*)z, count, pend,
+                                                          gamma, hcoef, bad, kfirst);
+  else if (dto == PSB_F64 && dtf == PSB_F64)
+    skip_chain_kernel<double, double><<<grid, 256, 0, st>>>((double*)x, (const double*)b,
+                                                           (const double*)h, (double*)z, count,
+                                                           pend, gamma, hcoef, bad, kfirst);
+  else
+    return fail(PSB_ERR_VALUE, "skip chain: unsupported dtype pair");
+  PSB_LAUNCHED("skip_chain");
+  return PSB_OK;
+}
 
 int proxskip_pre(int dto, int dtf, void* x, const void* gb, int ident, const void* h, void* z,
                  int64_t n, int64_t HW, const uint8_t* coins, double gamma, double hcoef,
@@ -179,6 +229,13 @@ int psb_proxskip_post(int dtype_outer, int dtype_fgp, void* x, const void* g_or_
   return psb::proxskip_post(dtype_outer, dtype_fgp, x, g_or_b, ident, h, z, q, q_pstride, active,
                             n_active, H, W, n_inner, nonneg, gamma, pg, bad_iter, k,
                             psb::as_stream(stream));
+}
+
+int psb_skip_chain(int dtype_outer, int dtype_fgp, void* x, const void* b, const void* h, void* z,
+                   int64_t count, int pend, double gamma, double hcoef, int32_t* bad_iter,
+                   int kfirst, void* stream) {
+  return psb::skip_chain(dtype_outer, dtype_fgp, x, b, h, z, count, pend, gamma, hcoef, bad_iter,
+                         kfirst, psb::as_stream(stream));
 }
 
 }  // extern "C"

@@ -124,11 +124,22 @@ class Slab3D:
                L.ptr(ha[0:3]) if ha is not None else None,
                L.ptr(ha[3:6]) if ha is not None else None, L.ptr(self.hx), 0, L.stream())
 
-    def post(self, k, gamma, p):
+    def chain_pre(self, pend, kfirst, gamma, p):
+        """Prox input after `pend` deferred skips, x left stale in memory."""
+        L.call("psb_skip_chain", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
+               L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), self.x.numel(), int(pend),
+               float(gamma), gamma - gamma / p, L.ptr(self.bad), int(kfirst), L.stream())
+
+    def flush(self, pend, kfirst, gamma):
+        L.call("psb_skip_chain", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
+               L.ptr(self.b), L.ptr(self.h), None, self.x.numel(), int(pend), float(gamma), 0.0,
+               L.ptr(self.bad), int(kfirst), L.stream())
+
+    def post(self, k, gamma, p, pend=0):
         L.call("psb_proxskip_post3d", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
                L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), L.ptr(self.q), L.ptr(self.hqn),
                self.D, self.H, self.W, self.z0, self.Dg, self.inner, int(self.nonneg),
-               float(gamma), p / gamma, L.ptr(self.bad), k, L.stream())
+               float(gamma), p / gamma, int(pend), L.ptr(self.bad), k, L.stream())
 
     def check_finite(self):
         kb = int(self.bad.item())
@@ -209,9 +220,16 @@ class DistExchange:
                 req.wait()
 
 
-def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_events=None):
+def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_events=None,
+                       defer_skips=True):
     """K outer ProxSkip iterations over a set of slabs (one global coin stream).
 
+    With ``defer_skips`` (default) a skipped iteration launches nothing: the
+    run of skips since the last prox call is executed in registers by the next
+    prox call's pre/post kernels (psb_skip_chain / psb_proxskip_post3d with
+    `pend`) or by the final flush -- the same arithmetic in the same order,
+    bit-identical to one pass per skip (``defer_skips=False``), without the
+    16 B/voxel HBM round trip per skipped iteration.
     ``fgp_events`` (optional list) collects (start, end) CUDA events around
     each FGP inner-iteration launch for roofline accounting."""
     exchange = exchange or LocalExchange()
@@ -219,11 +237,20 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
     alpha = s0.alpha
     weight = (gamma / p) * alpha  # prox_g(z, gamma/p) -> tv_prox(z, step * alpha)
     betas = _betas(s0.inner)
-    for k, theta in enumerate(np.asarray(coins, dtype=np.uint8)):
-        for s in slabs:
-            s.pre(k, int(theta), gamma, p)
-        if not theta:
-            continue
+    pend = 0
+    coins = np.asarray(coins, dtype=np.uint8)
+    for k, theta in enumerate(coins):
+        if defer_skips:
+            if not theta:
+                pend += 1
+                continue
+            for s in slabs:
+                s.chain_pre(pend, k - pend, gamma, p)
+        else:
+            for s in slabs:
+                s.pre(k, int(theta), gamma, p)
+            if not theta:
+                continue
         rep = s0.last_weight is not None and s0.last_weight != weight
         exchange.prox_input(slabs)
         for it in range(s0.inner):
@@ -240,16 +267,20 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
                 fgp_events.append(ev)
         exchange.final_dual(slabs)
         for s in slabs:
-            s.post(k, gamma, p)
+            s.post(k, gamma, p, pend)
             s.last_weight = weight
             s.prox_count += 1
+        pend = 0
+    if pend:
+        for s in slabs:
+            s.flush(pend, len(coins) - pend, gamma)
     for s in slabs:
         s.check_finite()
     return [s.x for s in slabs]
 
 
 def proxskip_denoise3d(b, alpha, p, seed, iters, inner_budget=20, *, n_slabs=1, precision="fp32",
-                       step=STEP_3D):
+                       step=STEP_3D, defer_skips=True):
     """Single-process config-5 entry point (``n_slabs`` > 1 emulates the slab
     decomposition on one GPU).  Returns x in the input's currency."""
     t = AR.to_dev(b, PRECISIONS[precision][0])
@@ -258,7 +289,8 @@ def proxskip_denoise3d(b, alpha, p, seed, iters, inner_budget=20, *, n_slabs=1, 
     for r in range(n_slabs):
         z0, z1 = slab_bounds(Dg, r, n_slabs)
         slabs.append(Slab3D(t[z0:z1], z0, Dg, alpha, inner_budget, precision=precision, step=step))
-    xs = run_proxskip_slabs(slabs, SkipConfig(p, seed).coins(iters), gamma=1.0, p=p)
+    xs = run_proxskip_slabs(slabs, SkipConfig(p, seed).coins(iters), gamma=1.0, p=p,
+                            defer_skips=defer_skips)
     return AR.like(torch.cat(xs, dim=0), b), slabs
 
 
@@ -299,7 +331,7 @@ def tv_prox3d(x, weight, state):
     h = torch.zeros_like(xd)
     L.call("psb_proxskip_post3d", L.dcode(dt), L.dcode(dt), L.ptr(u), L.ptr(u), L.ptr(h), L.ptr(xd),
            L.ptr(state.slots), None, D, H, W, 0, D, state.inner_iters, int(state.nonneg), 1.0, 1.0,
-           None, 0, L.stream())
+           0, None, 0, L.stream())
     state.last_weight = weight
     state.total_inner_iterations += state.inner_iters
     return AR.like(u, x)

@@ -75,3 +75,14 @@ def test_config5_reduced_size_vs_oracle():
     assert rel(x, xr) < 1e-4
     obj = lambda u: 0.5 * np.sum((u - b) ** 2) + 0.08 * o3.tv_total3(u)
     assert abs(obj(x) - obj(xr)) / obj(xr) < 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_deferred_skips_are_bitwise_identical(precision):
+    vol = phantoms.random_ellipsoids((12, 20, 36), 6, np.random.default_rng(3))
+    b = phantoms.add_noise(vol, 0.1, 3)
+    xa, _ = v3.proxskip_denoise3d(b, 0.08, 0.2, 9, 37, 4, n_slabs=2, precision=precision,
+                                  defer_skips=True)
+    xb, _ = v3.proxskip_denoise3d(b, 0.08, 0.2, 9, 37, 4, n_slabs=2, precision=precision,
+                                  defer_skips=False)
+    np.testing.assert_array_equal(xa, xb)
