@@ -118,7 +118,7 @@ __global__ void proxskip_post3d_kernel(TO* __restrict__ x, const TO* __restrict_
 // through shuffles plus one predicated halo column per warp edge, planes
 // through registers.  HBM: x + q_k(3) + q_{k-1}(3) read, q_{k+1}(3) written
 // once per voxel-iteration (40 B fp32), row/column halos re-read from L2.
-constexpr int MTY = 16;
+constexpr int MTY = 8;
 
 template <class T, int V>
 struct Row3 {
@@ -239,7 +239,7 @@ __device__ __forceinline__ void read_plane(const Fgp3Args<T>& a, bool mom, bool 
 }
 
 template <class T, int V>
-__global__ void __launch_bounds__((MTY + 2) * 32) fgp3d_march_kernel(Fgp3Args<T> a) {
+__global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args<T> a) {
   using A = Ar<T>;
   constexpr int BW = 32 * V;
   __shared__ T s_yy[MTY + 2][BW + 1];
@@ -442,9 +442,9 @@ int fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z0, i
   if (zchunk <= 0) {
     // enough CTAs for ~4 waves; long chunks amortise the two halo planes
     const int64_t tiles = (int64_t)((W + 127) / 128) * ((H + MTY - 1) / MTY);
-    const int64_t want = 4LL * sm_count();
+    const int64_t want = 32LL * sm_count();  // ~16 waves at 2 CTAs/SM: small tail
     int nz = (int)std::max<int64_t>(1, std::min<int64_t>(D, (want + tiles - 1) / tiles));
-    zchunk = std::max(8, (D + nz - 1) / nz);
+    zchunk = std::max(16, (D + nz - 1) / nz);
   }
   if (dtype == PSB_F32) {
     Fgp3Args<float> a{(const float*)x, (float*)q, D, H, W, z0, Dg, it, (float)beta, (float)step,
