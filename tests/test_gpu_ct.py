@@ -137,3 +137,23 @@ def test_config3_full_geometry_parity_150_iters():
     o_dev = psb.objective_tv(x, prob, guarded=False)
     o_ref = oc.tv_objective(xr, pr, guarded=False)
     assert abs(o_dev - o_ref) / abs(o_ref) < 1e-5
+
+
+def test_ct_implicit_saddle_pdhgskip2_fp64(golden):
+    """PDHGSkip-2 on the implicit saddle form (K = A, TV in
+    the warm-started FGP prox with nonneg) -- build_tv_saddle_implicit,
+    problems.py:162-184 -- against the reference trajectory."""
+    g = golden
+    sino = g["ct_b"]
+    R = psb.radon_map(psb.RadonGeometry(image_side=16, n_angles=7, n_bins=23))
+    prob = psb.build_tv_saddle_implicit(R, sino, 0.05, nonneg=True, inner_budget=6,
+                                        precision="fp64")
+    sp = prob.saddle_problem
+    assert sp.norm_K_sq == pytest.approx(float(g["cti_nsq"]), rel=1e-10)
+    s = 1.0 / np.sqrt(float(g["cti_nsq"]))
+    sp.norm_K_sq = float(g["cti_nsq"])
+    xs, fl, log = _traj()
+    psb.run_pdhgskip2(sp, np.zeros((16, 16)), np.zeros((7, 23)), None, s, s,
+                      psb.SkipConfig(0.3, 1), 12, log)
+    np.testing.assert_array_equal(np.array(fl), g["cti_skip_flags"])
+    np.testing.assert_allclose(np.stack(xs), g["cti_skip_traj"], rtol=1e-10, atol=1e-12)
