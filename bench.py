@@ -43,11 +43,13 @@ if CLUSTER:
     KERNEL = ("fgp_cluster_kernel<float>: the whole coin-fired prox step (pre + 50 FGP iterations "
               "+ post) per 16-CTA cluster, FGP state in registers; the 28 B/px-iter of the "
               "streaming formulation stay on-chip, so frac > 1 is expected")
-    # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch / (launch px) -- see profiles/
-    TRAFFIC = None
+    # ncu dram__bytes_read.sum + dram__bytes_write.sum of fgp_cluster_kernel in this bench
+    # (profiles/r01_launches_bench_cluster.csv): 2.23 MB per coin-fired problem per launch
+    TRAFFIC_PER_PROBLEM = 2.23e6
 else:
     KERNEL = "fgp2d_iter_kernel<float,4> (streaming, one launch per inner iteration)"
-    TRAFFIC = None
+    # profiles/r01_fgp2d_iter_ncu_details.csv: 795 MB per launch at 422 problems
+    TRAFFIC_PER_PROBLEM = 795e6 / 422 * INNER
 METRIC = "ProxSkip TV outer iter/s (config 4: 4096 x 256^2 batch, FGP-50, p=0.1)"
 WORKLOAD = "config4: batched ProxSkip TV denoising, 4096 x 256x256, alpha=0.1, p=0.1, FGP-50"
 
@@ -301,7 +303,8 @@ def run_gpu(args):
         "fgp_inner_iter_per_s": inner_rate,
         "fgp_mpx_iter_per_s": inner_rate * HW / 1e6,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": TRAFFIC,
+                     "frac": achieved / peak,
+                     "traffic": TRAFFIC_PER_PROBLEM * float(active.sum()) / max(n_fired_steps, 1),
                      "kernel": KERNEL,
                      "bytes_per_unit": "28 B/pixel-iteration (20 B at the first inner iteration), "
                                        "SURVEY 8(d); x per launch = coin-fired problems x 65536 px "

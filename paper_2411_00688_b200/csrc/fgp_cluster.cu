@@ -40,6 +40,7 @@ constexpr int CCL = 16;           // CTAs per cluster
 constexpr int CH = CCL * CRG * CRPT;  // image height = 256
 constexpr int CTHREADS = CW * CRG;    // 1024
 constexpr int CWARPS_ROW = CW / 32;   // 8 warps across a row group
+constexpr int kMaxBetas = 1024;       // momentum table staged in shared memory
 
 template <class TO>
 struct ClusterArgs {
@@ -69,6 +70,20 @@ __device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
   return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
 }
 
+static_assert(CRPT == 4, "edge exchange packs one float4 per thread row group");
+
+// 32-bit shared::cluster address of `p` in CTA `rank` of this cluster, and a load from it
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
+  uint32_t local = (uint32_t)__cvta_generic_to_shared(p), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  return remote;
+}
+__device__ __forceinline__ float dsmem_ld(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -84,7 +99,7 @@ __device__ __forceinline__ void cluster_wait() {
 // bottom row group also recomputes u for the first row of the CTA below, so
 // no u ever crosses a CTA boundary.  Row groups inside a CTA and warp edges
 // exchange through shared memory with __syncthreads.
-template <class TO>
+template <class TO, bool NONNEG>
 __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO> a) {
   using A = Ar<TO>;
   using F = Ar<float>;
@@ -104,8 +119,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   __shared__ float pub_bot[2][CW];     // [parity][col]: last row of q, row channel
   __shared__ float s_rg_yy[CRG][CW];   // each row group's last-row y_y (for the group below)
   __shared__ float s_rg_u[CRG][CW];    // each row group's first-row u (for the group above)
-  __shared__ float s_edge_yx[CRG][CWARPS_ROW][CRPT + 1];
-  __shared__ float s_edge_u[CRG][CWARPS_ROW][CRPT + 1];
+  __shared__ __align__(16) float s_edge_yx[CRG][CWARPS_ROW][CRPT + 4];  // float4 + extra row
+  __shared__ __align__(16) float s_edge_u[CRG][CWARPS_ROW][CRPT];
+  __shared__ float s_beta[kMaxBetas];
 
   TO* xp = a.x + (int64_t)p * HW;
   const TO* bp = a.b + (int64_t)p * HW;
@@ -116,7 +132,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool rp = a.rep ? a.rep[entry] != 0 : false;
   const TO g = a.gamma;
   const float w = a.weight;
-  const bool nonneg = a.nonneg != 0;
+  constexpr bool nonneg = NONNEG;
+  // momentum table in shared memory (uniform per iteration)
+  for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
 
   float z[CRPT], qky[CRPT], qkx[CRPT], qmy[CRPT], qmx[CRPT];
   int kbad = 0x7fffffff;
@@ -165,11 +183,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool right_edge = lane == 31 && wc == CWARPS_ROW - 1;  // global column W-1
   const bool left_fetch = lane == 0 && wc > 0;
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
+  // neighbours' publish buffers as 32-bit shared::cluster addresses, resolved once
+  const uint32_t nb_bot = dsmem_addr(&pub_bot[0][0], has_up ? cr - 1 : cr);
+  const uint32_t nb_top = dsmem_addr(&pub_top[0][0][0], has_dn ? cr + 1 : cr);
+  const bool betas_in_smem = a.n_inner <= kMaxBetas;
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
                    int it) {
-    const float beta = (a.accelerated && it > 0) ? a.betas[it - 1] : 0.f;
+    const float beta = (a.accelerated && it > 0) ? (betas_in_smem ? s_beta[it - 1] : a.betas[it - 1]) : 0.f;
     const int par = (it - 1) & 1;
     float yy[CRPT], yx[CRPT];
 #pragma unroll
@@ -180,14 +202,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     cluster_wait();
     float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
     if (rg_top && has_up) {
-      const float v = cluster.map_shared_rank(&pub_bot[par][0], cr - 1)[j];
+      const float v = dsmem_ld(nb_bot + 4u * (par * CW + j));
       up_m = it == 0 ? v : up_k;
       up_k = v;
       y_up = up_k + beta * (up_k - up_m);
     }
     if (rg_bot && has_dn) {
-      const float* rt = cluster.map_shared_rank(&pub_top[par][0][0], cr + 1);
-      const float vy = rt[j], vx = rt[CW + j];
+      const uint32_t rt = nb_top + 4u * (par * 2 * CW + j);
+      const float vy = dsmem_ld(rt), vx = dsmem_ld(rt + 4u * CW);
       dn_my = it == 0 ? vy : dn_ky;
       dn_mx = it == 0 ? vx : dn_kx;
       dn_ky = vy;
@@ -197,17 +219,23 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     }
     s_rg_yy[rg][j] = yy[CRPT - 1];
     if (lane == 31) {
-#pragma unroll
-      for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = yx[t];
+      *reinterpret_cast<float4*>(&s_edge_yx[rg][wc][0]) = make_float4(yx[0], yx[1], yx[2], yx[3]);
       s_edge_yx[rg][wc][CRPT] = ex_x;
     }
     __syncthreads();
+    float4 ledge = make_float4(0.f, 0.f, 0.f, 0.f);
+    float ledge_x = 0.f;
+    if (left_fetch) {
+      ledge = *reinterpret_cast<const float4*>(&s_edge_yx[rg][wc - 1][0]);
+      ledge_x = s_edge_yx[rg][wc - 1][CRPT];
+    }
+    const float le[CRPT] = {ledge.x, ledge.y, ledge.z, ledge.w};
     const float yy_above = rg_top ? y_up : s_rg_yy[rg - 1][j];
     float u[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float left = __shfl_up_sync(0xffffffffu, yx[t], 1);
-      if (lane == 0) left = left_fetch ? s_edge_yx[rg][wc - 1][t] : 0.f;
+      if (lane == 0) left = le[t];
       // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded
       const float d = ((yy[t] - (t > 0 ? yy[t - 1] : yy_above)) + yx[t]) - left;
       const float v = z[t] + d;
@@ -216,23 +244,29 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     float u_ex;
     {
       float left = __shfl_up_sync(0xffffffffu, ex_x, 1);
-      if (lane == 0) left = left_fetch ? s_edge_yx[rg][wc - 1][CRPT] : 0.f;
+      if (lane == 0) left = ledge_x;
       const float d = ((ex_y - yy[CRPT - 1]) + ex_x) - left;
       const float v = z_ex + d;
       u_ex = nonneg ? fmaxf(v, 0.f) : v;
     }
     s_rg_u[rg][j] = u[0];
-    if (lane == 0) {
-#pragma unroll
-      for (int t = 0; t < CRPT; ++t) s_edge_u[rg][wc][t] = u[t];
-    }
+    if (lane == 0)
+      *reinterpret_cast<float4*>(&s_edge_u[rg][wc][0]) = make_float4(u[0], u[1], u[2], u[3]);
     __syncthreads();
+    float re[CRPT] = {u[0], u[1], u[2], u[3]};  // global column W-1: right := u (gx = 0)
+    if (right_fetch) {
+      const float4 r4 = *reinterpret_cast<const float4*>(&s_edge_u[rg][wc + 1][0]);
+      re[0] = r4.x;
+      re[1] = r4.y;
+      re[2] = r4.z;
+      re[3] = r4.w;
+    }
     // the global last row has no row below: gy = 0 (below := u)
     const float u_below = !rg_bot ? s_rg_u[rg + 1][j] : (last_row_thread ? u[CRPT - 1] : u_ex);
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       float right = __shfl_down_sync(0xffffffffu, u[t], 1);
-      if (lane == 31) right = right_fetch ? s_edge_u[rg][wc + 1][t] : u[t];  // W-1: gx = 0
+      if (lane == 31) right = re[t];
       const float below = t < CRPT - 1 ? u[t + 1] : u_below;
       const float ay = yy[t] + a.step * (below - u[t]);
       const float ax = yx[t] + a.step * (right - u[t]);
@@ -269,11 +303,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   cluster_wait();
   float yy_above = 0.f;
   if (rg_top && has_up)
-    yy_above = cluster.map_shared_rank(&pub_bot[(a.n_inner - 1) & 1][0], cr - 1)[j];
+    yy_above = dsmem_ld(nb_bot + 4u * (((a.n_inner - 1) & 1) * CW + j));
   s_rg_yy[rg][j] = qky[CRPT - 1];
   if (lane == 31) {
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = qkx[t];
+    for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = qkx[t];  // epilogue: once
   }
   __syncthreads();
   if (!rg_top) yy_above = s_rg_yy[rg - 1][j];
@@ -355,27 +389,19 @@ int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (dto == PSB_F32) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float>,
-                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr_set = true;
-    }
+    auto kern = nonneg ? fgp_cluster_kernel<float, true> : fgp_cluster_kernel<float, false>;
+    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     ClusterArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, active, pend,
                          kfirst, rep, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
                          (float)hc, (float)pg, (float)step, bad, k, betas};
-    PSB_CUDA(cudaLaunchKernelEx(&cfg, fgp_cluster_kernel<float>, a));
+    PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   } else if (dto == PSB_F64) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<double>,
-                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr_set = true;
-    }
+    auto kern = nonneg ? fgp_cluster_kernel<double, true> : fgp_cluster_kernel<double, false>;
+    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     ClusterArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, active, pend,
                           kfirst, rep, n_inner, accelerated, nonneg, (float)weight, gamma, hc, pg,
                           (float)step, bad, k, betas};
-    PSB_CUDA(cudaLaunchKernelEx(&cfg, fgp_cluster_kernel<double>, a));
+    PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   } else {
     return fail(PSB_ERR_VALUE, "cluster prox: unknown dtype");
   }
@@ -411,9 +437,9 @@ int cluster_max_active(int* out) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float>,
+  PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float, false>,
                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  PSB_CUDA(cudaOccupancyMaxActiveClusters(out, fgp_cluster_kernel<float>, &cfg));
+  PSB_CUDA(cudaOccupancyMaxActiveClusters(out, fgp_cluster_kernel<float, false>, &cfg));
   return PSB_OK;
 }
 
