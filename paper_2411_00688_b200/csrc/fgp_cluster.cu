@@ -62,6 +62,7 @@ struct ClusterArgs {
   int32_t* bad;
   int k;               // this outer iteration (for DivergenceError)
   const float* betas;  // device table beta[0..n_inner-1]
+  int n_active;        // entries in `active`
 };
 
 template <class TO>
@@ -84,6 +85,15 @@ __device__ __forceinline__ float dsmem_ld(uint32_t addr) {
   return v;
 }
 
+template <int B>
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = pred ? B : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(B), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit_c() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -105,8 +115,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   using F = Ar<float>;
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
-  const int entry = blockIdx.x / CCL;
-  const int p = a.active ? a.active[entry] : entry;
   const int tid = threadIdx.x;
   const int j = tid % CW, rg = tid / CW;
   const int lane = tid & 31, wc = j >> 5;
@@ -123,6 +131,46 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   __shared__ __align__(16) float s_edge_u[CRG][CWARPS_ROW][CRPT];
   __shared__ float s_beta[kMaxBetas];
 
+  const TO g = a.gamma;
+  const float w = a.weight;
+  constexpr bool nonneg = NONNEG;
+  // momentum table in shared memory (uniform per iteration)
+  for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
+
+  // Persistent clusters: cluster c handles entries c, c + G, ...; the next
+  // entry's x, b, h, q_warm rows of this CTA are prefetched with cp.async into
+  // shared memory while the current entry iterates (each thread stages exactly
+  // the elements it later reads, so no barrier is needed for the stage).
+  extern __shared__ __align__(16) unsigned char stage_raw[];
+  constexpr int SR = CRG * CRPT + 1;  // staged rows: this CTA's 16 + the next CTA's first
+  TO* sxbh = reinterpret_cast<TO*>(stage_raw);                       // [3][SR][CW]
+  float* sq = reinterpret_cast<float*>(stage_raw + sizeof(TO) * 3 * SR * CW);  // [2][SR-1][CW]
+  const int G = gridDim.x / CCL;
+  auto issue_stage = [&](int e) {
+    const int pe = a.active ? a.active[e] : e;
+    const TO* src[3] = {a.x + (int64_t)pe * HW, a.b + (int64_t)pe * HW, a.h + (int64_t)pe * HW};
+    const float* qs = a.q + (int64_t)pe * a.qps;
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      const int lr = rg * CRPT + t;
+      const int64_t o = (int64_t)(row0 + t) * CW + j;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cp_async_el<sizeof(TO)>(sxbh + (c * SR + lr) * CW + j, src[c] + o, true);
+      cp_async_el<4>(sq + lr * CW + j, qs + o, true);
+      cp_async_el<4>(sq + ((SR - 1) + lr) * CW + j, qs + HW + o, true);
+    }
+    if (rg_bot) {
+      const int64_t o = (int64_t)(row0 + CRPT) * CW + j;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        cp_async_el<sizeof(TO)>(sxbh + (c * SR + SR - 1) * CW + j, has_dn ? src[c] + o : src[c], has_dn);
+    }
+    cp_async_commit_c();
+  };
+  if ((int)(blockIdx.x / CCL) < a.n_active) issue_stage(blockIdx.x / CCL);
+
+  for (int entry = blockIdx.x / CCL; entry < a.n_active; entry += G) {
+  const int p = a.active ? a.active[entry] : entry;
   TO* xp = a.x + (int64_t)p * HW;
   const TO* bp = a.b + (int64_t)p * HW;
   TO* hp = a.h + (int64_t)p * HW;
@@ -130,17 +178,12 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const int m = a.pend ? a.pend[entry] : 0;
   const int kf = a.kfirst ? a.kfirst[entry] : 0;
   const bool rp = a.rep ? a.rep[entry] != 0 : false;
-  const TO g = a.gamma;
-  const float w = a.weight;
-  constexpr bool nonneg = NONNEG;
-  // momentum table in shared memory (uniform per iteration)
-  for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
-
+  cp_async_wait_all();
   float z[CRPT], qky[CRPT], qkx[CRPT], qmy[CRPT], qmx[CRPT];
   int kbad = 0x7fffffff;
-  auto prox_input = [&](int64_t o, bool track) {
-    TO xo = xp[o];
-    const TO bo = bp[o], ho = hp[o];
+  auto prox_input = [&](int lr, bool track) {
+    TO xo = sxbh[(0 * SR + lr) * CW + j];
+    const TO bo = sxbh[(1 * SR + lr) * CW + j], ho = sxbh[(2 * SR + lr) * CW + j];
     for (int s = 0; s < m; ++s) {
       xo = skip_update(xo, bo, ho, g);
       if (track && !finite(xo)) kbad = min(kbad, kf + s);
@@ -150,9 +193,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   // ---- prologue: deferred skips, prox input, warm start --------------------
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
-    const int64_t o = (int64_t)(row0 + t) * CW + j;
-    z[t] = prox_input(o, true);
-    float vy = q0[o], vx = q0[HW + o];
+    const int lr = rg * CRPT + t;
+    z[t] = prox_input(lr, true);
+    float vy = sq[lr * CW + j], vx = sq[((SR - 1) + lr) * CW + j];
     if (rp) {
       const float sc = F::ball_scale(vy, vx, w);
       vy *= sc;
@@ -169,7 +212,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   }
   // the bottom row group also owns the CTA-below's first row for u
   float z_ex = 0.f;
-  if (rg_bot && has_dn) z_ex = prox_input((int64_t)(row0 + CRPT) * CW + j, false);
+  if (rg_bot && has_dn) z_ex = prox_input(SR - 1, false);
+  // the stage is consumed: prefetch the next entry of this cluster
+  if (entry + G < a.n_active) issue_stage(entry + G);
   if (rg_top) {
     pub_top[1][0][j] = qky[0];
     pub_top[1][1][j] = qkx[0];
@@ -338,8 +383,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   }
   if (!ok) kbad = min(kbad, a.k);
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
-  cluster_arrive();  // keep shared memory alive until every neighbour has read it
+  kbad = 0x7fffffff;
+  cluster_arrive();  // neighbours' DSMEM reads of this entry are done before reuse / exit
   cluster_wait();
+  }  // entries
 }
 
 // Apply each problem's remaining deferred skips (end of a run).
@@ -370,16 +417,30 @@ __global__ void skip_flush_kernel(TO* __restrict__ x, const TO* __restrict__ b,
 
 bool cluster_shape_ok(int H, int W) { return H == CH && W == CW; }
 
+size_t stage_bytes(int dto) {
+  const size_t SR = CRG * CRPT + 1;
+  const size_t eb = dto == PSB_F64 ? 8 : 4;
+  return eb * 3 * SR * CW + 4 * 2 * (SR - 1) * CW;
+}
+
+int cluster_max_active(int* out);
+
 int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
                       const int32_t* active, int n_active, const int32_t* pend,
                       const int32_t* kfirst, const uint8_t* rep, int n_inner, int accelerated,
                       int nonneg, double weight, double gamma, double hc, double pg, double step,
                       const float* betas, int32_t* bad, int k, cudaStream_t st) {
   if (n_active == 0) return PSB_OK;
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    int mc = 0;
+    if (cluster_max_active(&mc) != PSB_OK || mc <= 0) mc = 1;
+    max_clusters = mc;
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)n_active * CCL);
+  cfg.gridDim = dim3((unsigned)std::min(n_active, max_clusters) * CCL);
   cfg.blockDim = dim3(CTHREADS);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = stage_bytes(dto);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -391,16 +452,18 @@ int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t
   if (dto == PSB_F32) {
     auto kern = nonneg ? fgp_cluster_kernel<float, true> : fgp_cluster_kernel<float, false>;
     PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
     ClusterArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, active, pend,
                          kfirst, rep, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
-                         (float)hc, (float)pg, (float)step, bad, k, betas};
+                         (float)hc, (float)pg, (float)step, bad, k, betas, n_active};
     PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   } else if (dto == PSB_F64) {
     auto kern = nonneg ? fgp_cluster_kernel<double, true> : fgp_cluster_kernel<double, false>;
     PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
     ClusterArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, active, pend,
                           kfirst, rep, n_inner, accelerated, nonneg, (float)weight, gamma, hc, pg,
-                          (float)step, bad, k, betas};
+                          (float)step, bad, k, betas, n_active};
     PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   } else {
     return fail(PSB_ERR_VALUE, "cluster prox: unknown dtype");
@@ -437,8 +500,12 @@ int cluster_max_active(int* out) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  cfg.dynamicSmemBytes = stage_bytes(PSB_F64);
   PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float, false>,
                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)cfg.dynamicSmemBytes));
   PSB_CUDA(cudaOccupancyMaxActiveClusters(out, fgp_cluster_kernel<float, false>, &cfg));
   return PSB_OK;
 }
