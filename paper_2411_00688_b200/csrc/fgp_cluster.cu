@@ -143,8 +143,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   // the elements it later reads, so no barrier is needed for the stage).
   extern __shared__ __align__(16) unsigned char stage_raw[];
   constexpr int SR = CRG * CRPT + 1;  // staged rows: this CTA's 16 + the next CTA's first
+  // fp32 outer state: two stages (the epilogue re-reads x, b, h from the
+  // stage); fp64: one stage (the epilogue re-reads them from global / L2)
+  constexpr int NST = sizeof(TO) == 4 ? 2 : 1;
+  constexpr size_t STB = sizeof(TO) * 3 * SR * CW + 4 * 2 * (SR - 1) * CW;
   TO* sxbh = reinterpret_cast<TO*>(stage_raw);                       // [3][SR][CW]
   float* sq = reinterpret_cast<float*>(stage_raw + sizeof(TO) * 3 * SR * CW);  // [2][SR-1][CW]
+  auto set_stage = [&](int sidx) {
+    sxbh = reinterpret_cast<TO*>(stage_raw + sidx * STB);
+    sq = reinterpret_cast<float*>(stage_raw + sidx * STB + sizeof(TO) * 3 * SR * CW);
+  };
   const int G = gridDim.x / CCL;
   auto issue_stage = [&](int e) {
     const int pe = a.active ? a.active[e] : e;
@@ -169,7 +177,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   };
   if ((int)(blockIdx.x / CCL) < a.n_active) issue_stage(blockIdx.x / CCL);
 
-  for (int entry = blockIdx.x / CCL; entry < a.n_active; entry += G) {
+  int li = 0;  // local entry counter (stage parity)
+  for (int entry = blockIdx.x / CCL; entry < a.n_active; entry += G, ++li) {
+  set_stage(li % NST);
   const int p = a.active ? a.active[entry] : entry;
   TO* xp = a.x + (int64_t)p * HW;
   const TO* bp = a.b + (int64_t)p * HW;
@@ -214,7 +224,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   float z_ex = 0.f;
   if (rg_bot && has_dn) z_ex = prox_input(SR - 1, false);
   // the stage is consumed: prefetch the next entry of this cluster
-  if (entry + G < a.n_active) issue_stage(entry + G);
+  if (entry + G < a.n_active) {
+    set_stage((li + 1) % NST);
+    issue_stage(entry + G);
+    set_stage(li % NST);
+  }
   if (rg_top) {
     pub_top[1][0][j] = qky[0];
     pub_top[1][1][j] = qkx[0];
@@ -370,8 +384,17 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     float uf = z[t] + d;
     if (nonneg) uf = fmaxf(uf, 0.f);
     const int64_t o = (int64_t)r * CW + j;
-    TO xo = xp[o];
-    const TO bo = bp[o], ho = hp[o];
+    const int lr = rg * CRPT + t;
+    TO xo, bo, ho;
+    if constexpr (NST == 2) {
+      xo = sxbh[(0 * SR + lr) * CW + j];
+      bo = sxbh[(1 * SR + lr) * CW + j];
+      ho = sxbh[(2 * SR + lr) * CW + j];
+    } else {
+      xo = xp[o];
+      bo = bp[o];
+      ho = hp[o];
+    }
     for (int s = 0; s < m; ++s) xo = skip_update(xo, bo, ho, g);
     const TO xhat = skip_update(xo, bo, ho, g);
     const TO xn = (TO)uf;
@@ -420,7 +443,8 @@ bool cluster_shape_ok(int H, int W) { return H == CH && W == CW; }
 size_t stage_bytes(int dto) {
   const size_t SR = CRG * CRPT + 1;
   const size_t eb = dto == PSB_F64 ? 8 : 4;
-  return eb * 3 * SR * CW + 4 * 2 * (SR - 1) * CW;
+  const size_t nst = dto == PSB_F64 ? 1 : 2;
+  return nst * (eb * 3 * SR * CW + 4 * 2 * (SR - 1) * CW);
 }
 
 int cluster_max_active(int* out);
