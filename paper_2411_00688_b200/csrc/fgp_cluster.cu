@@ -94,6 +94,42 @@ __device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool pre
 __device__ __forceinline__ void cp_async_commit_c() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// ---- point-to-point halo rows: st.async into the neighbour's shared memory,
+// completion counted in bytes on the neighbour's mbarrier (no cluster-wide
+// barrier, no memory fence on the critical path) -----------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(raddr),
+               "r"(__float_as_uint(v)), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, float v0, float v1, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(rmbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -123,8 +159,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool has_up = cr > 0, has_dn = cr < CCL - 1;
   constexpr int64_t HW = (int64_t)CH * CW;
 
-  __shared__ float pub_top[2][2][CW];  // [parity][channel][col]: first row of q
-  __shared__ float pub_bot[2][CW];     // [parity][col]: last row of q, row channel
+  // halo rows received from the neighbours, double-buffered by round parity
+  __shared__ __align__(8) float rx_dn[2][CW][2];  // CTA below's first row of q (y, x)
+  __shared__ float rx_up[2][CW];                  // CTA above's last row of q (y)
+  __shared__ __align__(8) uint64_t mb_dn[2], mb_up[2];
   __shared__ float s_rg_yy[CRG][CW];   // each row group's last-row y_y (for the group below)
   __shared__ float s_rg_u[CRG][CW];    // each row group's first-row u (for the group above)
   __shared__ __align__(16) float s_edge_yx[CRG][CWARPS_ROW][CRPT + 4];  // float4 + extra row
@@ -136,6 +174,43 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   constexpr bool nonneg = NONNEG;
   // momentum table in shared memory (uniform per iteration)
   for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
+  if (tid == 0) {
+    mbar_init(&mb_dn[0], 1);
+    mbar_init(&mb_dn[1], 1);
+    mbar_init(&mb_up[0], 1);
+    mbar_init(&mb_up[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  cluster_arrive();  // every CTA's mbarriers exist before anyone pushes
+  cluster_wait();
+  // Round r carries the rows published after iteration r-1 (round 0: the warm
+  // start) and lands in buffer r&1; the counter runs across entries.
+  constexpr unsigned BYTES_DN = CW * 2 * 4, BYTES_UP = CW * 4;
+  const uint32_t up_rx_remote = dsmem_addr(&rx_dn[0][0][0], cr > 0 ? cr - 1 : cr);   // my top row -> CTA above
+  const uint32_t up_mb_remote = dsmem_addr(&mb_dn[0], cr > 0 ? cr - 1 : cr);
+  const uint32_t dn_rx_remote = dsmem_addr(&rx_up[0][0], cr < CCL - 1 ? cr + 1 : cr); // my bottom row -> CTA below
+  const uint32_t dn_mb_remote = dsmem_addr(&mb_up[0], cr < CCL - 1 ? cr + 1 : cr);
+  unsigned round = 0;
+  auto push_rows = [&](float top_y, float top_x, float bot_y) {
+    const unsigned b = round & 1;
+    if (rg_top && cr > 0)
+      st_async_v2(up_rx_remote + 4u * (b * CW * 2 + j * 2), top_y, top_x, up_mb_remote + 8u * b);
+    if (rg_bot && cr < CCL - 1)
+      st_async_f32(dn_rx_remote + 4u * (b * CW + j), bot_y, dn_mb_remote + 8u * b);
+  };
+  // wait for round `r` (consumer side); returns the buffer index
+  auto recv_rows = [&](unsigned r) {
+    const unsigned b = r & 1, ph = (r >> 1) & 1;
+    if (cr < CCL - 1) {
+      if (tid == CTHREADS - 1) mbar_expect_tx(&mb_dn[b], BYTES_DN);
+      if (rg_bot) mbar_wait(&mb_dn[b], ph);
+    }
+    if (cr > 0) {
+      if (tid == 0) mbar_expect_tx(&mb_up[b], BYTES_UP);
+      if (rg_top) mbar_wait(&mb_up[b], ph);
+    }
+    return b;
+  };
 
   // Persistent clusters: cluster c handles entries c, c + G, ...; the next
   // entry's x, b, h, q_warm rows of this CTA are prefetched with cp.async into
@@ -229,12 +304,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     issue_stage(entry + G);
     set_stage(li % NST);
   }
-  if (rg_top) {
-    pub_top[1][0][j] = qky[0];
-    pub_top[1][1][j] = qkx[0];
-  }
-  if (rg_bot) pub_bot[1][j] = qky[CRPT - 1];
-  cluster_arrive();
+  const unsigned round0 = round;  // this entry's warm-start round
+  push_rows(qky[0], qkx[0], qky[CRPT - 1]);
+  ++round;
 
   float up_k = 0.f, up_m = 0.f;                          // row above, row channel
   float dn_ky = 0.f, dn_kx = 0.f, dn_my = 0.f, dn_mx = 0.f;  // row below, both channels
@@ -242,33 +314,28 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool right_edge = lane == 31 && wc == CWARPS_ROW - 1;  // global column W-1
   const bool left_fetch = lane == 0 && wc > 0;
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
-  // neighbours' publish buffers as 32-bit shared::cluster addresses, resolved once
-  const uint32_t nb_bot = dsmem_addr(&pub_bot[0][0], has_up ? cr - 1 : cr);
-  const uint32_t nb_top = dsmem_addr(&pub_top[0][0][0], has_dn ? cr + 1 : cr);
   const bool betas_in_smem = a.n_inner <= kMaxBetas;
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
                    int it) {
     const float beta = (a.accelerated && it > 0) ? (betas_in_smem ? s_beta[it - 1] : a.betas[it - 1]) : 0.f;
-    const int par = (it - 1) & 1;
     float yy[CRPT], yx[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
       yy[t] = QKy[t] + beta * (QKy[t] - QMy[t]);
       yx[t] = QKx[t] + beta * (QKx[t] - QMx[t]);
     }
-    cluster_wait();
+    const unsigned par = recv_rows(round0 + it);
     float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
     if (rg_top && has_up) {
-      const float v = dsmem_ld(nb_bot + 4u * (par * CW + j));
+      const float v = rx_up[par][j];
       up_m = it == 0 ? v : up_k;
       up_k = v;
       y_up = up_k + beta * (up_k - up_m);
     }
     if (rg_bot && has_dn) {
-      const uint32_t rt = nb_top + 4u * (par * 2 * CW + j);
-      const float vy = dsmem_ld(rt), vx = dsmem_ld(rt + 4u * CW);
+      const float vy = rx_dn[par][j][0], vx = rx_dn[par][j][1];
       dn_my = it == 0 ? vy : dn_ky;
       dn_mx = it == 0 ? vx : dn_kx;
       dn_ky = vy;
@@ -335,13 +402,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       QMx[t] = ax * sc;
     }
     (void)right_edge;
-    const int pw = it & 1;
-    if (rg_top) {
-      pub_top[pw][0][j] = QMy[0];
-      pub_top[pw][1][j] = QMx[0];
-    }
-    if (rg_bot) pub_bot[pw][j] = QMy[CRPT - 1];
-    cluster_arrive();
+    push_rows(QMy[0], QMx[0], QMy[CRPT - 1]);
+    ++round;
   };
 
   int it = 0;
@@ -359,10 +421,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   }
 
   // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
-  cluster_wait();
+  const unsigned pe = recv_rows(round0 + a.n_inner);
   float yy_above = 0.f;
-  if (rg_top && has_up)
-    yy_above = dsmem_ld(nb_bot + 4u * (((a.n_inner - 1) & 1) * CW + j));
+  if (rg_top && has_up) yy_above = rx_up[pe][j];
   s_rg_yy[rg][j] = qky[CRPT - 1];
   if (lane == 31) {
 #pragma unroll
@@ -407,9 +468,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   if (!ok) kbad = min(kbad, a.k);
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
   kbad = 0x7fffffff;
-  cluster_arrive();  // neighbours' DSMEM reads of this entry are done before reuse / exit
-  cluster_wait();
   }  // entries
+  cluster_arrive();  // no CTA leaves while a neighbour may still push into it
+  cluster_wait();
 }
 
 // Apply each problem's remaining deferred skips (end of a run).
