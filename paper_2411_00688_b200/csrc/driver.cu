@@ -115,7 +115,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   // and executed in registers at the next prox call / the final flush.
   const char* no_cluster = std::getenv("PSB_NO_CLUSTER");
   const bool use_cluster = fid.kind == 0 && dtf == PSB_F32 && cluster_shape_ok(H, W) &&
-                           !(no_cluster && no_cluster[0] == '1');
+                           n_inner <= 1024 && !(no_cluster && no_cluster[0] == '1');
   std::vector<int32_t> pend, kfirst, fl_pend(n, 0), fl_kfirst(n, 0);
   std::vector<float> beta_f(n_inner, 0.f);
   if (use_cluster) {

@@ -130,6 +130,15 @@ __device__ __forceinline__ void st_async_v2(uint32_t raddr, float v0, float v1, 
                : "memory");
 }
 
+// MUFU.RSQ without the denormal rescaling rsqrtf() wraps around it (|a|^2 of a
+// dual vector is never denormal in a way that matters: the ball test is
+// min(1, w / |a|)); 1 instruction instead of ~6 per pixel.
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -199,15 +208,19 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       st_async_f32(dn_rx_remote + 4u * (b * CW + j), bot_y, dn_mb_remote + 8u * b);
   };
   // wait for round `r` (consumer side); returns the buffer index
+  // warp-uniform roles: the bottom row group waits for the CTA below, the top
+  // one for the CTA above; lane 0 of the role's first warp arms the barrier
+  const bool wait_dn = rg_bot && cr < CCL - 1, wait_up = rg_top && cr > 0;
+  const bool arm = lane == 0 && wc == 0;
   auto recv_rows = [&](unsigned r) {
     const unsigned b = r & 1, ph = (r >> 1) & 1;
-    if (cr < CCL - 1) {
-      if (tid == CTHREADS - 1) mbar_expect_tx(&mb_dn[b], BYTES_DN);
-      if (rg_bot) mbar_wait(&mb_dn[b], ph);
+    if (wait_dn) {
+      if (arm) mbar_expect_tx(&mb_dn[b], BYTES_DN);
+      mbar_wait(&mb_dn[b], ph);
     }
-    if (cr > 0) {
-      if (tid == 0) mbar_expect_tx(&mb_up[b], BYTES_UP);
-      if (rg_top) mbar_wait(&mb_up[b], ph);
+    if (wait_up) {
+      if (arm) mbar_expect_tx(&mb_up[b], BYTES_UP);
+      mbar_wait(&mb_up[b], ph);
     }
     return b;
   };
@@ -314,12 +327,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool right_edge = lane == 31 && wc == CWARPS_ROW - 1;  // global column W-1
   const bool left_fetch = lane == 0 && wc > 0;
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
-  const bool betas_in_smem = a.n_inner <= kMaxBetas;
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
                    int it) {
-    const float beta = (a.accelerated && it > 0) ? (betas_in_smem ? s_beta[it - 1] : a.betas[it - 1]) : 0.f;
+    const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
     float yy[CRPT], yx[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       const float ay = yy[t] + a.step * (below - u[t]);
       const float ax = yx[t] + a.step * (right - u[t]);
       const float m2 = fmaf(ay, ay, ax * ax);
-      const float sc = fminf(1.f, w * rsqrtf(m2));  // w / max(w, |a|)
+      const float sc = fminf(1.f, w * rsqrt_approx(m2));  // w / max(w, |a|)
       QMy[t] = ay * sc;
       QMx[t] = ax * sc;
     }
