@@ -70,14 +70,17 @@ template <> struct Ar<float> {
   static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
   static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
-  // Same projection with one MUFU: scale = 1 inside the ball, r/|q| outside.
+  // Same projection with one MUFU (no denormal rescaling): min(1, r/|q|).
+  static __device__ __forceinline__ float rsq(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
   static __device__ __forceinline__ float ball_scale(float a, float b, float r) {
-    float m2 = fmaf(a, a, b * b);
-    return m2 > r * r ? r * rsqrtf(m2) : 1.0f;
+    return fminf(1.0f, r * rsq(fmaf(a, a, b * b)));
   }
   static __device__ __forceinline__ float ball_scale3(float a, float b, float c, float r) {
-    float m2 = fmaf(a, a, fmaf(b, b, c * c));
-    return m2 > r * r ? r * rsqrtf(m2) : 1.0f;
+    return fminf(1.0f, r * rsq(fmaf(a, a, fmaf(b, b, c * c))));
   }
 };
 
