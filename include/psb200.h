@@ -180,10 +180,7 @@ int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void
  * radon_system_matrix (operators.py:224-229): `tables` is a DEVICE double
  * array [offsets (n_bins) | steps (n_steps) | cos(angles) | sin(angles)]
  * computed on the host with numpy exactly as the reference does, so sample
- * positions are bit-identical.  step_spacing = 2*half_span/(n_steps-1).
- * `prod` is a DEVICE double array of the reference-rounded products
- * [off*cos (n_angles x n_bins) | off*sin | step*(-sin) (n_angles x n_steps) |
- * step*cos], so a sample position costs two additions on the device. */
+ * positions are bit-identical.  step_spacing = 2*half_span/(n_steps-1). */
 typedef struct psb_radon_geom {
   int n;
   int n_angles;
@@ -194,7 +191,6 @@ typedef struct psb_radon_geom {
   double step_spacing;
   double bin_spacing;
   const double* tables;
-  const double* prod;
 } psb_radon_geom;
 
 /* psb_radon_fwd: sino = A img (CSR SpMV of operators.py:273-277, ray-driven)

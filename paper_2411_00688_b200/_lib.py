@@ -30,7 +30,7 @@ class RadonGeom(C.Structure):
     _fields_ = [("n", C.c_int), ("n_angles", C.c_int), ("n_bins", C.c_int),
                 ("n_steps", C.c_int), ("center", C.c_double), ("half_span", C.c_double),
                 ("step_spacing", C.c_double), ("bin_spacing", C.c_double),
-                ("tables", C.c_void_p), ("prod", C.c_void_p)]
+                ("tables", C.c_void_p)]
 
 
 _geo = C.POINTER(RadonGeom)

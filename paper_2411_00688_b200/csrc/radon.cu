@@ -33,12 +33,6 @@ struct Geo {
   const double* stp;  // [ns]
   const double* cs;   // [na]
   const double* sn;   // [na]
-  // reference-rounded products (host numpy): off*cos, off*sin  [na][nb];
-  // step*(-sin), step*cos  [na][ns]
-  const double* ax;
-  const double* ay;
-  const double* bx;
-  const double* by;
 };
 
 Geo make_geo(const psb_radon_geom* g) {
@@ -55,22 +49,16 @@ Geo make_geo(const psb_radon_geom* g) {
   o.stp = g->tables + o.nb;
   o.cs = g->tables + o.nb + o.ns;
   o.sn = g->tables + o.nb + o.ns + o.na;
-  o.ax = g->prod;
-  o.ay = g->prod + (size_t)o.na * o.nb;
-  o.bx = g->prod + (size_t)2 * o.na * o.nb;
-  o.by = g->prod + (size_t)2 * o.na * o.nb + (size_t)o.na * o.ns;
   return o;
 }
 
 // Sample position (operators.py:233-236) with the reference's rounding:
-// px = (off*nx + step*dx) + center, py = (off*ny + step*dy) + center, the two
-// products read from host-computed tables (identical rounding), so only the
-// two additions are done here.
-__device__ __forceinline__ void sample_pos(const Geo& G, double pax, double pay, int ia, int is,
+// px = (off*nx + step*dx) + center, py = (off*ny + step*dy) + center.
+__device__ __forceinline__ void sample_pos(const Geo& G, double c, double s, int ib, int is,
                                            double& px, double& py) {
-  const size_t o = (size_t)ia * G.ns + is;
-  px = __dadd_rn(__dadd_rn(pax, G.bx[o]), G.center);
-  py = __dadd_rn(__dadd_rn(pay, G.by[o]), G.center);
+  const double o = G.off[ib], st = G.stp[is];
+  px = __dadd_rn(__dadd_rn(__dmul_rn(o, c), __dmul_rn(st, -s)), G.center);
+  py = __dadd_rn(__dadd_rn(__dmul_rn(o, s), __dmul_rn(st, c)), G.center);
 }
 
 // Forward projection of one ray; the result is valid in lane 0 and is a
@@ -78,12 +66,12 @@ __device__ __forceinline__ void sample_pos(const Geo& G, double pax, double pay,
 template <class T>
 __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int ia, int ib,
                                      int lane) {
+  const double c = G.cs[ia], s = G.sn[ia];
   const int n = G.n;
-  const double pax = G.ax[(size_t)ia * G.nb + ib], pay = G.ay[(size_t)ia * G.nb + ib];
   T acc = T(0);
   for (int is = lane; is < G.ns; is += 32) {
     double px, py;
-    sample_pos(G, pax, pay, ia, is, px, py);
+    sample_pos(G, c, s, ib, is, px, py);
     const double fx0 = floor(px), fy0 = floor(py);
     const int x0 = (int)fx0, y0 = (int)fy0;
     if (x0 < -1 || x0 >= n || y0 < -1 || y0 >= n) continue;
@@ -119,10 +107,9 @@ __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y,
     const int s_lo = max(0, (int)ceil(os - rs)), s_hi = min(G.ns - 1, (int)floor(os + rs));
     const T* yrow = y + (int64_t)ia * G.nb;
     for (int ib = b_lo; ib <= b_hi; ++ib) {
-      const double pax = G.ax[(size_t)ia * G.nb + ib], pay = G.ay[(size_t)ia * G.nb + ib];
       for (int is = s_lo; is <= s_hi; ++is) {
         double px, py;
-        sample_pos(G, pax, pay, ia, is, px, py);
+        sample_pos(G, c, s, ib, is, px, py);
         const double fx0 = floor(px), fy0 = floor(py);
         const int dx = cc - (int)fx0, dy = r - (int)fy0;
         if ((unsigned)dx > 1u || (unsigned)dy > 1u) continue;
@@ -232,8 +219,7 @@ __global__ void pdhg_dual_tv_kernel(int n, const T* __restrict__ xbar, T* __rest
 }
 
 inline int check_geo(const psb_radon_geom* g) {
-  PSB_REQUIRE(g != nullptr && g->tables != nullptr && g->prod != nullptr,
-              "radon: missing geometry tables");
+  PSB_REQUIRE(g != nullptr && g->tables != nullptr, "radon: missing geometry tables");
   PSB_REQUIRE(g->n >= 2 && g->n_angles >= 1 && g->n_bins >= g->n && g->n_steps >= 2,
               "RadonGeometry: need image_side >= 2, n_angles >= 1, n_bins >= image_side");
   PSB_REQUIRE(g->bin_spacing > 0 && g->step_spacing > 0, "radon: spacings must be positive");

@@ -225,18 +225,11 @@ class RadonGeometry:
             cs = np.array([np.cos(t) for t in self.angles])
             sn = np.array([np.sin(t) for t in self.angles])
             tab = np.concatenate([offsets, steps, cs, sn])
-            # the four products of operators.py:233-236, rounded by numpy exactly
-            # as the reference's broadcast expressions round them
-            prod = np.concatenate([(offsets[None, :] * cs[:, None]).ravel(),
-                                   (offsets[None, :] * sn[:, None]).ravel(),
-                                   (steps[None, :] * (-sn)[:, None]).ravel(),
-                                   (steps[None, :] * cs[:, None]).ravel()])
             tdev = AR.to_dev(tab, torch.float64)
-            pdev = AR.to_dev(prod, torch.float64)
             g = L.RadonGeom(n, len(self.angles), self.n_bins, n_steps, center, half_span,
                             2.0 * half_span / (n_steps - 1), float(self.bin_spacing),
-                            tdev.data_ptr(), pdev.data_ptr())
-            self._dev = (g, (tdev, pdev))
+                            tdev.data_ptr())
+            self._dev = (g, tdev)
         return self._dev
 
     @property
