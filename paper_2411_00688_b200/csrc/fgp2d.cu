@@ -11,6 +11,9 @@
 // re-read (L2 hits).
 #include <cooperative_groups.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -487,6 +490,24 @@ void fista_betas(int n, double* out) {
   }
 }
 
+const double* device_betas(int n) {
+  static std::mutex mu;
+  static std::map<int, double*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(n);
+  if (it != cache.end()) return it->second;
+  std::vector<double> b(n);
+  fista_betas(n, b.data());
+  double* d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double) * n) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  cudaMemcpy(d, b.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
+  cache[n] = d;
+  return d;
+}
+
 int tv_prox2d(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step, void* u,
@@ -495,16 +516,11 @@ int tv_prox2d(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const
   PSB_REQUIRE(wts != nullptr || weight > 0, "tv_prox: weight must be positive");
   std::vector<double> beta(n_inner, 0.0);
   if (accelerated) fista_betas(n_inner, beta.data());
-  // device copy of the momentum table for the cooperative path (stream-ordered)
-  double* bdev = nullptr;
-  if (accelerated) {
-    PSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bdev), sizeof(double) * n_inner, st));
-    PSB_CUDA(cudaMemcpyAsync(bdev, beta.data(), sizeof(double) * n_inner, cudaMemcpyHostToDevice, st));
-  }
+  // device copy of the momentum table for the cooperative path, cached per
+  // budget (the table depends only on n_inner) so repeated prox calls stay async
+  const double* bdev = accelerated ? device_betas(n_inner) : nullptr;
   int rc = fgp2d_run(dtype, x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W,
                      n_inner, accelerated, nonneg, step, beta.data(), bdev, st);
-  // (a pageable-source cudaMemcpyAsync returns once the table is staged)
-  if (bdev) cudaFreeAsync(bdev, st);
   if (rc) return rc;
   return fgp2d_finalize(dtype, x, xps, q, qps, active, n_active, H, W, n_inner, nonneg, u, ups, st);
 }
