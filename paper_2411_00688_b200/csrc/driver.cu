@@ -37,7 +37,7 @@ int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t
 int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
-              const double* betas_host, const double* betas_dev, cudaStream_t st);
+              const double* betas_host, cudaStream_t st);
 int skip_flush(int dto, void* x, const void* b, const void* h, const int32_t* pend,
                const int32_t* kfirst, int64_t n, int64_t HW, double gamma, int32_t* bad,
                cudaStream_t st);
@@ -140,11 +140,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     for (int i = 0; i < n_inner; ++i) beta_f[i] = (float)beta[i];
   }
 
-  DevBuf d_coins, d_act, d_rep, d_pend, d_kfirst, d_flp, d_flk, d_beta, d_betad;
-  if (accelerated) {  // double momentum table for the cooperative FGP path
-    PSB_CUDA(cudaMalloc(&d_betad.p, n_inner * sizeof(double)));
-    PSB_CUDA(cudaMemcpy(d_betad.p, beta.data(), n_inner * sizeof(double), cudaMemcpyHostToDevice));
-  }
+  DevBuf d_coins, d_act, d_rep, d_pend, d_kfirst, d_flp, d_flk, d_beta;
   if (use_cluster) {
     if (!act.empty()) {
       PSB_CUDA(cudaMalloc(&d_pend.p, pend.size() * sizeof(int32_t)));
@@ -228,8 +224,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (rc || na == 0) continue;
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
     rc = fgp2d_run(dtf, z, HW, q, qps, act_d + off[k], na, weight, nullptr, 0, rep_d + off[k], H, W,
-                   n_inner, accelerated, nonneg, 0.125, beta.data(),
-                   static_cast<const double*>(d_betad.p), st);
+                   n_inner, accelerated, nonneg, 0.125, beta.data(), st);
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
     if (rc == PSB_OK)
       rc = proxskip_post(dto, dtf, x, ident ? b : fid.g, ident, h, z, q, qps, act_d + off[k], na,

@@ -9,14 +9,9 @@
 // neighbours come from warp shuffles; the two band-edge columns come from one
 // predicated scalar load per row by lanes 0 and 31.  Strip-edge rows are
 // re-read (L2 hits).
-#include <cooperative_groups.h>
-
-#include <map>
-#include <mutex>
 
 #include "common.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace psb {
 
@@ -216,28 +211,6 @@ __global__ void __launch_bounds__(128) fgp2d_iter_kernel(FgpArgs<T, V> a) {
   fgp2d_item(a, item, blockIdx.y);
 }
 
-// All n_inner iterations of a small batch in ONE cooperative launch: the CTAs
-// stay resident, sweep every (problem, band, strip) work item per iteration and
-// meet at a grid-wide barrier.  For a single 256^2/512^2 problem the state
-// (<= 5 MB fp32) lives in L2, so an iteration costs a grid sync plus an
-// L2-bound sweep instead of a kernel launch.
-template <class T, int V>
-__global__ void __launch_bounds__(128) fgp2d_persistent_kernel(FgpArgs<T, V> a,
-                                                                const double* __restrict__ betas,
-                                                                int n_inner, int accelerated,
-                                                                int n_active) {
-  cg::grid_group grid = cg::this_grid();
-  const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nw = gridDim.x * (blockDim.x >> 5);
-  const int total = a.nitems * n_active;
-  for (int it = 0; it < n_inner; ++it) {
-    a.it = it;
-    a.beta = (accelerated && it > 0) ? (T)betas[it - 1] : T(0);
-    for (int wi = wg; wi < total; wi += nw) fgp2d_item(a, wi % a.nitems, wi / a.nitems);
-    grid.sync();
-  }
-}
-
 // u = clamp(x + div q_n) and q_n -> slot 0 (tv.py:86-89)
 template <class T>
 __global__ void fgp2d_finalize_kernel(const T* __restrict__ x, int64_t xps, T* q, int64_t qps,
@@ -290,7 +263,7 @@ int launch_iter(const void* x, int64_t xps, void* q, int64_t qps, const int32_t*
   const int64_t warps_per_row = (int64_t)a.nbands * n_active;
   const int64_t target = 4LL * sm_count() * 16;  // ~16 warps per SM, 4 waves
   int rs = 32;
-  while (rs > 4 && warps_per_row * ((H + rs - 1) / rs) < target) rs >>= 1;
+  while (rs > 1 && warps_per_row * ((H + rs - 1) / rs) < target) rs >>= 1;
   a.rs = rs;
   a.nitems = a.nbands * ((H + rs - 1) / rs);
   dim3 block(128);
@@ -315,120 +288,18 @@ int dispatch_iter(const void* x, int64_t xps, void* q, int64_t qps, const int32_
                            beta, step, nonneg, st);
 }
 
-template <class T, int V>
-FgpArgs<T, V> make_args(const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
-                        double weight, const double* wts, int rep_all, const uint8_t* rep, int H,
-                        int W, double step, int nonneg, int rs) {
-  FgpArgs<T, V> a;
-  a.x = static_cast<const T*>(x);
-  a.xps = xps;
-  a.q = static_cast<T*>(q);
-  a.qps = qps;
-  a.active = active;
-  a.wts = wts;
-  a.w_all = weight;
-  a.rep = rep;
-  a.rep_all = rep_all;
-  a.H = H;
-  a.W = W;
-  a.it = 0;
-  a.beta = T(0);
-  a.step = (T)step;
-  a.nonneg = nonneg;
-  a.nbands = (W + 32 * V - 1) / (32 * V);
-  a.rs = rs;
-  a.nitems = a.nbands * ((H + rs - 1) / rs);
-  return a;
-}
-
-// Cooperative persistent launch of all n_inner iterations; returns 1 (not
-// launched) when the batch is too large to profit or cannot be co-resident.
-template <class T, int V>
-int launch_persistent(const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
-                      int n_active, double weight, const double* wts, int rep_all,
-                      const uint8_t* rep, int H, int W, int n_inner, int accelerated, int nonneg,
-                      double step, const double* betas, cudaStream_t st, bool* used) {
-  *used = false;
-  static int max_blocks = 0;
-  if (max_blocks == 0) {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fgp2d_persistent_kernel<T, V>, 128,
-                                                      0) != cudaSuccess ||
-        per_sm <= 0) {
-      (void)cudaGetLastError();
-      per_sm = 0;
-    }
-    max_blocks = std::max(1, per_sm) * sm_count();
-    if (per_sm == 0) max_blocks = -1;
-  }
-  if (max_blocks < 0) return PSB_OK;
-  const FgpArgs<T, V> a = make_args<T, V>(x, xps, q, qps, active, weight, wts, rep_all, rep, H, W,
-                                          step, nonneg, 4);
-  const int64_t total_warps = (int64_t)a.nitems * n_active;
-  // only small batches: one launch per iteration already fills the GPU otherwise
-  if (total_warps > 4LL * max_blocks * 4) return PSB_OK;
-  const int blocks = (int)std::min<int64_t>(max_blocks, (total_warps + 3) / 4);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(128);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PSB_CUDA(cudaLaunchKernelEx(&cfg, fgp2d_persistent_kernel<T, V>, a, betas, n_inner, accelerated,
-                              n_active));
-  PSB_LAUNCHED("fgp2d_persistent");
-  *used = true;
-  return PSB_OK;
-}
-
 }  // namespace
 
 int fgp2d_iter(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
                int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
                int H, int W, int it, double beta, double step, int nonneg, cudaStream_t st);
 
-// All n_inner FGP iterations for a batch: one cooperative launch for small
-// batches (PSB_NO_PERSIST=1 disables), else one launch per iteration.
-// `betas_dev` = device copy of the momentum table (may be NULL when
-// accelerated == 0); `betas_host` = the same table on the host.
+// All n_inner FGP iterations for a batch (one launch per inner iteration;
+// inside a captured CUDA graph the launches are back to back).
 int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
-              const double* betas_host, const double* betas_dev, cudaStream_t st) {
-  PSB_REQUIRE(H >= 2 && W >= 2, "fgp2d: need a 2-D grid with both sides >= 2");
-  PSB_REQUIRE(n_active >= 0 && n_active <= 65535, "fgp2d: n_active out of range");
-  PSB_REQUIRE(qps >= 6LL * H * W, "fgp2d: q_pstride must hold three (2,H,W) slots");
-  if (n_active == 0) return PSB_OK;
-  const char* off = std::getenv("PSB_NO_PERSIST");
-  if ((betas_dev || !accelerated) && !(off && off[0] == '1')) {
-    bool used = false;
-    int rc = PSB_OK;
-    constexpr int V4 = 4, V2 = 2;
-    if (dtype == PSB_F32) {
-      const bool al = (W % V4 == 0) && (xps % V4 == 0) && (qps % V4 == 0) &&
-                      reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(q) % 16 == 0;
-      rc = al ? launch_persistent<float, V4>(x, xps, q, qps, active, n_active, weight, wts, rep_all,
-                                             rep, H, W, n_inner, accelerated, nonneg, step,
-                                             betas_dev, st, &used)
-              : launch_persistent<float, 1>(x, xps, q, qps, active, n_active, weight, wts, rep_all,
-                                            rep, H, W, n_inner, accelerated, nonneg, step,
-                                            betas_dev, st, &used);
-    } else if (dtype == PSB_F64) {
-      const bool al = (W % V2 == 0) && (xps % V2 == 0) && (qps % V2 == 0) &&
-                      reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(q) % 16 == 0;
-      rc = al ? launch_persistent<double, V2>(x, xps, q, qps, active, n_active, weight, wts,
-                                              rep_all, rep, H, W, n_inner, accelerated, nonneg,
-                                              step, betas_dev, st, &used)
-              : launch_persistent<double, 1>(x, xps, q, qps, active, n_active, weight, wts,
-                                             rep_all, rep, H, W, n_inner, accelerated, nonneg,
-                                             step, betas_dev, st, &used);
-    }
-    if (rc) return rc;
-    if (used) return PSB_OK;
-  }
+              const double* betas_host, cudaStream_t st) {
   for (int it = 0; it < n_inner; ++it) {
     // y_it = q_it + beta_{it-1} (q_it - q_{it-1}); beta_{-1} := 0 (y_0 = q_0)
     const double b = (accelerated && it > 0) ? betas_host[it - 1] : 0.0;
@@ -490,24 +361,6 @@ void fista_betas(int n, double* out) {
   }
 }
 
-const double* device_betas(int n) {
-  static std::mutex mu;
-  static std::map<int, double*> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(n);
-  if (it != cache.end()) return it->second;
-  std::vector<double> b(n);
-  fista_betas(n, b.data());
-  double* d = nullptr;
-  if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double) * n) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return nullptr;
-  }
-  cudaMemcpy(d, b.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
-  cache[n] = d;
-  return d;
-}
-
 int tv_prox2d(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step, void* u,
@@ -516,11 +369,8 @@ int tv_prox2d(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const
   PSB_REQUIRE(wts != nullptr || weight > 0, "tv_prox: weight must be positive");
   std::vector<double> beta(n_inner, 0.0);
   if (accelerated) fista_betas(n_inner, beta.data());
-  // device copy of the momentum table for the cooperative path, cached per
-  // budget (the table depends only on n_inner) so repeated prox calls stay async
-  const double* bdev = accelerated ? device_betas(n_inner) : nullptr;
   int rc = fgp2d_run(dtype, x, xps, q, qps, active, n_active, weight, wts, rep_all, rep, H, W,
-                     n_inner, accelerated, nonneg, step, beta.data(), bdev, st);
+                     n_inner, accelerated, nonneg, step, beta.data(), st);
   if (rc) return rc;
   return fgp2d_finalize(dtype, x, xps, q, qps, active, n_active, H, W, n_inner, nonneg, u, ups, st);
 }
