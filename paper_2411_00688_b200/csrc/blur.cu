@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict_
                                                             T* __restrict__ g, int H, int W,
                                                             Taps t) {
   extern __shared__ unsigned char smem_raw[];
+  pdl_enter();
   T* sm = reinterpret_cast<T*>(smem_raw);
   const int R = t.k / 2;
   const int NU = TS + 4 * R;  // u tile side (2R halo each side)
@@ -137,8 +138,8 @@ int launch_sep(const void* u, const void* b, void* g, int H, int W, const Taps& 
   PSB_CUDA(cudaFuncSetAttribute(blur_grad_sep_kernel<T, TS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   dim3 grid((W + TS - 1) / TS, (H + TS - 1) / TS);
-  blur_grad_sep_kernel<T, TS><<<grid, 256, sm, st>>>((const T*)u, (const T*)b, (T*)g, H, W, t);
-  PSB_LAUNCHED("blur_grad_sep");
+  PSB_CUDA(launch_chain(blur_grad_sep_kernel<T, TS>, grid, dim3(256), sm, st, (const T*)u,
+                        (const T*)b, (T*)g, H, W, t));
   return PSB_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <vector>
 #include <cmath>
 #include <algorithm>
+#include <utility>
 
 #include "../../include/psb200.h"
 
@@ -128,5 +129,38 @@ __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
 }
 
 template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
+
+// ---- programmatic dependent launch -------------------------------------------
+// Every kernel of a launch chain starts with pdl_enter(): it lets the NEXT
+// kernel in the stream begin launching right away and then waits until the
+// previous kernel has completed and its writes are visible.  Without the
+// launch attribute both instructions are no-ops, so a kernel is correct
+// whichever way it was launched.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+// Launch with the programmatic-stream-serialization attribute when the grid
+// fits in one wave (small, latency-bound launches: single 256^2 / 512^2
+// problems); large multi-wave grids keep plain stream ordering.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  const long long ctas = (long long)grid.x * grid.y * grid.z;
+  if (ctas <= 2LL * sm_count()) {
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace psb

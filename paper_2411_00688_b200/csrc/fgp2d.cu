@@ -206,6 +206,7 @@ __device__ __forceinline__ void fgp2d_item(const FgpArgs<T, V>& a, int item, int
 
 template <class T, int V>
 __global__ void __launch_bounds__(128) fgp2d_iter_kernel(FgpArgs<T, V> a) {
+  pdl_enter();
   const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (item >= a.nitems) return;  // whole warp exits together
   fgp2d_item(a, item, blockIdx.y);
@@ -217,6 +218,7 @@ __global__ void fgp2d_finalize_kernel(const T* __restrict__ x, int64_t xps, T* q
                                       const int32_t* __restrict__ active, int H, int W, int n_inner,
                                       int nonneg, T* __restrict__ u, int64_t ups) {
   using A = Ar<T>;
+  pdl_enter();
   const int p = active ? active[blockIdx.y] : (int)blockIdx.y;
   const int64_t HW = (int64_t)H * W;
   const int slot = n_inner % 3;
@@ -268,8 +270,7 @@ int launch_iter(const void* x, int64_t xps, void* q, int64_t qps, const int32_t*
   a.nitems = a.nbands * ((H + rs - 1) / rs);
   dim3 block(128);
   dim3 grid((a.nitems + 3) / 4, n_active);
-  fgp2d_iter_kernel<T, V><<<grid, block, 0, st>>>(a);
-  PSB_LAUNCHED("fgp2d_iter");
+  PSB_CUDA(launch_chain(fgp2d_iter_kernel<T, V>, grid, block, 0, st, a));
   return PSB_OK;
 }
 
@@ -337,16 +338,15 @@ int fgp2d_finalize(int dtype, const void* x, int64_t xps, void* q, int64_t qps,
   dim3 block(256);
   dim3 grid((unsigned)std::min<int64_t>((HW + 255) / 256, 1024), n_active);
   if (dtype == PSB_F32)
-    fgp2d_finalize_kernel<float><<<grid, block, 0, st>>>(
-        static_cast<const float*>(x), xps, static_cast<float*>(q), qps, active, H, W, n_inner,
-        nonneg, static_cast<float*>(u), ups);
+    PSB_CUDA(launch_chain(fgp2d_finalize_kernel<float>, grid, block, 0, st,
+                          static_cast<const float*>(x), xps, static_cast<float*>(q), qps, active,
+                          H, W, n_inner, nonneg, static_cast<float*>(u), ups));
   else if (dtype == PSB_F64)
-    fgp2d_finalize_kernel<double><<<grid, block, 0, st>>>(
-        static_cast<const double*>(x), xps, static_cast<double*>(q), qps, active, H, W, n_inner,
-        nonneg, static_cast<double*>(u), ups);
+    PSB_CUDA(launch_chain(fgp2d_finalize_kernel<double>, grid, block, 0, st,
+                          static_cast<const double*>(x), xps, static_cast<double*>(q), qps, active,
+                          H, W, n_inner, nonneg, static_cast<double*>(u), ups));
   else
     return fail(PSB_ERR_VALUE, "fgp2d: unknown dtype");
-  PSB_LAUNCHED("fgp2d_finalize");
   return PSB_OK;
 }
 

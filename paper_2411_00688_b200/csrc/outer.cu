@@ -26,6 +26,7 @@ __global__ void proxskip_pre_kernel(TO* __restrict__ x, const TO* __restrict__ g
                                     const uint8_t* __restrict__ coins, TO gamma, TO hcoef,
                                     int32_t* __restrict__ bad, int k) {
   using A = Ar<TO>;
+  pdl_enter();
   const int64_t p = blockIdx.y;
   const bool theta = coins ? coins[p] != 0 : true;
   const int64_t base = p * HW;
@@ -54,6 +55,7 @@ __global__ void proxskip_post_kernel(TO* __restrict__ x, const TO* __restrict__ 
                                      int32_t* __restrict__ bad, int k) {
   using A = Ar<TO>;
   using F = Ar<TF>;
+  pdl_enter();
   const int p = active ? active[blockIdx.y] : (int)blockIdx.y;
   const int64_t HW = (int64_t)H * W;
   const int slot = n_inner % 3;
@@ -95,11 +97,11 @@ void launch_pre(void* x, const void* gb, int ident, const void* h, void* z, int6
   const int64_t want = (HW + 255) / 256;
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(1, 4LL * sm_count() * 8 / std::max<int64_t>(n, 1)))), (unsigned)n);
   if (ident)
-    proxskip_pre_kernel<TO, TF, true><<<grid, block, 0, st>>>(
-        (TO*)x, (const TO*)gb, (const TO*)h, (TF*)z, HW, coins, (TO)gamma, (TO)hcoef, bad, k);
+    (void)launch_chain(proxskip_pre_kernel<TO, TF, true>, grid, block, 0, st, (TO*)x,
+                       (const TO*)gb, (const TO*)h, (TF*)z, HW, coins, (TO)gamma, (TO)hcoef, bad, k);
   else
-    proxskip_pre_kernel<TO, TF, false><<<grid, block, 0, st>>>(
-        (TO*)x, (const TO*)gb, (const TO*)h, (TF*)z, HW, coins, (TO)gamma, (TO)hcoef, bad, k);
+    (void)launch_chain(proxskip_pre_kernel<TO, TF, false>, grid, block, 0, st, (TO*)x,
+                       (const TO*)gb, (const TO*)h, (TF*)z, HW, coins, (TO)gamma, (TO)hcoef, bad, k);
 }
 
 template <class TO, class TF>
@@ -111,13 +113,13 @@ void launch_post(void* x, const void* gb, int ident, void* h, const void* z, voi
   const int64_t want = (HW + 255) / 256;
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(1, 4LL * sm_count() * 8 / n_active))), (unsigned)n_active);
   if (ident)
-    proxskip_post_kernel<TO, TF, true><<<grid, block, 0, st>>>(
-        (TO*)x, (const TO*)gb, (TO*)h, (const TF*)z, (TF*)q, qps, active, H, W, n_inner, nonneg,
-        (TO)gamma, (TO)pg, bad, k);
+    (void)launch_chain(proxskip_post_kernel<TO, TF, true>, grid, block, 0, st, (TO*)x,
+                       (const TO*)gb, (TO*)h, (const TF*)z, (TF*)q, qps, active, H, W, n_inner,
+                       nonneg, (TO)gamma, (TO)pg, bad, k);
   else
-    proxskip_post_kernel<TO, TF, false><<<grid, block, 0, st>>>(
-        (TO*)x, (const TO*)gb, (TO*)h, (const TF*)z, (TF*)q, qps, active, H, W, n_inner, nonneg,
-        (TO)gamma, (TO)pg, bad, k);
+    (void)launch_chain(proxskip_post_kernel<TO, TF, false>, grid, block, 0, st, (TO*)x,
+                       (const TO*)gb, (TO*)h, (const TF*)z, (TF*)q, qps, active, H, W, n_inner,
+                       nonneg, (TO)gamma, (TO)pg, bad, k);
 }
 
 // Deferred skip iterations of the identity-fidelity ProxSkip (skip.py:68 with
