@@ -120,18 +120,61 @@ __device__ __forceinline__ void fgp2d_item(const FgpArgs<T, V>& a, int item, int
 #pragma unroll
   for (int v = 0; v < V; ++v) yyu[v] = yy[v] = yx[v] = u[v] = T(0);
 
-  auto load_row = [&](int r, T(&ty)[V], T(&tx)[V], T(&tu)[V], T& ty1, T& tx1, T& tu1) {
+  // Raw loads of one row (issued early, consumed one row later) and their
+  // completion into y = q_k + beta (q_k - q_{k-1}) (re-projection at it == 0)
+  // and u := x (prim_row adds the divergence).
+  struct Raw {
+    T ky[V], kx[V], my[V], mx[V], xv[V];
+    T hky, hkx, hmy, hmx, hx;
+  };
+  auto issue_row = [&](int r, Raw& R) {
     const int64_t ro = (int64_t)r * W;
     if (lin) {
-      load_y<T, V>(qk, qm, ro + cl, HW, mom, rp, beta, w, ty, tx);
-      ldv<T, V>(tu, xp + ro + cl);
+      ldv<T, V>(R.ky, qk + ro + cl);
+      ldv<T, V>(R.kx, qk + HW + ro + cl);
+      if (mom) {
+        ldv<T, V>(R.my, qm + ro + cl);
+        ldv<T, V>(R.mx, qm + HW + ro + cl);
+      }
+      ldv<T, V>(R.xv, xp + ro + cl);
     }
     if (hval) {
-      T a1[1], b1[1];
-      load_y<T, 1>(qk, qm, ro + hc, HW, mom, rp, beta, w, a1, b1);
-      ty1 = a1[0];
-      tx1 = b1[0];
-      tu1 = __ldg(xp + ro + hc);
+      R.hky = __ldg(qk + ro + hc);
+      R.hkx = __ldg(qk + HW + ro + hc);
+      if (mom) {
+        R.hmy = __ldg(qm + ro + hc);
+        R.hmx = __ldg(qm + HW + ro + hc);
+      }
+      R.hx = __ldg(xp + ro + hc);
+    }
+  };
+  auto finish_row = [&](const Raw& R, T(&ty)[V], T(&tx)[V], T(&tu)[V], T& ty1, T& tx1, T& tu1) {
+    auto y_of = [&](T k0, T k1, T m0, T m1, T& o0, T& o1) {
+      if (rp) {
+        const T sc = A::ball_scale(k0, k1, w);
+        k0 = A::mul(k0, sc);
+        k1 = A::mul(k1, sc);
+      }
+      if (mom) {
+        k0 = A::add(k0, A::mul(beta, A::sub(k0, m0)));
+        k1 = A::add(k1, A::mul(beta, A::sub(k1, m1)));
+      }
+      o0 = k0;
+      o1 = k1;
+    };
+    if (lin) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        y_of(R.ky[v], R.kx[v], mom ? R.my[v] : T(0), mom ? R.mx[v] : T(0), ty[v], tx[v]);
+        tu[v] = R.xv[v];
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) ty[v] = tx[v] = tu[v] = T(0);
+    }
+    if (hval) {
+      y_of(R.hky, R.hkx, mom ? R.hmy : T(0), mom ? R.hmx : T(0), ty1, tx1);
+      tu1 = R.hx;
     }
   };
 
@@ -148,14 +191,19 @@ __device__ __forceinline__ void fgp2d_item(const FgpArgs<T, V>& a, int item, int
     if (lane == 31) tu1 = clampu(A::add(tu1, div_at<T>(r, hc, H, W, ty1, tyu1, tx1, tx[V - 1])), a.nonneg);
   };
 
-  // prologue: y_y at row r0-1, then row r0 and u(r0)
+  // prologue: issue rows r0-1, r0, r0+1 together (one memory round trip),
+  // then y_y(r0-1), y(r0), u(r0)
+  Raw Rup, Rc, Rn;
+  if (r0 > 0) issue_row(r0 - 1, Rup);
+  issue_row(r0, Rc);
+  if (r0 + 1 < H) issue_row(r0 + 1, Rn);
   if (r0 > 0) {
     T tx[V], tu[V], tx1 = T(0), tu1 = T(0);
-    load_row(r0 - 1, yyu, tx, tu, hyyu, tx1, tu1);
+    finish_row(Rup, yyu, tx, tu, hyyu, tx1, tu1);
   }
   {
     T hx1 = T(0);
-    load_row(r0, yy, yx, u, hyy, hyx, hx1);
+    finish_row(Rc, yy, yx, u, hyy, hyx, hx1);
     hu = hx1;
     prim_row(r0, yy, yyu, yx, u, hyy, hyyu, hyx, hu);
   }
@@ -167,7 +215,9 @@ __device__ __forceinline__ void fgp2d_item(const FgpArgs<T, V>& a, int item, int
 #pragma unroll
     for (int v = 0; v < V; ++v) nyy[v] = nyx[v] = nu[v] = T(0);
     if (nxt) {
-      load_row(i + 1, nyy, nyx, nu, nhyy, nhyx, nhu);
+      finish_row(Rn, nyy, nyx, nu, nhyy, nhyx, nhu);
+      // row i+2 is needed only if row i+1 is still in this strip
+      if (i + 2 < H && i + 1 < r1) issue_row(i + 2, Rn);
       prim_row(i + 1, nyy, yy, nyx, nu, nhyy, hyy, nhyx, nhu);
     }
     T right = __shfl_down_sync(0xffffffffu, u[0], 1);
