@@ -66,6 +66,21 @@ int psb_project_nonneg(int dtype, const void* u, void* out, int64_t count, void*
 int psb_lincomb(int dtype, double a, const void* x, double b, const void* y, void* out,
                 int64_t count, void* stream);
 
+/* ---- diagonal-step PDHG building blocks (solvers.py:187-234, problems.py:139-146)
+ * psb_axpy_arr:   out = x + sign * (s .* y), s an array (diagonal steps)
+ * psb_fidprox:    out = (v - t .* b) / (1 + t), t scalar or t_arr per element
+ * psb_recip_floor: out = 1 / max(x, floor)  (diagonal_steps, solvers.py:212-224)
+ * psb_absgrad2d / psb_absdiv2d: |D| u and |D|^T q, the abs maps of grad_map
+ *   (operators.py:81-94) that back diagonal preconditioning */
+int psb_axpy_arr(int dtype, const void* x, int sign, const void* s, const void* y, void* out,
+                 int64_t count, void* stream);
+int psb_fidprox(int dtype, const void* v, double t, const void* t_arr, const void* b, void* out,
+                int64_t count, void* stream);
+int psb_recip_floor(int dtype, const void* x, double floor_, void* out, int64_t count,
+                    void* stream);
+int psb_absgrad2d(int dtype, const void* u, void* g, int H, int W, void* stream);
+int psb_absdiv2d(int dtype, const void* q, void* d, int H, int W, void* stream);
+
 /* ---- FGP TV prox, tv.py:53-89 -------------------------------------------
  * psb_fgp2d_iter: ONE inner iteration (tv.py:75-80) for every problem in
  *   `active` (device int32[n_active]; NULL = problems 0..n_active-1):

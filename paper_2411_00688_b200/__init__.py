@@ -12,14 +12,16 @@ from . import _lib  # noqa: F401  (fails loudly when libpsb200.so is missing)
 from .batched import BatchedTvDenoise, coin_table, run_proxskip_batched, shard_indices
 from .errors import DivergenceError, ReferenceRejectedError
 from .operators import (BlurKernel, LinearMap, RadonGeometry, blur_adjoint, blur_forward, blur_map,
-                        block_stack, divergence, gaussian_kernel, grad_forward, grad_map,
-                        identity_map, power_method, radon_map)
-from .problems import (GRAD_NORM_SQ, TvReconstructionProblem, build_tv_recon,
-                       build_tv_saddle_implicit, objective_tv)
+                        block_stack, diagonal_map, divergence, gaussian_kernel, grad_forward,
+                        grad_map, identity_map, power_method, radon_map)
+from .problems import (GRAD_NORM_SQ, DualRofProblem, TvReconstructionProblem, build_dual_rof,
+                       build_tv_recon, build_tv_saddle_implicit, objective_tv, primal_from_dual)
 from .proximal import project_ball, project_nonneg, prox_zero
-from .skip import SkipConfig, optimal_probability, run_pdhgskip2, run_proxskip
+from .skip import (SkipConfig, bernoulli_op, optimal_probability, run_pdhgskip1, run_pdhgskip2,
+                   run_proxskip)
 from .solvers import (IterationLog, ProxProblem, RunRecord, SaddleProblem, SmoothProblem,
-                      run_aprojgd, run_fista, run_pdhg, run_pgd)
+                      diagonal_steps, run_aprojgd, run_fista, run_gd, run_pdhg,
+                      run_pdhg_preconditioned, run_pgd)
 from .tensor import axpby, dot, norm2, rel_error
 from .tv import INNER_STEP, TvProxState, dual_gap_rof, tv_prox, tv_value
 

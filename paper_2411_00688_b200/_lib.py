@@ -45,6 +45,11 @@ SIGNATURES = {
     "psb_project_ball2d": [_i32, _vp, _vp, _i64, _i64, _dbl, _vp],
     "psb_project_nonneg": [_i32, _vp, _vp, _i64, _vp],
     "psb_lincomb": [_i32, _dbl, _vp, _dbl, _vp, _vp, _i64, _vp],
+    "psb_axpy_arr": [_i32, _vp, _i32, _vp, _vp, _vp, _i64, _vp],
+    "psb_fidprox": [_i32, _vp, _dbl, _vp, _vp, _vp, _i64, _vp],
+    "psb_recip_floor": [_i32, _vp, _dbl, _vp, _i64, _vp],
+    "psb_absgrad2d": [_i32, _vp, _vp, _i32, _i32, _vp],
+    "psb_absdiv2d": [_i32, _vp, _vp, _i32, _i32, _vp],
     "psb_fgp2d_iter": [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _dbl, _vp, _i32, _vp, _i32, _i32,
                        _i32, _dbl, _dbl, _i32, _vp],
     "psb_fgp2d_finalize": [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _vp,

@@ -90,6 +90,73 @@ __global__ void lincomb_kernel(T a, const T* __restrict__ x, T b, const T* __res
   }
 }
 
+// out = x + sgn * (s .* y) with an ARRAY coefficient s (diagonal PDHG steps,
+// solvers.py:200-204): x - sigma*K^T y (sgn = -1), y + tau*K xbar (sgn = +1).
+template <class T>
+__global__ void axpy_arr_kernel(const T* __restrict__ x, int sgn, const T* __restrict__ sc,
+                                const T* __restrict__ y, T* __restrict__ out, int64_t count) {
+  using A = Ar<T>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T t = A::mul(sc[i], y[i]);
+    out[i] = sgn < 0 ? A::sub(x[i], t) : A::add(x[i], t);
+  }
+}
+
+// conjugate prox of 0.5||. - b||^2: (v - t b) / (1 + t), t scalar (t_arr == NULL)
+// or per element (problems.py:143-144, 178)
+template <class T>
+__global__ void fidprox_kernel(const T* __restrict__ v, T t, const T* __restrict__ t_arr,
+                               const T* __restrict__ b, T* __restrict__ out, int64_t count) {
+  using A = Ar<T>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T ti = t_arr ? t_arr[i] : t;
+    out[i] = A::div(A::sub(v[i], A::mul(ti, b[i])), A::add(T(1), ti));
+  }
+}
+
+// 1 / max(x, floor)  (diagonal_steps, solvers.py:212-224)
+template <class T>
+__global__ void recip_floor_kernel(const T* __restrict__ x, T fl, T* __restrict__ out,
+                                   int64_t count) {
+  using A = Ar<T>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = x[i];
+    out[i] = A::div(T(1), v > fl ? v : (v == v ? fl : v));
+  }
+}
+
+// |D| u and |D|^T q (operators.py:81-94): the entrywise-absolute gradient maps
+template <class T>
+__global__ void absgrad2d_kernel(const T* __restrict__ u, T* __restrict__ g, int H, int W) {
+  using A = Ar<T>;
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HW;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / W), c = (int)(i % W);
+    g[i] = r < H - 1 ? A::add(u[i + W], u[i]) : T(0);
+    g[HW + i] = c < W - 1 ? A::add(u[i + 1], u[i]) : T(0);
+  }
+}
+
+template <class T>
+__global__ void absdiv2d_kernel(const T* __restrict__ q, T* __restrict__ d, int H, int W) {
+  using A = Ar<T>;
+  const int64_t HW = (int64_t)H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HW;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / W), c = (int)(i % W);
+    T s = T(0);
+    if (r < H - 1) s = A::add(s, q[i]);
+    if (r > 0) s = A::add(s, q[i - W]);
+    if (c < W - 1) s = A::add(s, q[HW + i]);
+    if (c > 0) s = A::add(s, q[HW + i - 1]);
+    d[i] = s;
+  }
+}
+
 inline dim3 grid_for(int64_t count) {
   return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 32LL * sm_count())));
 }
@@ -158,6 +225,61 @@ int psb_lincomb(int dtype, double a, const void* x, double b, const void* y, voi
     return psb::fail(PSB_ERR_VALUE, "lincomb: unknown dtype");
   PSB_LAUNCHED("lincomb");
   return PSB_OK;
+}
+
+#define PSB_DISPATCH(name, ...)                                                     \
+  do {                                                                              \
+    if (dtype == PSB_F32) {                                                         \
+      using T = float;                                                              \
+      __VA_ARGS__;                                                                  \
+    } else if (dtype == PSB_F64) {                                                  \
+      using T = double;                                                             \
+      __VA_ARGS__;                                                                  \
+    } else {                                                                        \
+      return psb::fail(PSB_ERR_VALUE, name ": unknown dtype");                      \
+    }                                                                               \
+    PSB_LAUNCHED(name);                                                             \
+    return PSB_OK;                                                                  \
+  } while (0)
+
+int psb_axpy_arr(int dtype, const void* x, int sign, const void* s, const void* y, void* out,
+                 int64_t count, void* stream) {
+  if (count == 0) return PSB_OK;
+  auto st = psb::as_stream(stream);
+  PSB_DISPATCH("axpy_arr", psb::axpy_arr_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
+                               (const T*)x, sign, (const T*)s, (const T*)y, (T*)out, count));
+}
+
+int psb_fidprox(int dtype, const void* v, double t, const void* t_arr, const void* b, void* out,
+                int64_t count, void* stream) {
+  if (count == 0) return PSB_OK;
+  auto st = psb::as_stream(stream);
+  PSB_DISPATCH("fidprox", psb::fidprox_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
+                              (const T*)v, (T)t, (const T*)t_arr, (const T*)b, (T*)out, count));
+}
+
+int psb_recip_floor(int dtype, const void* x, double floor_, void* out, int64_t count,
+                    void* stream) {
+  if (count == 0) return PSB_OK;
+  auto st = psb::as_stream(stream);
+  PSB_DISPATCH("recip_floor", psb::recip_floor_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
+                                  (const T*)x, (T)floor_, (T*)out, count));
+}
+
+int psb_absgrad2d(int dtype, const void* u, void* g, int H, int W, void* stream) {
+  PSB_REQUIRE(H >= 2 && W >= 2, "grad_map: need a 2-D grid with both sides >= 2");
+  auto st = psb::as_stream(stream);
+  const int64_t cnt = (int64_t)H * W;
+  PSB_DISPATCH("absgrad2d", psb::absgrad2d_kernel<T><<<psb::grid_for(cnt), 256, 0, st>>>(
+                                (const T*)u, (T*)g, H, W));
+}
+
+int psb_absdiv2d(int dtype, const void* q, void* d, int H, int W, void* stream) {
+  PSB_REQUIRE(H >= 2 && W >= 2, "grad_map: need a 2-D grid with both sides >= 2");
+  auto st = psb::as_stream(stream);
+  const int64_t cnt = (int64_t)H * W;
+  PSB_DISPATCH("absdiv2d", psb::absdiv2d_kernel<T><<<psb::grid_for(cnt), 256, 0, st>>>(
+                               (const T*)q, (T*)d, H, W));
 }
 
 int psb_project_nonneg(int dtype, const void* u, void* out, int64_t count, void* stream) {

@@ -82,13 +82,29 @@ divergence = _wrap(div_dev)
 divergence.__doc__ = "Discrete divergence = -grad^T (operators.py:60-71)."
 
 
+def _absgrad_dev(u):
+    H, W = u.shape
+    g = torch.empty((2, H, W), dtype=u.dtype, device="cuda")
+    L.call("psb_absgrad2d", L.dcode(u.dtype), L.ptr(u), L.ptr(g), H, W, L.stream())
+    return g
+
+
+def _absdiv_dev(q):
+    H, W = q.shape[1:]
+    d = torch.empty((H, W), dtype=q.dtype, device="cuda")
+    L.call("psb_absdiv2d", L.dcode(q.dtype), L.ptr(q), L.ptr(d), H, W, L.stream())
+    return d
+
+
 def grad_map(shape, norm_sq_estimate=None):
-    """LinearMap of grad_forward on a fixed grid (operators.py:74-104)."""
+    """LinearMap of grad_forward on a fixed grid with its entrywise-absolute
+    maps for diagonal preconditioning (operators.py:74-104)."""
     h, w = shape
     return LinearMap(
         domain_shape=(h, w), range_shape=(2, h, w), forward=grad_forward,
         adjoint=_wrap(lambda q: T.lincomb(-1.0, div_dev(q))),
-        norm_sq_estimate=norm_sq_estimate, kind="grad")
+        norm_sq_estimate=norm_sq_estimate, abs_forward=_wrap(_absgrad_dev),
+        abs_adjoint=_wrap(_absdiv_dev), kind="grad")
 
 
 # -- periodic blur (operators.py:109-184) ---------------------------------------
@@ -272,6 +288,18 @@ def identity_map(shape):
                      abs_forward=copy, abs_adjoint=copy, kind="identity")
 
 
+def diagonal_map(diag):
+    """Elementwise multiplication by a fixed array (operators.py:310-320)."""
+    dd = AR.to_dev(diag, torch.float64)
+    ad = T.lincomb(1.0, dd)
+    ad = torch.where(ad < 0, -ad, ad)  # |diag| (setup, once)
+    mul = _wrap(lambda t: T.axpy_arr(torch.zeros_like(t), 1, dd.to(t.dtype), t))
+    amul = _wrap(lambda t: T.axpy_arr(torch.zeros_like(t), 1, ad.to(t.dtype), t))
+    return LinearMap(tuple(dd.shape), tuple(dd.shape), mul, mul,
+                     norm_sq_estimate=float(np.max(np.abs(np.asarray(AR.to_host(dd))))) ** 2,
+                     abs_forward=amul, abs_adjoint=amul, kind="diagonal")
+
+
 # -- composition (operators.py:323-365) ---------------------------------------
 
 def block_stack(a, d):
@@ -292,8 +320,20 @@ def block_stack(a, d):
         yd = y[na:].reshape(d.range_shape)
         return T.lincomb(1.0, _dev_apply(a.adjoint, ya), 1.0, _dev_apply(d.adjoint, yd))
 
-    return LinearMap(tuple(a.domain_shape), (na + nd,), _wrap(fwd), _wrap(adj), kind="stack",
-                     params=(a, d))
+    abs_fwd = abs_adj = None
+    if a.abs_forward is not None and d.abs_forward is not None:
+        def afwd(x):
+            return torch.cat([_dev_apply(a.abs_forward, x).reshape(-1),
+                              _dev_apply(d.abs_forward, x).reshape(-1)])
+
+        def aadj(y):
+            ya = y[:na].reshape(a.range_shape)
+            yd = y[na:].reshape(d.range_shape)
+            return T.lincomb(1.0, _dev_apply(a.abs_adjoint, ya), 1.0, _dev_apply(d.abs_adjoint, yd))
+
+        abs_fwd, abs_adj = _wrap(afwd), _wrap(aadj)
+    return LinearMap(tuple(a.domain_shape), (na + nd,), _wrap(fwd), _wrap(adj),
+                     abs_forward=abs_fwd, abs_adjoint=abs_adj, kind="stack", params=(a, d))
 
 
 def _dev_apply(fn, t):

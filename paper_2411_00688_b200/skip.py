@@ -202,13 +202,54 @@ def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_grap
     return AR.like(x, x0), log
 
 
+def bernoulli_op(x, p, draw):
+    """x/p on a success draw, zeros otherwise (skip.py:38-43)."""
+    if not 0.0 < p <= 1.0:
+        raise ValueError(f"bernoulli_op: p must be in (0, 1], got {p}")
+    t = AR.to_dev(x, torch.float64)
+    return AR.like(T.lincomb(1.0 / p, t) if draw else torch.zeros_like(t), x)
+
+
+def run_pdhgskip1(problem, x0, y0, sigma, tau, omega, skip, iters, log=None):
+    """PDHGSkip-1 (skip.py:82-114): on a success draw xhat = (prox(x - s K^T y) - x)/p,
+    else 0 (prox and K^T skipped); x <- x + xhat/(1 + omega);
+    y <- prox_{tau f*}(y + tau K(x + xhat))."""
+    if sigma <= 0 or tau <= 0:
+        raise ValueError("run_pdhgskip1: steps must be positive")
+    if omega < 0:
+        raise ValueError("run_pdhgskip1: omega must be nonnegative")
+    log = _ensure_log(log)
+    log.start(AR.is_host(x0))
+    p = skip.p
+    coins = skip.coins(iters)
+    K = problem.K
+    x = AR.to_dev(x0, torch.float64).clone()
+    y = AR.to_dev(y0, torch.float64).clone()
+    prox_count = 0
+    for k in range(iters):
+        theta = bool(coins[k])
+        if theta:
+            px = _dev(problem.prox_g(T.lincomb(1.0, x, -sigma, apply_adjoint(K, y)), sigma), x)
+            xhat = T.lincomb(1.0 / p, T.lincomb(1.0, px, -1.0, x))
+            prox_count += 1
+        else:
+            xhat = torch.zeros_like(x)
+        x_new = T.lincomb(1.0, x, 1.0 / (1.0 + omega), xhat)
+        y = _dev(problem.prox_fstar(T.lincomb(1.0, y, tau, apply_forward(K, T.lincomb(1.0, x_new, 1.0, xhat))), tau), y)
+        x = x_new
+        _check_finite(x, k, "pdhgskip1")
+        if log.observe(k + 1, x, prox_count, theta):
+            break
+    return AR.like(x, x0), log
+
+
 # -- PDHGSkip-2 (skip.py:117-150) ----------------------------------------------
 
 def run_pdhgskip2(problem, x0, y0, h0, sigma, tau, skip, iters, log=None):
     """PDHG with a ProxSkip control variate on the primal prox (Alg. 6)."""
     _check_step_rule(sigma, tau, problem.norm_K_sq)
     fused = getattr(problem, "_fused", None)
-    if fused is not None:
+    if fused is not None and np.isscalar(sigma) and np.isscalar(tau):
         return _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, "pdhgskip2")
     log = _ensure_log(log)
     log.start(AR.is_host(x0))

@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
+
 import torch
 
 from . import _arrays as AR
@@ -91,3 +93,45 @@ def axpby(alpha, x, beta, y):
     if tuple(x.shape) != tuple(y.shape):
         raise ValueError(f"axpby: shape mismatch {tuple(x.shape)} vs {tuple(y.shape)}")
     return AR.like(lincomb(alpha, x, beta, y), x)
+
+
+def axpy_arr(x, sign, s, y):
+    """x + sign * (s .* y) with an array coefficient s (diagonal PDHG steps)."""
+    x = _dev(x)
+    s = AR.to_dev(s, x.dtype)
+    y = AR.to_dev(y, x.dtype)
+    out = torch.empty_like(x)
+    L.call("psb_axpy_arr", L.dcode(x.dtype), L.ptr(x), int(sign), L.ptr(s), L.ptr(y), L.ptr(out),
+           x.numel(), L.stream())
+    return out
+
+
+def scaled(x, sign, s, y):
+    """x + sign * s * y for a scalar or array step s, rounded like the reference."""
+    if isinstance(s, (int, float, np.floating)):
+        return lincomb(1.0, x, sign * float(s), y)
+    return axpy_arr(x, sign, s, y)
+
+
+def fidprox(v, t, b):
+    """(v - t b) / (1 + t), t scalar or array (problems.py:143-144)."""
+    v = _dev(v)
+    b = AR.to_dev(b, v.dtype).reshape(v.shape)
+    out = torch.empty_like(v)
+    if isinstance(t, (int, float, np.floating)):
+        L.call("psb_fidprox", L.dcode(v.dtype), L.ptr(v), float(t), None, L.ptr(b), L.ptr(out),
+               v.numel(), L.stream())
+    else:
+        ta = AR.to_dev(t, v.dtype).reshape(v.shape)
+        L.call("psb_fidprox", L.dcode(v.dtype), L.ptr(v), 0.0, L.ptr(ta), L.ptr(b), L.ptr(out),
+               v.numel(), L.stream())
+    return out
+
+
+def recip_floor(x, floor):
+    """1 / max(x, floor) elementwise (solvers.py:222-223)."""
+    x = _dev(x)
+    out = torch.empty_like(x)
+    L.call("psb_recip_floor", L.dcode(x.dtype), L.ptr(x), float(floor), L.ptr(out), x.numel(),
+           L.stream())
+    return out
