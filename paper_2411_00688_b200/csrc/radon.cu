@@ -90,14 +90,15 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
 }
 
 // Adjoint at pixel (r, c): sum over angles and the lattice samples that
-// deposit into it of w * y(angle, bin).
-template <class T>
-__device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y, int r, int cc) {
+// deposit into it of w * y(angle, bin).  Exact path (double): positions and
+// tap decisions bit-identical to the reference (fp64 debug / parity path).
+__device__ __forceinline__ double pixel_gather_exact(const Geo& G, const double* __restrict__ y,
+                                                     int r, int cc) {
   const double dxp = (double)cc - G.center, dyp = (double)r - G.center;
   const double mid = 0.5 * (G.nb - 1);
   const double rb = 1.41421356237309515 / G.spacing + 1e-9;
   const double rs = 1.41421356237309515 / G.dstep + 1e-9;
-  T acc = T(0);
+  double acc = 0.0;
   for (int ia = 0; ia < G.na; ++ia) {
     const double c = G.cs[ia], s = G.sn[ia];
     // pixel centre in lattice coordinates (inverse rotation)
@@ -105,7 +106,7 @@ __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y,
     const double os = (-dxp * s + dyp * c + G.half_span) / G.dstep;
     const int b_lo = max(0, (int)ceil(ob - rb)), b_hi = min(G.nb - 1, (int)floor(ob + rb));
     const int s_lo = max(0, (int)ceil(os - rs)), s_hi = min(G.ns - 1, (int)floor(os + rs));
-    const T* yrow = y + (int64_t)ia * G.nb;
+    const double* yrow = y + (int64_t)ia * G.nb;
     for (int ib = b_lo; ib <= b_hi; ++ib) {
       for (int is = s_lo; is <= s_hi; ++is) {
         double px, py;
@@ -117,11 +118,61 @@ __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y,
         const double wy = dy ? fy : 1.0 - fy;
         const double wx = dx ? fx : 1.0 - fx;
         const double w = __dmul_rn(wy, wx);
-        if (w > 0) acc += (T)w * yrow[ib];
+        if (w > 0) acc += w * yrow[ib];
       }
     }
   }
   return acc;
+}
+
+// fp32 path: the bilinear tap weight of a sample at offset (dx, dy) from the
+// pixel centre is the tent product (1-|dx|)(1-|dy|) on |dx|,|dy| < 1 (the
+// reference's (1-f)/f split, operators.py:247-252, folded), so the gather needs
+// no floor / tap test: the pixel's lattice coordinates come from one fp64
+// inverse rotation per angle, the per-sample offsets are small fp32 numbers
+// relative to the pixel (|d| < 3), i.e. the same weights as the fp64 path to
+// ~1e-7 absolute.
+__device__ __forceinline__ float pixel_gather_tent(const Geo& G, const float* __restrict__ y, int r,
+                                                   int cc) {
+  const double dxp = (double)cc - G.center, dyp = (double)r - G.center;
+  const double mid = 0.5 * (G.nb - 1);
+  const double rb = 1.41421356237309515 / G.spacing + 1e-9;
+  const double rs = 1.41421356237309515 / G.dstep + 1e-9;
+  const double isp = 1.0 / G.spacing, ids = 1.0 / G.dstep;
+  const float spf = (float)G.spacing, dsf = (float)G.dstep;
+  float acc = 0.f;
+  for (int ia = 0; ia < G.na; ++ia) {
+    const double c = G.cs[ia], s = G.sn[ia];
+    const double ob = (dxp * c + dyp * s) * isp + mid;
+    const double os = (-dxp * s + dyp * c + G.half_span) * ids;
+    const int b_lo = max(0, (int)ceil(ob - rb)), b_hi = min(G.nb - 1, (int)floor(ob + rb));
+    const int s_lo = max(0, (int)ceil(os - rs)), s_hi = min(G.ns - 1, (int)floor(os + rs));
+    const float cf = (float)c, sf = (float)s;
+    const float eb = (float)((double)b_lo - ob) * spf;  // n-hat offset of bin b_lo
+    const float es = (float)((double)s_lo - os) * dsf;  // d-hat offset of step s_lo
+    const float* yrow = y + (int64_t)ia * G.nb;
+    for (int ib = b_lo; ib <= b_hi; ++ib) {
+      const float db = fmaf((float)(ib - b_lo), spf, eb);
+      const float bx = db * cf, by = db * sf;
+      float wsum = 0.f;
+      for (int is = s_lo; is <= s_hi; ++is) {
+        const float ds = fmaf((float)(is - s_lo), dsf, es);
+        const float dx = fmaf(-ds, sf, bx), dy = fmaf(ds, cf, by);
+        const float wx = fmaxf(0.f, 1.f - fabsf(dx)), wy = fmaxf(0.f, 1.f - fabsf(dy));
+        wsum = fmaf(wx, wy, wsum);
+      }
+      acc = fmaf(wsum, yrow[ib], acc);
+    }
+  }
+  return acc;
+}
+
+template <class T>
+__device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y, int r, int cc) {
+  if constexpr (sizeof(T) == 4)
+    return pixel_gather_tent(G, y, r, cc);
+  else
+    return pixel_gather_exact(G, y, r, cc);
 }
 
 template <class T>

@@ -157,3 +157,27 @@ def test_ct_implicit_saddle_pdhgskip2_fp64(golden):
                       psb.SkipConfig(0.3, 1), 12, log)
     np.testing.assert_array_equal(np.array(fl), g["cti_skip_flags"])
     np.testing.assert_allclose(np.stack(xs), g["cti_skip_traj"], rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.slow
+def test_config3_fp32_tent_gather_full_run_vs_fp64():
+    """The fp32 CT path (tent-weight gather, csrc/radon.cu pixel_gather_tent)
+    over the full config-3 run (512^2, 60 x 725, PDHGSkip-2 p=0.1, 2000
+    iterations) against the exact fp64 path, which is pinned to the reference
+    by the golden trajectories above: rel-L2(u) <= 1e-4, objective <= 1e-5."""
+    n = 512
+    u_true = phantoms.shepp_like(n, 10, np.random.default_rng(0))
+    R = psb.radon_map(psb.RadonGeometry(image_side=n, n_angles=60, n_bins=725))
+    s = R.forward(u_true)
+    b = phantoms.add_noise(s, 0.01 * s.max(), 0)
+    out = {}
+    for prec in ("fp64", "fp32"):
+        prob = psb.build_tv_recon(R, b, 0.05, nonneg=True, splitting="explicit", precision=prec)
+        sp = prob.saddle_problem
+        sp.norm_K_sq = 29740.8629  # same steps for both arms
+        st = 1.0 / np.sqrt(sp.norm_K_sq)
+        x, log = psb.run_pdhgskip2(sp, np.zeros((n, n)), np.zeros(60 * 725 + 2 * n * n), None, st,
+                                   st, psb.SkipConfig(0.1, 0), 2000)
+        out[prec] = (x, psb.objective_tv(x, prob, guarded=False))
+    assert rel(out["fp32"][0], out["fp64"][0]) < 1e-4
+    assert abs(out["fp32"][1] - out["fp64"][1]) / abs(out["fp64"][1]) < 1e-5
