@@ -233,6 +233,19 @@ int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* 
                  double p, double alpha, int nonneg, int skip, int32_t* bad_iter, int use_graph,
                  double* elapsed_host, void* stream);
 
+/* PDHGSkip-2 / PDHG on the implicit splitting K = A (Radon), TV in the
+ * warm-started FGP prox with optional u >= 0 (problems.py:162-184,
+ * skip.py:117-150).  y: sinogram (n_angles*n_bins, dtype_outer);
+ * h, xbar: n*n (dtype_outer); z: n*n and q: 3*2*n*n FGP slots (dtype_fgp,
+ * q_warm in slot 0); p = 1 with all coins set is PDHG.  last_weight_host /
+ * prox_count_host are the TvProxState accounting (in/out). */
+int psb_ct_implicit_run(int dtype_outer, int dtype_fgp, const psb_radon_geom* geom, void* x,
+                        void* y, void* h, void* xbar, void* z, void* q, const void* b,
+                        const uint8_t* coins_host, int K, double sigma, double tau, double p,
+                        double alpha, int n_inner, int accelerated, int nonneg,
+                        double* last_weight_host, int64_t* prox_count_host, int32_t* bad_iter,
+                        int use_graph, double* elapsed_host, void* stream);
+
 /* ---- 3-D TV prox + ProxSkip for BASELINE config 5 -----
  * Volume (D, H, W) with dual channels (z, y, x), dual step 1/12 (pass it as
  * `step`), the 2-D reference algorithm otherwise.  Slots as in 2-D, each of

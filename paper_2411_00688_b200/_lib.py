@@ -79,6 +79,8 @@ SIGNATURES = {
                       _dbl, _i32, _vp],
     "psb_pdhg_run": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl, _dbl, _dbl, _dbl, _i32,
                      _i32, _vp, _i32, _vp, _vp],
+    "psb_ct_implicit_run": [_i32, _i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl,
+                            _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp],
     "psb_blur2d": [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _i32, _i32, _vp],
     "psb_blur_grad2d": [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _vp],
     "psb_proxskip_deblur_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp,

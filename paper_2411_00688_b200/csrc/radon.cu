@@ -269,6 +269,67 @@ __global__ void pdhg_dual_tv_kernel(int n, const T* __restrict__ xbar, T* __rest
   yD[(int64_t)n * n + idx] = bb * sc;
 }
 
+// ---- implicit splitting K = A, TV inside the warm-started FGP prox --------
+// (problems.py:162-184 with skip.py:117-150).  y holds only
+// the sinogram block.  Coin iterations split around the FGP:
+//   pre : kty = A^T y ; t = x - sigma kty ; xhat = t + sigma h ;
+//         z = t + hc h (prox input, FGP precision) ; xbar <- xhat (parked)
+//   FGP : u = prox_{(sigma/p) alpha TV (+ u >= 0)}(z)   (fgp2d_run, warm q)
+//   post: x' = u ; h += ps (x' - xhat) ; xbar = 2 x' - x ; x = x'
+// Skipped iterations do pre + post in one pass with x' = xhat.
+template <class T, class TF>
+__global__ void ct_implicit_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
+                                          T* __restrict__ h, T* __restrict__ xbar,
+                                          TF* __restrict__ z, int coin, T sigma, T hc, T ps,
+                                          int32_t* bad, int k) {
+  const int n = G.n;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * n) return;
+  const T kty = pixel_gather(G, y, idx / n, idx % n);
+  const T xo = x[idx], ho = h[idx];
+  const T t = xo - sigma * kty;
+  const T xhat = t + sigma * ho;
+  if (coin) {
+    z[idx] = (TF)(t + hc * ho);
+    xbar[idx] = xhat;
+    return;
+  }
+  const T xn = xhat;
+  h[idx] = ho + ps * (xn - xhat);
+  x[idx] = xn;
+  xbar[idx] = T(2) * xn - xo;
+  if (bad && !isfinite(xn)) atomicMin(bad, k);
+}
+
+template <class T, class TF>
+__global__ void ct_implicit_post_kernel(int n, T* __restrict__ x, T* __restrict__ h,
+                                        T* __restrict__ xbar, const TF* __restrict__ z, TF* q,
+                                        int n_inner, int nonneg, T ps, int32_t* bad, int k) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * n) return;
+  const int64_t HW = (int64_t)n * n;
+  const int r = idx / n, c = idx % n;
+  const int slot = n_inner % 3;
+  const TF* qn = q + (int64_t)slot * 2 * HW;
+  const TF yy = qn[idx], yx = qn[HW + idx];
+  TF d = TF(0);  // div q (operators.py:66-70 order), then u = clamp(z + div q)  (tv.py:89)
+  if (r < n - 1) d = d + yy;
+  if (r > 0) d = d - qn[idx - n];
+  if (c < n - 1) d = d + yx;
+  if (c > 0) d = d - qn[HW + idx - 1];
+  TF u = z[idx] + d;
+  if (nonneg) u = u > TF(0) ? u : TF(0);
+  if (slot != 0) {  // q_warm lives in slot 0 between prox calls (tv.py:86-87)
+    q[idx] = yy;
+    q[HW + idx] = yx;
+  }
+  const T xo = x[idx], xhat = xbar[idx], xn = (T)u;
+  h[idx] = h[idx] + ps * (xn - xhat);
+  x[idx] = xn;
+  xbar[idx] = T(2) * xn - xo;
+  if (bad && !isfinite(xn)) atomicMin(bad, k);
+}
+
 inline int check_geo(const psb_radon_geom* g) {
   PSB_REQUIRE(g != nullptr && g->tables != nullptr, "radon: missing geometry tables");
   PSB_REQUIRE(g->n >= 2 && g->n_angles >= 1 && g->n_bins >= g->n && g->n_steps >= 2,
@@ -335,6 +396,148 @@ int pdhg_step(int dtype, const psb_radon_geom* g, void* x, void* y, void* h, voi
     return pdhg_step_t<double>(G, (double*)x, (double*)y, (double*)h, (double*)xbar,
                                (const double*)b, bad, k, coin, sigma, tau, hc, ps, alpha, nonneg, st);
   return fail(PSB_ERR_VALUE, "pdhg: unknown dtype");
+}
+
+int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
+              int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
+              int H, int W, int n_inner, int accelerated, int nonneg, double step,
+              const double* betas_host, cudaStream_t st);
+void fista_betas(int n, double* out);
+
+template <class T, class TF>
+int ct_implicit_step(const Geo& G, T* x, T* y, T* h, T* xbar, TF* z, TF* q, const T* b,
+                     const int32_t* one_d, const uint8_t* rep_d, int coin, double sigma, double tau,
+                     double hc, double ps, double weight, int n_inner, int accelerated, int nonneg,
+                     const double* betas, int32_t* bad, int k, cudaStream_t st) {
+  const int npx = G.n * G.n;
+  const int dtf = sizeof(TF) == 4 ? PSB_F32 : PSB_F64;
+  ct_implicit_primal_kernel<T, TF><<<(npx + 255) / 256, 256, 0, st>>>(
+      G, x, y, h, xbar, z, coin, (T)sigma, (T)hc, (T)ps, bad, k);
+  PSB_LAUNCHED("ct_implicit_primal");
+  if (coin) {
+    if (int rc = fgp2d_run(dtf, z, npx, q, 6LL * npx, one_d, 1, weight, nullptr, 0, rep_d, G.n, G.n,
+                           n_inner, accelerated, nonneg, 0.125, betas, st))
+      return rc;
+    ct_implicit_post_kernel<T, TF><<<(npx + 255) / 256, 256, 0, st>>>(
+        G.n, x, h, xbar, z, q, n_inner, nonneg, (T)ps, bad, k);
+    PSB_LAUNCHED("ct_implicit_post");
+  }
+  pdhg_dual_fid_kernel<T><<<(G.na * G.nb + 7) / 8, 256, 0, st>>>(G, xbar, y, b, (T)tau);
+  PSB_LAUNCHED("pdhg_dual_fid");
+  return PSB_OK;
+}
+
+int ct_implicit_run(int dto, int dtf, const psb_radon_geom* g, void* x, void* y, void* h,
+                    void* xbar, void* z, void* q, const void* b, const uint8_t* coins_host, int K,
+                    double sigma, double tau, double p, double alpha, int n_inner, int accelerated,
+                    int nonneg, double* last_weight, int64_t* prox_count, int32_t* bad,
+                    int use_graph, double* elapsed, cudaStream_t user) {
+  if (int rc = check_geo(g)) return rc;
+  PSB_REQUIRE(sigma > 0 && tau > 0, "pdhg: steps must be positive");
+  PSB_REQUIRE(p > 0 && p <= 1, "SkipConfig: p must be in (0, 1]");
+  PSB_REQUIRE(alpha > 0, "build_tv_saddle_implicit: alpha must be positive");
+  PSB_REQUIRE(n_inner >= 1, "TvProxState: inner_iters must be >= 1");
+  PSB_REQUIRE((dto == PSB_F32 || dto == PSB_F64) && (dtf == PSB_F32 || dtf == PSB_F64) &&
+                  !(dto == PSB_F32 && dtf == PSB_F64),
+              "ct implicit: unsupported precision pair");
+  if (K <= 0) return PSB_OK;
+  Geo G = make_geo(g);
+  const double hc = sigma - sigma / p;       // skip.py:133
+  const double ps = p / sigma;               // skip.py:145
+  const double weight = (sigma / p) * alpha; // prox_g(u, sigma/p) -> tv_prox(u, step*alpha)
+  // reprojection flag of the first prox call of the run (tv.py:68-69)
+  uint8_t rep_h[2] = {0, 0};
+  int first_coin = -1;
+  for (int k = 0; k < K; ++k)
+    if (coins_host[k]) {
+      first_coin = k;
+      break;
+    }
+  if (first_coin >= 0) {
+    rep_h[1] = (!std::isnan(*last_weight) && *last_weight != weight) ? 1 : 0;
+    *last_weight = weight;
+  }
+  for (int k = 0; k < K; ++k) *prox_count += coins_host[k] ? 1 : 0;
+  std::vector<double> beta(n_inner, 0.0);
+  if (accelerated) fista_betas(n_inner, beta.data());
+  int32_t* d_small = nullptr;  // [0] = active index 0, then two rep bytes
+  PSB_CUDA(cudaMalloc(&d_small, 16));
+  const int32_t zero = 0;
+  cudaMemcpy(d_small, &zero, sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(reinterpret_cast<uint8_t*>(d_small) + 8, rep_h, 2, cudaMemcpyHostToDevice);
+  const uint8_t* rep_plain = reinterpret_cast<const uint8_t*>(d_small) + 8;
+  const uint8_t* rep_first = rep_plain + 1;
+
+  cudaStream_t st = user, priv = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  int rc = PSB_OK;
+  if (use_graph) {
+    PSB_CUDA(cudaStreamCreateWithFlags(&priv, cudaStreamNonBlocking));
+    PSB_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    PSB_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    PSB_CUDA(cudaEventRecord(ev_in, user));
+    PSB_CUDA(cudaStreamWaitEvent(priv, ev_in, 0));
+    st = priv;
+    PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  }
+  const unsigned rf = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+  std::vector<cudaEvent_t> evs;
+  if (elapsed) {
+    evs.resize(K + 1, nullptr);
+    for (auto& e : evs) cudaEventCreate(&e);
+    cudaEventRecordWithFlags(evs[0], st, rf);
+  }
+  for (int k = 0; k < K && rc == PSB_OK; ++k) {
+    const int coin = coins_host[k] ? 1 : 0;
+    const uint8_t* rep_d = k == first_coin ? rep_first : rep_plain;
+    if (dto == PSB_F64 && dtf == PSB_F64)
+      rc = ct_implicit_step<double, double>(G, (double*)x, (double*)y, (double*)h, (double*)xbar,
+                                            (double*)z, (double*)q, (const double*)b, d_small,
+                                            rep_d, coin, sigma, tau, hc, ps, weight, n_inner,
+                                            accelerated, nonneg, beta.data(), bad, k, st);
+    else if (dto == PSB_F64)
+      rc = ct_implicit_step<double, float>(G, (double*)x, (double*)y, (double*)h, (double*)xbar,
+                                           (float*)z, (float*)q, (const double*)b, d_small, rep_d,
+                                           coin, sigma, tau, hc, ps, weight, n_inner, accelerated,
+                                           nonneg, beta.data(), bad, k, st);
+    else
+      rc = ct_implicit_step<float, float>(G, (float*)x, (float*)y, (float*)h, (float*)xbar,
+                                          (float*)z, (float*)q, (const float*)b, d_small, rep_d,
+                                          coin, sigma, tau, hc, ps, weight, n_inner, accelerated,
+                                          nonneg, beta.data(), bad, k, st);
+    if (elapsed) cudaEventRecordWithFlags(evs[k + 1], st, rf);
+  }
+  if (use_graph) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (rc == PSB_OK && e != cudaSuccess) rc = fail(PSB_ERR_CUDA, "ct implicit graph capture failed");
+    if (rc == PSB_OK && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, "ct implicit graph instantiate failed");
+    if (rc == PSB_OK && cudaGraphLaunch(exec, st) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, "ct implicit graph launch failed");
+    cudaEventRecord(ev_out, st);
+    cudaStreamWaitEvent(user, ev_out, 0);
+    cudaStreamSynchronize(user);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_out);
+    cudaStreamDestroy(priv);
+  }
+  if (elapsed) {
+    cudaStreamSynchronize(user);
+    for (int k = 0; k < K; ++k) {
+      float ms = 0.f;
+      if (rc == PSB_OK && cudaEventElapsedTime(&ms, evs[0], evs[k + 1]) == cudaSuccess)
+        elapsed[k] = ms * 1e-3;
+      else
+        elapsed[k] = std::nan(""), (void)cudaGetLastError();
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+  cudaFree(d_small);  // synchronises the device: no launch outlives the tables
+  return rc;
 }
 
 }  // namespace psb
@@ -421,6 +624,18 @@ int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* 
     for (auto e : evs) cudaEventDestroy(e);
   }
   return rc;
+}
+
+int psb_ct_implicit_run(int dtype_outer, int dtype_fgp, const psb_radon_geom* geom, void* x,
+                        void* y, void* h, void* xbar, void* z, void* q, const void* b,
+                        const uint8_t* coins_host, int K, double sigma, double tau, double p,
+                        double alpha, int n_inner, int accelerated, int nonneg,
+                        double* last_weight_host, int64_t* prox_count_host, int32_t* bad_iter,
+                        int use_graph, double* elapsed_host, void* stream) {
+  return psb::ct_implicit_run(dtype_outer, dtype_fgp, geom, x, y, h, xbar, z, q, b, coins_host, K,
+                              sigma, tau, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
+                              prox_count_host, bad_iter, use_graph, elapsed_host,
+                              psb::as_stream(stream));
 }
 
 }  // extern "C"

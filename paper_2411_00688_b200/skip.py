@@ -250,7 +250,13 @@ def run_pdhgskip2(problem, x0, y0, h0, sigma, tau, skip, iters, log=None):
     _check_step_rule(sigma, tau, problem.norm_K_sq)
     fused = getattr(problem, "_fused", None)
     if fused is not None and np.isscalar(sigma) and np.isscalar(tau):
-        return _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, "pdhgskip2")
+        if fused["kind"] == "ct_implicit":
+            if log is None or log.passive:
+                return _ct_implicit_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log,
+                                          "pdhgskip2")
+        else:
+            return _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log,
+                                      "pdhgskip2")
     log = _ensure_log(log)
     log.start(AR.is_host(x0))
     p = skip.p
@@ -279,6 +285,48 @@ def run_pdhgskip2(problem, x0, y0, h0, sigma, tau, skip, iters, log=None):
         _check_finite(x, k, "pdhgskip2")
         if log.observe(k + 1, x, prox_count, theta):
             break
+    return AR.like(x, x0), log
+
+
+def _ct_implicit_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, use_graph=True):
+    """Whole PDHGSkip-2 / PDHG run on the implicit CT saddle problem inside the
+    native driver (psb_ct_implicit_run): Radon gather + outer update, FGP prox
+    on coin iterations, forward projection + fidelity dual prox -- no host
+    round trip per iteration.  Passive logs only (observing logs step through
+    the generic driver with the same kernels)."""
+    f = problem._fused
+    st = f["tv_state"]
+    dt = f["dtype"]
+    log = _ensure_log(log)
+    log.start(AR.is_host(x0))
+    g, _ = f["geom"].device()
+    n = g.n
+    x = AR.to_dev(x0, dt).clone()
+    y = AR.to_dev(y0, dt).clone().reshape(-1)
+    h = AR.to_dev(h0, dt).clone() if h0 is not None else torch.zeros_like(x)
+    xbar = torch.empty_like(x)
+    z = torch.empty((n, n), dtype=st.dtype, device="cuda")
+    p = skip.p if skip is not None else 1.0
+    coins = skip.coins(iters) if skip is not None else np.ones(iters, dtype=np.uint8)
+    lw = np.array([np.nan if st.last_weight is None else st.last_weight], dtype=np.float64)
+    pc = np.zeros(1, dtype=np.int64)
+    bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
+    elapsed = np.zeros(max(iters, 1), dtype=np.float64)
+    base_inner = st.total_inner_iterations
+    vp = L.C.c_void_p
+    L.call("psb_ct_implicit_run", L.dcode(dt), L.dcode(st.dtype), L.C.byref(g), L.ptr(x), L.ptr(y),
+           L.ptr(h), L.ptr(xbar), L.ptr(z), L.ptr(st.slots), L.ptr(f["b_dev"]),
+           coins.ctypes.data_as(vp), iters, float(sigma), float(tau), float(p), float(f["alpha"]),
+           st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)), lw.ctypes.data_as(vp),
+           pc.ctypes.data_as(vp), L.ptr(bad), int(bool(use_graph)), elapsed.ctypes.data_as(vp),
+           L.stream())
+    k_bad = int(bad.item())
+    if k_bad != INT32_MAX:
+        raise DivergenceError(k_bad, algo)
+    st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
+    st.total_inner_iterations += st.inner_iters * int(pc[0])
+    _finish_passive(log, coins[:iters], elapsed, base_inner, st.inner_iters)
+    log.y_final = y
     return AR.like(x, x0), log
 
 

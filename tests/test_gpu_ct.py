@@ -181,3 +181,51 @@ def test_config3_fp32_tent_gather_full_run_vs_fp64():
         out[prec] = (x, psb.objective_tv(x, prob, guarded=False))
     assert rel(out["fp32"][0], out["fp64"][0]) < 1e-4
     assert abs(out["fp32"][1] - out["fp64"][1]) / abs(out["fp64"][1]) < 1e-5
+
+
+def test_ct_implicit_native_driver_matches_reference_fp64(golden):
+    """The native implicit driver (psb_ct_implicit_run, passive log) reaches the
+    reference's final iterate and the same TvProxState accounting."""
+    g = golden
+    R = psb.radon_map(psb.RadonGeometry(image_side=16, n_angles=7, n_bins=23))
+    prob = psb.build_tv_saddle_implicit(R, g["ct_b"], 0.05, nonneg=True, inner_budget=6,
+                                        precision="fp64")
+    sp = prob.saddle_problem
+    sp.norm_K_sq = float(g["cti_nsq"])
+    s = 1.0 / np.sqrt(sp.norm_K_sq)
+    x, log = psb.run_pdhgskip2(sp, np.zeros((16, 16)), np.zeros((7, 23)), None, s, s,
+                               psb.SkipConfig(0.3, 1), 12)
+    np.testing.assert_allclose(x, g["cti_skip_traj"][-1], rtol=1e-10, atol=1e-12)
+    np.testing.assert_array_equal([r.prox_applied for r in log.records], g["cti_skip_flags"])
+    n_prox = int(np.sum(g["cti_skip_flags"]))
+    assert prob.tv_state.total_inner_iterations == 6 * n_prox
+    assert prob.tv_state.last_weight == (s / 0.3) * 0.05
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-12), ("mixed", 1e-4), ("fp32", 1e-4)])
+def test_ct_implicit_native_vs_oracle(prec, tol):
+    """64^2 implicit CT (nonneg, PDHGSkip-2 p=0.2, 60 iterations, FGP-20)
+    against the oracle; then PDHG (p=1) through run_pdhg on the same driver."""
+    n, na, nb = 64, 30, 91
+    u_true = phantoms.shepp_like(n, 6, np.random.default_rng(3))
+    ref_op = oc.radon_op(n, na, nb)
+    sino = ref_op.fwd(u_true)
+    b = phantoms.add_noise(sino, 0.01 * sino.max(), 3)
+    R = psb.radon_map(psb.RadonGeometry(image_side=n, n_angles=na, n_bins=nb))
+    for p, iters in ((0.2, 60), (1.0, 25)):
+        prob = psb.build_tv_saddle_implicit(R, b, 0.05, nonneg=True, inner_budget=20,
+                                            precision=prec)
+        sp = prob.saddle_problem
+        pr = oc.make_saddle_implicit(ref_op, b, 0.05, nonneg=True, inner=20)
+        nsq = pr.K_nsq
+        sp.norm_K_sq = nsq
+        st = 1.0 / np.sqrt(nsq)
+        if p < 1.0:
+            x, log = psb.run_pdhgskip2(sp, np.zeros((n, n)), np.zeros((na, nb)), None, st, st,
+                                       psb.SkipConfig(p, 4), iters)
+            assert log.records[-1].prox_count == int(np.sum(oc.coin_draws(p, 4, iters)))
+        else:
+            x, _ = psb.run_pdhg(sp, np.zeros((n, n)), np.zeros((na, nb)), st, st, iters)
+        xr = oc.pdhgskip2(pr.K, pr.prox_fstar, pr.prox_g, nsq, np.zeros((n, n)),
+                          np.zeros((na, nb)), None, st, st, p, 4, iters)[0]
+        assert rel(x, xr) < tol, (p, rel(x, xr))

@@ -117,6 +117,44 @@ def cfg3():
     return out
 
 
+def cfg3i(inner=50, K=2000, p=0.1):
+    """PDHGSkip-2 on the implicit CT saddle problem (K = A,
+    TV in the warm-started FGP prox with u >= 0) at config-3 geometry, through
+    the native driver psb_ct_implicit_run; PDHG (p = 1) alongside."""
+    n = 512
+    u = phantoms.shepp_like(n, 10, np.random.default_rng(0))
+    R = psb.radon_map(psb.RadonGeometry(image_side=n, n_angles=60, n_bins=725))
+    s = R.forward(u)
+    b = phantoms.add_noise(s, 0.01 * s.max(), 0)
+    out = {"config": "3i", "inner": inner, "p": p, "iters": K}
+    coins = psb.SkipConfig(p, 0).coins(K)
+    for prec in ("mixed", "fp32"):
+        prob = psb.build_tv_saddle_implicit(R, b, 0.05, nonneg=True, inner_budget=inner,
+                                            precision=prec)
+        nsq = prob.saddle_problem.norm_K_sq
+
+        def run():
+            pr = psb.build_tv_saddle_implicit(R, b, 0.05, nonneg=True, inner_budget=inner,
+                                              precision=prec)
+            pr.saddle_problem.norm_K_sq = nsq
+            st = 1.0 / np.sqrt(nsq)
+            run.x, _ = psb.run_pdhgskip2(pr.saddle_problem, np.zeros((n, n)), np.zeros((60, 725)),
+                                         None, st, st, psb.SkipConfig(p, 0), K)
+        t, _ = timed(run, reps=2)
+
+        def run_p():
+            pr = psb.build_tv_saddle_implicit(R, b, 0.05, nonneg=True, inner_budget=inner,
+                                              precision=prec)
+            pr.saddle_problem.norm_K_sq = nsq
+            st = 1.0 / np.sqrt(nsq)
+            run_p.x, _ = psb.run_pdhg(pr.saddle_problem, np.zeros((n, n)), np.zeros((60, 725)),
+                                      st, st, K // 10)
+        tp, _ = timed(run_p, reps=1)
+        out[prec] = {"Anorm_sq": nsq, "pdhgskip2_it_s": K / t, "pdhg_it_s": (K // 10) / tp,
+                     "prox_calls": int(coins.sum())}
+    return out
+
+
 def cfg5(side=1024, K=200, inner=20):
     torch.manual_seed(0)
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -162,7 +200,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,5")
     ap.add_argument("--side5", type=int, default=1024)
     args = ap.parse_args()
-    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "5": lambda: cfg5(args.side5)}
+    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "3i": cfg3i, "5": lambda: cfg5(args.side5)}
     for c in args.configs.split(","):
         r = fns[c]()
         print(json.dumps(r), flush=True)
