@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define PSB_ABI_VERSION 1
+#define PSB_ABI_VERSION 2
 
 #define PSB_OK 0
 #define PSB_ERR_VALUE 1    /* maps to ValueError */
@@ -134,6 +134,15 @@ int psb_dot(int dtype, const void* a, const void* b, int64_t n, int64_t len, dou
             void* stream);
 int psb_tv2d(int dtype, const void* u, int64_t n, int H, int W, double* out, void* stream);
 int psb_count_nonfinite(int dtype, const void* a, int64_t count, double* out, void* stream);
+/* Batched logging reductions over an iterate history a[n][len] (device
+ * IterationLog): psb_sumsq_bcast = sum((a_p - b)^2) with one
+ * shared b (rel_error against the reference solution, tensor.py:42-51, and the
+ * identity fidelity of objective_tv, problems.py:187-192); psb_count_below =
+ * number of entries < thresh (the nonneg guard of objective_tv). */
+int psb_sumsq_bcast(int dtype, const void* a, const void* b, int64_t n, int64_t len, double* out,
+                    void* stream);
+int psb_count_below(int dtype, const void* a, int64_t n, int64_t len, double thresh, double* out,
+                    void* stream);
 
 /* ---- ProxSkip outer step, skip.py:46-79 -------------------------------------
  * State x, h (dtype_outer) and prox input z (dtype_fgp), all (n, H, W).
@@ -182,13 +191,18 @@ int psb_skip_chain(int dtype_outer, int dtype_fgp, void* x, const void* b, const
  *   (IterationLog.elapsed_s, solvers.py:84-86), from CUDA events.
  *   fgp_time_host (nullable, host double[K]) receives the device time of the
  *   FGP inner-iteration burst of each outer iteration (0 when no coin fired),
- *   for the benchmark's roofline accounting. */
+ *   for the benchmark's roofline accounting.
+ *   x_hist (nullable, device, K*n*H*W of dtype_outer) receives the iterate
+ *   after every outer iteration (device IterationLog; forces the streaming
+ *   path, since the cluster path defers skipped iterations).  The PDHG and
+ *   implicit-CT drivers below take the same x_hist (K*n*n). */
 int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
                              void* z, void* q, int64_t n, int H, int W, const uint8_t* coins_host,
                              int K, double gamma, double p, double alpha, int n_inner,
                              int accelerated, int nonneg, double* last_weight_host,
                              int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
-                             double* elapsed_host, double* fgp_time_host, void* stream);
+                             double* elapsed_host, double* fgp_time_host, void* x_hist,
+                             void* stream);
 
 /* ---- parallel-beam projector, operators.py:189-292 (matrix-free) ------------
  * Geometry of RadonGeometry (operators.py:189-215) plus the sample lattice of
@@ -231,7 +245,7 @@ int psb_pdhg_step(int dtype, const psb_radon_geom* geom, void* x, void* y, void*
 int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
                  const void* b, const uint8_t* coins_host, int K, double sigma, double tau,
                  double p, double alpha, int nonneg, int skip, int32_t* bad_iter, int use_graph,
-                 double* elapsed_host, void* stream);
+                 double* elapsed_host, void* x_hist, void* stream);
 
 /* PDHGSkip-2 / PDHG on the implicit splitting K = A (Radon), TV in the
  * warm-started FGP prox with optional u >= 0 (problems.py:162-184,
@@ -244,7 +258,7 @@ int psb_ct_implicit_run(int dtype_outer, int dtype_fgp, const psb_radon_geom* ge
                         const uint8_t* coins_host, int K, double sigma, double tau, double p,
                         double alpha, int n_inner, int accelerated, int nonneg,
                         double* last_weight_host, int64_t* prox_count_host, int32_t* bad_iter,
-                        int use_graph, double* elapsed_host, void* stream);
+                        int use_graph, double* elapsed_host, void* x_hist, void* stream);
 
 /* ---- 3-D TV prox + ProxSkip for BASELINE config 5 -----
  * Volume (D, H, W) with dual channels (z, y, x), dual step 1/12 (pass it as
@@ -281,7 +295,8 @@ int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void*
                             const uint8_t* coins_host, int K, double gamma, double p, double alpha,
                             int n_inner, int accelerated, int nonneg, double* last_weight_host,
                             int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
-                            double* elapsed_host, double* fgp_time_host, void* stream);
+                            double* elapsed_host, double* fgp_time_host, void* x_hist,
+                            void* stream);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,8 @@ SIGNATURES = {
     "psb_sumsq": [_i32, _vp, _vp, _i64, _i64, _vp, _vp],
     "psb_dot": [_i32, _vp, _vp, _i64, _i64, _vp, _vp],
     "psb_tv2d": [_i32, _vp, _i64, _i32, _i32, _vp, _vp],
+    "psb_sumsq_bcast": [_i32, _vp, _vp, _i64, _i64, _vp, _vp],
+    "psb_count_below": [_i32, _vp, _i64, _i64, _dbl, _vp, _vp],
     "psb_count_nonfinite": [_i32, _vp, _i64, _vp, _vp],
     "psb_proxskip_pre": [_i32, _i32, _vp, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _vp,
                          _i32, _vp],
@@ -66,7 +68,7 @@ SIGNATURES = {
                           _i32, _i32, _dbl, _dbl, _vp, _i32, _vp],
     "psb_proxskip_denoise_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp,
                                  _i32, _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32,
-                                 _vp, _vp, _vp],
+                                 _vp, _vp, _vp, _vp],
     "psb_cluster_max_active": [_vp],
     "psb_fgp3d_iter": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32,
                        _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
@@ -78,14 +80,14 @@ SIGNATURES = {
     "psb_pdhg_step": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _dbl, _dbl, _dbl, _dbl,
                       _dbl, _i32, _vp],
     "psb_pdhg_run": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl, _dbl, _dbl, _dbl, _i32,
-                     _i32, _vp, _i32, _vp, _vp],
+                     _i32, _vp, _i32, _vp, _vp, _vp],
     "psb_ct_implicit_run": [_i32, _i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl,
-                            _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp],
+                            _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp],
     "psb_blur2d": [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _i32, _i32, _vp],
     "psb_blur_grad2d": [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _vp],
     "psb_proxskip_deblur_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp,
                                 _vp, _i32, _i32, _vp, _i32, _dbl, _dbl, _dbl, _i32, _i32, _i32,
-                                _vp, _vp, _vp, _i32, _vp, _vp, _vp],
+                                _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
 }
 
 

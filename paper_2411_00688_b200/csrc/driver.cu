@@ -70,7 +70,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                     void* q, int64_t n, int H, int W, const uint8_t* coins_host, int K,
                     double gamma, double p, double alpha, int n_inner, int accelerated, int nonneg,
                     double* last_weight, int64_t* prox_count, int32_t* bad, int use_graph,
-                    double* elapsed, double* fgp_time, cudaStream_t user_stream) {
+                    double* elapsed, double* fgp_time, void* x_hist, cudaStream_t user_stream) {
   PSB_REQUIRE(fid.kind == 0 || n == 1, "proxskip run: a blur fidelity runs one problem at a time");
   PSB_REQUIRE(gamma > 0, "run_proxskip: gamma must be positive");
   PSB_REQUIRE(p > 0 && p <= 1, "SkipConfig: p must be in (0, 1]");
@@ -118,8 +118,11 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   // problems with an fp32 FGP.  Skipped iterations are deferred per problem
   // and executed in registers at the next prox call / the final flush.
   const char* no_cluster = std::getenv("PSB_NO_CLUSTER");
+  // (an iterate history needs x materialised every iteration: streaming path)
   const bool use_cluster = fid.kind == 0 && dtf == PSB_F32 && cluster_shape_ok(H, W) &&
-                           n_inner <= 1024 && !(no_cluster && no_cluster[0] == '1');
+                           n_inner <= 1024 && !(no_cluster && no_cluster[0] == '1') &&
+                           x_hist == nullptr;
+  const size_t x_bytes = (size_t)n * HW * (dto == PSB_F32 ? 4 : 8);
   std::vector<int32_t> pend, kfirst, fl_pend(n, 0), fl_kfirst(n, 0);
   std::vector<float> beta_f(n_inner, 0.f);
   if (use_cluster) {
@@ -200,6 +203,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   int rc = PSB_OK;
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
     if (elapsed && k > 0) cudaEventRecordWithFlags(evs[k], st, rec_flags);
+    if (x_hist && k > 0 && rc == PSB_OK)  // iterate of outer iteration k-1 (device IterationLog)
+      if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (k - 1) * x_bytes, x, x_bytes,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        rc = fail(PSB_ERR_CUDA, "x history copy failed");
     if (use_cluster) {
       const int na = (int)(off[k + 1] - off[k]);
       if (na == 0) continue;
@@ -234,6 +241,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   if (use_cluster && rc == PSB_OK)  // remaining deferred skip iterations
     rc = skip_flush(dto, x, b, h, static_cast<const int32_t*>(d_flp.p),
                     static_cast<const int32_t*>(d_flk.p), n, HW, gamma, bad, st);
+  if (x_hist && rc == PSB_OK)
+    if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, x, x_bytes,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, "x history copy failed");
   if (elapsed && rc == PSB_OK) cudaEventRecordWithFlags(evs[K], st, rec_flags);
   if (use_graph) {
     cudaGraph_t graph = nullptr;
@@ -299,12 +310,12 @@ extern "C" int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x,
                                         double alpha, int n_inner, int accelerated, int nonneg,
                                         double* last_weight_host, int64_t* prox_count_host,
                                         int32_t* bad_iter, int use_graph, double* elapsed_host,
-                                        double* fgp_time_host, void* stream) {
+                                        double* fgp_time_host, void* x_hist, void* stream) {
   psb::Fidelity fid;
   return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
                               gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
                               prox_count_host, bad_iter, use_graph, elapsed_host, fgp_time_host,
-                              psb::as_stream(stream));
+                              x_hist, psb::as_stream(stream));
 }
 
 extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void* b,
@@ -314,7 +325,8 @@ extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, 
                                        double gamma, double p, double alpha, int n_inner,
                                        int accelerated, int nonneg, double* last_weight_host,
                                        int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
-                                       double* elapsed_host, double* fgp_time_host, void* stream) {
+                                       double* elapsed_host, double* fgp_time_host, void* x_hist,
+                                       void* stream) {
   psb::Fidelity fid;
   fid.kind = 1;
   fid.taps2d = taps2d;
@@ -326,5 +338,5 @@ extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, 
   return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, 1, H, W, coins_host, K,
                               gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
                               prox_count_host, bad_iter, use_graph, elapsed_host, fgp_time_host,
-                              psb::as_stream(stream));
+                              x_hist, psb::as_stream(stream));
 }

@@ -33,16 +33,17 @@ __device__ __forceinline__ double block_sum(double v) {
   return r;  // valid in thread 0
 }
 
-enum Op { SUMSQ = 0, DOT = 1, NONFINITE = 2 };
+enum Op { SUMSQ = 0, DOT = 1, NONFINITE = 2, BELOW = 3 };
 
 template <class T, int OP>
 __global__ void __launch_bounds__(RB) elem_reduce(const T* __restrict__ a, const T* __restrict__ b,
-                                                  int64_t len, int chunks, double* __restrict__ part) {
+                                                  int64_t len, int64_t bstride, double thr,
+                                                  int chunks, double* __restrict__ part) {
   const int64_t p = blockIdx.y;
   const int64_t per = (len + chunks - 1) / chunks;
   const int64_t lo = blockIdx.x * per, hi = min(len, lo + per);
   const T* ap = a + p * len;
-  const T* bp = b ? b + p * len : nullptr;
+  const T* bp = b ? b + p * bstride : nullptr;
   double acc = 0.0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += RB) {
     const double av = (double)ap[i];
@@ -51,8 +52,10 @@ __global__ void __launch_bounds__(RB) elem_reduce(const T* __restrict__ a, const
       acc += d * d;
     } else if (OP == DOT) {
       acc += av * (double)bp[i];
-    } else {
+    } else if (OP == NONFINITE) {
       acc += isfinite(av) ? 0.0 : 1.0;
+    } else {
+      acc += av < thr ? 1.0 : 0.0;
     }
   }
   const double r = block_sum(acc);
@@ -118,14 +121,17 @@ int two_pass(int64_t n, int64_t len, double* out, cudaStream_t st, Launch launch
 
 template <int OP>
 int elem(int dtype, const void* a, const void* b, int64_t n, int64_t len, double* out,
-         cudaStream_t st) {
+         cudaStream_t st, int64_t bstride = -1, double thr = 0.0) {
+  if (bstride < 0) bstride = len;
   if (dtype == PSB_F32)
     return two_pass(n, len, out, st, [&](dim3 g, int chunks, double* part) {
-      elem_reduce<float, OP><<<g, RB, 0, st>>>((const float*)a, (const float*)b, len, chunks, part);
+      elem_reduce<float, OP><<<g, RB, 0, st>>>((const float*)a, (const float*)b, len, bstride, thr,
+                                               chunks, part);
     });
   if (dtype == PSB_F64)
     return two_pass(n, len, out, st, [&](dim3 g, int chunks, double* part) {
-      elem_reduce<double, OP><<<g, RB, 0, st>>>((const double*)a, (const double*)b, len, chunks, part);
+      elem_reduce<double, OP><<<g, RB, 0, st>>>((const double*)a, (const double*)b, len, bstride,
+                                                thr, chunks, part);
     });
   return fail(PSB_ERR_VALUE, "reduce: unknown dtype");
 }
@@ -145,6 +151,17 @@ int psb_dot(int dtype, const void* a, const void* b, int64_t n, int64_t len, dou
             void* stream) {
   PSB_REQUIRE(b != nullptr, "dot: second operand missing");
   return psb::elem<psb::DOT>(dtype, a, b, n, len, out, psb::as_stream(stream));
+}
+
+int psb_sumsq_bcast(int dtype, const void* a, const void* b, int64_t n, int64_t len, double* out,
+                    void* stream) {
+  PSB_REQUIRE(b != nullptr, "sumsq_bcast: shared operand missing");
+  return psb::elem<psb::SUMSQ>(dtype, a, b, n, len, out, psb::as_stream(stream), 0);
+}
+
+int psb_count_below(int dtype, const void* a, int64_t n, int64_t len, double thresh, double* out,
+                    void* stream) {
+  return psb::elem<psb::BELOW>(dtype, a, nullptr, n, len, out, psb::as_stream(stream), len, thresh);
 }
 
 int psb_count_nonfinite(int dtype, const void* a, int64_t count, double* out, void* stream) {

@@ -26,6 +26,7 @@ from . import _lib as L
 from . import tensor as T
 from .errors import DivergenceError
 from .operators import apply_adjoint, apply_forward
+from .devlog import device_loggable, run_logged
 from .solvers import IterationLog, RunRecord, _check_finite, _check_step_rule, _dev, _ensure_log
 
 INT32_MAX = 2 ** 31 - 1
@@ -72,7 +73,8 @@ def run_proxskip(problem, x0, h0, gamma, skip, iters, log=None, *, use_graph=Non
         raise ValueError("run_proxskip: gamma must be positive")
     log = _ensure_log(log)
     fused = getattr(problem, "_fused", None)
-    if fused is not None and fused.get("kind") in ("denoise", "deblur") and log.passive:
+    if (fused is not None and fused.get("kind") in ("denoise", "deblur")
+            and (log.passive or device_loggable(log))):
         return _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph)
     log.start(AR.is_host(x0))
     p = skip.p
@@ -154,6 +156,33 @@ def _betas(n):
     return out
 
 
+def _tv_snapshot(st, *tensors):
+    return ([t.clone() if t is not None else None for t in tensors], st.slots.clone() if st else None,
+            st.last_weight if st else None, st.total_inner_iterations if st else 0)
+
+
+def _tv_restore(snap, st, *tensors):
+    saved, slots, lw, tot = snap
+    for t, v in zip(tensors, saved):
+        if t is not None:
+            t.copy_(v)
+    if st is not None:
+        st.slots.copy_(slots)
+        st.last_weight = lw
+        st.total_inner_iterations = tot
+
+
+def _drive(log, iters, coins, shape, dtype, chunk, state, tensors, base_inner, inner_per_prox):
+    """Passive log: one native call for the whole run.  Device-loggable log:
+    chunked native calls with an iterate history (devlog.run_logged)."""
+    if log.passive:
+        el = chunk(0, coins, None)
+        _finish_passive(log, coins[:iters], el, base_inner, inner_per_prox)
+        return
+    run_logged(log, iters, coins, shape, dtype, chunk, lambda: _tv_snapshot(state, *tensors),
+               lambda sn: _tv_restore(sn, state, *tensors), inner_per_prox, base_inner)
+
+
 def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph,
                        fgp_time=None):
     """Whole run inside the native driver (psb_proxskip_denoise_run /
@@ -166,39 +195,47 @@ def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_grap
     h = AR.to_dev(h0, dt).clone() if h0 is not None else torch.zeros_like(x)
     z = torch.empty((H, W), dtype=st.dtype, device="cuda")
     coins = skip.coins(iters)
-    lw = np.array([np.nan if st.last_weight is None else st.last_weight], dtype=np.float64)
-    pc = np.zeros(1, dtype=np.int64)
     bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
-    elapsed = np.zeros(max(iters, 1), dtype=np.float64)
     if use_graph is None:
         use_graph = H * W <= 1024 * 1024
     base_inner = st.total_inner_iterations
     vp = L.C.c_void_p
-    ft = fgp_time.ctypes.data_as(vp) if fgp_time is not None else None
-    common_tail = (coins.ctypes.data_as(vp), iters, float(gamma), float(skip.p),
-                   float(problem.alpha), st.inner_iters, int(bool(st.accelerated)),
-                   int(bool(st.nonneg)), lw.ctypes.data_as(vp), pc.ctypes.data_as(vp), L.ptr(bad),
-                   int(bool(use_graph)), elapsed.ctypes.data_as(vp), ft, L.stream())
-    if fused["kind"] == "denoise":
-        L.call("psb_proxskip_denoise_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
-               L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), 1, H, W, *common_tail)
-    else:
+    if fused["kind"] == "deblur":
         ker = fused["kernel"]
         sep = bool(fused["separable"] and ker.factor is not None)
         w2 = np.ascontiguousarray(ker.weights, dtype=np.float64)
         w1 = np.ascontiguousarray(ker.factor if sep else np.zeros(1), dtype=np.float64)
         g = torch.empty_like(x)
         scratch = None if sep else torch.empty_like(x)
-        L.call("psb_proxskip_deblur_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
-               L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), L.ptr(g),
-               L.ptr(scratch), H, W, w2.ctypes.data_as(vp), w1.ctypes.data_as(vp), ker.size,
-               int(sep), *common_tail)
-    k_bad = int(bad.item())
-    if k_bad != INT32_MAX:
-        raise DivergenceError(k_bad, "proxskip")
-    st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
-    st.total_inner_iterations += st.inner_iters * int(pc[0])
-    _finish_passive(log, coins[:iters], elapsed, base_inner, st.inner_iters)
+
+    def chunk(k0, cc, hist):
+        cc = np.ascontiguousarray(cc, dtype=np.uint8)
+        K = len(cc)
+        lw = np.array([np.nan if st.last_weight is None else st.last_weight], dtype=np.float64)
+        pc = np.zeros(1, dtype=np.int64)
+        el = np.zeros(max(K, 1), dtype=np.float64)
+        bad.fill_(INT32_MAX)
+        ft = fgp_time.ctypes.data_as(vp) if (fgp_time is not None and hist is None) else None
+        tail = (cc.ctypes.data_as(vp), K, float(gamma), float(skip.p), float(problem.alpha),
+                st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)),
+                lw.ctypes.data_as(vp), pc.ctypes.data_as(vp), L.ptr(bad), int(bool(use_graph)),
+                el.ctypes.data_as(vp), ft, L.ptr(hist), L.stream())
+        if fused["kind"] == "denoise":
+            L.call("psb_proxskip_denoise_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
+                   L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), 1, H, W, *tail)
+        else:
+            L.call("psb_proxskip_deblur_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
+                   L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), L.ptr(g),
+                   L.ptr(scratch), H, W, w2.ctypes.data_as(vp), w1.ctypes.data_as(vp), ker.size,
+                   int(sep), *tail)
+        k_bad = int(bad.item())
+        if k_bad != INT32_MAX:
+            raise DivergenceError(k0 + k_bad, "proxskip")
+        st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
+        st.total_inner_iterations += st.inner_iters * int(pc[0])
+        return el
+
+    _drive(log, iters, coins, (H, W), dt, chunk, st, (x, h), base_inner, st.inner_iters)
     return AR.like(x, x0), log
 
 
@@ -251,7 +288,7 @@ def run_pdhgskip2(problem, x0, y0, h0, sigma, tau, skip, iters, log=None):
     fused = getattr(problem, "_fused", None)
     if fused is not None and np.isscalar(sigma) and np.isscalar(tau):
         if fused["kind"] == "ct_implicit":
-            if log is None or log.passive:
+            if log is None or log.passive or device_loggable(log):
                 return _ct_implicit_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log,
                                           "pdhgskip2")
         else:
@@ -292,8 +329,8 @@ def _ct_implicit_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
     """Whole PDHGSkip-2 / PDHG run on the implicit CT saddle problem inside the
     native driver (psb_ct_implicit_run): Radon gather + outer update, FGP prox
     on coin iterations, forward projection + fidelity dual prox -- no host
-    round trip per iteration.  Passive logs only (observing logs step through
-    the generic driver with the same kernels)."""
+    round trip per iteration.  Passive and device-loggable logs (devlog.py);
+    other observing logs step through the generic driver with the same kernels."""
     f = problem._fused
     st = f["tv_state"]
     dt = f["dtype"]
@@ -308,24 +345,31 @@ def _ct_implicit_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
     z = torch.empty((n, n), dtype=st.dtype, device="cuda")
     p = skip.p if skip is not None else 1.0
     coins = skip.coins(iters) if skip is not None else np.ones(iters, dtype=np.uint8)
-    lw = np.array([np.nan if st.last_weight is None else st.last_weight], dtype=np.float64)
-    pc = np.zeros(1, dtype=np.int64)
     bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
-    elapsed = np.zeros(max(iters, 1), dtype=np.float64)
     base_inner = st.total_inner_iterations
     vp = L.C.c_void_p
-    L.call("psb_ct_implicit_run", L.dcode(dt), L.dcode(st.dtype), L.C.byref(g), L.ptr(x), L.ptr(y),
-           L.ptr(h), L.ptr(xbar), L.ptr(z), L.ptr(st.slots), L.ptr(f["b_dev"]),
-           coins.ctypes.data_as(vp), iters, float(sigma), float(tau), float(p), float(f["alpha"]),
-           st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)), lw.ctypes.data_as(vp),
-           pc.ctypes.data_as(vp), L.ptr(bad), int(bool(use_graph)), elapsed.ctypes.data_as(vp),
-           L.stream())
-    k_bad = int(bad.item())
-    if k_bad != INT32_MAX:
-        raise DivergenceError(k_bad, algo)
-    st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
-    st.total_inner_iterations += st.inner_iters * int(pc[0])
-    _finish_passive(log, coins[:iters], elapsed, base_inner, st.inner_iters)
+
+    def chunk(k0, cc, hist):
+        cc = np.ascontiguousarray(cc, dtype=np.uint8)
+        K = len(cc)
+        lw = np.array([np.nan if st.last_weight is None else st.last_weight], dtype=np.float64)
+        pc = np.zeros(1, dtype=np.int64)
+        el = np.zeros(max(K, 1), dtype=np.float64)
+        bad.fill_(INT32_MAX)
+        L.call("psb_ct_implicit_run", L.dcode(dt), L.dcode(st.dtype), L.C.byref(g), L.ptr(x),
+               L.ptr(y), L.ptr(h), L.ptr(xbar), L.ptr(z), L.ptr(st.slots), L.ptr(f["b_dev"]),
+               cc.ctypes.data_as(vp), K, float(sigma), float(tau), float(p), float(f["alpha"]),
+               st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)),
+               lw.ctypes.data_as(vp), pc.ctypes.data_as(vp), L.ptr(bad), int(bool(use_graph)),
+               el.ctypes.data_as(vp), L.ptr(hist), L.stream())
+        k_bad = int(bad.item())
+        if k_bad != INT32_MAX:
+            raise DivergenceError(k0 + k_bad, algo)
+        st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
+        st.total_inner_iterations += st.inner_iters * int(pc[0])
+        return el
+
+    _drive(log, iters, coins, (n, n), dt, chunk, st, (x, y, h), base_inner, st.inner_iters)
     log.y_final = y
     return AR.like(x, x0), log
 
@@ -349,16 +393,23 @@ def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
     bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
     p = skip.p if is_skip else 1.0
     coins = skip.coins(iters) if is_skip else np.ones(iters, dtype=np.uint8)
-    if log.passive:
-        elapsed = np.zeros(max(iters, 1))
-        L.call("psb_pdhg_run", L.dcode(dt), L.C.byref(g), L.ptr(x), L.ptr(y), L.ptr(h), L.ptr(xbar),
-               L.ptr(f["b_dev"]), coins.ctypes.data_as(L.C.c_void_p), iters, float(sigma),
-               float(tau), float(p), float(f["alpha"]), int(bool(f["nonneg"])), int(is_skip),
-               L.ptr(bad), int(bool(use_graph)), elapsed.ctypes.data_as(L.C.c_void_p), L.stream())
-        k_bad = int(bad.item())
-        if k_bad != INT32_MAX:
-            raise DivergenceError(k_bad, algo)
-        _finish_passive(log, coins[:iters], elapsed, 0, 0)
+    if log.passive or device_loggable(log):
+        def chunk(k0, cc, hist):
+            cc = np.ascontiguousarray(cc, dtype=np.uint8)
+            K = len(cc)
+            el = np.zeros(max(K, 1))
+            bad.fill_(INT32_MAX)
+            L.call("psb_pdhg_run", L.dcode(dt), L.C.byref(g), L.ptr(x), L.ptr(y), L.ptr(h),
+                   L.ptr(xbar), L.ptr(f["b_dev"]), cc.ctypes.data_as(L.C.c_void_p), K,
+                   float(sigma), float(tau), float(p), float(f["alpha"]), int(bool(f["nonneg"])),
+                   int(is_skip), L.ptr(bad), int(bool(use_graph)), el.ctypes.data_as(L.C.c_void_p),
+                   L.ptr(hist), L.stream())
+            k_bad = int(bad.item())
+            if k_bad != INT32_MAX:
+                raise DivergenceError(k0 + k_bad, algo)
+            return el
+
+        _drive(log, iters, coins, tuple(x.shape), dt, chunk, None, (x, y, h), 0, 0)
     else:
         hc = sigma - sigma / p if is_skip else 0.0
         ps = p / sigma if is_skip else 0.0

@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(L.LIB, s), f"libpsb200.so does not export {s}"
         assert s in L.SIGNATURES, f"ctypes binding for {s} missing"
     assert set(L.SIGNATURES) == set(syms), "binding table and header disagree"
-    assert L.LIB.psb_abi_version() == 1
+    assert L.LIB.psb_abi_version() == 2
 
 
 def test_last_error_is_a_string():
@@ -94,3 +94,33 @@ def test_headers_cite_reference():
     text = open(HEADER).read()
     for ref in ("tv.py:53-89", "skip.py:46-79", "operators.py:44-57", "proximal.py:10-21"):
         assert ref in text
+
+
+def test_emit_csv_matches_reference_writer(tmp_path):
+    """devlog.emit_csv is byte-identical to the reference harness writer
+    (harness.py:447-466) on the golden records (tests/golden/make_golden_csv.py)."""
+    from paper_2411_00688_b200.devlog import emit_csv
+    from paper_2411_00688_b200.solvers import RunRecord
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "make_golden_csv", os.path.join(ROOT, "tests", "golden", "make_golden_csv.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    out = tmp_path / "log.csv"
+    emit_csv(mod.records(RunRecord), str(out))
+    golden = open(os.path.join(ROOT, "tests", "golden", "ref_log.csv"), "rb").read()
+    assert out.read_bytes() == golden
+    with pytest.raises(OSError):
+        emit_csv([], str(tmp_path / "missing-dir" / "x.csv"))
+
+
+def test_device_loggable_rules():
+    from paper_2411_00688_b200.devlog import DeviceObjective, device_loggable
+    from paper_2411_00688_b200.solvers import IterationLog
+    ref = np.zeros((4, 4))
+    assert device_loggable(IterationLog(reference=ref))
+    assert device_loggable(IterationLog(objective_fn=DeviceObjective(None), tol=1e-3, reference=ref))
+    assert not device_loggable(IterationLog())
+    assert not device_loggable(IterationLog(reference=ref, callback=lambda r, x: None))
+    assert not device_loggable(IterationLog(reference=ref, transform=lambda x: x))
+    assert not device_loggable(IterationLog(objective_fn=lambda u: 0.0))
