@@ -102,6 +102,13 @@ int psb_fgp2d_iter(int dtype, const void* x, int64_t x_pstride, void* q, int64_t
 int psb_fgp2d_finalize(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
                        const int32_t* active, int n_active, int H, int W, int n_inner, int nonneg,
                        void* u, int64_t u_pstride, void* stream);
+/* Accelerated projected gradient on the dual ROF problem (run_aprojgd on
+ * build_dual_rof(b, alpha) with huber_eps = 0, solvers.py:148-174,
+ * problems.py:22-71): q = 3 (2,H,W) slots with the start point in slot 0; on
+ * return slot 0 holds the final dual iterate and u = b + div q
+ * (primal_from_dual, problems.py:78-84).  step = gamma (1/8 = 1/L). */
+int psb_aprojgd_dual_rof(int dtype, const void* b, void* q, int H, int W, double alpha,
+                         double step, int iters, void* u, void* stream);
 int psb_tv_prox2d(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
                   const int32_t* active, int n_active, double weight, const double* weights,
                   int reproject_all, const uint8_t* reproject, int H, int W, int n_inner,
@@ -238,14 +245,17 @@ int psb_radon_adj(int dtype, const psb_radon_geom* geom, const void* sino, void*
  * h == NULL: plain PDHG (solvers.py:187-209); else PDHGSkip-2 (skip.py:117-150)
  * with coin = this iteration's Bernoulli draw, hcoef = sigma - sigma/p,
  * ps = p/sigma.  psb_pdhg_run loops K steps (coins_host: host uint8[K]; skip=0
- * runs PDHG), optionally as one CUDA graph. */
+ * runs PDHG), optionally as one CUDA graph; sigma_arr (n*n) / tau_arr (the
+ * flat dual length) are the optional diagonal (Pock-Chambolle) steps of
+ * run_pdhg_preconditioned (solvers.py:212-234), PDHG only. */
 int psb_pdhg_step(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
                   const void* b, int32_t* bad_iter, int k, int coin, double sigma, double tau,
                   double hcoef, double ps, double alpha, int nonneg, void* stream);
 int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
                  const void* b, const uint8_t* coins_host, int K, double sigma, double tau,
-                 double p, double alpha, int nonneg, int skip, int32_t* bad_iter, int use_graph,
-                 double* elapsed_host, void* x_hist, void* stream);
+                 const void* sigma_arr, const void* tau_arr, double p, double alpha, int nonneg,
+                 int skip, int32_t* bad_iter, int use_graph, double* elapsed_host, void* x_hist,
+                 void* stream);
 
 /* PDHGSkip-2 / PDHG on the implicit splitting K = A (Radon), TV in the
  * warm-started FGP prox with optional u >= 0 (problems.py:162-184,

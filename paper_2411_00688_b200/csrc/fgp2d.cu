@@ -425,9 +425,33 @@ int tv_prox2d(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const
   return fgp2d_finalize(dtype, x, xps, q, qps, active, n_active, H, W, n_inner, nonneg, u, ups, st);
 }
 
+// Accelerated projected gradient on the dual ROF problem (run_aprojgd on
+// build_dual_rof(b, alpha), solvers.py:148-174 with problems.py:22-71): the
+// FGP iteration with x = b, weight = alpha, step = gamma, except that FISTA
+// forms its extrapolation at iteration k with (t_k - 1)/t_{k+1}, one entry
+// later in the Beck-Teboulle table than FGP's (t_{k-1} - 1)/t_k (tv.py:77-80).
+int aprojgd_dual_rof(int dtype, const void* b, void* q, int H, int W, double alpha, double step,
+                     int iters, void* u, cudaStream_t st) {
+  PSB_REQUIRE(iters >= 1, "run_aprojgd: iters must be >= 1");
+  PSB_REQUIRE(alpha > 0, "DualRofProblem: alpha must be positive");
+  PSB_REQUIRE(step > 0, "run_fista: gamma must be positive");
+  std::vector<double> beta(iters + 1, 0.0);
+  fista_betas(iters + 1, beta.data());
+  const int64_t HW = (int64_t)H * W;
+  int rc = fgp2d_run(dtype, b, HW, q, 6 * HW, nullptr, 1, alpha, nullptr, 0, nullptr, H, W, iters,
+                     1, 0, step, beta.data() + 1, st);
+  if (rc) return rc;
+  return fgp2d_finalize(dtype, b, HW, q, 6 * HW, nullptr, 1, H, W, iters, 0, u, HW, st);
+}
+
 }  // namespace psb
 
 extern "C" {
+
+int psb_aprojgd_dual_rof(int dtype, const void* b, void* q, int H, int W, double alpha,
+                         double step, int iters, void* u, void* stream) {
+  return psb::aprojgd_dual_rof(dtype, b, q, H, W, alpha, step, iters, u, psb::as_stream(stream));
+}
 
 int psb_fgp2d_iter(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
                    const int32_t* active, int n_active, double weight, const double* weights,

@@ -393,6 +393,11 @@ def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
     bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
     p = skip.p if is_skip else 1.0
     coins = skip.coins(iters) if is_skip else np.ones(iters, dtype=np.uint8)
+    # diagonal (preconditioned) steps of run_pdhg_preconditioned: device arrays
+    sig_a = None if np.isscalar(sigma) else AR.to_dev(sigma, dt).reshape(-1)
+    tau_a = None if np.isscalar(tau) else AR.to_dev(tau, dt).reshape(-1)
+    sig_s = float(sigma) if sig_a is None else 0.0
+    tau_s = float(tau) if tau_a is None else 0.0
     if log.passive or device_loggable(log):
         def chunk(k0, cc, hist):
             cc = np.ascontiguousarray(cc, dtype=np.uint8)
@@ -401,7 +406,8 @@ def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
             bad.fill_(INT32_MAX)
             L.call("psb_pdhg_run", L.dcode(dt), L.C.byref(g), L.ptr(x), L.ptr(y), L.ptr(h),
                    L.ptr(xbar), L.ptr(f["b_dev"]), cc.ctypes.data_as(L.C.c_void_p), K,
-                   float(sigma), float(tau), float(p), float(f["alpha"]), int(bool(f["nonneg"])),
+                   sig_s, tau_s, L.ptr(sig_a), L.ptr(tau_a), float(p), float(f["alpha"]),
+                   int(bool(f["nonneg"])),
                    int(is_skip), L.ptr(bad), int(bool(use_graph)), el.ctypes.data_as(L.C.c_void_p),
                    L.ptr(hist), L.stream())
             k_bad = int(bad.item())

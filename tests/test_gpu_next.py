@@ -110,3 +110,47 @@ def test_bernoulli_op():
     np.testing.assert_array_equal(psb.bernoulli_op(x, 0.25, False), 0.0)
     with pytest.raises(ValueError):
         psb.bernoulli_op(x, 0.0, True)
+
+
+def test_aprojgd_dual_fused_fgp_path(gn):
+    """run_aprojgd on the plain dual-ROF problem with a passive log is one FGP
+    burst; it reproduces the reference trajectory's end point and the stepped
+    (observed) run bit for bit over a longer run."""
+    b = gn["dr_b"]
+    prob = psb.build_dual_rof(b, 0.5)
+    g = 1.0 / prob.smooth.lipschitz
+    q, log = psb.run_aprojgd(prob.smooth, prob.projector, prob.zero_dual(), g, 10)
+    np.testing.assert_allclose(q, gn["dr_aprojgd_traj"][-1], rtol=1e-12, atol=1e-13)
+    assert [r.prox_count for r in log.records] == list(range(1, 11))
+    q_fast, _ = psb.run_aprojgd(prob.smooth, prob.projector, prob.zero_dual(), g, 300)
+    xs, _, lg = _traj()
+    q_step, _ = psb.run_aprojgd(prob.smooth, prob.projector, prob.zero_dual(), g, 300, lg)
+    np.testing.assert_allclose(q_fast, q_step, rtol=1e-13, atol=1e-14)
+
+
+def test_pdhg_preconditioned_native(gn):
+    sp = _ct(gn)
+    x, log = psb.run_pdhg_preconditioned(sp, 20)
+    np.testing.assert_allclose(x, gn["ct_precond_traj"][-1], rtol=1e-10, atol=1e-12)
+    assert len(log.records) == 20
+
+
+def test_compute_reference_solution(gn):
+    R = psb.radon_map(psb.RadonGeometry(image_side=16, n_angles=7, n_bins=23))
+    sino = R.forward(gn["abs_u"][:9, :9].repeat(2, 0).repeat(2, 1)[:16, :16] ** 2)
+    sp_prob = psb.build_tv_recon(R, sino, 0.05, nonneg=True, splitting="explicit",
+                                 precision="fp64")
+    ref = psb.compute_reference_solution(sp_prob, 20000)
+    assert ref.provenance["method"] == "pdhg-preconditioned-explicit"
+    assert ref.provenance["self_consistency_error"] <= psb.SELF_CONSISTENCY_TOL
+    # the split run is exactly one run
+    x1, _ = psb.run_pdhg_preconditioned(sp_prob.saddle_problem, 20000)
+    np.testing.assert_array_equal(ref.u_star, x1)
+    with pytest.raises(psb.ReferenceRejectedError):
+        psb.compute_reference_solution(sp_prob, 10)
+    b = np.random.default_rng(1).random((16, 16))
+    dual = psb.build_dual_rof(b, 0.2)
+    ref_d = psb.compute_reference_solution(dual, 6000)
+    assert ref_d.provenance["method"] == "aprojgd-dual"
+    q, _ = psb.run_aprojgd(dual.smooth, dual.projector, dual.zero_dual(), 1.0 / 8.0, 6000)
+    np.testing.assert_array_equal(ref_d.u_star, psb.primal_from_dual(q, b))
