@@ -108,6 +108,26 @@ __device__ __forceinline__ void ldv(T (&d)[V], const T* p) {
 
 // Vector store (the kernels never re-read what they write in the same launch,
 // so all loads above may use the read-only path).
+// Vector load without the read-only path (shared memory, or data written
+// earlier by the same kernel).
+template <class T, int V>
+__device__ __forceinline__ void ldv_s(T (&d)[V], const T* p) {
+  if constexpr (sizeof(T) * V == 16) {
+    const float4 r = *reinterpret_cast<const float4*>(p);
+    const T* s = reinterpret_cast<const T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+  } else if constexpr (sizeof(T) * V == 8) {
+    const float2 r = *reinterpret_cast<const float2*>(p);
+    const T* s = reinterpret_cast<const T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = p[i];
+  }
+}
+
 template <class T, int V>
 __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
   if constexpr (sizeof(T) * V == 16) {

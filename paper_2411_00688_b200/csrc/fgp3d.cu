@@ -200,14 +200,10 @@ __device__ __forceinline__ void read_plane(const Fgp3Args<T>& a, bool mom, bool 
   T k[3][V], m[3][V];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      k[c][v] = st[c * BW + lane * V + v];
-      m[c][v] = st[(3 + c) * BW + lane * V + v];
-    }
+    ldv_s<T, V>(k[c], st + c * BW + lane * V);
+    if (mom) ldv_s<T, V>(m[c], st + (3 + c) * BW + lane * V);
   }
-#pragma unroll
-  for (int v = 0; v < V; ++v) xv[v] = st[6 * BW + lane * V + v];
+  ldv_s<T, V>(xv, st + 6 * BW + lane * V);
   auto y_of = [&](T& v0, T& v1, T& v2, T n0, T n1, T n2) {
     if (rp) {
       const T s = A::ball_scale3(v0, v1, v2, a.w);
@@ -242,8 +238,10 @@ template <class T, int V>
 __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args<T> a) {
   using A = Ar<T>;
   constexpr int BW = 32 * V;
-  __shared__ T s_yy[MTY + 2][BW + 1];
-  __shared__ T s_u[2][MTY + 2][BW];
+  // row exchange (vector-aligned rows; the band's right halo column apart)
+  __shared__ __align__(16) T s_yy[MTY + 2][BW];
+  __shared__ T s_yyh[MTY + 2];
+  __shared__ __align__(16) T s_u[2][MTY + 2][BW];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * BW;
   const int i = blockIdx.y * MTY - 1 + w;
@@ -267,6 +265,8 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
   auto prim = [&](int kg, Row3<T, V>& R, const T (&yzp)[V], T hyzp, const T (&xv)[V], T hx) {
     T left = __shfl_up_sync(0xffffffffu, R.y[2][V - 1], 1);
     if (lane == 0) left = R.h[2];
+    T yup[V];
+    if (w > 0) ldv_s<T, V>(yup, &s_yy[w - 1][lane * V]);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int c = cl + v;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
       if (kg < a.Dg - 1) d = A::add(d, R.y[0][v]);
       if (kg > 0) d = A::sub(d, yzp[v]);
       if (i < H - 1) d = A::add(d, R.y[1][v]);
-      if (i > 0) d = A::sub(d, w > 0 ? s_yy[w - 1][lane * V + v] : T(0));
+      if (i > 0) d = A::sub(d, w > 0 ? yup[v] : T(0));
       if (c < W - 1) d = A::add(d, R.y[2][v]);
       if (c > 0) d = A::sub(d, v > 0 ? R.y[2][v - 1] : left);
       T u = A::add(xv[v], d);
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
       if (kg < a.Dg - 1) d = A::add(d, R.h[0]);
       if (kg > 0) d = A::sub(d, hyzp);
       if (i < H - 1) d = A::add(d, R.h[1]);
-      if (i > 0) d = A::sub(d, w > 0 ? s_yy[w - 1][BW] : T(0));
+      if (i > 0) d = A::sub(d, w > 0 ? s_yyh[w - 1] : T(0));
       if (c < W - 1) d = A::add(d, R.h[2]);
       if (c > 0) d = A::sub(d, R.y[2][V - 1]);
       T u = A::add(hx, d);
@@ -294,14 +294,10 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
     }
   };
   auto publish_yy = [&](const Row3<T, V>& R) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) s_yy[w][lane * V + v] = R.y[1][v];
-    if (lane == 31) s_yy[w][BW] = R.h[1];
+    stv<T, V>(&s_yy[w][lane * V], R.y[1]);
+    if (lane == 31) s_yyh[w] = R.h[1];
   };
-  auto publish_u = [&](const Row3<T, V>& R, int par) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) s_u[par][w][lane * V + v] = R.u[v];
-  };
+  auto publish_u = [&](const Row3<T, V>& R, int par) { stv<T, V>(&s_u[par][w][lane * V], R.u); };
 
   extern __shared__ unsigned char dyn_smem[];
   T* stage0 = reinterpret_cast<T*>(dyn_smem);
@@ -368,13 +364,14 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
     if (out_row) {
       T right = __shfl_down_sync(0xffffffffu, C.u[0], 1);
       if (lane == 31) right = C.hu;
-      T oz[V], oy[V], ox[V];
+      T oz[V], oy[V], ox[V], udn[V];
+      ldv_s<T, V>(udn, &s_u[k & 1][w + 1][lane * V]);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int c = cl + v;
         const T uc = C.u[v];
         const T gz = nxt ? A::sub(N.u[v], uc) : T(0);
-        const T gy = i < H - 1 ? A::sub(s_u[k & 1][w + 1][lane * V + v], uc) : T(0);
+        const T gy = i < H - 1 ? A::sub(udn[v], uc) : T(0);
         const T ur = v < V - 1 ? C.u[v + 1] : right;
         const T gx = c < W - 1 ? A::sub(ur, uc) : T(0);
         const T az = A::add(C.y[0][v], A::mul(a.step, gz));
