@@ -114,7 +114,7 @@ __global__ void proxskip_post3d_kernel(TO* __restrict__ x, const TO* __restrict_
 // columns and marches along z keeping y(k), u(k) of its row in registers.
 // Warps 1..MTY produce output; warp 0 (row i0-1) only supplies y_y for warp
 // 1's divergence and warp MTY+1 (row i0+MTY) only supplies u for warp MTY's
-// y-gradient.  Rows meet in shared memory (2 __syncthreads per plane), columns
+// y-gradient.  Rows meet in shared memory (1 __syncthreads per plane), columns
 // through shuffles plus one predicated halo column per warp edge, planes
 // through registers.  HBM: x + q_k(3) + q_{k-1}(3) read, q_{k+1}(3) written
 // once per voxel-iteration (40 B fp32), row/column halos re-read from L2.
@@ -239,8 +239,8 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
   using A = Ar<T>;
   constexpr int BW = 32 * V;
   // row exchange (vector-aligned rows; the band's right halo column apart)
-  __shared__ __align__(16) T s_yy[MTY + 2][BW];
-  __shared__ T s_yyh[MTY + 2];
+  __shared__ __align__(16) T s_yy[2][MTY + 2][BW];
+  __shared__ T s_yyh[2][MTY + 2];
   __shared__ __align__(16) T s_u[2][MTY + 2][BW];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * BW;
@@ -262,11 +262,12 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
 
   // u(plane) of this row from its y (cur), y_z of the plane below (yzp, hyzp),
   // y_y of the row above (s_yy[w-1]) and the left neighbour's y_x.
-  auto prim = [&](int kg, Row3<T, V>& R, const T (&yzp)[V], T hyzp, const T (&xv)[V], T hx) {
+  auto prim = [&](int kg, Row3<T, V>& R, const T (&yzp)[V], T hyzp, const T (&xv)[V], T hx,
+                  int par) {
     T left = __shfl_up_sync(0xffffffffu, R.y[2][V - 1], 1);
     if (lane == 0) left = R.h[2];
     T yup[V];
-    if (w > 0) ldv_s<T, V>(yup, &s_yy[w - 1][lane * V]);
+    if (w > 0) ldv_s<T, V>(yup, &s_yy[par][w - 1][lane * V]);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int c = cl + v;
@@ -286,16 +287,16 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
       if (kg < a.Dg - 1) d = A::add(d, R.h[0]);
       if (kg > 0) d = A::sub(d, hyzp);
       if (i < H - 1) d = A::add(d, R.h[1]);
-      if (i > 0) d = A::sub(d, w > 0 ? s_yyh[w - 1] : T(0));
+      if (i > 0) d = A::sub(d, w > 0 ? s_yyh[par][w - 1] : T(0));
       if (c < W - 1) d = A::add(d, R.h[2]);
       if (c > 0) d = A::sub(d, R.y[2][V - 1]);
       T u = A::add(hx, d);
       R.hu = a.nonneg ? (u > T(0) ? u : T(0)) : u;
     }
   };
-  auto publish_yy = [&](const Row3<T, V>& R) {
-    stv<T, V>(&s_yy[w][lane * V], R.y[1]);
-    if (lane == 31) s_yyh[w] = R.h[1];
+  auto publish_yy = [&](const Row3<T, V>& R, int par) {
+    stv<T, V>(&s_yy[par][w][lane * V], R.y[1]);
+    if (lane == 31) s_yyh[par][w] = R.h[1];
   };
   auto publish_u = [&](const Row3<T, V>& R, int par) { stv<T, V>(&s_u[par][w][lane * V], R.u); };
 
@@ -331,11 +332,14 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
   cp_async_wait<1>();
   __syncwarp();
   read_plane<T, V>(a, mom, rp, lane, st_ptr(0), hs_ptr(0), C, xv, hx);
-  publish_yy(C);
+  publish_yy(C, ks & 1);
   __syncthreads();
-  prim(a.z0 + ks, C, yzp, hyzp, xv, hx);
+  prim(a.z0 + ks, C, yzp, hyzp, xv, hx, ks & 1);
   publish_u(C, ks & 1);
-  __syncthreads();
+
+  // One barrier per plane: y_y rows and u rows are double-buffered by plane
+  // parity, so the barrier that publishes y_y(k+1) also publishes u(k) (written
+  // in the previous step) for this step's y-gradient.
 
   for (int k = ks; k < ke; ++k) {
     const int kg = a.z0 + k;
@@ -350,17 +354,16 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
       cp_async_wait<1>();
       __syncwarp();
       read_plane<T, V>(a, mom, rp, lane, st_ptr(sn), hs_ptr(sn), N, xv, hx);
-      publish_yy(N);
+      publish_yy(N, (k + 1) & 1);
     }
     __syncthreads();
     if (nxt) {
       T yzc[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) yzc[v] = C.y[0][v];
-      prim(kg + 1, N, yzc, C.h[0], xv, hx);
+      prim(kg + 1, N, yzc, C.h[0], xv, hx, (k + 1) & 1);
       publish_u(N, (k + 1) & 1);
     }
-    __syncthreads();
     if (out_row) {
       T right = __shfl_down_sync(0xffffffffu, C.u[0], 1);
       if (lane == 31) right = C.hu;
