@@ -6,7 +6,7 @@
 //           prox input z = (x - g(x - b)) + hc h            (skip.py:66-70)
 //   FGP   : all n_inner accelerated iterations (tv.py:75-80) with the
 //           problem's x, q_k, q_{k-1} resident in REGISTERS of a 16-CTA
-//           thread-block cluster (16 SMs, 1024 threads each, 4 pixels per
+//           thread-block cluster (16 SMs, 512 threads each, 8 pixels per
 //           thread); row halos cross CTA boundaries through distributed
 //           shared memory, column halos through warp shuffles and shared
 //           memory; one cluster barrier per inner iteration
@@ -34,11 +34,11 @@ namespace psb {
 namespace {
 
 constexpr int CW = 256;           // image width  (columns = threads per row group)
-constexpr int CRG = 4;            // row groups per CTA
-constexpr int CRPT = 4;           // rows per thread
+constexpr int CRG = 2;            // row groups per CTA
+constexpr int CRPT = 8;           // rows per thread
 constexpr int CCL = 16;           // CTAs per cluster
 constexpr int CH = CCL * CRG * CRPT;  // image height = 256
-constexpr int CTHREADS = CW * CRG;    // 1024
+constexpr int CTHREADS = CW * CRG;    // 512 (8 rows per thread: up to 128 registers)
 constexpr int CWARPS_ROW = CW / 32;   // 8 warps across a row group
 constexpr int kMaxBetas = 1024;       // momentum table staged in shared memory
 
@@ -71,7 +71,7 @@ __device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
   return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
 }
 
-static_assert(CRPT == 4, "edge exchange packs one float4 per thread row group");
+static_assert(CRPT % 4 == 0, "edge exchange packs float4s per thread row group");
 
 // 32-bit shared::cluster address of `p` in CTA `rank` of this cluster, and a load from it
 __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
@@ -332,11 +332,20 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
                    int it) {
     const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
+    // rows in pairs with Blackwell's packed f32x2 FFMA2 / FADD2 / FMUL2 (each
+    // lane an IEEE fp32 op, same rounding as the scalar form); a - b = fma(b, -1, a)
+    const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
     float yy[CRPT], yx[CRPT];
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      yy[t] = QKy[t] + beta * (QKy[t] - QMy[t]);
-      yx[t] = QKx[t] + beta * (QKx[t] - QMx[t]);
+    for (int P = 0; P < CRPT / 2; ++P) {
+      const float2 ky = make_float2(QKy[2 * P], QKy[2 * P + 1]);
+      const float2 kx = make_float2(QKx[2 * P], QKx[2 * P + 1]);
+      const float2 ry = __ffma2_rn(b2, __ffma2_rn(make_float2(QMy[2 * P], QMy[2 * P + 1]), m1, ky), ky);
+      const float2 rx = __ffma2_rn(b2, __ffma2_rn(make_float2(QMx[2 * P], QMx[2 * P + 1]), m1, kx), kx);
+      yy[2 * P] = ry.x;
+      yy[2 * P + 1] = ry.y;
+      yx[2 * P] = rx.x;
+      yx[2 * P + 1] = rx.y;
     }
     const unsigned par = recv_rows(round0 + it);
     float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
@@ -357,27 +366,46 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     }
     s_rg_yy[rg][j] = yy[CRPT - 1];
     if (lane == 31) {
-      *reinterpret_cast<float4*>(&s_edge_yx[rg][wc][0]) = make_float4(yx[0], yx[1], yx[2], yx[3]);
+#pragma unroll
+      for (int c4 = 0; c4 < CRPT / 4; ++c4)
+        *reinterpret_cast<float4*>(&s_edge_yx[rg][wc][4 * c4]) =
+            make_float4(yx[4 * c4], yx[4 * c4 + 1], yx[4 * c4 + 2], yx[4 * c4 + 3]);
       s_edge_yx[rg][wc][CRPT] = ex_x;
     }
     __syncthreads();
-    float4 ledge = make_float4(0.f, 0.f, 0.f, 0.f);
+    float le[CRPT];
     float ledge_x = 0.f;
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) le[t] = 0.f;
     if (left_fetch) {
-      ledge = *reinterpret_cast<const float4*>(&s_edge_yx[rg][wc - 1][0]);
+#pragma unroll
+      for (int c4 = 0; c4 < CRPT / 4; ++c4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(&s_edge_yx[rg][wc - 1][4 * c4]);
+        le[4 * c4] = l4.x;
+        le[4 * c4 + 1] = l4.y;
+        le[4 * c4 + 2] = l4.z;
+        le[4 * c4 + 3] = l4.w;
+      }
       ledge_x = s_edge_yx[rg][wc - 1][CRPT];
     }
-    const float le[CRPT] = {ledge.x, ledge.y, ledge.z, ledge.w};
     const float yy_above = rg_top ? y_up : s_rg_yy[rg - 1][j];
-    float u[CRPT];
+    float left[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
-      float left = __shfl_up_sync(0xffffffffu, yx[t], 1);
-      if (lane == 0) left = le[t];
-      // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded
-      const float d = ((yy[t] - (t > 0 ? yy[t - 1] : yy_above)) + yx[t]) - left;
-      const float v = z[t] + d;
-      u[t] = nonneg ? fmaxf(v, 0.f) : v;
+      left[t] = __shfl_up_sync(0xffffffffu, yx[t], 1);
+      if (lane == 0) left[t] = le[t];
+    }
+    float u[CRPT];
+#pragma unroll
+    for (int P = 0; P < CRPT / 2; ++P) {
+      // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
+      const float2 ab2 = make_float2(P == 0 ? yy_above : yy[2 * P - 1], yy[2 * P]);
+      const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, make_float2(yy[2 * P], yy[2 * P + 1])),
+                                   make_float2(yx[2 * P], yx[2 * P + 1]));
+      const float2 d2 = __ffma2_rn(make_float2(left[2 * P], left[2 * P + 1]), m1, d1);
+      const float2 v = __fadd2_rn(make_float2(z[2 * P], z[2 * P + 1]), d2);
+      u[2 * P] = nonneg ? fmaxf(v.x, 0.f) : v.x;
+      u[2 * P + 1] = nonneg ? fmaxf(v.y, 0.f) : v.y;
     }
     float u_ex;
     {
@@ -389,29 +417,50 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     }
     s_rg_u[rg][j] = u[0];
     if (lane == 0)
-      *reinterpret_cast<float4*>(&s_edge_u[rg][wc][0]) = make_float4(u[0], u[1], u[2], u[3]);
+#pragma unroll
+      for (int c4 = 0; c4 < CRPT / 4; ++c4)
+        *reinterpret_cast<float4*>(&s_edge_u[rg][wc][4 * c4]) =
+            make_float4(u[4 * c4], u[4 * c4 + 1], u[4 * c4 + 2], u[4 * c4 + 3]);
     __syncthreads();
-    float re[CRPT] = {u[0], u[1], u[2], u[3]};  // global column W-1: right := u (gx = 0)
+    float re[CRPT];  // global column W-1: right := u (gx = 0)
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) re[t] = u[t];
     if (right_fetch) {
-      const float4 r4 = *reinterpret_cast<const float4*>(&s_edge_u[rg][wc + 1][0]);
-      re[0] = r4.x;
-      re[1] = r4.y;
-      re[2] = r4.z;
-      re[3] = r4.w;
+#pragma unroll
+      for (int c4 = 0; c4 < CRPT / 4; ++c4) {
+        const float4 r4 = *reinterpret_cast<const float4*>(&s_edge_u[rg][wc + 1][4 * c4]);
+        re[4 * c4] = r4.x;
+        re[4 * c4 + 1] = r4.y;
+        re[4 * c4 + 2] = r4.z;
+        re[4 * c4 + 3] = r4.w;
+      }
     }
     // the global last row has no row below: gy = 0 (below := u)
     const float u_below = !rg_bot ? s_rg_u[rg + 1][j] : (last_row_thread ? u[CRPT - 1] : u_ex);
+    float right[CRPT];
 #pragma unroll
     for (int t = 0; t < CRPT; ++t) {
-      float right = __shfl_down_sync(0xffffffffu, u[t], 1);
-      if (lane == 31) right = re[t];
-      const float below = t < CRPT - 1 ? u[t + 1] : u_below;
-      const float ay = yy[t] + a.step * (below - u[t]);
-      const float ax = yx[t] + a.step * (right - u[t]);
-      const float m2 = fmaf(ay, ay, ax * ax);
-      const float sc = fminf(1.f, w * rsqrt_approx(m2));  // w / max(w, |a|)
-      QMy[t] = ay * sc;
-      QMx[t] = ax * sc;
+      right[t] = __shfl_down_sync(0xffffffffu, u[t], 1);
+      if (lane == 31) right[t] = re[t];
+    }
+    const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(w, w);
+#pragma unroll
+    for (int P = 0; P < CRPT / 2; ++P) {
+      const float2 u2 = make_float2(u[2 * P], u[2 * P + 1]);
+      const float2 bl2 = make_float2(u[2 * P + 1], P == CRPT / 2 - 1 ? u_below : u[2 * P + 2]);
+      const float2 gy = __ffma2_rn(u2, m1, bl2);
+      const float2 gx = __ffma2_rn(u2, m1, make_float2(right[2 * P], right[2 * P + 1]));
+      const float2 ay = __ffma2_rn(st2, gy, make_float2(yy[2 * P], yy[2 * P + 1]));
+      const float2 ax = __ffma2_rn(st2, gx, make_float2(yx[2 * P], yx[2 * P + 1]));
+      const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
+      float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
+      sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
+      sc.y = fminf(1.f, sc.y);
+      const float2 ny = __fmul2_rn(ay, sc), nx = __fmul2_rn(ax, sc);
+      QMy[2 * P] = ny.x;
+      QMy[2 * P + 1] = ny.y;
+      QMx[2 * P] = nx.x;
+      QMx[2 * P + 1] = nx.y;
     }
     (void)right_edge;
     push_rows(QMy[0], QMx[0], QMy[CRPT - 1]);
