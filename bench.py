@@ -270,6 +270,10 @@ def run_gpu(args):
     peak, peak_kind = _peaks()
 
     # ---- e2e: the public API with host buffers, copies inside the region ----
+    # (the device-resident solver above is released first: the e2e call owns
+    # its whole footprint, as a user's single call would)
+    del solver
+    torch.cuda.empty_cache()
     b_pin = torch.from_numpy(b_host).pin_memory()
     sync_all()
     t0 = time.perf_counter()
