@@ -44,8 +44,9 @@ if CLUSTER:
               "+ post) per 16-CTA cluster, FGP state in registers; the 28 B/px-iter of the "
               "streaming formulation stay on-chip, so frac > 1 is expected")
     # ncu dram__bytes_read.sum + dram__bytes_write.sum of fgp_cluster_kernel in this bench
-    # (profiles/r01_launches_bench_cluster.csv): 2.23 MB per coin-fired problem per launch
-    TRAFFIC_PER_PROBLEM = 2.23e6
+    # (profiles/r01_launches_bench_cluster_v10.csv): 895.1 MB per launch at 405.3 coin-fired
+    # problems on average = 2.21 MB per problem per launch
+    TRAFFIC_PER_PROBLEM = 895.1e6 / 405.3
 else:
     KERNEL = "fgp2d_iter_kernel<float,4> (streaming, one launch per inner iteration)"
     # profiles/r01_fgp2d_iter_ncu_details.csv: 795 MB per launch at 422 problems
