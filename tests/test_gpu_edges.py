@@ -1,0 +1,191 @@
+"""Edge cases on the device: ragged and minimal shapes (vector and scalar
+kernel variants), non-aligned widths, empty runs, nonneg clamps in the
+cluster path, non-finite inputs, and size-independent properties at large
+sizes -- the reference's validation behaviour (test_operators.py:98-112,
+test_tv.py:36-43, test_skip.py:42-46, test_solvers.py:60-68) included."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2411_00688_b200 as psb  # noqa: E402
+from paper_2411_00688_b200 import phantoms, volume3d  # noqa: E402
+from paper_2411_00688_b200.operators import div_dev  # noqa: E402
+from oracle import imgskip_cpu as oc  # noqa: E402
+from oracle import tv3d_cpu as o3  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+SHAPES = [(2, 2), (2, 3), (3, 2), (5, 7), (17, 33), (64, 130), (130, 64), (129, 257), (2, 300)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_tv_prox_ragged_shapes_fp64_bitwise(shape, nonneg):
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal(shape)
+    st = psb.TvProxState.cold(shape, 9, nonneg=nonneg, dtype=torch.float64)
+    ref = oc.FgpState.zeros(shape, 9, nonneg=nonneg)
+    for wgt in (0.3, 0.3, 0.7):  # warm start + re-projection on the weight change
+        u = psb.tv_prox(x, wgt, st)
+        ur = oc.fgp_prox(x, wgt, ref)
+        np.testing.assert_array_equal(u, ur)
+    np.testing.assert_array_equal(st.q_warm, ref.q)
+    assert st.total_inner_iterations == ref.inner_total == 27
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tv_prox_ragged_shapes_fp32(shape):
+    rng = np.random.default_rng(7 + sum(shape))
+    x = rng.standard_normal(shape)
+    st = psb.TvProxState.cold(shape, 20)
+    ref = oc.FgpState.zeros(shape, 20)
+    u = psb.tv_prox(x, 0.25, st)
+    ur = oc.fgp_prox(x, 0.25, ref)
+    assert rel(u, ur) < 2e-6
+
+
+def test_validation_matches_reference():
+    with pytest.raises(ValueError):
+        psb.grad_forward(np.zeros((1, 5)))
+    with pytest.raises(ValueError):
+        psb.divergence(np.zeros((2, 1, 5)))
+    with pytest.raises(ValueError):
+        psb.TvProxState.cold((5, 7), 0)
+    with pytest.raises(ValueError):
+        psb.tv_prox(np.zeros((4, 4)), 0.0, psb.TvProxState.cold((4, 4), 3))
+    with pytest.raises(ValueError):
+        psb.SkipConfig(0.0, 0)
+    with pytest.raises(ValueError):
+        psb.SkipConfig(1.2, 0)
+    with pytest.raises(ValueError):
+        psb.RadonGeometry(image_side=8, n_angles=4, n_bins=6)
+    with pytest.raises(ValueError):
+        psb.block_stack(psb.identity_map((4, 4)), psb.grad_map((5, 5)))
+    A = psb.identity_map((6, 6))
+    with pytest.raises(ValueError):
+        psb.build_tv_recon(A, np.zeros((6, 6)), -1.0)
+    with pytest.raises(ValueError):
+        psb.build_tv_recon(A, np.zeros((6, 6)), 0.1, splitting="magic")
+    with pytest.raises(ValueError):
+        psb.build_tv_recon(A, np.zeros((6, 6)), 0.1, inner_budget=0)
+    prob = psb.build_tv_recon(A, np.zeros((6, 6)), 0.1)
+    with pytest.raises(ValueError):
+        psb.run_proxskip(prob.prox_problem, np.zeros((6, 6)), None, 0.0, psb.SkipConfig(0.5, 0), 3)
+    with pytest.raises(ValueError):
+        psb.run_pgd(prob.prox_problem, np.zeros((6, 6)), -1.0, 3)
+
+
+@pytest.mark.parametrize("prec", ["mixed", "fp64"])
+def test_zero_iterations_return_a_copy(prec):
+    b = np.random.default_rng(1).random((16, 16))
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=5, precision=prec)
+    x0 = np.full_like(b, 0.5)
+    x, log = psb.run_proxskip(prob.prox_problem, x0, None, 1.0, psb.SkipConfig(0.3, 0), 0)
+    np.testing.assert_array_equal(x, x0)
+    assert x is not x0 and log.records == []
+    assert prob.tv_state.total_inner_iterations == 0
+
+
+def test_run_with_no_coin_fired():
+    """A run whose coins never fire executes only skip updates (skip.py:72-74)."""
+    b = np.random.default_rng(2).random((256, 256))
+    seed = next(s for s in range(1000) if not psb.SkipConfig(0.05, s).coins(4).any())
+    for prec in ("mixed", "fp32"):
+        prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=5, precision=prec)
+        x, log = psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0,
+                                  psb.SkipConfig(0.05, seed), 4)
+        ref = oc.make_recon(oc.identity_op(b.shape), b, 0.1, inner=5)
+        xr = oc.proxskip(ref.grad, ref.prox, np.zeros_like(b), None, 1.0, 0.05, seed, 4)[0]
+        assert rel(x, xr) < 1e-6
+        assert log.records[-1].prox_count == 0
+
+
+def test_cluster_path_nonneg_matches_oracle():
+    """256^2 fp32 problems take the cluster kernel; nonneg selects its clamped
+    instantiation (tv.py:65,76)."""
+    u = phantoms.random_shapes((256, 256), 8, np.random.default_rng(3))
+    b = phantoms.add_noise(u, 0.2, 3) - 0.1
+    prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, nonneg=True, inner_budget=20,
+                              precision="fp32")
+    x, _ = psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0,
+                            psb.SkipConfig(0.2, 4), 30)
+    pr = oc.make_recon(oc.identity_op(b.shape), b, 0.1, nonneg=True, inner=20)
+    xr = oc.proxskip(pr.grad, pr.prox, np.zeros_like(b), None, 1.0, 0.2, 4, 30)[0]
+    assert rel(x, xr) < 1e-5
+
+
+@pytest.mark.parametrize("n,shape", [(1, (256, 256)), (3, (40, 72)), (2, (33, 17))])
+def test_batched_odd_batches_and_shapes(n, shape):
+    rng = np.random.default_rng(n)
+    b = rng.random((n,) + shape)
+    seeds = np.arange(n) + 11
+    x, counts = psb.run_proxskip_batched(b, 0.1, 0.3, seeds, 12, 8, precision="fp32")
+    for i in range(n):
+        xr, _, npx, _ = oc.proxskip_denoise(b[i], 0.1, 0.3, int(seeds[i]), 12, 8)
+        assert counts[i] == npx
+        assert rel(x[i], xr) < 2e-5
+
+
+def test_nonfinite_input_raises_divergence():
+    b = np.random.default_rng(4).random((256, 256))
+    b[3, 5] = np.nan
+    for prec in ("fp32", "mixed"):
+        prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=5,
+                                  precision=prec)
+        with pytest.raises(psb.DivergenceError) as ei:
+            psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0,
+                             psb.SkipConfig(0.5, 0), 5)
+        assert ei.value.iteration == 0 and ei.value.algorithm == "proxskip"
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 7), (4, 9, 130), (6, 2, 2), (2, 33, 20)])
+def test_tv_prox3d_ragged_fp64_bitwise(shape):
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal(shape)
+    st = volume3d.TvProxState3D(shape, 6, dtype=torch.float64)
+    ref = o3.Fgp3State.zeros(shape, 6)
+    for wgt in (0.2, 0.5):
+        u = volume3d.tv_prox3d(x, wgt, st)
+        ur = o3.fgp_prox3(x, wgt, ref)
+        np.testing.assert_array_equal(u, ur)
+
+
+def test_radon_minimal_geometries():
+    for n, na, nb in ((2, 1, 2), (3, 2, 3), (8, 1, 8)):
+        op = psb.radon_map(psb.RadonGeometry(image_side=n, n_angles=na, n_bins=nb))
+        ref = oc.radon_op(n, na, nb)
+        x = np.random.default_rng(n).random((n, n))
+        y = np.random.default_rng(na).random((na, nb))
+        np.testing.assert_allclose(op.forward(x), ref.fwd(x), rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(op.adjoint(y), ref.adj(y), rtol=1e-12, atol=1e-13)
+
+
+def test_large_tv_prox_properties():
+    """4096^2 fp32: size-independent properties -- the dual iterate is
+    feasible (|q| <= w), u = x + div q, and the ROF duality gap shrinks with
+    the inner budget (tv.py:92-105)."""
+    n = 4096
+    x = torch.rand((n, n), device="cuda", dtype=torch.float32)
+    gaps = []
+    for inner in (10, 40):
+        st = psb.TvProxState.cold((n, n), inner)
+        u = psb.tv_prox(x, 0.05, st)
+        q = st.slots[0].double()
+        assert float(torch.sqrt(q[0] ** 2 + q[1] ** 2).max()) <= 0.05 * (1 + 1e-6)
+        div = div_dev(q)
+        assert float((u.double() - (x.double() + div)).abs().max()) < 1e-5
+        # fp32 ball scaling (rsqrt.approx) may leave |q| a few ulp above w:
+        # project onto the ball in fp64 before evaluating the gap
+        mag = torch.sqrt(q[0] ** 2 + q[1] ** 2)
+        qf = q * torch.clamp(0.05 / torch.clamp(mag, min=1e-300), max=1.0)
+        gaps.append(psb.dual_gap_rof(x.double(), qf, 0.05))
+    assert gaps[1] < gaps[0]
