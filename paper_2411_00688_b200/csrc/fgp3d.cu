@@ -13,6 +13,11 @@
 // (above) come from halo buffers holding the neighbours' (q_k, q_{k-1}) planes
 // (and x for the plane above); the boundary tests use GLOBAL plane indices, so
 // a slab computes exactly what the whole-volume kernel computes on its planes.
+#include <cuda.h>
+#include <cstring>
+#include <cstdlib>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace psb {
@@ -234,8 +239,152 @@ __device__ __forceinline__ void read_plane(const Fgp3Args<T>& a, bool mom, bool 
   hx = hs[6 * 2 + hi];
 }
 
-template <class T, int V>
-__global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args<T> a) {
+// ---- TMA staging (fp32, 16-B vector rows) ----------------------------------
+// One elected thread loads a whole plane tile of the CTA -- rows i0-1 ..
+// i0+MTY, columns c0-4 .. c0+131 (the band plus one 16-B chunk on each side
+// for the halo columns) -- with three tensor-map copies (q_k: 3 channels, q_{k-1}:
+// 3 channels, x); out-of-range rows / columns are zero-filled by the copy
+// engine, which is what the per-lane cp.async path does with zero-size
+// copies.  Completion is counted in bytes on one mbarrier per stage.
+constexpr int TBW = 32 * 4 + 8;           // 136 columns per tile row
+constexpr int TROWS = MTY + 2;            // 10 rows
+constexpr int TQ = 3 * TROWS * TBW;       // floats of a 3-channel q tile
+constexpr int TX = TROWS * TBW;           // floats of an x tile
+constexpr int TQ_PAD = (TQ * 4 + 127) / 128 * 32;  // floats, 128-B aligned regions
+constexpr int TX_PAD = (TX * 4 + 127) / 128 * 32;
+constexpr int TSTAGE = 2 * TQ_PAD + TX_PAD;        // floats per stage
+
+struct Fgp3Maps {
+  CUtensorMap q;      // (9 = slot*3 + channel, D, H, W) main dual slots
+  CUtensorMap x;      // (D, H, W)
+  CUtensorMap hb_qk;  // (3, H, W) halo planes (slabs)
+  CUtensorMap hb_qm;
+  CUtensorMap ha_qk;
+  CUtensorMap ha_qm;
+  CUtensorMap ha_x;   // (H, W)
+};
+
+__device__ __forceinline__ uint32_t sm32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_ld4(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                        int c3, uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(sm32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(sm32(mb))
+      : "memory");
+}
+__device__ __forceinline__ void tma_ld3(void* dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                        uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(sm32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(sm32(mb))
+      : "memory");
+}
+__device__ __forceinline__ void tma_ld2(void* dst, const CUtensorMap* m, int c0, int c1,
+                                        uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(sm32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(sm32(mb))
+      : "memory");
+}
+__device__ __forceinline__ void mb_init(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm32(m)));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* m, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra W_%=;\n}\n" ::"r"(sm32(m)),
+      "r"(parity)
+      : "memory");
+}
+
+// issue plane kl (local index in [-1, D]) into stage `st` (thread 0 only)
+__device__ __forceinline__ void tma_issue_plane(const Fgp3Args<float>& a, const Fgp3Maps& M,
+                                                int kl, bool mom, int c0, int i0, float* st,
+                                                uint64_t* mb) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  const bool has_x = kl >= 0;  // plane z0-1 is only read for its y_z
+  const unsigned bytes = (unsigned)(4 * (TQ + (mom ? TQ : 0) + (has_x ? TX : 0)));
+  mb_expect(mb, bytes);
+  const int sk = (a.it % 3) * 3, sm = ((a.it + 2) % 3) * 3;
+  if (kl >= 0 && kl < a.D) {
+    tma_ld4(st, &M.q, c0 - 4, i0, kl, sk, mb);
+    if (mom) tma_ld4(st + TQ_PAD, &M.q, c0 - 4, i0, kl, sm, mb);
+    tma_ld3(st + 2 * TQ_PAD, &M.x, c0 - 4, i0, kl, mb);
+  } else if (kl < 0) {
+    tma_ld3(st, &M.hb_qk, c0 - 4, i0, 0, mb);
+    if (mom) tma_ld3(st + TQ_PAD, &M.hb_qm, c0 - 4, i0, 0, mb);
+  } else {
+    tma_ld3(st, &M.ha_qk, c0 - 4, i0, 0, mb);
+    if (mom) tma_ld3(st + TQ_PAD, &M.ha_qm, c0 - 4, i0, 0, mb);
+    tma_ld2(st + 2 * TQ_PAD, &M.ha_x, c0 - 4, i0, mb);
+  }
+}
+
+// the row of warp w from a TMA stage: same values the cp.async path stages
+__device__ __forceinline__ void tma_read_plane(const Fgp3Args<float>& a, bool mom, bool rp,
+                                               int w, int lane, const float* st,
+                                               Row3<float, 4>& R, float (&xv)[4], float& hx) {
+  using A = Ar<float>;
+  const float* qk = st + w * TBW + 4 + lane * 4;
+  const float* qm = qk + TQ_PAD;
+  const float* xs = st + 2 * TQ_PAD + w * TBW + 4 + lane * 4;
+  float k[3][4], m[3][4];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    ldv_s<float, 4>(k[c], qk + c * TROWS * TBW);
+    if (mom) ldv_s<float, 4>(m[c], qm + c * TROWS * TBW);
+  }
+  ldv_s<float, 4>(xv, xs);
+  auto y_of = [&](float& v0, float& v1, float& v2, float n0, float n1, float n2) {
+    if (rp) {
+      const float s = A::ball_scale3(v0, v1, v2, a.w);
+      v0 = A::mul(v0, s);
+      v1 = A::mul(v1, s);
+      v2 = A::mul(v2, s);
+    }
+    if (mom) {
+      v0 = A::add(v0, A::mul(a.beta, A::sub(v0, n0)));
+      v1 = A::add(v1, A::mul(a.beta, A::sub(v1, n1)));
+      v2 = A::add(v2, A::mul(a.beta, A::sub(v2, n2)));
+    }
+  };
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    float v0 = k[0][v], v1 = k[1][v], v2 = k[2][v];
+    y_of(v0, v1, v2, mom ? m[0][v] : 0.f, mom ? m[1][v] : 0.f, mom ? m[2][v] : 0.f);
+    R.y[0][v] = v0;
+    R.y[1][v] = v1;
+    R.y[2][v] = v2;
+  }
+  // halo columns: lane 0 -> column c0-1 (tile column 3), lane 31 -> c0+128 (tile column 132)
+  const int hcol = lane == 31 ? 4 + 128 - (4 + lane * 4) : 3 - (4 + lane * 4);
+  float h0 = qk[hcol], h1 = qk[TROWS * TBW + hcol], h2 = qk[2 * TROWS * TBW + hcol];
+  float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+  if (mom) {
+    n0 = qm[hcol];
+    n1 = qm[TROWS * TBW + hcol];
+    n2 = qm[2 * TROWS * TBW + hcol];
+  }
+  y_of(h0, h1, h2, n0, n1, n2);
+  R.h[0] = h0;
+  R.h[1] = h1;
+  R.h[2] = h2;
+  hx = xs[hcol];
+}
+
+template <class T, int V, bool TMA>
+__global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args<T> a, const __grid_constant__ Fgp3Maps maps) {
   using A = Ar<T>;
   constexpr int BW = 32 * V;
   // row exchange (vector-aligned rows; the band's right halo column apart)
@@ -300,12 +449,54 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
   };
   auto publish_u = [&](const Row3<T, V>& R, int par) { stv<T, V>(&s_u[par][w][lane * V], R.u); };
 
-  extern __shared__ unsigned char dyn_smem[];
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
   T* stage0 = reinterpret_cast<T*>(dyn_smem);
   constexpr int SW = 7 * BW;  // per-warp stage floats
   T* hs_all = stage0 + (size_t)2 * (MTY + 2) * SW;
   auto st_ptr = [&](int sidx) { return stage0 + (size_t)(sidx * (MTY + 2) + w) * SW; };
   auto hs_ptr = [&](int sidx) { return hs_all + (size_t)(sidx * (MTY + 2) + w) * 14; };
+  // staging back ends: per-lane cp.async into per-warp rows, or (TMA) one
+  // tensor-map tile per CTA and plane completing on a per-stage mbarrier
+  __shared__ __align__(8) uint64_t s_tmb[2];
+  unsigned tph = 0;  // TMA: parity of the next wait, per stage
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mb_init(&s_tmb[0]);
+      mb_init(&s_tmb[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  auto t_stage = [&](int sidx) { return reinterpret_cast<float*>(dyn_smem) + sidx * TSTAGE; };
+  auto stage_issue = [&](int kl, int sidx) {
+    if constexpr (TMA) {
+      if (threadIdx.x == 0)
+        tma_issue_plane(a, maps, kl, mom, c0, blockIdx.y * MTY - 1, t_stage(sidx), &s_tmb[sidx]);
+    } else {
+      issue_plane<T, V>(a, kl, i, cl, lin, hc, hval, mom, lane, st_ptr(sidx), hs_ptr(sidx));
+    }
+  };
+  auto stage_commit = [&]() {
+    if constexpr (!TMA) cp_async_commit();
+  };
+  auto stage_wait = [&](int sidx, bool newer) {
+    if constexpr (TMA) {
+      mb_wait(&s_tmb[sidx], (tph >> sidx) & 1u);
+      tph ^= 1u << sidx;
+    } else {
+      if (newer)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+      __syncwarp();
+    }
+  };
+  auto stage_read = [&](int sidx, Row3<T, V>& R, T (&xr)[V], T& hxr) {
+    if constexpr (TMA)
+      tma_read_plane(a, mom, rp, w, lane, t_stage(sidx), R, xr, hxr);
+    else
+      read_plane<T, V>(a, mom, rp, lane, st_ptr(sidx), hs_ptr(sidx), R, xr, hxr);
+  };
 
   Row3<T, V> C, N;
   T yzp[V], hyzp = T(0), xv[V], hx;
@@ -314,24 +505,24 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
   // prologue: y_z of plane ks-1 (synchronously), then planes ks and ks+1 in flight
   if (a.z0 + ks > 0) {
     T xd[V], hxd;
-    issue_plane<T, V>(a, ks - 1, i, cl, lin, hc, hval, mom, lane, st_ptr(0), hs_ptr(0));
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    read_plane<T, V>(a, mom, rp, lane, st_ptr(0), hs_ptr(0), N, xd, hxd);
+    stage_issue(ks - 1, 0);
+    stage_commit();
+    stage_wait(0, false);
+    stage_read(0, N, xd, hxd);
 #pragma unroll
     for (int v = 0; v < V; ++v) yzp[v] = N.y[0][v];
     hyzp = N.h[0];
-    __syncwarp();
+    if constexpr (TMA)
+      __syncthreads();  // every warp has read stage 0 before it is refilled
+    else
+      __syncwarp();
   }
-  issue_plane<T, V>(a, ks, i, cl, lin, hc, hval, mom, lane, st_ptr(0), hs_ptr(0));
-  cp_async_commit();
-  if (a.z0 + ks + 1 < a.Dg)
-    issue_plane<T, V>(a, ks + 1, i, cl, lin, hc, hval, mom, lane, st_ptr(1), hs_ptr(1));
-  cp_async_commit();
-  cp_async_wait<1>();
-  __syncwarp();
-  read_plane<T, V>(a, mom, rp, lane, st_ptr(0), hs_ptr(0), C, xv, hx);
+  stage_issue(ks, 0);
+  stage_commit();
+  if (a.z0 + ks + 1 < a.Dg) stage_issue(ks + 1, 1);
+  stage_commit();
+  stage_wait(0, true);
+  stage_read(0, C, xv, hx);
   publish_yy(C, ks & 1);
   __syncthreads();
   prim(a.z0 + ks, C, yzp, hyzp, xv, hx, ks & 1);
@@ -348,12 +539,12 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
       // plane k+1 was issued one step ago into stage (k+1-ks)&1; put plane k+2
       // into the stage plane k used, then wait for plane k+1 only
       const int sn = (k + 1 - ks) & 1;
-      if (kg + 2 < a.Dg)
-        issue_plane<T, V>(a, k + 2, i, cl, lin, hc, hval, mom, lane, st_ptr(sn ^ 1), hs_ptr(sn ^ 1));
-      cp_async_commit();
-      cp_async_wait<1>();
-      __syncwarp();
-      read_plane<T, V>(a, mom, rp, lane, st_ptr(sn), hs_ptr(sn), N, xv, hx);
+      // plane k+2 is read by this chunk only when k+1 < ke (no load may be
+      // left in flight at exit)
+      if (kg + 2 < a.Dg && k + 1 < ke) stage_issue(k + 2, sn ^ 1);
+      stage_commit();
+      stage_wait(sn, true);
+      stage_read(sn, N, xv, hx);
       publish_yy(N, (k + 1) & 1);
     }
     __syncthreads();
@@ -404,6 +595,68 @@ size_t march_smem() {
   return sizeof(T) * ((size_t)2 * (MTY + 2) * 7 * 32 * V + (size_t)2 * (MTY + 2) * 14);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+    (void)cudaGetLastError();
+  }
+  return fn;
+}
+
+// fp32 tile map: dims innermost first (W, H, ...), byte strides of dims 1.., box
+bool encode_f32(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+                const cuuint64_t* strides, const cuuint32_t* box) {
+  EncodeTiled fn = encode_fn();
+  if (!fn || !base || reinterpret_cast<uintptr_t>(base) % 16) return false;
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), dims,
+            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the TMA staging maps of one launch; false -> use the cp.async path
+bool make_maps(const Fgp3Args<float>& a, Fgp3Maps& M) {
+  const char* off = std::getenv("PSB_NO_TMA3D");
+  if (off && off[0] == '1') return false;
+  if (a.W % 4 != 0) return false;
+  std::memset(&M, 0, sizeof(M));
+  const cuuint64_t W = a.W, H = a.H, D = a.D, E = 4;
+  const cuuint32_t bw = TBW, br = TROWS;
+  {
+    const cuuint64_t dims[4] = {W, H, D, 9}, str[3] = {W * E, W * H * E, W * H * D * E};
+    const cuuint32_t box[4] = {bw, br, 1, 3};
+    if (!encode_f32(&M.q, a.q, 4, dims, str, box)) return false;
+  }
+  {
+    const cuuint64_t dims[3] = {W, H, D}, str[2] = {W * E, W * H * E};
+    const cuuint32_t box[3] = {bw, br, 1};
+    if (!encode_f32(&M.x, a.x, 3, dims, str, box)) return false;
+  }
+  const cuuint64_t hd[3] = {W, H, 3}, hs[2] = {W * E, W * H * E};
+  const cuuint32_t hbx[3] = {bw, br, 3};
+  if (a.hb_qk && (!encode_f32(&M.hb_qk, a.hb_qk, 3, hd, hs, hbx) ||
+                  !encode_f32(&M.hb_qm, a.hb_qm, 3, hd, hs, hbx)))
+    return false;
+  if (a.ha_qk) {
+    const cuuint64_t xd[2] = {W, H}, xs[1] = {W * E};
+    const cuuint32_t xb[2] = {bw, br};
+    if (!encode_f32(&M.ha_qk, a.ha_qk, 3, hd, hs, hbx) ||
+        !encode_f32(&M.ha_qm, a.ha_qm, 3, hd, hs, hbx) || !encode_f32(&M.ha_x, a.ha_x, 2, xd, xs, xb))
+      return false;
+  }
+  return true;
+}
+
 template <class T>
 int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   constexpr int VMAX = 16 / sizeof(T);
@@ -411,18 +664,31 @@ int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   const int nz = (a.D + zc - 1) / zc;
   const bool vec = (a.W % VMAX == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(a.q) % 16 == 0);
+  Fgp3Maps maps;
+  if constexpr (sizeof(T) == 4) {
+    if (vec && make_maps(a, maps)) {
+      const size_t sm = sizeof(float) * (size_t)2 * TSTAGE;
+      PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, VMAX, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      dim3 grid((a.W + 32 * VMAX - 1) / (32 * VMAX), (a.H + MTY - 1) / MTY, nz);
+      fgp3d_march_kernel<T, VMAX, true><<<grid, (MTY + 2) * 32, sm, st>>>(a, maps);
+      PSB_LAUNCHED("fgp3d_march_tma");
+      return PSB_OK;
+    }
+  }
+  std::memset(&maps, 0, sizeof(maps));
   if (vec) {
     const size_t sm = march_smem<T, VMAX>();
-    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, VMAX>,
+    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, VMAX, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 grid((a.W + 32 * VMAX - 1) / (32 * VMAX), (a.H + MTY - 1) / MTY, nz);
-    fgp3d_march_kernel<T, VMAX><<<grid, (MTY + 2) * 32, sm, st>>>(a);
+    fgp3d_march_kernel<T, VMAX, false><<<grid, (MTY + 2) * 32, sm, st>>>(a, maps);
   } else {
     const size_t sm = march_smem<T, 1>();
-    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, 1>,
+    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, 1, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 grid((a.W + 31) / 32, (a.H + MTY - 1) / MTY, nz);
-    fgp3d_march_kernel<T, 1><<<grid, (MTY + 2) * 32, sm, st>>>(a);
+    fgp3d_march_kernel<T, 1, false><<<grid, (MTY + 2) * 32, sm, st>>>(a, maps);
   }
   PSB_LAUNCHED("fgp3d_march");
   return PSB_OK;

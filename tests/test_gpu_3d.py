@@ -86,3 +86,19 @@ def test_deferred_skips_are_bitwise_identical(precision):
     xb, _ = v3.proxskip_denoise3d(b, 0.08, 0.2, 9, 37, 4, n_slabs=2, precision=precision,
                                   defer_skips=False)
     np.testing.assert_array_equal(xa, xb)
+
+
+@pytest.mark.parametrize("shape,n_slabs", [((23, 20, 36), 3), ((9, 33, 260), 2), ((40, 17, 128), 1)])
+def test_tma_staging_is_bitwise_the_cp_async_path(monkeypatch, shape, n_slabs):
+    """The fp32 3-D kernel stages planes with tensor-map TMA tiles (zero-filled
+    out of range) by default; PSB_NO_TMA3D=1 selects the per-lane cp.async
+    staging.  Same values reach the arithmetic, so the runs agree bit for bit
+    (slab halo planes, band edges and ragged tiles included)."""
+    vol = phantoms.random_ellipsoids(shape, 5, np.random.default_rng(5))
+    b = phantoms.add_noise(vol, 0.1, 5)
+    xa, sa = v3.proxskip_denoise3d(b, 0.08, 0.3, 2, 15, 6, n_slabs=n_slabs, precision="fp32")
+    monkeypatch.setenv("PSB_NO_TMA3D", "1")
+    xb, sb = v3.proxskip_denoise3d(b, 0.08, 0.3, 2, 15, 6, n_slabs=n_slabs, precision="fp32")
+    np.testing.assert_array_equal(xa, xb)
+    for p, q in zip(sa, sb):
+        np.testing.assert_array_equal(p.q.cpu().numpy(), q.q.cpu().numpy())
