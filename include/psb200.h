@@ -109,6 +109,17 @@ int psb_fgp2d_finalize(int dtype, const void* x, int64_t x_pstride, void* q, int
  * (primal_from_dual, problems.py:78-84).  step = gamma (1/8 = 1/L). */
 int psb_aprojgd_dual_rof(int dtype, const void* b, void* q, int H, int W, double alpha,
                          double step, int iters, void* u, void* stream);
+/* Dual-ROF light-prox drivers (build_dual_rof, problems.py:22-84; SURVEY 8(f)
+ * row 4): algo 0 = GD, 1 = PGD / ProjGD, 2 = FISTA / AProjGD, 3 = ProxSkip
+ * (solvers.py:116-174, skip.py:46-79) on q (2,H,W) in place; h: ProxSkip
+ * control variate (2,H,W) or NULL; work: 4*H*W scratch; huber_mu =
+ * huber_eps / alpha; coins_host: uint8[K] (ProxSkip only).  Optional per-
+ * iteration device elapsed times and iterate history as in the other run
+ * drivers. */
+int psb_dual_rof_run(int dtype, int algo, const void* b, void* q, void* h, void* work, int H,
+                     int W, double alpha, double huber_mu, double gamma, double p,
+                     const uint8_t* coins_host, int K, int32_t* bad_iter, int use_graph,
+                     double* elapsed_host, void* x_hist, void* stream);
 int psb_tv_prox2d(int dtype, const void* x, int64_t x_pstride, void* q, int64_t q_pstride,
                   const int32_t* active, int n_active, double weight, const double* weights,
                   int reproject_all, const uint8_t* reproject, int H, int W, int n_inner,
@@ -247,15 +258,17 @@ int psb_radon_adj(int dtype, const psb_radon_geom* geom, const void* sino, void*
  * ps = p/sigma.  psb_pdhg_run loops K steps (coins_host: host uint8[K]; skip=0
  * runs PDHG), optionally as one CUDA graph; sigma_arr (n*n) / tau_arr (the
  * flat dual length) are the optional diagonal (Pock-Chambolle) steps of
- * run_pdhg_preconditioned (solvers.py:212-234), PDHG only. */
+ * run_pdhg_preconditioned (solvers.py:212-234), PDHG only.  skip: 0 PDHG,
+ * 1 PDHGSkip-2 (h = control variate), 2 PDHGSkip-1 (skip.py:82-114, omega;
+ * K^T and the prox only on success draws). */
 int psb_pdhg_step(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
                   const void* b, int32_t* bad_iter, int k, int coin, double sigma, double tau,
                   double hcoef, double ps, double alpha, int nonneg, void* stream);
 int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* h, void* xbar,
                  const void* b, const uint8_t* coins_host, int K, double sigma, double tau,
                  const void* sigma_arr, const void* tau_arr, double p, double alpha, int nonneg,
-                 int skip, int32_t* bad_iter, int use_graph, double* elapsed_host, void* x_hist,
-                 void* stream);
+                 int skip, double omega, int32_t* bad_iter, int use_graph, double* elapsed_host,
+                 void* x_hist, void* stream);
 
 /* PDHGSkip-2 / PDHG on the implicit splitting K = A (Radon), TV in the
  * warm-started FGP prox with optional u >= 0 (problems.py:162-184,

@@ -55,6 +55,8 @@ SIGNATURES = {
     "psb_fgp2d_finalize": [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _vp,
                            _i64, _vp],
     "psb_aprojgd_dual_rof": [_i32, _vp, _vp, _i32, _i32, _dbl, _dbl, _i32, _vp, _vp],
+    "psb_dual_rof_run": [_i32, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _dbl, _dbl, _dbl, _dbl, _vp,
+                         _i32, _vp, _i32, _vp, _vp, _vp],
     "psb_tv_prox2d": [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _dbl, _vp, _i32, _vp, _i32, _i32,
                       _i32, _i32, _i32, _dbl, _vp, _i64, _vp],
     "psb_sumsq": [_i32, _vp, _vp, _i64, _i64, _vp, _vp],
@@ -81,7 +83,7 @@ SIGNATURES = {
     "psb_pdhg_step": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _dbl, _dbl, _dbl, _dbl,
                       _dbl, _i32, _vp],
     "psb_pdhg_run": [_i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl, _dbl, _vp, _vp, _dbl,
-                     _dbl, _i32, _i32, _vp, _i32, _vp, _vp, _vp],
+                     _dbl, _i32, _i32, _dbl, _vp, _i32, _vp, _vp, _vp],
     "psb_ct_implicit_run": [_i32, _i32, _geo, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _dbl,
                             _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp],
     "psb_blur2d": [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _i32, _i32, _vp],

@@ -150,6 +150,62 @@ __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
 
 template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
 
+// ---- sparse per-iteration device clock of the run drivers ------------------
+// An event record is a graph node that costs several microseconds inside a
+// captured run -- as much as a whole 256^2 iteration -- so the drivers record
+// the device clock at most ~64 times per run (every `stride`-th iteration and
+// the last one) and fill elapsed[k] in between by linear interpolation; the
+// final value (the run's total device time) is exact.
+struct IterClock {
+  std::vector<cudaEvent_t> ev;  // ev[0] = start, ev[j + 1] = after iteration at[j]
+  std::vector<int> at;
+  int K = 0, stride = 1;
+  unsigned flags = 0;
+  bool on = false;
+  void begin(double* out, int K_, cudaStream_t st, bool graph) {
+    on = out != nullptr && K_ > 0;
+    if (!on) return;
+    K = K_;
+    stride = K > 64 ? (K + 63) / 64 : 1;
+    flags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+    ev.resize(1);
+    cudaEventCreate(&ev[0]);
+    cudaEventRecordWithFlags(ev[0], st, flags);
+  }
+  void mark(int k, cudaStream_t st) {  // after iteration k was enqueued
+    if (!on || ((k + 1) % stride != 0 && k != K - 1)) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecordWithFlags(e, st, flags);
+    ev.push_back(e);
+    at.push_back(k);
+  }
+  void finish(double* out, cudaStream_t sync_stream, bool ok) {
+    if (!on) return;
+    cudaStreamSynchronize(sync_stream);
+    std::vector<double> t(at.size(), std::nan(""));
+    for (size_t j = 0; j < at.size(); ++j) {
+      float ms = 0.f;
+      if (ok && cudaEventElapsedTime(&ms, ev[0], ev[j + 1]) == cudaSuccess)
+        t[j] = ms * 1e-3;
+      else
+        (void)cudaGetLastError();
+    }
+    int k0 = -1;
+    double t0 = 0.0;
+    for (size_t j = 0; j < at.size(); ++j) {
+      const int k1 = at[j];
+      for (int k = k0 + 1; k <= k1; ++k) out[k] = t0 + (t[j] - t0) * (k - k0) / (double)(k1 - k0);
+      k0 = k1;
+      t0 = t[j];
+    }
+    for (int k = k0 + 1; k < K; ++k) out[k] = std::nan("");  // run stopped early
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    at.clear();
+  }
+};
+
 // ---- programmatic dependent launch -------------------------------------------
 // Every kernel of a launch chain starts with pdl_enter(): it lets the NEXT
 // kernel in the stream begin launching right away and then waits until the

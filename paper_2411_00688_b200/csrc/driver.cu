@@ -188,12 +188,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   // inside a capture an event record must be an explicit (external) graph node
   // to be usable for timing afterwards
   const unsigned rec_flags = use_graph ? cudaEventRecordExternal : cudaEventRecordDefault;
-  std::vector<cudaEvent_t> evs;
-  if (elapsed) {
-    evs.resize(K + 1, nullptr);
-    for (auto& e : evs) PSB_CUDA(cudaEventCreate(&e));
-    PSB_CUDA(cudaEventRecordWithFlags(evs[0], st, rec_flags));
-  }
+  IterClock clk;
+  clk.begin(elapsed, K, st, use_graph != 0);
   // optional per-iteration timing of the FGP burst (bench roofline)
   std::vector<cudaEvent_t> fev;
   if (fgp_time) {
@@ -202,7 +198,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   }
   int rc = PSB_OK;
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
-    if (elapsed && k > 0) cudaEventRecordWithFlags(evs[k], st, rec_flags);
+    if (k > 0) clk.mark(k - 1, st);
     if (x_hist && k > 0 && rc == PSB_OK)  // iterate of outer iteration k-1 (device IterationLog)
       if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (k - 1) * x_bytes, x, x_bytes,
                           cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -245,7 +241,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, x, x_bytes,
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       rc = fail(PSB_ERR_CUDA, "x history copy failed");
-  if (elapsed && rc == PSB_OK) cudaEventRecordWithFlags(evs[K], st, rec_flags);
+  if (rc == PSB_OK) clk.mark(K - 1, st);
   if (use_graph) {
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &graph);
@@ -290,15 +286,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     cudaError_t e = cudaStreamSynchronize(use_graph ? user_stream : st);
     if (rc == PSB_OK && e != cudaSuccess)
       rc = fail(PSB_ERR_CUDA, std::string("run: ") + cudaGetErrorString(e));
-    for (int k = 0; k < K && rc == PSB_OK; ++k) {
-      float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, evs[0], evs[k + 1]) == cudaSuccess)
-        elapsed[k] = ms * 1e-3;
-      else
-        elapsed[k] = std::nan(""), (void)cudaGetLastError();
-    }
-    for (auto e : evs) cudaEventDestroy(e);
   }
+  clk.finish(elapsed, use_graph ? user_stream : st, rc == PSB_OK);
   return rc;
 }
 

@@ -72,6 +72,10 @@ def run_proxskip(problem, x0, h0, gamma, skip, iters, log=None, *, use_graph=Non
     if gamma <= 0:
         raise ValueError("run_proxskip: gamma must be positive")
     log = _ensure_log(log)
+    dual = getattr(problem, "_dual_rof", None)
+    if dual is not None and log.passive and iters >= 1:
+        from .solvers import _dual_rof_fused
+        return _dual_rof_fused(dual, "proxskip", x0, gamma, iters, log, skip=skip, h0=h0)
     fused = getattr(problem, "_fused", None)
     if (fused is not None and fused.get("kind") in ("denoise", "deblur")
             and (log.passive or device_loggable(log))):
@@ -256,6 +260,12 @@ def run_pdhgskip1(problem, x0, y0, sigma, tau, omega, skip, iters, log=None):
     if omega < 0:
         raise ValueError("run_pdhgskip1: omega must be nonnegative")
     log = _ensure_log(log)
+    fused = getattr(problem, "_fused", None)
+    if (fused is not None and fused["kind"] == "ct_explicit" and np.isscalar(sigma)
+            and np.isscalar(tau) and (log.passive or device_loggable(log))):
+        # native driver: psb_pdhg_run variant 2 (K^T and the prox on success draws only)
+        return _pdhg_family_fused(problem, x0, y0, None, sigma, tau, skip, iters, log,
+                                  "pdhgskip1", omega=omega)
     log.start(AR.is_host(x0))
     p = skip.p
     coins = skip.coins(iters)
@@ -374,7 +384,8 @@ def _ct_implicit_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
     return AR.like(x, x0), log
 
 
-def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, use_graph=True):
+def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, use_graph=True,
+                       omega=0.0):
     """PDHG (skip is None) / PDHGSkip-2 on K = [A; D] with the fused kernels of
     csrc/radon.cu.  Passive logs run the whole loop natively (psb_pdhg_run);
     observing logs step it from here with the same kernels."""
@@ -386,8 +397,9 @@ def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
     x = AR.to_dev(x0, dt).clone()
     y = AR.to_dev(y0, dt).clone().reshape(-1)
     is_skip = skip is not None
+    variant = 0 if not is_skip else (2 if algo == "pdhgskip1" else 1)
     h = None
-    if is_skip:
+    if variant == 1:
         h = AR.to_dev(h0, dt).clone() if h0 is not None else torch.zeros_like(x)
     xbar = torch.empty_like(x)
     bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
@@ -407,8 +419,8 @@ def _pdhg_family_fused(problem, x0, y0, h0, sigma, tau, skip, iters, log, algo, 
             L.call("psb_pdhg_run", L.dcode(dt), L.C.byref(g), L.ptr(x), L.ptr(y), L.ptr(h),
                    L.ptr(xbar), L.ptr(f["b_dev"]), cc.ctypes.data_as(L.C.c_void_p), K,
                    sig_s, tau_s, L.ptr(sig_a), L.ptr(tau_a), float(p), float(f["alpha"]),
-                   int(bool(f["nonneg"])),
-                   int(is_skip), L.ptr(bad), int(bool(use_graph)), el.ctypes.data_as(L.C.c_void_p),
+                   int(bool(f["nonneg"])), variant, float(omega), L.ptr(bad), int(bool(use_graph)),
+                   el.ctypes.data_as(L.C.c_void_p),
                    L.ptr(hist), L.stream())
             k_bad = int(bad.item())
             if k_bad != INT32_MAX:

@@ -154,3 +154,63 @@ def test_compute_reference_solution(gn):
     assert ref_d.provenance["method"] == "aprojgd-dual"
     q, _ = psb.run_aprojgd(dual.smooth, dual.projector, dual.zero_dual(), 1.0 / 8.0, 6000)
     np.testing.assert_array_equal(ref_d.u_star, psb.primal_from_dual(q, b))
+
+
+def test_dual_rof_fused_drivers_match_reference_and_stepping(gn):
+    """Passive logs run the dual-ROF problems in the native driver
+    (csrc/dualrof.cu): the end points equal the reference trajectories, and
+    longer runs are bitwise the observed (stepped) runs -- same operations in
+    the same order."""
+    b = gn["dr_b"]
+    prob = psb.build_dual_rof(b, 0.5)
+    q0 = prob.zero_dual()
+    g = 1.0 / prob.smooth.lipschitz
+    q, log = psb.run_proxskip(prob.prox_problem(), q0, None, g, psb.SkipConfig(0.3, 1), 30)
+    np.testing.assert_allclose(q, gn["dr_ps_traj"][-1], rtol=1e-12, atol=1e-13)
+    np.testing.assert_array_equal([r.prox_applied for r in log.records], gn["dr_ps_flags"])
+    q, _ = psb.run_pgd(prob.prox_problem(), q0, g, 10)
+    np.testing.assert_allclose(q, gn["dr_pgd_traj"][-1], rtol=1e-12, atol=1e-13)
+    q, _ = psb.run_fista(prob.prox_problem(), q0, g, 10)
+    np.testing.assert_allclose(q, gn["dr_aprojgd_traj"][-1], rtol=1e-12, atol=1e-13)
+    q, _ = psb.run_gd(prob.smooth, q0, g, 5)
+    np.testing.assert_allclose(q, gn["dr_gd_traj"][-1], rtol=1e-12, atol=1e-13)
+
+    rng = np.random.default_rng(8)
+    b2 = rng.random((48, 64))
+    for huber in (0.0, 0.1):
+        pr = psb.build_dual_rof(b2, 0.3, huber)
+        z = pr.zero_dual()
+        g = 1.0 / pr.smooth.lipschitz
+        runs = {
+            "proxskip": lambda log: psb.run_proxskip(pr.prox_problem(), z, None, g,
+                                                     psb.SkipConfig(0.2, 3), 300, log),
+            "pgd": lambda log: psb.run_pgd(pr.prox_problem(), z, g, 200, log),
+            "fista": lambda log: psb.run_fista(pr.prox_problem(), z, g, 200, log),
+            "gd": lambda log: psb.run_gd(pr.smooth, z, g, 100, log),
+            "aprojgd": lambda log: psb.run_aprojgd(pr.smooth, pr.projector, z, g, 200, log),
+        }
+        for name, run in runs.items():
+            fast, _ = run(None)
+            stepped, _ = run(psb.IterationLog(callback=lambda r, x: None))
+            if name == "aprojgd" and huber == 0.0:
+                # plain dual: the FGP-kernel path (different but exact-order kernel)
+                np.testing.assert_allclose(fast, stepped, rtol=1e-12, atol=1e-14)
+            else:
+                np.testing.assert_array_equal(fast, stepped, err_msg=f"{name} huber={huber}")
+
+
+def test_pdhgskip1_native_driver(gn):
+    """PDHGSkip-1 on the explicit CT splitting in the native driver (passive
+    log): the reference's end point, coin accounting, and the stepped run."""
+    sp = _ct(gn)
+    s = 1.0 / np.sqrt(float(gn["ct_nsq"]))
+    p = 0.3
+    x, log = psb.run_pdhgskip1(sp, np.zeros((16, 16)), np.zeros(7 * 23 + 512), s, s, 1.0 / p - 1.0,
+                               psb.SkipConfig(p, 2), 20)
+    np.testing.assert_allclose(x, gn["ct_skip1_traj"][-1], rtol=1e-10, atol=1e-12)
+    np.testing.assert_array_equal([r.prox_applied for r in log.records], gn["ct_skip1_flags"])
+    assert log.records[-1].prox_count == int(np.sum(gn["ct_skip1_flags"]))
+    xs, _, lg = _traj()
+    xstep, _ = psb.run_pdhgskip1(sp, np.zeros((16, 16)), np.zeros(7 * 23 + 512), s, s,
+                                 1.0 / p - 1.0, psb.SkipConfig(p, 2), 20, lg)
+    np.testing.assert_allclose(x, xstep, rtol=1e-12, atol=1e-14)

@@ -155,6 +155,56 @@ def cfg3i(inner=50, K=2000, p=0.1):
     return out
 
 
+def cfg8f():
+    """SURVEY 8(f) rows 2-4 through the native drivers: dual-ROF light-prox
+    ProxSkip / PGD / FISTA (denoise-dual), reference-solution generators,
+    PDHGSkip-1 on the explicit CT splitting, and the device IterationLog."""
+    out = {"config": "8f"}
+    n = 256
+    u = phantoms.random_shapes((n, n), 10, np.random.default_rng(0))
+    b = phantoms.add_noise(u, 0.05, 0)
+    dual = psb.build_dual_rof(b, 0.5)
+    g = 1.0 / dual.smooth.lipschitz
+    K = 20000
+    for name, run in (("proxskip_p0.3", lambda: psb.run_proxskip(dual.prox_problem(), dual.zero_dual(),
+                                                                 None, g, psb.SkipConfig(0.3, 0), K)),
+                      ("pgd", lambda: psb.run_pgd(dual.prox_problem(), dual.zero_dual(), g, K)),
+                      ("fista", lambda: psb.run_fista(dual.prox_problem(), dual.zero_dual(), g, K))):
+        t, _ = timed(run, reps=2)
+        out[f"dual_rof_{name}_it_s"] = K / t
+    t, _ = timed(lambda: psb.run_aprojgd(dual.smooth, dual.projector, dual.zero_dual(), g, 100000),
+                 reps=1)
+    out["aprojgd_dual_100k_seconds"] = t
+    # CT explicit (config 3 geometry, fp64 state): preconditioned PDHG, PDHGSkip-1
+    R = psb.radon_map(psb.RadonGeometry(image_side=512, n_angles=60, n_bins=725))
+    s = R.forward(phantoms.shepp_like(512, 10, np.random.default_rng(0)))
+    bb = phantoms.add_noise(s, 0.01 * s.max(), 0)
+    for prec in ("mixed", "fp32"):
+        prob = psb.build_tv_recon(R, bb, 0.05, nonneg=True, splitting="explicit", precision=prec)
+        sp = prob.saddle_problem
+        t, _ = timed(lambda: psb.run_pdhg_preconditioned(sp, 1000), reps=1)
+        out[f"pdhg_precond_{prec}_it_s"] = 1000 / t
+        st = 1.0 / np.sqrt(sp.norm_K_sq)
+        y0 = np.zeros(60 * 725 + 2 * 512 * 512)
+        t, _ = timed(lambda: psb.run_pdhgskip1(sp, np.zeros((512, 512)), y0, st, st, 9.0,
+                                               psb.SkipConfig(0.1, 0), 2000), reps=1)
+        out[f"pdhgskip1_{prec}_it_s"] = 2000 / t
+    # device IterationLog: config 1 with rel_error + objective every iteration
+    _, b1 = phantoms.config1_data(0)
+    ref = b1
+    for mode in ("passive", "device_log"):
+        def run():
+            prob = psb.build_tv_recon(psb.identity_map(b1.shape), b1, 0.1, inner_budget=100,
+                                      precision="mixed")
+            log = None if mode == "passive" else psb.IterationLog(
+                reference=ref, objective_fn=psb.device_objective(prob))
+            psb.run_proxskip(prob.prox_problem, np.zeros_like(b1), None, 1.0,
+                             psb.SkipConfig(0.1, 0), 500, log)
+        t, _ = timed(run, reps=2)
+        out[f"config1_{mode}_it_s"] = 500 / t
+    return out
+
+
 def cfg5(side=1024, K=200, inner=20):
     torch.manual_seed(0)
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -200,7 +250,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,5")
     ap.add_argument("--side5", type=int, default=1024)
     args = ap.parse_args()
-    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "3i": cfg3i, "5": lambda: cfg5(args.side5)}
+    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "3i": cfg3i, "8f": cfg8f, "5": lambda: cfg5(args.side5)}
     for c in args.configs.split(","):
         r = fns[c]()
         print(json.dumps(r), flush=True)
