@@ -213,14 +213,16 @@ int psb_skip_chain(int dtype_outer, int dtype_fgp, void* x, const void* b, const
  *   x_hist (nullable, device, K*n*H*W of dtype_outer) receives the iterate
  *   after every outer iteration (device IterationLog; forces the streaming
  *   path, since the cluster path defers skipped iterations).  The PDHG and
- *   implicit-CT drivers below take the same x_hist (K*n*n). */
+ *   implicit-CT drivers below take the same x_hist (K*n*n).
+ *   algo 0 = ProxSkip, 1 = FISTA (solvers.py:148-168; coins all set, p = 1,
+ *   aux = x_prev then xbar, 2*n*H*W of dtype_outer, x_prev initialised to x0). */
 int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
                              void* z, void* q, int64_t n, int H, int W, const uint8_t* coins_host,
                              int K, double gamma, double p, double alpha, int n_inner,
                              int accelerated, int nonneg, double* last_weight_host,
                              int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
-                             double* elapsed_host, double* fgp_time_host, void* x_hist,
-                             void* stream);
+                             double* elapsed_host, double* fgp_time_host, void* x_hist, int algo,
+                             void* aux, void* stream);
 
 /* ---- parallel-beam projector, operators.py:189-292 (matrix-free) ------------
  * Geometry of RadonGeometry (operators.py:189-215) plus the sample lattice of
@@ -318,8 +320,8 @@ int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void*
                             const uint8_t* coins_host, int K, double gamma, double p, double alpha,
                             int n_inner, int accelerated, int nonneg, double* last_weight_host,
                             int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
-                            double* elapsed_host, double* fgp_time_host, void* x_hist,
-                            void* stream);
+                            double* elapsed_host, double* fgp_time_host, void* x_hist, int algo,
+                            void* aux, void* stream);
 
 #ifdef __cplusplus
 }

@@ -71,7 +71,7 @@ SIGNATURES = {
                           _i32, _i32, _dbl, _dbl, _vp, _i32, _vp],
     "psb_proxskip_denoise_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp,
                                  _i32, _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp, _vp, _vp, _i32,
-                                 _vp, _vp, _vp, _vp],
+                                 _vp, _vp, _vp, _i32, _vp, _vp],
     "psb_cluster_max_active": [_vp],
     "psb_fgp3d_iter": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32,
                        _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
@@ -90,7 +90,7 @@ SIGNATURES = {
     "psb_blur_grad2d": [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _vp],
     "psb_proxskip_deblur_run": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp,
                                 _vp, _i32, _i32, _vp, _i32, _dbl, _dbl, _dbl, _i32, _i32, _i32,
-                                _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
+                                _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp],
 }
 
 

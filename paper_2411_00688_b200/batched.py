@@ -101,7 +101,7 @@ class BatchedTvDenoise:
                self.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(self.bad), int(bool(use_graph)),
                self.elapsed.ctypes.data_as(L.C.c_void_p) if record_elapsed else None,
                fgp_time.ctypes.data_as(L.C.c_void_p) if fgp_time is not None else None,
-               None, L.stream())
+               None, 0, None, L.stream())
         return self.x
 
     def check_finite(self):

@@ -38,6 +38,10 @@ int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
               const double* betas_host, cudaStream_t st);
+int fista_extrap(int dto, void* x, void* xprev, void* xbar, int64_t count, double beta,
+                 cudaStream_t st);
+int fista_pre(int dto, int dtf, const void* xbar, const void* gb, int ident, void* z, int64_t count,
+              double gamma, cudaStream_t st);
 int skip_flush(int dto, void* x, const void* b, const void* h, const int32_t* pend,
                const int32_t* kfirst, int64_t n, int64_t HW, double gamma, int32_t* bad,
                cudaStream_t st);
@@ -53,6 +57,10 @@ struct Fidelity {
   int separable = 1;
   void* g = nullptr;
   void* scratch = nullptr;
+  // FISTA (algo 1): x_prev and xbar buffers (n*H*W of the outer dtype each)
+  int fista = 0;
+  void* xprev = nullptr;
+  void* xbar = nullptr;
 };
 
 namespace {
@@ -121,7 +129,14 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   // (an iterate history needs x materialised every iteration: streaming path)
   const bool use_cluster = fid.kind == 0 && dtf == PSB_F32 && cluster_shape_ok(H, W) &&
                            n_inner <= 1024 && !(no_cluster && no_cluster[0] == '1') &&
-                           x_hist == nullptr;
+                           x_hist == nullptr && !fid.fista;
+  PSB_REQUIRE(!fid.fista || (fid.xprev && fid.xbar), "fista: x_prev / xbar buffers missing");
+  // FISTA's outer momentum (solvers.py:156-160): beta_k = (t_k - 1)/t_{k+1}, t_0 = 1
+  std::vector<double> fbeta;
+  if (fid.fista) {
+    fbeta.resize(K);
+    fista_betas(K, fbeta.data());
+  }
   const size_t x_bytes = (size_t)n * HW * (dto == PSB_F32 ? 4 : 8);
   std::vector<int32_t> pend, kfirst, fl_pend(n, 0), fl_kfirst(n, 0);
   std::vector<float> beta_f(n_inner, 0.f);
@@ -216,6 +231,14 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       continue;
     }
     const int ident = fid.kind == 0;
+    if (fid.fista) {  // xbar = x + beta (x - x_prev); z = xbar - gamma g(xbar)
+      rc = fista_extrap(dto, x, fid.xprev, fid.xbar, n * HW, fbeta[k], st);
+      if (!rc && !ident)
+        rc = blur_grad2d(dto, fid.xbar, b, fid.g, H, W, fid.taps2d, fid.taps1d, fid.ksize,
+                         fid.separable, fid.scratch, st);
+      if (!rc) rc = fista_pre(dto, dtf, fid.xbar, ident ? b : fid.g, ident, z, n * HW, gamma, st);
+      if (rc) break;
+    } else {
     if (!ident) {
       rc = blur_grad2d(dto, x, b, fid.g, H, W, fid.taps2d, fid.taps1d, fid.ksize, fid.separable,
                        fid.scratch, st);
@@ -223,6 +246,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     }
     rc = proxskip_pre(dto, dtf, x, ident ? b : fid.g, ident, h, z, n, HW, coins_d + (int64_t)k * n,
                       gamma, hcoef, bad, k, st);
+    }
     const int na = (int)(off[k + 1] - off[k]);
     if (rc || na == 0) continue;
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
@@ -230,8 +254,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                    n_inner, accelerated, nonneg, 0.125, beta.data(), st);
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
     if (rc == PSB_OK)
-      rc = proxskip_post(dto, dtf, x, ident ? b : fid.g, ident, h, z, q, qps, act_d + off[k], na,
-                         H, W, n_inner, nonneg, gamma, pg, bad, k, st);
+      rc = proxskip_post(dto, dtf, x, ident ? b : fid.g, ident, fid.fista ? nullptr : h, z, q, qps,
+                         act_d + off[k], na, H, W, n_inner, nonneg, gamma, pg, bad, k, st);
   }
 
   if (use_cluster && rc == PSB_OK)  // remaining deferred skip iterations
@@ -299,8 +323,13 @@ extern "C" int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x,
                                         double alpha, int n_inner, int accelerated, int nonneg,
                                         double* last_weight_host, int64_t* prox_count_host,
                                         int32_t* bad_iter, int use_graph, double* elapsed_host,
-                                        double* fgp_time_host, void* x_hist, void* stream) {
+                                        double* fgp_time_host, void* x_hist, int algo, void* aux,
+                                        void* stream) {
   psb::Fidelity fid;
+  fid.fista = algo == 1;
+  fid.xprev = aux;
+  fid.xbar = aux ? static_cast<char*>(aux) + (size_t)n * H * W * (dtype_outer == PSB_F32 ? 4 : 8)
+                 : nullptr;
   return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
                               gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
                               prox_count_host, bad_iter, use_graph, elapsed_host, fgp_time_host,
@@ -315,9 +344,13 @@ extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, 
                                        int accelerated, int nonneg, double* last_weight_host,
                                        int64_t* prox_count_host, int32_t* bad_iter, int use_graph,
                                        double* elapsed_host, double* fgp_time_host, void* x_hist,
-                                       void* stream) {
+                                       int algo, void* aux, void* stream) {
   psb::Fidelity fid;
   fid.kind = 1;
+  fid.fista = algo == 1;
+  fid.xprev = aux;
+  fid.xbar = aux ? static_cast<char*>(aux) + (size_t)H * W * (dtype_outer == PSB_F32 ? 4 : 8)
+                 : nullptr;
   fid.taps2d = taps2d;
   fid.taps1d = taps1d;
   fid.ksize = ksize;

@@ -79,10 +79,12 @@ __global__ void proxskip_post_kernel(TO* __restrict__ x, const TO* __restrict__ 
       qb[HW + i] = yx;
     }
     const int64_t o = base + i;
-    const TO xo = x[o], ho = h[o];
-    const TO xhat = A::add(A::sub(xo, A::mul(gamma, grad_at<TO, IDENT>(xo, gb, o))), A::mul(gamma, ho));
     const TO xn = (TO)uf;
-    h[o] = A::add(ho, A::mul(pg, A::sub(xn, xhat)));
+    if (h) {  // ProxSkip control variate (skip.py:74); FISTA passes h = NULL
+      const TO xo = x[o], ho = h[o];
+      const TO xhat = A::add(A::sub(xo, A::mul(gamma, grad_at<TO, IDENT>(xo, gb, o))), A::mul(gamma, ho));
+      h[o] = A::add(ho, A::mul(pg, A::sub(xn, xhat)));
+    }
     x[o] = xn;
     ok &= finite(xn);
   }
@@ -171,6 +173,72 @@ int skip_chain(int dto, int dtf, void* x, const void* b, const void* h, void* z,
   else
     return fail(PSB_ERR_VALUE, "skip chain: unsupported dtype pair");
   PSB_LAUNCHED("skip_chain");
+  return PSB_OK;
+}
+
+// ---- FISTA on the implicit splitting (solvers.py:148-168) -------------------
+// xbar = x + beta (x - x_prev), x_prev <- x; then the prox input
+// z = xbar - gamma g(xbar) (identity: g = xbar - b; blur: g from
+// blur_grad2d(xbar)), the FGP prox, and the post kernel with h = NULL (x = u).
+template <class TO>
+__global__ void fista_extrap_kernel(TO* __restrict__ x, TO* __restrict__ xprev,
+                                    TO* __restrict__ xbar, int64_t count, TO beta) {
+  using A = Ar<TO>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const TO xo = x[i];
+    xbar[i] = A::add(xo, A::mul(beta, A::sub(xo, xprev[i])));
+    xprev[i] = xo;
+  }
+}
+
+template <class TO, class TF, bool IDENT>
+__global__ void fista_pre_kernel(const TO* __restrict__ xbar, const TO* __restrict__ gb,
+                                 TF* __restrict__ z, int64_t count, TO gamma) {
+  using A = Ar<TO>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const TO xb = xbar[i];
+    const TO g = IDENT ? A::sub(xb, gb[i]) : gb[i];
+    z[i] = (TF)A::add(xb, A::mul(-gamma, g));
+  }
+}
+
+int fista_extrap(int dto, void* x, void* xprev, void* xbar, int64_t count, double beta,
+                 cudaStream_t st) {
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 16LL * sm_count())));
+  if (dto == PSB_F32)
+    fista_extrap_kernel<float><<<grid, 256, 0, st>>>((float*)x, (float*)xprev, (float*)xbar, count,
+                                                     (float)beta);
+  else
+    fista_extrap_kernel<double><<<grid, 256, 0, st>>>((double*)x, (double*)xprev, (double*)xbar,
+                                                      count, beta);
+  PSB_LAUNCHED("fista_extrap");
+  return PSB_OK;
+}
+
+int fista_pre(int dto, int dtf, const void* xbar, const void* gb, int ident, void* z, int64_t count,
+              double gamma, cudaStream_t st) {
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 16LL * sm_count())));
+  auto go = [&](auto to, auto tf) {
+    using TO = decltype(to);
+    using TF = decltype(tf);
+    if (ident)
+      fista_pre_kernel<TO, TF, true><<<grid, 256, 0, st>>>((const TO*)xbar, (const TO*)gb, (TF*)z,
+                                                           count, (TO)gamma);
+    else
+      fista_pre_kernel<TO, TF, false><<<grid, 256, 0, st>>>((const TO*)xbar, (const TO*)gb, (TF*)z,
+                                                            count, (TO)gamma);
+  };
+  if (dto == PSB_F32 && dtf == PSB_F32)
+    go(float{}, float{});
+  else if (dto == PSB_F64 && dtf == PSB_F32)
+    go(double{}, float{});
+  else if (dto == PSB_F64 && dtf == PSB_F64)
+    go(double{}, double{});
+  else
+    return fail(PSB_ERR_VALUE, "fista: unsupported dtype pair");
+  PSB_LAUNCHED("fista_pre");
   return PSB_OK;
 }
 

@@ -188,9 +188,10 @@ def _drive(log, iters, coins, shape, dtype, chunk, state, tensors, base_inner, i
 
 
 def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_graph,
-                       fgp_time=None):
+                       fgp_time=None, algo="proxskip"):
     """Whole run inside the native driver (psb_proxskip_denoise_run /
-    psb_proxskip_deblur_run): no host round trip per iteration."""
+    psb_proxskip_deblur_run): no host round trip per iteration.  algo="fista"
+    runs FISTA (solvers.py:148-168) in the same driver (every coin set)."""
     log.start(AR.is_host(x0))
     st = problem.tv_state
     H, W = st.shape
@@ -202,6 +203,10 @@ def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_grap
     bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
     if use_graph is None:
         use_graph = H * W <= 1024 * 1024
+    aux = None
+    if algo == "fista":  # x_prev (= x0) and xbar buffers
+        aux = torch.empty((2,) + tuple(x.shape), dtype=dt, device="cuda")
+        aux[0].copy_(x)
     base_inner = st.total_inner_iterations
     vp = L.C.c_void_p
     if fused["kind"] == "deblur":
@@ -223,7 +228,8 @@ def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_grap
         tail = (cc.ctypes.data_as(vp), K, float(gamma), float(skip.p), float(problem.alpha),
                 st.inner_iters, int(bool(st.accelerated)), int(bool(st.nonneg)),
                 lw.ctypes.data_as(vp), pc.ctypes.data_as(vp), L.ptr(bad), int(bool(use_graph)),
-                el.ctypes.data_as(vp), ft, L.ptr(hist), L.stream())
+                el.ctypes.data_as(vp), ft, L.ptr(hist), 1 if algo == "fista" else 0, L.ptr(aux),
+                L.stream())
         if fused["kind"] == "denoise":
             L.call("psb_proxskip_denoise_run", L.dcode(dt), L.dcode(st.dtype), L.ptr(x),
                    L.ptr(fused["b_dev"]), L.ptr(h), L.ptr(z), L.ptr(st.slots), 1, H, W, *tail)
@@ -234,7 +240,7 @@ def _proxskip_tv_fused(problem, fused, x0, h0, gamma, skip, iters, log, use_grap
                    int(sep), *tail)
         k_bad = int(bad.item())
         if k_bad != INT32_MAX:
-            raise DivergenceError(k0 + k_bad, "proxskip")
+            raise DivergenceError(k0 + k_bad, algo)
         st.last_weight = None if np.isnan(lw[0]) else float(lw[0])
         st.total_inner_iterations += st.inner_iters * int(pc[0])
         return el

@@ -189,3 +189,19 @@ def test_large_tv_prox_properties():
         qf = q * torch.clamp(0.05 / torch.clamp(mag, min=1e-300), max=1.0)
         gaps.append(psb.dual_gap_rof(x.double(), qf, 0.05))
     assert gaps[1] < gaps[0]
+
+
+@pytest.mark.parametrize("prec", ["mixed", "fp64"])
+def test_fista_native_equals_stepped_denoise(prec):
+    """FISTA on the identity fidelity: the native driver (passive log) and the
+    stepped run (observing log) execute the same operations."""
+    b = np.random.default_rng(9).random((40, 52))
+    out = []
+    for log in (None, psb.IterationLog(callback=lambda r, x: None)):
+        prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=7, precision=prec)
+        x, _ = psb.run_fista(prob.prox_problem, np.zeros_like(b), 1.0, 25, log)
+        out.append(x)
+    if prec == "fp64":
+        np.testing.assert_array_equal(out[0], out[1])
+    else:
+        assert rel(out[0], out[1]) < 1e-12

@@ -295,6 +295,12 @@ def test_deblur_trajectories_fp64(golden):
     xs, _, log = _traj_log()
     psb.run_fista(prob.prox_problem, np.zeros_like(b), 1.0 / L, 8, log)
     np.testing.assert_allclose(np.stack(xs), g["db_fista_traj"], rtol=1e-13, atol=1e-15)
+    # FISTA in the native driver (passive log) reaches the same end point
+    prob = psb.build_tv_recon(A, b, 0.02, inner_budget=5, precision="fp64")
+    x, log = psb.run_fista(prob.prox_problem, np.zeros_like(b), 1.0 / L, 8)
+    np.testing.assert_allclose(x, g["db_fista_traj"][-1], rtol=1e-13, atol=1e-15)
+    assert [r.prox_count for r in log.records] == list(range(1, 9))
+    assert prob.tv_state.total_inner_iterations == 8 * 5
 
 
 @pytest.mark.slow
