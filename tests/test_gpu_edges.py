@@ -205,3 +205,20 @@ def test_fista_native_equals_stepped_denoise(prec):
         np.testing.assert_array_equal(out[0], out[1])
     else:
         assert rel(out[0], out[1]) < 1e-12
+
+
+@pytest.mark.parametrize("prec,shape", [("fp64", (40, 52)), ("mixed", (256, 256))])
+def test_pgd_native_equals_stepped(prec, shape):
+    """run_pgd with a passive log runs the native driver as ProxSkip(p = 1),
+    which is PGD operation for operation (skip.py:62-64)."""
+    b = np.random.default_rng(10).random(shape)
+    out = []
+    for log in (None, psb.IterationLog(callback=lambda r, x: None)):
+        prob = psb.build_tv_recon(psb.identity_map(b.shape), b, 0.1, inner_budget=7, precision=prec)
+        x, lg = psb.run_pgd(prob.prox_problem, np.zeros_like(b), 1.0, 12, log)
+        out.append(x)
+        assert lg.records[-1].prox_count == 12
+    if prec == "fp64":
+        np.testing.assert_array_equal(out[0], out[1])
+    else:
+        assert rel(out[0], out[1]) < 2e-6  # cluster kernel (fp32 FGP) vs streaming path
