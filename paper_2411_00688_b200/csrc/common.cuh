@@ -150,6 +150,52 @@ __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
 
 template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
 
+// ---- optional CUDA-graph capture of a run driver's launch sequence ---------
+// Capture needs a capturable (non-legacy) stream: the run is enqueued on a
+// private stream ordered after the caller's stream, captured, instantiated,
+// launched once, and the caller's stream is ordered after it.  Without
+// use_graph the launches go to the caller's stream directly.
+struct CapturedRun {
+  cudaStream_t user = nullptr, st = nullptr, priv = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  bool graph = false;
+  int begin(cudaStream_t user_stream, bool use_graph) {
+    user = st = user_stream;
+    graph = use_graph;
+    if (!graph) return PSB_OK;
+    PSB_CUDA(cudaStreamCreateWithFlags(&priv, cudaStreamNonBlocking));
+    PSB_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    PSB_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    PSB_CUDA(cudaEventRecord(ev_in, user));
+    PSB_CUDA(cudaStreamWaitEvent(priv, ev_in, 0));
+    st = priv;
+    PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    return PSB_OK;
+  }
+  // ends the capture (always), launches the graph if rc is still OK
+  int end(int rc) {
+    if (!graph) return rc;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (rc == PSB_OK && e != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (rc == PSB_OK && (e = cudaGraphInstantiate(&exec, g, 0)) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    if (rc == PSB_OK && (e = cudaGraphLaunch(exec, st)) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+    cudaEventRecord(ev_out, st);
+    cudaStreamWaitEvent(user, ev_out, 0);
+    if (exec) cudaGraphExecDestroy(exec);  // deferred by the runtime until the launch completes
+    if (g) cudaGraphDestroy(g);
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_out);
+    cudaStreamDestroy(priv);
+    (void)cudaGetLastError();
+    return rc;
+  }
+};
+
 // ---- sparse per-iteration device clock of the run drivers ------------------
 // An event record is a graph node that costs several microseconds inside a
 // captured run -- as much as a whole 256^2 iteration -- so the drivers record

@@ -185,20 +185,9 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   const int32_t* act_d = static_cast<const int32_t*>(d_act.p);
   const uint8_t* rep_d = static_cast<const uint8_t*>(d_rep.p);
 
-  // Graph capture needs a capturable (non-legacy) stream: run on a private
-  // stream ordered after / before the caller's stream with events.
-  cudaStream_t st = user_stream;
-  cudaStream_t priv = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  if (use_graph) {
-    PSB_CUDA(cudaStreamCreateWithFlags(&priv, cudaStreamNonBlocking));
-    PSB_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-    PSB_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-    PSB_CUDA(cudaEventRecord(ev_in, user_stream));
-    PSB_CUDA(cudaStreamWaitEvent(priv, ev_in, 0));
-    st = priv;
-    PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  }
+  CapturedRun cap;
+  if (int rc0 = cap.begin(user_stream, use_graph != 0)) return rc0;
+  cudaStream_t st = cap.st;
 
   // inside a capture an event record must be an explicit (external) graph node
   // to be usable for timing afterwards
@@ -266,30 +255,9 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       rc = fail(PSB_ERR_CUDA, "x history copy failed");
   if (rc == PSB_OK) clk.mark(K - 1, st);
-  if (use_graph) {
-    cudaGraph_t graph = nullptr;
-    cudaError_t e = cudaStreamEndCapture(st, &graph);
-    if (rc == PSB_OK && e != cudaSuccess)
-      rc = fail(PSB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    cudaGraphExec_t exec = nullptr;
-    if (rc == PSB_OK) {
-      e = cudaGraphInstantiate(&exec, graph, 0);
-      if (e != cudaSuccess) rc = fail(PSB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    }
-    if (rc == PSB_OK) {
-      e = cudaGraphLaunch(exec, st);
-      if (e != cudaSuccess) rc = fail(PSB_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
-    }
-    cudaEventRecord(ev_out, st);
-    cudaStreamWaitEvent(user_stream, ev_out, 0);
-    // The device buffers above are freed by DevBuf below; cudaFree waits for
-    // the whole device, so no launch can outlive them.
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    cudaEventDestroy(ev_in);
-    cudaEventDestroy(ev_out);
-    cudaStreamDestroy(priv);
-  }
+  // The device buffers above are freed by DevBuf below; cudaFree waits for the
+  // whole device, so no launch can outlive them.
+  rc = cap.end(rc);
   if (fgp_time) {
     cudaError_t e = cudaStreamSynchronize(use_graph ? user_stream : st);
     if (rc == PSB_OK && e != cudaSuccess)

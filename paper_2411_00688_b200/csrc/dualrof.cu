@@ -120,17 +120,9 @@ int run_t(int algo, const T* b, T* q, T* h, T* work, int H, int W, double alpha,
     }
   }
   const double hc = gamma - gamma / p, pg = p / gamma;  // skip.py:59-74
-  cudaStream_t st = user, priv = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  if (use_graph) {
-    PSB_CUDA(cudaStreamCreateWithFlags(&priv, cudaStreamNonBlocking));
-    PSB_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-    PSB_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-    PSB_CUDA(cudaEventRecord(ev_in, user));
-    PSB_CUDA(cudaStreamWaitEvent(priv, ev_in, 0));
-    st = priv;
-    PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  }
+  CapturedRun cap;
+  if (int rc0 = cap.begin(user, use_graph != 0)) return rc0;
+  cudaStream_t st = cap.st;
   IterClock clk;
   clk.begin(elapsed, K, st, use_graph != 0);
   int rc = PSB_OK;
@@ -155,24 +147,8 @@ int run_t(int algo, const T* b, T* q, T* h, T* work, int H, int W, double alpha,
   if (rc == PSB_OK && cur != 0 &&
       cudaMemcpyAsync(q, slot[cur], sizeof(T) * 2 * HW, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     rc = fail(PSB_ERR_CUDA, "dual rof result copy failed");
-  if (use_graph) {
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    cudaError_t e = cudaStreamEndCapture(st, &graph);
-    if (rc == PSB_OK && e != cudaSuccess) rc = fail(PSB_ERR_CUDA, "dual rof graph capture failed");
-    if (rc == PSB_OK && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess)
-      rc = fail(PSB_ERR_CUDA, "dual rof graph instantiate failed");
-    if (rc == PSB_OK && cudaGraphLaunch(exec, st) != cudaSuccess)
-      rc = fail(PSB_ERR_CUDA, "dual rof graph launch failed");
-    cudaEventRecord(ev_out, st);
-    cudaStreamWaitEvent(user, ev_out, 0);
-    cudaStreamSynchronize(user);
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    cudaEventDestroy(ev_in);
-    cudaEventDestroy(ev_out);
-    cudaStreamDestroy(priv);
-  }
+  rc = cap.end(rc);
+  if (use_graph) cudaStreamSynchronize(user);
   clk.finish(elapsed, user, rc == PSB_OK);
   return rc;
 }
