@@ -50,6 +50,23 @@ int psb_abi_version(void);
 const char* psb_last_error(void);
 int psb_device_sm_count(int* out);
 
+/* ---- context + device buffers: for hosts without a CUDA
+ * runtime of their own.  Every compute entry point below takes plain device
+ * pointers and a stream; psb_ctx_stream() provides one, psb_buf_alloc() the
+ * device memory (zero-filled, stream-ordered), psb_upload()/psb_download()
+ * synchronous host copies staged through pinned memory.  A context is used
+ * by one host thread at a time (the reference's runs are single-threaded,
+ * SURVEY 8(b) "Threading"). */
+typedef struct psb_ctx psb_ctx;
+int psb_ctx_create(int device, psb_ctx** out);
+int psb_ctx_destroy(psb_ctx* ctx);
+void* psb_ctx_stream(psb_ctx* ctx);
+int psb_ctx_sync(psb_ctx* ctx);
+int psb_buf_alloc(psb_ctx* ctx, int64_t bytes, void** dptr);
+int psb_buf_free(psb_ctx* ctx, void* dptr);
+int psb_upload(psb_ctx* ctx, void* dptr, const void* host, int64_t bytes);
+int psb_download(psb_ctx* ctx, void* host, const void* dptr, int64_t bytes);
+
 /* ---- finite differences: operators.py:44-57 (grad_forward), :60-71 (divergence) */
 int psb_grad2d(int dtype, const void* u, void* g, int64_t n, int H, int W, void* stream);
 int psb_div2d(int dtype, const void* q, void* d, int64_t n, int H, int W, void* stream);

@@ -37,6 +37,14 @@ _geo = C.POINTER(RadonGeom)
 
 # name -> argtypes, mirroring include/psb200.h one for one.
 SIGNATURES = {
+    "psb_ctx_create": [_i32, _vp],
+    "psb_ctx_destroy": [_vp],
+    "psb_ctx_stream": [_vp],
+    "psb_ctx_sync": [_vp],
+    "psb_buf_alloc": [_vp, _i64, _vp],
+    "psb_buf_free": [_vp, _vp],
+    "psb_upload": [_vp, _vp, _vp, _i64],
+    "psb_download": [_vp, _vp, _vp, _i64],
     "psb_abi_version": [],
     "psb_last_error": [],
     "psb_device_sm_count": [_vp],
@@ -103,7 +111,8 @@ def _load():
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args
-        fn.restype = C.c_char_p if name == "psb_last_error" else C.c_int
+        fn.restype = (C.c_char_p if name == "psb_last_error" else
+                      C.c_void_p if name == "psb_ctx_stream" else C.c_int)
     return lib
 
 

@@ -222,3 +222,30 @@ def test_pgd_native_equals_stepped(prec, shape):
         np.testing.assert_array_equal(out[0], out[1])
     else:
         assert rel(out[0], out[1]) < 2e-6  # cluster kernel (fp32 FGP) vs streaming path
+
+
+def test_c_host_through_the_abi(tmp_path):
+    """A plain C program (tests/c_host/tv_prox_demo.c) drives the library
+    through include/psb200.h only -- context, buffers, copies, the fp64 TV
+    prox twice (warm start) -- and matches the oracle bit for bit."""
+    import os
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gcc = shutil.which("gcc") or shutil.which("cc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    libdir = os.path.join(root, "paper_2411_00688_b200")
+    exe = tmp_path / "tv_prox_demo"
+    subprocess.run([gcc, "-O2", "-std=c11", os.path.join(root, "tests", "c_host", "tv_prox_demo.c"),
+                    "-I", os.path.join(root, "include"), "-L", libdir, "-lpsb200",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    H, W, inner, wgt = 37, 61, 12, 0.3
+    x = np.random.default_rng(11).standard_normal((H, W))
+    x.tofile(tmp_path / "in.bin")
+    subprocess.run([str(exe), str(H), str(W), str(inner), str(wgt), str(tmp_path / "in.bin"),
+                    str(tmp_path / "out.bin")], check=True)
+    u = np.fromfile(tmp_path / "out.bin", dtype=np.float64).reshape(H, W)
+    st = oc.FgpState.zeros((H, W), inner)
+    oc.fgp_prox(x, wgt, st)
+    np.testing.assert_array_equal(u, oc.fgp_prox(x, wgt, st))

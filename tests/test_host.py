@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "psb200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(psb_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void\*)\s+(psb_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
