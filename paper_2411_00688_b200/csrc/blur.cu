@@ -135,7 +135,7 @@ template <class T>
 int launch_sep(const void* u, const void* b, void* g, int H, int W, const Taps& t, cudaStream_t st) {
   constexpr int TS = 32;
   const size_t sm = sep_smem<T, TS>(t.k);
-  PSB_CUDA(cudaFuncSetAttribute(blur_grad_sep_kernel<T, TS>,
+  PSB_CHECK(func_attr(blur_grad_sep_kernel<T, TS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   dim3 grid((W + TS - 1) / TS, (H + TS - 1) / TS);
   PSB_CUDA(launch_chain(blur_grad_sep_kernel<T, TS>, grid, dim3(256), sm, st, (const T*)u,

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <algorithm>
 #include <utility>
+#include <mutex>
+#include <tuple>
 
 #include "../../include/psb200.h"
 
@@ -31,6 +33,12 @@ int fail(int status, const std::string& msg);
     if (e_ != cudaSuccess)                                                         \
       return ::psb::fail(PSB_ERR_CUDA, std::string(name) + " launch: " +           \
                                            cudaGetErrorString(e_));                \
+  } while (0)
+
+#define PSB_CHECK(call)                                                            \
+  do {                                                                             \
+    const int rc_ = (call);                                                        \
+    if (rc_ != PSB_OK) return rc_;                                                 \
   } while (0)
 
 #define PSB_REQUIRE(cond, msg)                                                     \
@@ -149,6 +157,37 @@ __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
 }
 
 template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
+
+// ---- kernel attributes, set once ---------------------------------------------
+// cudaFuncSetAttribute on a function that has launches in flight can make the
+// driver wait for them, which serialises back-to-back launches of a long
+// kernel; set each (device, kernel, attribute) value once per process.
+inline int func_attr(const void* fn, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, const void*, int, int>> done;  // device, fn, attr, value
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  std::tuple<int, const void*, int, int>* hit = nullptr;
+  for (auto& t : done)
+    if (std::get<0>(t) == dev && std::get<1>(t) == fn && std::get<2>(t) == (int)attr) hit = &t;
+  // a larger dynamic shared memory limit already covers a smaller request
+  if (hit && (std::get<3>(*hit) == value ||
+              (attr == cudaFuncAttributeMaxDynamicSharedMemorySize && std::get<3>(*hit) > value)))
+    return PSB_OK;
+  const cudaError_t e = cudaFuncSetAttribute(fn, attr, value);
+  if (e != cudaSuccess)
+    return fail(PSB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  if (hit)
+    std::get<3>(*hit) = value;
+  else
+    done.emplace_back(dev, fn, (int)attr, value);
+  return PSB_OK;
+}
+template <class K>
+int func_attr(K* kern, cudaFuncAttribute attr, int value) {
+  return func_attr(reinterpret_cast<const void*>(kern), attr, value);
+}
 
 // ---- optional CUDA-graph capture of a run driver's launch sequence ---------
 // Capture needs a capturable (non-legacy) stream: the run is enqueued on a

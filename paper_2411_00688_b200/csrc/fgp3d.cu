@@ -668,7 +668,7 @@ int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     if (vec && make_maps(a, maps)) {
       const size_t sm = sizeof(float) * (size_t)2 * TSTAGE;
-      PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, VMAX, true>,
+      PSB_CHECK(func_attr(fgp3d_march_kernel<T, VMAX, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       dim3 grid((a.W + 32 * VMAX - 1) / (32 * VMAX), (a.H + MTY - 1) / MTY, nz);
       fgp3d_march_kernel<T, VMAX, true><<<grid, (MTY + 2) * 32, sm, st>>>(a, maps);
@@ -679,13 +679,13 @@ int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   std::memset(&maps, 0, sizeof(maps));
   if (vec) {
     const size_t sm = march_smem<T, VMAX>();
-    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, VMAX, false>,
+    PSB_CHECK(func_attr(fgp3d_march_kernel<T, VMAX, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 grid((a.W + 32 * VMAX - 1) / (32 * VMAX), (a.H + MTY - 1) / MTY, nz);
     fgp3d_march_kernel<T, VMAX, false><<<grid, (MTY + 2) * 32, sm, st>>>(a, maps);
   } else {
     const size_t sm = march_smem<T, 1>();
-    PSB_CUDA(cudaFuncSetAttribute(fgp3d_march_kernel<T, 1, false>,
+    PSB_CHECK(func_attr(fgp3d_march_kernel<T, 1, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 grid((a.W + 31) / 32, (a.H + MTY - 1) / MTY, nz);
     fgp3d_march_kernel<T, 1, false><<<grid, (MTY + 2) * 32, sm, st>>>(a, maps);

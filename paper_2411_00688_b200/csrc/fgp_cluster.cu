@@ -597,16 +597,16 @@ int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t
   cfg.numAttrs = 1;
   if (dto == PSB_F32) {
     auto kern = nonneg ? fgp_cluster_kernel<float, true> : fgp_cluster_kernel<float, false>;
-    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
+    PSB_CHECK(func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
     ClusterArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, active, pend,
                          kfirst, rep, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
                          (float)hc, (float)pg, (float)step, bad, k, betas, n_active};
     PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   } else if (dto == PSB_F64) {
     auto kern = nonneg ? fgp_cluster_kernel<double, true> : fgp_cluster_kernel<double, false>;
-    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    PSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
+    PSB_CHECK(func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
     ClusterArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, active, pend,
                           kfirst, rep, n_inner, accelerated, nonneg, (float)weight, gamma, hc, pg,
                           (float)step, bad, k, betas, n_active};
@@ -647,9 +647,9 @@ int cluster_max_active(int* out) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.dynamicSmemBytes = stage_bytes(PSB_F64);
-  PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float, false>,
+  PSB_CHECK(func_attr(fgp_cluster_kernel<float, false>,
                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  PSB_CUDA(cudaFuncSetAttribute(fgp_cluster_kernel<float, false>,
+  PSB_CHECK(func_attr(fgp_cluster_kernel<float, false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)cfg.dynamicSmemBytes));
   PSB_CUDA(cudaOccupancyMaxActiveClusters(out, fgp_cluster_kernel<float, false>, &cfg));
