@@ -9,6 +9,7 @@
 // whole launch sequence is captured into one CUDA graph first (a 256^2 FGP
 // iteration is only a few microseconds of GPU work, so launch cost matters).
 #include <climits>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -65,10 +66,15 @@ struct Fidelity {
 
 namespace {
 
+// Stream-ordered scratch: allocated and released on the caller's stream, so
+// the driver returns as soon as the run is enqueued (a synchronous cudaFree
+// would block the host -- and any timer that waits for the call -- until the
+// device is idle).
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t st = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
   }
 };
 
@@ -158,32 +164,42 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     for (int i = 0; i < n_inner; ++i) beta_f[i] = (float)beta[i];
   }
 
-  DevBuf d_coins, d_act, d_rep, d_pend, d_kfirst, d_flp, d_flk, d_beta;
+  // The whole schedule goes to the device as ONE buffer (one allocation, one
+  // copy): the coin table (streaming path only), active lists, re-projection
+  // flags and, for the cluster path, deferred-skip counts and the momentum table.
+  std::vector<unsigned char> pack;
+  auto put = [&](const void* src, size_t bytes) {
+    const size_t at = (pack.size() + 15) & ~size_t(15);
+    pack.resize(at + bytes);
+    if (bytes) std::memcpy(pack.data() + at, src, bytes);
+    return at;
+  };
+  const size_t o_coins = use_cluster ? 0 : put(coins_host, (size_t)K * n);
+  const size_t o_act = put(act.data(), act.size() * sizeof(int32_t));
+  const size_t o_rep = put(rep.data(), rep.size());
+  size_t o_pend = 0, o_kfirst = 0, o_flp = 0, o_flk = 0, o_beta = 0;
   if (use_cluster) {
-    if (!act.empty()) {
-      PSB_CUDA(cudaMalloc(&d_pend.p, pend.size() * sizeof(int32_t)));
-      PSB_CUDA(cudaMalloc(&d_kfirst.p, kfirst.size() * sizeof(int32_t)));
-      PSB_CUDA(cudaMemcpy(d_pend.p, pend.data(), pend.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-      PSB_CUDA(cudaMemcpy(d_kfirst.p, kfirst.data(), kfirst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    }
-    PSB_CUDA(cudaMalloc(&d_flp.p, n * sizeof(int32_t)));
-    PSB_CUDA(cudaMalloc(&d_flk.p, n * sizeof(int32_t)));
-    PSB_CUDA(cudaMalloc(&d_beta.p, n_inner * sizeof(float)));
-    PSB_CUDA(cudaMemcpy(d_flp.p, fl_pend.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
-    PSB_CUDA(cudaMemcpy(d_flk.p, fl_kfirst.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
-    PSB_CUDA(cudaMemcpy(d_beta.p, beta_f.data(), n_inner * sizeof(float), cudaMemcpyHostToDevice));
+    o_pend = put(pend.data(), pend.size() * sizeof(int32_t));
+    o_kfirst = put(kfirst.data(), kfirst.size() * sizeof(int32_t));
+    o_flp = put(fl_pend.data(), n * sizeof(int32_t));
+    o_flk = put(fl_kfirst.data(), n * sizeof(int32_t));
+    o_beta = put(beta_f.data(), n_inner * sizeof(float));
   }
-  PSB_CUDA(cudaMalloc(&d_coins.p, (size_t)K * n));
-  PSB_CUDA(cudaMemcpy(d_coins.p, coins_host, (size_t)K * n, cudaMemcpyHostToDevice));
-  if (!act.empty()) {
-    PSB_CUDA(cudaMalloc(&d_act.p, act.size() * sizeof(int32_t)));
-    PSB_CUDA(cudaMalloc(&d_rep.p, rep.size()));
-    PSB_CUDA(cudaMemcpy(d_act.p, act.data(), act.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    PSB_CUDA(cudaMemcpy(d_rep.p, rep.data(), rep.size(), cudaMemcpyHostToDevice));
-  }
-  const uint8_t* coins_d = static_cast<const uint8_t*>(d_coins.p);
-  const int32_t* act_d = static_cast<const int32_t*>(d_act.p);
-  const uint8_t* rep_d = static_cast<const uint8_t*>(d_rep.p);
+  DevBuf d_sched;
+  d_sched.st = user_stream;
+  PSB_CUDA(cudaMallocAsync(&d_sched.p, std::max<size_t>(pack.size(), 16), user_stream));
+  PSB_CUDA(cudaMemcpyAsync(d_sched.p, pack.data(), pack.size(), cudaMemcpyHostToDevice,
+                           user_stream));
+  // (pageable source: cudaMemcpyAsync stages `pack` before it returns)
+  unsigned char* dev = static_cast<unsigned char*>(d_sched.p);
+  const uint8_t* coins_d = use_cluster ? nullptr : dev + o_coins;
+  const int32_t* act_d = reinterpret_cast<const int32_t*>(dev + o_act);
+  const uint8_t* rep_d = dev + o_rep;
+  const int32_t* pend_d = reinterpret_cast<const int32_t*>(dev + o_pend);
+  const int32_t* kfirst_d = reinterpret_cast<const int32_t*>(dev + o_kfirst);
+  const int32_t* flp_d = reinterpret_cast<const int32_t*>(dev + o_flp);
+  const int32_t* flk_d = reinterpret_cast<const int32_t*>(dev + o_flk);
+  const float* beta_d = reinterpret_cast<const float*>(dev + o_beta);
 
   CapturedRun cap;
   if (int rc0 = cap.begin(user_stream, use_graph != 0)) return rc0;
@@ -211,11 +227,9 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       const int na = (int)(off[k + 1] - off[k]);
       if (na == 0) continue;
       if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
-      rc = cluster_prox_step(dto, x, b, h, q, qps, act_d + off[k], na,
-                             static_cast<const int32_t*>(d_pend.p) + off[k],
-                             static_cast<const int32_t*>(d_kfirst.p) + off[k], rep_d + off[k],
-                             n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
-                             static_cast<const float*>(d_beta.p), bad, k, st);
+      rc = cluster_prox_step(dto, x, b, h, q, qps, act_d + off[k], na, pend_d + off[k],
+                             kfirst_d + off[k], rep_d + off[k], n_inner, accelerated, nonneg,
+                             weight, gamma, hcoef, pg, 0.125, beta_d, bad, k, st);
       if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
       continue;
     }
@@ -248,15 +262,13 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   }
 
   if (use_cluster && rc == PSB_OK)  // remaining deferred skip iterations
-    rc = skip_flush(dto, x, b, h, static_cast<const int32_t*>(d_flp.p),
-                    static_cast<const int32_t*>(d_flk.p), n, HW, gamma, bad, st);
+    rc = skip_flush(dto, x, b, h, flp_d, flk_d, n, HW, gamma, bad, st);
   if (x_hist && rc == PSB_OK)
     if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, x, x_bytes,
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       rc = fail(PSB_ERR_CUDA, "x history copy failed");
   if (rc == PSB_OK) clk.mark(K - 1, st);
-  // The device buffers above are freed by DevBuf below; cudaFree waits for the
-  // whole device, so no launch can outlive them.
+  // The schedule buffer is released stream-ordered after the run (DevBuf).
   rc = cap.end(rc);
   if (fgp_time) {
     cudaError_t e = cudaStreamSynchronize(use_graph ? user_stream : st);

@@ -16,18 +16,20 @@ idx = np.arange(4096)
 b_host = bench.make_inputs(idx)
 coins = batched.coin_table(0.1, idx, 300)
 s = psb.BatchedTvDenoise(b_host, 0.1, 50, precision="fp32")
-for rep in range(3):
+for variant in ("events", "plain", "graph", "events", "plain", "graph"):
     s.reset()
     s.run_proxskip(coins[:5], 1.0, 0.1)
     torch.cuda.synchronize()
-    f = np.zeros(295)
+    f = np.zeros(295) if variant == "events" else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h0 = time.perf_counter()
     e0.record()
-    s.run_proxskip(coins[5:], 1.0, 0.1, fgp_time=f)
+    s.run_proxskip(coins[5:], 1.0, 0.1, fgp_time=f, use_graph=variant == "graph")
+    h_launch = time.perf_counter() - h0
     e1.record()
     torch.cuda.synchronize()
     h1 = time.perf_counter()
     tot = e0.elapsed_time(e1) / 1e3
-    print(f"rep {rep}: region {tot:.3f}s  kernels {f.sum():.3f}s  gaps {tot - f.sum():.3f}s  "
-          f"host {h1 - h0:.3f}s  -> {295 / tot:.1f} it/s", flush=True)
+    kern = f.sum() if f is not None else float("nan")
+    print(f"{variant:6s}: region {tot:.3f}s  kernels {kern:.3f}s  host-return {h_launch:.3f}s  "
+          f"-> {295 / tot:.1f} it/s", flush=True)
