@@ -165,6 +165,9 @@ class LocalExchange:
         for i, s in enumerate(slabs[1:], start=1):
             s.set_final_dual_below(slabs[i - 1].final_dual_top())
 
+    def agree_bad(self, k):
+        return k
+
 
 class DistExchange:
     """Halo exchange between ranks (one slab per rank, rank order = z order)
@@ -206,6 +209,15 @@ class DistExchange:
         if ops:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
+
+    def agree_bad(self, k):
+        """Global first non-finite iteration: every rank raises the same
+        DivergenceError (the reference stops at the first one, solvers.py:111-113)."""
+        d = self.dist
+        dev = "cuda" if d.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([int(k)], dtype=torch.int64, device=dev)
+        d.all_reduce(t, op=d.ReduceOp.MIN, group=self.group)
+        return int(t.item())
 
     def final_dual(self, slabs):
         (s,) = slabs
@@ -274,8 +286,9 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
     if pend:
         for s in slabs:
             s.flush(pend, len(coins) - pend, gamma)
-    for s in slabs:
-        s.check_finite()
+    kb = exchange.agree_bad(min(int(s.bad.item()) for s in slabs))
+    if kb != INT32_MAX:
+        raise DivergenceError(kb, "proxskip3d")
     return [s.x for s in slabs]
 
 

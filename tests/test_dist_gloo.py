@@ -184,6 +184,33 @@ def test_problem_sharding_two_ranks():
     assert not set(parts[0]) & set(parts[1])
 
 
+def _bad_worker(rank, world, port, local, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out_q.put((rank, DistExchange().agree_bad(local[rank])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_divergence_iteration_agreed_across_ranks():
+    """A non-finite iterate on one slab makes every rank report the same
+    (first) iteration -- the whole-volume run's DivergenceError."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    local = [2 ** 31 - 1, 17, 9]
+    procs = [ctx.Process(target=_bad_worker, args=(r, 3, port, local, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: 9, 1: 9, 2: 9}
+
+
 def test_slab_bounds():
     for Dg, world in [(1024, 8), (23, 5), (7, 7)]:
         b = [slab_bounds(Dg, r, world) for r in range(world)]
