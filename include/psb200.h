@@ -179,6 +179,12 @@ int psb_sumsq_bcast(int dtype, const void* a, const void* b, int64_t n, int64_t 
 int psb_count_below(int dtype, const void* a, int64_t n, int64_t len, double thresh, double* out,
                     void* stream);
 
+/* Bernoulli coin table of many problems (skip.py:16-28): coins[k*n + i] =
+ * Generator(Philox(seeds[i])).random() < p for k < K, bit-identical to numpy
+ * (SeedSequence key derivation + Philox4x64-10 on the device); host in/out. */
+int psb_coin_table(const int64_t* seeds_host, int64_t n, int K, double p, uint8_t* coins_host,
+                   void* stream);
+
 /* ---- ProxSkip outer step, skip.py:46-79 -------------------------------------
  * State x, h (dtype_outer) and prox input z (dtype_fgp), all (n, H, W).
  * `g_or_b`: when ident != 0 it is b and the gradient x - b of the identity

@@ -45,6 +45,7 @@ SIGNATURES = {
     "psb_buf_free": [_vp, _vp],
     "psb_upload": [_vp, _vp, _vp, _i64],
     "psb_download": [_vp, _vp, _vp, _i64],
+    "psb_coin_table": [_vp, _i64, _i32, _dbl, _vp, _vp],
     "psb_abi_version": [],
     "psb_last_error": [],
     "psb_device_sm_count": [_vp],

@@ -34,8 +34,17 @@ def shard_indices(n_total, rank, world):
 
 
 def coin_table(p, seeds, iters):
-    """(iters, N) uint8: column i is SkipConfig(p, seeds[i]).coins(iters)."""
-    return np.ascontiguousarray(np.stack([SkipConfig(p, int(s)).coins(iters) for s in seeds], axis=1))
+    """(iters, N) uint8: column i is SkipConfig(p, seeds[i]).coins(iters), i.e.
+    Generator(Philox(seed)).random() < p per draw (skip.py:27-28) -- generated
+    on the device (psb_coin_table), bit-identical to the numpy stream."""
+    if not 0.0 < p <= 1.0:
+        raise ValueError(f"SkipConfig: p must be in (0, 1], got {p}")
+    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64).reshape(-1))
+    out = np.empty((int(iters), seeds.size), dtype=np.uint8)
+    if out.size:
+        L.call("psb_coin_table", seeds.ctypes.data_as(L.C.c_void_p), seeds.size, int(iters),
+               float(p), out.ctypes.data_as(L.C.c_void_p), L.stream())
+    return out
 
 
 class BatchedTvDenoise:

@@ -249,3 +249,19 @@ def test_c_host_through_the_abi(tmp_path):
     st = oc.FgpState.zeros((H, W), inner)
     oc.fgp_prox(x, wgt, st)
     np.testing.assert_array_equal(u, oc.fgp_prox(x, wgt, st))
+
+
+def test_device_coin_table_is_numpys_philox_stream():
+    """psb_coin_table (SeedSequence + Philox4x64-10 on the device) reproduces
+    Generator(Philox(seed)).random() < p bit for bit (skip.py:27-28)."""
+    seeds = [0, 1, 7, 4095, 2 ** 31 + 5, 2 ** 32, 2 ** 40 + 3, 2 ** 62 + 11] + list(range(100, 140))
+    for p in (0.1, 0.5, 1.0):
+        t = psb.coin_table(p, seeds, 301)
+        assert t.shape == (301, len(seeds)) and t.dtype == np.uint8
+        for j, s in enumerate(seeds):
+            draws = np.random.Generator(np.random.Philox(s)).random(301)
+            np.testing.assert_array_equal(t[:, j], (draws < p).astype(np.uint8))
+    big = psb.coin_table(0.1, np.arange(4096), 300)
+    assert abs(big.mean() - 0.1) < 0.005
+    with pytest.raises(ValueError):
+        psb.coin_table(0.0, [1], 3)

@@ -52,13 +52,8 @@ def test_betas_match_oracle():
     assert _betas(3)[0] == 0.0
 
 
-def test_coin_table_matches_reference_stream():
-    from paper_2411_00688_b200 import SkipConfig, coin_table
-    t = coin_table(0.1, [0, 7, 4095], 300)
-    assert t.shape == (300, 3) and t.dtype == np.uint8
-    for j, s in enumerate([0, 7, 4095]):
-        draws = np.random.Generator(np.random.Philox(s)).random(300)
-        np.testing.assert_array_equal(t[:, j], (draws < 0.1).astype(np.uint8))
+def test_skip_config_coins_match_reference_stream():
+    from paper_2411_00688_b200 import SkipConfig
     np.testing.assert_array_equal(SkipConfig(0.3, 5).coins(25),
                                   np.random.Generator(np.random.Philox(5)).random(25) < 0.3)
 
