@@ -1,0 +1,38 @@
+"""Config-4 strong scaling projected from one GPU: the per-rank workload at
+N ranks is shard_indices(4096, r, N) with no collective on the data path, so
+each rank's device time can be measured alone.  Prints T_1 / (N * T_N) for
+the slowest shard (all shards of N are timed)."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_2411_00688_b200 as psb  # noqa: E402
+from paper_2411_00688_b200 import batched  # noqa: E402
+
+W, K = 5, 295
+out = {}
+b_all = bench.make_inputs(np.arange(4096))
+for n in (1, 2, 4, 8):
+    worst = 0.0
+    for r in range(n):
+        idx = batched.shard_indices(4096, r, n)
+        coins = batched.coin_table(0.1, idx, W + K)
+        s = psb.BatchedTvDenoise(b_all[idx], 0.1, 50, precision="fp32")
+        s.run_proxskip(coins[:W], 1.0, 0.1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s.run_proxskip(coins[W:], 1.0, 0.1)
+        e1.record()
+        torch.cuda.synchronize()
+        worst = max(worst, e0.elapsed_time(e1) / 1e3)
+        del s
+    out[n] = worst
+    print(json.dumps({"n": n, "slowest_rank_s": worst, "it_s": K / worst,
+                      "projected_efficiency": out[1] / (n * worst)}), flush=True)
