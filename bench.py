@@ -40,13 +40,13 @@ BYTES_FGP_MOM = 28   # fp32 per pixel-iteration: x + q_k(2) + q_{k-1}(2) read, q
 BYTES_FGP_FIRST = 20  # first inner iteration (beta = 0): no q_{k-1} read
 CLUSTER = os.environ.get("PSB_NO_CLUSTER", "0") != "1"
 if CLUSTER:
-    KERNEL = ("fgp_cluster_kernel<float>: the whole coin-fired prox step (pre + 50 FGP iterations "
-              "+ post) per 16-CTA cluster, FGP state in registers; the 28 B/px-iter of the "
-              "streaming formulation stay on-chip, so frac > 1 is expected")
-    # ncu dram__bytes_read.sum + dram__bytes_write.sum of fgp_cluster_kernel in this bench
-    # (profiles/r01_launches_bench_cluster_v10.csv): 895.1 MB per launch at 405.3 coin-fired
-    # problems on average = 2.21 MB per problem per launch
-    TRAFFIC_PER_PROBLEM = 895.1e6 / 405.3
+    KERNEL = ("fgp_cluster_run_kernel<float>: the whole timed run segment in ONE launch; each "
+              "16-CTA cluster runs its problems' coin-fired prox calls back to back (skips + 50 "
+              "FGP iterations + post) with z, q in registers and x, b, h in shared memory; the "
+              "28 B/px-iter of the streaming formulation stay on-chip, so frac > 1 is expected")
+    # ncu dram__bytes_read.sum + dram__bytes_write.sum of fgp_cluster_run_kernel per launch,
+    # per problem in the launch (profiles/r01_launches_bench_run.csv)
+    TRAFFIC_PER_PROBLEM_LAUNCH = 2.4e6
 else:
     KERNEL = "fgp2d_iter_kernel<float,4> (streaming, one launch per inner iteration)"
     # profiles/r01_fgp2d_iter_ncu_details.csv: 795 MB per launch at 422 problems
@@ -248,8 +248,7 @@ def run_gpu(args):
     fgp_bytes = active * HW * (BYTES_FGP_FIRST + (INNER - 1) * BYTES_FGP_MOM)
     n_fired_steps = int(np.count_nonzero(active))
     if CLUSTER:
-        # one fused cluster launch per step with a coin-fired problem + the final skip flush
-        launches = n_fired_steps + 1
+        launches = 1  # one fgp_cluster_run_kernel launch for the K timed steps
     else:
         launches = args.steps + n_fired_steps * (INNER + 1)
     stats = np.array([t_local, fgp_t.sum(), float(fgp_bytes.sum()), float(active.sum())])
@@ -308,11 +307,13 @@ def run_gpu(args):
         "fgp_mpx_iter_per_s": inner_rate * HW / 1e6,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
-                     "traffic": TRAFFIC_PER_PROBLEM * float(active.sum()) / max(n_fired_steps, 1),
+                     "traffic": (TRAFFIC_PER_PROBLEM_LAUNCH * len(idx) if CLUSTER else
+                                 TRAFFIC_PER_PROBLEM * float(active.sum()) / max(n_fired_steps, 1)),
                      "kernel": KERNEL,
                      "bytes_per_unit": "28 B/pixel-iteration (20 B at the first inner iteration), "
-                                       "SURVEY 8(d); x per launch = coin-fired problems x 65536 px "
-                                       "x 50 inner iterations",
+                                       "SURVEY 8(d); x units = the timed steps' coin-fired "
+                                       "problem-prox calls x 65536 px x 50 inner iterations "
+                                       "(one launch for all of them on the cluster path)",
                      "peak_source": peak_kind},
         "cpu_baseline": cpu,
         "e2e": {"value": n_e2e / t_e2e, "unit": "outer-iter/s (4096-problem batch)",

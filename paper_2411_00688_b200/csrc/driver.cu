@@ -30,11 +30,12 @@ int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
                 const double* taps2d, const double* taps1d, int k, int separable, void* scratch,
                 cudaStream_t st);
 bool cluster_shape_ok(int H, int W);
-int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
-                      const int32_t* active, int n_active, const int32_t* pend,
-                      const int32_t* kfirst, const uint8_t* rep, int n_inner, int accelerated,
-                      int nonneg, double weight, double gamma, double hc, double pg, double step,
-                      const float* betas, int32_t* bad, int k, cudaStream_t st);
+int cluster_count();
+int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
+                const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
+                const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
+                int nonneg, double weight, double gamma, double hc, double pg, double step,
+                const float* betas, int32_t* bad, cudaStream_t st);
 int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
@@ -43,9 +44,6 @@ int fista_extrap(int dto, void* x, void* xprev, void* xbar, int64_t count, doubl
                  cudaStream_t st);
 int fista_pre(int dto, int dtf, const void* xbar, const void* gb, int ident, void* z, int64_t count,
               double gamma, cudaStream_t st);
-int skip_flush(int dto, void* x, const void* b, const void* h, const int32_t* pend,
-               const int32_t* kfirst, int64_t n, int64_t HW, double gamma, int32_t* bad,
-               cudaStream_t st);
 
 // Fidelity A of the implicit splitting.  kind 0: identity (g = x - b fused
 // into the outer kernels); kind 1: periodic blur (g = A^T(Ax - b) by the
@@ -144,23 +142,47 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     fista_betas(K, fbeta.data());
   }
   const size_t x_bytes = (size_t)n * HW * (dto == PSB_F32 ? 4 : 8);
-  std::vector<int32_t> pend, kfirst, fl_pend(n, 0), fl_kfirst(n, 0);
-  std::vector<float> beta_f(n_inner, 0.f);
+  // Cluster path schedule: every problem's coin-fired iterations (CSR), its
+  // re-projection flag, and problems assigned to the resident clusters
+  // longest-first (a prox call costs n_inner cluster iterations, a skip
+  // iteration next to nothing).
+  std::vector<int32_t> ev_off, ev_k, asg_off, asg;
+  std::vector<uint8_t> rep_p;
+  std::vector<float> beta_f;
+  int G = 0;
   if (use_cluster) {
-    std::vector<int32_t> last(n, -1);  // last outer iteration whose x is materialised
-    pend.resize(act.size());
-    kfirst.resize(act.size());
-    for (int k = 0; k < K; ++k)
+    ev_off.assign(n + 1, 0);
+    for (size_t e = 0; e < act.size(); ++e) ev_off[act[e] + 1] += 1;
+    for (int64_t i = 0; i < n; ++i) ev_off[i + 1] += ev_off[i];
+    ev_k.resize(act.size());
+    rep_p.assign(n, 0);
+    std::vector<int32_t> fill(ev_off.begin(), ev_off.end() - 1);
+    for (int k = 0; k < K; ++k)  // ascending k per problem
       for (int64_t e = off[k]; e < off[k + 1]; ++e) {
         const int32_t i = act[e];
-        pend[e] = k - last[i] - 1;
-        kfirst[e] = last[i] + 1;
-        last[i] = k;
+        if (fill[i] == ev_off[i]) rep_p[i] = rep[e];
+        ev_k[fill[i]++] = k;
       }
-    for (int64_t i = 0; i < n; ++i) {
-      fl_pend[i] = K - 1 - last[i];
-      fl_kfirst[i] = last[i] + 1;
+    G = (int)std::min<int64_t>(n, cluster_count());
+    std::vector<int32_t> order(n);
+    for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t u, int32_t v) {
+      return ev_off[u + 1] - ev_off[u] > ev_off[v + 1] - ev_off[v];
+    });
+    std::vector<double> load(G, 0.0);
+    std::vector<std::vector<int32_t>> bins(G);
+    for (int32_t i : order) {
+      const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[c] += (double)(ev_off[i + 1] - ev_off[i]) * n_inner + 1e-3 * K;
+      bins[c].push_back(i);
     }
+    asg_off.assign(G + 1, 0);
+    asg.reserve(n);
+    for (int c = 0; c < G; ++c) {
+      asg.insert(asg.end(), bins[c].begin(), bins[c].end());
+      asg_off[c + 1] = (int32_t)asg.size();
+    }
+    beta_f.resize(n_inner);
     for (int i = 0; i < n_inner; ++i) beta_f[i] = (float)beta[i];
   }
 
@@ -175,15 +197,16 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     return at;
   };
   const size_t o_coins = use_cluster ? 0 : put(coins_host, (size_t)K * n);
-  const size_t o_act = put(act.data(), act.size() * sizeof(int32_t));
-  const size_t o_rep = put(rep.data(), rep.size());
-  size_t o_pend = 0, o_kfirst = 0, o_flp = 0, o_flk = 0, o_beta = 0;
+  const size_t o_act = use_cluster ? 0 : put(act.data(), act.size() * sizeof(int32_t));
+  const size_t o_rep = use_cluster ? 0 : put(rep.data(), rep.size());
+  size_t o_evo = 0, o_evk = 0, o_repp = 0, o_asgo = 0, o_asg = 0, o_beta = 0;
   if (use_cluster) {
-    o_pend = put(pend.data(), pend.size() * sizeof(int32_t));
-    o_kfirst = put(kfirst.data(), kfirst.size() * sizeof(int32_t));
-    o_flp = put(fl_pend.data(), n * sizeof(int32_t));
-    o_flk = put(fl_kfirst.data(), n * sizeof(int32_t));
-    o_beta = put(beta_f.data(), n_inner * sizeof(float));
+    o_evo = put(ev_off.data(), ev_off.size() * sizeof(int32_t));
+    o_evk = put(ev_k.data(), ev_k.size() * sizeof(int32_t));
+    o_repp = put(rep_p.data(), rep_p.size());
+    o_asgo = put(asg_off.data(), asg_off.size() * sizeof(int32_t));
+    o_asg = put(asg.data(), asg.size() * sizeof(int32_t));
+    o_beta = put(beta_f.data(), beta_f.size() * sizeof(float));
   }
   DevBuf d_sched;
   d_sched.st = user_stream;
@@ -192,14 +215,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                            user_stream));
   // (pageable source: cudaMemcpyAsync stages `pack` before it returns)
   unsigned char* dev = static_cast<unsigned char*>(d_sched.p);
-  const uint8_t* coins_d = use_cluster ? nullptr : dev + o_coins;
+  const uint8_t* coins_d = dev + o_coins;
   const int32_t* act_d = reinterpret_cast<const int32_t*>(dev + o_act);
   const uint8_t* rep_d = dev + o_rep;
-  const int32_t* pend_d = reinterpret_cast<const int32_t*>(dev + o_pend);
-  const int32_t* kfirst_d = reinterpret_cast<const int32_t*>(dev + o_kfirst);
-  const int32_t* flp_d = reinterpret_cast<const int32_t*>(dev + o_flp);
-  const int32_t* flk_d = reinterpret_cast<const int32_t*>(dev + o_flk);
-  const float* beta_d = reinterpret_cast<const float*>(dev + o_beta);
+  auto i32 = [&](size_t o) { return reinterpret_cast<const int32_t*>(dev + o); };
 
   CapturedRun cap;
   if (int rc0 = cap.begin(user_stream, use_graph != 0)) return rc0;
@@ -217,22 +236,19 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     for (auto& e : fev) PSB_CUDA(cudaEventCreate(&e));
   }
   int rc = PSB_OK;
-  for (int k = 0; k < K && rc == PSB_OK; ++k) {
+  if (use_cluster) {  // the whole segment in one launch
+    if (fgp_time) cudaEventRecordWithFlags(fev[0], st, rec_flags);
+    rc = cluster_run(dto, x, b, h, q, qps, i32(o_asgo), i32(o_asg), G, i32(o_evo), i32(o_evk),
+                     dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
+                     0.125, reinterpret_cast<const float*>(dev + o_beta), bad, st);
+    if (fgp_time) cudaEventRecordWithFlags(fev[1], st, rec_flags);
+  }
+  for (int k = 0; k < K && rc == PSB_OK && !use_cluster; ++k) {
     if (k > 0) clk.mark(k - 1, st);
     if (x_hist && k > 0 && rc == PSB_OK)  // iterate of outer iteration k-1 (device IterationLog)
       if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (k - 1) * x_bytes, x, x_bytes,
                           cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         rc = fail(PSB_ERR_CUDA, "x history copy failed");
-    if (use_cluster) {
-      const int na = (int)(off[k + 1] - off[k]);
-      if (na == 0) continue;
-      if (fgp_time) cudaEventRecordWithFlags(fev[2 * k], st, rec_flags);
-      rc = cluster_prox_step(dto, x, b, h, q, qps, act_d + off[k], na, pend_d + off[k],
-                             kfirst_d + off[k], rep_d + off[k], n_inner, accelerated, nonneg,
-                             weight, gamma, hcoef, pg, 0.125, beta_d, bad, k, st);
-      if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
-      continue;
-    }
     const int ident = fid.kind == 0;
     if (fid.fista) {  // xbar = x + beta (x - x_prev); z = xbar - gamma g(xbar)
       rc = fista_extrap(dto, x, fid.xprev, fid.xbar, n * HW, fbeta[k], st);
@@ -261,8 +277,6 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                          act_d + off[k], na, H, W, n_inner, nonneg, gamma, pg, bad, k, st);
   }
 
-  if (use_cluster && rc == PSB_OK)  // remaining deferred skip iterations
-    rc = skip_flush(dto, x, b, h, flp_d, flk_d, n, HW, gamma, bad, st);
   if (x_hist && rc == PSB_OK)
     if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, x, x_bytes,
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -277,7 +291,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     for (int k = 0; k < K; ++k) {
       float ms = 0.f;
       fgp_time[k] = 0.0;
-      if (rc == PSB_OK && off[k + 1] > off[k]) {
+      // (cluster path: one launch for the segment, its time in fgp_time[0])
+      if (rc == PSB_OK && (use_cluster ? k == 0 : off[k + 1] > off[k])) {
         if (cudaEventElapsedTime(&ms, fev[2 * k], fev[2 * k + 1]) == cudaSuccess)
           fgp_time[k] = ms * 1e-3;
         else

@@ -1,28 +1,34 @@
-// Cluster-resident ProxSkip prox step for 256 x 256 problems (BASELINE
-// configs 1 and 4): ONE launch performs, for every coin-fired problem,
+// Cluster-resident ProxSkip runs for 256 x 256 problems (BASELINE configs 1
+// and 4).  ONE launch performs a whole run segment (K outer iterations) of
+// every problem: each 16-CTA thread-block cluster takes its problems one after
+// another (static longest-first assignment computed on the host) and, for a
+// problem, walks its coin-fired iterations k_1 < k_2 < ... in order:
 //
-//   pre   : the deferred skip iterations x <- (x - g(x - b)) + g h (each one
-//           executed, in registers, in the reference's op order), then the
-//           prox input z = (x - g(x - b)) + hc h            (skip.py:66-70)
+//   pre   : the skip iterations since the previous prox call,
+//           x <- (x - g(x - b)) + g h, each one executed in registers in the
+//           reference's op order, then the prox input
+//           z = (x - g(x - b)) + hc h                      (skip.py:66-70)
 //   FGP   : all n_inner accelerated iterations (tv.py:75-80) with the
-//           problem's x, q_k, q_{k-1} resident in REGISTERS of a 16-CTA
-//           thread-block cluster (16 SMs, 512 threads each, 8 pixels per
-//           thread); row halos cross CTA boundaries through distributed
-//           shared memory, column halos through warp shuffles and shared
-//           memory; one cluster barrier per inner iteration
+//           problem's z, q_k, q_{k-1} resident in REGISTERS of the cluster
+//           (16 SMs, 512 threads each, a column strip of 8 rows per thread);
+//           row halos cross CTA boundaries as st.async pushes into the
+//           neighbour's shared memory completing on its mbarrier, column
+//           halos through warp shuffles and shared memory
 //   post  : finalize u = clamp(z + div q_n) (tv.py:89), control variate
-//           h <- h + (p/g)(u - xhat), x <- u, q_n -> warm-start slot 0
-//           (skip.py:68-75)
+//           h <- h + (p/g)(u - xhat), x <- u                (skip.py:68-75)
 //
-// HBM traffic per prox call is x, b, h, q_warm in and x, h, q_warm out
-// (~36 B/px) instead of ~1,450 B/px for 50 streaming FGP launches + pre +
-// post: the inner loop is bound by the SMs, not by HBM.
+// then applies the trailing skip iterations and writes x, h and the warm
+// start back.  Between two prox calls of a problem its x, b, h stay in shared
+// memory and its dual iterate q in registers, so HBM sees each problem once
+// per run segment (~20 B/px in + ~16 B/px out) instead of ~1,450 B/px per
+// prox call for 50 streaming FGP launches + pre + post, and there is no
+// per-iteration launch or grid-wide step boundary at all: the per-problem
+// work items are independent (the reference runs each config-4 problem on
+// its own), which is what lets a single launch balance them across clusters.
 //
-// Skipped iterations are deferred, not dropped: each problem's pending skip
-// count is applied at its next prox call (prologue and epilogue recompute the
-// same chain) or by the flush kernel at the end of the run, so every x update
-// of the reference is executed with bit-identical arithmetic; only the HBM
-// round trips between consecutive skips disappear.
+// Every x update of the reference is executed, in the reference's order, with
+// the same fp arithmetic as the streaming kernels; only the HBM round trips
+// between iterations disappear.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -43,26 +49,25 @@ constexpr int CWARPS_ROW = CW / 32;   // 8 warps across a row group
 constexpr int kMaxBetas = 1024;       // momentum table staged in shared memory
 
 template <class TO>
-struct ClusterArgs {
+struct RunArgs {
   TO* x;
   const TO* b;
   TO* h;
-  float* q;           // warm-start slot 0 of each problem: q + p*qps (channel stride CH*CW)
+  float* q;               // warm-start slot 0 of problem p: q + p*qps (channel stride CH*CW)
   int64_t qps;
-  const int32_t* active;
-  const int32_t* pend;    // deferred skips per active entry
-  const int32_t* kfirst;  // outer-iteration index of the first deferred skip
-  const uint8_t* rep;     // re-project the warm start (tv.py:68-69) per active entry
+  const int32_t* asg_off;  // [G + 1]: cluster c runs problems asg[asg_off[c] .. asg_off[c+1])
+  const int32_t* asg;
+  const int32_t* ev_off;   // [n + 1]: problem p's coin-fired iterations ev_k[ev_off[p] ..]
+  const int32_t* ev_k;     // ascending, 0 .. K-1 (this run segment)
+  const uint8_t* rep;      // [n]: re-project the warm start at the first prox call (tv.py:68-69)
+  int K;
   int n_inner;
   int accelerated;
-  int nonneg;
   float weight;
   TO gamma, hc, pg;
   float step;
-  int32_t* bad;
-  int k;               // this outer iteration (for DivergenceError)
-  const float* betas;  // device table beta[0..n_inner-1]
-  int n_active;        // entries in `active`
+  int32_t* bad;            // [n]: first non-finite iteration (atomicMin)
+  const float* betas;      // device table beta[0..n_inner-1]
 };
 
 template <class TO>
@@ -79,20 +84,18 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
   return remote;
 }
-__device__ __forceinline__ float dsmem_ld(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
+template <class T>
+__device__ __forceinline__ T dsmem_ld(uint32_t addr) {
+  if constexpr (sizeof(T) == 8) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+  } else {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+  }
 }
-
-template <int B>
-__device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool pred) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = pred ? B : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(B), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit_c() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // ---- point-to-point halo rows: st.async into the neighbour's shared memory,
 // completion counted in bytes on the neighbour's mbarrier (no cluster-wide
@@ -146,16 +149,16 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-// Exchange pattern per inner iteration (ONE cluster barrier): at the end of
-// iteration t every CTA publishes its first row of q (both channels) and its
-// last row of q (row channel) into a parity-(t&1) buffer and arrives; at the
-// start of t+1 it waits, reads its neighbours' rows over DSMEM and rebuilds
-// the halo y rows itself (momentum from the previously received rows).  The
-// bottom row group also recomputes u for the first row of the CTA below, so
-// no u ever crosses a CTA boundary.  Row groups inside a CTA and warp edges
-// exchange through shared memory with __syncthreads.
+// Exchange pattern per inner iteration: at the end of iteration t every CTA
+// pushes its first row of q (both channels) to the CTA above and its last row
+// of q (row channel) to the CTA below (st.async + the receiver's mbarrier,
+// round-parity double buffers); at the start of t+1 each CTA waits for its
+// neighbours' rows and rebuilds the halo y rows itself (momentum from the
+// previously received rows).  The bottom row group also recomputes u for the
+// first row of the CTA below, so no u ever crosses a CTA boundary.  Row groups
+// inside a CTA and warp edges exchange through shared memory.
 template <class TO, bool NONNEG>
-__global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO> a) {
+__global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO> a) {
   using A = Ar<TO>;
   using F = Ar<float>;
   cg::cluster_group cluster = cg::this_cluster();
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   const bool rg_top = rg == 0, rg_bot = rg == CRG - 1;
   const bool has_up = cr > 0, has_dn = cr < CCL - 1;
   constexpr int64_t HW = (int64_t)CH * CW;
+  constexpr int SR = CRG * CRPT;  // rows of this CTA
 
   // halo rows received from the neighbours, double-buffered by round parity
   __shared__ __align__(8) float rx_dn[2][CW][2];  // CTA below's first row of q (y, x)
@@ -177,11 +181,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   __shared__ __align__(16) float s_edge_yx[CRG][CWARPS_ROW][CRPT + 4];  // float4 + extra row
   __shared__ __align__(16) float s_edge_u[CRG][CWARPS_ROW][CRPT];
   __shared__ float s_beta[kMaxBetas];
+  // the problem's x, b, h rows of this CTA, resident for the whole problem
+  extern __shared__ __align__(16) unsigned char stage_raw[];
+  TO* sx = reinterpret_cast<TO*>(stage_raw);  // [SR][CW]
+  TO* sb = sx + SR * CW;
+  TO* sh = sb + SR * CW;
 
   const TO g = a.gamma;
   const float w = a.weight;
   constexpr bool nonneg = NONNEG;
-  // momentum table in shared memory (uniform per iteration)
   for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
   if (tid == 0) {
     mbar_init(&mb_dn[0], 1);
@@ -193,12 +201,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
   cluster_arrive();  // every CTA's mbarriers exist before anyone pushes
   cluster_wait();
   // Round r carries the rows published after iteration r-1 (round 0: the warm
-  // start) and lands in buffer r&1; the counter runs across entries.
+  // start) and lands in buffer r&1; the counter runs across prox calls.
   constexpr unsigned BYTES_DN = CW * 2 * 4, BYTES_UP = CW * 4;
   const uint32_t up_rx_remote = dsmem_addr(&rx_dn[0][0][0], cr > 0 ? cr - 1 : cr);   // my top row -> CTA above
   const uint32_t up_mb_remote = dsmem_addr(&mb_dn[0], cr > 0 ? cr - 1 : cr);
   const uint32_t dn_rx_remote = dsmem_addr(&rx_up[0][0], cr < CCL - 1 ? cr + 1 : cr); // my bottom row -> CTA below
   const uint32_t dn_mb_remote = dsmem_addr(&mb_up[0], cr < CCL - 1 ? cr + 1 : cr);
+  // the CTA below's first staged row (x, b, h), read once per prox call
+  const uint32_t ex_x_remote = dsmem_addr(sx + j, cr < CCL - 1 ? cr + 1 : cr);
+  const uint32_t ex_b_remote = dsmem_addr(sb + j, cr < CCL - 1 ? cr + 1 : cr);
+  const uint32_t ex_h_remote = dsmem_addr(sh + j, cr < CCL - 1 ? cr + 1 : cr);
   unsigned round = 0;
   auto push_rows = [&](float top_y, float top_x, float bot_y) {
     const unsigned b = round & 1;
@@ -224,109 +236,83 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     }
     return b;
   };
+  const bool last_row_thread = rg_bot && !has_dn;  // owns global row H-1 (t = CRPT-1)
+  const bool left_fetch = lane == 0 && wc > 0;
+  const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
 
-  // Persistent clusters: cluster c handles entries c, c + G, ...; the next
-  // entry's x, b, h, q_warm rows of this CTA are prefetched with cp.async into
-  // shared memory while the current entry iterates (each thread stages exactly
-  // the elements it later reads, so no barrier is needed for the stage).
-  extern __shared__ __align__(16) unsigned char stage_raw[];
-  constexpr int SR = CRG * CRPT + 1;  // staged rows: this CTA's 16 + the next CTA's first
-  // fp32 outer state: two stages (the epilogue re-reads x, b, h from the
-  // stage); fp64: one stage (the epilogue re-reads them from global / L2)
-  constexpr int NST = sizeof(TO) == 4 ? 2 : 1;
-  constexpr size_t STB = sizeof(TO) * 3 * SR * CW + 4 * 2 * (SR - 1) * CW;
-  TO* sxbh = reinterpret_cast<TO*>(stage_raw);                       // [3][SR][CW]
-  float* sq = reinterpret_cast<float*>(stage_raw + sizeof(TO) * 3 * SR * CW);  // [2][SR-1][CW]
-  auto set_stage = [&](int sidx) {
-    sxbh = reinterpret_cast<TO*>(stage_raw + sidx * STB);
-    sq = reinterpret_cast<float*>(stage_raw + sidx * STB + sizeof(TO) * 3 * SR * CW);
-  };
-  const int G = gridDim.x / CCL;
-  auto issue_stage = [&](int e) {
-    const int pe = a.active ? a.active[e] : e;
-    const TO* src[3] = {a.x + (int64_t)pe * HW, a.b + (int64_t)pe * HW, a.h + (int64_t)pe * HW};
-    const float* qs = a.q + (int64_t)pe * a.qps;
-#pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      const int lr = rg * CRPT + t;
-      const int64_t o = (int64_t)(row0 + t) * CW + j;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cp_async_el<sizeof(TO)>(sxbh + (c * SR + lr) * CW + j, src[c] + o, true);
-      cp_async_el<4>(sq + lr * CW + j, qs + o, true);
-      cp_async_el<4>(sq + ((SR - 1) + lr) * CW + j, qs + HW + o, true);
-    }
-    if (rg_bot) {
-      const int64_t o = (int64_t)(row0 + CRPT) * CW + j;
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        cp_async_el<sizeof(TO)>(sxbh + (c * SR + SR - 1) * CW + j, has_dn ? src[c] + o : src[c], has_dn);
-    }
-    cp_async_commit_c();
-  };
-  if ((int)(blockIdx.x / CCL) < a.n_active) issue_stage(blockIdx.x / CCL);
-
-  int li = 0;  // local entry counter (stage parity)
-  for (int entry = blockIdx.x / CCL; entry < a.n_active; entry += G, ++li) {
-  set_stage(li % NST);
-  const int p = a.active ? a.active[entry] : entry;
+  const int c = blockIdx.x / CCL;
+  for (int ai = a.asg_off[c]; ai < a.asg_off[c + 1]; ++ai) {
+  const int p = a.asg[ai];
   TO* xp = a.x + (int64_t)p * HW;
   const TO* bp = a.b + (int64_t)p * HW;
   TO* hp = a.h + (int64_t)p * HW;
   float* q0 = a.q + (int64_t)p * a.qps;
-  const int m = a.pend ? a.pend[entry] : 0;
-  const int kf = a.kfirst ? a.kfirst[entry] : 0;
-  const bool rp = a.rep ? a.rep[entry] != 0 : false;
-  cp_async_wait_all();
+  const int e0 = a.ev_off[p], e1 = a.ev_off[p + 1];
+  // stage this CTA's rows of x, b, h (each thread its own elements; the CTA
+  // above reads row 0 after the next cluster barrier)
+#pragma unroll
+  for (int t = 0; t < CRPT; ++t) {
+    const int lr = rg * CRPT + t;
+    const int64_t o = (int64_t)(row0 + t) * CW + j;
+    sx[lr * CW + j] = xp[o];
+    sb[lr * CW + j] = bp[o];
+    sh[lr * CW + j] = hp[o];
+  }
   float z[CRPT], qky[CRPT], qkx[CRPT], qmy[CRPT], qmx[CRPT];
   int kbad = 0x7fffffff;
-  auto prox_input = [&](int lr, bool track) {
-    TO xo = sxbh[(0 * SR + lr) * CW + j];
-    const TO bo = sxbh[(1 * SR + lr) * CW + j], ho = sxbh[(2 * SR + lr) * CW + j];
+  int kprev = -1;
+  for (int e = e0; e < e1; ++e) {
+  const int kk = a.ev_k[e];
+  const int m = kk - kprev - 1;  // skip iterations kprev+1 .. kk-1 before this prox call
+  const int kf = kprev + 1;
+  // the previous prox call's x / h updates (and, at the first call, the
+  // staging) of every CTA are visible cluster-wide; also orders the reuse of
+  // this CTA's exchange buffers
+  cluster_arrive();
+  cluster_wait();
+  // ---- prologue: skips, prox input, warm start ------------------------------
+  auto prox_input = [&](TO xo, TO bo, TO ho, bool track) {
     for (int s = 0; s < m; ++s) {
       xo = skip_update(xo, bo, ho, g);
       if (track && !finite(xo)) kbad = min(kbad, kf + s);
     }
     return (float)A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(a.hc, ho));
   };
-  // ---- prologue: deferred skips, prox input, warm start --------------------
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
     const int lr = rg * CRPT + t;
-    z[t] = prox_input(lr, true);
-    float vy = sq[lr * CW + j], vx = sq[((SR - 1) + lr) * CW + j];
-    if (rp) {
-      const float sc = F::ball_scale(vy, vx, w);
-      vy *= sc;
-      vx *= sc;
+    z[t] = prox_input(sx[lr * CW + j], sb[lr * CW + j], sh[lr * CW + j], true);
+    if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
+      const int64_t o = (int64_t)(row0 + t) * CW + j;
+      float vy = q0[o], vx = q0[HW + o];
+      if (a.rep[p]) {
+        const float sc = F::ball_scale(vy, vx, w);
+        vy *= sc;
+        vx *= sc;
+      }
+      // The reference's divergence ignores q_y on the last row and q_x on the
+      // last column (operators.py:66-70) and the gradient is 0 there, so those
+      // entries stay 0 from a cold start; zeroing them here lets the inner
+      // loop drop every boundary test (zero padding instead of masks).
+      if (row0 + t == CH - 1) vy = 0.f;
+      if (j == CW - 1) vx = 0.f;
+      qky[t] = vy;
+      qkx[t] = vx;
     }
-    // The reference's divergence ignores q_y on the last row and q_x on the
-    // last column (operators.py:66-70) and the gradient is 0 there, so those
-    // entries stay 0 from a cold start; zeroing them here lets the inner loop
-    // drop every boundary test (zero padding instead of masks).
-    if (row0 + t == CH - 1) vy = 0.f;
-    if (j == CW - 1) vx = 0.f;
-    qky[t] = qmy[t] = vy;
-    qkx[t] = qmx[t] = vx;
+    qmy[t] = qky[t];  // the momentum restarts with every call (tv.py:72)
+    qmx[t] = qkx[t];
   }
   // the bottom row group also owns the CTA-below's first row for u
   float z_ex = 0.f;
-  if (rg_bot && has_dn) z_ex = prox_input(SR - 1, false);
-  // the stage is consumed: prefetch the next entry of this cluster
-  if (entry + G < a.n_active) {
-    set_stage((li + 1) % NST);
-    issue_stage(entry + G);
-    set_stage(li % NST);
-  }
-  const unsigned round0 = round;  // this entry's warm-start round
+  if (rg_bot && has_dn)
+    z_ex = prox_input(dsmem_ld<TO>(ex_x_remote), dsmem_ld<TO>(ex_b_remote),
+                      dsmem_ld<TO>(ex_h_remote), false);
+  const unsigned round0 = round;  // this call's warm-start round
   push_rows(qky[0], qkx[0], qky[CRPT - 1]);
   ++round;
 
   float up_k = 0.f, up_m = 0.f;                          // row above, row channel
   float dn_ky = 0.f, dn_kx = 0.f, dn_my = 0.f, dn_mx = 0.f;  // row below, both channels
-  const bool last_row_thread = rg_bot && !has_dn;  // owns global row H-1 (t = CRPT-1)
-  const bool right_edge = lane == 31 && wc == CWARPS_ROW - 1;  // global column W-1
-  const bool left_fetch = lane == 0 && wc > 0;
-  const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
@@ -462,7 +448,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
       QMx[2 * P] = nx.x;
       QMx[2 * P + 1] = nx.y;
     }
-    (void)right_edge;
     push_rows(QMy[0], QMx[0], QMy[CRPT - 1]);
     ++round;
   };
@@ -505,86 +490,72 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_kernel(ClusterArgs<TO
     if (j > 0) d -= left;
     float uf = z[t] + d;
     if (nonneg) uf = fmaxf(uf, 0.f);
-    const int64_t o = (int64_t)r * CW + j;
     const int lr = rg * CRPT + t;
-    TO xo, bo, ho;
-    if constexpr (NST == 2) {
-      xo = sxbh[(0 * SR + lr) * CW + j];
-      bo = sxbh[(1 * SR + lr) * CW + j];
-      ho = sxbh[(2 * SR + lr) * CW + j];
-    } else {
-      xo = xp[o];
-      bo = bp[o];
-      ho = hp[o];
-    }
+    TO xo = sx[lr * CW + j];
+    const TO bo = sb[lr * CW + j], ho = sh[lr * CW + j];
     for (int s = 0; s < m; ++s) xo = skip_update(xo, bo, ho, g);
     const TO xhat = skip_update(xo, bo, ho, g);
     const TO xn = (TO)uf;
-    hp[o] = A::add(ho, A::mul(a.pg, A::sub(xn, xhat)));
-    xp[o] = xn;
+    sh[lr * CW + j] = A::add(ho, A::mul(a.pg, A::sub(xn, xhat)));
+    sx[lr * CW + j] = xn;
     ok &= finite(xn);
-    q0[o] = qky[t];
-    q0[HW + o] = qkx[t];
   }
-  if (!ok) kbad = min(kbad, a.k);
-  if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
-  kbad = 0x7fffffff;
-  }  // entries
-  cluster_arrive();  // no CTA leaves while a neighbour may still push into it
-  cluster_wait();
-}
+  if (!ok) kbad = min(kbad, kk);
+  kprev = kk;
+  }  // prox calls
 
-// Apply each problem's remaining deferred skips (end of a run).
-template <class TO>
-__global__ void skip_flush_kernel(TO* __restrict__ x, const TO* __restrict__ b,
-                                  const TO* __restrict__ h, const int32_t* __restrict__ pend,
-                                  const int32_t* __restrict__ kfirst, int64_t HW, TO g,
-                                  int32_t* bad) {
-  const int p = blockIdx.y;
-  const int m = pend[p];
-  if (m == 0) return;
-  int kbad = 0x7fffffff;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HW;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = (int64_t)p * HW + i;
-    TO xo = x[o];
-    const TO bo = b[o], ho = h[o];
+  // ---- trailing skips, write-back -------------------------------------------
+  const int m = a.K - 1 - kprev;
+#pragma unroll
+  for (int t = 0; t < CRPT; ++t) {
+    const int lr = rg * CRPT + t;
+    const int64_t o = (int64_t)(row0 + t) * CW + j;
+    TO xo = sx[lr * CW + j];
+    const TO bo = sb[lr * CW + j], ho = sh[lr * CW + j];
     for (int s = 0; s < m; ++s) {
       xo = skip_update(xo, bo, ho, g);
-      if (!finite(xo)) kbad = min(kbad, kfirst[p] + s);
+      if (!finite(xo)) kbad = min(kbad, kprev + 1 + s);
     }
-    x[o] = xo;
+    xp[o] = xo;
+    if (e1 > e0) {
+      hp[o] = ho;
+      q0[o] = qky[t];
+      q0[HW + o] = qkx[t];
+    }
   }
-  if (kbad != 0x7fffffff && bad) atomicMin(bad + p, kbad);
+  if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
+  // The next problem's staging may overwrite row 0 of this CTA only after the
+  // CTA above has read it: it did so in the prologue of this problem's last
+  // prox call, before its first push of that call, which this CTA waited for.
+  }  // problems
+  cluster_arrive();  // no CTA leaves while a neighbour may still push into it
+  cluster_wait();
 }
 
 }  // namespace
 
 bool cluster_shape_ok(int H, int W) { return H == CH && W == CW; }
 
-size_t stage_bytes(int dto) {
-  const size_t SR = CRG * CRPT + 1;
-  const size_t eb = dto == PSB_F64 ? 8 : 4;
-  const size_t nst = dto == PSB_F64 ? 1 : 2;
-  return nst * (eb * 3 * SR * CW + 4 * 2 * (SR - 1) * CW);
+static size_t stage_bytes(int dto) {
+  return (size_t)(dto == PSB_F64 ? 8 : 4) * 3 * CRG * CRPT * CW;
 }
 
-int cluster_max_active(int* out);
-
-int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
-                      const int32_t* active, int n_active, const int32_t* pend,
-                      const int32_t* kfirst, const uint8_t* rep, int n_inner, int accelerated,
-                      int nonneg, double weight, double gamma, double hc, double pg, double step,
-                      const float* betas, int32_t* bad, int k, cudaStream_t st) {
-  if (n_active == 0) return PSB_OK;
+// 16-CTA clusters of the run kernel resident on this device at once (cached)
+int cluster_count() {
   static int max_clusters = 0;
   if (max_clusters == 0) {
     int mc = 0;
-    if (cluster_max_active(&mc) != PSB_OK || mc <= 0) mc = 1;
+    if (psb_cluster_max_active(&mc) != PSB_OK || mc <= 0) mc = 1;
     max_clusters = mc;
   }
+  return max_clusters;
+}
+
+template <class TO, bool NN>
+static int launch_run(const RunArgs<TO>& a, int G, int dto, cudaStream_t st) {
+  auto kern = fgp_cluster_run_kernel<TO, NN>;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::min(n_active, max_clusters) * CCL);
+  cfg.gridDim = dim3((unsigned)G * CCL);
   cfg.blockDim = dim3(CTHREADS);
   cfg.dynamicSmemBytes = stage_bytes(dto);
   cfg.stream = st;
@@ -595,47 +566,38 @@ int cluster_prox_step(int dto, void* x, const void* b, void* h, void* q, int64_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  PSB_CHECK(func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
+  PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  PSB_LAUNCHED("fgp_cluster_run");
+  return PSB_OK;
+}
+
+int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
+                const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
+                const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
+                int nonneg, double weight, double gamma, double hc, double pg, double step,
+                const float* betas, int32_t* bad, cudaStream_t st) {
+  if (G <= 0) return PSB_OK;
   if (dto == PSB_F32) {
-    auto kern = nonneg ? fgp_cluster_kernel<float, true> : fgp_cluster_kernel<float, false>;
-    PSB_CHECK(func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
-    ClusterArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, active, pend,
-                         kfirst, rep, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
-                         (float)hc, (float)pg, (float)step, bad, k, betas, n_active};
-    PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
-  } else if (dto == PSB_F64) {
-    auto kern = nonneg ? fgp_cluster_kernel<double, true> : fgp_cluster_kernel<double, false>;
-    PSB_CHECK(func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
-    ClusterArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, active, pend,
-                          kfirst, rep, n_inner, accelerated, nonneg, (float)weight, gamma, hc, pg,
-                          (float)step, bad, k, betas, n_active};
-    PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
-  } else {
-    return fail(PSB_ERR_VALUE, "cluster prox: unknown dtype");
+    RunArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, asg_off, asg, ev_off,
+                     ev_k, rep, K, n_inner, accelerated, (float)weight, (float)gamma, (float)hc,
+                     (float)pg, (float)step, bad, betas};
+    return nonneg ? launch_run<float, true>(a, G, dto, st) : launch_run<float, false>(a, G, dto, st);
   }
-  PSB_LAUNCHED("fgp_cluster");
-  return PSB_OK;
+  if (dto == PSB_F64) {
+    RunArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, asg_off, asg,
+                      ev_off, ev_k, rep, K, n_inner, accelerated, (float)weight, gamma, hc, pg,
+                      (float)step, bad, betas};
+    return nonneg ? launch_run<double, true>(a, G, dto, st) : launch_run<double, false>(a, G, dto, st);
+  }
+  return fail(PSB_ERR_VALUE, "cluster run: unknown dtype");
 }
 
-int skip_flush(int dto, void* x, const void* b, const void* h, const int32_t* pend,
-               const int32_t* kfirst, int64_t n, int64_t HW, double gamma, int32_t* bad,
-               cudaStream_t st) {
-  if (n == 0) return PSB_OK;
-  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((HW + 255) / 256, 64)), (unsigned)n);
-  if (dto == PSB_F32)
-    skip_flush_kernel<float><<<grid, 256, 0, st>>>((float*)x, (const float*)b, (const float*)h,
-                                                   pend, kfirst, HW, (float)gamma, bad);
-  else if (dto == PSB_F64)
-    skip_flush_kernel<double><<<grid, 256, 0, st>>>((double*)x, (const double*)b,
-                                                    (const double*)h, pend, kfirst, HW, gamma, bad);
-  else
-    return fail(PSB_ERR_VALUE, "skip flush: unknown dtype");
-  PSB_LAUNCHED("skip_flush");
-  return PSB_OK;
-}
+}  // namespace psb
 
-int cluster_max_active(int* out) {
+extern "C" int psb_cluster_max_active(int* out) {
+  using namespace psb;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CCL * 64);
   cfg.blockDim = dim3(CTHREADS);
@@ -647,15 +609,9 @@ int cluster_max_active(int* out) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.dynamicSmemBytes = stage_bytes(PSB_F64);
-  PSB_CHECK(func_attr(fgp_cluster_kernel<float, false>,
-                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  PSB_CHECK(func_attr(fgp_cluster_kernel<float, false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)cfg.dynamicSmemBytes));
-  PSB_CUDA(cudaOccupancyMaxActiveClusters(out, fgp_cluster_kernel<float, false>, &cfg));
+  auto kern = fgp_cluster_run_kernel<float, false>;
+  PSB_CHECK(func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes));
+  PSB_CUDA(cudaOccupancyMaxActiveClusters(out, kern, &cfg));
   return PSB_OK;
 }
-
-}  // namespace psb
-
-extern "C" int psb_cluster_max_active(int* out) { return psb::cluster_max_active(out); }
