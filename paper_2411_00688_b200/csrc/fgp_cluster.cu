@@ -149,6 +149,17 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// Per-thread column strips are held as row PAIRS (t, t + 4) in float2
+// registers, so Blackwell's packed f32x2 FFMA2 / FADD2 / FMUL2 work on
+// naturally aligned register pairs: the vertical neighbours of pair P are the
+// pairs P - 1 / P + 1, and only the strip ends (rows -1 and 8) build a pair
+// from two halves.  rowref(v, t) names row t (t a compile-time constant
+// after unrolling).
+constexpr int NP = CRPT / 2;
+__device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
+  return t < NP ? v[t].x : v[t - NP].y;
+}
+
 // Exchange pattern per inner iteration: at the end of iteration t every CTA
 // pushes its first row of q (both channels) to the CTA above and its last row
 // of q (row channel) to the CTA below (st.async + the receiver's mbarrier,
@@ -178,8 +189,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   __shared__ __align__(8) uint64_t mb_dn[2], mb_up[2];
   __shared__ float s_rg_yy[CRG][CW];   // each row group's last-row y_y (for the group below)
   __shared__ float s_rg_u[CRG][CW];    // each row group's first-row u (for the group above)
-  __shared__ __align__(16) float s_edge_yx[CRG][CWARPS_ROW][CRPT + 4];  // float4 + extra row
-  __shared__ __align__(16) float s_edge_u[CRG][CWARPS_ROW][CRPT];
+  // warp-edge columns as row pairs: s_edge_yx[rg][.][w + 1] = last lane of warp w
+  // (slot 0 stays zero: nothing left of column 0; [NP].x = the halo row's y_x),
+  // s_edge_u[rg][.][w] = first lane of warp w (pair-major: one STS.64 per pair)
+  __shared__ __align__(16) float2 s_edge_yx[CRG][NP + 1][CWARPS_ROW + 1];
+  __shared__ __align__(16) float2 s_edge_u[CRG][NP][CWARPS_ROW];
   __shared__ float s_beta[kMaxBetas];
   // the problem's x, b, h rows of this CTA, resident for the whole problem
   extern __shared__ __align__(16) unsigned char stage_raw[];
@@ -191,6 +205,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const float w = a.weight;
   constexpr bool nonneg = NONNEG;
   for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
+  if (tid < CRG * (NP + 1)) s_edge_yx[tid / (NP + 1)][tid % (NP + 1)][0] = make_float2(0.f, 0.f);
   if (tid == 0) {
     mbar_init(&mb_dn[0], 1);
     mbar_init(&mb_dn[1], 1);
@@ -237,7 +252,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     return b;
   };
   const bool last_row_thread = rg_bot && !has_dn;  // owns global row H-1 (t = CRPT-1)
-  const bool left_fetch = lane == 0 && wc > 0;
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
 
   const int c = blockIdx.x / CCL;
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     sb[lr * CW + j] = bp[o];
     sh[lr * CW + j] = hp[o];
   }
-  float z[CRPT], qky[CRPT], qkx[CRPT], qmy[CRPT], qmx[CRPT];
+  float2 z[NP], qky[NP], qkx[NP], qmy[NP], qmx[NP];
   int kbad = 0x7fffffff;
   int kprev = -1;
   for (int e = e0; e < e1; ++e) {
@@ -281,7 +295,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
     const int lr = rg * CRPT + t;
-    z[t] = prox_input(sx[lr * CW + j], sb[lr * CW + j], sh[lr * CW + j], true);
+    rowref(z, t) = prox_input(sx[lr * CW + j], sb[lr * CW + j], sh[lr * CW + j], true);
     if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
       const int64_t o = (int64_t)(row0 + t) * CW + j;
       float vy = q0[o], vx = q0[HW + o];
@@ -296,11 +310,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       // loop drop every boundary test (zero padding instead of masks).
       if (row0 + t == CH - 1) vy = 0.f;
       if (j == CW - 1) vx = 0.f;
-      qky[t] = vy;
-      qkx[t] = vx;
+      rowref(qky, t) = vy;
+      rowref(qkx, t) = vx;
     }
-    qmy[t] = qky[t];  // the momentum restarts with every call (tv.py:72)
-    qmx[t] = qkx[t];
+  }
+#pragma unroll
+  for (int P = 0; P < NP; ++P) {
+    qmy[P] = qky[P];  // the momentum restarts with every call (tv.py:72)
+    qmx[P] = qkx[P];
   }
   // the bottom row group also owns the CTA-below's first row for u
   float z_ex = 0.f;
@@ -308,30 +325,24 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     z_ex = prox_input(dsmem_ld<TO>(ex_x_remote), dsmem_ld<TO>(ex_b_remote),
                       dsmem_ld<TO>(ex_h_remote), false);
   const unsigned round0 = round;  // this call's warm-start round
-  push_rows(qky[0], qkx[0], qky[CRPT - 1]);
+  push_rows(qky[0].x, qkx[0].x, rowref(qky, CRPT - 1));
   ++round;
 
   float up_k = 0.f, up_m = 0.f;                          // row above, row channel
   float dn_ky = 0.f, dn_kx = 0.f, dn_my = 0.f, dn_mx = 0.f;  // row below, both channels
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
-  auto inner = [&](float(&QKy)[CRPT], float(&QKx)[CRPT], float(&QMy)[CRPT], float(&QMx)[CRPT],
+  // Each pixel's arithmetic is the scalar FGP step (each f32x2 lane an IEEE
+  // fp32 op; a - b = fma(b, -1, a)).
+  auto inner = [&](float2(&QKy)[NP], float2(&QKx)[NP], float2(&QMy)[NP], float2(&QMx)[NP],
                    int it) {
     const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
-    // rows in pairs with Blackwell's packed f32x2 FFMA2 / FADD2 / FMUL2 (each
-    // lane an IEEE fp32 op, same rounding as the scalar form); a - b = fma(b, -1, a)
     const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
-    float yy[CRPT], yx[CRPT];
+    float2 yy[NP], yx[NP];
 #pragma unroll
-    for (int P = 0; P < CRPT / 2; ++P) {
-      const float2 ky = make_float2(QKy[2 * P], QKy[2 * P + 1]);
-      const float2 kx = make_float2(QKx[2 * P], QKx[2 * P + 1]);
-      const float2 ry = __ffma2_rn(b2, __ffma2_rn(make_float2(QMy[2 * P], QMy[2 * P + 1]), m1, ky), ky);
-      const float2 rx = __ffma2_rn(b2, __ffma2_rn(make_float2(QMx[2 * P], QMx[2 * P + 1]), m1, kx), kx);
-      yy[2 * P] = ry.x;
-      yy[2 * P + 1] = ry.y;
-      yx[2 * P] = rx.x;
-      yx[2 * P + 1] = rx.y;
+    for (int P = 0; P < NP; ++P) {
+      yy[P] = __ffma2_rn(b2, __ffma2_rn(QMy[P], m1, QKy[P]), QKy[P]);
+      yx[P] = __ffma2_rn(b2, __ffma2_rn(QMx[P], m1, QKx[P]), QKx[P]);
     }
     const unsigned par = recv_rows(round0 + it);
     float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
@@ -350,105 +361,80 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       ex_y = dn_ky + beta * (dn_ky - dn_my);
       ex_x = dn_kx + beta * (dn_kx - dn_mx);
     }
-    s_rg_yy[rg][j] = yy[CRPT - 1];
+    s_rg_yy[rg][j] = yy[NP - 1].y;  // row CRPT-1
     if (lane == 31) {
 #pragma unroll
-      for (int c4 = 0; c4 < CRPT / 4; ++c4)
-        *reinterpret_cast<float4*>(&s_edge_yx[rg][wc][4 * c4]) =
-            make_float4(yx[4 * c4], yx[4 * c4 + 1], yx[4 * c4 + 2], yx[4 * c4 + 3]);
-      s_edge_yx[rg][wc][CRPT] = ex_x;
+      for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[P];
+      s_edge_yx[rg][NP][wc + 1].x = ex_x;
     }
     __syncthreads();
-    float le[CRPT];
-    float ledge_x = 0.f;
+    // left neighbours: shuffles inside the warp, the warp to the left's last
+    // lane from shared memory (zeros left of column 0)
+    float2 left[NP];
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) le[t] = 0.f;
-    if (left_fetch) {
+    for (int P = 0; P < NP; ++P) {
+      left[P].x = __shfl_up_sync(0xffffffffu, yx[P].x, 1);
+      left[P].y = __shfl_up_sync(0xffffffffu, yx[P].y, 1);
+    }
+    float ledge_x = __shfl_up_sync(0xffffffffu, ex_x, 1);
+    if (lane == 0) {
 #pragma unroll
-      for (int c4 = 0; c4 < CRPT / 4; ++c4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(&s_edge_yx[rg][wc - 1][4 * c4]);
-        le[4 * c4] = l4.x;
-        le[4 * c4 + 1] = l4.y;
-        le[4 * c4 + 2] = l4.z;
-        le[4 * c4 + 3] = l4.w;
-      }
-      ledge_x = s_edge_yx[rg][wc - 1][CRPT];
+      for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
+      ledge_x = s_edge_yx[rg][NP][wc].x;
     }
     const float yy_above = rg_top ? y_up : s_rg_yy[rg - 1][j];
-    float left[CRPT];
+    float2 u[NP];
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      left[t] = __shfl_up_sync(0xffffffffu, yx[t], 1);
-      if (lane == 0) left[t] = le[t];
-    }
-    float u[CRPT];
-#pragma unroll
-    for (int P = 0; P < CRPT / 2; ++P) {
+    for (int P = 0; P < NP; ++P) {
       // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
-      const float2 ab2 = make_float2(P == 0 ? yy_above : yy[2 * P - 1], yy[2 * P]);
-      const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, make_float2(yy[2 * P], yy[2 * P + 1])),
-                                   make_float2(yx[2 * P], yx[2 * P + 1]));
-      const float2 d2 = __ffma2_rn(make_float2(left[2 * P], left[2 * P + 1]), m1, d1);
-      const float2 v = __fadd2_rn(make_float2(z[2 * P], z[2 * P + 1]), d2);
-      u[2 * P] = nonneg ? fmaxf(v.x, 0.f) : v.x;
-      u[2 * P + 1] = nonneg ? fmaxf(v.y, 0.f) : v.y;
+      const float2 ab2 = P == 0 ? make_float2(yy_above, yy[NP - 1].x) : yy[P - 1];
+      const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[P]), yx[P]);
+      const float2 d2 = __ffma2_rn(left[P], m1, d1);
+      const float2 v = __fadd2_rn(z[P], d2);
+      u[P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
     }
     float u_ex;
     {
-      float left = __shfl_up_sync(0xffffffffu, ex_x, 1);
-      if (lane == 0) left = ledge_x;
-      const float d = ((ex_y - yy[CRPT - 1]) + ex_x) - left;
+      const float d = ((ex_y - yy[NP - 1].y) + ex_x) - ledge_x;
       const float v = z_ex + d;
       u_ex = nonneg ? fmaxf(v, 0.f) : v;
     }
-    s_rg_u[rg][j] = u[0];
-    if (lane == 0)
+    s_rg_u[rg][j] = u[0].x;
+    if (lane == 0) {
 #pragma unroll
-      for (int c4 = 0; c4 < CRPT / 4; ++c4)
-        *reinterpret_cast<float4*>(&s_edge_u[rg][wc][4 * c4]) =
-            make_float4(u[4 * c4], u[4 * c4 + 1], u[4 * c4 + 2], u[4 * c4 + 3]);
+      for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[P];
+    }
     __syncthreads();
-    float re[CRPT];  // global column W-1: right := u (gx = 0)
+    // right neighbours: shuffles (lane 31 keeps its own u: at the global last
+    // column gx = 0), the warp to the right's first lane from shared memory
+    float2 right[NP];
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) re[t] = u[t];
+    for (int P = 0; P < NP; ++P) {
+      right[P].x = __shfl_down_sync(0xffffffffu, u[P].x, 1);
+      right[P].y = __shfl_down_sync(0xffffffffu, u[P].y, 1);
+    }
     if (right_fetch) {
 #pragma unroll
-      for (int c4 = 0; c4 < CRPT / 4; ++c4) {
-        const float4 r4 = *reinterpret_cast<const float4*>(&s_edge_u[rg][wc + 1][4 * c4]);
-        re[4 * c4] = r4.x;
-        re[4 * c4 + 1] = r4.y;
-        re[4 * c4 + 2] = r4.z;
-        re[4 * c4 + 3] = r4.w;
-      }
+      for (int P = 0; P < NP; ++P) right[P] = s_edge_u[rg][P][wc + 1];
     }
     // the global last row has no row below: gy = 0 (below := u)
-    const float u_below = !rg_bot ? s_rg_u[rg + 1][j] : (last_row_thread ? u[CRPT - 1] : u_ex);
-    float right[CRPT];
-#pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      right[t] = __shfl_down_sync(0xffffffffu, u[t], 1);
-      if (lane == 31) right[t] = re[t];
-    }
+    const float u_below = !rg_bot ? s_rg_u[rg + 1][j] : (last_row_thread ? u[NP - 1].y : u_ex);
     const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(w, w);
 #pragma unroll
-    for (int P = 0; P < CRPT / 2; ++P) {
-      const float2 u2 = make_float2(u[2 * P], u[2 * P + 1]);
-      const float2 bl2 = make_float2(u[2 * P + 1], P == CRPT / 2 - 1 ? u_below : u[2 * P + 2]);
-      const float2 gy = __ffma2_rn(u2, m1, bl2);
-      const float2 gx = __ffma2_rn(u2, m1, make_float2(right[2 * P], right[2 * P + 1]));
-      const float2 ay = __ffma2_rn(st2, gy, make_float2(yy[2 * P], yy[2 * P + 1]));
-      const float2 ax = __ffma2_rn(st2, gx, make_float2(yx[2 * P], yx[2 * P + 1]));
+    for (int P = 0; P < NP; ++P) {
+      const float2 bl2 = P < NP - 1 ? u[P + 1] : make_float2(u[0].y, u_below);
+      const float2 gy = __ffma2_rn(u[P], m1, bl2);
+      const float2 gx = __ffma2_rn(u[P], m1, right[P]);
+      const float2 ay = __ffma2_rn(st2, gy, yy[P]);
+      const float2 ax = __ffma2_rn(st2, gx, yx[P]);
       const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
       float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
       sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
       sc.y = fminf(1.f, sc.y);
-      const float2 ny = __fmul2_rn(ay, sc), nx = __fmul2_rn(ax, sc);
-      QMy[2 * P] = ny.x;
-      QMy[2 * P + 1] = ny.y;
-      QMx[2 * P] = nx.x;
-      QMx[2 * P + 1] = nx.y;
+      QMy[P] = __fmul2_rn(ay, sc);
+      QMx[P] = __fmul2_rn(ax, sc);
     }
-    push_rows(QMy[0], QMx[0], QMy[CRPT - 1]);
+    push_rows(QMy[0].x, QMx[0].x, QMy[NP - 1].y);
     ++round;
   };
 
@@ -460,9 +446,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   if (it < a.n_inner) {
     inner(qky, qkx, qmy, qmx, it);
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) {
-      qky[t] = qmy[t];
-      qkx[t] = qmx[t];
+    for (int P = 0; P < NP; ++P) {
+      qky[P] = qmy[P];
+      qkx[P] = qmx[P];
     }
   }
 
@@ -470,25 +456,34 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const unsigned pe = recv_rows(round0 + a.n_inner);
   float yy_above = 0.f;
   if (rg_top && has_up) yy_above = rx_up[pe][j];
-  s_rg_yy[rg][j] = qky[CRPT - 1];
+  s_rg_yy[rg][j] = rowref(qky, CRPT - 1);
   if (lane == 31) {
 #pragma unroll
-    for (int t = 0; t < CRPT; ++t) s_edge_yx[rg][wc][t] = qkx[t];  // epilogue: once
+    for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = qkx[P];
   }
   __syncthreads();
+  float2 qleft[NP];
+#pragma unroll
+  for (int P = 0; P < NP; ++P) {
+    qleft[P].x = __shfl_up_sync(0xffffffffu, qkx[P].x, 1);
+    qleft[P].y = __shfl_up_sync(0xffffffffu, qkx[P].y, 1);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int P = 0; P < NP; ++P) qleft[P] = s_edge_yx[rg][P][wc];
+  }
   if (!rg_top) yy_above = s_rg_yy[rg - 1][j];
   bool ok = true;
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
-    float left = __shfl_up_sync(0xffffffffu, qkx[t], 1);
-    if (lane == 0) left = wc > 0 ? s_edge_yx[rg][wc - 1][t] : 0.f;
+    const float left = rowref(qleft, t);
     const int r = row0 + t;
     float d = 0.f;
-    if (r < CH - 1) d += qky[t];
-    if (r > 0) d -= (t > 0 ? qky[t - 1] : yy_above);
-    if (j < CW - 1) d += qkx[t];
+    if (r < CH - 1) d += rowref(qky, t);
+    if (r > 0) d -= (t > 0 ? rowref(qky, t - 1) : yy_above);
+    if (j < CW - 1) d += rowref(qkx, t);
     if (j > 0) d -= left;
-    float uf = z[t] + d;
+    float uf = rowref(z, t) + d;
     if (nonneg) uf = fmaxf(uf, 0.f);
     const int lr = rg * CRPT + t;
     TO xo = sx[lr * CW + j];
@@ -519,8 +514,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     xp[o] = xo;
     if (e1 > e0) {
       hp[o] = ho;
-      q0[o] = qky[t];
-      q0[HW + o] = qkx[t];
+      q0[o] = rowref(qky, t);
+      q0[HW + o] = rowref(qkx, t);
     }
   }
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
