@@ -248,7 +248,9 @@ def run_gpu(args):
     fgp_bytes = active * HW * (BYTES_FGP_FIRST + (INNER - 1) * BYTES_FGP_MOM)
     n_fired_steps = int(np.count_nonzero(active))
     if CLUSTER:
-        launches = 1  # one fgp_cluster_run_kernel launch for the K timed steps
+        # one fgp_cluster_run_kernel launch for the K timed steps, plus one
+        # fgp_sm_run_kernel launch on the SMs the clusters leave
+        launches = 1 + (os.environ.get("PSB_NO_SMWORK", "0") != "1")
     else:
         launches = args.steps + n_fired_steps * (INNER + 1)
     stats = np.array([t_local, fgp_t.sum(), float(fgp_bytes.sum()), float(active.sum())])

@@ -16,7 +16,7 @@ import torch
 from .errors import DivergenceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsb200.so")
+LIB_PATH = os.environ.get("PSB_LIB_PATH") or os.path.join(_HERE, "libpsb200.so")
 
 PSB_OK, PSB_ERR_VALUE, PSB_ERR_CUDA, PSB_ERR_DIVERGED = 0, 1, 2, 3
 F32, F64 = 0, 1

@@ -9,6 +9,7 @@
 // whole launch sequence is captured into one CUDA graph first (a 256^2 FGP
 // iteration is only a few microseconds of GPU work, so launch cost matters).
 #include <climits>
+#include <cstdio>
 #include <cstring>
 
 #include "common.cuh"
@@ -31,6 +32,11 @@ int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
                 cudaStream_t st);
 bool cluster_shape_ok(int H, int W);
 int cluster_count();
+int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const int32_t* asg_off,
+           const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
+           const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
+           double gamma, double hc, double pg, double step, const float* betas, int32_t* bad,
+           cudaStream_t st);
 int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
                 const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
                 const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
@@ -146,10 +152,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   // re-projection flag, and problems assigned to the resident clusters
   // longest-first (a prox call costs n_inner cluster iterations, a skip
   // iteration next to nothing).
-  std::vector<int32_t> ev_off, ev_k, asg_off, asg;
+  std::vector<int32_t> ev_off, ev_k, asg_off, asg, sw_off, sw;
   std::vector<uint8_t> rep_p;
   std::vector<float> beta_f;
-  int G = 0;
+  int G = 0, NW = 0;
   if (use_cluster) {
     ev_off.assign(n + 1, 0);
     for (size_t e = 0; e < act.size(); ++e) ev_off[act[e] + 1] += 1;
@@ -164,23 +170,47 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
         ev_k[fill[i]++] = k;
       }
     G = (int)std::min<int64_t>(n, cluster_count());
+    // SMs the clusters leave idle run fgp_sm_run_kernel (one problem per SM,
+    // L2-resident) on a second stream.  The split is a static cost model --
+    // an SM worker needs ~ratio times a cluster's time per prox call -- so
+    // the kernel that runs a problem never depends on timing.  (Not inside a
+    // captured graph: there the two launches have no placement order, and the
+    // SM workers could take the GPC space the clusters need.)
+    const char* no_sm = std::getenv("PSB_NO_SMWORK");
+    const char* ratio_env = std::getenv("PSB_SM_RATIO");
+    const double ratio = ratio_env ? std::atof(ratio_env) : 38.0;
+    if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1') && ratio > 0)
+      NW = std::max(0, sm_count() - G * 16);
     std::vector<int32_t> order(n);
     for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
     std::stable_sort(order.begin(), order.end(), [&](int32_t u, int32_t v) {
       return ev_off[u + 1] - ev_off[u] > ev_off[v + 1] - ev_off[v];
     });
-    std::vector<double> load(G, 0.0);
-    std::vector<std::vector<int32_t>> bins(G);
+    // longest first onto the machine (G clusters, NW SM workers) that would
+    // finish it earliest
+    std::vector<double> load(G + NW, 0.0);
+    std::vector<std::vector<int32_t>> bins(G + NW);
     for (int32_t i : order) {
-      const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-      load[c] += (double)(ev_off[i + 1] - ev_off[i]) * n_inner + 1e-3 * K;
-      bins[c].push_back(i);
+      const double c = (double)(ev_off[i + 1] - ev_off[i]) * n_inner + 1e-3 * K;
+      int best = 0;
+      double bt = 0.0;
+      for (int mch = 0; mch < G + NW; ++mch) {
+        const double t = load[mch] + (mch < G ? c : c * ratio);
+        if (mch == 0 || t < bt) best = mch, bt = t;
+      }
+      load[best] = bt;
+      bins[best].push_back(i);
     }
     asg_off.assign(G + 1, 0);
     asg.reserve(n);
     for (int c = 0; c < G; ++c) {
       asg.insert(asg.end(), bins[c].begin(), bins[c].end());
       asg_off[c + 1] = (int32_t)asg.size();
+    }
+    sw_off.assign(NW + 1, 0);
+    for (int w = 0; w < NW; ++w) {
+      sw.insert(sw.end(), bins[G + w].begin(), bins[G + w].end());
+      sw_off[w + 1] = (int32_t)sw.size();
     }
     beta_f.resize(n_inner);
     for (int i = 0; i < n_inner; ++i) beta_f[i] = (float)beta[i];
@@ -199,7 +229,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   const size_t o_coins = use_cluster ? 0 : put(coins_host, (size_t)K * n);
   const size_t o_act = use_cluster ? 0 : put(act.data(), act.size() * sizeof(int32_t));
   const size_t o_rep = use_cluster ? 0 : put(rep.data(), rep.size());
-  size_t o_evo = 0, o_evk = 0, o_repp = 0, o_asgo = 0, o_asg = 0, o_beta = 0;
+  size_t o_evo = 0, o_evk = 0, o_repp = 0, o_asgo = 0, o_asg = 0, o_beta = 0, o_swo = 0, o_sw = 0;
   if (use_cluster) {
     o_evo = put(ev_off.data(), ev_off.size() * sizeof(int32_t));
     o_evk = put(ev_k.data(), ev_k.size() * sizeof(int32_t));
@@ -207,6 +237,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     o_asgo = put(asg_off.data(), asg_off.size() * sizeof(int32_t));
     o_asg = put(asg.data(), asg.size() * sizeof(int32_t));
     o_beta = put(beta_f.data(), beta_f.size() * sizeof(float));
+    if (NW > 0) {
+      o_swo = put(sw_off.data(), sw_off.size() * sizeof(int32_t));
+      o_sw = put(sw.data(), sw.size() * sizeof(int32_t));
+    }
   }
   DevBuf d_sched;
   d_sched.st = user_stream;
@@ -238,9 +272,54 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   int rc = PSB_OK;
   if (use_cluster) {  // the whole segment in one launch
     if (fgp_time) cudaEventRecordWithFlags(fev[0], st, rec_flags);
-    rc = cluster_run(dto, x, b, h, q, qps, i32(o_asgo), i32(o_asg), G, i32(o_evo), i32(o_evk),
-                     dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
-                     0.125, reinterpret_cast<const float*>(dev + o_beta), bad, st);
+    const float* beta_d = reinterpret_cast<const float*>(dev + o_beta);
+    // SM workers go on a second stream, forked BEFORE the cluster launch (so
+    // they do not wait for it) and launched AFTER it (so the clusters are
+    // placed first), joined back into `st`
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (NW > 0) {
+      if (cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess)
+        rc = fail(PSB_ERR_CUDA, "sm workers: stream/event creation failed");
+      if (rc == PSB_OK) {
+        cudaEventRecord(fork, st);
+        cudaStreamWaitEvent(st2, fork, 0);
+      }
+    }
+    if (rc == PSB_OK)
+      rc = cluster_run(dto, x, b, h, q, qps, i32(o_asgo), i32(o_asg), G, i32(o_evo), i32(o_evk),
+                       dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
+                       0.125, beta_d, bad, st);
+    const char* dbg = std::getenv("PSB_DEBUG_TIMES");
+    cudaEvent_t d0 = nullptr, d1 = nullptr, d2 = nullptr;
+    if (dbg) {
+      cudaEventCreate(&d0);
+      cudaEventCreate(&d1);
+      cudaEventCreate(&d2);
+      cudaEventRecord(d1, st);
+    }
+    if (NW > 0 && st2 && fork && join) {
+      if (dbg) cudaEventRecord(d0, st2);
+      if (rc == PSB_OK)
+        rc = sm_run(x, b, h, q, qps, z, i32(o_swo), i32(o_sw), NW, i32(o_evo), i32(o_evk),
+                    dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
+                    beta_d, bad, st2);
+      if (dbg) cudaEventRecord(d2, st2);
+      cudaEventRecord(join, st2);
+      cudaStreamWaitEvent(st, join, 0);
+    }
+    if (dbg) {
+      cudaDeviceSynchronize();
+      float a = 0, b2 = 0;
+      cudaEventElapsedTime(&a, fev.empty() ? d1 : fev[0], d1);
+      if (NW > 0) cudaEventElapsedTime(&b2, d0, d2);
+      fprintf(stderr, "[psb] clusters %d: %.3f ms; sm workers %d: %.3f ms\n", G, a, NW, b2);
+    }
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (st2) cudaStreamDestroy(st2);  // released by the runtime once its work completes
     if (fgp_time) cudaEventRecordWithFlags(fev[1], st, rec_flags);
   }
   for (int k = 0; k < K && rc == PSB_OK && !use_cluster; ++k) {

@@ -83,8 +83,31 @@ __device__ __forceinline__ T clampu(T v, int nonneg) {
   return nonneg ? (v > T(0) ? v : T(0)) : v;  // np.maximum(v, 0); NaN -> 0 differs only for NaN
 }
 
+// Loads of the item: read-only path (one inner iteration per launch), or
+// L2-coherent (CG: a persistent kernel that rewrites the same arrays between
+// inner iterations must not hit stale L1 / texture lines).
+template <bool CG, class T, int V>
+__device__ __forceinline__ void ldq(T (&d)[V], const T* p) {
+  if constexpr (CG && sizeof(T) * V == 16) {
+    const float4 r = __ldcg(reinterpret_cast<const float4*>(p));
+    const T* s = reinterpret_cast<const T*>(&r);
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = s[i];
+  } else if constexpr (CG) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) d[i] = __ldcg(p + i);
+  } else {
+    ldv<T, V>(d, p);
+  }
+}
+template <bool CG, class T>
+__device__ __forceinline__ T ld1(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return __ldg(p);
+}
+
 // One work item = one (band, strip) of one problem (active-list entry `entry`).
-template <class T, int V>
+template <class T, int V, bool CG = false>
 __device__ __forceinline__ void fgp2d_item(const FgpArgs<T, V>& a, int item, int entry) {
   using A = Ar<T>;
   const int lane = threadIdx.x & 31;
@@ -130,22 +153,22 @@ __device__ __forceinline__ void fgp2d_item(const FgpArgs<T, V>& a, int item, int
   auto issue_row = [&](int r, Raw& R) {
     const int64_t ro = (int64_t)r * W;
     if (lin) {
-      ldv<T, V>(R.ky, qk + ro + cl);
-      ldv<T, V>(R.kx, qk + HW + ro + cl);
+      ldq<CG, T, V>(R.ky, qk + ro + cl);
+      ldq<CG, T, V>(R.kx, qk + HW + ro + cl);
       if (mom) {
-        ldv<T, V>(R.my, qm + ro + cl);
-        ldv<T, V>(R.mx, qm + HW + ro + cl);
+        ldq<CG, T, V>(R.my, qm + ro + cl);
+        ldq<CG, T, V>(R.mx, qm + HW + ro + cl);
       }
-      ldv<T, V>(R.xv, xp + ro + cl);
+      ldq<CG, T, V>(R.xv, xp + ro + cl);
     }
     if (hval) {
-      R.hky = __ldg(qk + ro + hc);
-      R.hkx = __ldg(qk + HW + ro + hc);
+      R.hky = ld1<CG>(qk + ro + hc);
+      R.hkx = ld1<CG>(qk + HW + ro + hc);
       if (mom) {
-        R.hmy = __ldg(qm + ro + hc);
-        R.hmx = __ldg(qm + HW + ro + hc);
+        R.hmy = ld1<CG>(qm + ro + hc);
+        R.hmx = ld1<CG>(qm + HW + ro + hc);
       }
-      R.hx = __ldg(xp + ro + hc);
+      R.hx = ld1<CG>(xp + ro + hc);
     }
   };
   auto finish_row = [&](const Raw& R, T(&ty)[V], T(&tx)[V], T(&tu)[V], T& ty1, T& tx1, T& tu1) {
@@ -286,6 +309,314 @@ __global__ void fgp2d_finalize_kernel(const T* __restrict__ x, int64_t xps, T* q
       qb[idx] = yy;
       qb[HW + idx] = yx;
     }
+  }
+}
+
+// ---- SM-resident ProxSkip worker (config 4, the SMs the clusters leave) ----
+//
+// The 16-CTA clusters of fgp_cluster.cu fit only 7 times on a B200 (one per
+// GPC with >= 16 free SMs); the remaining SMs run this kernel concurrently,
+// one 512-thread CTA per SM, each working through its own list of whole
+// problems: for every coin-fired iteration of a problem the CTA runs the skip
+// chain + prox input, the n_inner FGP iterations (the streaming item above
+// with L2-coherent loads and a CTA barrier between iterations: the problem's
+// ~2 MB working set stays L2-resident), finalize + control variate, then the
+// trailing skips.  Same arithmetic as the streaming driver (proxskip_pre /
+// fgp2d_iter / fgp2d_finalize / proxskip_post).  The host splits the problems
+// between clusters and these workers by a static cost model, so which kernel
+// runs a problem does not depend on timing.
+struct SmRunArgs {
+  float* x;
+  const float* b;
+  float* h;
+  float* q;
+  int64_t qps;
+  float* z;                // prox-input scratch, (N, H, W)
+  const int32_t* asg_off;  // [n_workers + 1]
+  const int32_t* asg;
+  const int32_t* ev_off;
+  const int32_t* ev_k;
+  const uint8_t* rep;
+  int K;
+  int n_inner;
+  int accelerated;
+  int nonneg;
+  float weight, gamma, hc, pg, step;
+  int32_t* bad;
+  const float* betas;
+};
+
+constexpr int SM_THREADS = 512;
+constexpr int SM_SIDE = 256;
+
+__device__ __forceinline__ float sm_skip(float xo, float bo, float ho, float g) {
+  using A = Ar<float>;
+  return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
+}
+
+// rsqrt without the denormal rescaling (as the cluster kernel)
+__device__ __forceinline__ float sm_rsq(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// One FGP inner iteration of a 256 x 256 problem by one 512-thread CTA: warp w
+// marches rows 16w .. 16w+15, lane l owns columns 8l .. 8l+7 (two float4 per
+// array and row), so a row's column neighbours need one shuffle each way and
+// the previous row stays in registers.  Zero padding (q_y = 0 on the last row,
+// q_x = 0 on the last column: the FGP keeps both, see the cluster kernel)
+// replaces the boundary tests; the arithmetic is the cluster kernel's
+// operation for operation (packed f32x2, same FMA forms).
+template <bool mom, bool rp>
+__device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const float* qk,
+                                            const float* qm, float* qo, float beta, float step,
+                                            float w, int nonneg) {
+  constexpr int W = SM_SIDE, H = SM_SIDE;
+  constexpr int HW = H * W;
+  constexpr int RS = H / (SM_THREADS / 32);  // rows per warp strip
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = warp * RS, r1 = r0 + RS;
+  const int c0 = lane * 8;
+  const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
+  const float2 st2 = make_float2(step, step), w2 = make_float2(w, w);
+  struct Raw {
+    float4 ky[2], kx[2], my[2], mx[2], zz[2];
+  };
+  auto ld4 = [](const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); };
+  auto load = [&](int r, Raw& R, bool with_z) {
+    const int o = r * W + c0;
+    R.ky[0] = ld4(qk + o);
+    R.ky[1] = ld4(qk + o + 4);
+    R.kx[0] = ld4(qk + HW + o);
+    R.kx[1] = ld4(qk + HW + o + 4);
+    if constexpr (mom) {
+      R.my[0] = ld4(qm + o);
+      R.my[1] = ld4(qm + o + 4);
+      R.mx[0] = ld4(qm + HW + o);
+      R.mx[1] = ld4(qm + HW + o + 4);
+    }
+    if (with_z) {
+      R.zz[0] = ld4(z + o);
+      R.zz[1] = ld4(z + o + 4);
+    }
+  };
+  // float4 pair halves as float2 (columns (0,1), (2,3) of each float4)
+  auto lo = [](const float4& v) { return make_float2(v.x, v.y); };
+  auto hi = [](const float4& v) { return make_float2(v.z, v.w); };
+  // y = q_k + beta (q_k - q_{k-1}) (re-projected q_k at the first iteration)
+  auto y_of = [&](const Raw& R, float2 (&yy)[4], float2 (&yx)[4]) {
+#pragma unroll
+    for (int P = 0; P < 4; ++P) {
+      float2 ky = (P & 1) ? hi(R.ky[P >> 1]) : lo(R.ky[P >> 1]);
+      float2 kx = (P & 1) ? hi(R.kx[P >> 1]) : lo(R.kx[P >> 1]);
+      if constexpr (rp) {
+        const float sx = fminf(1.f, w * sm_rsq(fmaf(ky.x, ky.x, kx.x * kx.x)));
+        const float sy = fminf(1.f, w * sm_rsq(fmaf(ky.y, ky.y, kx.y * kx.y)));
+        ky = make_float2(ky.x * sx, ky.y * sy);
+        kx = make_float2(kx.x * sx, kx.y * sy);
+      }
+      if constexpr (mom) {
+        const float2 my = (P & 1) ? hi(R.my[P >> 1]) : lo(R.my[P >> 1]);
+        const float2 mx = (P & 1) ? hi(R.mx[P >> 1]) : lo(R.mx[P >> 1]);
+        yy[P] = __ffma2_rn(b2, __ffma2_rn(my, m1, ky), ky);
+        yx[P] = __ffma2_rn(b2, __ffma2_rn(mx, m1, kx), kx);
+      } else {
+        yy[P] = ky;
+        yx[P] = kx;
+      }
+    }
+  };
+  // u = clamp(z + ((yy - yy_up) + yx) - yx_left)
+  auto u_of = [&](const float2 (&yy)[4], const float2 (&yx)[4], const float2 (&yyu)[4],
+                  const Raw& R, float2 (&u)[4]) {
+    float left = __shfl_up_sync(0xffffffffu, yx[3].y, 1);
+    if (lane == 0) left = 0.f;
+#pragma unroll
+    for (int P = 0; P < 4; ++P) {
+      const float2 l2 = make_float2(P == 0 ? left : yx[P - 1].y, yx[P].x);
+      const float2 d1 = __fadd2_rn(__ffma2_rn(yyu[P], m1, yy[P]), yx[P]);
+      const float2 d2 = __ffma2_rn(l2, m1, d1);
+      const float2 zz = (P & 1) ? hi(R.zz[P >> 1]) : lo(R.zz[P >> 1]);
+      const float2 v = __fadd2_rn(zz, d2);
+      u[P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
+    }
+  };
+  // row i: y(i+1), u(i+1) from the prefetched row, then q_{k+1}(i); the two
+  // register sets alternate between "this row" and "next row" (no copies)
+  Raw Rn;
+  auto row = [&](int i, const float2 (&yy)[4], const float2 (&yx)[4], const float2 (&u)[4],
+                 float2 (&nyy)[4], float2 (&nyx)[4], float2 (&nu)[4]) {
+    if (i + 1 < H) {
+      y_of(Rn, nyy, nyx);
+      u_of(nyy, nyx, yy, Rn, nu);
+      if (i + 2 < H && i + 1 < r1) load(i + 2, Rn, true);
+    } else {
+#pragma unroll
+      for (int P = 0; P < 4; ++P) nu[P] = u[P];  // last row: gy = 0
+    }
+    float right = __shfl_down_sync(0xffffffffu, u[0].x, 1);
+    if (lane == 31) right = u[3].y;  // column W-1: gx = 0
+    float4 oy[2], ox[2];
+#pragma unroll
+    for (int P = 0; P < 4; ++P) {
+      const float2 rt = make_float2(u[P].y, P == 3 ? right : u[P + 1].x);
+      const float2 gy = __ffma2_rn(u[P], m1, nu[P]);
+      const float2 gx = __ffma2_rn(u[P], m1, rt);
+      const float2 ay = __ffma2_rn(st2, gy, yy[P]);
+      const float2 ax = __ffma2_rn(st2, gx, yx[P]);
+      const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
+      float2 sc = __fmul2_rn(w2, make_float2(sm_rsq(m2.x), sm_rsq(m2.y)));
+      sc.x = fminf(1.f, sc.x);
+      sc.y = fminf(1.f, sc.y);
+      const float2 ny = __fmul2_rn(ay, sc), nx = __fmul2_rn(ax, sc);
+      float* py = (P & 1) ? &oy[P >> 1].z : &oy[P >> 1].x;
+      float* px = (P & 1) ? &ox[P >> 1].z : &ox[P >> 1].x;
+      py[0] = ny.x;
+      py[1] = ny.y;
+      px[0] = nx.x;
+      px[1] = nx.y;
+    }
+    const int o = i * W + c0;
+    __stcg(reinterpret_cast<float4*>(qo + o), oy[0]);
+    __stcg(reinterpret_cast<float4*>(qo + o + 4), oy[1]);
+    __stcg(reinterpret_cast<float4*>(qo + HW + o), ox[0]);
+    __stcg(reinterpret_cast<float4*>(qo + HW + o + 4), ox[1]);
+  };
+  float2 ya[4], xa[4], ua[4], yb[4], xb[4], ub[4];
+  {
+    float2 yyu[4];
+#pragma unroll
+    for (int P = 0; P < 4; ++P) yyu[P] = make_float2(0.f, 0.f);
+    if (r0 > 0) {
+      Raw Ru;
+      load(r0 - 1, Ru, false);
+      float2 tx[4];
+      y_of(Ru, yyu, tx);
+    }
+    Raw Rc;
+    load(r0, Rc, true);
+    load(r0 + 1, Rn, true);  // r0 + 1 < H for every strip (RS >= 2)
+    y_of(Rc, ya, xa);
+    u_of(ya, xa, yyu, Rc, ua);
+  }
+  static_assert(RS % 2 == 0, "rows are processed in pairs");
+  for (int i = r0; i < r1; i += 2) {
+    row(i, ya, xa, ua, yb, xb, ub);
+    row(i + 1, yb, xb, ub, ya, xa, ua);
+  }
+}
+
+__global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) {
+  using A = Ar<float>;
+  constexpr int H = SM_SIDE, W = SM_SIDE;
+  constexpr int64_t HW = (int64_t)H * W;
+  constexpr int NV = (int)(HW / 4);
+  const int tid = threadIdx.x;
+  const float g = a.gamma;
+  for (int ai = a.asg_off[blockIdx.x]; ai < a.asg_off[blockIdx.x + 1]; ++ai) {
+    const int p = a.asg[ai];
+    float* xp = a.x + (int64_t)p * HW;
+    const float* bp = a.b + (int64_t)p * HW;
+    float* hp = a.h + (int64_t)p * HW;
+    float* zp = a.z + (int64_t)p * HW;
+    float* q0 = a.q + (int64_t)p * a.qps;
+    const int e0 = a.ev_off[p], e1 = a.ev_off[p + 1];
+    int kbad = 0x7fffffff;
+    int kprev = -1;
+    for (int e = e0; e < e1; ++e) {
+      const int kk = a.ev_k[e];
+      const int m = kk - kprev - 1, kf = kprev + 1;
+      // skips kprev+1 .. kk-1 (x materialised), prox input z (skip.py:66-70)
+      for (int v = tid; v < NV; v += SM_THREADS) {
+        float4 xv = __ldcg(reinterpret_cast<const float4*>(xp) + v);
+        const float4 bv = __ldcg(reinterpret_cast<const float4*>(bp) + v);
+        const float4 hv = __ldcg(reinterpret_cast<const float4*>(hp) + v);
+        float* xs = &xv.x;
+        const float* bs = &bv.x;
+        const float* hs = &hv.x;
+        float4 zv;
+        float* zs = &zv.x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float xo = xs[c];
+          for (int s2 = 0; s2 < m; ++s2) {
+            xo = sm_skip(xo, bs[c], hs[c], g);
+            if (!finite(xo)) kbad = min(kbad, kf + s2);
+          }
+          xs[c] = xo;
+          zs[c] = A::add(A::sub(xo, A::mul(g, A::sub(xo, bs[c]))), A::mul(a.hc, hs[c]));
+        }
+        if (m > 0) __stcg(reinterpret_cast<float4*>(xp) + v, xv);
+        __stcg(reinterpret_cast<float4*>(zp) + v, zv);
+      }
+      __syncthreads();
+      // FGP on z with the warm start in slot 0 (re-projected at the run's
+      // first call if the weight changed, tv.py:68-69)
+      const bool rp0 = e == e0 && a.rep[p];
+      for (int it = 0; it < a.n_inner; ++it) {
+        const float beta = (a.accelerated && it > 0) ? a.betas[it - 1] : 0.f;
+        const float* qk = q0 + (int64_t)(it % 3) * 2 * HW;
+        const float* qm = q0 + (int64_t)((it + 2) % 3) * 2 * HW;
+        float* qo = q0 + (int64_t)((it + 1) % 3) * 2 * HW;
+        if (beta != 0.f)
+          sm_fgp_iter<true, false>(zp, qk, qm, qo, beta, a.step, a.weight, a.nonneg);
+        else if (it == 0 && rp0)
+          sm_fgp_iter<false, true>(zp, qk, qm, qo, beta, a.step, a.weight, a.nonneg);
+        else
+          sm_fgp_iter<false, false>(zp, qk, qm, qo, beta, a.step, a.weight, a.nonneg);
+        __syncthreads();
+      }
+      // finalize u = clamp(z + div q_n) (tv.py:89), ProxSkip post (skip.py:68-75),
+      // q_n -> warm-start slot 0
+      const int slot = a.n_inner % 3;
+      const float* qn = q0 + (int64_t)slot * 2 * HW;
+      bool ok = true;
+      for (int idx = tid; idx < (int)HW; idx += SM_THREADS) {
+        const int i = idx / W, c = idx % W;
+        const float yy = __ldcg(qn + idx), yx = __ldcg(qn + HW + idx);
+        const float yyu = i > 0 ? __ldcg(qn + idx - W) : 0.f;
+        const float yxl = c > 0 ? __ldcg(qn + HW + idx - 1) : 0.f;
+        const float d = div_at<float>(i, c, H, W, yy, yyu, yx, yxl);
+        const float u = clampu(A::add(__ldcg(zp + idx), d), a.nonneg);
+        const float xo = __ldcg(xp + idx), bo = __ldcg(bp + idx), ho = __ldcg(hp + idx);
+        const float xhat = sm_skip(xo, bo, ho, g);
+        __stcg(hp + idx, A::add(ho, A::mul(a.pg, A::sub(u, xhat))));
+        __stcg(xp + idx, u);
+        ok &= finite(u);
+        if (slot != 0) {
+          __stcg(q0 + idx, yy);
+          __stcg(q0 + HW + idx, yx);
+        }
+      }
+      if (!ok) kbad = min(kbad, kk);
+      kprev = kk;
+      __syncthreads();
+    }
+    // trailing skips kprev+1 .. K-1
+    const int m = a.K - 1 - kprev;
+    if (m > 0) {
+      for (int v = tid; v < NV; v += SM_THREADS) {
+        float4 xv = __ldcg(reinterpret_cast<const float4*>(xp) + v);
+        const float4 bv = __ldcg(reinterpret_cast<const float4*>(bp) + v);
+        const float4 hv = __ldcg(reinterpret_cast<const float4*>(hp) + v);
+        float* xs = &xv.x;
+        const float* bs = &bv.x;
+        const float* hs = &hv.x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float xo = xs[c];
+          for (int s2 = 0; s2 < m; ++s2) {
+            xo = sm_skip(xo, bs[c], hs[c], g);
+            if (!finite(xo)) kbad = min(kbad, kprev + 1 + s2);
+          }
+          xs[c] = xo;
+        }
+        __stcg(reinterpret_cast<float4*>(xp) + v, xv);
+      }
+    }
+    if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
+    __syncthreads();
   }
 }
 
@@ -442,6 +773,20 @@ int aprojgd_dual_rof(int dtype, const void* b, void* q, int H, int W, double alp
                      1, 0, step, beta.data() + 1, st);
   if (rc) return rc;
   return fgp2d_finalize(dtype, b, HW, q, 6 * HW, nullptr, 1, H, W, iters, 0, u, HW, st);
+}
+
+int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const int32_t* asg_off,
+           const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
+           const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
+           double gamma, double hc, double pg, double step, const float* betas, int32_t* bad,
+           cudaStream_t st) {
+  if (n_workers <= 0) return PSB_OK;
+  SmRunArgs a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, (float*)z, asg_off, asg,
+              ev_off, ev_k, rep, K, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
+              (float)hc, (float)pg, (float)step, bad, betas};
+  fgp_sm_run_kernel<<<n_workers, SM_THREADS, 0, st>>>(a);
+  PSB_LAUNCHED("fgp_sm_run");
+  return PSB_OK;
 }
 
 }  // namespace psb

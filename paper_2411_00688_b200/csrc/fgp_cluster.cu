@@ -40,8 +40,12 @@ namespace psb {
 namespace {
 
 constexpr int CW = 256;           // image width  (columns = threads per row group)
-constexpr int CRG = 2;            // row groups per CTA
-constexpr int CRPT = 8;           // rows per thread
+#ifndef PSB_CLUSTER_CRG
+#define PSB_CLUSTER_CRG 2
+#define PSB_CLUSTER_CRPT 8
+#endif
+constexpr int CRG = PSB_CLUSTER_CRG;    // row groups per CTA
+constexpr int CRPT = PSB_CLUSTER_CRPT;  // rows per thread
 constexpr int CCL = 16;           // CTAs per cluster
 constexpr int CH = CCL * CRG * CRPT;  // image height = 256
 constexpr int CTHREADS = CW * CRG;    // 512 (8 rows per thread: up to 128 registers)
@@ -76,7 +80,7 @@ __device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
   return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
 }
 
-static_assert(CRPT % 4 == 0, "edge exchange packs float4s per thread row group");
+static_assert(CRPT % 2 == 0 && CRG * CRPT == 16, "row pairs; 16 rows per CTA");
 
 // 32-bit shared::cluster address of `p` in CTA `rank` of this cluster, and a load from it
 __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {

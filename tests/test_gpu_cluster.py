@@ -114,3 +114,47 @@ def test_cluster_occupancy_query():
     L.call("psb_cluster_max_active", ctypes.byref(n))
     assert n.value >= 1
     print("max active 16-CTA clusters:", n.value)
+
+
+@pytest.mark.parametrize("ratio", ["2", "18"])
+def test_cluster_with_sm_workers_matches_streaming_and_oracle(ratio, monkeypatch):
+    """More problems than resident clusters: the SMs the clusters leave run
+    fgp_sm_run_kernel on a share of the problems (PSB_SM_RATIO = 2 hands them
+    most of the batch)."""
+    idx = np.arange(40) * 97 % 4096
+    b = _batch(idx)
+    K, inner, p = 30, 10, 0.2
+    monkeypatch.setenv("PSB_SM_RATIO", ratio)
+    xc, cc = _run(b, idx, K, inner, p, stream_only=False)
+    xs, cs = _run(b, idx, K, inner, p, stream_only=True)
+    np.testing.assert_array_equal(cc, cs)
+    for j in range(len(idx)):
+        assert rel(xc[j], xs[j]) < 2e-6, j
+    for j in (0, 17, 39):
+        xr, _, n_prox, _ = oc.proxskip_denoise(b[j], 0.1, p, int(idx[j]), K, inner)
+        assert cc[j] == n_prox
+        assert rel(xc[j], xr) < 1e-5
+
+
+def test_sm_workers_warm_restart_and_divergence(monkeypatch):
+    """Two run segments on one solver with SM workers (x, h, warm starts carry
+    over), and a non-finite problem reported with its first bad iteration."""
+    idx = np.arange(20)
+    b = _batch(idx).astype(np.float32)
+    b[13, 5, 5] = np.nan
+    monkeypatch.setenv("PSB_SM_RATIO", "2")
+    s = psb.BatchedTvDenoise(b, 0.1, 8, precision="fp32")
+    s.run_proxskip(psb.coin_table(0.3, idx, 12), 1.0, 0.3)
+    s.run_proxskip(psb.coin_table(0.3, idx + 500, 9), 1.0, 0.3)
+    monkeypatch.setenv("PSB_NO_CLUSTER", "1")
+    r = psb.BatchedTvDenoise(b, 0.1, 8, precision="fp32")
+    r.run_proxskip(psb.coin_table(0.3, idx, 12), 1.0, 0.3)
+    r.run_proxskip(psb.coin_table(0.3, idx + 500, 9), 1.0, 0.3)
+    for j in range(20):
+        if j == 13:
+            continue
+        assert rel(s.x[j].cpu().numpy(), r.x[j].cpu().numpy()) < 2e-6
+        assert rel(s.slots[j, 0].cpu().numpy(), r.slots[j, 0].cpu().numpy()) < 1e-5
+    with pytest.raises(psb.DivergenceError) as ei:
+        s.check_finite()
+    assert ei.value.iteration == 0

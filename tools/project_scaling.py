@@ -20,19 +20,26 @@ out = {}
 b_all = bench.make_inputs(np.arange(4096))
 for n in (1, 2, 4, 8):
     worst = 0.0
+    per = []
     for r in range(n):
         idx = batched.shard_indices(4096, r, n)
         coins = batched.coin_table(0.1, idx, W + K)
         s = psb.BatchedTvDenoise(b_all[idx], 0.1, 50, precision="fp32")
-        s.run_proxskip(coins[:W], 1.0, 0.1)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        s.run_proxskip(coins[W:], 1.0, 0.1)
-        e1.record()
-        torch.cuda.synchronize()
-        worst = max(worst, e0.elapsed_time(e1) / 1e3)
+        best = None
+        for rep in range(2):  # best of two cold runs (host-side one-offs excluded)
+            s.reset()
+            s.run_proxskip(coins[:W], 1.0, 0.1)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s.run_proxskip(coins[W:], 1.0, 0.1)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None else min(best, t)
+        per.append(round(best, 5))
+        worst = max(worst, best)
         del s
     out[n] = worst
     print(json.dumps({"n": n, "slowest_rank_s": worst, "it_s": K / worst,
-                      "projected_efficiency": out[1] / (n * worst)}), flush=True)
+                      "projected_efficiency": out[1] / (n * worst), "per_rank_s": per}), flush=True)
