@@ -362,9 +362,10 @@ __device__ __forceinline__ float sm_rsq(float x) {
 }
 
 // One FGP inner iteration of a 256 x 256 problem by one 512-thread CTA: warp w
-// marches rows 16w .. 16w+15, lane l owns columns 8l .. 8l+7 (two float4 per
-// array and row), so a row's column neighbours need one shuffle each way and
-// the previous row stays in registers.  Zero padding (q_y = 0 on the last row,
+// marches rows 16w .. 16w+15, lane l owns columns 4l .. 4l+3 (half A) and
+// 128+4l .. 128+4l+3 (half B) -- one fully coalesced float4 per half, array
+// and row -- so a row's column neighbours need two shuffles each way and the
+// previous row stays in registers.  Zero padding (q_y = 0 on the last row,
 // q_x = 0 on the last column: the FGP keeps both, see the cluster kernel)
 // replaces the boundary tests; the arithmetic is the cluster kernel's
 // operation for operation (packed f32x2, same FMA forms).
@@ -377,7 +378,7 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
   constexpr int RS = H / (SM_THREADS / 32);  // rows per warp strip
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = warp * RS, r1 = r0 + RS;
-  const int c0 = lane * 8;
+  const int c0 = lane * 4;  // half A; half B at c0 + W/2
   const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
   const float2 st2 = make_float2(step, step), w2 = make_float2(w, w);
   struct Raw {
@@ -386,19 +387,20 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
   auto ld4 = [](const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); };
   auto load = [&](int r, Raw& R, bool with_z) {
     const int o = r * W + c0;
+    constexpr int B = W / 2;
     R.ky[0] = ld4(qk + o);
-    R.ky[1] = ld4(qk + o + 4);
+    R.ky[1] = ld4(qk + o + B);
     R.kx[0] = ld4(qk + HW + o);
-    R.kx[1] = ld4(qk + HW + o + 4);
+    R.kx[1] = ld4(qk + HW + o + B);
     if constexpr (mom) {
       R.my[0] = ld4(qm + o);
-      R.my[1] = ld4(qm + o + 4);
+      R.my[1] = ld4(qm + o + B);
       R.mx[0] = ld4(qm + HW + o);
-      R.mx[1] = ld4(qm + HW + o + 4);
+      R.mx[1] = ld4(qm + HW + o + B);
     }
     if (with_z) {
       R.zz[0] = ld4(z + o);
-      R.zz[1] = ld4(z + o + 4);
+      R.zz[1] = ld4(z + o + B);
     }
   };
   // float4 pair halves as float2 (columns (0,1), (2,3) of each float4)
@@ -430,11 +432,14 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
   // u = clamp(z + ((yy - yy_up) + yx) - yx_left)
   auto u_of = [&](const float2 (&yy)[4], const float2 (&yx)[4], const float2 (&yyu)[4],
                   const Raw& R, float2 (&u)[4]) {
-    float left = __shfl_up_sync(0xffffffffu, yx[3].y, 1);
-    if (lane == 0) left = 0.f;
+    // column left of half A: lane l-1's half A (0 left of column 0); of half
+    // B: lane l-1's half B, lane 0 takes lane 31's half A (column 127)
+    float left_a = __shfl_up_sync(0xffffffffu, yx[1].y, 1);
+    if (lane == 0) left_a = 0.f;
+    const float left_b = __shfl_sync(0xffffffffu, lane == 31 ? yx[1].y : yx[3].y, (lane + 31) & 31);
 #pragma unroll
     for (int P = 0; P < 4; ++P) {
-      const float2 l2 = make_float2(P == 0 ? left : yx[P - 1].y, yx[P].x);
+      const float2 l2 = make_float2(P == 0 ? left_a : P == 2 ? left_b : yx[P - 1].y, yx[P].x);
       const float2 d1 = __fadd2_rn(__ffma2_rn(yyu[P], m1, yy[P]), yx[P]);
       const float2 d2 = __ffma2_rn(l2, m1, d1);
       const float2 zz = (P & 1) ? hi(R.zz[P >> 1]) : lo(R.zz[P >> 1]);
@@ -455,12 +460,16 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
 #pragma unroll
       for (int P = 0; P < 4; ++P) nu[P] = u[P];  // last row: gy = 0
     }
-    float right = __shfl_down_sync(0xffffffffu, u[0].x, 1);
-    if (lane == 31) right = u[3].y;  // column W-1: gx = 0
+    // column right of half A: lane l+1's half A, lane 31 takes lane 0's half
+    // B (column 128); of half B: lane l+1's half B, lane 31 keeps its own
+    // (column W-1: gx = 0)
+    const float right_a = __shfl_sync(0xffffffffu, lane == 0 ? u[2].x : u[0].x, (lane + 1) & 31);
+    float right_b = __shfl_down_sync(0xffffffffu, u[2].x, 1);
+    if (lane == 31) right_b = u[3].y;
     float4 oy[2], ox[2];
 #pragma unroll
     for (int P = 0; P < 4; ++P) {
-      const float2 rt = make_float2(u[P].y, P == 3 ? right : u[P + 1].x);
+      const float2 rt = make_float2(u[P].y, P == 1 ? right_a : P == 3 ? right_b : u[P + 1].x);
       const float2 gy = __ffma2_rn(u[P], m1, nu[P]);
       const float2 gx = __ffma2_rn(u[P], m1, rt);
       const float2 ay = __ffma2_rn(st2, gy, yy[P]);
@@ -479,9 +488,9 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
     }
     const int o = i * W + c0;
     __stcg(reinterpret_cast<float4*>(qo + o), oy[0]);
-    __stcg(reinterpret_cast<float4*>(qo + o + 4), oy[1]);
+    __stcg(reinterpret_cast<float4*>(qo + o + W / 2), oy[1]);
     __stcg(reinterpret_cast<float4*>(qo + HW + o), ox[0]);
-    __stcg(reinterpret_cast<float4*>(qo + HW + o + 4), ox[1]);
+    __stcg(reinterpret_cast<float4*>(qo + HW + o + W / 2), ox[1]);
   };
   float2 ya[4], xa[4], ua[4], yb[4], xb[4], ub[4];
   {
