@@ -581,21 +581,35 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
       const int slot = a.n_inner % 3;
       const float* qn = q0 + (int64_t)slot * 2 * HW;
       bool ok = true;
-      for (int idx = tid; idx < (int)HW; idx += SM_THREADS) {
-        const int i = idx / W, c = idx % W;
-        const float yy = __ldcg(qn + idx), yx = __ldcg(qn + HW + idx);
-        const float yyu = i > 0 ? __ldcg(qn + idx - W) : 0.f;
+      for (int v = tid; v < NV; v += SM_THREADS) {  // 4 columns of one row
+        const int idx = 4 * v, i = idx / W, c = idx % W;
+        const float4 yy4 = __ldcg(reinterpret_cast<const float4*>(qn + idx));
+        const float4 yx4 = __ldcg(reinterpret_cast<const float4*>(qn + HW + idx));
+        const float4 yu4 = i > 0 ? __ldcg(reinterpret_cast<const float4*>(qn + idx - W))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         const float yxl = c > 0 ? __ldcg(qn + HW + idx - 1) : 0.f;
-        const float d = div_at<float>(i, c, H, W, yy, yyu, yx, yxl);
-        const float u = clampu(A::add(__ldcg(zp + idx), d), a.nonneg);
-        const float xo = __ldcg(xp + idx), bo = __ldcg(bp + idx), ho = __ldcg(hp + idx);
-        const float xhat = sm_skip(xo, bo, ho, g);
-        __stcg(hp + idx, A::add(ho, A::mul(a.pg, A::sub(u, xhat))));
-        __stcg(xp + idx, u);
-        ok &= finite(u);
+        const float4 z4 = __ldcg(reinterpret_cast<const float4*>(zp) + v);
+        const float4 x4 = __ldcg(reinterpret_cast<const float4*>(xp) + v);
+        const float4 b4 = __ldcg(reinterpret_cast<const float4*>(bp) + v);
+        const float4 h4 = __ldcg(reinterpret_cast<const float4*>(hp) + v);
+        const float yys[4] = {yy4.x, yy4.y, yy4.z, yy4.w}, yxs[4] = {yx4.x, yx4.y, yx4.z, yx4.w};
+        const float yus[4] = {yu4.x, yu4.y, yu4.z, yu4.w}, zs[4] = {z4.x, z4.y, z4.z, z4.w};
+        const float xs[4] = {x4.x, x4.y, x4.z, x4.w}, bs[4] = {b4.x, b4.y, b4.z, b4.w};
+        const float hs[4] = {h4.x, h4.y, h4.z, h4.w};
+        float un[4], hn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float d = div_at<float>(i, c + k, H, W, yys[k], yus[k], yxs[k], k > 0 ? yxs[k - 1] : yxl);
+          un[k] = clampu(A::add(zs[k], d), a.nonneg);
+          const float xhat = sm_skip(xs[k], bs[k], hs[k], g);
+          hn[k] = A::add(hs[k], A::mul(a.pg, A::sub(un[k], xhat)));
+          ok &= finite(un[k]);
+        }
+        __stcg(reinterpret_cast<float4*>(hp) + v, make_float4(hn[0], hn[1], hn[2], hn[3]));
+        __stcg(reinterpret_cast<float4*>(xp) + v, make_float4(un[0], un[1], un[2], un[3]));
         if (slot != 0) {
-          __stcg(q0 + idx, yy);
-          __stcg(q0 + HW + idx, yx);
+          __stcg(reinterpret_cast<float4*>(q0 + idx), yy4);
+          __stcg(reinterpret_cast<float4*>(q0 + HW + idx), yx4);
         }
       }
       if (!ok) kbad = min(kbad, kk);
