@@ -178,7 +178,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     // SM workers could take the GPC space the clusters need.)
     const char* no_sm = std::getenv("PSB_NO_SMWORK");
     const char* ratio_env = std::getenv("PSB_SM_RATIO");
-    const double ratio = ratio_env ? std::atof(ratio_env) : 20.0;
+    const double ratio = ratio_env ? std::atof(ratio_env) : 21.0;
     if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1') && ratio > 0)
       NW = std::max(0, sm_count() - G * 16);
     std::vector<int32_t> order(n);

@@ -39,17 +39,15 @@ namespace psb {
 
 namespace {
 
-constexpr int CW = 256;           // image width  (columns = threads per row group)
-#ifndef PSB_CLUSTER_CRG
-#define PSB_CLUSTER_CRG 2
-#define PSB_CLUSTER_CRPT 8
-#endif
-constexpr int CRG = PSB_CLUSTER_CRG;    // row groups per CTA
-constexpr int CRPT = PSB_CLUSTER_CRPT;  // rows per thread
-constexpr int CCL = 16;           // CTAs per cluster
-constexpr int CH = CCL * CRG * CRPT;  // image height = 256
-constexpr int CTHREADS = CW * CRG;    // 512 (8 rows per thread: up to 128 registers)
-constexpr int CWARPS_ROW = CW / 32;   // 8 warps across a row group
+constexpr int CW = 256;    // image width
+constexpr int CCOLS = 2;   // columns per thread
+constexpr int CRPT = 4;    // rows per thread
+constexpr int CTPR = CW / CCOLS;           // threads per row group (128)
+constexpr int CRG = 4;                     // row groups per CTA
+constexpr int CCL = 16;                    // CTAs per cluster
+constexpr int CH = CCL * CRG * CRPT;       // image height = 256
+constexpr int CTHREADS = CTPR * CRG;       // 512 (8 pixels per thread: up to 128 registers)
+constexpr int CWARPS_ROW = CTPR / 32;      // 4 warps across a row group
 constexpr int kMaxBetas = 1024;       // momentum table staged in shared memory
 
 template <class TO>
@@ -80,7 +78,7 @@ __device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
   return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
 }
 
-static_assert(CRPT % 2 == 0 && CRG * CRPT == 16, "row pairs; 16 rows per CTA");
+static_assert(CRG * CRPT == 16, "16 rows per CTA");
 
 // 32-bit shared::cluster address of `p` in CTA `rank` of this cluster, and a load from it
 __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
@@ -137,6 +135,14 @@ __device__ __forceinline__ void st_async_v2(uint32_t raddr, float v0, float v1, 
                : "memory");
 }
 
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float v0, float v1, float v2, float v3,
+                                            uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(raddr),
+               "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(__float_as_uint(v2)),
+               "r"(__float_as_uint(v3)), "r"(rmbar)
+               : "memory");
+}
+
 // MUFU.RSQ without the denormal rescaling rsqrtf() wraps around it (|a|^2 of a
 // dual vector is never denormal in a way that matters: the ball test is
 // min(1, w / |a|)); 1 instruction instead of ~6 per pixel.
@@ -153,15 +159,18 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-// Per-thread column strips are held as row PAIRS (t, t + 4) in float2
-// registers, so Blackwell's packed f32x2 FFMA2 / FADD2 / FMUL2 work on
-// naturally aligned register pairs: the vertical neighbours of pair P are the
-// pairs P - 1 / P + 1, and only the strip ends (rows -1 and 8) build a pair
-// from two halves.  rowref(v, t) names row t (t a compile-time constant
-// after unrolling).
+// Thread tile: 2 adjacent columns x CRPT (= 4) rows.  Each column strip is
+// held as row PAIRS (t, t + 2) in float2 registers, so Blackwell's packed
+// f32x2 FFMA2 / FADD2 / FMUL2 work on naturally aligned register pairs: the
+// vertical neighbours of pair P are the pairs P^1 (one strip end builds a
+// pair from two halves), the horizontal neighbour of column 0 is column 1 of
+// the same thread, and only one column per side crosses to another lane
+// (one shuffle per row and direction instead of two).  rowref(v, t) names
+// row t of a column strip (t a compile-time constant after unrolling).
 constexpr int NP = CRPT / 2;
+static_assert(NP == 2, "row pairs (t, t+2) of a 4-row strip");
 __device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
-  return t < NP ? v[t].x : v[t - NP].y;
+  return (t & 1) ? ((t >> 1) ? v[1].y : v[1].x) : ((t >> 1) ? v[0].y : v[0].x);
 }
 
 // Exchange pattern per inner iteration: at the end of iteration t every CTA
@@ -179,8 +188,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank();
   const int tid = threadIdx.x;
-  const int j = tid % CW, rg = tid / CW;
-  const int lane = tid & 31, wc = j >> 5;
+  const int jt = tid % CTPR, rg = tid / CTPR;  // column pair, row group
+  const int j0 = 2 * jt;                        // columns j0, j0 + 1
+  const int lane = tid & 31, wc = jt >> 5;
   const int row0 = cr * (CRG * CRPT) + rg * CRPT;
   const bool rg_top = rg == 0, rg_bot = rg == CRG - 1;
   const bool has_up = cr > 0, has_dn = cr < CCL - 1;
@@ -188,14 +198,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   constexpr int SR = CRG * CRPT;  // rows of this CTA
 
   // halo rows received from the neighbours, double-buffered by round parity
-  __shared__ __align__(8) float rx_dn[2][CW][2];  // CTA below's first row of q (y, x)
-  __shared__ float rx_up[2][CW];                  // CTA above's last row of q (y)
+  __shared__ __align__(16) float rx_dn[2][CW][2];  // CTA below's first row of q (y, x)
+  __shared__ __align__(8) float rx_up[2][CW];      // CTA above's last row of q (y)
   __shared__ __align__(8) uint64_t mb_dn[2], mb_up[2];
-  __shared__ float s_rg_yy[CRG][CW];   // each row group's last-row y_y (for the group below)
-  __shared__ float s_rg_u[CRG][CW];    // each row group's first-row u (for the group above)
-  // warp-edge columns as row pairs: s_edge_yx[rg][.][w + 1] = last lane of warp w
-  // (slot 0 stays zero: nothing left of column 0; [NP].x = the halo row's y_x),
-  // s_edge_u[rg][.][w] = first lane of warp w (pair-major: one STS.64 per pair)
+  __shared__ __align__(8) float s_rg_yy[CRG][CW];  // each row group's last-row y_y (for the group below)
+  __shared__ __align__(8) float s_rg_u[CRG][CW];   // each row group's first-row u (for the group above)
+  // warp-edge columns as row pairs: s_edge_yx[rg][.][w + 1] = last column of
+  // warp w (slot 0 stays zero: nothing left of column 0; [NP].x = the halo
+  // row's y_x), s_edge_u[rg][.][w] = first column of warp w
   __shared__ __align__(16) float2 s_edge_yx[CRG][NP + 1][CWARPS_ROW + 1];
   __shared__ __align__(16) float2 s_edge_u[CRG][NP][CWARPS_ROW];
   __shared__ float s_beta[kMaxBetas];
@@ -227,16 +237,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const uint32_t dn_rx_remote = dsmem_addr(&rx_up[0][0], cr < CCL - 1 ? cr + 1 : cr); // my bottom row -> CTA below
   const uint32_t dn_mb_remote = dsmem_addr(&mb_up[0], cr < CCL - 1 ? cr + 1 : cr);
   // the CTA below's first staged row (x, b, h), read once per prox call
-  const uint32_t ex_x_remote = dsmem_addr(sx + j, cr < CCL - 1 ? cr + 1 : cr);
-  const uint32_t ex_b_remote = dsmem_addr(sb + j, cr < CCL - 1 ? cr + 1 : cr);
-  const uint32_t ex_h_remote = dsmem_addr(sh + j, cr < CCL - 1 ? cr + 1 : cr);
+  const uint32_t ex_x_remote = dsmem_addr(sx + j0, cr < CCL - 1 ? cr + 1 : cr);
+  const uint32_t ex_b_remote = dsmem_addr(sb + j0, cr < CCL - 1 ? cr + 1 : cr);
+  const uint32_t ex_h_remote = dsmem_addr(sh + j0, cr < CCL - 1 ? cr + 1 : cr);
   unsigned round = 0;
-  auto push_rows = [&](float top_y, float top_x, float bot_y) {
+  auto push_rows = [&](float ty0, float tx0, float ty1, float tx1, float by0, float by1) {
     const unsigned b = round & 1;
     if (rg_top && cr > 0)
-      st_async_v2(up_rx_remote + 4u * (b * CW * 2 + j * 2), top_y, top_x, up_mb_remote + 8u * b);
+      st_async_v4(up_rx_remote + 4u * (b * CW * 2 + j0 * 2), ty0, tx0, ty1, tx1, up_mb_remote + 8u * b);
     if (rg_bot && cr < CCL - 1)
-      st_async_f32(dn_rx_remote + 4u * (b * CW + j), bot_y, dn_mb_remote + 8u * b);
+      st_async_v2(dn_rx_remote + 4u * (b * CW + j0), by0, by1, dn_mb_remote + 8u * b);
   };
   // wait for round `r` (consumer side); returns the buffer index
   // warp-uniform roles: the bottom row group waits for the CTA below, the top
@@ -257,6 +267,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   };
   const bool last_row_thread = rg_bot && !has_dn;  // owns global row H-1 (t = CRPT-1)
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
+  const bool last_col = lane == 31 && wc == CWARPS_ROW - 1;  // owns global column W-1
 
   const int c = blockIdx.x / CCL;
   for (int ai = a.asg_off[c]; ai < a.asg_off[c + 1]; ++ai) {
@@ -271,12 +282,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
     const int lr = rg * CRPT + t;
-    const int64_t o = (int64_t)(row0 + t) * CW + j;
-    sx[lr * CW + j] = xp[o];
-    sb[lr * CW + j] = bp[o];
-    sh[lr * CW + j] = hp[o];
+    const int64_t o = (int64_t)(row0 + t) * CW + j0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      sx[lr * CW + j0 + k] = xp[o + k];
+      sb[lr * CW + j0 + k] = bp[o + k];
+      sh[lr * CW + j0 + k] = hp[o + k];
+    }
   }
-  float2 z[NP], qky[NP], qkx[NP], qmy[NP], qmx[NP];
+  // per column k: z, q_k, q_{k-1} as row pairs
+  float2 z[2][NP], qky[2][NP], qkx[2][NP], qmy[2][NP], qmx[2][NP];
   int kbad = 0x7fffffff;
   int kprev = -1;
   for (int e = e0; e < e1; ++e) {
@@ -297,148 +312,190 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     return (float)A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(a.hc, ho));
   };
 #pragma unroll
-  for (int t = 0; t < CRPT; ++t) {
-    const int lr = rg * CRPT + t;
-    rowref(z, t) = prox_input(sx[lr * CW + j], sb[lr * CW + j], sh[lr * CW + j], true);
-    if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
-      const int64_t o = (int64_t)(row0 + t) * CW + j;
-      float vy = q0[o], vx = q0[HW + o];
-      if (a.rep[p]) {
-        const float sc = F::ball_scale(vy, vx, w);
-        vy *= sc;
-        vx *= sc;
+  for (int k = 0; k < 2; ++k) {
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      const int lr = rg * CRPT + t;
+      const int sj = lr * CW + j0 + k;
+      rowref(z[k], t) = prox_input(sx[sj], sb[sj], sh[sj], true);
+      if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
+        const int64_t o = (int64_t)(row0 + t) * CW + j0 + k;
+        float vy = q0[o], vx = q0[HW + o];
+        if (a.rep[p]) {
+          const float sc = F::ball_scale(vy, vx, w);
+          vy *= sc;
+          vx *= sc;
+        }
+        // The reference's divergence ignores q_y on the last row and q_x on
+        // the last column (operators.py:66-70) and the gradient is 0 there,
+        // so those entries stay 0 from a cold start; zeroing them here lets
+        // the inner loop drop every boundary test (zero padding, not masks).
+        if (row0 + t == CH - 1) vy = 0.f;
+        if (j0 + k == CW - 1) vx = 0.f;
+        rowref(qky[k], t) = vy;
+        rowref(qkx[k], t) = vx;
       }
-      // The reference's divergence ignores q_y on the last row and q_x on the
-      // last column (operators.py:66-70) and the gradient is 0 there, so those
-      // entries stay 0 from a cold start; zeroing them here lets the inner
-      // loop drop every boundary test (zero padding instead of masks).
-      if (row0 + t == CH - 1) vy = 0.f;
-      if (j == CW - 1) vx = 0.f;
-      rowref(qky, t) = vy;
-      rowref(qkx, t) = vx;
+    }
+#pragma unroll
+    for (int P = 0; P < NP; ++P) {
+      qmy[k][P] = qky[k][P];  // the momentum restarts with every call (tv.py:72)
+      qmx[k][P] = qkx[k][P];
     }
   }
-#pragma unroll
-  for (int P = 0; P < NP; ++P) {
-    qmy[P] = qky[P];  // the momentum restarts with every call (tv.py:72)
-    qmx[P] = qkx[P];
-  }
   // the bottom row group also owns the CTA-below's first row for u
-  float z_ex = 0.f;
-  if (rg_bot && has_dn)
-    z_ex = prox_input(dsmem_ld<TO>(ex_x_remote), dsmem_ld<TO>(ex_b_remote),
-                      dsmem_ld<TO>(ex_h_remote), false);
+  float z_ex[2] = {0.f, 0.f};
+  if (rg_bot && has_dn) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      z_ex[k] = prox_input(dsmem_ld<TO>(ex_x_remote + k * sizeof(TO)),
+                           dsmem_ld<TO>(ex_b_remote + k * sizeof(TO)),
+                           dsmem_ld<TO>(ex_h_remote + k * sizeof(TO)), false);
+  }
   const unsigned round0 = round;  // this call's warm-start round
-  push_rows(qky[0].x, qkx[0].x, rowref(qky, CRPT - 1));
+  push_rows(qky[0][0].x, qkx[0][0].x, qky[1][0].x, qkx[1][0].x, qky[0][1].y, qky[1][1].y);
   ++round;
 
-  float up_k = 0.f, up_m = 0.f;                          // row above, row channel
-  float dn_ky = 0.f, dn_kx = 0.f, dn_my = 0.f, dn_mx = 0.f;  // row below, both channels
+  float up_k[2] = {0.f, 0.f}, up_m[2] = {0.f, 0.f};  // row above, row channel
+  float dn_ky[2] = {0.f, 0.f}, dn_kx[2] = {0.f, 0.f}, dn_my[2] = {0.f, 0.f}, dn_mx[2] = {0.f, 0.f};
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   // Each pixel's arithmetic is the scalar FGP step (each f32x2 lane an IEEE
   // fp32 op; a - b = fma(b, -1, a)).
-  auto inner = [&](float2(&QKy)[NP], float2(&QKx)[NP], float2(&QMy)[NP], float2(&QMx)[NP],
-                   int it) {
+  auto inner = [&](float2(&QKy)[2][NP], float2(&QKx)[2][NP], float2(&QMy)[2][NP],
+                   float2(&QMx)[2][NP], int it) {
     const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
     const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
-    float2 yy[NP], yx[NP];
+    float2 yy[2][NP], yx[2][NP];
 #pragma unroll
-    for (int P = 0; P < NP; ++P) {
-      yy[P] = __ffma2_rn(b2, __ffma2_rn(QMy[P], m1, QKy[P]), QKy[P]);
-      yx[P] = __ffma2_rn(b2, __ffma2_rn(QMx[P], m1, QKx[P]), QKx[P]);
-    }
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        yy[k][P] = __ffma2_rn(b2, __ffma2_rn(QMy[k][P], m1, QKy[k][P]), QKy[k][P]);
+        yx[k][P] = __ffma2_rn(b2, __ffma2_rn(QMx[k][P], m1, QKx[k][P]), QKx[k][P]);
+      }
     const unsigned par = recv_rows(round0 + it);
-    float y_up = 0.f, ex_y = 0.f, ex_x = 0.f;
+    float y_up[2] = {0.f, 0.f}, ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f};
     if (rg_top && has_up) {
-      const float v = rx_up[par][j];
-      up_m = it == 0 ? v : up_k;
-      up_k = v;
-      y_up = up_k + beta * (up_k - up_m);
+      const float2 v = *reinterpret_cast<const float2*>(&rx_up[par][j0]);
+      const float vv[2] = {v.x, v.y};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        up_m[k] = it == 0 ? vv[k] : up_k[k];
+        up_k[k] = vv[k];
+        y_up[k] = up_k[k] + beta * (up_k[k] - up_m[k]);
+      }
     }
     if (rg_bot && has_dn) {
-      const float vy = rx_dn[par][j][0], vx = rx_dn[par][j][1];
-      dn_my = it == 0 ? vy : dn_ky;
-      dn_mx = it == 0 ? vx : dn_kx;
-      dn_ky = vy;
-      dn_kx = vx;
-      ex_y = dn_ky + beta * (dn_ky - dn_my);
-      ex_x = dn_kx + beta * (dn_kx - dn_mx);
+      const float4 v = *reinterpret_cast<const float4*>(&rx_dn[par][j0][0]);
+      const float vy[2] = {v.x, v.z}, vx[2] = {v.y, v.w};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        dn_my[k] = it == 0 ? vy[k] : dn_ky[k];
+        dn_mx[k] = it == 0 ? vx[k] : dn_kx[k];
+        dn_ky[k] = vy[k];
+        dn_kx[k] = vx[k];
+        ex_y[k] = dn_ky[k] + beta * (dn_ky[k] - dn_my[k]);
+        ex_x[k] = dn_kx[k] + beta * (dn_kx[k] - dn_mx[k]);
+      }
     }
-    s_rg_yy[rg][j] = yy[NP - 1].y;  // row CRPT-1
+    s_rg_yy[rg][j0] = yy[0][1].y;  // row CRPT-1
+    s_rg_yy[rg][j0 + 1] = yy[1][1].y;
     if (lane == 31) {
 #pragma unroll
-      for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[P];
-      s_edge_yx[rg][NP][wc + 1].x = ex_x;
+      for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
+      s_edge_yx[rg][NP][wc + 1].x = ex_x[1];
     }
     __syncthreads();
-    // left neighbours: shuffles inside the warp, the warp to the left's last
-    // lane from shared memory (zeros left of column 0)
+    // left neighbours of column 0: shuffles inside the warp, the warp to the
+    // left's last column from shared memory (zeros left of column 0); column
+    // 1's left neighbour is this thread's column 0
     float2 left[NP];
 #pragma unroll
     for (int P = 0; P < NP; ++P) {
-      left[P].x = __shfl_up_sync(0xffffffffu, yx[P].x, 1);
-      left[P].y = __shfl_up_sync(0xffffffffu, yx[P].y, 1);
+      left[P].x = __shfl_up_sync(0xffffffffu, yx[1][P].x, 1);
+      left[P].y = __shfl_up_sync(0xffffffffu, yx[1][P].y, 1);
     }
-    float ledge_x = __shfl_up_sync(0xffffffffu, ex_x, 1);
+    float ledge_x = __shfl_up_sync(0xffffffffu, ex_x[1], 1);
     if (lane == 0) {
 #pragma unroll
       for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
       ledge_x = s_edge_yx[rg][NP][wc].x;
     }
-    const float yy_above = rg_top ? y_up : s_rg_yy[rg - 1][j];
-    float2 u[NP];
+    const float2 ya2 = rg_top ? make_float2(y_up[0], y_up[1])
+                              : *reinterpret_cast<const float2*>(&s_rg_yy[rg - 1][j0]);
+    const float yy_above[2] = {ya2.x, ya2.y};
+    float2 u[2][NP];
 #pragma unroll
-    for (int P = 0; P < NP; ++P) {
-      // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
-      const float2 ab2 = P == 0 ? make_float2(yy_above, yy[NP - 1].x) : yy[P - 1];
-      const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[P]), yx[P]);
-      const float2 d2 = __ffma2_rn(left[P], m1, d1);
-      const float2 v = __fadd2_rn(z[P], d2);
-      u[P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
+        const float2 ab2 = P == 0 ? make_float2(yy_above[k], yy[k][1].x) : yy[k][0];
+        const float2 l2 = k == 0 ? left[P] : yx[0][P];
+        const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[k][P]), yx[k][P]);
+        const float2 d2 = __ffma2_rn(l2, m1, d1);
+        const float2 v = __fadd2_rn(z[k][P], d2);
+        u[k][P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
+      }
+    float u_ex[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float d = ((ex_y[k] - yy[k][1].y) + ex_x[k]) - (k == 0 ? ledge_x : ex_x[0]);
+      const float v = z_ex[k] + d;
+      u_ex[k] = nonneg ? fmaxf(v, 0.f) : v;
     }
-    float u_ex;
-    {
-      const float d = ((ex_y - yy[NP - 1].y) + ex_x) - ledge_x;
-      const float v = z_ex + d;
-      u_ex = nonneg ? fmaxf(v, 0.f) : v;
-    }
-    s_rg_u[rg][j] = u[0].x;
+    s_rg_u[rg][j0] = u[0][0].x;
+    s_rg_u[rg][j0 + 1] = u[1][0].x;
     if (lane == 0) {
 #pragma unroll
-      for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[P];
+      for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[0][P];
     }
     __syncthreads();
-    // right neighbours: shuffles (lane 31 keeps its own u: at the global last
-    // column gx = 0), the warp to the right's first lane from shared memory
+    // right neighbour of column 1: shuffles (lane 31 keeps its own column 1 at
+    // the global last column: gx = 0), the warp to the right's first column
+    // from shared memory; column 0's right neighbour is column 1
     float2 right[NP];
 #pragma unroll
     for (int P = 0; P < NP; ++P) {
-      right[P].x = __shfl_down_sync(0xffffffffu, u[P].x, 1);
-      right[P].y = __shfl_down_sync(0xffffffffu, u[P].y, 1);
+      right[P].x = __shfl_down_sync(0xffffffffu, u[0][P].x, 1);
+      right[P].y = __shfl_down_sync(0xffffffffu, u[0][P].y, 1);
     }
     if (right_fetch) {
 #pragma unroll
       for (int P = 0; P < NP; ++P) right[P] = s_edge_u[rg][P][wc + 1];
     }
+    if (last_col) {
+#pragma unroll
+      for (int P = 0; P < NP; ++P) right[P] = u[1][P];
+    }
     // the global last row has no row below: gy = 0 (below := u)
-    const float u_below = !rg_bot ? s_rg_u[rg + 1][j] : (last_row_thread ? u[NP - 1].y : u_ex);
+    float u_below[2];
+    {
+      const float2 ub = !rg_bot ? *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0])
+                                : (last_row_thread ? make_float2(u[0][1].y, u[1][1].y)
+                                                   : make_float2(u_ex[0], u_ex[1]));
+      u_below[0] = ub.x;
+      u_below[1] = ub.y;
+    }
     const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(w, w);
 #pragma unroll
-    for (int P = 0; P < NP; ++P) {
-      const float2 bl2 = P < NP - 1 ? u[P + 1] : make_float2(u[0].y, u_below);
-      const float2 gy = __ffma2_rn(u[P], m1, bl2);
-      const float2 gx = __ffma2_rn(u[P], m1, right[P]);
-      const float2 ay = __ffma2_rn(st2, gy, yy[P]);
-      const float2 ax = __ffma2_rn(st2, gx, yx[P]);
-      const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
-      float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
-      sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
-      sc.y = fminf(1.f, sc.y);
-      QMy[P] = __fmul2_rn(ay, sc);
-      QMx[P] = __fmul2_rn(ax, sc);
-    }
-    push_rows(QMy[0].x, QMx[0].x, QMy[NP - 1].y);
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        const float2 bl2 = P == 0 ? u[k][1] : make_float2(u[k][0].y, u_below[k]);
+        const float2 rt = k == 0 ? u[1][P] : right[P];
+        const float2 gy = __ffma2_rn(u[k][P], m1, bl2);
+        const float2 gx = __ffma2_rn(u[k][P], m1, rt);
+        const float2 ay = __ffma2_rn(st2, gy, yy[k][P]);
+        const float2 ax = __ffma2_rn(st2, gx, yx[k][P]);
+        const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
+        float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
+        sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
+        sc.y = fminf(1.f, sc.y);
+        QMy[k][P] = __fmul2_rn(ay, sc);
+        QMx[k][P] = __fmul2_rn(ax, sc);
+      }
+    push_rows(QMy[0][0].x, QMx[0][0].x, QMy[1][0].x, QMx[1][0].x, QMy[0][1].y, QMy[1][1].y);
     ++round;
   };
 
@@ -450,54 +507,66 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   if (it < a.n_inner) {
     inner(qky, qkx, qmy, qmx, it);
 #pragma unroll
-    for (int P = 0; P < NP; ++P) {
-      qky[P] = qmy[P];
-      qkx[P] = qmx[P];
-    }
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        qky[k][P] = qmy[k][P];
+        qkx[k][P] = qmx[k][P];
+      }
   }
 
   // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
   const unsigned pe = recv_rows(round0 + a.n_inner);
-  float yy_above = 0.f;
-  if (rg_top && has_up) yy_above = rx_up[pe][j];
-  s_rg_yy[rg][j] = rowref(qky, CRPT - 1);
+  float yy_above[2] = {0.f, 0.f};
+  if (rg_top && has_up) {
+    yy_above[0] = rx_up[pe][j0];
+    yy_above[1] = rx_up[pe][j0 + 1];
+  }
+  s_rg_yy[rg][j0] = rowref(qky[0], CRPT - 1);
+  s_rg_yy[rg][j0 + 1] = rowref(qky[1], CRPT - 1);
   if (lane == 31) {
 #pragma unroll
-    for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = qkx[P];
+    for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = qkx[1][P];
   }
   __syncthreads();
   float2 qleft[NP];
 #pragma unroll
   for (int P = 0; P < NP; ++P) {
-    qleft[P].x = __shfl_up_sync(0xffffffffu, qkx[P].x, 1);
-    qleft[P].y = __shfl_up_sync(0xffffffffu, qkx[P].y, 1);
+    qleft[P].x = __shfl_up_sync(0xffffffffu, qkx[1][P].x, 1);
+    qleft[P].y = __shfl_up_sync(0xffffffffu, qkx[1][P].y, 1);
   }
   if (lane == 0) {
 #pragma unroll
     for (int P = 0; P < NP; ++P) qleft[P] = s_edge_yx[rg][P][wc];
   }
-  if (!rg_top) yy_above = s_rg_yy[rg - 1][j];
+  if (!rg_top) {
+    yy_above[0] = s_rg_yy[rg - 1][j0];
+    yy_above[1] = s_rg_yy[rg - 1][j0 + 1];
+  }
   bool ok = true;
 #pragma unroll
-  for (int t = 0; t < CRPT; ++t) {
-    const float left = rowref(qleft, t);
-    const int r = row0 + t;
-    float d = 0.f;
-    if (r < CH - 1) d += rowref(qky, t);
-    if (r > 0) d -= (t > 0 ? rowref(qky, t - 1) : yy_above);
-    if (j < CW - 1) d += rowref(qkx, t);
-    if (j > 0) d -= left;
-    float uf = rowref(z, t) + d;
-    if (nonneg) uf = fmaxf(uf, 0.f);
-    const int lr = rg * CRPT + t;
-    TO xo = sx[lr * CW + j];
-    const TO bo = sb[lr * CW + j], ho = sh[lr * CW + j];
-    for (int s = 0; s < m; ++s) xo = skip_update(xo, bo, ho, g);
-    const TO xhat = skip_update(xo, bo, ho, g);
-    const TO xn = (TO)uf;
-    sh[lr * CW + j] = A::add(ho, A::mul(a.pg, A::sub(xn, xhat)));
-    sx[lr * CW + j] = xn;
-    ok &= finite(xn);
+  for (int k = 0; k < 2; ++k) {
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      const float left = k == 0 ? rowref(qleft, t) : rowref(qkx[0], t);
+      const int r = row0 + t, j = j0 + k;
+      float d = 0.f;
+      if (r < CH - 1) d += rowref(qky[k], t);
+      if (r > 0) d -= (t > 0 ? rowref(qky[k], t - 1) : yy_above[k]);
+      if (j < CW - 1) d += rowref(qkx[k], t);
+      if (j > 0) d -= left;
+      float uf = rowref(z[k], t) + d;
+      if (nonneg) uf = fmaxf(uf, 0.f);
+      const int sj = (rg * CRPT + t) * CW + j;
+      TO xo = sx[sj];
+      const TO bo = sb[sj], ho = sh[sj];
+      for (int s = 0; s < m; ++s) xo = skip_update(xo, bo, ho, g);
+      const TO xhat = skip_update(xo, bo, ho, g);
+      const TO xn = (TO)uf;
+      sh[sj] = A::add(ho, A::mul(a.pg, A::sub(xn, xhat)));
+      sx[sj] = xn;
+      ok &= finite(xn);
+    }
   }
   if (!ok) kbad = min(kbad, kk);
   kprev = kk;
@@ -506,20 +575,23 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   // ---- trailing skips, write-back -------------------------------------------
   const int m = a.K - 1 - kprev;
 #pragma unroll
-  for (int t = 0; t < CRPT; ++t) {
-    const int lr = rg * CRPT + t;
-    const int64_t o = (int64_t)(row0 + t) * CW + j;
-    TO xo = sx[lr * CW + j];
-    const TO bo = sb[lr * CW + j], ho = sh[lr * CW + j];
-    for (int s = 0; s < m; ++s) {
-      xo = skip_update(xo, bo, ho, g);
-      if (!finite(xo)) kbad = min(kbad, kprev + 1 + s);
-    }
-    xp[o] = xo;
-    if (e1 > e0) {
-      hp[o] = ho;
-      q0[o] = rowref(qky, t);
-      q0[HW + o] = rowref(qkx, t);
+  for (int k = 0; k < 2; ++k) {
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      const int sj = (rg * CRPT + t) * CW + j0 + k;
+      const int64_t o = (int64_t)(row0 + t) * CW + j0 + k;
+      TO xo = sx[sj];
+      const TO bo = sb[sj], ho = sh[sj];
+      for (int s = 0; s < m; ++s) {
+        xo = skip_update(xo, bo, ho, g);
+        if (!finite(xo)) kbad = min(kbad, kprev + 1 + s);
+      }
+      xp[o] = xo;
+      if (e1 > e0) {
+        hp[o] = ho;
+        q0[o] = rowref(qky[k], t);
+        q0[HW + o] = rowref(qkx[k], t);
+      }
     }
   }
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
