@@ -4,11 +4,13 @@
 noise sigma_i ~ U[0.05, 0.15], alpha = 0.1, gamma = 1, p = 0.1 per-problem
 Philox coin streams, FGP-50 inner iterations), sharded over N GPUs (one
 process per GPU, contiguous problem blocks, no collective on the data path).
-A "step" is one outer ProxSkip iteration over the whole batch: a fused
-pre-kernel over all problems, 50 FGP inner-iteration launches over the
-coin-fired (~10%) problems, and a fused post-kernel.  W warm-up steps are
-outer iterations 0..W-1 of the run; the K timed steps are iterations
-W..W+K-1 (default W+K = 300, the full config-4 run).
+A "step" is one outer ProxSkip iteration over the whole batch.  The native
+driver runs the K timed steps as ONE segment: fgp_cluster_run_kernel (16-CTA
+clusters, one problem each at a time, all of its coin-fired prox calls back to
+back with the FGP state in registers) plus fgp_sm_run_kernel on the SMs the
+clusters leave, each problem advanced by exactly K outer iterations.  W
+warm-up steps are outer iterations 0..W-1 of the run; the K timed steps are
+iterations W..W+K-1 (default W+K = 300, the full config-4 run).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -40,10 +42,12 @@ BYTES_FGP_MOM = 28   # fp32 per pixel-iteration: x + q_k(2) + q_{k-1}(2) read, q
 BYTES_FGP_FIRST = 20  # first inner iteration (beta = 0): no q_{k-1} read
 CLUSTER = os.environ.get("PSB_NO_CLUSTER", "0") != "1"
 if CLUSTER:
-    KERNEL = ("fgp_cluster_run_kernel<float>: the whole timed run segment in ONE launch; each "
-              "16-CTA cluster runs its problems' coin-fired prox calls back to back (skips + 50 "
-              "FGP iterations + post) with z, q in registers and x, b, h in shared memory; the "
-              "28 B/px-iter of the streaming formulation stay on-chip, so frac > 1 is expected")
+    KERNEL = ("fgp_cluster_run_kernel<float> (+ fgp_sm_run_kernel on the 36 SMs the clusters "
+              "leave): the whole timed run segment in ONE launch each; a 16-CTA cluster runs its "
+              "problems' coin-fired prox calls back to back (skips + 50 FGP iterations + post) "
+              "with z, q in registers and x, b, h in shared memory; the 28 B/px-iter of the "
+              "streaming formulation stay on-chip / in L2, so frac > 1 is expected; time = both "
+              "kernels (events around the pair)")
     # ncu dram__bytes_read.sum + dram__bytes_write.sum of fgp_cluster_run_kernel per launch,
     # per problem in the launch (profiles/r01_launches_bench_run.csv)
     TRAFFIC_PER_PROBLEM_LAUNCH = 2.4e6
