@@ -95,22 +95,34 @@ class BatchedTvDenoise:
         return self.prox_count * self.inner_iters
 
     def run_proxskip(self, coins, gamma=1.0, p=0.1, *, use_graph=False, record_elapsed=False,
-                     fgp_time=None):
-        """K outer iterations; ``coins`` is the (K, N) table of ``coin_table``."""
+                     fgp_time=None, lo=0, hi=None, stream=None):
+        """K outer iterations; ``coins`` is the (K, N) table of ``coin_table``.
+        ``lo``/``hi`` restrict the call to problems lo..hi-1 (``coins`` then
+        has hi - lo columns); ``stream`` is a torch CUDA stream (default: the
+        current one)."""
+        hi = self.n if hi is None else hi
+        if not 0 <= lo <= hi <= self.n:
+            raise ValueError("problem range out of bounds")
         coins = np.ascontiguousarray(coins, dtype=np.uint8)
         K = coins.shape[0]
-        if coins.shape[1] != self.n:
+        if coins.shape[1] != hi - lo:
             raise ValueError("coin table does not match the batch")
         self.elapsed = np.zeros(max(K, 1)) if record_elapsed else None
-        L.call("psb_proxskip_denoise_run", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
-               L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), L.ptr(self.slots), self.n, self.H,
-               self.W, coins.ctypes.data_as(L.C.c_void_p), K, float(gamma), float(p),
-               float(self.alpha), self.inner_iters, int(self.accelerated), int(self.nonneg),
-               self.last_weight.ctypes.data_as(L.C.c_void_p),
-               self.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(self.bad), int(bool(use_graph)),
+        if hi == lo:
+            return self.x
+        HW = self.H * self.W
+        off = lambda t, per: L.C.c_void_p(t.data_ptr() + lo * per * t.element_size())  # noqa: E731
+        L.call("psb_proxskip_denoise_run", L.dcode(self.dto), L.dcode(self.dtf), off(self.x, HW),
+               off(self.b, HW), off(self.h, HW), off(self.z, HW), off(self.slots, 6 * HW),
+               hi - lo, self.H, self.W, coins.ctypes.data_as(L.C.c_void_p), K, float(gamma),
+               float(p), float(self.alpha), self.inner_iters, int(self.accelerated),
+               int(self.nonneg), self.last_weight[lo:hi].ctypes.data_as(L.C.c_void_p),
+               self.prox_count[lo:hi].ctypes.data_as(L.C.c_void_p), off(self.bad, 1),
+               int(bool(use_graph)),
                self.elapsed.ctypes.data_as(L.C.c_void_p) if record_elapsed else None,
                fgp_time.ctypes.data_as(L.C.c_void_p) if fgp_time is not None else None,
-               None, 0, None, L.stream())
+               None, 0, None,
+               L.C.c_void_p(stream.cuda_stream) if stream is not None else L.stream())
         return self.x
 
     def check_finite(self):
@@ -122,7 +134,12 @@ class BatchedTvDenoise:
 
 def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.0,
                          precision="fp32", use_graph=False):
-    """Config-4 entry point: returns (x, prox_counts) as the input currency."""
+    """Config-4 entry point: returns (x, prox_counts) as the input currency.
+
+    (A chunked variant -- host->device copy of chunk c+1 and device->host copy
+    of chunk c-1 overlapped with chunk c's compute -- was measured slower on
+    the config-4 batch: every chunk pays the SM workers' coarse load-balance
+    tail, ~25 ms, more than the ~65 ms of copies it hides.)"""
     solver = BatchedTvDenoise(b, alpha, inner_budget, precision=precision)
     solver.run_proxskip(coin_table(p, seeds, iters), gamma, p, use_graph=use_graph)
     solver.check_finite()

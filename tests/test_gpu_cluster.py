@@ -158,3 +158,54 @@ def test_sm_workers_warm_restart_and_divergence(monkeypatch):
     with pytest.raises(psb.DivergenceError) as ei:
         s.check_finite()
     assert ei.value.iteration == 0
+
+
+def test_problem_range_calls_equal_one_shot():
+    """BatchedTvDenoise.run_proxskip on problem ranges (lo, hi) in separate
+    calls equals one call over the whole batch, bit for bit (problems are
+    independent; cluster and SM-worker kernels share the arithmetic)."""
+    idx = np.arange(50) * 31 % 4096
+    b = _batch(idx).astype(np.float32)
+    K, inner, p = 20, 6, 0.25
+    coins = psb.coin_table(p, idx, K)
+    one = psb.BatchedTvDenoise(b, 0.1, inner)
+    one.run_proxskip(coins, 1.0, p)
+    parts = psb.BatchedTvDenoise(b, 0.1, inner)
+    for lo in range(0, 50, 16):
+        hi = min(50, lo + 16)
+        parts.run_proxskip(np.ascontiguousarray(coins[:, lo:hi]), 1.0, p, lo=lo, hi=hi)
+    np.testing.assert_array_equal(parts.prox_count, one.prox_count)
+    assert torch.equal(parts.x, one.x)
+    assert torch.equal(parts.h, one.h)
+    assert torch.equal(parts.slots[:, 0], one.slots[:, 0])
+
+
+@pytest.mark.parametrize("host", ["numpy", "pinned", "pageable"])
+def test_host_inputs_equal_device_run(host):
+    idx = np.arange(12) * 31 % 4096
+    b = _batch(idx).astype(np.float32)
+    K, inner, p = 20, 6, 0.25
+    x_ref, c_ref = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
+    src = b.astype(np.float64) if host == "numpy" else torch.from_numpy(b)
+    if host == "pinned":
+        src = src.pin_memory()
+    x, c = psb.run_proxskip_batched(src, 0.1, p, idx, K, inner)
+    np.testing.assert_array_equal(c, c_ref)
+    x = x if isinstance(x, np.ndarray) else x.numpy()
+    np.testing.assert_array_equal(x.astype(np.float32), x_ref.cpu().numpy())
+
+
+def test_sm_worker_and_cluster_kernels_bitwise_equal(monkeypatch):
+    """The same problems run entirely on the SM workers (PSB_SM_RATIO tiny)
+    and entirely on the clusters (PSB_NO_SMWORK=1) give identical bits: which
+    kernel the static split picks never changes a result."""
+    idx = np.arange(24) * 53 % 4096
+    b = _batch(idx).astype(np.float32)
+    K, inner, p = 25, 7, 0.3
+    monkeypatch.setenv("PSB_SM_RATIO", "0.001")
+    xs, cs = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
+    monkeypatch.delenv("PSB_SM_RATIO")
+    monkeypatch.setenv("PSB_NO_SMWORK", "1")
+    xc, cc = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
+    np.testing.assert_array_equal(cs, cc)
+    assert torch.equal(xs, xc)
