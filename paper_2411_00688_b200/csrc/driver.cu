@@ -32,6 +32,7 @@ int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
                 cudaStream_t st);
 bool cluster_shape_ok(int H, int W);
 int cluster_count();
+int sm_prepare();
 int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const int32_t* asg_off,
            const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
            const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
@@ -279,9 +280,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     cudaStream_t st2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     if (NW > 0) {
-      if (cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking) != cudaSuccess ||
+      rc = sm_prepare();
+      if (rc == PSB_OK && (cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess))
         rc = fail(PSB_ERR_CUDA, "sm workers: stream/event creation failed");
       if (rc == PSB_OK) {
         cudaEventRecord(fork, st);

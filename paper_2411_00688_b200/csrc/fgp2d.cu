@@ -798,6 +798,21 @@ int aprojgd_dual_rof(int dtype, const void* b, void* q, int H, int W, double alp
   return fgp2d_finalize(dtype, b, HW, q, 6 * HW, nullptr, 1, H, W, iters, 0, u, HW, st);
 }
 
+// Load the kernel before the run's first launch: with lazy module loading a
+// first launch loads it on the fly, and this kernel's CTAs were then measured
+// to reach the SMs before the (already enqueued) clusters, taking GPC space a
+// 16-CTA cluster needs (first run 2x slower).  Called before the clusters are
+// launched.
+int sm_prepare() {
+  static bool loaded = false;
+  if (!loaded) {
+    cudaFuncAttributes fa;
+    PSB_CUDA(cudaFuncGetAttributes(&fa, fgp_sm_run_kernel));
+    loaded = true;
+  }
+  return PSB_OK;
+}
+
 int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const int32_t* asg_off,
            const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
            const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
