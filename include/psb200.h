@@ -247,6 +247,30 @@ int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void
                              double* elapsed_host, double* fgp_time_host, void* x_hist, int algo,
                              void* aux, void* stream);
 
+/* psb_proxskip_denoise_run_streamed: psb_proxskip_denoise_run (fp32 FGP,
+ *   256x256, no graph, no log) whose kernels start before their inputs have
+ *   arrived.  Problems form chunks of `chunk` (n_chunks * chunk >= n); the
+ *   run kernels wait, per problem, until ready[p / chunk] != 0 (device
+ *   int32[n_chunks + 1], zeroed; the caller's copy stream writes 1 after the
+ *   chunk's H2D copy with psb_stream_write_u32), and add 16 per finished
+ *   problem to done[p / chunk] (device int32[n_chunks], zeroed) so the copy
+ *   stream can psb_stream_wait_geq_u32 for 16 * (problems in the chunk)
+ *   before the chunk's D2H copy.  ready[n_chunks] becomes 1 if a wait timed
+ *   out (20 s).  Same results as psb_proxskip_denoise_run (bit-identical). */
+int psb_proxskip_denoise_run_streamed(int dtype_outer, int dtype_fgp, void* x, const void* b,
+                                      void* h, void* z, void* q, int64_t n, int H, int W,
+                                      const uint8_t* coins_host, int K, double gamma, double p,
+                                      double alpha, int n_inner, int accelerated, int nonneg,
+                                      double* last_weight_host, int64_t* prox_count_host,
+                                      int32_t* bad_iter, const int32_t* ready, int32_t* done,
+                                      int chunk, int n_chunks, void* stream);
+/* Stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32 with
+ * GEQ), used to order copies against the streamed run without a host
+ * round trip; psb_stream_memops_supported reports whether the driver has them. */
+int psb_stream_memops_supported(int* out);
+int psb_stream_write_u32(void* stream, void* dptr, uint32_t value);
+int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value);
+
 /* ---- parallel-beam projector, operators.py:189-292 (matrix-free) ------------
  * Geometry of RadonGeometry (operators.py:189-215) plus the sample lattice of
  * radon_system_matrix (operators.py:224-229): `tables` is a DEVICE double

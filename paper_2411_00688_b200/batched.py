@@ -16,6 +16,8 @@ oracle.  Multi-GPU: problems are sharded across ranks with no collective
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -132,15 +134,83 @@ class BatchedTvDenoise:
             raise DivergenceError(int(bad[hit].min()), f"proxskip[problem {int(hit[0])}]")
 
 
+def _memops():
+    if not hasattr(_memops, "ok"):
+        v = L.C.c_int(0)
+        L.call("psb_stream_memops_supported", L.C.byref(v))
+        _memops.ok = bool(v.value)
+    return _memops.ok
+
+
 def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.0,
-                         precision="fp32", use_graph=False):
+                         precision="fp32", use_graph=False, chunk=512):
     """Config-4 entry point: returns (x, prox_counts) as the input currency.
 
-    (A chunked variant -- host->device copy of chunk c+1 and device->host copy
-    of chunk c-1 overlapped with chunk c's compute -- was measured slower on
-    the config-4 batch: every chunk pays the SM workers' coarse load-balance
-    tail, ~25 ms, more than the ~65 ms of copies it hides.)"""
+    Host input on the cluster path is streamed: the run kernels are launched
+    first and wait per problem for its input chunk (``chunk`` problems),
+    whose host->device copy the copy stream announces with a stream memory
+    write; each chunk's result goes back to the host as soon as its problems
+    are done (stream memory wait on a device counter) while later chunks
+    still compute.  Same arithmetic and results as the resident run."""
+    seeds = np.asarray(seeds).reshape(-1)
+    n = int(seeds.size)
+    shape = tuple(b.shape) if hasattr(b, "shape") else np.shape(b)
+    # (streamed only for float32 host data: a dtype conversion would need a
+    # kernel on the copy stream, which cannot run while the waiting run
+    # kernels hold every SM)
+    f32 = (b.dtype == torch.float32) if isinstance(b, torch.Tensor) else (
+        getattr(b, "dtype", None) == np.float32)
+    if (AR.is_host(b) and f32 and not use_graph and precision == "fp32" and chunk and n > chunk
+            and len(shape) == 3 and shape[1:] == (256, 256) and _memops()
+            and os.environ.get("PSB_NO_CLUSTER", "0") != "1"):
+        return _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk)
     solver = BatchedTvDenoise(b, alpha, inner_budget, precision=precision)
     solver.run_proxskip(coin_table(p, seeds, iters), gamma, p, use_graph=use_graph)
     solver.check_finite()
     return AR.like(solver.x, b), solver.prox_count.copy()
+
+
+def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk):
+    tensor_in = isinstance(b, torch.Tensor)
+    src = b.detach().contiguous() if tensor_in else torch.from_numpy(np.ascontiguousarray(b))
+    n, H, W = src.shape
+    if n != seeds.size:
+        raise ValueError("one seed per problem")
+    solver = BatchedTvDenoise(torch.empty((n, H, W), dtype=torch.float32, device="cuda"), alpha,
+                              inner_budget, precision="fp32")
+    coins = coin_table(p, seeds, iters)
+    bounds = [(lo, min(n, lo + chunk)) for lo in range(0, n, chunk)]
+    nc = len(bounds)
+    flags = torch.zeros(2 * nc + 1, dtype=torch.int32, device="cuda")  # ready[nc + 1], done[nc]
+    ready, done = flags[:nc + 1], flags[nc + 1:]
+    main = torch.cuda.current_stream()
+    start = torch.cuda.Event()
+    start.record(main)  # buffers allocated and zeroed
+    copy = torch.cuda.Stream()
+    copy.wait_event(start)
+    # 1) the run: its kernels wait for the chunks below
+    L.call("psb_proxskip_denoise_run_streamed", L.dcode(solver.dto), L.dcode(solver.dtf),
+           L.ptr(solver.x), L.ptr(solver.b), L.ptr(solver.h), L.ptr(solver.z),
+           L.ptr(solver.slots), n, H, W, coins.ctypes.data_as(L.C.c_void_p), coins.shape[0],
+           float(gamma), float(p), float(alpha), inner_budget, 1, 0,
+           solver.last_weight.ctypes.data_as(L.C.c_void_p),
+           solver.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(solver.bad), L.ptr(ready),
+           L.ptr(done), chunk, nc, L.stream())
+    cs = L.C.c_void_p(copy.cuda_stream)
+    out = torch.empty((n, H, W), dtype=torch.float32)
+    with torch.cuda.stream(copy):
+        # 2) inputs, chunk by chunk, each announced to the waiting kernels
+        for c, (lo, hi) in enumerate(bounds):
+            part = src[lo:hi]  # float32 H2D: a DMA, no kernel on this stream
+            solver.b[lo:hi].copy_(part, non_blocking=part.is_pinned())
+            L.call("psb_stream_write_u32", cs, L.C.c_void_p(ready.data_ptr() + 4 * c), 1)
+        # 3) results, chunk by chunk, as soon as the chunk's problems are done
+        for c, (lo, hi) in enumerate(bounds):
+            L.call("psb_stream_wait_geq_u32", cs, L.C.c_void_p(done.data_ptr() + 4 * c),
+                   16 * (hi - lo))
+            AR.download_into(out[lo:hi], solver.x[lo:hi])
+    main.wait_stream(copy)
+    if int(ready[nc].item()) != 0:
+        raise RuntimeError("streamed run: an input chunk never arrived (device wait timed out)")
+    solver.check_finite()
+    return (out if tensor_in else out.numpy()), solver.prox_count.copy()

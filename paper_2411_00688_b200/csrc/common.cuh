@@ -158,6 +158,48 @@ __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
 
 template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
 
+// ---- host->device chunk streaming (run drivers) ------------------------------
+// The run kernels can start before their inputs have arrived: problem p's
+// chunk c = p / chunk is ready once ready[c] != 0 (written by the copy stream
+// after the chunk's H2D copy, cuStreamWriteValue32), and every finished
+// problem adds 16 to done[c] (a cluster: 1 per CTA; an SM worker: 16), which
+// the copy stream waits for (cuStreamWaitValue32 >= 16 * problems) before the
+// chunk's D2H copy.  ready[n_chunks] is an error flag: a wait that times out
+// (20 s) sets it instead of hanging the device.
+struct ChunkSync {
+  const int32_t* ready = nullptr;  // null: inputs already resident
+  int32_t* done = nullptr;
+  int chunk = 0;
+  int n_chunks = 0;
+};
+
+__device__ __forceinline__ void chunk_wait(const ChunkSync& cs, int p) {
+  if (cs.ready == nullptr) return;
+  const int32_t* f = cs.ready + p / cs.chunk;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) {
+      atomicExch(const_cast<int32_t*>(cs.ready) + cs.n_chunks, 1);
+      return;
+    }
+    __nanosleep(2000);
+  }
+}
+
+// after this thread's writes of problem p: (all threads) fence; one thread adds
+__device__ __forceinline__ void chunk_done(const ChunkSync& cs, int p, int add, bool leader) {
+  if (cs.done == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (leader) atomicAdd(cs.done + p / cs.chunk, add);
+}
+
 // ---- kernel attributes, set once ---------------------------------------------
 // cudaFuncSetAttribute on a function that has launches in flight can make the
 // driver wait for them, which serialises back-to-back launches of a long

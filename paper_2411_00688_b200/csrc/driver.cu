@@ -37,12 +37,12 @@ int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const
            const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
            const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
            double gamma, double hc, double pg, double step, const float* betas, int32_t* bad,
-           cudaStream_t st);
+           const ChunkSync& cs, cudaStream_t st);
 int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
                 const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
                 const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
                 int nonneg, double weight, double gamma, double hc, double pg, double step,
-                const float* betas, int32_t* bad, cudaStream_t st);
+                const float* betas, int32_t* bad, const ChunkSync& cs, cudaStream_t st);
 int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
@@ -89,7 +89,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                     void* q, int64_t n, int H, int W, const uint8_t* coins_host, int K,
                     double gamma, double p, double alpha, int n_inner, int accelerated, int nonneg,
                     double* last_weight, int64_t* prox_count, int32_t* bad, int use_graph,
-                    double* elapsed, double* fgp_time, void* x_hist, cudaStream_t user_stream) {
+                    double* elapsed, double* fgp_time, void* x_hist, cudaStream_t user_stream,
+                    const ChunkSync* chunks = nullptr) {
   PSB_REQUIRE(fid.kind == 0 || n == 1, "proxskip run: a blur fidelity runs one problem at a time");
   PSB_REQUIRE(gamma > 0, "run_proxskip: gamma must be positive");
   PSB_REQUIRE(p > 0 && p <= 1, "SkipConfig: p must be in (0, 1]");
@@ -142,6 +143,11 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                            n_inner <= 1024 && !(no_cluster && no_cluster[0] == '1') &&
                            x_hist == nullptr && !fid.fista;
   PSB_REQUIRE(!fid.fista || (fid.xprev && fid.xbar), "fista: x_prev / xbar buffers missing");
+  const ChunkSync cs = chunks ? *chunks : ChunkSync{};
+  PSB_REQUIRE(cs.ready == nullptr || (use_cluster && !use_graph && cs.chunk > 0 && cs.done &&
+                                      (int64_t)cs.n_chunks * cs.chunk >= n),
+              "streamed run: needs the cluster path (256x256, fp32 FGP, no graph) and a "
+              "chunking that covers the batch");
   // FISTA's outer momentum (solvers.py:156-160): beta_k = (t_k - 1)/t_{k+1}, t_0 = 1
   std::vector<double> fbeta;
   if (fid.fista) {
@@ -202,6 +208,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       load[best] = bt;
       bins[best].push_back(i);
     }
+    if (cs.ready)  // each machine takes its problems in input-chunk order
+      for (auto& bin : bins)
+        std::stable_sort(bin.begin(), bin.end(),
+                         [&](int32_t u, int32_t v) { return u / cs.chunk < v / cs.chunk; });
     asg_off.assign(G + 1, 0);
     asg.reserve(n);
     for (int c = 0; c < G; ++c) {
@@ -293,7 +303,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (rc == PSB_OK)
       rc = cluster_run(dto, x, b, h, q, qps, i32(o_asgo), i32(o_asg), G, i32(o_evo), i32(o_evk),
                        dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
-                       0.125, beta_d, bad, st);
+                       0.125, beta_d, bad, cs, st);
     const char* dbg = std::getenv("PSB_DEBUG_TIMES");
     cudaEvent_t d0 = nullptr, d1 = nullptr, d2 = nullptr;
     if (dbg) {
@@ -307,7 +317,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       if (rc == PSB_OK)
         rc = sm_run(x, b, h, q, qps, z, i32(o_swo), i32(o_sw), NW, i32(o_evo), i32(o_evk),
                     dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
-                    beta_d, bad, st2);
+                    beta_d, bad, cs, st2);
       if (dbg) cudaEventRecord(d2, st2);
       cudaEventRecord(join, st2);
       cudaStreamWaitEvent(st, join, 0);
@@ -410,6 +420,69 @@ extern "C" int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x,
                               gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
                               prox_count_host, bad_iter, use_graph, elapsed_host, fgp_time_host,
                               x_hist, psb::as_stream(stream));
+}
+
+extern "C" int psb_proxskip_denoise_run_streamed(
+    int dtype_outer, int dtype_fgp, void* x, const void* b, void* h, void* z, void* q, int64_t n,
+    int H, int W, const uint8_t* coins_host, int K, double gamma, double p, double alpha,
+    int n_inner, int accelerated, int nonneg, double* last_weight_host, int64_t* prox_count_host,
+    int32_t* bad_iter, const int32_t* ready, int32_t* done, int chunk, int n_chunks,
+    void* stream) {
+  psb::Fidelity fid;
+  psb::ChunkSync cs;
+  cs.ready = ready;
+  cs.done = done;
+  cs.chunk = chunk;
+  cs.n_chunks = n_chunks;
+  return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
+                              gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
+                              prox_count_host, bad_iter, 0, nullptr, nullptr, nullptr,
+                              psb::as_stream(stream), &cs);
+}
+
+// Stream memory operations (driver API, resolved at run time through the
+// runtime's entry-point query so the library does not link libcuda).
+namespace {
+typedef int (*StreamValueFn)(void* stream, unsigned long long addr, uint32_t value,
+                             unsigned int flags);
+StreamValueFn stream_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<StreamValueFn>(fn);
+}
+}  // namespace
+
+extern "C" int psb_stream_memops_supported(int* out) {
+  int dev = 0, v = 0;
+  *out = 0;
+  PSB_CUDA(cudaGetDevice(&dev));
+  // CU_DEVICE_ATTRIBUTE_CAN_USE_STREAM_MEM_OPS_V1 (driver attribute 92) is
+  // not exposed by the runtime enum; probe by resolving the entry points
+  (void)v;
+  *out = stream_fn("cuStreamWriteValue32") != nullptr && stream_fn("cuStreamWaitValue32") != nullptr;
+  return PSB_OK;
+}
+
+extern "C" int psb_stream_write_u32(void* stream, void* dptr, uint32_t value) {
+  static StreamValueFn fn = stream_fn("cuStreamWriteValue32");
+  if (!fn) return psb::fail(PSB_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  // CU_STREAM_WRITE_VALUE_DEFAULT: a memory fence precedes the write, so the
+  // chunk copied before it on this stream is visible when the flag is
+  if (fn(stream, reinterpret_cast<unsigned long long>(dptr), value, 0) != 0)
+    return psb::fail(PSB_ERR_CUDA, "cuStreamWriteValue32 failed");
+  return PSB_OK;
+}
+
+extern "C" int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value) {
+  static StreamValueFn fn = stream_fn("cuStreamWaitValue32");
+  if (!fn) return psb::fail(PSB_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  // CU_STREAM_WAIT_VALUE_GEQ = 0x0: (int32_t)(*addr - value) >= 0
+  if (fn(stream, reinterpret_cast<unsigned long long>(dptr), value, 0x0) != 0)
+    return psb::fail(PSB_ERR_CUDA, "cuStreamWaitValue32 failed");
+  return PSB_OK;
 }
 
 extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void* b,

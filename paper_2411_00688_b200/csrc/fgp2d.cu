@@ -344,6 +344,7 @@ struct SmRunArgs {
   float weight, gamma, hc, pg, step;
   int32_t* bad;
   const float* betas;
+  ChunkSync cs;
 };
 
 constexpr int SM_THREADS = 512;
@@ -531,6 +532,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
     float* zp = a.z + (int64_t)p * HW;
     float* q0 = a.q + (int64_t)p * a.qps;
     const int e0 = a.ev_off[p], e1 = a.ev_off[p + 1];
+    if (a.cs.ready) {  // this problem's input chunk has arrived
+      if (tid == 0) chunk_wait(a.cs, p);
+      __syncthreads();
+    }
     int kbad = 0x7fffffff;
     int kprev = -1;
     for (int e = e0; e < e1; ++e) {
@@ -639,6 +644,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
       }
     }
     if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
+    chunk_done(a.cs, p, 16, tid == 0);
     __syncthreads();
   }
 }
@@ -817,11 +823,11 @@ int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const
            const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
            const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
            double gamma, double hc, double pg, double step, const float* betas, int32_t* bad,
-           cudaStream_t st) {
+           const ChunkSync& cs, cudaStream_t st) {
   if (n_workers <= 0) return PSB_OK;
   SmRunArgs a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, (float*)z, asg_off, asg,
               ev_off, ev_k, rep, K, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
-              (float)hc, (float)pg, (float)step, bad, betas};
+              (float)hc, (float)pg, (float)step, bad, betas, cs};
   fgp_sm_run_kernel<<<n_workers, SM_THREADS, 0, st>>>(a);
   PSB_LAUNCHED("fgp_sm_run");
   return PSB_OK;

@@ -70,6 +70,7 @@ struct RunArgs {
   float step;
   int32_t* bad;            // [n]: first non-finite iteration (atomicMin)
   const float* betas;      // device table beta[0..n_inner-1]
+  ChunkSync cs;            // optional input/output chunk streaming (common.cuh)
 };
 
 template <class TO>
@@ -277,6 +278,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   TO* hp = a.h + (int64_t)p * HW;
   float* q0 = a.q + (int64_t)p * a.qps;
   const int e0 = a.ev_off[p], e1 = a.ev_off[p + 1];
+  if (a.cs.ready) {  // this problem's input chunk has arrived
+    if (tid == 0) chunk_wait(a.cs, p);
+    __syncthreads();
+  }
   // stage this CTA's rows of x, b, h (each thread its own elements; the CTA
   // above reads row 0 after the next cluster barrier)
 #pragma unroll
@@ -595,6 +600,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     }
   }
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
+  chunk_done(a.cs, p, 1, tid == 0);  // this CTA's rows of the problem are written
   // The next problem's staging may overwrite row 0 of this CTA only after the
   // CTA above has read it: it did so in the prologue of this problem's last
   // prox call, before its first push of that call, which this CTA waited for.
@@ -648,18 +654,18 @@ int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
                 const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
                 const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
                 int nonneg, double weight, double gamma, double hc, double pg, double step,
-                const float* betas, int32_t* bad, cudaStream_t st) {
+                const float* betas, int32_t* bad, const ChunkSync& cs, cudaStream_t st) {
   if (G <= 0) return PSB_OK;
   if (dto == PSB_F32) {
     RunArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, asg_off, asg, ev_off,
                      ev_k, rep, K, n_inner, accelerated, (float)weight, (float)gamma, (float)hc,
-                     (float)pg, (float)step, bad, betas};
+                     (float)pg, (float)step, bad, betas, cs};
     return nonneg ? launch_run<float, true>(a, G, dto, st) : launch_run<float, false>(a, G, dto, st);
   }
   if (dto == PSB_F64) {
     RunArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, asg_off, asg,
                       ev_off, ev_k, rep, K, n_inner, accelerated, (float)weight, gamma, hc, pg,
-                      (float)step, bad, betas};
+                      (float)step, bad, betas, cs};
     return nonneg ? launch_run<double, true>(a, G, dto, st) : launch_run<double, false>(a, G, dto, st);
   }
   return fail(PSB_ERR_VALUE, "cluster run: unknown dtype");

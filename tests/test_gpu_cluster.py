@@ -209,3 +209,23 @@ def test_sm_worker_and_cluster_kernels_bitwise_equal(monkeypatch):
     xc, cc = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
     np.testing.assert_array_equal(cs, cc)
     assert torch.equal(xs, xc)
+
+
+@pytest.mark.parametrize("host", ["numpy", "numpy64", "pinned", "pageable"])
+def test_streamed_host_run_equals_resident_run(host):
+    """Host input streams in chunks (kernels wait on per-chunk ready flags,
+    results leave per chunk behind a device counter); results bit-identical
+    to the run on device-resident input."""
+    idx = np.arange(60) * 29 % 4096
+    b = _batch(idx).astype(np.float32)
+    K, inner, p = 24, 6, 0.25
+    x_ref, c_ref = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
+    src = {"numpy": b, "numpy64": b.astype(np.float64)}.get(host)
+    if src is None:
+        src = torch.from_numpy(b)
+    if host == "pinned":
+        src = src.pin_memory()
+    x, c = psb.run_proxskip_batched(src, 0.1, p, idx, K, inner, chunk=16)
+    np.testing.assert_array_equal(c, c_ref)
+    x = x if isinstance(x, np.ndarray) else x.numpy()
+    np.testing.assert_array_equal(x.astype(np.float32), x_ref.cpu().numpy())
