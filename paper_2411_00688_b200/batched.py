@@ -143,7 +143,7 @@ def _memops():
 
 
 def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.0,
-                         precision="fp32", use_graph=False, chunk=512):
+                         precision="fp32", use_graph=False, chunk=256):
     """Config-4 entry point: returns (x, prox_counts) as the input currency.
 
     Host input on the cluster path is streamed: the run kernels are launched
