@@ -8,7 +8,9 @@
 // per outer iteration without any host synchronisation.  With use_graph the
 // whole launch sequence is captured into one CUDA graph first (a 256^2 FGP
 // iteration is only a few microseconds of GPU work, so launch cost matters).
+#include <chrono>
 #include <climits>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 
@@ -42,7 +44,8 @@ int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
                 const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
                 const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
                 int nonneg, double weight, double gamma, double hc, double pg, double step,
-                const float* betas, int32_t* bad, const ChunkSync& cs, cudaStream_t st);
+                const float* betas, int32_t* bad, const ChunkSync& cs, volatile int* started,
+                int seq, cudaStream_t st);
 int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
@@ -300,11 +303,40 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
         cudaStreamWaitEvent(st2, fork, 0);
       }
     }
+    // With SM workers, the clusters must be resident before the workers'
+    // CTAs reach the SMs (a worker CTA placed first can take GPC space a
+    // 16-CTA cluster needs, measured: 6 instead of 7 clusters, -14 %).  Each
+    // cluster reports its start in host-mapped memory; the workers are
+    // launched once all have started (or after 200 ms, e.g. on a busy GPU).
+    static volatile int* started_h = nullptr;
+    static int* started_d = nullptr;
+    static int seq = 0;
+    if (NW > 0 && rc == PSB_OK && started_h == nullptr) {
+      void* hp = nullptr;
+      if (cudaHostAlloc(&hp, 64 * sizeof(int), cudaHostAllocMapped) == cudaSuccess &&
+          cudaHostGetDevicePointer(reinterpret_cast<void**>(&started_d), hp, 0) == cudaSuccess) {
+        started_h = static_cast<volatile int*>(hp);
+        for (int i = 0; i < 64; ++i) started_h[i] = 0;
+      }
+    }
+    const bool gate = NW > 0 && started_h != nullptr && G <= 64;
+    if (gate) ++seq;
     if (rc == PSB_OK)
       rc = cluster_run(dto, x, b, h, q, qps, i32(o_asgo), i32(o_asg), G, i32(o_evo), i32(o_evk),
                        dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
-                       0.125, beta_d, bad, cs, st);
-    const char* dbg = std::getenv("PSB_DEBUG_TIMES");
+                       0.125, beta_d, bad, cs, gate ? started_d : nullptr, seq, st);
+    if (gate && rc == PSB_OK) {
+      const auto t_end = std::chrono::steady_clock::now() + std::chrono::milliseconds(200);
+      for (;;) {
+        int ok = 0;
+        for (int c = 0; c < G; ++c) ok += started_h[c] == seq;
+        if (ok == G || std::chrono::steady_clock::now() > t_end) break;
+        std::this_thread::yield();
+      }
+    }
+    // (never in a streamed run: the synchronisation below would wait for
+    // kernels that wait for copies the caller has not enqueued yet)
+    const char* dbg = cs.ready ? nullptr : std::getenv("PSB_DEBUG_TIMES");
     cudaEvent_t d0 = nullptr, d1 = nullptr, d2 = nullptr;
     if (dbg) {
       cudaEventCreate(&d0);

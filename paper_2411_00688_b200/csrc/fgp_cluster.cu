@@ -71,6 +71,8 @@ struct RunArgs {
   int32_t* bad;            // [n]: first non-finite iteration (atomicMin)
   const float* betas;      // device table beta[0..n_inner-1]
   ChunkSync cs;            // optional input/output chunk streaming (common.cuh)
+  volatile int* started;   // optional, host-mapped: started[c] = seq once cluster c runs
+  int seq;
 };
 
 template <class TO>
@@ -227,6 +229,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     mbar_init(&mb_up[0], 1);
     mbar_init(&mb_up[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (a.started && cr == 0 && tid == 0) {  // tell the host this cluster is resident
+    a.started[blockIdx.x / CCL] = a.seq;
+    __threadfence_system();
   }
   cluster_arrive();  // every CTA's mbarriers exist before anyone pushes
   cluster_wait();
@@ -654,18 +660,19 @@ int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
                 const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
                 const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
                 int nonneg, double weight, double gamma, double hc, double pg, double step,
-                const float* betas, int32_t* bad, const ChunkSync& cs, cudaStream_t st) {
+                const float* betas, int32_t* bad, const ChunkSync& cs, volatile int* started,
+                int seq, cudaStream_t st) {
   if (G <= 0) return PSB_OK;
   if (dto == PSB_F32) {
     RunArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, asg_off, asg, ev_off,
                      ev_k, rep, K, n_inner, accelerated, (float)weight, (float)gamma, (float)hc,
-                     (float)pg, (float)step, bad, betas, cs};
+                     (float)pg, (float)step, bad, betas, cs, started, seq};
     return nonneg ? launch_run<float, true>(a, G, dto, st) : launch_run<float, false>(a, G, dto, st);
   }
   if (dto == PSB_F64) {
     RunArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, asg_off, asg,
                       ev_off, ev_k, rep, K, n_inner, accelerated, (float)weight, gamma, hc, pg,
-                      (float)step, bad, betas, cs};
+                      (float)step, bad, betas, cs, started, seq};
     return nonneg ? launch_run<double, true>(a, G, dto, st) : launch_run<double, false>(a, G, dto, st);
   }
   return fail(PSB_ERR_VALUE, "cluster run: unknown dtype");
