@@ -57,8 +57,15 @@ __global__ void blur_direct_kernel(const T* __restrict__ u, T* __restrict__ out,
   }
 }
 
-// Fused g = A^T (A u - b) (or r = A u - b only when `fwd_only`), separable.
-template <class T, int TS>
+__device__ __forceinline__ int wrap1(int i, int n) {  // periodic index, cheap near [0, n)
+  while (i < 0) i += n;
+  while (i >= n) i -= n;
+  return i;
+}
+
+// Fused g = A^T (A u - b), separable, kernel size K at compile time (tile
+// sides and the index arithmetic below are constants).
+template <class T, int TS, int K>
 __global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict__ u,
                                                             const T* __restrict__ bdat,
                                                             T* __restrict__ g, int H, int W,
@@ -66,35 +73,39 @@ __global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict_
   extern __shared__ unsigned char smem_raw[];
   pdl_enter();
   T* sm = reinterpret_cast<T*>(smem_raw);
-  const int R = t.k / 2;
-  const int NU = TS + 4 * R;  // u tile side (2R halo each side)
-  const int NR = TS + 2 * R;  // r tile side
-  T* su = sm;                 // NU x NU
-  T* sh = su + NU * NU;       // NU rows x NR cols  (row pass of A)
-  T* sr = sh + NU * NR;       // NR x NR            (r = A u - b)
-  T* sh2 = sr + NR * NR;      // NR rows x TS cols  (row pass of A^T)
-#define w1(q) ((T)t.w1[q])  // kernel-parameter (constant bank) reads
+  constexpr int R = K / 2;
+  constexpr int NU = TS + 4 * R;  // u tile side (2R halo each side)
+  constexpr int NR = TS + 2 * R;  // r tile side
+  T* su = sm;                     // NU x NU
+  T* sh = su + NU * NU;           // NU rows x NR cols  (row pass of A)
+  T* sr = sh + NU * NR;           // NR x NR            (r = A u - b)
+  T* sh2 = sr + NR * NR;          // NR rows x TS cols  (row pass of A^T)
+  T w1[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) w1[q] = (T)t.w1[q];
 
   const int i0 = blockIdx.y * TS, j0 = blockIdx.x * TS;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < NU * NU; e += nt) {
     const int a = e / NU, b = e % NU;
-    su[e] = u[(int64_t)wrap(i0 - 2 * R + a, H) * W + wrap(j0 - 2 * R + b, W)];
+    su[e] = u[(int64_t)wrap1(i0 - 2 * R + a, H) * W + wrap1(j0 - 2 * R + b, W)];
   }
   __syncthreads();
   // forward A: out(i,j) = sum_a sum_b w1[a] w1[b] u(i-a+c, j-b+c)
   for (int e = tid; e < NU * NR; e += nt) {
     const int a = e / NR, jc = e % NR;  // jc: r-tile column; u column jc + R + (c - b)
     T acc = T(0);
-    for (int q = 0; q < t.k; ++q) acc += w1(q) * su[a * NU + jc + R + (R - q)];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc += w1[q] * su[a * NU + jc + R + (R - q)];
     sh[e] = acc;
   }
   __syncthreads();
   for (int e = tid; e < NR * NR; e += nt) {
     const int ic = e / NR, jc = e % NR;
     T acc = T(0);
-    for (int q = 0; q < t.k; ++q) acc += w1(q) * sh[(ic + R + (R - q)) * NR + jc];
-    const int gi = wrap(i0 - R + ic, H), gj = wrap(j0 - R + jc, W);
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc += w1[q] * sh[(ic + R + (R - q)) * NR + jc];
+    const int gi = wrap1(i0 - R + ic, H), gj = wrap1(j0 - R + jc, W);
     sr[e] = acc - bdat[(int64_t)gi * W + gj];
   }
   __syncthreads();
@@ -102,7 +113,8 @@ __global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict_
   for (int e = tid; e < NR * TS; e += nt) {
     const int ic = e / TS, jt = e % TS;
     T acc = T(0);
-    for (int q = 0; q < t.k; ++q) acc += w1(q) * sr[ic * NR + jt + q];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc += w1[q] * sr[ic * NR + jt + q];
     sh2[e] = acc;
   }
   __syncthreads();
@@ -111,10 +123,10 @@ __global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict_
     const int gi = i0 + it, gj = j0 + jt;
     if (gi >= H || gj >= W) continue;
     T acc = T(0);
-    for (int q = 0; q < t.k; ++q) acc += w1(q) * sh2[(it + q) * TS + jt];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc += w1[q] * sh2[(it + q) * TS + jt];
     g[(int64_t)gi * W + gj] = acc;
   }
-#undef w1
 }
 
 template <class T, int TS>
@@ -131,16 +143,32 @@ int make_taps(const double* taps2d, const double* taps1d, int k, Taps& t) {
   return PSB_OK;
 }
 
-template <class T>
-int launch_sep(const void* u, const void* b, void* g, int H, int W, const Taps& t, cudaStream_t st) {
+template <class T, int K>
+int launch_sep_k(const void* u, const void* b, void* g, int H, int W, const Taps& t,
+                 cudaStream_t st) {
   constexpr int TS = 32;
-  const size_t sm = sep_smem<T, TS>(t.k);
-  PSB_CHECK(func_attr(blur_grad_sep_kernel<T, TS>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const size_t sm = sep_smem<T, TS>(K);
+  PSB_CHECK(func_attr(blur_grad_sep_kernel<T, TS, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                      (int)sm));
   dim3 grid((W + TS - 1) / TS, (H + TS - 1) / TS);
-  PSB_CUDA(launch_chain(blur_grad_sep_kernel<T, TS>, grid, dim3(256), sm, st, (const T*)u,
+  PSB_CUDA(launch_chain(blur_grad_sep_kernel<T, TS, K>, grid, dim3(256), sm, st, (const T*)u,
                         (const T*)b, (T*)g, H, W, t));
   return PSB_OK;
+}
+
+template <class T>
+int launch_sep(const void* u, const void* b, void* g, int H, int W, const Taps& t, cudaStream_t st) {
+  switch (t.k) {
+    case 1: return launch_sep_k<T, 1>(u, b, g, H, W, t, st);
+    case 3: return launch_sep_k<T, 3>(u, b, g, H, W, t, st);
+    case 5: return launch_sep_k<T, 5>(u, b, g, H, W, t, st);
+    case 7: return launch_sep_k<T, 7>(u, b, g, H, W, t, st);
+    case 9: return launch_sep_k<T, 9>(u, b, g, H, W, t, st);
+    case 11: return launch_sep_k<T, 11>(u, b, g, H, W, t, st);
+    case 13: return launch_sep_k<T, 13>(u, b, g, H, W, t, st);
+    case 15: return launch_sep_k<T, 15>(u, b, g, H, W, t, st);
+    default: return fail(PSB_ERR_VALUE, "blur: kernel size must be odd and <= 15");
+  }
 }
 
 }  // namespace
