@@ -271,6 +271,19 @@ int psb_stream_memops_supported(int* out);
 int psb_stream_write_u32(void* stream, void* dptr, uint32_t value);
 int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value);
 
+/* Peer memory for the config-5 z-slab exchange (the reference has
+ * no multi-GPU path -- this replaces the halo transfer of the decomposed
+ * tv.py:53-89 loop).  A rank exports its halo receive rings and flags with
+ * psb_ipc_get_handle (psb_ipc_handle_size() bytes), its neighbours map them
+ * with psb_ipc_open_handle and deposit planes there: the edge kernel's
+ * send_lo / send_hi stores (psb_fgp3d_iter_part) or psb_copy_async, each
+ * followed by psb_stream_write_u32 on the receiver's flag. */
+int psb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int psb_ipc_handle_size(void);
+int psb_ipc_get_handle(const void* dptr, void* handle_out);
+int psb_ipc_open_handle(const void* handle, void** dptr_out);
+int psb_ipc_close(void* dptr);
+
 /* ---- parallel-beam projector, operators.py:189-292 (matrix-free) ------------
  * Geometry of RadonGeometry (operators.py:189-215) plus the sample lattice of
  * radon_system_matrix (operators.py:224-229): `tables` is a DEVICE double
@@ -346,6 +359,20 @@ int psb_fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z
                    double beta_prev, double step, double weight, int reproject, int nonneg,
                    const void* halo_below_qk, const void* halo_below_qm, const void* halo_above_qk,
                    const void* halo_above_qm, const void* halo_above_x, int zchunk, void* stream);
+/* psb_fgp3d_iter_part: psb_fgp3d_iter restricted to a plane subset, for the
+ * overlapped slab schedule: part 1 = interior planes [1, D-1),
+ * which read no halo plane and so run while the halo exchange is in flight;
+ * part 2 = the edge planes 0 and D-1, launched once the halos have arrived.
+ * send_lo / send_hi (optional, (3, H, W)) receive a copy of the new q_{it+1}
+ * of plane 0 / D-1 from the same store -- a local send buffer or, for the
+ * peer-memory exchange, the neighbour's receive ring mapped over NVLink.
+ * part 0 = all planes (psb_fgp3d_iter). */
+int psb_fgp3d_iter_part(int dtype, const void* x, void* q, int D, int H, int W, int z0, int Dg,
+                        int it, double beta_prev, double step, double weight, int reproject,
+                        int nonneg, const void* halo_below_qk, const void* halo_below_qm,
+                        const void* halo_above_qk, const void* halo_above_qm,
+                        const void* halo_above_x, int zchunk, int part, void* send_lo,
+                        void* send_hi, void* stream);
 int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,
                         const void* z, void* q, const void* halo_below_qn, int D, int H, int W,
                         int z0, int Dg, int n_inner, int nonneg, double gamma, double pg,

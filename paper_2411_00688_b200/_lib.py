@@ -88,8 +88,15 @@ SIGNATURES = {
     "psb_stream_write_u32": [_vp, _vp, C.c_uint32],
     "psb_stream_wait_geq_u32": [_vp, _vp, C.c_uint32],
     "psb_cluster_max_active": [_vp],
+    "psb_copy_async": [_vp, _vp, _i64, _vp],
+    "psb_ipc_handle_size": [],
+    "psb_ipc_get_handle": [_vp, _vp],
+    "psb_ipc_open_handle": [_vp, _vp],
+    "psb_ipc_close": [_vp],
     "psb_fgp3d_iter": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32,
                        _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
+    "psb_fgp3d_iter_part": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl,
+                            _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp],
     "psb_proxskip_post3d": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
                             _i32, _i32, _i32, _dbl, _dbl, _i32, _vp, _i32, _vp],
     "psb_skip_chain": [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _dbl, _dbl, _vp, _i32, _vp],

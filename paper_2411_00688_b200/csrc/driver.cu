@@ -517,6 +517,38 @@ extern "C" int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value)
   return PSB_OK;
 }
 
+// Peer memory for the config-5 slab exchange: a rank exports
+// its receive rings / flags with a CUDA IPC handle, its z-neighbours map them
+// and deposit halo planes there directly (kernel stores or copies over
+// NVLink), ordered by stream memory operations on the flags.
+extern "C" int psb_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  PSB_REQUIRE(bytes >= 0, "psb_copy_async: negative size");
+  if (bytes == 0) return PSB_OK;
+  PSB_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, psb::as_stream(stream)));
+  return PSB_OK;
+}
+
+extern "C" int psb_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+extern "C" int psb_ipc_get_handle(const void* dptr, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  PSB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return PSB_OK;
+}
+
+extern "C" int psb_ipc_open_handle(const void* handle, void** dptr_out) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  PSB_CUDA(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return PSB_OK;
+}
+
+extern "C" int psb_ipc_close(void* dptr) {
+  PSB_CUDA(cudaIpcCloseMemHandle(dptr));
+  return PSB_OK;
+}
+
 extern "C" int psb_proxskip_deblur_run(int dtype_outer, int dtype_fgp, void* x, const void* b,
                                        void* h, void* z, void* q, void* g, void* scratch, int H,
                                        int W, const double* taps2d, const double* taps1d,

@@ -40,6 +40,14 @@ struct Fgp3Args {
   const T* ha_qm;
   const T* ha_x;
   int zchunk;  // planes per CTA along z
+  // plane subset (overlapped slab schedule): 0 = all planes [0, D),
+  // 1 = interior [1, D-1) (needs no halo), 2 = the two edge planes 0, D-1
+  int part;
+  // optional copies of the new q_{it+1} of plane 0 / plane D-1 (3, H, W),
+  // written next to the slot store: the neighbours' receive rings (peer
+  // memory over NVLink) or a local send buffer
+  T* send_lo;
+  T* send_hi;
 };
 
 template <class T>
@@ -394,8 +402,18 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * BW;
   const int i = blockIdx.y * MTY - 1 + w;
-  const int ks = blockIdx.z * a.zchunk;
-  const int ke = min(a.D, ks + a.zchunk);
+  int ks, ke;
+  if (a.part == 0) {
+    ks = blockIdx.z * a.zchunk;
+    ke = min(a.D, ks + a.zchunk);
+  } else if (a.part == 1) {
+    ks = 1 + blockIdx.z * a.zchunk;
+    ke = min(a.D - 1, ks + a.zchunk);
+  } else {
+    ks = blockIdx.z == 0 ? 0 : a.D - 1;
+    ke = ks + 1;
+    if (blockIdx.z == 1 && a.D == 1) return;
+  }
   if (ks >= ke) return;
   const int H = a.H, W = a.W;
   const bool row_ok = i >= 0 && i < H;
@@ -581,6 +599,19 @@ __global__ void __launch_bounds__((MTY + 2) * 32, 2) fgp3d_march_kernel(Fgp3Args
         stv<T, V>(qo + o, oz);
         stv<T, V>(qo + N3 + o, oy);
         stv<T, V>(qo + 2 * N3 + o, ox);
+        T* sd = k == 0 ? a.send_lo : (k == a.D - 1 ? a.send_hi : nullptr);
+        if (sd) {
+          const int64_t op = (int64_t)i * W + cl;
+          stv<T, V>(sd + op, oz);
+          stv<T, V>(sd + HW + op, oy);
+          stv<T, V>(sd + 2 * HW + op, ox);
+        }
+        if (k == 0 && a.D == 1 && a.send_hi) {
+          const int64_t op = (int64_t)i * W + cl;
+          stv<T, V>(a.send_hi + op, oz);
+          stv<T, V>(a.send_hi + HW + op, oy);
+          stv<T, V>(a.send_hi + 2 * HW + op, ox);
+        }
       }
     } else {
       // keep the shuffle participation uniform across the warp
@@ -661,9 +692,13 @@ template <class T>
 int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
   constexpr int VMAX = 16 / sizeof(T);
   const int zc = a.zchunk;
-  const int nz = (a.D + zc - 1) / zc;
+  const int nz = a.part == 2 ? 2 : a.part == 1 ? std::max(1, (a.D - 2 + zc - 1) / zc)
+                                              : (a.D + zc - 1) / zc;
+  if (a.part == 1 && a.D <= 2) return PSB_OK;  // no interior planes
   const bool vec = (a.W % VMAX == 0) && (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
-                   (reinterpret_cast<uintptr_t>(a.q) % 16 == 0);
+                   (reinterpret_cast<uintptr_t>(a.q) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.send_lo) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(a.send_hi) % 16 == 0);
   Fgp3Maps maps;
   if constexpr (sizeof(T) == 4) {
     if (vec && make_maps(a, maps)) {
@@ -696,32 +731,40 @@ int launch3(const Fgp3Args<T>& a, cudaStream_t st) {
 
 }  // namespace
 
-int fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z0, int Dg, int it,
-               double beta, double step, double weight, int rep, int nonneg, const void* hb_qk,
-               const void* hb_qm, const void* ha_qk, const void* ha_qm, const void* ha_x,
-               int zchunk, cudaStream_t st) {
+int fgp3d_iter_part(int dtype, const void* x, void* q, int D, int H, int W, int z0, int Dg,
+                    int it, double beta, double step, double weight, int rep, int nonneg,
+                    const void* hb_qk, const void* hb_qm, const void* ha_qk, const void* ha_qm,
+                    const void* ha_x, int zchunk, int part, void* send_lo, void* send_hi,
+                    cudaStream_t st) {
   PSB_REQUIRE(D >= 1 && H >= 2 && W >= 2 && Dg >= 2, "fgp3d: need a 3-D grid with sides >= 2");
   PSB_REQUIRE(z0 >= 0 && z0 + D <= Dg, "fgp3d: slab outside the volume");
   PSB_REQUIRE(weight > 0, "tv_prox: weight must be positive");
-  PSB_REQUIRE(z0 == 0 || (hb_qk && hb_qm), "fgp3d: slab above plane 0 needs the halo below");
-  PSB_REQUIRE(z0 + D == Dg || (ha_qk && ha_qm && ha_x), "fgp3d: slab below the top needs the halo above");
+  PSB_REQUIRE(part >= 0 && part <= 2, "fgp3d: part must be 0 (all), 1 (interior) or 2 (edges)");
+  // the interior planes [1, D-1) never read a halo plane
+  PSB_REQUIRE(part == 1 || z0 == 0 || (hb_qk && hb_qm),
+              "fgp3d: slab above plane 0 needs the halo below");
+  PSB_REQUIRE(part == 1 || z0 + D == Dg || (ha_qk && ha_qm && ha_x),
+              "fgp3d: slab below the top needs the halo above");
   if (zchunk <= 0) {
     // enough CTAs for ~4 waves; long chunks amortise the two halo planes
+    const int Dp = part == 1 ? std::max(1, D - 2) : D;
     const int64_t tiles = (int64_t)((W + 127) / 128) * ((H + MTY - 1) / MTY);
     const int64_t want = 32LL * sm_count();  // ~16 waves at 2 CTAs/SM: small tail
-    int nz = (int)std::max<int64_t>(1, std::min<int64_t>(D, (want + tiles - 1) / tiles));
-    zchunk = std::max(16, (D + nz - 1) / nz);
+    int nz = (int)std::max<int64_t>(1, std::min<int64_t>(Dp, (want + tiles - 1) / tiles));
+    zchunk = std::max(16, (Dp + nz - 1) / nz);
   }
   if (dtype == PSB_F32) {
     Fgp3Args<float> a{(const float*)x, (float*)q, D, H, W, z0, Dg, it, (float)beta, (float)step,
                       (float)weight, rep, nonneg, (const float*)hb_qk, (const float*)hb_qm,
-                      (const float*)ha_qk, (const float*)ha_qm, (const float*)ha_x, zchunk};
+                      (const float*)ha_qk, (const float*)ha_qm, (const float*)ha_x, zchunk,
+                      part, (float*)send_lo, (float*)send_hi};
     return launch3(a, st);
   }
   if (dtype == PSB_F64) {
     Fgp3Args<double> a{(const double*)x, (double*)q, D, H, W, z0, Dg, it, beta, step, weight, rep,
                        nonneg, (const double*)hb_qk, (const double*)hb_qm, (const double*)ha_qk,
-                       (const double*)ha_qm, (const double*)ha_x, zchunk};
+                       (const double*)ha_qm, (const double*)ha_x, zchunk, part,
+                       (double*)send_lo, (double*)send_hi};
     return launch3(a, st);
   }
   return fail(PSB_ERR_VALUE, "fgp3d: unknown dtype");
@@ -761,9 +804,22 @@ int psb_fgp3d_iter(int dtype, const void* x, void* q, int D, int H, int W, int z
                    double beta_prev, double step, double weight, int reproject, int nonneg,
                    const void* halo_below_qk, const void* halo_below_qm, const void* halo_above_qk,
                    const void* halo_above_qm, const void* halo_above_x, int zchunk, void* stream) {
-  return psb::fgp3d_iter(dtype, x, q, D, H, W, z0, Dg, it, beta_prev, step, weight, reproject,
-                         nonneg, halo_below_qk, halo_below_qm, halo_above_qk, halo_above_qm,
-                         halo_above_x, zchunk, psb::as_stream(stream));
+  return psb::fgp3d_iter_part(dtype, x, q, D, H, W, z0, Dg, it, beta_prev, step, weight,
+                              reproject, nonneg, halo_below_qk, halo_below_qm, halo_above_qk,
+                              halo_above_qm, halo_above_x, zchunk, 0, nullptr, nullptr,
+                              psb::as_stream(stream));
+}
+
+int psb_fgp3d_iter_part(int dtype, const void* x, void* q, int D, int H, int W, int z0, int Dg,
+                        int it, double beta_prev, double step, double weight, int reproject,
+                        int nonneg, const void* halo_below_qk, const void* halo_below_qm,
+                        const void* halo_above_qk, const void* halo_above_qm,
+                        const void* halo_above_x, int zchunk, int part, void* send_lo,
+                        void* send_hi, void* stream) {
+  return psb::fgp3d_iter_part(dtype, x, q, D, H, W, z0, Dg, it, beta_prev, step, weight,
+                              reproject, nonneg, halo_below_qk, halo_below_qm, halo_above_qk,
+                              halo_above_qm, halo_above_x, zchunk, part, send_lo, send_hi,
+                              psb::as_stream(stream));
 }
 
 int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, void* h,

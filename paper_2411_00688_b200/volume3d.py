@@ -24,6 +24,7 @@ check.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import numpy as np
@@ -46,7 +47,15 @@ def slab_bounds(Dg, rank, world):
 
 
 class Slab3D:
-    """One z-slab of a config-5 problem on the current CUDA device."""
+    """One z-slab of a config-5 problem on the current CUDA device.
+
+    Halo planes live in receive rings: ``rb[s]`` holds plane z0-1 of the dual
+    iterate q_s (slot s % 3, channels z, y, x), ``ra[s]`` plane z0+D; the
+    kernel of inner iteration ``it`` reads ring slots it % 3 (q_k) and
+    (it + 2) % 3 (q_{k-1}), exactly as it reads the slab's own slots, so one
+    3-channel plane per neighbour and inner iteration is exchanged (the new
+    q_{it+1}), not the (q_k, q_{k-1}) pair.  ``hx`` is plane z0+D of the prox
+    input, exchanged once per prox call."""
 
     def __init__(self, b, z0, Dg, alpha, inner_budget=20, *, precision="fp32", accelerated=True,
                  nonneg=False, step=STEP_3D):
@@ -67,79 +76,95 @@ class Slab3D:
         plane = (self.H, self.W)
         self.has_below = z0 > 0
         self.has_above = z0 + self.D < Dg
-        self.hb = torch.zeros((6,) + plane, dtype=dtf, device="cuda") if self.has_below else None
-        self.ha = torch.zeros((6,) + plane, dtype=dtf, device="cuda") if self.has_above else None
+        ring = (3, 3) + plane
+        self.rb = torch.zeros(ring, dtype=dtf, device="cuda") if self.has_below else None
+        self.ra = torch.zeros(ring, dtype=dtf, device="cuda") if self.has_above else None
         self.hx = torch.zeros(plane, dtype=dtf, device="cuda") if self.has_above else None
-        self.hqn = torch.zeros((3,) + plane, dtype=dtf, device="cuda") if self.has_below else None
+        # local send buffers of the new edge planes (used by exchanges that copy)
+        self.sb = torch.zeros((3,) + plane, dtype=dtf, device="cuda") if self.has_below else None
+        self.sa = torch.zeros((3,) + plane, dtype=dtf, device="cuda") if self.has_above else None
+        # direct deposit (peer exchange): (base address of the neighbour's ring,
+        # bytes per ring slot) -- the edge kernel stores the new plane there
+        self.out_lo = None
+        self.out_hi = None
+        self.stream = None  # torch.cuda.Stream of this slab's work (None: current)
         self.bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device="cuda")
         self.last_weight = None
         self.prox_count = 0
         self._coin = {v: torch.tensor([v], dtype=torch.uint8, device="cuda") for v in (0, 1)}
 
-    # -- data exchanged with the neighbours ------------------------------------
-    def _slot(self, s):
-        return self.q[s % 3]
+    @property
+    def plane_bytes(self):
+        return self.H * self.W * self.z.element_size()
 
-    def edge_planes(self, it):
-        """(bottom, top): this slab's first / last plane of (q_it, q_it-1), each (6, H, W)."""
-        qk, qm = self._slot(it), self._slot(it + 2)
-        bot = torch.cat([qk[:, 0], qm[:, 0]]) if self.has_below else None
-        top = torch.cat([qk[:, -1], qm[:, -1]]) if self.has_above else None
-        return bot, top
+    @property
+    def neighbours(self):
+        return self.has_below or self.has_above
 
-    def set_halos(self, below, above):
-        if self.has_below:
-            self.hb.copy_(below)
-        if self.has_above:
-            self.ha.copy_(above)
+    def _st(self):
+        return C.c_void_p(self.stream.cuda_stream) if self.stream is not None else L.stream()
 
-    def prox_input_bottom(self):
-        return self.z[0] if self.has_below else None
-
-    def set_prox_input_above(self, plane):
-        if self.has_above:
-            self.hx.copy_(plane)
-
-    def final_dual_top(self):
-        return self._slot(self.inner)[:, -1] if self.has_above else None
-
-    def set_final_dual_below(self, plane):
-        if self.has_below:
-            self.hqn.copy_(plane)
+    def _send(self, s, hi):
+        out = self.out_hi if hi else self.out_lo
+        if out is not None:
+            return C.c_void_p(out[0] + (s % 3) * out[1])
+        return L.ptr(self.sa if hi else self.sb)
 
     # -- compute phases (one ProxSkip outer iteration) ----------------------------
     def pre(self, k, theta, gamma, p):
         L.call("psb_proxskip_pre", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
                L.ptr(self.b), 1, L.ptr(self.h), L.ptr(self.z), 1, self.x.numel(),
                L.ptr(self._coin[int(theta)]), float(gamma), gamma - gamma / p, L.ptr(self.bad), k,
-               L.stream())
+               self._st())
+
+    def fgp_part(self, it, part, weight, rep, beta_prev):
+        """Inner iteration ``it`` on a plane subset: 0 = all planes, 1 = the
+        interior (no halo read: runs while the exchange is in flight), 2 = the
+        two edge planes (after the halos of q_it arrived; their new q_{it+1}
+        planes also go to the send buffers / the neighbours' rings)."""
+        sk, sm = it % 3, (it + 2) % 3
+        rb, ra = self.rb, self.ra
+        lo = self._send(it + 1, False) if (part != 1 and self.has_below) else None
+        hi = self._send(it + 1, True) if (part != 1 and self.has_above) else None
+        L.call("psb_fgp3d_iter_part", L.dcode(self.dtf), L.ptr(self.z), L.ptr(self.q), self.D,
+               self.H, self.W, self.z0, self.Dg, it, beta_prev, self.step, weight, int(rep),
+               int(self.nonneg), L.ptr(rb[sk]) if rb is not None else None,
+               L.ptr(rb[sm]) if rb is not None else None,
+               L.ptr(ra[sk]) if ra is not None else None,
+               L.ptr(ra[sm]) if ra is not None else None, L.ptr(self.hx), 0, int(part), lo, hi,
+               self._st())
 
     def fgp_iter(self, it, weight, rep, beta_prev):
-        hb, ha = self.hb, self.ha
-        plane = self.H * self.W
-        L.call("psb_fgp3d_iter", L.dcode(self.dtf), L.ptr(self.z), L.ptr(self.q), self.D, self.H,
-               self.W, self.z0, self.Dg, it, beta_prev, self.step, weight, int(rep),
-               int(self.nonneg), L.ptr(hb[0:3]) if hb is not None else None,
-               L.ptr(hb[3:6]) if hb is not None else None,
-               L.ptr(ha[0:3]) if ha is not None else None,
-               L.ptr(ha[3:6]) if ha is not None else None, L.ptr(self.hx), 0, L.stream())
+        self.fgp_part(it, 0, weight, rep, beta_prev)
+
+    def rotate_rings(self, n):
+        """Start of a prox call: q_0 is the previous call's q_n (the post kernel
+        moved it to slot 0), whose halo planes are already in ring slot n % 3."""
+        s = n % 3
+        if s == 0:
+            return
+        with torch.cuda.stream(self.stream) if self.stream is not None else _nullctx():
+            for r in (self.rb, self.ra):
+                if r is not None:
+                    r[0].copy_(r[s])
 
     def chain_pre(self, pend, kfirst, gamma, p):
         """Prox input after `pend` deferred skips, x left stale in memory."""
         L.call("psb_skip_chain", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
                L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), self.x.numel(), int(pend),
-               float(gamma), gamma - gamma / p, L.ptr(self.bad), int(kfirst), L.stream())
+               float(gamma), gamma - gamma / p, L.ptr(self.bad), int(kfirst), self._st())
 
     def flush(self, pend, kfirst, gamma):
         L.call("psb_skip_chain", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
                L.ptr(self.b), L.ptr(self.h), None, self.x.numel(), int(pend), float(gamma), 0.0,
-               L.ptr(self.bad), int(kfirst), L.stream())
+               L.ptr(self.bad), int(kfirst), self._st())
 
     def post(self, k, gamma, p, pend=0):
+        hqn = self.rb[self.inner % 3] if self.rb is not None else None
         L.call("psb_proxskip_post3d", L.dcode(self.dto), L.dcode(self.dtf), L.ptr(self.x),
-               L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), L.ptr(self.q), L.ptr(self.hqn),
+               L.ptr(self.b), L.ptr(self.h), L.ptr(self.z), L.ptr(self.q), L.ptr(hqn),
                self.D, self.H, self.W, self.z0, self.Dg, self.inner, int(self.nonneg),
-               float(gamma), p / gamma, int(pend), L.ptr(self.bad), k, L.stream())
+               float(gamma), p / gamma, int(pend), L.ptr(self.bad), k, self._st())
 
     def check_finite(self):
         kb = int(self.bad.item())
@@ -147,23 +172,149 @@ class Slab3D:
             raise DivergenceError(kb, "proxskip3d")
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 class LocalExchange:
-    """Halo exchange between slabs that live in this process (device copies)."""
+    """Slabs of this process on one stream (the 1-GPU emulation of the
+    decomposition).  ``direct`` (default): each edge kernel stores its new
+    planes straight into the neighbours' rings (the peer-memory data path,
+    with plain device pointers); otherwise the planes go through the local
+    send buffers and a device copy (the NCCL data path)."""
 
-    def halos(self, slabs, it):
-        edges = [s.edge_planes(it) for s in slabs]
+    def __init__(self, direct=True):
+        self.direct = direct
+
+    def setup(self, slabs):
         for i, s in enumerate(slabs):
-            below = edges[i - 1][1] if i > 0 else None
-            above = edges[i + 1][0] if i + 1 < len(slabs) else None
-            s.set_halos(below, above)
+            slot = 3 * s.plane_bytes
+            if self.direct:
+                s.out_lo = (slabs[i - 1].ra.data_ptr(), slot) if s.has_below else None
+                s.out_hi = (slabs[i + 1].rb.data_ptr(), slot) if s.has_above else None
 
-    def prox_input(self, slabs):
+    def begin_prox(self, slabs):
         for i, s in enumerate(slabs[:-1]):
-            s.set_prox_input_above(slabs[i + 1].prox_input_bottom())
+            s.hx.copy_(slabs[i + 1].z[0])
 
-    def final_dual(self, slabs):
-        for i, s in enumerate(slabs[1:], start=1):
-            s.set_final_dual_below(slabs[i - 1].final_dual_top())
+    def wait_ring(self, slabs, m):
+        pass
+
+    def send(self, slabs, m):
+        if self.direct:
+            return
+        for i, s in enumerate(slabs):
+            if s.has_below:
+                slabs[i - 1].ra[m % 3].copy_(s.sb)
+            if s.has_above:
+                slabs[i + 1].rb[m % 3].copy_(s.sa)
+
+    def finish(self, slabs):
+        pass
+
+    def agree_bad(self, k):
+        return k
+
+
+class PeerExchange:
+    """Peer-memory halo exchange with stream-ordered flags (no NCCL, no host
+    synchronisation): every slab runs on its own stream; a slab's edge kernel
+    stores its new q_{it+1} planes directly into the neighbours' receive rings
+    (NVLink peer memory across GPUs), then the stream writes the receiver's
+    flag (cuStreamWriteValue32, fenced); a receiver's stream waits on its flag
+    (cuStreamWaitValue32 >= seq) before the kernel that reads the ring.
+
+    Per prox call and direction the flag advances by n + 1: "ready" (the
+    sender has rotated its rings, computed its prox input and deposited its
+    bottom plane into the lower neighbour's ``hx``) and one per edge kernel.
+    The waits also cover the reuse hazards: a ring slot is rewritten only
+    after the receiver's kernel that last read it (its edge kernel of the
+    previous inner iteration, or its post kernel) has finished.
+
+    ``peers`` maps slab index -> {"below": (ring_ptr, flag_ptr),
+    "above": (ring_ptr, flag_ptr), "hx_below": ptr} -- addresses of the
+    neighbours' buffers in this process (IPC-mapped for other ranks, plain
+    pointers for slabs of this process: ``PeerExchange.local(slabs)``)."""
+
+    def __init__(self, flags, peers):
+        self.flags = flags  # per slab: int32 tensor [from_below, from_above] in its own memory
+        self.peers = peers
+        self.seq = 0
+
+    @classmethod
+    def local(cls, slabs):
+        """In-process wiring (one GPU, one stream per slab): the protocol of
+        the multi-GPU run with local addresses."""
+        flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in slabs]
+        peers = []
+        for i, s in enumerate(slabs):
+            d = {}
+            if s.has_below:
+                nb = slabs[i - 1]
+                d["below"] = (nb.ra.data_ptr(), flags[i - 1].data_ptr() + 4)
+                d["hx_below"] = nb.hx.data_ptr()
+            if s.has_above:
+                na = slabs[i + 1]
+                d["above"] = (na.rb.data_ptr(), flags[i + 1].data_ptr())
+            peers.append(d)
+        for s in slabs:
+            if s.stream is None:
+                s.stream = torch.cuda.Stream()
+        return cls(flags, peers)
+
+    def setup(self, slabs):
+        cur = torch.cuda.current_stream()
+        for i, s in enumerate(slabs):
+            slot = 3 * s.plane_bytes
+            p = self.peers[i]
+            s.out_lo = (p["below"][0], slot) if s.has_below else None
+            s.out_hi = (p["above"][0], slot) if s.has_above else None
+            if s.stream is not None:
+                s.stream.wait_stream(cur)
+
+    def _signal(self, s, i, value):
+        p = self.peers[i]
+        if s.has_below:
+            L.call("psb_stream_write_u32", s._st(), C.c_void_p(p["below"][1]), value)
+        if s.has_above:
+            L.call("psb_stream_write_u32", s._st(), C.c_void_p(p["above"][1]), value)
+
+    def _wait(self, s, i, value):
+        f = self.flags[i].data_ptr()
+        if s.has_below:
+            L.call("psb_stream_wait_geq_u32", s._st(), C.c_void_p(f), value)
+        if s.has_above:
+            L.call("psb_stream_wait_geq_u32", s._st(), C.c_void_p(f + 4), value)
+
+    def begin_prox(self, slabs):
+        self.seq += 1
+        for i, s in enumerate(slabs):
+            if s.has_below:  # bottom plane of the prox input -> hx of the slab below
+                L.call("psb_copy_async", C.c_void_p(self.peers[i]["hx_below"]), L.ptr(s.z[0]),
+                       s.plane_bytes, s._st())
+            self._signal(s, i, self.seq)
+        for i, s in enumerate(slabs):
+            self._wait(s, i, self.seq)
+
+    def wait_ring(self, slabs, m):
+        # ring slot m % 3 holds q_m once the neighbour's edge kernel of
+        # iteration m-1 has run (m >= 1); slot 0 (m = 0) is local (rotate_rings)
+        if m == 0:
+            return
+        for i, s in enumerate(slabs):
+            self._wait(s, i, self.seq + m)
+
+    def send(self, slabs, m):
+        for i, s in enumerate(slabs):
+            self._signal(s, i, self.seq + m)
+
+    def finish(self, slabs):
+        """End of a prox call (after the post kernels)."""
+        self.seq += slabs[0].inner
 
     def agree_bad(self, k):
         return k
@@ -171,7 +322,11 @@ class LocalExchange:
 
 class DistExchange:
     """Halo exchange between ranks (one slab per rank, rank order = z order)
-    with torch.distributed point-to-point (NCCL over NVLink; gloo in tests)."""
+    with torch.distributed point-to-point (NCCL over NVLink; gloo in tests).
+
+    On CUDA tensors the transfers run on a side stream: the edge planes of
+    q_{it+1} leave while the interior kernel of iteration it+1 runs, and the
+    compute stream waits for the transfer only before the next edge kernel."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -179,36 +334,55 @@ class DistExchange:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.comm = None
 
-    def _swap(self, send_down, send_up, recv_below, recv_above):
+    def setup(self, slabs):
+        (s,) = slabs
+        if s.sb is not None and s.sb.is_cuda or s.sa is not None and s.sa.is_cuda:
+            self.comm = torch.cuda.Stream()
+
+    def _p2p(self, sends, recvs):
         d = self.dist
-        ops = []
-        if self.rank > 0:
-            ops.append(d.P2POp(d.isend, send_down.contiguous(), self.rank - 1, self.group))
-            ops.append(d.P2POp(d.irecv, recv_below, self.rank - 1, self.group))
-        if self.rank + 1 < self.world:
-            ops.append(d.P2POp(d.isend, send_up.contiguous(), self.rank + 1, self.group))
-            ops.append(d.P2POp(d.irecv, recv_above, self.rank + 1, self.group))
-        if ops:
+        ops = [d.P2POp(d.isend, t.contiguous(), peer, self.group) for t, peer in sends]
+        ops += [d.P2POp(d.irecv, t, peer, self.group) for t, peer in recvs]
+        if not ops:
+            return
+        if self.comm is None:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
+            return
+        self.comm.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.comm):
+            for req in d.batch_isend_irecv(ops):
+                req.wait()  # orders the comm stream after NCCL, host does not block
 
-    def halos(self, slabs, it):
+    def begin_prox(self, slabs):
         (s,) = slabs
-        bot, top = s.edge_planes(it)
-        self._swap(bot, top, s.hb, s.ha)
+        sends = [(s.z[0], self.rank - 1)] if s.has_below else []
+        recvs = [(s.hx, self.rank + 1)] if s.has_above else []
+        self._p2p(sends, recvs)
+        self._join()
 
-    def prox_input(self, slabs):
+    def _join(self):
+        if self.comm is not None:
+            torch.cuda.current_stream().wait_stream(self.comm)
+
+    def wait_ring(self, slabs, m):
+        self._join()
+
+    def send(self, slabs, m):
         (s,) = slabs
-        d = self.dist
-        ops = []
+        sends, recvs = [], []
         if s.has_below:
-            ops.append(d.P2POp(d.isend, s.prox_input_bottom().contiguous(), self.rank - 1, self.group))
+            sends.append((s.sb, self.rank - 1))
+            recvs.append((s.rb[m % 3], self.rank - 1))
         if s.has_above:
-            ops.append(d.P2POp(d.irecv, s.hx, self.rank + 1, self.group))
-        if ops:
-            for req in d.batch_isend_irecv(ops):
-                req.wait()
+            sends.append((s.sa, self.rank + 1))
+            recvs.append((s.ra[m % 3], self.rank + 1))
+        self._p2p(sends, recvs)
+
+    def finish(self, slabs):
+        pass
 
     def agree_bad(self, k):
         """Global first non-finite iteration: every rank raises the same
@@ -219,22 +393,17 @@ class DistExchange:
         d.all_reduce(t, op=d.ReduceOp.MIN, group=self.group)
         return int(t.item())
 
-    def final_dual(self, slabs):
-        (s,) = slabs
-        d = self.dist
-        ops = []
-        if s.has_above:
-            ops.append(d.P2POp(d.isend, s.final_dual_top().contiguous(), self.rank + 1, self.group))
-        if s.has_below:
-            ops.append(d.P2POp(d.irecv, s.hqn, self.rank - 1, self.group))
-        if ops:
-            for req in d.batch_isend_irecv(ops):
-                req.wait()
-
 
 def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_events=None,
                        defer_skips=True):
     """K outer ProxSkip iterations over a set of slabs (one global coin stream).
+
+    Every FGP inner iteration of a decomposed volume is two launches per slab:
+    the interior planes (no halo: overlaps the exchange of the previous
+    iteration's edge planes) and then the two edge planes, whose new dual
+    planes go to the neighbours (``exchange``: LocalExchange in one process,
+    PeerExchange over peer memory, DistExchange over torch.distributed).  A
+    slab without neighbours runs one whole-slab launch per inner iteration.
 
     With ``defer_skips`` (default) a skipped iteration launches nothing: the
     run of skips since the last prox call is executed in registers by the next
@@ -243,9 +412,11 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
     bit-identical to one pass per skip (``defer_skips=False``), without the
     16 B/voxel HBM round trip per skipped iteration.
     ``fgp_events`` (optional list) collects (start, end) CUDA events around
-    each FGP inner-iteration launch for roofline accounting."""
+    each FGP inner iteration (current stream) for roofline accounting."""
     exchange = exchange or LocalExchange()
+    exchange.setup(slabs)
     s0 = slabs[0]
+    split = any(s.neighbours for s in slabs)
     alpha = s0.alpha
     weight = (gamma / p) * alpha  # prox_g(z, gamma/p) -> tv_prox(z, step * alpha)
     betas = _betas(s0.inner)
@@ -264,28 +435,42 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
             if not theta:
                 continue
         rep = s0.last_weight is not None and s0.last_weight != weight
-        exchange.prox_input(slabs)
+        exchange.begin_prox(slabs)
         for it in range(s0.inner):
-            exchange.halos(slabs, it)
             bprev = betas[it - 1] if (s0.acc and it > 0) else 0.0
             ev = None
             if fgp_events is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            for s in slabs:
-                s.fgp_iter(it, weight, rep, bprev)
+            if split:
+                for s in slabs:
+                    s.fgp_part(it, 1, weight, rep, bprev)
+                exchange.wait_ring(slabs, it)
+                for s in slabs:
+                    s.fgp_part(it, 2, weight, rep, bprev)
+                exchange.send(slabs, it + 1)
+            else:
+                for s in slabs:
+                    s.fgp_part(it, 0, weight, rep, bprev)
             if ev is not None:
                 ev[1].record()
                 fgp_events.append(ev)
-        exchange.final_dual(slabs)
+        if split:
+            exchange.wait_ring(slabs, s0.inner)
         for s in slabs:
             s.post(k, gamma, p, pend)
+            s.rotate_rings(s.inner)
             s.last_weight = weight
             s.prox_count += 1
+        exchange.finish(slabs)
         pend = 0
     if pend:
         for s in slabs:
             s.flush(pend, len(coins) - pend, gamma)
+    cur = torch.cuda.current_stream()
+    for s in slabs:
+        if s.stream is not None:
+            cur.wait_stream(s.stream)
     kb = exchange.agree_bad(min(int(s.bad.item()) for s in slabs))
     if kb != INT32_MAX:
         raise DivergenceError(kb, "proxskip3d")
@@ -293,17 +478,26 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
 
 
 def proxskip_denoise3d(b, alpha, p, seed, iters, inner_budget=20, *, n_slabs=1, precision="fp32",
-                       step=STEP_3D, defer_skips=True):
+                       step=STEP_3D, defer_skips=True, exchange="direct"):
     """Single-process config-5 entry point (``n_slabs`` > 1 emulates the slab
-    decomposition on one GPU).  Returns x in the input's currency."""
+    decomposition on one GPU).  ``exchange``: "direct" (edge kernels store
+    into the neighbours' rings, one stream), "copy" (send buffers + copies:
+    the NCCL data path), "peer" (one stream per slab, flags in device memory:
+    the multi-GPU peer-memory protocol).  Returns x in the input's currency."""
     t = AR.to_dev(b, PRECISIONS[precision][0])
     Dg = t.shape[0]
     slabs = []
     for r in range(n_slabs):
         z0, z1 = slab_bounds(Dg, r, n_slabs)
         slabs.append(Slab3D(t[z0:z1], z0, Dg, alpha, inner_budget, precision=precision, step=step))
+    if exchange == "peer":
+        ex = PeerExchange.local(slabs)
+    elif exchange in ("direct", "copy"):
+        ex = LocalExchange(direct=exchange == "direct")
+    else:
+        raise ValueError(f"proxskip_denoise3d: unknown exchange {exchange!r}")
     xs = run_proxskip_slabs(slabs, SkipConfig(p, seed).coins(iters), gamma=1.0, p=p,
-                            defer_skips=defer_skips)
+                            defer_skips=defer_skips, exchange=ex)
     return AR.like(torch.cat(xs, dim=0), b), slabs
 
 

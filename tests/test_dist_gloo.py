@@ -37,72 +37,59 @@ def _oracle_iter(x, qk, qm, beta, w, step=o3.STEP_3D):
 
 
 class OracleSlab:
-    """CPU stand-in for Slab3D with the same exchange interface; compute by
-    embedding the slab + halos into a zero volume and running the oracle."""
+    """CPU stand-in for Slab3D with the same exchange interface (receive rings
+    rb / ra of the neighbours' edge planes of q_s in slot s % 3, prox-input
+    plane hx, send buffers sb / sa); compute by embedding the slab + halos into
+    a zero volume and running the oracle, storing only the planes of the
+    requested part (1 = interior, 2 = edges + send buffers), like
+    psb_fgp3d_iter_part."""
 
     def __init__(self, x_full, z0, z1, n_inner):
         self.Dg, self.H, self.W = x_full.shape
-        self.z0, self.z1 = z0, z1
-        self.x = torch.from_numpy(x_full[z0:z1].copy())
+        self.z0, self.z1, self.D = z0, z1, z1 - z0
+        self.z = torch.from_numpy(x_full[z0:z1].copy())
         self.q = torch.zeros((3, 3, z1 - z0, self.H, self.W), dtype=torch.float64)
         self.has_below, self.has_above = z0 > 0, z1 < self.Dg
         plane = (self.H, self.W)
-        self.hb = torch.zeros((6,) + plane, dtype=torch.float64) if self.has_below else None
-        self.ha = torch.zeros((6,) + plane, dtype=torch.float64) if self.has_above else None
+        ring = (3, 3) + plane
+        self.rb = torch.zeros(ring, dtype=torch.float64) if self.has_below else None
+        self.ra = torch.zeros(ring, dtype=torch.float64) if self.has_above else None
         self.hx = torch.zeros(plane, dtype=torch.float64) if self.has_above else None
-        self.hqn = torch.zeros((3,) + plane, dtype=torch.float64) if self.has_below else None
+        self.sb = torch.zeros((3,) + plane, dtype=torch.float64) if self.has_below else None
+        self.sa = torch.zeros((3,) + plane, dtype=torch.float64) if self.has_above else None
         self.inner = n_inner
 
-    def edge_planes(self, it):
-        qk, qm = self.q[it % 3], self.q[(it + 2) % 3]
-        bot = torch.cat([qk[:, 0], qm[:, 0]]) if self.has_below else None
-        top = torch.cat([qk[:, -1], qm[:, -1]]) if self.has_above else None
-        return bot, top
-
-    def set_halos(self, below, above):
-        if self.has_below:
-            self.hb.copy_(below)
-        if self.has_above:
-            self.ha.copy_(above)
-
-    def prox_input_bottom(self):
-        return self.x[0] if self.has_below else None
-
-    def set_prox_input_above(self, plane):
-        if self.has_above:
-            self.hx.copy_(plane)
-
-    def final_dual_top(self):
-        return self.q[self.inner % 3][:, -1] if self.has_above else None
-
-    def set_final_dual_below(self, plane):
-        if self.has_below:
-            self.hqn.copy_(plane)
-
-    def step(self, it, beta, w):
+    def fgp_part(self, it, part, beta, w):
         X = np.zeros((self.Dg, self.H, self.W))
         QK = np.zeros((3, self.Dg, self.H, self.W))
         QM = np.zeros_like(QK)
-        X[self.z0:self.z1] = self.x.numpy()
+        X[self.z0:self.z1] = self.z.numpy()
         QK[:, self.z0:self.z1] = self.q[it % 3].numpy()
         QM[:, self.z0:self.z1] = self.q[(it + 2) % 3].numpy()
-        if self.has_below:
-            QK[:, self.z0 - 1] = self.hb[0:3].numpy()
-            QM[:, self.z0 - 1] = self.hb[3:6].numpy()
-        if self.has_above:
-            QK[:, self.z1] = self.ha[0:3].numpy()
-            QM[:, self.z1] = self.ha[3:6].numpy()
+        if part == 2 and self.has_below:
+            QK[:, self.z0 - 1] = self.rb[it % 3].numpy()
+            QM[:, self.z0 - 1] = self.rb[(it + 2) % 3].numpy()
+        if part == 2 and self.has_above:
+            QK[:, self.z1] = self.ra[it % 3].numpy()
+            QM[:, self.z1] = self.ra[(it + 2) % 3].numpy()
             X[self.z1] = self.hx.numpy()
-        out = _oracle_iter(X, QK, QM, beta, w)
-        self.q[(it + 1) % 3] = torch.from_numpy(out[:, self.z0:self.z1].copy())
+        out = torch.from_numpy(_oracle_iter(X, QK, QM, beta, w)[:, self.z0:self.z1].copy())
+        planes = range(1, self.D - 1) if part == 1 else sorted({0, self.D - 1})
+        for k in planes:
+            self.q[(it + 1) % 3][:, k] = out[:, k]
+        if part == 2:
+            if self.has_below:
+                self.sb.copy_(out[:, 0])
+            if self.has_above:
+                self.sa.copy_(out[:, -1])
 
     def finalize(self):
-        """u = x + div q_n on the slab (the z-term below needs the halo)."""
+        """u = x + div q_n on the slab (the z-term below needs ring slot n % 3)."""
         Q = np.zeros((3, self.Dg, self.H, self.W))
         Q[:, self.z0:self.z1] = self.q[self.inner % 3].numpy()
         if self.has_below:
-            Q[:, self.z0 - 1] = self.hqn.numpy()
-        return self.x.numpy() + o3.fd_div3(Q)[self.z0:self.z1]
+            Q[:, self.z0 - 1] = self.rb[self.inner % 3].numpy()
+        return self.z.numpy() + o3.fd_div3(Q)[self.z0:self.z1]
 
 
 def _worker(rank, world, port, shape, n_inner, w, out_q):
@@ -114,12 +101,17 @@ def _worker(rank, world, port, shape, n_inner, w, out_q):
         z0, z1 = slab_bounds(shape[0], rank, world)
         slab = OracleSlab(x_full, z0, z1, n_inner)
         ex = DistExchange()
+        ex.setup([slab])
         betas = fista_betas(n_inner)
-        ex.prox_input([slab])
+        # the schedule of run_proxskip_slabs: interior, ring wait, edges, send
+        ex.begin_prox([slab])
         for it in range(n_inner):
-            ex.halos([slab], it)
-            slab.step(it, betas[it - 1] if it > 0 else 0.0, w)
-        ex.final_dual([slab])
+            beta = betas[it - 1] if it > 0 else 0.0
+            slab.fgp_part(it, 1, beta, w)
+            ex.wait_ring([slab], it)
+            slab.fgp_part(it, 2, beta, w)
+            ex.send([slab], it + 1)
+        ex.wait_ring([slab], n_inner)
         u = slab.finalize()
         gathered = [None] * world
         dist.all_gather_object(gathered, (z0, z1, u, slab.q[n_inner % 3].numpy()))
@@ -129,7 +121,7 @@ def _worker(rank, world, port, shape, n_inner, w, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 5])
 def test_slab_exchange_matches_whole_volume(world):
     shape, n_inner, w = (11, 6, 9), 6, 0.3
     ctx = mp.get_context("spawn")

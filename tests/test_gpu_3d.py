@@ -53,13 +53,35 @@ def test_tv_prox3d_fp32_tolerance():
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("n_slabs", [2, 3, 5])
-def test_slab_decomposition_is_exact(precision, n_slabs):
+@pytest.mark.parametrize("exchange", ["direct", "copy", "peer"])
+def test_slab_decomposition_is_exact(precision, n_slabs, exchange):
+    """Overlapped slab schedule (interior launch, then the edge planes once the
+    halo ring slot arrived) == the whole volume, bit for bit, for the three
+    data paths: edge kernels storing into the neighbours' rings, send buffers +
+    copies (NCCL's), and one stream per slab ordered only by device flags
+    (the peer-memory protocol of the multi-GPU run)."""
     vol = phantoms.random_ellipsoids((23, 20, 36), 6, np.random.default_rng(1))
     b = phantoms.add_noise(vol, 0.1, 1)
     x1, s1 = v3.proxskip_denoise3d(b, 0.08, 0.3, 4, 20, 5, n_slabs=1, precision=precision)
-    xn, sn = v3.proxskip_denoise3d(b, 0.08, 0.3, 4, 20, 5, n_slabs=n_slabs, precision=precision)
+    xn, sn = v3.proxskip_denoise3d(b, 0.08, 0.3, 4, 20, 5, n_slabs=n_slabs, precision=precision,
+                                   exchange=exchange)
     np.testing.assert_array_equal(x1, xn)
     assert s1[0].prox_count == sn[-1].prox_count
+    for s in sn:  # the warm start left in slot 0 matches the whole volume's
+        np.testing.assert_array_equal(s.q[0].cpu().numpy(),
+                                      s1[0].q[0][:, s.z0:s.z0 + s.D].cpu().numpy())
+
+
+@pytest.mark.parametrize("exchange", ["direct", "peer"])
+def test_thin_slabs_exact(exchange):
+    """Slabs of one and two planes (no interior; both edges on one plane)."""
+    vol = phantoms.random_ellipsoids((9, 16, 40), 4, np.random.default_rng(2))
+    b = phantoms.add_noise(vol, 0.1, 2)
+    x1, _ = v3.proxskip_denoise3d(b, 0.08, 0.4, 6, 12, 4, n_slabs=1, precision="fp64")
+    xn, sn = v3.proxskip_denoise3d(b, 0.08, 0.4, 6, 12, 4, n_slabs=7, precision="fp64",
+                                   exchange=exchange)
+    assert sorted({s.D for s in sn}) == [1, 2]
+    np.testing.assert_array_equal(x1, xn)
 
 
 def test_config5_reduced_size_vs_oracle():
