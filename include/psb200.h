@@ -280,7 +280,7 @@ int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value);
  * followed by psb_stream_write_u32 on the receiver's flag. */
 int psb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 int psb_ipc_handle_size(void);
-int psb_ipc_get_handle(const void* dptr, void* handle_out);
+int psb_ipc_get_handle(const void* dptr, void* handle_out, int64_t* offset);
 int psb_ipc_open_handle(const void* handle, void** dptr_out);
 int psb_ipc_close(void* dptr);
 

@@ -90,7 +90,7 @@ SIGNATURES = {
     "psb_cluster_max_active": [_vp],
     "psb_copy_async": [_vp, _vp, _i64, _vp],
     "psb_ipc_handle_size": [],
-    "psb_ipc_get_handle": [_vp, _vp],
+    "psb_ipc_get_handle": [_vp, _vp, _vp],
     "psb_ipc_open_handle": [_vp, _vp],
     "psb_ipc_close": [_vp],
     "psb_fgp3d_iter": [_i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32,

@@ -530,10 +530,29 @@ extern "C" int psb_copy_async(void* dst, const void* src, int64_t bytes, void* s
 
 extern "C" int psb_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 
-extern "C" int psb_ipc_get_handle(const void* dptr, void* handle_out) {
+// dptr may point inside a larger allocation (torch's caching allocator hands
+// out sub-blocks of its segments): the handle names the allocation, *offset
+// is dptr's distance from its base, added back by the importer.
+extern "C" int psb_ipc_get_handle(const void* dptr, void* handle_out, int64_t* offset) {
+  typedef int (*RangeFn)(unsigned long long* base, size_t* size, unsigned long long dptr);
+  static RangeFn range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<RangeFn>(fn);
+  }();
+  if (!range) return psb::fail(PSB_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<unsigned long long>(dptr)) != 0)
+    return psb::fail(PSB_ERR_CUDA, "cuMemGetAddressRange failed");
   cudaIpcMemHandle_t h;
-  PSB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  PSB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
   std::memcpy(handle_out, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<unsigned long long>(dptr) - base);
   return PSB_OK;
 }
 

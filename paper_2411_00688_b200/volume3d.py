@@ -244,6 +244,7 @@ class PeerExchange:
         self.flags = flags  # per slab: int32 tensor [from_below, from_above] in its own memory
         self.peers = peers
         self.seq = 0
+        self.group = False  # torch.distributed group of a multi-rank run (dist())
 
     @classmethod
     def local(cls, slabs):
@@ -265,6 +266,61 @@ class PeerExchange:
             if s.stream is None:
                 s.stream = torch.cuda.Stream()
         return cls(flags, peers)
+
+    @classmethod
+    def dist(cls, slab, group=None):
+        """Multi-GPU wiring, one slab per rank (rank order = z order): every
+        rank exports its rings, prox-input halo plane and flags as CUDA IPC
+        handles, gathers its neighbours' handles over torch.distributed and
+        maps them (peer access over NVLink).  Collective: every rank of the
+        group calls it.  Call ``close()`` when the run is over."""
+        import torch.distributed as tdist
+        rank, world = tdist.get_rank(group), tdist.get_world_size(group)
+        flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()  # zeroed flags before any neighbour can write them
+        hsize = L.LIB.psb_ipc_handle_size()
+
+        def export(t):
+            if t is None:
+                return None
+            h = C.create_string_buffer(hsize)
+            off = C.c_int64(0)
+            L.call("psb_ipc_get_handle", L.ptr(t), h, C.byref(off))
+            return (h.raw, off.value)
+
+        mine = {"ra": export(slab.ra), "rb": export(slab.rb), "hx": export(slab.hx),
+                "flags": export(flags), "z0": slab.z0, "D": slab.D}
+        allh = [None] * world
+        tdist.all_gather_object(allh, mine, group=group)
+        opened = {}
+
+        def imp(r, key):
+            h, off = allh[r][key]
+            if (r, key) not in opened:
+                p = C.c_void_p()
+                L.call("psb_ipc_open_handle", C.create_string_buffer(h, hsize), C.byref(p))
+                opened[(r, key)] = p.value
+            return opened[(r, key)] + off
+
+        d = {}
+        if slab.has_below:
+            if allh[rank - 1]["z0"] + allh[rank - 1]["D"] != slab.z0:
+                raise ValueError("PeerExchange.dist: ranks must own consecutive slabs in z order")
+            d["below"] = (imp(rank - 1, "ra"), imp(rank - 1, "flags") + 4)
+            d["hx_below"] = imp(rank - 1, "hx")
+        if slab.has_above:
+            d["above"] = (imp(rank + 1, "rb"), imp(rank + 1, "flags"))
+        ex = cls([flags], [d])
+        ex.group, ex._opened = group, opened
+        tdist.barrier(group=group)
+        return ex
+
+    def close(self):
+        """Unmap the neighbours' buffers (after a device synchronisation)."""
+        torch.cuda.synchronize()
+        for p in getattr(self, "_opened", {}).values():
+            L.call("psb_ipc_close", C.c_void_p(p))
+        self._opened = {}
 
     def setup(self, slabs):
         cur = torch.cuda.current_stream()
@@ -317,7 +373,12 @@ class PeerExchange:
         self.seq += slabs[0].inner
 
     def agree_bad(self, k):
-        return k
+        if getattr(self, "group", False) is False:
+            return k
+        import torch.distributed as tdist
+        t = torch.tensor([int(k)], dtype=torch.int64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
 
 
 class DistExchange:

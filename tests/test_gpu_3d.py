@@ -124,3 +124,29 @@ def test_tma_staging_is_bitwise_the_cp_async_path(monkeypatch, shape, n_slabs):
     np.testing.assert_array_equal(xa, xb)
     for p, q in zip(sa, sb):
         np.testing.assert_array_equal(p.q.cpu().numpy(), q.q.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_peer_exchange_across_processes(n):
+    """The multi-GPU wiring of the config-5 peer exchange (CUDA IPC handles
+    swapped over a gloo group, edge kernels storing into the other process's
+    rings, flags written / waited on by stream memory operations) with n
+    processes sharing this box's one GPU: the gathered slabs equal the
+    whole-volume run bit for bit.  A protocol check, not a timing (no kernel
+    waits on another; the streams do)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tools", "run_config5_dist.py"), "--side", "40", "--iters", "30",
+           "--inner", "5", "--p", "0.3", "--check", "--share-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert '"bitwise_equal_whole_volume": true' in r.stdout

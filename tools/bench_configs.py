@@ -205,7 +205,8 @@ def cfg8f():
     return out
 
 
-def cfg5(side=1024, K=200, inner=20):
+def config5_volume(side=1024):
+    """Config-5 input on the device (seeded): 50 ellipsoids U[0,1] + noise 0.1."""
     torch.manual_seed(0)
     g = torch.Generator(device="cuda").manual_seed(0)
     # setup on the device (seeded torch generator): ellipsoid phantom + noise
@@ -225,6 +226,12 @@ def cfg5(side=1024, K=200, inner=20):
             vol[z][m] = val
     b = vol + 0.1 * torch.randn((D, H, W), generator=g, device="cuda")
     del vol
+    return b
+
+
+def cfg5(side=1024, K=200, inner=20):
+    b = config5_volume(side)
+    D = H = W = side
     coins = psb.SkipConfig(0.1, 0).coins(K)
     slab = v3.Slab3D(b, 0, D, 0.08, inner, precision="fp32")
     del b
