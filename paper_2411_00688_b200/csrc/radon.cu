@@ -61,6 +61,13 @@ __device__ __forceinline__ void sample_pos(const Geo& G, double c, double s, int
   py = __dadd_rn(__dadd_rn(__dmul_rn(o, s), __dmul_rn(st, c)), G.center);
 }
 
+template <class T>
+__device__ __forceinline__ T warp_sum(T acc) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
 // Forward projection of one ray; the result is valid in lane 0 and is a
 // deterministic shuffle reduction.
 template <class T>
@@ -69,7 +76,65 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
   const double c = G.cs[ia], s = G.sn[ia];
   const int n = G.n;
   T acc = T(0);
-  for (int is = lane; is < G.ns; is += 32) {
+  // Samples that can deposit into the image have px, py in [-1, n).  With
+  // px = A - st*s, py = B + st*c that is an interval of st, computed here with
+  // a 2-sample margin (the exact per-sample test below stays the arbiter).
+  // The loop starts at a multiple of 32, so every lane visits the same
+  // samples as a loop over [0, ns) minus some that deposit nothing: the
+  // per-lane sums, and therefore the result, are bit-identical.
+  double lo = -G.half_span, hi = G.half_span;
+  {
+    const double o = G.off[ib];
+    const double av[2] = {o * c + G.center, o * s + G.center}, kv[2] = {-s, c};
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const double a = av[d], k = kv[d];
+      if (fabs(k) < 1e-9) {
+        if (a < -2.0 || a > n + 1.0) hi = lo - 1.0;
+        continue;
+      }
+      double t0 = (-1.0 - a) / k, t1 = ((double)n - a) / k;
+      if (t0 > t1) {
+        const double tt = t0;
+        t0 = t1;
+        t1 = tt;
+      }
+      lo = fmax(lo, t0);
+      hi = fmin(hi, t1);
+    }
+  }
+  int is_lo = 0, is_hi = -1;
+  if (lo <= hi) {
+    is_lo = max(0, (int)floor((lo + G.half_span) / G.dstep) - 2);
+    is_hi = min(G.ns - 1, (int)ceil((hi + G.half_span) / G.dstep) + 2);
+  }
+  if constexpr (sizeof(T) == 4) {
+    // fp32 state: each lane's first sample position exactly as the reference
+    // computes it, then the lattice step along the ray (32 samples per lane
+    // step) as one fp64 FMA per coordinate; the fractional offsets and the
+    // bilinear weights in fp32 (weights agree with the fp64 path to ~1e-7)
+    const int is0 = (is_lo & ~31) + lane;
+    const int nj = is0 <= is_hi ? (is_hi - is0) / 32 + 1 : 0;
+    double px0, py0;
+    sample_pos(G, c, s, ib, min(is0, G.ns - 1), px0, py0);
+    const double sx = -32.0 * G.dstep * s, sy = 32.0 * G.dstep * c;
+    for (int j = 0; j < nj; ++j) {
+      const double px = fma((double)j, sx, px0), py = fma((double)j, sy, py0);
+      const double fx0 = floor(px), fy0 = floor(py);
+      const int x0 = (int)fx0, y0 = (int)fy0;
+      if (x0 < -1 || x0 >= n || y0 < -1 || y0 >= n) continue;
+      const float fx = (float)(px - fx0), fy = (float)(py - fy0);
+      const float gx = 1.f - fx, gy = 1.f - fy;
+      const bool xa = x0 >= 0, xb = x0 + 1 < n, ya = y0 >= 0, yb = y0 + 1 < n;
+      const float* ur = u + y0 * n + x0;
+      if (ya && xa) acc = fmaf(gy * gx, ur[0], acc);
+      if (ya && xb && fx > 0.f) acc = fmaf(gy * fx, ur[1], acc);
+      if (yb && xa && fy > 0.f) acc = fmaf(fy * gx, ur[n], acc);
+      if (yb && xb && fx > 0.f && fy > 0.f) acc = fmaf(fy * fx, ur[n + 1], acc);
+    }
+    return warp_sum(acc);
+  }
+  for (int is = (is_lo & ~31) + lane; is <= is_hi; is += 32) {
     double px, py;
     sample_pos(G, c, s, ib, is, px, py);
     const double fx0 = floor(px), fy0 = floor(py);
@@ -84,9 +149,7 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
     if (yb && xa && w10 > 0) acc += (T)w10 * u[(y0 + 1) * n + x0];
     if (yb && xb && w11 > 0) acc += (T)w11 * u[(y0 + 1) * n + x0 + 1];
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  return acc;
+  return warp_sum(acc);
 }
 
 // Adjoint at pixel (r, c): sum over angles and the lattice samples that
