@@ -253,6 +253,32 @@ struct CapturedRun {
     PSB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     return PSB_OK;
   }
+  // Chunked capture: every `chunk` outer iterations the graph captured so far
+  // is instantiated and launched, and capture restarts on the same stream, so
+  // the host builds chunk c+1 while the device runs chunk c (one graph of a
+  // whole 1000-iteration run cost ~17 ms of capture + instantiation before
+  // the first kernel ran).  Call after outer iteration k was enqueued.
+  int chunk = 32;
+  int tick(int k, int K) {
+    if (!graph || (k + 1) % chunk != 0 || k + 1 >= K) return PSB_OK;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &g);
+    int rc = PSB_OK;
+    if (e != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (rc == PSB_OK && (e = cudaGraphInstantiate(&exec, g, 0)) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    if (rc == PSB_OK && (e = cudaGraphLaunch(exec, st)) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+    if (exec) cudaGraphExecDestroy(exec);
+    if (g) cudaGraphDestroy(g);
+    // capture restarts even after an error: end() always ends one capture
+    e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (rc == PSB_OK && e != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    return rc;
+  }
   // ends the capture (always), launches the graph if rc is still OK
   int end(int rc) {
     if (!graph) return rc;

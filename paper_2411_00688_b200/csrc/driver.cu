@@ -367,6 +367,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (fgp_time) cudaEventRecordWithFlags(fev[1], st, rec_flags);
   }
   for (int k = 0; k < K && rc == PSB_OK && !use_cluster; ++k) {
+    if (k > 0 && (rc = cap.tick(k - 1, K)) != PSB_OK) break;
     if (k > 0) clk.mark(k - 1, st);
     if (x_hist && k > 0 && rc == PSB_OK)  // iterate of outer iteration k-1 (device IterationLog)
       if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (k - 1) * x_bytes, x, x_bytes,

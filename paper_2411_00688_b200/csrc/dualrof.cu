@@ -129,6 +129,7 @@ int run_t(int algo, const T* b, T* q, T* h, T* work, int H, int W, double alpha,
   int cur = 0, prev = 0;  // slot indices of x_k and x_{k-1}
   const unsigned grid = (unsigned)((HW + 255) / 256);
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
+    if (k > 0 && (rc = cap.tick(k - 1, K)) != PSB_OK) break;
     const int nxt = algo == ALGO_FISTA ? (cur + 1 + (cur + 1 == prev ? 1 : 0)) % nslot
                                        : (cur + 1) % nslot;
     DualArgs<T> a{b, slot[cur], slot[prev], slot[nxt], h, H, W, (T)alpha, (T)mu, (T)gamma,

@@ -605,6 +605,7 @@ int ct_implicit_run(int dto, int dtf, const psb_radon_geom* g, void* x, void* y,
   IterClock clk;
   clk.begin(elapsed, K, st, use_graph != 0);
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
+    if (k > 0 && (rc = cap.tick(k - 1, K)) != PSB_OK) break;
     const int coin = coins_host[k] ? 1 : 0;
     const uint8_t* rep_d = k == first_coin ? rep_first : rep_plain;
     if (dto == PSB_F64 && dtf == PSB_F64)
@@ -676,6 +677,7 @@ int psb_pdhg_run(int dtype, const psb_radon_geom* geom, void* x, void* y, void* 
   clk.begin(elapsed_host, K, st, use_graph != 0);
   int rc = PSB_OK;
   for (int k = 0; k < K && rc == PSB_OK; ++k) {
+    if (k > 0 && (rc = cap.tick(k - 1, K)) != PSB_OK) break;
     const int coin = skip ? coins_host[k] : 1;
     if (skip == 2)
       rc = psb::pdhg1_step(dtype, geom, x, y, xbar, b, bad_iter, k, coin, sigma, tau, p,
