@@ -12,6 +12,8 @@
 //              memory, forms r = A u - b on the tile plus an R halo, and then
 //              applies the flipped (correlation) pass to produce g -- u, b
 //              read once, g written once (12 B/px fp32, 24 B/px fp64).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace psb {
@@ -63,13 +65,26 @@ __device__ __forceinline__ int wrap1(int i, int n) {  // periodic index, cheap n
   return i;
 }
 
-// Fused g = A^T (A u - b), separable, kernel size K at compile time (tile
-// sides and the index arithmetic below are constants).
+// Fused g = A^T (A u - b), separable, kernel size K and tile side TS at
+// compile time: every loop below has a constant trip count over the 256
+// threads (unrolled, no runtime division), and the periodic tile rows /
+// columns are wrapped once per element with a compare (|offset| < H, W).
+// One CTA per TS x TS output tile; TS = 16 gives 1024 CTAs at 512^2, all
+// resident at once (22 KB of shared memory each in fp64).
+constexpr int SEP_NT = 256;
+__device__ __forceinline__ int wrap_near(int i, int n, bool near) {
+  if (!near) {  // image smaller than a tile: any offset
+    i %= n;
+    return i < 0 ? i + n : i;
+  }
+  return i < 0 ? i + n : (i >= n ? i - n : i);  // i in [-n, 2n)
+}
+
 template <class T, int TS, int K>
-__global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict__ u,
-                                                            const T* __restrict__ bdat,
-                                                            T* __restrict__ g, int H, int W,
-                                                            Taps t) {
+__global__ void __launch_bounds__(SEP_NT) blur_grad_sep_kernel(const T* __restrict__ u,
+                                                               const T* __restrict__ bdat,
+                                                               T* __restrict__ g, int H, int W,
+                                                               Taps t) {
   extern __shared__ unsigned char smem_raw[];
   pdl_enter();
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -85,47 +100,70 @@ __global__ void __launch_bounds__(256) blur_grad_sep_kernel(const T* __restrict_
   for (int q = 0; q < K; ++q) w1[q] = (T)t.w1[q];
 
   const int i0 = blockIdx.y * TS, j0 = blockIdx.x * TS;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < NU * NU; e += nt) {
-    const int a = e / NU, b = e % NU;
-    su[e] = u[(int64_t)wrap1(i0 - 2 * R + a, H) * W + wrap1(j0 - 2 * R + b, W)];
+  const int tid = threadIdx.x;
+  const bool near = H >= NU && W >= NU;  // every tile index within one period
+#pragma unroll
+  for (int e0 = 0; e0 < NU * NU; e0 += SEP_NT) {
+    const int e = e0 + tid;
+    if (NU * NU % SEP_NT == 0 || e < NU * NU) {
+      const int a = e / NU, b = e % NU;
+      su[e] = u[(int64_t)wrap_near(i0 - 2 * R + a, H, near) * W +
+                wrap_near(j0 - 2 * R + b, W, near)];
+    }
   }
   __syncthreads();
   // forward A: out(i,j) = sum_a sum_b w1[a] w1[b] u(i-a+c, j-b+c)
-  for (int e = tid; e < NU * NR; e += nt) {
-    const int a = e / NR, jc = e % NR;  // jc: r-tile column; u column jc + R + (c - b)
-    T acc = T(0);
 #pragma unroll
-    for (int q = 0; q < K; ++q) acc += w1[q] * su[a * NU + jc + R + (R - q)];
-    sh[e] = acc;
+  for (int e0 = 0; e0 < NU * NR; e0 += SEP_NT) {
+    const int e = e0 + tid;
+    if (NU * NR % SEP_NT == 0 || e < NU * NR) {
+      const int a = e / NR, jc = e % NR;  // jc: r-tile column; u column jc + R + (c - b)
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc += w1[q] * su[a * NU + jc + R + (R - q)];
+      sh[e] = acc;
+    }
   }
   __syncthreads();
-  for (int e = tid; e < NR * NR; e += nt) {
-    const int ic = e / NR, jc = e % NR;
-    T acc = T(0);
 #pragma unroll
-    for (int q = 0; q < K; ++q) acc += w1[q] * sh[(ic + R + (R - q)) * NR + jc];
-    const int gi = wrap1(i0 - R + ic, H), gj = wrap1(j0 - R + jc, W);
-    sr[e] = acc - bdat[(int64_t)gi * W + gj];
+  for (int e0 = 0; e0 < NR * NR; e0 += SEP_NT) {
+    const int e = e0 + tid;
+    if (NR * NR % SEP_NT == 0 || e < NR * NR) {
+      const int ic = e / NR, jc = e % NR;
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc += w1[q] * sh[(ic + R + (R - q)) * NR + jc];
+      const int gi = wrap_near(i0 - R + ic, H, near), gj = wrap_near(j0 - R + jc, W, near);
+      sr[e] = acc - bdat[(int64_t)gi * W + gj];
+    }
   }
   __syncthreads();
   // adjoint A^T: out(i,j) = sum_a sum_b w1[a] w1[b] r(i+a-c, j+b-c)
-  for (int e = tid; e < NR * TS; e += nt) {
-    const int ic = e / TS, jt = e % TS;
-    T acc = T(0);
 #pragma unroll
-    for (int q = 0; q < K; ++q) acc += w1[q] * sr[ic * NR + jt + q];
-    sh2[e] = acc;
+  for (int e0 = 0; e0 < NR * TS; e0 += SEP_NT) {
+    const int e = e0 + tid;
+    if (NR * TS % SEP_NT == 0 || e < NR * TS) {
+      const int ic = e / TS, jt = e % TS;
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc += w1[q] * sr[ic * NR + jt + q];
+      sh2[e] = acc;
+    }
   }
   __syncthreads();
-  for (int e = tid; e < TS * TS; e += nt) {
-    const int it = e / TS, jt = e % TS;
-    const int gi = i0 + it, gj = j0 + jt;
-    if (gi >= H || gj >= W) continue;
-    T acc = T(0);
 #pragma unroll
-    for (int q = 0; q < K; ++q) acc += w1[q] * sh2[(it + q) * TS + jt];
-    g[(int64_t)gi * W + gj] = acc;
+  for (int e0 = 0; e0 < TS * TS; e0 += SEP_NT) {
+    const int e = e0 + tid;
+    if (TS * TS % SEP_NT == 0 || e < TS * TS) {
+      const int it = e / TS, jt = e % TS;
+      const int gi = i0 + it, gj = j0 + jt;
+      if (gi < H && gj < W) {
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc += w1[q] * sh2[(it + q) * TS + jt];
+        g[(int64_t)gi * W + gj] = acc;
+      }
+    }
   }
 }
 
@@ -143,17 +181,26 @@ int make_taps(const double* taps2d, const double* taps1d, int k, Taps& t) {
   return PSB_OK;
 }
 
-template <class T, int K>
-int launch_sep_k(const void* u, const void* b, void* g, int H, int W, const Taps& t,
-                 cudaStream_t st) {
-  constexpr int TS = 32;
+template <class T, int K, int TS>
+int launch_sep_kt(const void* u, const void* b, void* g, int H, int W, const Taps& t,
+                  cudaStream_t st) {
   const size_t sm = sep_smem<T, TS>(K);
   PSB_CHECK(func_attr(blur_grad_sep_kernel<T, TS, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                       (int)sm));
   dim3 grid((W + TS - 1) / TS, (H + TS - 1) / TS);
-  PSB_CUDA(launch_chain(blur_grad_sep_kernel<T, TS, K>, grid, dim3(256), sm, st, (const T*)u,
+  PSB_CUDA(launch_chain(blur_grad_sep_kernel<T, TS, K>, grid, dim3(SEP_NT), sm, st, (const T*)u,
                         (const T*)b, (T*)g, H, W, t));
   return PSB_OK;
+}
+
+template <class T, int K>
+int launch_sep_k(const void* u, const void* b, void* g, int H, int W, const Taps& t,
+                 cudaStream_t st) {
+  // 16 x 16 tiles while the grid fills the GPU; 32 x 32 for large images
+  // (less halo traffic once there are enough tiles anyway)
+  if ((int64_t)((H + 15) / 16) * ((W + 15) / 16) <= 8LL * sm_count())
+    return launch_sep_kt<T, K, 16>(u, b, g, H, W, t, st);
+  return launch_sep_kt<T, K, 32>(u, b, g, H, W, t, st);
 }
 
 template <class T>

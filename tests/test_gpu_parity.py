@@ -259,7 +259,7 @@ def test_blur_bitwise_golden(golden):
     assert L == pytest.approx(float(g["blur_L_32"]), rel=1e-12)
 
 
-@pytest.mark.parametrize("shape", [(16, 20), (33, 47), (512, 512)])
+@pytest.mark.parametrize("shape", [(9, 11), (16, 20), (33, 47), (512, 512), (640, 600)])
 @pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-14), (torch.float32, 2e-6)])
 def test_blur_grad_fused_separable(shape, dtype, tol):
     from paper_2411_00688_b200.operators import blur_grad_dev
