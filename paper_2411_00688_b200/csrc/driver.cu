@@ -13,6 +13,7 @@
 #include <thread>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -58,6 +59,11 @@ int fista_pre(int dto, int dtf, const void* xbar, const void* gb, int ident, voi
 // Fidelity A of the implicit splitting.  kind 0: identity (g = x - b fused
 // into the outer kernels); kind 1: periodic blur (g = A^T(Ax - b) by the
 // fused separable kernel, or the bit-exact direct path, into `g`).
+int blur_grad_pre2d(int dto, int dtf, const void* x, const void* b, void* g, int H, int W,
+                    const double* taps1d, int k, void* x_next, const void* h, void* z,
+                    double gamma, double hcoef, int coin, int32_t* bad, int kiter,
+                    cudaStream_t st);
+
 struct Fidelity {
   int kind = 0;
   const double* taps2d = nullptr;
@@ -268,6 +274,21 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   const uint8_t* rep_d = dev + o_rep;
   auto i32 = [&](size_t o) { return reinterpret_cast<const int32_t*>(dev + o); };
 
+  // Deblurring (separable blur, not FISTA): the gradient kernel also does the
+  // pre step; a skipped iteration writes x-hat to the other of two x buffers
+  // (the kernel still stages x halos), so x lives in x or x_alt by turns.
+  const char* nf = std::getenv("PSB_NO_FUSED_PRE");  // the two-kernel form (tests)
+  const bool no_fuse = nf && nf[0] == '1';
+  const bool fuse_pre = fid.kind == 1 && fid.separable && !fid.fista && !use_cluster && !no_fuse;
+  DevBuf d_xalt;
+  d_xalt.st = user_stream;
+  void* xcur = x;
+  void* xalt = nullptr;
+  if (fuse_pre) {
+    PSB_CUDA(cudaMallocAsync(&d_xalt.p, (size_t)HW * (dto == PSB_F32 ? 4 : 8), user_stream));
+    xalt = d_xalt.p;
+  }
+
   CapturedRun cap;
   if (int rc0 = cap.begin(user_stream, use_graph != 0)) return rc0;
   cudaStream_t st = cap.st;
@@ -370,7 +391,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (k > 0 && (rc = cap.tick(k - 1, K)) != PSB_OK) break;
     if (k > 0) clk.mark(k - 1, st);
     if (x_hist && k > 0 && rc == PSB_OK)  // iterate of outer iteration k-1 (device IterationLog)
-      if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (k - 1) * x_bytes, x, x_bytes,
+      if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (k - 1) * x_bytes, xcur, x_bytes,
                           cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         rc = fail(PSB_ERR_CUDA, "x history copy failed");
     const int ident = fid.kind == 0;
@@ -381,6 +402,12 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                          fid.separable, fid.scratch, st);
       if (!rc) rc = fista_pre(dto, dtf, fid.xbar, ident ? b : fid.g, ident, z, n * HW, gamma, st);
       if (rc) break;
+    } else if (fuse_pre) {
+      const int coin = coins_host[k] ? 1 : 0;
+      rc = blur_grad_pre2d(dto, dtf, xcur, b, fid.g, H, W, fid.taps1d, fid.ksize, xalt, h, z,
+                           gamma, hcoef, coin, bad, k, st);
+      if (rc) break;
+      if (!coin) std::swap(xcur, xalt);
     } else {
     if (!ident) {
       rc = blur_grad2d(dto, x, b, fid.g, H, W, fid.taps2d, fid.taps1d, fid.ksize, fid.separable,
@@ -397,14 +424,17 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                    n_inner, accelerated, nonneg, 0.125, beta.data(), st);
     if (fgp_time) cudaEventRecordWithFlags(fev[2 * k + 1], st, rec_flags);
     if (rc == PSB_OK)
-      rc = proxskip_post(dto, dtf, x, ident ? b : fid.g, ident, fid.fista ? nullptr : h, z, q, qps,
+      rc = proxskip_post(dto, dtf, xcur, ident ? b : fid.g, ident, fid.fista ? nullptr : h, z, q, qps,
                          act_d + off[k], na, H, W, n_inner, nonneg, gamma, pg, bad, k, st);
   }
 
   if (x_hist && rc == PSB_OK)
-    if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, x, x_bytes,
+    if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, xcur, x_bytes,
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       rc = fail(PSB_ERR_CUDA, "x history copy failed");
+  if (xcur != x && rc == PSB_OK &&
+      cudaMemcpyAsync(x, xcur, x_bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    rc = fail(PSB_ERR_CUDA, "x copy-back failed");
   if (rc == PSB_OK) clk.mark(K - 1, st);
   // The schedule buffer is released stream-ordered after the run (DevBuf).
   rc = cap.end(rc);

@@ -323,3 +323,29 @@ def test_config2_full_size_parity_100_outer():
     assert rel(x, xr) < U_TOL
     o_dev, o_ref = psb.objective_tv(x, prob), oc.tv_objective(xr, pr)
     assert abs(o_dev - o_ref) / abs(o_ref) < OBJ_TOL
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp32"])
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_deblur_fused_pre_is_bitwise_the_two_kernel_form(monkeypatch, precision, use_graph):
+    """The deblurring driver runs the ProxSkip pre step inside the blur
+    gradient kernel (x in two buffers by turns); PSB_NO_FUSED_PRE=1 selects
+    the gradient kernel + pre kernel: same arithmetic, same iterates, and the
+    same final x in the caller's buffer (odd and even numbers of skips)."""
+    truth = phantoms.random_shapes((96, 80), 6, np.random.default_rng(2), rects=False)
+    k = psb.gaussian_kernel(9, 2.0)
+    b = phantoms.add_noise(oc.conv_periodic(truth, k.weights), 0.01, 2)
+    A = psb.blur_map(k, b.shape)
+    L = psb.build_tv_recon(A, b, 0.02, inner_budget=7, precision=precision).prox_problem.smooth.lipschitz
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PSB_NO_FUSED_PRE", flag)
+        res = []
+        for iters in (37, 38):
+            prob = psb.build_tv_recon(A, b, 0.02, inner_budget=7, precision=precision)
+            x, _ = psb.run_proxskip(prob.prox_problem, np.zeros_like(b), None, 1.0 / L,
+                                    psb.SkipConfig(0.3, 5), iters, use_graph=use_graph)
+            res.append(x)
+        out.append(res)
+    for a, c in zip(*out):
+        np.testing.assert_array_equal(a, c)
