@@ -282,12 +282,17 @@ def run_gpu(args):
     b_pin = torch.from_numpy(b_host).pin_memory()
     # untimed warm-up of the e2e path on a slice (its one-time host set-up:
     # pinned staging buffers, copy stream, stream-memop entry points)
+    # The result lands in a page-locked host buffer allocated up front, like
+    # the pinned input (a pageable one costs a staged copy plus first-touch
+    # page faults on 1 GB inside the timed call: e2e varied 290-500 it/s).
+    x_pin = torch.empty(b_pin.shape, dtype=torch.float32).pin_memory()
     nw = min(len(idx), 512)
-    psb.run_proxskip_batched(b_pin[:nw], ALPHA, P, idx[:nw], args.warmup, INNER, precision="fp32")
+    psb.run_proxskip_batched(b_pin[:nw], ALPHA, P, idx[:nw], args.warmup, INNER, precision="fp32",
+                             out=x_pin[:nw])
     sync_all()
     t0 = time.perf_counter()
     x_e2e, counts = psb.run_proxskip_batched(b_pin, ALPHA, P, idx, args.warmup + args.steps, INNER,
-                                             precision="fp32")
+                                             precision="fp32", out=x_pin)
     assert x_e2e.device.type == "cpu"
     t_e2e_local = time.perf_counter() - t0
     if world > 1:
@@ -328,7 +333,7 @@ def run_gpu(args):
         "cpu_baseline": cpu,
         "e2e": {"value": n_e2e / t_e2e, "unit": "outer-iter/s (4096-problem batch)",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, host out)"},
+                "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, pinned host out)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

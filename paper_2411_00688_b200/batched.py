@@ -143,8 +143,12 @@ def _memops():
 
 
 def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.0,
-                         precision="fp32", use_graph=False, chunk=256):
+                         precision="fp32", use_graph=False, chunk=256, out=None):
     """Config-4 entry point: returns (x, prox_counts) as the input currency.
+
+    ``out`` (optional, host input only): a contiguous float32 CPU tensor of
+    b's shape that receives x -- page-locked, the results go straight from
+    the device into it by DMA (no staging, no page faults inside the call).
 
     Host input on the cluster path is streamed: the run kernels are launched
     first and wait per problem for its input chunk (``chunk`` problems),
@@ -163,19 +167,29 @@ def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.
     if (AR.is_host(b) and f32 and not use_graph and precision == "fp32" and chunk and n > chunk
             and len(shape) == 3 and shape[1:] == (256, 256) and _memops()
             and os.environ.get("PSB_NO_CLUSTER", "0") != "1"):
-        return _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk)
+        return _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out)
     solver = BatchedTvDenoise(b, alpha, inner_budget, precision=precision)
     solver.run_proxskip(coin_table(p, seeds, iters), gamma, p, use_graph=use_graph)
     solver.check_finite()
+    if out is not None:
+        AR.download_into(out, solver.x.to(out.dtype))
+        return (out if isinstance(b, torch.Tensor) else out.numpy()), solver.prox_count.copy()
     return AR.like(solver.x, b), solver.prox_count.copy()
 
 
-def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk):
+def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=None):
     tensor_in = isinstance(b, torch.Tensor)
     src = b.detach().contiguous() if tensor_in else torch.from_numpy(np.ascontiguousarray(b))
     n, H, W = src.shape
     if n != seeds.size:
         raise ValueError("one seed per problem")
+    # (validated before anything is launched: the run kernels wait for input)
+    if out is None:
+        out = torch.empty((n, H, W), dtype=torch.float32)
+    elif (not isinstance(out, torch.Tensor) or tuple(out.shape) != (n, H, W)
+          or out.dtype != torch.float32 or out.is_cuda or not out.is_contiguous()):
+        raise ValueError("run_proxskip_batched: out must be a contiguous float32 CPU tensor "
+                         "of b's shape")
     solver = BatchedTvDenoise(torch.empty((n, H, W), dtype=torch.float32, device="cuda"), alpha,
                               inner_budget, precision="fp32")
     coins = coin_table(p, seeds, iters)
@@ -197,7 +211,7 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk):
            solver.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(solver.bad), L.ptr(ready),
            L.ptr(done), chunk, nc, L.stream())
     cs = L.C.c_void_p(copy.cuda_stream)
-    out = torch.empty((n, H, W), dtype=torch.float32)
+    pinned = out.is_pinned()
     with torch.cuda.stream(copy):
         # 2) inputs, chunk by chunk, each announced to the waiting kernels
         for c, (lo, hi) in enumerate(bounds):
@@ -208,8 +222,13 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk):
         for c, (lo, hi) in enumerate(bounds):
             L.call("psb_stream_wait_geq_u32", cs, L.C.c_void_p(done.data_ptr() + 4 * c),
                    16 * (hi - lo))
-            AR.download_into(out[lo:hi], solver.x[lo:hi])
+            if pinned:  # DMA straight into the caller's page-locked buffer
+                out[lo:hi].copy_(solver.x[lo:hi], non_blocking=True)
+            else:
+                AR.download_into(out[lo:hi], solver.x[lo:hi])
     main.wait_stream(copy)
+    if pinned:
+        copy.synchronize()
     if int(ready[nc].item()) != 0:
         raise RuntimeError("streamed run: an input chunk never arrived (device wait timed out)")
     solver.check_finite()

@@ -229,3 +229,25 @@ def test_streamed_host_run_equals_resident_run(host):
     np.testing.assert_array_equal(c, c_ref)
     x = x if isinstance(x, np.ndarray) else x.numpy()
     np.testing.assert_array_equal(x.astype(np.float32), x_ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_streamed_run_into_caller_buffer(pinned):
+    """out=: the streamed run writes x into the caller's CPU buffer (DMA when
+    page-locked) -- the same bits as the resident run; a wrong buffer is a
+    ValueError."""
+    idx = np.arange(40) * 31 % 4096
+    b = _batch(idx).astype(np.float32)
+    K, inner, p = 20, 5, 0.3
+    x_ref, c_ref = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
+    src = torch.from_numpy(b).pin_memory()
+    out = torch.full(b.shape, float("nan"), dtype=torch.float32)
+    if pinned:
+        out = out.pin_memory()
+    x, c = psb.run_proxskip_batched(src, 0.1, p, idx, K, inner, chunk=16, out=out)
+    assert x is out
+    np.testing.assert_array_equal(c, c_ref)
+    np.testing.assert_array_equal(out.numpy(), x_ref.cpu().numpy())
+    with pytest.raises(ValueError):
+        psb.run_proxskip_batched(src, 0.1, p, idx, K, inner, chunk=16,
+                                 out=torch.empty((3, 256, 256), dtype=torch.float32))
