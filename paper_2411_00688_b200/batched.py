@@ -17,6 +17,7 @@ oracle.  Multi-GPU: problems are sharded across ranks with no collective
 from __future__ import annotations
 
 import os
+import time
 
 import numpy as np
 import torch
@@ -190,9 +191,12 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
           or out.dtype != torch.float32 or out.is_cuda or not out.is_contiguous()):
         raise ValueError("run_proxskip_batched: out must be a contiguous float32 CPU tensor "
                          "of b's shape")
+    dbg = os.environ.get("PSB_DEBUG_E2E") == "1"
+    t0 = time.perf_counter() if dbg else 0.0
     solver = BatchedTvDenoise(torch.empty((n, H, W), dtype=torch.float32, device="cuda"), alpha,
                               inner_budget, precision="fp32")
     coins = coin_table(p, seeds, iters)
+    t1 = time.perf_counter() if dbg else 0.0
     bounds = [(lo, min(n, lo + chunk)) for lo in range(0, n, chunk)]
     nc = len(bounds)
     flags = torch.zeros(2 * nc + 1, dtype=torch.int32, device="cuda")  # ready[nc + 1], done[nc]
@@ -226,9 +230,15 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
                 out[lo:hi].copy_(solver.x[lo:hi], non_blocking=True)
             else:
                 AR.download_into(out[lo:hi], solver.x[lo:hi])
+    t2 = time.perf_counter() if dbg else 0.0
     main.wait_stream(copy)
     if pinned:
         copy.synchronize()
+    if dbg:
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        print(f"[psb e2e] setup {1e3 * (t1 - t0):.1f} ms, enqueue {1e3 * (t2 - t1):.1f} ms, "
+              f"run {1e3 * (t3 - t2):.1f} ms", flush=True)
     if int(ready[nc].item()) != 0:
         raise RuntimeError("streamed run: an input chunk never arrived (device wait timed out)")
     solver.check_finite()
