@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(TB_THREADS, 1) fgp2d_tb_kernel(TbArgs a) {
   __shared__ float s_u[8][TBS];         // first-row u of each warp row
   __shared__ float s_yx[8][TBR];        // lane-31 column y_x of warp column 0, per warp row
   __shared__ float s_ul[8][TBR];        // lane-0 column u of warp column 1, per warp row
+  pdl_enter();  // launched as a chain: the next launch's CTAs wait here, not in the launch queue
   const int entry = blockIdx.y;
   const int p = a.active ? a.active[entry] : entry;
   const int H = a.H, W = a.W;
@@ -942,8 +943,9 @@ static int fgp2d_run_tb(const float* x, int64_t xps, float* q, int64_t qps, cons
       a.out_ps = sps;
       a.out_by_entry = 1;
     }
-    fgp2d_tb_kernel<<<dim3((unsigned)tiles, (unsigned)n_active), TB_THREADS, 0, st>>>(a);
-    if (cudaGetLastError() != cudaSuccess) rc = fail(PSB_ERR_CUDA, "fgp2d_tb launch failed");
+    if (launch_chain(fgp2d_tb_kernel, dim3((unsigned)tiles, (unsigned)n_active), dim3(TB_THREADS),
+                     0, st, a) != cudaSuccess)
+      rc = fail(PSB_ERR_CUDA, "fgp2d_tb launch failed");
   }
   cudaFreeAsync(scratch, st);
   return rc;
