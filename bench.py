@@ -37,6 +37,7 @@ SIDE = 256
 ALPHA = 0.1
 P = 0.1
 INNER = 50
+E2E_REPS = 3
 RUN_LEN = 300
 BYTES_FGP_MOM = 28   # fp32 per pixel-iteration: x + q_k(2) + q_{k-1}(2) read, q_{k+1}(2) write
 BYTES_FGP_FIRST = 20  # first inner iteration (beta = 0): no q_{k-1} read
@@ -289,12 +290,19 @@ def run_gpu(args):
     nw = min(len(idx), 512)
     psb.run_proxskip_batched(b_pin[:nw], ALPHA, P, idx[:nw], args.warmup, INNER, precision="fp32",
                              out=x_pin[:nw])
-    sync_all()
-    t0 = time.perf_counter()
-    x_e2e, counts = psb.run_proxskip_batched(b_pin, ALPHA, P, idx, args.warmup + args.steps, INNER,
-                                             precision="fp32", out=x_pin)
-    assert x_e2e.device.type == "cpu"
-    t_e2e_local = time.perf_counter() - t0
+    # Three timed calls, the median reported: the device part of a call is
+    # stable to 0.1 ms (CUDA-event timeline of the copies, PSB_DEBUG_E2E=1),
+    # but the host wall clock of a single call sometimes stalls for 0.1-1 s
+    # (seen in ~1 of 8 calls, with the device timeline unchanged).
+    e2e_samples = []
+    for _ in range(E2E_REPS):
+        sync_all()
+        t0 = time.perf_counter()
+        x_e2e, counts = psb.run_proxskip_batched(b_pin, ALPHA, P, idx, args.warmup + args.steps,
+                                                 INNER, precision="fp32", out=x_pin)
+        assert x_e2e.device.type == "cpu"
+        e2e_samples.append(time.perf_counter() - t0)
+    t_e2e_local = float(np.median(e2e_samples))
     if world > 1:
         tt = torch.tensor([t_e2e_local], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -333,7 +341,9 @@ def run_gpu(args):
         "cpu_baseline": cpu,
         "e2e": {"value": n_e2e / t_e2e, "unit": "outer-iter/s (4096-problem batch)",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, pinned host out)"},
+                "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, pinned host out)",
+                "timing": f"host wall clock per call, median of {E2E_REPS} calls (max over ranks)",
+                "samples_s": [round(t, 5) for t in e2e_samples]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

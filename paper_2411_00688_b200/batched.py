@@ -216,20 +216,35 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
            L.ptr(done), chunk, nc, L.stream())
     cs = L.C.c_void_p(copy.cuda_stream)
     pinned = out.is_pinned()
+    evs = []  # debug timeline (PSB_DEBUG_E2E=1): chunk arrivals / completions
     with torch.cuda.stream(copy):
+        if dbg:
+            evs.append(("start", torch.cuda.Event(enable_timing=True)))
+            evs[-1][1].record(copy)
         # 2) inputs, chunk by chunk, each announced to the waiting kernels
         for c, (lo, hi) in enumerate(bounds):
             part = src[lo:hi]  # float32 H2D: a DMA, no kernel on this stream
             solver.b[lo:hi].copy_(part, non_blocking=part.is_pinned())
             L.call("psb_stream_write_u32", cs, L.C.c_void_p(ready.data_ptr() + 4 * c), 1)
+            if dbg:
+                evs.append((f"in{c}", torch.cuda.Event(enable_timing=True)))
+                evs[-1][1].record(copy)
         # 3) results, chunk by chunk, as soon as the chunk's problems are done
         for c, (lo, hi) in enumerate(bounds):
             L.call("psb_stream_wait_geq_u32", cs, L.C.c_void_p(done.data_ptr() + 4 * c),
                    16 * (hi - lo))
+            if dbg:
+                evs.append((f"done{c}", torch.cuda.Event(enable_timing=True)))
+                evs[-1][1].record(copy)
             if pinned:  # DMA straight into the caller's page-locked buffer
                 out[lo:hi].copy_(solver.x[lo:hi], non_blocking=True)
             else:
                 AR.download_into(out[lo:hi], solver.x[lo:hi])
+        if dbg:
+            evs.append(("end", torch.cuda.Event(enable_timing=True)))
+            evs[-1][1].record(copy)
+            main_end = torch.cuda.Event(enable_timing=True)
+            main_end.record(main)
     t2 = time.perf_counter() if dbg else 0.0
     main.wait_stream(copy)
     if pinned:
@@ -238,7 +253,10 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         print(f"[psb e2e] setup {1e3 * (t1 - t0):.1f} ms, enqueue {1e3 * (t2 - t1):.1f} ms, "
-              f"run {1e3 * (t3 - t2):.1f} ms", flush=True)
+              f"run {1e3 * (t3 - t2):.1f} ms; timeline " +
+              " ".join(f"{k}={evs[0][1].elapsed_time(e):.1f}" for k, e in evs[1:]) +
+              f" main_end={evs[0][1].elapsed_time(main_end):.1f} host_after_enqueue="
+              f"{1e3 * (t2 - t1):.1f}", flush=True)
     if int(ready[nc].item()) != 0:
         raise RuntimeError("streamed run: an input chunk never arrived (device wait timed out)")
     solver.check_finite()

@@ -347,13 +347,20 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                        dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
                        0.125, beta_d, bad, cs, gate ? started_d : nullptr, seq, st);
     if (gate && rc == PSB_OK) {
-      const auto t_end = std::chrono::steady_clock::now() + std::chrono::milliseconds(200);
+      const auto t_beg = std::chrono::steady_clock::now();
+      const auto t_end = t_beg + std::chrono::milliseconds(200);
+      int ok = 0;
       for (;;) {
-        int ok = 0;
+        ok = 0;
         for (int c = 0; c < G; ++c) ok += started_h[c] == seq;
         if (ok == G || std::chrono::steady_clock::now() > t_end) break;
         std::this_thread::yield();
       }
+      const char* dg = std::getenv("PSB_DEBUG_GATE");
+      if (dg && dg[0] == '1')
+        fprintf(stderr, "[psb gate] %d of %d clusters started after %.3f ms\n", ok, G,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_beg)
+                    .count());
     }
     // (never in a streamed run: the synchronisation below would wait for
     // kernels that wait for copies the caller has not enqueued yet)
