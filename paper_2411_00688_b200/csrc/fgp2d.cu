@@ -329,9 +329,9 @@ __global__ void fgp2d_finalize_kernel(const T* __restrict__ x, int64_t xps, T* q
 // pixel-iteration, for (64/48)^2 = 1.78x redundant halo arithmetic.  Per-pixel
 // arithmetic is fgp2d_item's (same expressions), so results equal the
 // streaming kernel's.
-constexpr int TBI = 8;                    // inner iterations per launch (halo width)
+constexpr int TBI = 10;                   // inner iterations per launch (halo width)
 constexpr int TBS = 64;                   // window side
-constexpr int TBT = TBS - 2 * TBI;        // output tile side (48)
+constexpr int TBT = TBS - 2 * TBI;        // output tile side (44: 12 x 12 = 144 CTAs at 512^2, one wave)
 constexpr int TBR = 8;                    // rows per thread
 constexpr int TB_THREADS = 512;           // 2 warp columns x 8 warp rows
 
