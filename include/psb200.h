@@ -95,6 +95,10 @@ int psb_fidprox(int dtype, const void* v, double t, const void* t_arr, const voi
                 int64_t count, void* stream);
 int psb_recip_floor(int dtype, const void* x, double floor_, void* out, int64_t count,
                     void* stream);
+/* psb_prox_l2_fidelity: out = (x + t .* b) / (1 + t), t scalar or t_arr per
+ * element -- prox_l2_fidelity(x, b, tau), proximal.py:44-55 */
+int psb_prox_l2_fidelity(int dtype, const void* x, double t, const void* t_arr, const void* b,
+                         void* out, int64_t count, void* stream);
 int psb_absgrad2d(int dtype, const void* u, void* g, int H, int W, void* stream);
 int psb_absdiv2d(int dtype, const void* q, void* d, int H, int W, void* stream);
 
@@ -178,6 +182,11 @@ int psb_sumsq_bcast(int dtype, const void* a, const void* b, int64_t n, int64_t 
                     void* stream);
 int psb_count_below(int dtype, const void* a, int64_t n, int64_t len, double thresh, double* out,
                     void* stream);
+/* psb_count_outside_ball: number of pixels of a (2, len) dual field q with
+ * sqrt(q0^2 + q1^2) > r, evaluated in fp64 -- the feasibility test of
+ * dual_gap_rof (tv.py:98-100) */
+int psb_count_outside_ball(int dtype, const void* q, int64_t len, double r, double* out,
+                           void* stream);
 
 /* Bernoulli coin table of many problems (skip.py:16-28): coins[k*n + i] =
  * Generator(Philox(seeds[i])).random() < p for k < K, bit-identical to numpy

@@ -17,7 +17,8 @@ from .operators import (BlurKernel, LinearMap, RadonGeometry, blur_adjoint, blur
                         grad_map, identity_map, power_method, radon_map)
 from .problems import (GRAD_NORM_SQ, DualRofProblem, TvReconstructionProblem, build_dual_rof,
                        build_tv_recon, build_tv_saddle_implicit, objective_tv, primal_from_dual)
-from .proximal import project_ball, project_nonneg, prox_zero
+from .phantoms import add_noise
+from .proximal import project_ball, project_nonneg, prox_l2_fidelity, prox_zero
 from .refsol import SELF_CONSISTENCY_TOL, ReferenceSolution, compute_reference_solution
 from .skip import (SkipConfig, bernoulli_op, optimal_probability, run_pdhgskip1, run_pdhgskip2,
                    run_proxskip)

@@ -57,6 +57,7 @@ SIGNATURES = {
     "psb_axpy_arr": [_i32, _vp, _i32, _vp, _vp, _vp, _i64, _vp],
     "psb_fidprox": [_i32, _vp, _dbl, _vp, _vp, _vp, _i64, _vp],
     "psb_recip_floor": [_i32, _vp, _dbl, _vp, _i64, _vp],
+    "psb_prox_l2_fidelity": [_i32, _vp, _dbl, _vp, _vp, _vp, _i64, _vp],
     "psb_absgrad2d": [_i32, _vp, _vp, _i32, _i32, _vp],
     "psb_absdiv2d": [_i32, _vp, _vp, _i32, _i32, _vp],
     "psb_fgp2d_iter": [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _dbl, _vp, _i32, _vp, _i32, _i32,
@@ -73,6 +74,7 @@ SIGNATURES = {
     "psb_tv2d": [_i32, _vp, _i64, _i32, _i32, _vp, _vp],
     "psb_sumsq_bcast": [_i32, _vp, _vp, _i64, _i64, _vp, _vp],
     "psb_count_below": [_i32, _vp, _i64, _i64, _dbl, _vp, _vp],
+    "psb_count_outside_ball": [_i32, _vp, _i64, _dbl, _vp, _vp],
     "psb_count_nonfinite": [_i32, _vp, _i64, _vp, _vp],
     "psb_proxskip_pre": [_i32, _i32, _vp, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _vp,
                          _i32, _vp],

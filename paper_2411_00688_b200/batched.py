@@ -3,15 +3,21 @@
 The reference has no batch API: config 4 is 4096 independent
 ``build_tv_recon(identity_map, b_i, alpha, inner_budget=50)`` +
 ``run_proxskip(..., SkipConfig(p, seed_i), K)`` problems.  Here they live in
-one set of device buffers -- x, h, b, z: (N, H, W); dual slots (N, 3, 2, H, W)
--- and advance together: every outer iteration launches one fused pre kernel
-over all N problems, the FGP inner iterations over the compacted list of
-coin-fired problems only (each problem keeps its own Philox coin stream), and
-one post kernel over that list.  Per-problem semantics (coins, warm starts,
-last_weight re-projection, inner-iteration counters) equal N separate
-reference runs; tests/test_gpu_parity.py checks sampled problems against the
-oracle.  Multi-GPU: problems are sharded across ranks with no collective
-(``shard_indices``).
+one set of device buffers -- x, h, b, z: (N, H, W); dual slots (N, 3, 2, H, W).
+For 256 x 256 problems with an fp32 FGP (config 4) one native call runs the
+whole K-iteration segment of every problem in ONE launch of the cluster run
+kernel (csrc/fgp_cluster.cu: a 16-CTA cluster takes one problem at a time and
+executes all of its coin-fired prox calls back to back, FGP state in
+registers) plus the SM-worker kernel on the SMs the clusters leave
+(csrc/fgp2d.cu), both claiming problems from one device work queue.  Other
+shapes / precisions advance all problems together per outer iteration: one
+fused pre kernel over the batch, the FGP inner iterations over the compacted
+list of coin-fired problems only, one post kernel over that list.
+Per-problem semantics (own Philox coin stream, warm starts, last_weight
+re-projection, inner-iteration counters) equal N separate reference runs;
+tests/test_gpu_fullsize.py checks 32 config-4 problems at the full 300 x 50
+schedule against fixtures produced by the reference.  Multi-GPU: problems are
+sharded across ranks with no collective (``shard_indices``).
 """
 
 from __future__ import annotations
@@ -151,12 +157,12 @@ def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.
     b's shape that receives x -- page-locked, the results go straight from
     the device into it by DMA (no staging, no page faults inside the call).
 
-    Host input on the cluster path is streamed: the run kernels are launched
-    first and wait per problem for its input chunk (``chunk`` problems),
-    whose host->device copy the copy stream announces with a stream memory
-    write; each chunk's result goes back to the host as soon as its problems
-    are done (stream memory wait on a device counter) while later chunks
-    still compute.  Same arithmetic and results as the resident run."""
+    Host input on the cluster path is streamed: every chunk's host->device
+    copy (``chunk`` problems) is enqueued on a copy stream, each announced by
+    a stream memory write; the run kernels, launched next, wait per problem
+    for its chunk's flag; each chunk's result goes back to the host as soon as
+    its problems are done (stream memory wait on a device counter) while later
+    chunks still compute.  Same arithmetic and results as the resident run."""
     seeds = np.asarray(seeds).reshape(-1)
     n = int(seeds.size)
     shape = tuple(b.shape) if hasattr(b, "shape") else np.shape(b)
@@ -206,14 +212,6 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
     start.record(main)  # buffers allocated and zeroed
     copy = torch.cuda.Stream()
     copy.wait_event(start)
-    # 1) the run: its kernels wait for the chunks below
-    L.call("psb_proxskip_denoise_run_streamed", L.dcode(solver.dto), L.dcode(solver.dtf),
-           L.ptr(solver.x), L.ptr(solver.b), L.ptr(solver.h), L.ptr(solver.z),
-           L.ptr(solver.slots), n, H, W, coins.ctypes.data_as(L.C.c_void_p), coins.shape[0],
-           float(gamma), float(p), float(alpha), inner_budget, 1, 0,
-           solver.last_weight.ctypes.data_as(L.C.c_void_p),
-           solver.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(solver.bad), L.ptr(ready),
-           L.ptr(done), chunk, nc, L.stream())
     cs = L.C.c_void_p(copy.cuda_stream)
     pinned = out.is_pinned()
     evs = []  # debug timeline (PSB_DEBUG_E2E=1): chunk arrivals / completions
@@ -221,7 +219,10 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
         if dbg:
             evs.append(("start", torch.cuda.Event(enable_timing=True)))
             evs[-1][1].record(copy)
-        # 2) inputs, chunk by chunk, each announced to the waiting kernels
+        # 1) inputs, chunk by chunk, each announced to the run kernels -- all
+        #    enqueued BEFORE the run, so the copies never depend on the run
+        #    kernels making progress (serialised execution under
+        #    CUDA_LAUNCH_BLOCKING=1, compute-sanitizer or ncu stays correct)
         for c, (lo, hi) in enumerate(bounds):
             part = src[lo:hi]  # float32 H2D: a DMA, no kernel on this stream
             solver.b[lo:hi].copy_(part, non_blocking=part.is_pinned())
@@ -229,6 +230,15 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
             if dbg:
                 evs.append((f"in{c}", torch.cuda.Event(enable_timing=True)))
                 evs[-1][1].record(copy)
+    # 2) the run: its kernels wait per problem for the chunk flags above
+    L.call("psb_proxskip_denoise_run_streamed", L.dcode(solver.dto), L.dcode(solver.dtf),
+           L.ptr(solver.x), L.ptr(solver.b), L.ptr(solver.h), L.ptr(solver.z),
+           L.ptr(solver.slots), n, H, W, coins.ctypes.data_as(L.C.c_void_p), coins.shape[0],
+           float(gamma), float(p), float(alpha), inner_budget, 1, 0,
+           solver.last_weight.ctypes.data_as(L.C.c_void_p),
+           solver.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(solver.bad), L.ptr(ready),
+           L.ptr(done), chunk, nc, L.stream())
+    with torch.cuda.stream(copy):
         # 3) results, chunk by chunk, as soon as the chunk's problems are done
         for c, (lo, hi) in enumerate(bounds):
             L.call("psb_stream_wait_geq_u32", cs, L.C.c_void_p(done.data_ptr() + 4 * c),

@@ -73,6 +73,15 @@ template <> struct Ar<double> {
   }
 };
 
+// fp32 ball projections use the radius r * kBallShrink: rsqrt.approx (<= ~2^-22
+// relative error) plus the roundings of the scale and of q' = a * s could
+// otherwise leave |q'| a few ulp above r, and the reference's feasibility test
+// (tv.py:98-100, 1e-10 slack) would reject the fp32 dual iterate.  With the
+// 2^-20 shrink |q'| <= r holds for every input; the projected duals move by
+// < 1e-6 relative, far inside the fp32 parity tolerance.  (fp64 projections are
+// the reference's exact formula.)
+constexpr float kBallShrink = 1.0f - 0x1p-20f;
+
 template <> struct Ar<float> {
   static __device__ __forceinline__ float add(float a, float b) { return a + b; }
   static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
@@ -86,10 +95,10 @@ template <> struct Ar<float> {
     return y;
   }
   static __device__ __forceinline__ float ball_scale(float a, float b, float r) {
-    return fminf(1.0f, r * rsq(fmaf(a, a, b * b)));
+    return fminf(1.0f, (r * kBallShrink) * rsq(fmaf(a, a, b * b)));
   }
   static __device__ __forceinline__ float ball_scale3(float a, float b, float c, float r) {
-    return fminf(1.0f, r * rsq(fmaf(a, a, fmaf(b, b, c * c))));
+    return fminf(1.0f, (r * kBallShrink) * rsq(fmaf(a, a, fmaf(b, b, c * c))));
   }
 };
 
@@ -178,10 +187,14 @@ __device__ __forceinline__ void chunk_wait(const ChunkSync& cs, int p) {
   const int32_t* f = cs.ready + p / cs.chunk;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const int32_t* err = cs.ready + cs.n_chunks;
   for (;;) {
-    int v;
+    int v, e;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
     if (v) return;
+    // a wait that already timed out elsewhere aborts every later wait at once
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(e) : "l"(err) : "memory");
+    if (e) return;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > 20000000000ull) {
@@ -198,6 +211,66 @@ __device__ __forceinline__ void chunk_done(const ChunkSync& cs, int p, int add, 
   __threadfence();
   __syncthreads();
   if (leader) atomicAdd(cs.done + p / cs.chunk, add);
+}
+
+// ---- dynamic problem queue (run drivers, configs 1 / 4) ----------------------
+// The cluster run kernel and the SM-worker kernel claim problems from ONE
+// device queue: `order` lists the problems by input chunk, then longest first
+// (cost = prox calls x n_inner + 2), and `head` is the next position.  A
+// cluster claims with one atomicAdd.  An SM worker (about 20x slower per
+// problem than a 16-SM cluster) claims position i only while its expected
+// time for that problem does not exceed the clusters' expected time for the
+// rest of the queue -- both rates measured on the fly (globaltimer ns per cost
+// unit of finished problems, `stats`), so no cost ratio is assumed and the run
+// ends with the clusters, not with an SM worker's last problem.  Which kernel
+// runs a problem never changes a result (the two kernels are bit-identical).
+struct WorkQueue {
+  unsigned int* head = nullptr;         // next position of `order` to claim (zero at run start)
+  unsigned long long* stats = nullptr;  // [4]: cluster ns, cluster cost, worker ns, worker cost
+  const int32_t* order = nullptr;       // [n] problem indices in claim order
+  const float* cost = nullptr;          // [n] cost units of order[i]
+  const float* suffix = nullptr;        // [n + 1] sum of cost[i .. n)
+  int n = 0;
+  int clusters = 0;                     // clusters claiming beside the SM workers
+};
+
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// cluster side: next position, or -1 when the queue is empty
+__device__ __forceinline__ int wq_claim(const WorkQueue& q) {
+  const unsigned i = atomicAdd(q.head, 1u);
+  return i < (unsigned)q.n ? (int)i : -1;
+}
+
+// SM-worker side (see above); -1: nothing worth taking
+__device__ __forceinline__ int wq_claim_worker(const WorkQueue& q) {
+  for (;;) {
+    unsigned i;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(i) : "l"(q.head) : "memory");
+    if (i >= (unsigned)q.n) return -1;
+    if (q.clusters > 0) {
+      unsigned long long s[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(s[k]) : "l"(q.stats + k) : "memory");
+      if (s[1] > 0 && s[3] > 0) {
+        const double t_worker = (double)s[2] / (double)s[3] * (double)q.cost[i];
+        const double t_rest = (double)s[0] / (double)s[1] * (double)q.suffix[i + 1] / q.clusters;
+        if (t_worker > t_rest) return -1;
+      }
+    }
+    if (atomicCAS(q.head, i, i + 1) == i) return (int)i;
+  }
+}
+
+// a finished problem's time and cost (role 0: cluster, 1: SM worker)
+__device__ __forceinline__ void wq_record(const WorkQueue& q, int role, int pos, uint64_t t0) {
+  atomicAdd(q.stats + 2 * role, (unsigned long long)(gtimer_ns() - t0));
+  atomicAdd(q.stats + 2 * role + 1, (unsigned long long)q.cost[pos]);
 }
 
 // ---- kernel attributes, set once ---------------------------------------------

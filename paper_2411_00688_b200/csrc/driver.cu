@@ -8,9 +8,7 @@
 // per outer iteration without any host synchronisation.  With use_graph the
 // whole launch sequence is captured into one CUDA graph first (a 256^2 FGP
 // iteration is only a few microseconds of GPU work, so launch cost matters).
-#include <chrono>
 #include <climits>
-#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -36,17 +34,16 @@ int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
 bool cluster_shape_ok(int H, int W);
 int cluster_count();
 int sm_prepare();
-int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const int32_t* asg_off,
-           const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
-           const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
-           double gamma, double hc, double pg, double step, const float* betas, int32_t* bad,
-           const ChunkSync& cs, cudaStream_t st);
+int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const WorkQueue& wq,
+           int n_workers, const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K,
+           int n_inner, int accelerated, int nonneg, double weight, double gamma, double hc,
+           double pg, double step, const float* betas, int32_t* bad, const ChunkSync& cs,
+           bool after_clusters, cudaStream_t st);
 int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
-                const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
-                const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
-                int nonneg, double weight, double gamma, double hc, double pg, double step,
-                const float* betas, int32_t* bad, const ChunkSync& cs, volatile int* started,
-                int seq, cudaStream_t st);
+                const WorkQueue& wq, int G, const int32_t* ev_off, const int32_t* ev_k,
+                const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg,
+                double weight, double gamma, double hc, double pg, double step,
+                const float* betas, int32_t* bad, const ChunkSync& cs, cudaStream_t st);
 int fgp2d_run(int dtype, const void* x, int64_t xps, void* q, int64_t qps, const int32_t* active,
               int n_active, double weight, const double* wts, int rep_all, const uint8_t* rep,
               int H, int W, int n_inner, int accelerated, int nonneg, double step,
@@ -165,10 +162,11 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   }
   const size_t x_bytes = (size_t)n * HW * (dto == PSB_F32 ? 4 : 8);
   // Cluster path schedule: every problem's coin-fired iterations (CSR), its
-  // re-projection flag, and problems assigned to the resident clusters
-  // longest-first (a prox call costs n_inner cluster iterations, a skip
-  // iteration next to nothing).
-  std::vector<int32_t> ev_off, ev_k, asg_off, asg, sw_off, sw;
+  // re-projection flag, and the claim order of the device work queue
+  // (common.cuh): by input chunk, then longest first (a prox call costs
+  // n_inner cluster iterations, a skip iteration next to nothing).
+  std::vector<int32_t> ev_off, ev_k, order;
+  std::vector<float> qcost, qsuffix;
   std::vector<uint8_t> rep_p;
   std::vector<float> beta_f;
   int G = 0, NW = 0;
@@ -185,53 +183,31 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
         if (fill[i] == ev_off[i]) rep_p[i] = rep[e];
         ev_k[fill[i]++] = k;
       }
-    G = (int)std::min<int64_t>(n, cluster_count());
     // SMs the clusters leave idle run fgp_sm_run_kernel (one problem per SM,
-    // L2-resident) on a second stream.  The split is a static cost model --
-    // an SM worker needs ~ratio times a cluster's time per prox call -- so
-    // the kernel that runs a problem never depends on timing.  (Not inside a
-    // captured graph: there the two launches have no placement order, and the
-    // SM workers could take the GPC space the clusters need.)
+    // L2-resident), launched as a programmatic dependent of the cluster
+    // kernel so it is placed only after every cluster is resident.  (Not
+    // inside a captured graph, and not for fp64 outer state.)  Test hooks:
+    // PSB_NO_SMWORK=1 runs clusters only, PSB_SM_ONLY=1 SM workers only.
     const char* no_sm = std::getenv("PSB_NO_SMWORK");
-    const char* ratio_env = std::getenv("PSB_SM_RATIO");
-    const double ratio = ratio_env ? std::atof(ratio_env) : 21.0;
-    if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1') && ratio > 0)
+    const char* sm_only = std::getenv("PSB_SM_ONLY");
+    const bool only_sm = sm_only && sm_only[0] == '1' && dto == PSB_F32 && !use_graph;
+    G = only_sm ? 0 : (int)std::min<int64_t>(n, cluster_count());
+    if (only_sm)
+      NW = (int)std::min<int64_t>(n, sm_count());
+    else if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1'))
       NW = std::max(0, sm_count() - G * 16);
-    std::vector<int32_t> order(n);
+    auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
+    order.resize(n);
     for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
+    const int64_t chunk = cs.ready ? cs.chunk : n;
     std::stable_sort(order.begin(), order.end(), [&](int32_t u, int32_t v) {
-      return ev_off[u + 1] - ev_off[u] > ev_off[v + 1] - ev_off[v];
+      if (u / chunk != v / chunk) return u / chunk < v / chunk;
+      return cost(u) > cost(v);
     });
-    // longest first onto the machine (G clusters, NW SM workers) that would
-    // finish it earliest
-    std::vector<double> load(G + NW, 0.0);
-    std::vector<std::vector<int32_t>> bins(G + NW);
-    for (int32_t i : order) {
-      const double c = (double)(ev_off[i + 1] - ev_off[i]) * n_inner + 1e-3 * K;
-      int best = 0;
-      double bt = 0.0;
-      for (int mch = 0; mch < G + NW; ++mch) {
-        const double t = load[mch] + (mch < G ? c : c * ratio);
-        if (mch == 0 || t < bt) best = mch, bt = t;
-      }
-      load[best] = bt;
-      bins[best].push_back(i);
-    }
-    if (cs.ready)  // each machine takes its problems in input-chunk order
-      for (auto& bin : bins)
-        std::stable_sort(bin.begin(), bin.end(),
-                         [&](int32_t u, int32_t v) { return u / cs.chunk < v / cs.chunk; });
-    asg_off.assign(G + 1, 0);
-    asg.reserve(n);
-    for (int c = 0; c < G; ++c) {
-      asg.insert(asg.end(), bins[c].begin(), bins[c].end());
-      asg_off[c + 1] = (int32_t)asg.size();
-    }
-    sw_off.assign(NW + 1, 0);
-    for (int w = 0; w < NW; ++w) {
-      sw.insert(sw.end(), bins[G + w].begin(), bins[G + w].end());
-      sw_off[w + 1] = (int32_t)sw.size();
-    }
+    qcost.resize(n);
+    qsuffix.assign(n + 1, 0.0f);
+    for (int64_t i = 0; i < n; ++i) qcost[i] = cost(order[i]);
+    for (int64_t i = n - 1; i >= 0; --i) qsuffix[i] = qsuffix[i + 1] + qcost[i];
     beta_f.resize(n_inner);
     for (int i = 0; i < n_inner; ++i) beta_f[i] = (float)beta[i];
   }
@@ -249,18 +225,19 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   const size_t o_coins = use_cluster ? 0 : put(coins_host, (size_t)K * n);
   const size_t o_act = use_cluster ? 0 : put(act.data(), act.size() * sizeof(int32_t));
   const size_t o_rep = use_cluster ? 0 : put(rep.data(), rep.size());
-  size_t o_evo = 0, o_evk = 0, o_repp = 0, o_asgo = 0, o_asg = 0, o_beta = 0, o_swo = 0, o_sw = 0;
+  size_t o_evo = 0, o_evk = 0, o_repp = 0, o_beta = 0, o_head = 0, o_stats = 0, o_order = 0,
+         o_cost = 0, o_suffix = 0;
   if (use_cluster) {
     o_evo = put(ev_off.data(), ev_off.size() * sizeof(int32_t));
     o_evk = put(ev_k.data(), ev_k.size() * sizeof(int32_t));
     o_repp = put(rep_p.data(), rep_p.size());
-    o_asgo = put(asg_off.data(), asg_off.size() * sizeof(int32_t));
-    o_asg = put(asg.data(), asg.size() * sizeof(int32_t));
     o_beta = put(beta_f.data(), beta_f.size() * sizeof(float));
-    if (NW > 0) {
-      o_swo = put(sw_off.data(), sw_off.size() * sizeof(int32_t));
-      o_sw = put(sw.data(), sw.size() * sizeof(int32_t));
-    }
+    const uint64_t zeros[5] = {0, 0, 0, 0, 0};  // queue head + rate statistics start at 0
+    o_head = put(zeros, sizeof(uint32_t));
+    o_stats = put(zeros, 4 * sizeof(uint64_t));
+    o_order = put(order.data(), order.size() * sizeof(int32_t));
+    o_cost = put(qcost.data(), qcost.size() * sizeof(float));
+    o_suffix = put(qsuffix.data(), qsuffix.size() * sizeof(float));
   }
   DevBuf d_sched;
   d_sched.st = user_stream;
@@ -308,90 +285,52 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   if (use_cluster) {  // the whole segment in one launch
     if (fgp_time) cudaEventRecordWithFlags(fev[0], st, rec_flags);
     const float* beta_d = reinterpret_cast<const float*>(dev + o_beta);
-    // SM workers go on a second stream, forked BEFORE the cluster launch (so
-    // they do not wait for it) and launched AFTER it (so the clusters are
-    // placed first), joined back into `st`
-    cudaStream_t st2 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    if (NW > 0) {
-      rc = sm_prepare();
-      if (rc == PSB_OK && (cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess))
-        rc = fail(PSB_ERR_CUDA, "sm workers: stream/event creation failed");
-      if (rc == PSB_OK) {
-        cudaEventRecord(fork, st);
-        cudaStreamWaitEvent(st2, fork, 0);
-      }
-    }
-    // With SM workers, the clusters must be resident before the workers'
-    // CTAs reach the SMs (a worker CTA placed first can take GPC space a
-    // 16-CTA cluster needs, measured: 6 instead of 7 clusters, -14 %).  Each
-    // cluster reports its start in host-mapped memory; the workers are
-    // launched once all have started (or after 200 ms, e.g. on a busy GPU).
-    static volatile int* started_h = nullptr;
-    static int* started_d = nullptr;
-    static int seq = 0;
-    if (NW > 0 && rc == PSB_OK && started_h == nullptr) {
-      void* hp = nullptr;
-      if (cudaHostAlloc(&hp, 64 * sizeof(int), cudaHostAllocMapped) == cudaSuccess &&
-          cudaHostGetDevicePointer(reinterpret_cast<void**>(&started_d), hp, 0) == cudaSuccess) {
-        started_h = static_cast<volatile int*>(hp);
-        for (int i = 0; i < 64; ++i) started_h[i] = 0;
-      }
-    }
-    const bool gate = NW > 0 && started_h != nullptr && G <= 64;
-    if (gate) ++seq;
-    if (rc == PSB_OK)
-      rc = cluster_run(dto, x, b, h, q, qps, i32(o_asgo), i32(o_asg), G, i32(o_evo), i32(o_evk),
-                       dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg,
-                       0.125, beta_d, bad, cs, gate ? started_d : nullptr, seq, st);
-    if (gate && rc == PSB_OK) {
-      const auto t_beg = std::chrono::steady_clock::now();
-      const auto t_end = t_beg + std::chrono::milliseconds(200);
-      int ok = 0;
-      for (;;) {
-        ok = 0;
-        for (int c = 0; c < G; ++c) ok += started_h[c] == seq;
-        if (ok == G || std::chrono::steady_clock::now() > t_end) break;
-        std::this_thread::yield();
-      }
-      const char* dg = std::getenv("PSB_DEBUG_GATE");
-      if (dg && dg[0] == '1')
-        fprintf(stderr, "[psb gate] %d of %d clusters started after %.3f ms\n", ok, G,
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_beg)
-                    .count());
-    }
+    WorkQueue wq;
+    wq.head = reinterpret_cast<unsigned int*>(dev + o_head);
+    wq.stats = reinterpret_cast<unsigned long long*>(dev + o_stats);
+    wq.order = i32(o_order);
+    wq.cost = reinterpret_cast<const float*>(dev + o_cost);
+    wq.suffix = reinterpret_cast<const float*>(dev + o_suffix);
+    wq.n = (int)n;
+    wq.clusters = G;
+    if (NW > 0) rc = sm_prepare();  // module loaded before the clusters launch
     // (never in a streamed run: the synchronisation below would wait for
     // kernels that wait for copies the caller has not enqueued yet)
     const char* dbg = cs.ready ? nullptr : std::getenv("PSB_DEBUG_TIMES");
-    cudaEvent_t d0 = nullptr, d1 = nullptr, d2 = nullptr;
+    cudaEvent_t d0 = nullptr, d1 = nullptr;
     if (dbg) {
       cudaEventCreate(&d0);
       cudaEventCreate(&d1);
-      cudaEventCreate(&d2);
-      cudaEventRecord(d1, st);
+      cudaEventRecord(d0, st);
     }
-    if (NW > 0 && st2 && fork && join) {
-      if (dbg) cudaEventRecord(d0, st2);
-      if (rc == PSB_OK)
-        rc = sm_run(x, b, h, q, qps, z, i32(o_swo), i32(o_sw), NW, i32(o_evo), i32(o_evk),
-                    dev + o_repp, K, n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
-                    beta_d, bad, cs, st2);
-      if (dbg) cudaEventRecord(d2, st2);
-      cudaEventRecord(join, st2);
-      cudaStreamWaitEvent(st, join, 0);
-    }
+    if (rc == PSB_OK)
+      rc = cluster_run(dto, x, b, h, q, qps, wq, G, i32(o_evo), i32(o_evk), dev + o_repp, K,
+                       n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d, bad,
+                       cs, st);
+    // The SM workers follow in the same stream as a programmatic dependent:
+    // they are placed once every cluster CTA has started (griddepcontrol.
+    // launch_dependents at the top of the cluster kernel), so they can never
+    // take GPC space a 16-CTA cluster needs, and they finish only after the
+    // clusters (griddepcontrol.wait at their end) -- no host gate, no second
+    // stream.
+    if (NW > 0 && rc == PSB_OK)
+      rc = sm_run(x, b, h, q, qps, z, wq, NW, i32(o_evo), i32(o_evk), dev + o_repp, K, n_inner,
+                  accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d, bad, cs, G > 0, st);
     if (dbg) {
+      cudaEventRecord(d1, st);
       cudaDeviceSynchronize();
-      float a = 0, b2 = 0;
-      cudaEventElapsedTime(&a, fev.empty() ? d1 : fev[0], d1);
-      if (NW > 0) cudaEventElapsedTime(&b2, d0, d2);
-      fprintf(stderr, "[psb] clusters %d: %.3f ms; sm workers %d: %.3f ms\n", G, a, NW, b2);
+      float a = 0;
+      cudaEventElapsedTime(&a, d0, d1);
+      uint64_t stt[4] = {0, 0, 0, 0};
+      cudaMemcpy(stt, wq.stats, sizeof(stt), cudaMemcpyDeviceToHost);
+      fprintf(stderr,
+              "[psb] %d clusters + %d sm workers: %.3f ms; cluster %.1f ns/unit over %llu units, "
+              "worker %.1f ns/unit over %llu units\n",
+              G, NW, a, stt[1] ? (double)stt[0] / stt[1] : 0.0, (unsigned long long)stt[1],
+              stt[3] ? (double)stt[2] / stt[3] : 0.0, (unsigned long long)stt[3]);
+      cudaEventDestroy(d0);
+      cudaEventDestroy(d1);
     }
-    if (fork) cudaEventDestroy(fork);
-    if (join) cudaEventDestroy(join);
-    if (st2) cudaStreamDestroy(st2);  // released by the runtime once its work completes
     if (fgp_time) cudaEventRecordWithFlags(fev[1], st, rec_flags);
   }
   for (int k = 0; k < K && rc == PSB_OK && !use_cluster; ++k) {

@@ -505,8 +505,7 @@ struct SmRunArgs {
   float* q;
   int64_t qps;
   float* z;                // prox-input scratch, (N, H, W)
-  const int32_t* asg_off;  // [n_workers + 1]
-  const int32_t* asg;
+  WorkQueue wq;            // problems claimed dynamically (common.cuh)
   const int32_t* ev_off;
   const int32_t* ev_k;
   const uint8_t* rep;
@@ -554,7 +553,8 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
   const int r0 = warp * RS, r1 = r0 + RS;
   const int c0 = lane * 4;  // half A; half B at c0 + W/2
   const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
-  const float2 st2 = make_float2(step, step), w2 = make_float2(w, w);
+  const float wr = w * kBallShrink;  // (common.cuh)
+  const float2 st2 = make_float2(step, step), w2 = make_float2(wr, wr);
   struct Raw {
     float4 ky[2], kx[2], my[2], mx[2], zz[2];
   };
@@ -587,8 +587,8 @@ __device__ __forceinline__ void sm_fgp_iter(const float* __restrict__ z, const f
       float2 ky = (P & 1) ? hi(R.ky[P >> 1]) : lo(R.ky[P >> 1]);
       float2 kx = (P & 1) ? hi(R.kx[P >> 1]) : lo(R.kx[P >> 1]);
       if constexpr (rp) {
-        const float sx = fminf(1.f, w * sm_rsq(fmaf(ky.x, ky.x, kx.x * kx.x)));
-        const float sy = fminf(1.f, w * sm_rsq(fmaf(ky.y, ky.y, kx.y * kx.y)));
+        const float sx = fminf(1.f, wr * sm_rsq(fmaf(ky.x, ky.x, kx.x * kx.x)));
+        const float sy = fminf(1.f, wr * sm_rsq(fmaf(ky.y, ky.y, kx.y * kx.y)));
         ky = make_float2(ky.x * sx, ky.y * sy);
         kx = make_float2(kx.x * sx, kx.y * sy);
       }
@@ -697,8 +697,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
   constexpr int NV = (int)(HW / 4);
   const int tid = threadIdx.x;
   const float g = a.gamma;
-  for (int ai = a.asg_off[blockIdx.x]; ai < a.asg_off[blockIdx.x + 1]; ++ai) {
-    const int p = a.asg[ai];
+  __shared__ int s_pos;
+  for (;;) {
+    if (tid == 0) s_pos = wq_claim_worker(a.wq);
+    __syncthreads();
+    const int pos = s_pos;
+    if (pos < 0) break;
+    const int p = a.wq.order[pos];
     float* xp = a.x + (int64_t)p * HW;
     const float* bp = a.b + (int64_t)p * HW;
     float* hp = a.h + (int64_t)p * HW;
@@ -709,6 +714,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
       if (tid == 0) chunk_wait(a.cs, p);
       __syncthreads();
     }
+    const uint64_t t_claim = gtimer_ns();
     int kbad = 0x7fffffff;
     int kprev = -1;
     for (int e = e0; e < e1; ++e) {
@@ -818,8 +824,12 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
     }
     if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
     chunk_done(a.cs, p, 16, tid == 0);
+    if (tid == 0) wq_record(a.wq, 1, pos, t_claim);
     __syncthreads();
   }
+  // launched as a programmatic dependent of the cluster run: finish only after
+  // it (the stream's later work is then ordered after both kernels)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 template <class T, int V>
@@ -1071,16 +1081,27 @@ int sm_prepare() {
   return PSB_OK;
 }
 
-int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const int32_t* asg_off,
-           const int32_t* asg, int n_workers, const int32_t* ev_off, const int32_t* ev_k,
-           const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg, double weight,
-           double gamma, double hc, double pg, double step, const float* betas, int32_t* bad,
-           const ChunkSync& cs, cudaStream_t st) {
+int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const WorkQueue& wq,
+           int n_workers, const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K,
+           int n_inner, int accelerated, int nonneg, double weight, double gamma, double hc,
+           double pg, double step, const float* betas, int32_t* bad, const ChunkSync& cs,
+           bool after_clusters, cudaStream_t st) {
   if (n_workers <= 0) return PSB_OK;
-  SmRunArgs a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, (float*)z, asg_off, asg,
-              ev_off, ev_k, rep, K, n_inner, accelerated, nonneg, (float)weight, (float)gamma,
-              (float)hc, (float)pg, (float)step, bad, betas, cs};
-  fgp_sm_run_kernel<<<n_workers, SM_THREADS, 0, st>>>(a);
+  SmRunArgs a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, (float*)z, wq, ev_off, ev_k,
+              rep, K, n_inner, accelerated, nonneg, (float)weight, (float)gamma, (float)hc,
+              (float)pg, (float)step, bad, betas, cs};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n_workers);
+  cfg.blockDim = dim3(SM_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  if (after_clusters) {  // placed once every cluster CTA is resident (see fgp_cluster.cu)
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  PSB_CUDA(cudaLaunchKernelEx(&cfg, fgp_sm_run_kernel, a));
   PSB_LAUNCHED("fgp_sm_run");
   return PSB_OK;
 }

@@ -31,6 +31,8 @@
 // between iterations disappear.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -57,8 +59,7 @@ struct RunArgs {
   TO* h;
   float* q;               // warm-start slot 0 of problem p: q + p*qps (channel stride CH*CW)
   int64_t qps;
-  const int32_t* asg_off;  // [G + 1]: cluster c runs problems asg[asg_off[c] .. asg_off[c+1])
-  const int32_t* asg;
+  WorkQueue wq;            // problems claimed dynamically (common.cuh)
   const int32_t* ev_off;   // [n + 1]: problem p's coin-fired iterations ev_k[ev_off[p] ..]
   const int32_t* ev_k;     // ascending, 0 .. K-1 (this run segment)
   const uint8_t* rep;      // [n]: re-project the warm start at the first prox call (tv.py:68-69)
@@ -71,8 +72,6 @@ struct RunArgs {
   int32_t* bad;            // [n]: first non-finite iteration (atomicMin)
   const float* betas;      // device table beta[0..n_inner-1]
   ChunkSync cs;            // optional input/output chunk streaming (common.cuh)
-  volatile int* started;   // optional, host-mapped: started[c] = seq once cluster c runs
-  int seq;
 };
 
 template <class TO>
@@ -91,7 +90,11 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
 }
 template <class T>
 __device__ __forceinline__ T dsmem_ld(uint32_t addr) {
-  if constexpr (sizeof(T) == 8) {
+  if constexpr (std::is_same<T, int>::value) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+  } else if constexpr (sizeof(T) == 8) {
     double v;
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
     return v;
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   __shared__ __align__(16) float2 s_edge_yx[CRG][NP + 1][CWARPS_ROW + 1];
   __shared__ __align__(16) float2 s_edge_u[CRG][NP][CWARPS_ROW];
   __shared__ float s_beta[kMaxBetas];
+  __shared__ int s_next[2];  // rank 0: the claimed queue position, by problem parity
   // the problem's x, b, h rows of this CTA, resident for the whole problem
   extern __shared__ __align__(16) unsigned char stage_raw[];
   TO* sx = reinterpret_cast<TO*>(stage_raw);  // [SR][CW]
@@ -230,10 +234,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     mbar_init(&mb_up[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (a.started && cr == 0 && tid == 0) {  // tell the host this cluster is resident
-    a.started[blockIdx.x / CCL] = a.seq;
-    __threadfence_system();
-  }
+  // every CTA of this grid is resident: the SM-worker kernel (launched after
+  // this one as a programmatic dependent) may now be placed on the SMs the
+  // clusters left, without taking GPC space a cluster needs
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   cluster_arrive();  // every CTA's mbarriers exist before anyone pushes
   cluster_wait();
   // Round r carries the rows published after iteration r-1 (round 0: the warm
@@ -276,9 +280,17 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
   const bool last_col = lane == 31 && wc == CWARPS_ROW - 1;  // owns global column W-1
 
-  const int c = blockIdx.x / CCL;
-  for (int ai = a.asg_off[c]; ai < a.asg_off[c + 1]; ++ai) {
-  const int p = a.asg[ai];
+  const uint32_t next_remote = dsmem_addr(&s_next[0], 0);
+  uint64_t t_claim = 0;
+  for (unsigned pj = 0;; ++pj) {
+  // rank 0 claims the next problem; everyone reads it after the barrier
+  // (slot pj & 1 was last read before the previous problem's barrier)
+  if (cr == 0 && tid == 0) s_next[pj & 1] = wq_claim(a.wq);
+  cluster_arrive();
+  cluster_wait();
+  const int pos = dsmem_ld<int>(next_remote + 4u * (pj & 1));
+  if (pos < 0) break;
+  const int p = a.wq.order[pos];
   TO* xp = a.x + (int64_t)p * HW;
   const TO* bp = a.b + (int64_t)p * HW;
   TO* hp = a.h + (int64_t)p * HW;
@@ -288,6 +300,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     if (tid == 0) chunk_wait(a.cs, p);
     __syncthreads();
   }
+  if (cr == 0 && tid == 0) t_claim = gtimer_ns();
   // stage this CTA's rows of x, b, h (each thread its own elements; the CTA
   // above reads row 0 after the next cluster barrier)
 #pragma unroll
@@ -488,7 +501,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       u_below[0] = ub.x;
       u_below[1] = ub.y;
     }
-    const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(w, w);
+    const float wr = w * kBallShrink;  // (common.cuh)
+    const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(wr, wr);
 #pragma unroll
     for (int k = 0; k < 2; ++k)
 #pragma unroll
@@ -607,6 +621,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   }
   if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
   chunk_done(a.cs, p, 1, tid == 0);  // this CTA's rows of the problem are written
+  if (cr == 0 && tid == 0) wq_record(a.wq, 0, pos, t_claim);
   // The next problem's staging may overwrite row 0 of this CTA only after the
   // CTA above has read it: it did so in the prologue of this problem's last
   // prox call, before its first push of that call, which this CTA waited for.
@@ -657,22 +672,21 @@ static int launch_run(const RunArgs<TO>& a, int G, int dto, cudaStream_t st) {
 }
 
 int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
-                const int32_t* asg_off, const int32_t* asg, int G, const int32_t* ev_off,
-                const int32_t* ev_k, const uint8_t* rep, int K, int n_inner, int accelerated,
-                int nonneg, double weight, double gamma, double hc, double pg, double step,
-                const float* betas, int32_t* bad, const ChunkSync& cs, volatile int* started,
-                int seq, cudaStream_t st) {
+                const WorkQueue& wq, int G, const int32_t* ev_off, const int32_t* ev_k,
+                const uint8_t* rep, int K, int n_inner, int accelerated, int nonneg,
+                double weight, double gamma, double hc, double pg, double step,
+                const float* betas, int32_t* bad, const ChunkSync& cs, cudaStream_t st) {
   if (G <= 0) return PSB_OK;
   if (dto == PSB_F32) {
-    RunArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, asg_off, asg, ev_off,
-                     ev_k, rep, K, n_inner, accelerated, (float)weight, (float)gamma, (float)hc,
-                     (float)pg, (float)step, bad, betas, cs, started, seq};
+    RunArgs<float> a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, wq, ev_off, ev_k, rep,
+                     K, n_inner, accelerated, (float)weight, (float)gamma, (float)hc, (float)pg,
+                     (float)step, bad, betas, cs};
     return nonneg ? launch_run<float, true>(a, G, dto, st) : launch_run<float, false>(a, G, dto, st);
   }
   if (dto == PSB_F64) {
-    RunArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, asg_off, asg,
-                      ev_off, ev_k, rep, K, n_inner, accelerated, (float)weight, gamma, hc, pg,
-                      (float)step, bad, betas, cs, started, seq};
+    RunArgs<double> a{(double*)x, (const double*)b, (double*)h, (float*)q, qps, wq, ev_off, ev_k,
+                      rep, K, n_inner, accelerated, (float)weight, gamma, hc, pg, (float)step, bad,
+                      betas, cs};
     return nonneg ? launch_run<double, true>(a, G, dto, st) : launch_run<double, false>(a, G, dto, st);
   }
   return fail(PSB_ERR_VALUE, "cluster run: unknown dtype");

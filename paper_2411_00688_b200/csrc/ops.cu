@@ -116,6 +116,18 @@ __global__ void fidprox_kernel(const T* __restrict__ v, T t, const T* __restrict
   }
 }
 
+// prox of 0.5||z - b||^2 with step t at x: (x + t b) / (1 + t)  (proximal.py:44-55)
+template <class T>
+__global__ void prox_l2_fid_kernel(const T* __restrict__ x, T t, const T* __restrict__ t_arr,
+                                   const T* __restrict__ b, T* __restrict__ out, int64_t count) {
+  using A = Ar<T>;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T ti = t_arr ? t_arr[i] : t;
+    out[i] = A::div(A::add(x[i], A::mul(ti, b[i])), A::add(T(1), ti));
+  }
+}
+
 // 1 / max(x, floor)  (diagonal_steps, solvers.py:212-224)
 template <class T>
 __global__ void recip_floor_kernel(const T* __restrict__ x, T fl, T* __restrict__ out,
@@ -256,6 +268,15 @@ int psb_fidprox(int dtype, const void* v, double t, const void* t_arr, const voi
   auto st = psb::as_stream(stream);
   PSB_DISPATCH("fidprox", psb::fidprox_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
                               (const T*)v, (T)t, (const T*)t_arr, (const T*)b, (T*)out, count));
+}
+
+int psb_prox_l2_fidelity(int dtype, const void* x, double t, const void* t_arr, const void* b,
+                         void* out, int64_t count, void* stream) {
+  if (count == 0) return PSB_OK;
+  auto st = psb::as_stream(stream);
+  PSB_DISPATCH("prox_l2_fidelity",
+               psb::prox_l2_fid_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
+                   (const T*)x, (T)t, (const T*)t_arr, (const T*)b, (T*)out, count));
 }
 
 int psb_recip_floor(int dtype, const void* x, double floor_, void* out, int64_t count,

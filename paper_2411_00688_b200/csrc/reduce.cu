@@ -33,7 +33,7 @@ __device__ __forceinline__ double block_sum(double v) {
   return r;  // valid in thread 0
 }
 
-enum Op { SUMSQ = 0, DOT = 1, NONFINITE = 2, BELOW = 3 };
+enum Op { SUMSQ = 0, DOT = 1, NONFINITE = 2, BELOW = 3, OUTSIDE_BALL = 4 };
 
 template <class T, int OP>
 __global__ void __launch_bounds__(RB) elem_reduce(const T* __restrict__ a, const T* __restrict__ b,
@@ -54,6 +54,9 @@ __global__ void __launch_bounds__(RB) elem_reduce(const T* __restrict__ a, const
       acc += av * (double)bp[i];
     } else if (OP == NONFINITE) {
       acc += isfinite(av) ? 0.0 : 1.0;
+    } else if (OP == OUTSIDE_BALL) {  // tv.py:98-100: sqrt(q0^2 + q1^2) > thr, in fp64
+      const double bv = (double)bp[i];
+      acc += sqrt(av * av + bv * bv) > thr ? 1.0 : 0.0;
     } else {
       acc += av < thr ? 1.0 : 0.0;
     }
@@ -162,6 +165,13 @@ int psb_sumsq_bcast(int dtype, const void* a, const void* b, int64_t n, int64_t 
 int psb_count_below(int dtype, const void* a, int64_t n, int64_t len, double thresh, double* out,
                     void* stream) {
   return psb::elem<psb::BELOW>(dtype, a, nullptr, n, len, out, psb::as_stream(stream), len, thresh);
+}
+
+int psb_count_outside_ball(int dtype, const void* q, int64_t len, double r, double* out,
+                           void* stream) {
+  const size_t es = dtype == PSB_F32 ? 4 : 8;
+  const void* q1 = static_cast<const char*>(q) + es * (size_t)len;
+  return psb::elem<psb::OUTSIDE_BALL>(dtype, q, q1, 1, len, out, psb::as_stream(stream), 0, r);
 }
 
 int psb_count_nonfinite(int dtype, const void* a, int64_t count, double* out, void* stream) {

@@ -76,10 +76,18 @@ def div_dev(q):
     return d
 
 
-grad_forward = _wrap(grad_dev)
-grad_forward.__doc__ = "Neumann forward differences, (2, H, W) (operators.py:44-57)."
-divergence = _wrap(div_dev)
-divergence.__doc__ = "Discrete divergence = -grad^T (operators.py:60-71)."
+def grad_forward(u):
+    """Neumann forward differences, (2, H, W) (operators.py:44-57)."""
+    return AR.like(grad_dev(AR.to_dev(u, _fdtype(u))), u)
+
+
+def divergence(q):
+    """Discrete divergence = -grad^T (operators.py:60-71)."""
+    return AR.like(div_dev(AR.to_dev(q, _fdtype(q))), q)
+
+
+grad_forward.device_fn = grad_dev
+divergence.device_fn = div_dev
 
 
 def _absgrad_dev(u):

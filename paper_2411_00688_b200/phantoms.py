@@ -107,3 +107,41 @@ def config4_batch(indices, n=256, dtype=np.float32):
     for j, i in enumerate(indices):
         out[j] = config4_problem(int(i), n)[1]
     return out
+
+
+def config2_data(seed=0, n=512):
+    """512^2 deblurring: 10 seeded random ellipses, 9x9 sigma=2 periodic blur
+    (D2), noise 0.01.  Returns (truth, blurred-noisy b, kernel weights)."""
+    truth = random_shapes((n, n), 10, np.random.default_rng(seed), rects=False)
+    w = _gaussian_weights(9, 2.0)
+    return truth, add_noise(_conv_periodic(truth, w), 0.01, seed), w
+
+
+def config3_phantom(seed=0, n=512):
+    """512^2 Shepp-Logan-style CT phantom of 10 seeded ellipses (config 3)."""
+    return shepp_like(n, 10, np.random.default_rng(seed))
+
+
+def config3_noisy(sino, seed=0):
+    """Config-3 sinogram noise: sigma = 1 % of max(A u_true) (D10)."""
+    return add_noise(sino, 0.01 * float(np.max(sino)), seed)
+
+
+def _gaussian_weights(size, sigma):
+    """Normalised size x size Gaussian (the reference's gaussian_kernel,
+    operators.py:131-137)."""
+    ax = np.arange(size) - size // 2
+    g = np.exp(-(ax[:, None] ** 2 + ax[None, :] ** 2) / (2.0 * sigma**2))
+    return g / g.sum()
+
+
+def _conv_periodic(u, w):
+    """Periodic 2-D convolution in the reference's tap order
+    (operators.py:149-158): out = sum_a sum_b w[a,b] roll(u, (a-c, b-c))."""
+    c = w.shape[0] // 2
+    out = np.zeros_like(u)
+    for a in range(w.shape[0]):
+        for b in range(w.shape[1]):
+            if w[a, b] != 0.0:
+                out += w[a, b] * np.roll(u, (a - c, b - c), axis=(0, 1))
+    return out

@@ -2,6 +2,7 @@
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _arrays as AR
@@ -32,6 +33,28 @@ def project_nonneg(u):
     out = torch.empty_like(t)
     L.call("psb_project_nonneg", L.dcode(t.dtype), L.ptr(t), L.ptr(out), t.numel(), L.stream())
     return AR.like(out, u)
+
+
+def prox_l2_fidelity(x, b, tau):
+    """Prox of z -> 0.5||z - b||^2 at x with step tau: (x + tau b)/(1 + tau);
+    tau a scalar or an array of x's shape (diagonal steps) (proximal.py:44-55)."""
+    xt = AR.to_dev(x, _dt(x))
+    bt = AR.to_dev(b, xt.dtype)
+    if tuple(xt.shape) != tuple(bt.shape):
+        raise ValueError(f"prox_l2_fidelity: shape mismatch {tuple(xt.shape)} vs {tuple(bt.shape)}")
+    out = torch.empty_like(xt)
+    if np.isscalar(tau):
+        if tau == 0.0:
+            return AR.like(xt.clone(), x)
+        L.call("psb_prox_l2_fidelity", L.dcode(xt.dtype), L.ptr(xt), float(tau), None, L.ptr(bt),
+               L.ptr(out), xt.numel(), L.stream())
+    else:
+        ta = AR.to_dev(tau, xt.dtype)
+        if tuple(ta.shape) != tuple(xt.shape):
+            raise ValueError(f"prox_l2_fidelity: tau shape {tuple(ta.shape)} vs {tuple(xt.shape)}")
+        L.call("psb_prox_l2_fidelity", L.dcode(xt.dtype), L.ptr(xt), 0.0, L.ptr(ta), L.ptr(bt),
+               L.ptr(out), xt.numel(), L.stream())
+    return AR.like(out, x)
 
 
 def prox_zero(x):

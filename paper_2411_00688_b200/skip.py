@@ -51,11 +51,11 @@ class SkipConfig:
         return (self.stream().random(iters) < self.p).astype(np.uint8)
 
 
-def optimal_probability(mu, L_):
+def optimal_probability(mu, L):  # noqa: N803  (the reference's parameter name)
     """sqrt(mu / L) (skip.py:31-35)."""
-    if mu <= 0 or L_ <= 0 or mu > L_:
-        raise ValueError(f"optimal_probability: need 0 < mu <= L, got mu={mu}, L={L_}")
-    return float(np.sqrt(mu / L_))
+    if mu <= 0 or L <= 0 or mu > L:
+        raise ValueError(f"optimal_probability: need 0 < mu <= L, got mu={mu}, L={L}")
+    return float(np.sqrt(mu / L))
 
 
 def _finish_passive(log, coins, elapsed, base_inner, inner_iters):

@@ -110,12 +110,18 @@ def tv_prox(x, weight, state: TvProxState):
 
 def dual_gap_rof(x, q, weight):
     """ROF prox duality gap at u = x + div q (tv.py:92-105)."""
-    qd = AR.to_dev(q, torch.float64)
+    qd = AR.to_dev(q, q.dtype if isinstance(q, torch.Tensor) and q.dtype == torch.float32
+                   else torch.float64)
     xd = AR.to_dev(x, torch.float64)
-    mag = torch.sqrt(qd[0] ** 2 + qd[1] ** 2)  # feasibility check only (validation, not compute)
-    if bool((mag > weight * (1.0 + 1e-10)).any()):
+    if qd.dim() != 3 or qd.shape[0] != 2:
+        raise ValueError(f"dual_gap_rof: expected a (2, H, W) field, got {tuple(qd.shape)}")
+    qd = qd.contiguous()
+    cnt = torch.empty(1, dtype=torch.float64, device="cuda")
+    L.call("psb_count_outside_ball", L.dcode(qd.dtype), L.ptr(qd), qd[0].numel(),
+           float(weight * (1.0 + 1e-10)), L.ptr(cnt), L.stream())
+    if float(cnt.item()) > 0:
         raise ValueError("dual_gap_rof: q lies outside the feasibility ball")
-    dq = div_dev(qd)
+    dq = div_dev(qd.double())
     u = T.lincomb(1.0, xd, 1.0, dq)
     primal = 0.5 * float(T.reduce_sumsq(u, xd)) + weight * tv_value(u)
     dual = -0.5 * float(T.reduce_sumsq(T.lincomb(1.0, dq, 1.0, xd))) + 0.5 * float(T.reduce_sumsq(xd))

@@ -116,15 +116,16 @@ def test_cluster_occupancy_query():
     print("max active 16-CTA clusters:", n.value)
 
 
-@pytest.mark.parametrize("ratio", ["2", "18"])
-def test_cluster_with_sm_workers_matches_streaming_and_oracle(ratio, monkeypatch):
+@pytest.mark.parametrize("mode", ["queue", "sm_only"])
+def test_cluster_with_sm_workers_matches_streaming_and_oracle(mode, monkeypatch):
     """More problems than resident clusters: the SMs the clusters leave run
-    fgp_sm_run_kernel on a share of the problems (PSB_SM_RATIO = 2 hands them
-    most of the batch)."""
+    fgp_sm_run_kernel, both kernels claiming from one device work queue
+    ("queue"); PSB_SM_ONLY=1 hands the whole batch to the SM workers."""
     idx = np.arange(40) * 97 % 4096
     b = _batch(idx)
     K, inner, p = 30, 10, 0.2
-    monkeypatch.setenv("PSB_SM_RATIO", ratio)
+    if mode == "sm_only":
+        monkeypatch.setenv("PSB_SM_ONLY", "1")
     xc, cc = _run(b, idx, K, inner, p, stream_only=False)
     xs, cs = _run(b, idx, K, inner, p, stream_only=True)
     np.testing.assert_array_equal(cc, cs)
@@ -142,7 +143,7 @@ def test_sm_workers_warm_restart_and_divergence(monkeypatch):
     idx = np.arange(20)
     b = _batch(idx).astype(np.float32)
     b[13, 5, 5] = np.nan
-    monkeypatch.setenv("PSB_SM_RATIO", "2")
+    monkeypatch.setenv("PSB_SM_ONLY", "1")
     s = psb.BatchedTvDenoise(b, 0.1, 8, precision="fp32")
     s.run_proxskip(psb.coin_table(0.3, idx, 12), 1.0, 0.3)
     s.run_proxskip(psb.coin_table(0.3, idx + 500, 9), 1.0, 0.3)
@@ -196,19 +197,22 @@ def test_host_inputs_equal_device_run(host):
 
 
 def test_sm_worker_and_cluster_kernels_bitwise_equal(monkeypatch):
-    """The same problems run entirely on the SM workers (PSB_SM_RATIO tiny)
-    and entirely on the clusters (PSB_NO_SMWORK=1) give identical bits: which
-    kernel the static split picks never changes a result."""
+    """The same problems run entirely on the SM workers (PSB_SM_ONLY=1), on
+    the clusters only (PSB_NO_SMWORK=1) and through the shared work queue give
+    identical bits: which kernel claims a problem never changes a result."""
     idx = np.arange(24) * 53 % 4096
     b = _batch(idx).astype(np.float32)
     K, inner, p = 25, 7, 0.3
-    monkeypatch.setenv("PSB_SM_RATIO", "0.001")
+    xq, cq = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
+    monkeypatch.setenv("PSB_SM_ONLY", "1")
     xs, cs = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
-    monkeypatch.delenv("PSB_SM_RATIO")
+    monkeypatch.delenv("PSB_SM_ONLY")
     monkeypatch.setenv("PSB_NO_SMWORK", "1")
     xc, cc = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, p, idx, K, inner)
     np.testing.assert_array_equal(cs, cc)
+    np.testing.assert_array_equal(cq, cc)
     assert torch.equal(xs, xc)
+    assert torch.equal(xq, xc)
 
 
 @pytest.mark.parametrize("host", ["numpy", "numpy64", "pinned", "pageable"])
@@ -251,3 +255,36 @@ def test_streamed_run_into_caller_buffer(pinned):
     with pytest.raises(ValueError):
         psb.run_proxskip_batched(src, 0.1, p, idx, K, inner, chunk=16,
                                  out=torch.empty((3, 256, 256), dtype=torch.float32))
+
+
+_SERIAL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2411_00688_b200 as psb
+from paper_2411_00688_b200 import phantoms
+idx = np.arange(48) * 37 % 4096
+b = np.stack([phantoms.config4_problem(int(i))[1] for i in idx]).astype(np.float32)
+x_ref, c_ref = psb.run_proxskip_batched(torch.from_numpy(b).cuda(), 0.1, 0.3, idx, 12, 5)
+x, c = psb.run_proxskip_batched(torch.from_numpy(b).pin_memory(), 0.1, 0.3, idx, 12, 5, chunk=8)
+assert np.array_equal(c, c_ref)
+assert np.array_equal(x.numpy(), x_ref.cpu().numpy())
+print("serial ok")
+"""
+
+
+def test_streamed_run_under_serialised_execution():
+    """CUDA_LAUNCH_BLOCKING=1 serialises every launch: the streamed host-input
+    path must not depend on the copy stream running beside the waiting run
+    kernels (its H2D copies are enqueued before the run), so it completes
+    quickly with the resident run's bits instead of timing out."""
+    import subprocess
+    import sys
+    import time
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    t0 = time.time()
+    r = subprocess.run([sys.executable, "-c", _SERIAL_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "serial ok" in r.stdout
+    assert time.time() - t0 < 120  # no 20 s device-wait timeouts
