@@ -1,20 +1,27 @@
-"""Benchmark: BASELINE config 4 -- batched ProxSkip TV denoising.
+"""Benchmark: BASELINE config 4 (headline) and config 5 (sub-record).
 
-4096 independent 256x256 problems (seeded random-ellipse/rectangle phantoms,
-noise sigma_i ~ U[0.05, 0.15], alpha = 0.1, gamma = 1, p = 0.1 per-problem
-Philox coin streams, FGP-50 inner iterations), sharded over N GPUs (one
-process per GPU, contiguous problem blocks, no collective on the data path).
-A "step" is one outer ProxSkip iteration over the whole batch.  The native
-driver runs the K timed steps as ONE segment: fgp_cluster_run_kernel (16-CTA
-clusters, one problem each at a time, all of its coin-fired prox calls back to
-back with the FGP state in registers) plus fgp_sm_run_kernel on the SMs the
-clusters leave, each problem advanced by exactly K outer iterations.  W
-warm-up steps are outer iterations 0..W-1 of the run; the K timed steps are
-iterations W..W+K-1 (default W+K = 300, the full config-4 run).
+Config 4 -- 4096 independent 256x256 problems (seeded random-ellipse/rectangle
+phantoms, noise sigma_i ~ U[0.05, 0.15], alpha = 0.1, gamma = 1, p = 0.1
+per-problem Philox coin streams, FGP-50 inner iterations), sharded over N
+GPUs (one process per GPU, contiguous problem blocks, no collective on the
+data path).  A "step" is one outer ProxSkip iteration over the whole batch.
+The native driver runs the K timed steps as ONE segment: fgp_cluster_run_kernel
+(16-CTA clusters, one problem at a time, all of its coin-fired prox calls back
+to back with the FGP state in registers) plus fgp_sm_run_kernel on the SMs the
+clusters leave, both claiming problems from one device work queue; each problem
+is advanced by exactly K outer iterations.  W warm-up steps are outer
+iterations 0..W-1 of the run; the K timed steps are iterations W..W+K-1
+(default W+K = 300, the full config-4 run).
+
+Config 5 -- one 1024^3 volume (50 seeded ellipsoids + noise 0.1, alpha = 0.08,
+p = 0.1, 200 outer x FGP-20, dual step 1/12), z-slab decomposed over the N
+ranks with the peer-memory halo exchange (volume3d.PeerExchange over NVLink);
+W warm-up outer iterations, then the remaining 200 - W timed.  Reported in the
+same JSON line under "config5".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Prints one JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+Prints one JSON line (rank 0).  DESIGN.md "Measurement" documents every field.
 """
 
 from __future__ import annotations
@@ -39,34 +46,39 @@ P = 0.1
 INNER = 50
 E2E_REPS = 3
 RUN_LEN = 300
-BYTES_FGP_MOM = 28   # fp32 per pixel-iteration: x + q_k(2) + q_{k-1}(2) read, q_{k+1}(2) write
+HW = SIDE * SIDE
+U_TOL, OBJ_TOL = 1e-4, 1e-5          # BASELINE.json north_star parity tolerance
+FLOPS_PER_PXIT = 23                   # FGP step, FMA = 2
+BYTES_FGP_MOM = 28    # fp32 per pixel-iteration: x + q_k(2) + q_{k-1}(2) read, q_{k+1}(2) write
 BYTES_FGP_FIRST = 20  # first inner iteration (beta = 0): no q_{k-1} read
-CLUSTER = os.environ.get("PSB_NO_CLUSTER", "0") != "1"
-if CLUSTER:
-    KERNEL = ("fgp_cluster_run_kernel<float> (+ fgp_sm_run_kernel on the 36 SMs the clusters "
-              "leave): the whole timed run segment in ONE launch each; a 16-CTA cluster runs its "
-              "problems' coin-fired prox calls back to back (skips + 50 FGP iterations + post) "
-              "with z, q in registers and x, b, h in shared memory; the 28 B/px-iter of the "
-              "streaming formulation stay on-chip / in L2, so frac > 1 is expected; time = both "
-              "kernels (events around the pair)")
-    # ncu dram__bytes_read.sum + dram__bytes_write.sum of fgp_cluster_run_kernel per launch,
-    # per problem in the launch (profiles/r01_launches_bench_run.csv)
-    TRAFFIC_PER_PROBLEM_LAUNCH = 2.4e6
-else:
-    KERNEL = "fgp2d_iter_kernel<float,4> (streaming, one launch per inner iteration)"
-    # profiles/r01_fgp2d_iter_ncu_details.csv: 795 MB per launch at 422 problems
-    TRAFFIC_PER_PROBLEM = 795e6 / 422 * INNER
+# config 5
+SIDE5 = int(os.environ.get("PSB_BENCH_SIDE5", "1024"))
+ALPHA5, P5, ITERS5, INNER5 = 0.08, 0.1, 200, 20
+BYTES3_MOM, BYTES3_FIRST = 40, 28     # 3-D FGP bytes per voxel-iteration
+COUNTERS = os.path.join(ROOT, "profiles", "r02_run_kernel_counters.json")
 METRIC = "ProxSkip TV outer iter/s (config 4: 4096 x 256^2 batch, FGP-50, p=0.1)"
 WORKLOAD = "config4: batched ProxSkip TV denoising, 4096 x 256x256, alpha=0.1, p=0.1, FGP-50"
+UNIT = "outer-iter/s (4096-problem batch)"
+CLUSTER = os.environ.get("PSB_NO_CLUSTER", "0") != "1"
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _counters():
+    """Per-cost-unit instruction and DRAM counts of the two run kernels, from
+    the committed ncu capture (tools/run_kernel_counters.py)."""
+    try:
+        with open(COUNTERS) as f:
+            return json.load(f)
+    except Exception:
+        return None
 
 
 def _gen(idx):
@@ -84,53 +96,99 @@ def make_inputs(indices, procs=None):
 
 # -- CPU baseline: the oracle (numpy restatement of the reference) -------------
 
-def _oracle_problem(arg):
-    """Run problem i's outer loop with the oracle; time iterations W..W+K-1."""
-    i, warm, steps = arg
+def _oracle_problems(arg):
+    """Run problems ``ids`` with the oracle for W+K outer iterations each;
+    time iterations W..W+K-1.  Returns [(i, seconds, final x (float32),
+    prox calls, objective)]."""
+    ids, warm, steps = arg
     from oracle import imgskip_cpu as oc
     from paper_2411_00688_b200 import phantoms
-    b = phantoms.config4_problem(int(i), SIDE)[1]
-    pr = oc.make_recon(oc.identity_op(b.shape), b, ALPHA, inner=INNER)
-    marks = {}
+    out = []
+    for i in ids:
+        # the GPU arm holds b in float32 (phantoms.config4_batch): same input here
+        b = phantoms.config4_problem(int(i), SIDE)[1].astype(np.float32).astype(np.float64)
+        pr = oc.make_recon(oc.identity_op(b.shape), b, ALPHA, inner=INNER)
+        marks = {}
 
-    def obs(k, x, n, th):
-        if k == warm - 1:
-            marks["t0"] = time.perf_counter()
+        def obs(k, x, n, th):
+            if k == warm - 1:
+                marks["t0"] = time.perf_counter()
 
-    t_begin = time.perf_counter()
-    oc.proxskip(pr.grad, pr.prox, np.zeros_like(b), None, 1.0, P, int(i), warm + steps, obs)
-    return time.perf_counter() - marks.get("t0", t_begin)
+        t_begin = time.perf_counter()
+        x, _, n_prox, _ = oc.proxskip(pr.grad, pr.prox, np.zeros_like(b), None, 1.0, P, int(i),
+                                      warm + steps, obs)
+        dt = time.perf_counter() - marks.get("t0", t_begin)
+        out.append((int(i), dt, x.astype(np.float32), int(n_prox), float(oc.tv_objective(x, pr))))
+    return out
 
 
 def cpu_baseline(warm, steps, procs):
     """The reference algorithm (oracle port, float64 numpy) on ``procs`` host
-    processes, one config-4 problem each (indices spread over 0..4095),
-    timing the same outer iterations W..W+K-1 as the GPU arm.  Returns the
-    rate scaled to the 4096-problem batch (batch outer iter/s)."""
-    idx = np.linspace(0, N_PROBLEMS - 1, procs).astype(int)
+    processes x ``per`` problems each (indices spread evenly over 0..4095),
+    timing the same outer iterations W..W+K-1 as the GPU arm.  The batch rate
+    is extrapolated from the MEAN per-problem time: the 4096-problem batch is
+    4096 x mean core-seconds per step window, spread over ``procs`` cores.
+    ``per`` keeps the sample at ~10-25 s of wall time."""
+    est = max(steps, 1) * 0.0085  # s per problem for K steps (SURVEY §6: 2.54 s / 300)
+    per = int(np.clip(round(20.0 / est), 2, 16))
+    n = procs * per
+    idx = np.linspace(0, N_PROBLEMS - 1, n).astype(int)
     env = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")}
     os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = "1"
     try:
         with mp.get_context("fork").Pool(procs) as pool:
-            per = pool.map(_oracle_problem, [(int(i), warm, steps) for i in idx])
+            parts = pool.map(_oracle_problems,
+                             [(list(idx[r::procs]), warm, steps) for r in range(procs)])
     finally:
         for k, v in env.items():
             if v is None:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    wall = max(per)
-    value = procs * steps / wall / N_PROBLEMS
-    return {
-        "value": value,
-        "unit": "outer-iter/s (4096-problem batch)",
-        "cores": procs,
-        "kind": "port",
-        "sample": f"{procs} of 4096 problems (one per host process, 1 thread each), outer "
-                  f"iterations {warm}..{warm + steps - 1} of the {RUN_LEN}-iteration run, "
-                  f"oracle/imgskip_cpu.py float64 numpy; slowest process {wall:.2f}s; "
-                  f"rate scaled x{procs}/4096 to the full batch",
+    res = sorted((r for part in parts for r in part), key=lambda r: r[0])
+    per_t = np.array([r[1] for r in res])
+    mean_t = float(per_t.mean())
+    value = procs * steps / (N_PROBLEMS * mean_t)
+    info = {
+        "value": value, "unit": UNIT, "cores": procs, "kind": "port",
+        "sample": f"{n} of 4096 problems ({procs} host processes x {per}, 1 thread each), outer "
+                  f"iterations {warm}..{warm + steps - 1} of each problem's run, "
+                  f"oracle/imgskip_cpu.py float64 numpy; mean {mean_t:.3f} s / problem "
+                  f"(max/mean {per_t.max() / mean_t:.2f}); batch rate = {procs} cores x {steps} "
+                  f"steps / (4096 x mean), i.e. extrapolated x{N_PROBLEMS / n:.0f} from the sample",
     }
+    return info, res
+
+
+def cpu_baseline_3d(side=256):
+    """Config-5 CPU reference path: the 3-D oracle (oracle/tv3d_cpu.py, float64
+    numpy, 1 core) timed at side^3 -- two FGP inner iterations and one skip
+    iteration -- and extrapolated to 1024^3 (x (1024/side)^3) and to the
+    config's mix per outer iteration: p x 20 inner iterations + 1 outer
+    update."""
+    from oracle import tv3d_cpu as o3
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal((side, side, side))
+    x = np.zeros_like(b)
+    h = np.zeros_like(b)
+    st = o3.Fgp3State.zeros(b.shape, 2)
+    t0 = time.perf_counter()
+    o3.fgp_prox3(b, 0.8, st)
+    t_inner = (time.perf_counter() - t0) / 2
+    t0 = time.perf_counter()
+    g = x - b                                    # skip.py:65-74 with A = I, gamma = 1
+    xhat = x - 1.0 * g + 1.0 * h
+    x_new = xhat
+    h = h + (P5 / 1.0) * (x_new - xhat)
+    t_skip = time.perf_counter() - t0
+    scale = (1024 / side) ** 3
+    t_outer = scale * (P5 * INNER5 * t_inner + t_skip)
+    return {"value": 1.0 / t_outer, "unit": "outer-iter/s (1024^3 volume)", "cores": 1,
+            "kind": "port",
+            "sample": f"oracle/tv3d_cpu.py float64 numpy at {side}^3: {t_inner:.2f} s per FGP "
+                      f"inner iteration, {t_skip:.2f} s per outer update; extrapolated x{scale:.0f} "
+                      f"to 1024^3 and to {P5} x {INNER5} inner iterations per outer iteration "
+                      f"(a full 1024^3 CPU run is hours and > 62 GB at fp64)"}
 
 
 # -- clocks sampled during the timed region -------------------------------------
@@ -143,23 +201,24 @@ class Clocks:
     def __init__(self, dev):
         self.dev = dev
         self.proc = None
+        self.out = ""
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
         if self.proc is not None:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                out, _ = self.proc.communicate(timeout=5)
+                self.out += out or ""
             except Exception:
                 self.proc.kill()
 
@@ -179,25 +238,62 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-# -- arms -------------------------------------------------------------------------
+# -- distributed plumbing ------------------------------------------------------
 
-def dist_init():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+class Dist:
+    """One process per GPU (torchrun).  PSB_BENCH_BACKEND=gloo and
+    PSB_BENCH_SHARE_DEVICE=1 run every rank on cuda:0 (a protocol check on a
+    one-GPU box, never a measurement)."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = os.environ.get("PSB_BENCH_BACKEND", "nccl")
+        self.share = os.environ.get("PSB_BENCH_SHARE_DEVICE", "0") == "1"
+        self.dev = 0 if self.share else self.local
+
+    def init(self):
+        import torch
+        torch.cuda.set_device(self.dev)
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(self.backend)
+
+    def reduce(self, vals, op="max"):
+        """Element-wise max / sum of a list of floats over ranks."""
+        if self.world == 1:
+            return list(vals)
+        import torch
         import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=None)
-    return world, rank, local
+        t = torch.tensor(list(vals), dtype=torch.float64,
+                         device="cuda" if self.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return [float(v) for v in t.cpu()]
 
+    def barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def close(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+# -- arms -------------------------------------------------------------------------
 
 def run_reference(args):
     """The reference's algorithm on the host cores (rank 0 only under torchrun)."""
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
     procs = os.cpu_count() or 1
-    r = cpu_baseline(args.warmup, args.steps, procs)
+    r, _ = cpu_baseline(args.warmup, args.steps, procs)
     v = r["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": r["unit"],
@@ -214,142 +310,279 @@ def run_reference(args):
     return 0
 
 
-def run_gpu(args):
+def _roofline4(units, t, n_pxit, sm_mhz, sms):
+    """Config-4 run kernels: the FGP inner loop runs from registers / shared
+    memory / L2, so neither HBM nor FP32 is the limiter -- instruction issue
+    is (ncu).  achieved = live executed warp instructions (cost units each
+    kernel finished, this run's queue statistics, x the per-unit instruction
+    count of that kernel from the committed ncu capture) / live time; peak =
+    4 warp instructions per cycle per SM x SMs x SM clock."""
+    cnt = _counters()
+    hbm_peak, hbm_kind = _peaks()
+    f_ghz = (sm_mhz or 1965.0) / 1000.0
+    fp32_peak = sms * 128 * 2 * f_ghz / 1000.0  # TFLOP/s
+    fp32 = FLOPS_PER_PXIT * n_pxit / t / 1e12
+    model_gbs = n_pxit * BYTES_FGP_MOM / t / 1e9
+    out = {"bound": "issue", "unit": "Gwarp-inst/s", "achieved": None, "peak": sms * 4 * f_ghz,
+           "frac": None, "traffic": None,
+           "kernel": "fgp_cluster_run_kernel<float> + fgp_sm_run_kernel (one launch each for the "
+                     "K timed steps, problems claimed from one device work queue)",
+           "fp32": {"achieved_tflops": fp32, "peak_tflops": fp32_peak, "frac": fp32 / fp32_peak,
+                    "flops_per_unit": f"{FLOPS_PER_PXIT} per pixel-iteration (FMA = 2)"},
+           "hbm_model": {"achieved_gbs": model_gbs, "peak_gbs": hbm_peak,
+                         "frac": model_gbs / hbm_peak, "peak_source": hbm_kind,
+                         "note": "28 B/pixel-iteration of the streaming formulation (SURVEY "
+                                 "8(d)); these bytes stay on chip in the run kernels, so this "
+                                 "ratio is the speed-up over an HBM-bound streaming FGP, not a "
+                                 "bound"},
+           "peak_source": f"4 warp-inst/cycle/SM x {sms} SMs x {f_ghz * 1000:.0f} MHz "
+                          "(median SM clock under load)"}
+    if cnt is not None:
+        inst = units[0] * cnt["cluster"]["inst_per_unit"] + units[1] * cnt["sm_worker"]["inst_per_unit"]
+        dram = units[0] * cnt["cluster"]["dram_bytes_per_unit"] + \
+            units[1] * cnt["sm_worker"]["dram_bytes_per_unit"]
+        out["achieved"] = inst / t / 1e9
+        out["frac"] = out["achieved"] / out["peak"]
+        out["traffic"] = dram
+        out["counters"] = {"source": os.path.relpath(COUNTERS, ROOT),
+                           "cluster_units": units[0], "sm_worker_units": units[1],
+                           "issue_active_pct_ncu": cnt.get("issue_active_pct")}
+    return out
+
+
+def run_config4(args, D, dev):
     import torch
     import paper_2411_00688_b200 as psb
+    from paper_2411_00688_b200 import _lib as L
     from paper_2411_00688_b200 import batched
 
-    world, rank, local = dist_init()
-    torch.cuda.set_device(local)
-    dev = torch.cuda.current_device()
-    idx = batched.shard_indices(N_PROBLEMS, rank, world)
+    idx = batched.shard_indices(N_PROBLEMS, D.rank, D.world)
     b_host = make_inputs(idx)
     coins = batched.coin_table(P, idx, args.warmup + args.steps)
     solver = psb.BatchedTvDenoise(b_host, ALPHA, INNER, precision="fp32")
-    HW = SIDE * SIDE
-
-    def sync_all():
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-            torch.cuda.synchronize()
 
     # ---- device-resident throughput: warm-up steps, then K timed steps ----
     solver.reset()
     solver.run_proxskip(coins[:args.warmup], 1.0, P)
     fgp_t = np.zeros(args.steps)
-    sync_all()
+    D.barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(dev) as clk:
         e0.record(stream)
         solver.run_proxskip(coins[args.warmup:], 1.0, P, fgp_time=fgp_t)
         e1.record(stream)
-        sync_all()
+        D.barrier()
     solver.check_finite()
     t_local = e0.elapsed_time(e1) / 1000.0
+    qs = (L.C.c_double * 4)()
+    L.call("psb_queue_stats", qs)
+    units = (float(qs[1]), float(qs[3]))
     timed = coins[args.warmup:]
     active = timed.sum(axis=1)                       # coin-fired problems per step
-    fgp_bytes = active * HW * (BYTES_FGP_FIRST + (INNER - 1) * BYTES_FGP_MOM)
-    n_fired_steps = int(np.count_nonzero(active))
+    n_pxit = float(active.sum()) * INNER * HW
     if CLUSTER:
         # one fgp_cluster_run_kernel launch for the K timed steps, plus one
         # fgp_sm_run_kernel launch on the SMs the clusters leave
         launches = 1 + (os.environ.get("PSB_NO_SMWORK", "0") != "1")
     else:
-        launches = args.steps + n_fired_steps * (INNER + 1)
-    stats = np.array([t_local, fgp_t.sum(), float(fgp_bytes.sum()), float(active.sum())])
-    if world > 1:
-        import torch.distributed as dist
-        ts = torch.tensor(stats, device="cuda", dtype=torch.float64)
-        tmax = ts.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ts, op=dist.ReduceOp.SUM)
-        t_job = float(tmax[0])
-        sums = ts.cpu().numpy()
-    else:
-        t_job = t_local
-        sums = stats
+        launches = args.steps + int(np.count_nonzero(active)) * (INNER + 1)
+    t_job, = D.reduce([t_local], "max")
+    n_pxit_all, = D.reduce([n_pxit], "sum")
     value = args.steps / t_job                        # batch outer iterations / s
-    inner_rate = sums[3] * INNER / t_job               # problem-inner-iterations / s
-    fgp_time_local = fgp_t.sum()
-    achieved = fgp_bytes.sum() / fgp_time_local / 1e9 if fgp_time_local > 0 else 0.0
-    peak, peak_kind = _peaks()
+    inner_rate = n_pxit_all / HW / t_job              # problem-inner-iterations / s
+    clocks = clk.summary()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    roof = _roofline4(units, t_local, n_pxit, clocks["sm_mhz"], sms)
+    x_resident = solver.x.cpu().numpy()
 
     # ---- e2e: the public API with host buffers, copies inside the region ----
-    # (the device-resident solver above is released first; its blocks stay in
-    # torch's caching allocator, as in any process that has run a solve before)
     del solver
     b_pin = torch.from_numpy(b_host).pin_memory()
-    # untimed warm-up of the e2e path on a slice (its one-time host set-up:
-    # pinned staging buffers, copy stream, stream-memop entry points)
-    # The result lands in a page-locked host buffer allocated up front, like
-    # the pinned input (a pageable one costs a staged copy plus first-touch
-    # page faults on 1 GB inside the timed call: e2e varied 290-500 it/s).
+    # the result lands in a page-locked buffer allocated up front, like the
+    # pinned input (a pageable 1 GB result costs a staged copy plus first-touch
+    # page faults inside the timed call)
     x_pin = torch.empty(b_pin.shape, dtype=torch.float32).pin_memory()
     nw = min(len(idx), 512)
     psb.run_proxskip_batched(b_pin[:nw], ALPHA, P, idx[:nw], args.warmup, INNER, precision="fp32",
-                             out=x_pin[:nw])
-    # Three timed calls, the median reported: the device part of a call is
-    # stable to 0.1 ms (CUDA-event timeline of the copies, PSB_DEBUG_E2E=1),
-    # but the host wall clock of a single call sometimes stalls for 0.1-1 s
-    # (seen in ~1 of 8 calls, with the device timeline unchanged).
+                             out=x_pin[:nw])  # untimed: one-time host set-up of the path
     e2e_samples = []
     for _ in range(E2E_REPS):
-        sync_all()
+        D.barrier()
         t0 = time.perf_counter()
         x_e2e, counts = psb.run_proxskip_batched(b_pin, ALPHA, P, idx, args.warmup + args.steps,
                                                  INNER, precision="fp32", out=x_pin)
         assert x_e2e.device.type == "cpu"
         e2e_samples.append(time.perf_counter() - t0)
-    t_e2e_local = float(np.median(e2e_samples))
-    if world > 1:
-        tt = torch.tensor([t_e2e_local], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_e2e = float(tt[0])
-    else:
-        t_e2e = t_e2e_local
+    t_e2e, = D.reduce([float(np.median(e2e_samples))], "max")
     n_e2e = args.warmup + args.steps
-    h2d = b_host.nbytes * world / n_e2e
-    d2h = x_e2e.numel() * x_e2e.element_size() * world / n_e2e
+    h2d = b_host.nbytes * D.world / n_e2e
+    d2h = x_e2e.numel() * x_e2e.element_size() * D.world / n_e2e
+    x_e2e = x_e2e.numpy()
+    same = bool(np.array_equal(x_e2e, x_resident))
 
-    if rank != 0:
+    rec = {
+        "value": value, "t_job": t_job, "inner_rate": inner_rate, "roofline": roof,
+        "launches": launches, "clocks": clocks,
+        "e2e": {"value": n_e2e / t_e2e, "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, pinned "
+                        "host out; W+K outer iterations from a cold start per call)",
+                "timing": f"host wall clock per call, median of {E2E_REPS} calls (max over ranks)",
+                "samples_s": [round(t, 5) for t in e2e_samples]},
+        "idx": idx, "x_e2e": x_e2e, "counts": counts, "resident_equals_e2e": same,
+    }
+    return rec
+
+
+def parity_block(rec, ref, iters):
+    """The e2e run's final x (W+K outer iterations from cold) against the
+    oracle's run of the same problems (the cpu_baseline leg), on u and on the
+    objective, plus prox-call counts."""
+    import paper_2411_00688_b200 as psb
+    pos = {int(i): j for j, i in enumerate(rec["idx"])}
+    worst_u = worst_o = 0.0
+    counts_ok = True
+    for i, _, xr, n_prox, obj_r in ref:
+        j = pos[i]
+        x = rec["x_e2e"][j].astype(np.float64)
+        xr = xr.astype(np.float64)
+        worst_u = max(worst_u, float(np.linalg.norm(x - xr) / np.linalg.norm(xr)))
+        b = rec["b_host"][j].astype(np.float64)
+        prob = psb.build_tv_recon(psb.identity_map(b.shape), b, ALPHA, inner_budget=INNER)
+        obj = psb.objective_tv(x, prob)
+        worst_o = max(worst_o, abs(obj - obj_r) / abs(obj_r))
+        counts_ok &= int(rec["counts"][j]) == n_prox
+    return {"problems": len(ref), "outer_iterations": iters, "max_rel_l2_u": worst_u,
+            "max_rel_obj": worst_o, "prox_counts_equal": bool(counts_ok),
+            "resident_equals_e2e": rec["resident_equals_e2e"],
+            "tolerance": {"rel_l2_u": U_TOL, "rel_obj": OBJ_TOL},
+            "pass": bool(worst_u <= U_TOL and worst_o <= OBJ_TOL and counts_ok),
+            "oracle": "oracle/imgskip_cpu.py (pinned to reference golden vectors, "
+                      "tests/test_oracle_golden.py), same problems as cpu_baseline"}
+
+
+def run_config5(args, D, dev, with_cpu):
+    """Config 5 on the N ranks: one z-slab each, peer-memory halo exchange."""
+    import torch
+    from paper_2411_00688_b200 import SkipConfig, phantoms
+    from paper_2411_00688_b200 import volume3d as v3
+
+    side = SIDE5
+    b = phantoms.config5_volume(side, 0)
+    z0, z1 = v3.slab_bounds(side, D.rank, D.world)
+    slab = v3.Slab3D(b[z0:z1].clone() if D.world > 1 else b, z0, side, ALPHA5, INNER5,
+                     precision="fp32")
+    b_host = b.cpu().pin_memory() if D.world == 1 else None
+    del b
+    ex = v3.PeerExchange.dist(slab, None) if D.world > 1 else None
+    coins = SkipConfig(P5, 0).coins(ITERS5)
+    W = min(args.warmup, ITERS5 - 1)
+    v3.run_proxskip_slabs([slab], coins[:W], gamma=1.0, p=P5, exchange=ex)  # untimed warm-up
+    D.barrier()
+    ev = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        e0.record()
+        v3.run_proxskip_slabs([slab], coins[W:], gamma=1.0, p=P5, exchange=ex, fgp_events=ev)
+        e1.record()
+        D.barrier()
+    t_local = e0.elapsed_time(e1) / 1e3
+    t_fgp = sum(a.elapsed_time(c) for a, c in ev) / 1e3
+    t_job, = D.reduce([t_local], "max")
+    K5 = ITERS5 - W
+    n_prox = int(coins[W:].sum())
+    vox_local = (z1 - z0) * side * side
+    bytes_fgp = n_prox * vox_local * (BYTES3_FIRST + (INNER5 - 1) * BYTES3_MOM)
+    peak, kind = _peaks()
+    achieved = bytes_fgp / t_fgp / 1e9 if t_fgp > 0 else 0.0
+    if ex is not None and hasattr(ex, "close"):
+        ex.close()
+    del slab
+    rec = {
+        "metric": "ProxSkip 3-D TV outer iter/s (config 5: 1024^3, FGP-20, p=0.1)",
+        "value": K5 / t_job, "unit": "outer-iter/s (one volume)", "steps": K5, "warmup": W,
+        "ms_per_step": 1000.0 * t_job / K5, "scaling": "strong", "dtype": "f32",
+        "config": {"workload": "config5: 3-D TV denoising, z-slab decomposed", "side": side,
+                   "alpha": ALPHA5, "p": P5, "inner": INNER5, "outer": ITERS5,
+                   "parallelism": f"z-slab x{D.world}" +
+                                  (" (peer-memory halo exchange)" if D.world > 1 else ""),
+                   "l2": "inputs larger than L2 (56 GB of state)"},
+        "fgp_voxel_iter_per_s": n_prox * INNER5 * side ** 3 / t_job,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "fgp3d_march_kernel<float,4,TMA> (rank 0)",
+                     "bytes_per_unit": "40 B/voxel-iteration (28 B at the first inner iteration),"
+                                       " SURVEY 8(d); x units = the timed prox calls x the slab's "
+                                       "voxels x 20 inner iterations; time = CUDA events around "
+                                       "each FGP inner iteration",
+                     "peak_source": kind},
+        "clocks": clk.summary(),
+    }
+    if D.world == 1:
+        # e2e through the public entry point: host volume in, host x out
+        from paper_2411_00688_b200.volume3d import proxskip_denoise3d
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x_host, _ = proxskip_denoise3d(b_host, ALPHA5, P5, 0, ITERS5, INNER5)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        assert x_host.device.type == "cpu"
+        rec["e2e"] = {"value": ITERS5 / t_e2e, "unit": rec["unit"],
+                      "h2d_bytes_per_step": int(b_host.numel() * 4 / ITERS5),
+                      "d2h_bytes_per_step": int(x_host.numel() * 4 / ITERS5),
+                      "path": "paper_2411_00688_b200.volume3d.proxskip_denoise3d (pinned host "
+                              "volume in, host x out, all 200 outer iterations from cold)"}
+        del x_host
+    if with_cpu:
+        rec["cpu_baseline"] = cpu_baseline_3d()
+    return rec
+
+
+def run_gpu(args):
+    import torch
+    D = Dist()
+    D.init()
+    dev = torch.cuda.current_device()
+    rec = run_config4(args, D, dev)
+    rec["b_host"] = None
+    cpu, parity = None, None
+    if D.rank == 0 and D.world == 1 and not args.no_cpu:
+        cpu, ref = cpu_baseline(args.warmup, args.steps, os.cpu_count() or 1)
+        from paper_2411_00688_b200 import phantoms
+        rec["b_host"] = phantoms.config4_batch(rec["idx"], SIDE)
+        parity = parity_block(rec, ref, args.warmup + args.steps)
+    elif D.rank == 0:
+        parity = {"resident_equals_e2e": rec["resident_equals_e2e"],
+                  "note": "oracle comparison runs at N=1 only (cpu_baseline leg)"}
+    c5 = None
+    if not args.no_config5:
+        torch.cuda.empty_cache()
+        c5 = run_config5(args, D, dev, with_cpu=D.rank == 0 and D.world == 1 and not args.no_cpu)
+    if D.rank != 0:
+        D.close()
         return 0
-    procs = os.cpu_count() or 1
-    cpu = cpu_baseline(args.warmup, args.steps, procs) if (world == 1 and not args.no_cpu) else None
     line = {
-        "metric": METRIC, "value": value, "unit": "outer-iter/s (4096-problem batch)",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * t_job / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": rec["value"], "unit": UNIT,
+        "n_gpus": D.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * rec["t_job"] / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded random-shape phantoms, SURVEY D3; no public dataset)",
         "config": {"workload": WORKLOAD, "problems": N_PROBLEMS, "side": SIDE, "inner": INNER,
-                   "p": P, "alpha": ALPHA, "parallelism": f"problem-shard x{world}",
+                   "p": P, "alpha": ALPHA, "parallelism": f"problem-shard x{D.world}",
                    "l2": "inputs larger than L2 (~10 GB of state per GPU vs 126 MB L2)"},
-        "fgp_inner_iter_per_s": inner_rate,
-        "fgp_mpx_iter_per_s": inner_rate * HW / 1e6,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak,
-                     "traffic": (TRAFFIC_PER_PROBLEM_LAUNCH * len(idx) if CLUSTER else
-                                 TRAFFIC_PER_PROBLEM * float(active.sum()) / max(n_fired_steps, 1)),
-                     "kernel": KERNEL,
-                     "bytes_per_unit": "28 B/pixel-iteration (20 B at the first inner iteration), "
-                                       "SURVEY 8(d); x units = the timed steps' coin-fired "
-                                       "problem-prox calls x 65536 px x 50 inner iterations "
-                                       "(one launch for all of them on the cluster path)",
-                     "peak_source": peak_kind},
+        "fgp_inner_iter_per_s": rec["inner_rate"],
+        "fgp_mpx_iter_per_s": rec["inner_rate"] * HW / 1e6,
+        "roofline": rec["roofline"],
         "cpu_baseline": cpu,
-        "e2e": {"value": n_e2e / t_e2e, "unit": "outer-iter/s (4096-problem batch)",
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, pinned host out)",
-                "timing": f"host wall clock per call, median of {E2E_REPS} calls (max over ranks)",
-                "samples_s": [round(t, 5) for t in e2e_samples]},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "e2e": rec["e2e"],
+        "parity": parity,
+        "gpu_launches": int(rec["launches"]),
+        "clocks": rec["clocks"],
+        "config5": c5,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    D.close()
     return 0
 
 
@@ -359,7 +592,8 @@ def main():
     ap.add_argument("--steps", type=int, default=295)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline / parity legs")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 sub-record")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

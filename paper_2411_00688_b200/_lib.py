@@ -74,6 +74,7 @@ SIGNATURES = {
     "psb_tv2d": [_i32, _vp, _i64, _i32, _i32, _vp, _vp],
     "psb_sumsq_bcast": [_i32, _vp, _vp, _i64, _i64, _vp, _vp],
     "psb_count_below": [_i32, _vp, _i64, _i64, _dbl, _vp, _vp],
+    "psb_queue_stats": [_vp],
     "psb_count_outside_ball": [_i32, _vp, _i64, _dbl, _vp, _vp],
     "psb_count_nonfinite": [_i32, _vp, _i64, _vp, _vp],
     "psb_proxskip_pre": [_i32, _i32, _vp, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _vp,

@@ -91,6 +91,19 @@ struct DevBuf {
 
 }  // namespace
 
+// page-locked copy of the last cluster run's work-queue statistics
+static unsigned long long* queue_stats_host() {
+  static unsigned long long* p = nullptr;
+  if (p == nullptr) {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, 4 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
+      return nullptr;
+    p = static_cast<unsigned long long*>(h);
+    for (int i = 0; i < 4; ++i) p[i] = 0;
+  }
+  return p;
+}
+
 int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* b, void* h, void* z,
                     void* q, int64_t n, int H, int W, const uint8_t* coins_host, int K,
                     double gamma, double p, double alpha, int n_inner, int accelerated, int nonneg,
@@ -192,8 +205,11 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     const char* sm_only = std::getenv("PSB_SM_ONLY");
     const bool only_sm = sm_only && sm_only[0] == '1' && dto == PSB_F32 && !use_graph;
     G = only_sm ? 0 : (int)std::min<int64_t>(n, cluster_count());
-    if (only_sm)
-      NW = (int)std::min<int64_t>(n, sm_count());
+    if (only_sm) {  // PSB_SM_WORKERS caps the worker count (profiling the 36-SM share)
+      const char* nws = std::getenv("PSB_SM_WORKERS");
+      const int cap = nws ? std::max(1, std::atoi(nws)) : sm_count();
+      NW = (int)std::min<int64_t>(n, std::min(cap, sm_count()));
+    }
     else if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1'))
       NW = std::max(0, sm_count() - G * 16);
     auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
@@ -316,6 +332,14 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (NW > 0 && rc == PSB_OK)
       rc = sm_run(x, b, h, q, qps, z, wq, NW, i32(o_evo), i32(o_evk), dev + o_repp, K, n_inner,
                   accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d, bad, cs, G > 0, st);
+    // queue statistics of this run for psb_queue_stats (page-locked copy,
+    // valid once the stream has drained)
+    if (rc == PSB_OK && !use_graph) {
+      unsigned long long* hs = queue_stats_host();
+      if (hs && cudaMemcpyAsync(hs, wq.stats, 4 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(PSB_ERR_CUDA, "queue statistics copy failed");
+    }
     if (dbg) {
       cudaEventRecord(d1, st);
       cudaDeviceSynchronize();
@@ -411,6 +435,13 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
 }
 
 }  // namespace psb
+
+extern "C" int psb_queue_stats(double* out4) {
+  PSB_REQUIRE(out4 != nullptr, "queue_stats: output missing");
+  const unsigned long long* hs = psb::queue_stats_host();
+  for (int i = 0; i < 4; ++i) out4[i] = hs ? (double)hs[i] : 0.0;
+  return PSB_OK;
+}
 
 extern "C" int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void* b,
                                         void* h, void* z, void* q, int64_t n, int H, int W,

@@ -145,3 +145,28 @@ def _conv_periodic(u, w):
             if w[a, b] != 0.0:
                 out += w[a, b] * np.roll(u, (a - c, b - c), axis=(0, 1))
     return out
+
+
+def config5_volume(side=1024, seed=0, device="cuda"):
+    """Config-5 input generated on the device (a 1024^3 volume is 4.3 GB):
+    50 seeded ellipsoids with U[0,1] intensities (numpy ``default_rng(seed)``
+    draws the shapes, as random_ellipsoids) plus N(0, 0.1^2) noise from a
+    seeded torch generator.  Returns a float32 CUDA tensor (D, H, W)."""
+    import torch
+    D = H = W = side
+    vol = torch.zeros((D, H, W), dtype=torch.float32, device=device)
+    rng = np.random.default_rng(seed)
+    ax = (torch.arange(side, device=device, dtype=torch.float32) + 0.5) / side
+    for _ in range(50):
+        c = rng.uniform(0.15, 0.85, size=3)
+        r = rng.uniform(0.04, 0.25, size=3)
+        val = float(rng.uniform(0, 1))
+        z0, z1 = max(0, int((c[0] - r[0]) * D) - 1), min(D, int((c[0] + r[0]) * D) + 2)
+        yy = ((ax - float(c[1])) / float(r[1])) ** 2
+        xx = ((ax - float(c[2])) / float(r[2])) ** 2
+        zz = ((ax[z0:z1] - float(c[0])) / float(r[0])) ** 2
+        m = zz[:, None, None] + yy[None, :, None] + xx[None, None, :] <= 1.0
+        vol[z0:z1][m] = val
+    g = torch.Generator(device=device).manual_seed(seed)
+    vol.add_(torch.randn((D, H, W), generator=g, device=device), alpha=0.1)
+    return vol
