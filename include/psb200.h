@@ -95,6 +95,14 @@ int psb_fidprox(int dtype, const void* v, double t, const void* t_arr, const voi
                 int64_t count, void* stream);
 int psb_recip_floor(int dtype, const void* x, double floor_, void* out, int64_t count,
                     void* stream);
+/* Iteration loops replayed from one captured CUDA graph (no per-iteration
+ * host round trip): psb_mark_nonfinite sets *bad_iter = min(*bad_iter,
+ * *iter_ctr) if x has a non-finite entry (solvers.py:111-113, the 0-based
+ * iteration the reference's DivergenceError names); psb_counter_add adds v
+ * to the device counter. */
+int psb_mark_nonfinite(int dtype, const void* x, int64_t count, int32_t* bad_iter,
+                       const int32_t* iter_ctr, void* stream);
+int psb_counter_add(int32_t* ctr, int v, void* stream);
 /* psb_prox_l2_fidelity: out = (x + t .* b) / (1 + t), t scalar or t_arr per
  * element -- prox_l2_fidelity(x, b, tau), proximal.py:44-55 */
 int psb_prox_l2_fidelity(int dtype, const void* x, double t, const void* t_arr, const void* b,

@@ -58,6 +58,8 @@ SIGNATURES = {
     "psb_fidprox": [_i32, _vp, _dbl, _vp, _vp, _vp, _i64, _vp],
     "psb_recip_floor": [_i32, _vp, _dbl, _vp, _i64, _vp],
     "psb_prox_l2_fidelity": [_i32, _vp, _dbl, _vp, _vp, _vp, _i64, _vp],
+    "psb_mark_nonfinite": [_i32, _vp, _i64, _vp, _vp, _vp],
+    "psb_counter_add": [_vp, _i32, _vp],
     "psb_absgrad2d": [_i32, _vp, _vp, _i32, _i32, _vp],
     "psb_absdiv2d": [_i32, _vp, _vp, _i32, _i32, _vp],
     "psb_fgp2d_iter": [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _dbl, _vp, _i32, _vp, _i32, _i32,

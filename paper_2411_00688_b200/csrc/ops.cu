@@ -116,6 +116,20 @@ __global__ void fidprox_kernel(const T* __restrict__ v, T t, const T* __restrict
   }
 }
 
+// graph-replayed iteration loops: non-finite check against an iteration
+// counter kept in device memory (solvers.py:111-113, first bad k)
+template <class T>
+__global__ void mark_nonfinite_kernel(const T* __restrict__ x, int64_t count,
+                                      int32_t* __restrict__ bad, const int32_t* __restrict__ ctr) {
+  bool hit = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    hit |= !isfinite((double)x[i]);
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicMin(bad, *ctr);
+}
+
+__global__ void counter_add_kernel(int32_t* ctr, int v) { *ctr += v; }
+
 // prox of 0.5||z - b||^2 with step t at x: (x + t b) / (1 + t)  (proximal.py:44-55)
 template <class T>
 __global__ void prox_l2_fid_kernel(const T* __restrict__ x, T t, const T* __restrict__ t_arr,
@@ -268,6 +282,20 @@ int psb_fidprox(int dtype, const void* v, double t, const void* t_arr, const voi
   auto st = psb::as_stream(stream);
   PSB_DISPATCH("fidprox", psb::fidprox_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
                               (const T*)v, (T)t, (const T*)t_arr, (const T*)b, (T*)out, count));
+}
+
+int psb_mark_nonfinite(int dtype, const void* x, int64_t count, int32_t* bad_iter,
+                       const int32_t* iter_ctr, void* stream) {
+  if (count == 0) return PSB_OK;
+  auto st = psb::as_stream(stream);
+  PSB_DISPATCH("mark_nonfinite", psb::mark_nonfinite_kernel<T><<<psb::grid_for(count), 256, 0, st>>>(
+                                     (const T*)x, count, bad_iter, iter_ctr));
+}
+
+int psb_counter_add(int32_t* ctr, int v, void* stream) {
+  psb::counter_add_kernel<<<1, 1, 0, psb::as_stream(stream)>>>(ctr, v);
+  PSB_CUDA(cudaGetLastError());
+  return PSB_OK;
 }
 
 int psb_prox_l2_fidelity(int dtype, const void* x, double t, const void* t_arr, const void* b,

@@ -214,3 +214,40 @@ def test_pdhgskip1_native_driver(gn):
     xstep, _ = psb.run_pdhgskip1(sp, np.zeros((16, 16)), np.zeros(7 * 23 + 512), s, s,
                                  1.0 / p - 1.0, psb.SkipConfig(p, 2), 20, lg)
     np.testing.assert_allclose(x, xstep, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("diag", [True, False])
+def test_pdhg_explicit_blur_graph_replay_equals_stepped(monkeypatch, diag):
+    """PDHG on the explicit blur splitting K = [blur; D] (the deblurring
+    reference-solution path, harness.py:246-251 -> solvers.py:227-234) has no
+    fused kernel: a passive run replays one captured CUDA graph per
+    iteration.  Same kernels, same iterates as the stepped loop, bit for bit;
+    a non-finite iterate raises with the stepped loop's iteration."""
+    from paper_2411_00688_b200 import phantoms
+    _, b, _ = phantoms.config2_data(0, 48)
+    A = psb.blur_map(psb.gaussian_kernel(9, 2.0), b.shape)
+    prob = psb.build_tv_recon(A, b, 0.02, nonneg=True, splitting="explicit", precision="fp64")
+    sp = prob.saddle_problem
+    y0 = np.zeros(48 * 48 * 3)
+    if diag:
+        run = lambda: psb.run_pdhg_preconditioned(sp, 40)  # noqa: E731
+    else:
+        s = 1.0 / np.sqrt(sp.norm_K_sq)
+        run = lambda: psb.run_pdhg(sp, np.zeros((48, 48)), y0, s, s, 40)  # noqa: E731
+    xg, log = run()
+    assert len(log.records) == 40
+    monkeypatch.setenv("PSB_NO_GRAPH_PDHG", "1")
+    xs, _ = run()
+    np.testing.assert_array_equal(xg, xs)
+    # divergence: a NaN in the data poisons the iterate at the first step
+    bad = b.copy()
+    bad[3, 4] = np.nan
+    pb = psb.build_tv_recon(A, bad, 0.02, splitting="explicit", precision="fp64")
+    ks = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PSB_NO_GRAPH_PDHG", flag)
+        with pytest.raises(psb.DivergenceError) as ei:
+            s = 1.0 / np.sqrt(pb.saddle_problem.norm_K_sq)
+            psb.run_pdhg(pb.saddle_problem, np.zeros((48, 48)), y0, s, s, 20)
+        ks.append(ei.value.iteration)
+    assert ks[0] == ks[1]
