@@ -276,6 +276,27 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     }
     return b;
   };
+  // role-specialised halves of push_rows / recv_rows for the inner loop
+  auto push_up = [&](float ty0, float tx0, float ty1, float tx1) {  // top group, has_up
+    const unsigned b = round & 1;
+    st_async_v4(up_rx_remote + 4u * (b * CW * 2 + j0 * 2), ty0, tx0, ty1, tx1, up_mb_remote + 8u * b);
+  };
+  auto push_dn = [&](float by0, float by1) {  // bottom group, has_dn
+    const unsigned b = round & 1;
+    st_async_v2(dn_rx_remote + 4u * (b * CW + j0), by0, by1, dn_mb_remote + 8u * b);
+  };
+  auto recv_up = [&](unsigned r) {  // top group, has_up
+    const unsigned b = r & 1, ph = (r >> 1) & 1;
+    if (arm) mbar_expect_tx(&mb_up[b], BYTES_UP);
+    mbar_wait(&mb_up[b], ph);
+    return b;
+  };
+  auto recv_dn = [&](unsigned r) {  // bottom group, has_dn
+    const unsigned b = r & 1, ph = (r >> 1) & 1;
+    if (arm) mbar_expect_tx(&mb_dn[b], BYTES_DN);
+    mbar_wait(&mb_dn[b], ph);
+    return b;
+  };
   const bool last_row_thread = rg_bot && !has_dn;  // owns global row H-1 (t = CRPT-1)
   const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
   const bool last_col = lane == 31 && wc == CWARPS_ROW - 1;  // owns global column W-1
@@ -376,169 +397,217 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
                            dsmem_ld<TO>(ex_h_remote + k * sizeof(TO)), false);
   }
   const unsigned round0 = round;  // this call's warm-start round
-  push_rows(qky[0][0].x, qkx[0][0].x, qky[1][0].x, qkx[1][0].x, qky[0][1].y, qky[1][1].y);
+  // Halo rows travel as MOMENTUM iterates y (the receiver uses them as they
+  // are): the warm-start round carries y_0 = fma(0, q_0 - q_0, q_0), round
+  // it + 1 (it + 1 < n) carries y_{it+1} = fma(beta_{it+1}, q_{it+1} - q_it,
+  // q_{it+1}) -- the values the owner computes for its own pixels, bit for bit
+  // -- and the last round q_n itself (the finalize reads q_n).
+  {
+    float v[6];
+    const float y0s[6] = {qky[0][0].x, qkx[0][0].x, qky[1][0].x, qkx[1][0].x, qky[0][1].y,
+                          qky[1][1].y};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) v[i] = fmaf(0.f, fmaf(y0s[i], -1.f, y0s[i]), y0s[i]);
+    push_rows(v[0], v[1], v[2], v[3], v[4], v[5]);
+  }
   ++round;
-
-  float up_k[2] = {0.f, 0.f}, up_m[2] = {0.f, 0.f};  // row above, row channel
-  float dn_ky[2] = {0.f, 0.f}, dn_kx[2] = {0.f, 0.f}, dn_my[2] = {0.f, 0.f}, dn_mx[2] = {0.f, 0.f};
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   // Each pixel's arithmetic is the scalar FGP step (each f32x2 lane an IEEE
-  // fp32 op; a - b = fma(b, -1, a)).
-  auto inner = [&](float2(&QKy)[2][NP], float2(&QKx)[2][NP], float2(&QMy)[2][NP],
-                   float2(&QMx)[2][NP], int it) {
-    const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
-    const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
-    float2 yy[2][NP], yx[2][NP];
+  // fp32 op; a - b = fma(b, -1, a)).  ROLE (warp-uniform, fixed per warp):
+  // 0 = top row group (halo row from the CTA above), 1 = middle groups (all
+  // neighbours inside the CTA), 2 = bottom group (halo row from the CTA
+  // below, computes u of that row itself) -- one specialised copy each, so
+  // the middle groups carry no halo code at all.
+  auto run_inner = [&](auto role_tag) {
+    constexpr int ROLE = decltype(role_tag)::value;
+    constexpr bool TOP = ROLE == 0, BOT = ROLE == 2;
+    auto inner = [&](float2(&QKy)[2][NP], float2(&QKx)[2][NP], float2(&QMy)[2][NP],
+                     float2(&QMx)[2][NP], int it) {
+      const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
+      const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
+      float2 yy[2][NP], yx[2][NP];
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int P = 0; P < NP; ++P) {
+          yy[k][P] = __ffma2_rn(b2, __ffma2_rn(QMy[k][P], m1, QKy[k][P]), QKy[k][P]);
+          yx[k][P] = __ffma2_rn(b2, __ffma2_rn(QMx[k][P], m1, QKx[k][P]), QKx[k][P]);
+        }
+      float2 yyA = make_float2(0.f, 0.f);             // TOP: y row above (zeros at row 0)
+      float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
+      if constexpr (TOP) {
+        if (has_up) {
+          const unsigned par = recv_up(round0 + it);
+          yyA = *reinterpret_cast<const float2*>(&rx_up[par][j0]);
+        }
+      }
+      if constexpr (BOT) {
+        if (has_dn) {
+          const unsigned par = recv_dn(round0 + it);
+          const float4 v = *reinterpret_cast<const float4*>(&rx_dn[par][j0][0]);
+          ex_y[0] = v.x, ex_x[0] = v.y, ex_y[1] = v.z, ex_x[1] = v.w;
+          if (j0 > 0) ledge_x = rx_dn[par][j0 - 1][1];
+        }
+      }
+      if constexpr (!BOT) {  // last-row y_y for the group below
+        s_rg_yy[rg][j0] = yy[0][1].y;  // row CRPT-1
+        s_rg_yy[rg][j0 + 1] = yy[1][1].y;
+      }
+      if (lane == 31) {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
+      }
+      __syncthreads();
+      // left neighbours of column 0: shuffles inside the warp, the warp to the
+      // left's last column from shared memory (zeros left of column 0); column
+      // 1's left neighbour is this thread's column 0
+      float2 left[NP];
 #pragma unroll
       for (int P = 0; P < NP; ++P) {
-        yy[k][P] = __ffma2_rn(b2, __ffma2_rn(QMy[k][P], m1, QKy[k][P]), QKy[k][P]);
-        yx[k][P] = __ffma2_rn(b2, __ffma2_rn(QMx[k][P], m1, QKx[k][P]), QKx[k][P]);
+        left[P].x = __shfl_up_sync(0xffffffffu, yx[1][P].x, 1);
+        left[P].y = __shfl_up_sync(0xffffffffu, yx[1][P].y, 1);
       }
-    const unsigned par = recv_rows(round0 + it);
-    float y_up[2] = {0.f, 0.f}, ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f};
-    if (rg_top && has_up) {
-      const float2 v = *reinterpret_cast<const float2*>(&rx_up[par][j0]);
-      const float vv[2] = {v.x, v.y};
+      if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        up_m[k] = it == 0 ? vv[k] : up_k[k];
-        up_k[k] = vv[k];
-        y_up[k] = up_k[k] + beta * (up_k[k] - up_m[k]);
+        for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
       }
-    }
-    if (rg_bot && has_dn) {
-      const float4 v = *reinterpret_cast<const float4*>(&rx_dn[par][j0][0]);
-      const float vy[2] = {v.x, v.z}, vx[2] = {v.y, v.w};
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        dn_my[k] = it == 0 ? vy[k] : dn_ky[k];
-        dn_mx[k] = it == 0 ? vx[k] : dn_kx[k];
-        dn_ky[k] = vy[k];
-        dn_kx[k] = vx[k];
-        ex_y[k] = dn_ky[k] + beta * (dn_ky[k] - dn_my[k]);
-        ex_x[k] = dn_kx[k] + beta * (dn_kx[k] - dn_mx[k]);
+      float yy_above[2];
+      if constexpr (TOP) {
+        yy_above[0] = yyA.x;
+        yy_above[1] = yyA.y;
+      } else {
+        const float2 ya2 = *reinterpret_cast<const float2*>(&s_rg_yy[rg - 1][j0]);
+        yy_above[0] = ya2.x;
+        yy_above[1] = ya2.y;
       }
-    }
-    s_rg_yy[rg][j0] = yy[0][1].y;  // row CRPT-1
-    s_rg_yy[rg][j0 + 1] = yy[1][1].y;
-    if (lane == 31) {
+      float2 u[2][NP];
 #pragma unroll
-      for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
-      s_edge_yx[rg][NP][wc + 1].x = ex_x[1];
-    }
-    __syncthreads();
-    // left neighbours of column 0: shuffles inside the warp, the warp to the
-    // left's last column from shared memory (zeros left of column 0); column
-    // 1's left neighbour is this thread's column 0
-    float2 left[NP];
+      for (int k = 0; k < 2; ++k)
 #pragma unroll
-    for (int P = 0; P < NP; ++P) {
-      left[P].x = __shfl_up_sync(0xffffffffu, yx[1][P].x, 1);
-      left[P].y = __shfl_up_sync(0xffffffffu, yx[1][P].y, 1);
-    }
-    float ledge_x = __shfl_up_sync(0xffffffffu, ex_x[1], 1);
-    if (lane == 0) {
+        for (int P = 0; P < NP; ++P) {
+          // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
+          const float2 ab2 = P == 0 ? make_float2(yy_above[k], yy[k][1].x) : yy[k][0];
+          const float2 l2 = k == 0 ? left[P] : yx[0][P];
+          const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[k][P]), yx[k][P]);
+          const float2 d2 = __ffma2_rn(l2, m1, d1);
+          const float2 v = __fadd2_rn(z[k][P], d2);
+          u[k][P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
+        }
+      float u_below[2];
+      if constexpr (BOT) {
+        if (has_dn) {  // u of the CTA-below's first row, from its y row
 #pragma unroll
-      for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
-      ledge_x = s_edge_yx[rg][NP][wc].x;
-    }
-    const float2 ya2 = rg_top ? make_float2(y_up[0], y_up[1])
-                              : *reinterpret_cast<const float2*>(&s_rg_yy[rg - 1][j0]);
-    const float yy_above[2] = {ya2.x, ya2.y};
-    float2 u[2][NP];
+          for (int k = 0; k < 2; ++k) {
+            const float d = ((ex_y[k] - yy[k][1].y) + ex_x[k]) - (k == 0 ? ledge_x : ex_x[0]);
+            const float v = z_ex[k] + d;
+            u_below[k] = nonneg ? fmaxf(v, 0.f) : v;
+          }
+        } else {  // the global last row: gy = 0 (below := u)
+          u_below[0] = u[0][1].y;
+          u_below[1] = u[1][1].y;
+        }
+      }
+      if constexpr (!TOP) {  // first-row u for the group above
+        s_rg_u[rg][j0] = u[0][0].x;
+        s_rg_u[rg][j0 + 1] = u[1][0].x;
+      }
+      if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+        for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[0][P];
+      }
+      __syncthreads();
+      // right neighbour of column 1: shuffles (lane 31 keeps its own column 1 at
+      // the global last column: gx = 0), the warp to the right's first column
+      // from shared memory; column 0's right neighbour is column 1
+      float2 right[NP];
 #pragma unroll
       for (int P = 0; P < NP; ++P) {
-        // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
-        const float2 ab2 = P == 0 ? make_float2(yy_above[k], yy[k][1].x) : yy[k][0];
-        const float2 l2 = k == 0 ? left[P] : yx[0][P];
-        const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[k][P]), yx[k][P]);
-        const float2 d2 = __ffma2_rn(l2, m1, d1);
-        const float2 v = __fadd2_rn(z[k][P], d2);
-        u[k][P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
+        right[P].x = __shfl_down_sync(0xffffffffu, u[0][P].x, 1);
+        right[P].y = __shfl_down_sync(0xffffffffu, u[0][P].y, 1);
       }
-    float u_ex[2];
+      if (right_fetch) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const float d = ((ex_y[k] - yy[k][1].y) + ex_x[k]) - (k == 0 ? ledge_x : ex_x[0]);
-      const float v = z_ex[k] + d;
-      u_ex[k] = nonneg ? fmaxf(v, 0.f) : v;
-    }
-    s_rg_u[rg][j0] = u[0][0].x;
-    s_rg_u[rg][j0 + 1] = u[1][0].x;
-    if (lane == 0) {
-#pragma unroll
-      for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[0][P];
-    }
-    __syncthreads();
-    // right neighbour of column 1: shuffles (lane 31 keeps its own column 1 at
-    // the global last column: gx = 0), the warp to the right's first column
-    // from shared memory; column 0's right neighbour is column 1
-    float2 right[NP];
-#pragma unroll
-    for (int P = 0; P < NP; ++P) {
-      right[P].x = __shfl_down_sync(0xffffffffu, u[0][P].x, 1);
-      right[P].y = __shfl_down_sync(0xffffffffu, u[0][P].y, 1);
-    }
-    if (right_fetch) {
-#pragma unroll
-      for (int P = 0; P < NP; ++P) right[P] = s_edge_u[rg][P][wc + 1];
-    }
-    if (last_col) {
-#pragma unroll
-      for (int P = 0; P < NP; ++P) right[P] = u[1][P];
-    }
-    // the global last row has no row below: gy = 0 (below := u)
-    float u_below[2];
-    {
-      const float2 ub = !rg_bot ? *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0])
-                                : (last_row_thread ? make_float2(u[0][1].y, u[1][1].y)
-                                                   : make_float2(u_ex[0], u_ex[1]));
-      u_below[0] = ub.x;
-      u_below[1] = ub.y;
-    }
-    const float wr = w * kBallShrink;  // (common.cuh)
-    const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(wr, wr);
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int P = 0; P < NP; ++P) {
-        const float2 bl2 = P == 0 ? u[k][1] : make_float2(u[k][0].y, u_below[k]);
-        const float2 rt = k == 0 ? u[1][P] : right[P];
-        const float2 gy = __ffma2_rn(u[k][P], m1, bl2);
-        const float2 gx = __ffma2_rn(u[k][P], m1, rt);
-        const float2 ay = __ffma2_rn(st2, gy, yy[k][P]);
-        const float2 ax = __ffma2_rn(st2, gx, yx[k][P]);
-        const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
-        float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
-        sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
-        sc.y = fminf(1.f, sc.y);
-        QMy[k][P] = __fmul2_rn(ay, sc);
-        QMx[k][P] = __fmul2_rn(ax, sc);
+        for (int P = 0; P < NP; ++P) right[P] = s_edge_u[rg][P][wc + 1];
       }
-    push_rows(QMy[0][0].x, QMx[0][0].x, QMy[1][0].x, QMx[1][0].x, QMy[0][1].y, QMy[1][1].y);
-    ++round;
-  };
+      if (last_col) {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) right[P] = u[1][P];
+      }
+      if constexpr (!BOT) {
+        const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+        u_below[0] = ub.x;
+        u_below[1] = ub.y;
+      }
+      const float wr = w * kBallShrink;  // (common.cuh)
+      const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(wr, wr);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int P = 0; P < NP; ++P) {
+          const float2 bl2 = P == 0 ? u[k][1] : make_float2(u[k][0].y, u_below[k]);
+          const float2 rt = k == 0 ? u[1][P] : right[P];
+          const float2 gy = __ffma2_rn(u[k][P], m1, bl2);
+          const float2 gx = __ffma2_rn(u[k][P], m1, rt);
+          const float2 ay = __ffma2_rn(st2, gy, yy[k][P]);
+          const float2 ax = __ffma2_rn(st2, gx, yx[k][P]);
+          const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
+          float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
+          sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
+          sc.y = fminf(1.f, sc.y);
+          QMy[k][P] = __fmul2_rn(ay, sc);
+          QMx[k][P] = __fmul2_rn(ax, sc);
+        }
+      // halo rows of the new iterate: y_{it+1} (or q_n after the last iteration)
+      if constexpr (TOP) {
+        if (has_up) {
+          float v[4] = {QMy[0][0].x, QMx[0][0].x, QMy[1][0].x, QMx[1][0].x};
+          if (it + 1 < a.n_inner) {
+            const float b1 = a.accelerated ? s_beta[it] : 0.f;
+            const float o[4] = {QKy[0][0].x, QKx[0][0].x, QKy[1][0].x, QKx[1][0].x};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = fmaf(b1, fmaf(o[i], -1.f, v[i]), v[i]);
+          }
+          push_up(v[0], v[1], v[2], v[3]);
+        }
+      }
+      if constexpr (BOT) {
+        if (has_dn) {
+          float v[2] = {QMy[0][1].y, QMy[1][1].y};
+          if (it + 1 < a.n_inner) {
+            const float b1 = a.accelerated ? s_beta[it] : 0.f;
+            const float o[2] = {QKy[0][1].y, QKy[1][1].y};
+#pragma unroll
+            for (int i = 0; i < 2; ++i) v[i] = fmaf(b1, fmaf(o[i], -1.f, v[i]), v[i]);
+          }
+          push_dn(v[0], v[1]);
+        }
+      }
+      ++round;
+    };
 
-  int it = 0;
-  for (; it + 1 < a.n_inner; it += 2) {
-    inner(qky, qkx, qmy, qmx, it);      // new iterate in qm*
-    inner(qmy, qmx, qky, qkx, it + 1);  // new iterate in qk*
-  }
-  if (it < a.n_inner) {
-    inner(qky, qkx, qmy, qmx, it);
+    int it = 0;
+    for (; it + 1 < a.n_inner; it += 2) {
+      inner(qky, qkx, qmy, qmx, it);      // new iterate in qm*
+      inner(qmy, qmx, qky, qkx, it + 1);  // new iterate in qk*
+    }
+    if (it < a.n_inner) {
+      inner(qky, qkx, qmy, qmx, it);
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < 2; ++k)
 #pragma unroll
-      for (int P = 0; P < NP; ++P) {
-        qky[k][P] = qmy[k][P];
-        qkx[k][P] = qmx[k][P];
-      }
-  }
+        for (int P = 0; P < NP; ++P) {
+          qky[k][P] = qmy[k][P];
+          qkx[k][P] = qmx[k][P];
+        }
+    }
+  };
+  if (rg_top)
+    run_inner(std::integral_constant<int, 0>{});
+  else if (rg_bot)
+    run_inner(std::integral_constant<int, 2>{});
+  else
+    run_inner(std::integral_constant<int, 1>{});
 
   // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
   const unsigned pe = recv_rows(round0 + a.n_inner);
