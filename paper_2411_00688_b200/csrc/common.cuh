@@ -167,6 +167,43 @@ __device__ __forceinline__ void stv(T* p, const T (&s)[V]) {
 
 template <class T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
 
+__device__ __forceinline__ bool same_bits(float a, float b) {
+  return __float_as_uint(a) == __float_as_uint(b);
+}
+__device__ __forceinline__ bool same_bits(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// m skipped ProxSkip iterations of the identity fidelity,
+// x <- (x - g (x - b)) + g h (skip.py:68), with the reference's roundings.
+// The update is a fixed map of x (b, h, g do not change across a run of
+// skips), so once it returns its input bit for bit every later step does too
+// and the loop stops there: the result is exactly the m-step result.  A
+// non-finite x stays non-finite under the map, so only the final x is
+// tested; *first_bad = min(*first_bad, kfirst + first non-finite step).
+template <class T>
+__device__ __forceinline__ T skip_chain_px(T x, T b, T h, T g, int m, int kfirst,
+                                           int* first_bad) {
+  using A = Ar<T>;
+  const T x0 = x;
+  for (int s = 0; s < m; ++s) {
+    const T xn = A::add(A::sub(x, A::mul(g, A::sub(x, b))), A::mul(g, h));
+    if (same_bits(xn, x)) break;
+    x = xn;
+  }
+  if (m > 0 && !finite(x)) {
+    T xr = x0;
+    for (int s = 0; s < m; ++s) {
+      xr = A::add(A::sub(xr, A::mul(g, A::sub(xr, b))), A::mul(g, h));
+      if (!finite(xr)) {
+        *first_bad = min(*first_bad, kfirst + s);
+        break;
+      }
+    }
+  }
+  return x;
+}
+
 // ---- host->device chunk streaming (run drivers) ------------------------------
 // The run kernels can start before their inputs have arrived: problem p's
 // chunk c = p / chunk is ready once ready[c] != 0 (written by the copy stream

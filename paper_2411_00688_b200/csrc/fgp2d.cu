@@ -732,11 +732,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
         float* zs = &zv.x;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          float xo = xs[c];
-          for (int s2 = 0; s2 < m; ++s2) {
-            xo = sm_skip(xo, bs[c], hs[c], g);
-            if (!finite(xo)) kbad = min(kbad, kf + s2);
-          }
+          const float xo = skip_chain_px(xs[c], bs[c], hs[c], g, m, kf, &kbad);
           xs[c] = xo;
           zs[c] = A::add(A::sub(xo, A::mul(g, A::sub(xo, bs[c]))), A::mul(a.hc, hs[c]));
         }
@@ -812,12 +808,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
         const float* hs = &hv.x;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          float xo = xs[c];
-          for (int s2 = 0; s2 < m; ++s2) {
-            xo = sm_skip(xo, bs[c], hs[c], g);
-            if (!finite(xo)) kbad = min(kbad, kprev + 1 + s2);
-          }
-          xs[c] = xo;
+          xs[c] = skip_chain_px(xs[c], bs[c], hs[c], g, m, kprev + 1, &kbad);
         }
         __stcg(reinterpret_cast<float4*>(xp) + v, xv);
       }

@@ -108,11 +108,12 @@ __global__ void proxskip_post3d_kernel(TO* __restrict__ x, const TO* __restrict_
       q[N3 + i] = vy;
       q[2 * N3 + i] = vx;
     }
-    TO xo = x[i];
     const TO ho = h[i], bo = b[i];
-    // the `pend` deferred skip iterations since x was last stored (skip.py:68)
-    for (int s = 0; s < pend; ++s)
-      xo = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(gamma, ho));
+    // the `pend` deferred skip iterations since x was last stored (skip.py:68;
+    // fixed-point exit, common.cuh -- non-finite values were reported by the
+    // skip chain that formed z)
+    int unused = 0x7fffffff;
+    const TO xo = skip_chain_px(x[i], bo, ho, gamma, pend, 0, &unused);
     const TO xhat = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(gamma, ho));
     const TO xn = (TO)uf;
     h[i] = A::add(ho, A::mul(pg, A::sub(xn, xhat)));

@@ -130,6 +130,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+#ifdef PSB_DBG_NOGSYNC  // timing experiment only: row-group waits skipped (results invalid)
+#define GWAIT(m, ph) ((void)0)
+#else
+#define GWAIT(m, ph) mbar_wait(m, ph)
+#endif
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(m)) : "memory");
+}
 __device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rmbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(raddr),
                "r"(__float_as_uint(v)), "r"(rmbar)
@@ -207,6 +215,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   __shared__ __align__(16) float rx_dn[2][CW][2];  // CTA below's first row of q (y, x)
   __shared__ __align__(8) float rx_up[2][CW];      // CTA above's last row of q (y)
   __shared__ __align__(8) uint64_t mb_dn[2], mb_up[2];
+  // the CTA below's first row of the prox input z, pushed once per prox call
+  __shared__ __align__(16) float rx_z[CW];
+  __shared__ __align__(8) uint64_t mb_z;
+  // point-to-point row-group synchronisation of the inner loop (one phase per
+  // inner iteration, 128 arrivals = every thread of the producing group):
+  // gE1/gE2[g]: group g's warp-edge columns of y_x / u are in shared memory;
+  // gYY[g]: group g's last-row y_y is out (for g+1); gU[g]: group g's
+  // first-row u is out (for g-1)
+  __shared__ __align__(8) uint64_t gE1[CRG], gE2[CRG], gYY[CRG], gU[CRG];
   __shared__ __align__(8) float s_rg_yy[CRG][CW];  // each row group's last-row y_y (for the group below)
   __shared__ __align__(8) float s_rg_u[CRG][CW];   // each row group's first-row u (for the group above)
   // warp-edge columns as row pairs: s_edge_yx[rg][.][w + 1] = last column of
@@ -232,6 +249,13 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     mbar_init(&mb_dn[1], 1);
     mbar_init(&mb_up[0], 1);
     mbar_init(&mb_up[1], 1);
+    mbar_init(&mb_z, 1);
+    for (int gi = 0; gi < CRG; ++gi) {
+      mbar_init(&gE1[gi], CTPR);
+      mbar_init(&gE2[gi], CTPR);
+      mbar_init(&gYY[gi], CTPR);
+      mbar_init(&gU[gi], CTPR);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // every CTA of this grid is resident: the SM-worker kernel (launched after
@@ -247,12 +271,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const uint32_t up_mb_remote = dsmem_addr(&mb_dn[0], cr > 0 ? cr - 1 : cr);
   const uint32_t dn_rx_remote = dsmem_addr(&rx_up[0][0], cr < CCL - 1 ? cr + 1 : cr); // my bottom row -> CTA below
   const uint32_t dn_mb_remote = dsmem_addr(&mb_up[0], cr < CCL - 1 ? cr + 1 : cr);
-  // the CTA below's first staged row (x, b, h), read once per prox call
-  const uint32_t ex_x_remote = dsmem_addr(sx + j0, cr < CCL - 1 ? cr + 1 : cr);
-  const uint32_t ex_b_remote = dsmem_addr(sb + j0, cr < CCL - 1 ? cr + 1 : cr);
-  const uint32_t ex_h_remote = dsmem_addr(sh + j0, cr < CCL - 1 ? cr + 1 : cr);
+  // my first row of z -> the CTA above (once per prox call)
+  const uint32_t z_rx_remote = dsmem_addr(&rx_z[0], cr > 0 ? cr - 1 : cr);
+  const uint32_t z_mb_remote = dsmem_addr(&mb_z, cr > 0 ? cr - 1 : cr);
+  unsigned zph = 0;  // prox calls so far (mb_z phases)
   unsigned round = 0;
+  unsigned gph = 0;  // inner iterations so far (row-group mbarrier phases)
   auto push_rows = [&](float ty0, float tx0, float ty1, float tx1, float by0, float by1) {
+#ifdef PSB_DBG_NOHALO
+    return;
+#endif
     const unsigned b = round & 1;
     if (rg_top && cr > 0)
       st_async_v4(up_rx_remote + 4u * (b * CW * 2 + j0 * 2), ty0, tx0, ty1, tx1, up_mb_remote + 8u * b);
@@ -266,6 +294,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const bool arm = lane == 0 && wc == 0;
   auto recv_rows = [&](unsigned r) {
     const unsigned b = r & 1, ph = (r >> 1) & 1;
+#ifdef PSB_DBG_NOHALO
+    return b;
+#endif
     if (wait_dn) {
       if (arm) mbar_expect_tx(&mb_dn[b], BYTES_DN);
       mbar_wait(&mb_dn[b], ph);
@@ -278,21 +309,33 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   };
   // role-specialised halves of push_rows / recv_rows for the inner loop
   auto push_up = [&](float ty0, float tx0, float ty1, float tx1) {  // top group, has_up
+#ifdef PSB_DBG_NOHALO
+    return;
+#endif
     const unsigned b = round & 1;
     st_async_v4(up_rx_remote + 4u * (b * CW * 2 + j0 * 2), ty0, tx0, ty1, tx1, up_mb_remote + 8u * b);
   };
   auto push_dn = [&](float by0, float by1) {  // bottom group, has_dn
+#ifdef PSB_DBG_NOHALO
+    return;
+#endif
     const unsigned b = round & 1;
     st_async_v2(dn_rx_remote + 4u * (b * CW + j0), by0, by1, dn_mb_remote + 8u * b);
   };
   auto recv_up = [&](unsigned r) {  // top group, has_up
     const unsigned b = r & 1, ph = (r >> 1) & 1;
+#ifdef PSB_DBG_NOHALO
+    return b;
+#endif
     if (arm) mbar_expect_tx(&mb_up[b], BYTES_UP);
     mbar_wait(&mb_up[b], ph);
     return b;
   };
   auto recv_dn = [&](unsigned r) {  // bottom group, has_dn
     const unsigned b = r & 1, ph = (r >> 1) & 1;
+#ifdef PSB_DBG_NOHALO
+    return b;
+#endif
     if (arm) mbar_expect_tx(&mb_dn[b], BYTES_DN);
     mbar_wait(&mb_dn[b], ph);
     return b;
@@ -343,17 +386,18 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   const int kk = a.ev_k[e];
   const int m = kk - kprev - 1;  // skip iterations kprev+1 .. kk-1 before this prox call
   const int kf = kprev + 1;
-  // the previous prox call's x / h updates (and, at the first call, the
-  // staging) of every CTA are visible cluster-wide; also orders the reuse of
-  // this CTA's exchange buffers
-  cluster_arrive();
-  cluster_wait();
+  // (no cluster-wide barrier per prox call: the only data crossing CTAs are
+  // the halo rows and the z row, each tracked by the receiver's mbarrier)
+  __syncthreads();
   // ---- prologue: skips, prox input, warm start ------------------------------
-  auto prox_input = [&](TO xo, TO bo, TO ho, bool track) {
-    for (int s = 0; s < m; ++s) {
-      xo = skip_update(xo, bo, ho, g);
-      if (track && !finite(xo)) kbad = min(kbad, kf + s);
-    }
+  // The m skipped iterations since the last prox call (skip.py:68), executed
+  // in the reference's op order; x after them goes back to shared memory for
+  // the epilogue.  A non-finite x stays non-finite under the skip update, so
+  // only the final x is tested; the slow path finds the first bad iteration.
+  auto prox_input = [&](int sj) {
+    const TO bo = sb[sj], ho = sh[sj];
+    const TO xo = skip_chain_px(sx[sj], bo, ho, g, m, kf, &kbad);
+    if (m > 0) sx[sj] = xo;
     return (float)A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(a.hc, ho));
   };
 #pragma unroll
@@ -362,7 +406,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     for (int t = 0; t < CRPT; ++t) {
       const int lr = rg * CRPT + t;
       const int sj = lr * CW + j0 + k;
-      rowref(z[k], t) = prox_input(sx[sj], sb[sj], sh[sj], true);
+      rowref(z[k], t) = prox_input(sj);
       if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
         const int64_t o = (int64_t)(row0 + t) * CW + j0 + k;
         float vy = q0[o], vx = q0[HW + o];
@@ -387,15 +431,18 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       qmx[k][P] = qkx[k][P];
     }
   }
-  // the bottom row group also owns the CTA-below's first row for u
+  // the bottom row group also owns the CTA-below's first row for u: its z
+  // arrives from that CTA (st.async on mb_z); mine goes to the CTA above
+  if (rg_top && has_up)
+    st_async_v2(z_rx_remote + 4u * j0, z[0][0].x, z[1][0].x, z_mb_remote);
   float z_ex[2] = {0.f, 0.f};
   if (rg_bot && has_dn) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      z_ex[k] = prox_input(dsmem_ld<TO>(ex_x_remote + k * sizeof(TO)),
-                           dsmem_ld<TO>(ex_b_remote + k * sizeof(TO)),
-                           dsmem_ld<TO>(ex_h_remote + k * sizeof(TO)), false);
+    if (arm) mbar_expect_tx(&mb_z, CW * 4);
+    mbar_wait(&mb_z, zph & 1u);
+    z_ex[0] = rx_z[j0];
+    z_ex[1] = rx_z[j0 + 1];
   }
+  ++zph;
   const unsigned round0 = round;  // this call's warm-start round
   // Halo rows travel as MOMENTUM iterates y (the receiver uses them as they
   // are): the warm-start round carries y_0 = fma(0, q_0 - q_0, q_0), round
@@ -422,8 +469,19 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   auto run_inner = [&](auto role_tag) {
     constexpr int ROLE = decltype(role_tag)::value;
     constexpr bool TOP = ROLE == 0, BOT = ROLE == 2;
+    // Row groups synchronise point to point through the gE1/gE2/gYY/gU
+    // mbarriers (one phase per inner iteration) instead of two CTA-wide
+    // barriers: a group waits only for the data it reads -- its own warps'
+    // edge columns and one row of each adjacent group -- so the groups run
+    // skewed and the boundary groups compute their halo pair first: the top
+    // group pushes its first row to the CTA above before it needs the middle
+    // group's u, the bottom group pushes its last row before it needs the
+    // middle group's y.  Shared-memory reuse across iterations is ordered by
+    // the same waits (a group cannot reach iteration t+1's write of a row
+    // before its readers have passed their wait for iteration t).
     auto inner = [&](float2(&QKy)[2][NP], float2(&QKx)[2][NP], float2(&QMy)[2][NP],
                      float2(&QMx)[2][NP], int it) {
+      const unsigned ph = gph & 1u;
       const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
       const float2 b2 = make_float2(beta, beta), m1 = make_float2(-1.f, -1.f);
       float2 yy[2][NP], yx[2][NP];
@@ -434,6 +492,16 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
           yy[k][P] = __ffma2_rn(b2, __ffma2_rn(QMy[k][P], m1, QKy[k][P]), QKy[k][P]);
           yx[k][P] = __ffma2_rn(b2, __ffma2_rn(QMx[k][P], m1, QKx[k][P]), QKx[k][P]);
         }
+      if constexpr (!BOT) {  // last-row y_y for the group below
+        s_rg_yy[rg][j0] = yy[0][1].y;  // row CRPT-1
+        s_rg_yy[rg][j0 + 1] = yy[1][1].y;
+        mbar_arrive(&gYY[rg]);
+      }
+      if (lane == 31) {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
+      }
+      mbar_arrive(&gE1[rg]);
       float2 yyA = make_float2(0.f, 0.f);             // TOP: y row above (zeros at row 0)
       float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
       if constexpr (TOP) {
@@ -450,15 +518,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
           if (j0 > 0) ledge_x = rx_dn[par][j0 - 1][1];
         }
       }
-      if constexpr (!BOT) {  // last-row y_y for the group below
-        s_rg_yy[rg][j0] = yy[0][1].y;  // row CRPT-1
-        s_rg_yy[rg][j0 + 1] = yy[1][1].y;
-      }
-      if (lane == 31) {
-#pragma unroll
-        for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
-      }
-      __syncthreads();
+      GWAIT(&gE1[rg], ph);
       // left neighbours of column 0: shuffles inside the warp, the warp to the
       // left's last column from shared memory (zeros left of column 0); column
       // 1's left neighbour is this thread's column 0
@@ -472,28 +532,33 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
 #pragma unroll
         for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
       }
-      float yy_above[2];
-      if constexpr (TOP) {
-        yy_above[0] = yyA.x;
-        yy_above[1] = yyA.y;
-      } else {
+      float yy_above[2] = {yyA.x, yyA.y};
+      float2 u[2][NP];
+      // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
+      auto u_pair = [&](int k, int P) {
+        const float2 ab2 = P == 0 ? make_float2(yy_above[k], yy[k][1].x) : yy[k][0];
+        const float2 l2 = k == 0 ? left[P] : yx[0][P];
+        const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[k][P]), yx[k][P]);
+        const float2 d2 = __ffma2_rn(l2, m1, d1);
+        const float2 v = __fadd2_rn(z[k][P], d2);
+        u[k][P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
+      };
+      if constexpr (BOT) {  // pair 1 (rows 1, 3) needs no row above
+        u_pair(0, 1);
+        u_pair(1, 1);
+      }
+      if constexpr (!TOP) {
+        GWAIT(&gYY[rg - 1], ph);
         const float2 ya2 = *reinterpret_cast<const float2*>(&s_rg_yy[rg - 1][j0]);
         yy_above[0] = ya2.x;
         yy_above[1] = ya2.y;
       }
-      float2 u[2][NP];
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int P = 0; P < NP; ++P) {
-          // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
-          const float2 ab2 = P == 0 ? make_float2(yy_above[k], yy[k][1].x) : yy[k][0];
-          const float2 l2 = k == 0 ? left[P] : yx[0][P];
-          const float2 d1 = __fadd2_rn(__ffma2_rn(ab2, m1, yy[k][P]), yx[k][P]);
-          const float2 d2 = __ffma2_rn(l2, m1, d1);
-          const float2 v = __fadd2_rn(z[k][P], d2);
-          u[k][P] = nonneg ? make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f)) : v;
-        }
+      u_pair(0, 0);
+      u_pair(1, 0);
+      if constexpr (!BOT) {
+        u_pair(0, 1);
+        u_pair(1, 1);
+      }
       float u_below[2];
       if constexpr (BOT) {
         if (has_dn) {  // u of the CTA-below's first row, from its y row
@@ -511,12 +576,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       if constexpr (!TOP) {  // first-row u for the group above
         s_rg_u[rg][j0] = u[0][0].x;
         s_rg_u[rg][j0 + 1] = u[1][0].x;
+        mbar_arrive(&gU[rg]);
       }
       if (lane == 0) {
 #pragma unroll
         for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[0][P];
       }
-      __syncthreads();
+      mbar_arrive(&gE2[rg]);
+      GWAIT(&gE2[rg], ph);
       // right neighbour of column 1: shuffles (lane 31 keeps its own column 1 at
       // the global last column: gx = 0), the warp to the right's first column
       // from shared memory; column 0's right neighbour is column 1
@@ -534,56 +601,68 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
 #pragma unroll
         for (int P = 0; P < NP; ++P) right[P] = u[1][P];
       }
-      if constexpr (!BOT) {
-        const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
-        u_below[0] = ub.x;
-        u_below[1] = ub.y;
-      }
       const float wr = w * kBallShrink;  // (common.cuh)
       const float2 st2 = make_float2(a.step, a.step), w2 = make_float2(wr, wr);
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int P = 0; P < NP; ++P) {
-          const float2 bl2 = P == 0 ? u[k][1] : make_float2(u[k][0].y, u_below[k]);
-          const float2 rt = k == 0 ? u[1][P] : right[P];
-          const float2 gy = __ffma2_rn(u[k][P], m1, bl2);
-          const float2 gx = __ffma2_rn(u[k][P], m1, rt);
-          const float2 ay = __ffma2_rn(st2, gy, yy[k][P]);
-          const float2 ax = __ffma2_rn(st2, gx, yx[k][P]);
-          const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
-          float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
-          sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
-          sc.y = fminf(1.f, sc.y);
-          QMy[k][P] = __fmul2_rn(ay, sc);
-          QMx[k][P] = __fmul2_rn(ax, sc);
-        }
+      auto q_pair = [&](int k, int P) {
+        const float2 bl2 = P == 0 ? u[k][1] : make_float2(u[k][0].y, u_below[k]);
+        const float2 rt = k == 0 ? u[1][P] : right[P];
+        const float2 gy = __ffma2_rn(u[k][P], m1, bl2);
+        const float2 gx = __ffma2_rn(u[k][P], m1, rt);
+        const float2 ay = __ffma2_rn(st2, gy, yy[k][P]);
+        const float2 ax = __ffma2_rn(st2, gx, yx[k][P]);
+        const float2 m2 = __ffma2_rn(ay, ay, __fmul2_rn(ax, ax));
+        float2 sc = __fmul2_rn(w2, make_float2(rsqrt_approx(m2.x), rsqrt_approx(m2.y)));
+        sc.x = fminf(1.f, sc.x);  // w / max(w, |a|)
+        sc.y = fminf(1.f, sc.y);
+        QMy[k][P] = __fmul2_rn(ay, sc);
+        QMx[k][P] = __fmul2_rn(ax, sc);
+      };
       // halo rows of the new iterate: y_{it+1} (or q_n after the last iteration)
-      if constexpr (TOP) {
+      const float b1 = (a.accelerated && it + 1 < a.n_inner) ? s_beta[it] : 0.f;
+      if constexpr (TOP) {  // pair 0 holds row 0: compute it, push, then pair 1
+        q_pair(0, 0);
+        q_pair(1, 0);
         if (has_up) {
           float v[4] = {QMy[0][0].x, QMx[0][0].x, QMy[1][0].x, QMx[1][0].x};
           if (it + 1 < a.n_inner) {
-            const float b1 = a.accelerated ? s_beta[it] : 0.f;
             const float o[4] = {QKy[0][0].x, QKx[0][0].x, QKy[1][0].x, QKx[1][0].x};
 #pragma unroll
             for (int i = 0; i < 4; ++i) v[i] = fmaf(b1, fmaf(o[i], -1.f, v[i]), v[i]);
           }
           push_up(v[0], v[1], v[2], v[3]);
         }
-      }
-      if constexpr (BOT) {
+        GWAIT(&gU[rg + 1], ph);
+        const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+        u_below[0] = ub.x;
+        u_below[1] = ub.y;
+        q_pair(0, 1);
+        q_pair(1, 1);
+      } else if constexpr (BOT) {  // pair 1 holds row 3: compute it, push, then pair 0
+        q_pair(0, 1);
+        q_pair(1, 1);
         if (has_dn) {
           float v[2] = {QMy[0][1].y, QMy[1][1].y};
           if (it + 1 < a.n_inner) {
-            const float b1 = a.accelerated ? s_beta[it] : 0.f;
             const float o[2] = {QKy[0][1].y, QKy[1][1].y};
 #pragma unroll
             for (int i = 0; i < 2; ++i) v[i] = fmaf(b1, fmaf(o[i], -1.f, v[i]), v[i]);
           }
           push_dn(v[0], v[1]);
         }
+        q_pair(0, 0);
+        q_pair(1, 0);
+      } else {
+        GWAIT(&gU[rg + 1], ph);
+        const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+        u_below[0] = ub.x;
+        u_below[1] = ub.y;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int P = 0; P < NP; ++P) q_pair(k, P);
       }
       ++round;
+      ++gph;
     };
 
     int it = 0;
@@ -610,6 +689,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     run_inner(std::integral_constant<int, 1>{});
 
   // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
+  __syncthreads();  // every group is past its last inner iteration's reads
   const unsigned pe = recv_rows(round0 + a.n_inner);
   float yy_above[2] = {0.f, 0.f};
   if (rg_top && has_up) {
@@ -652,9 +732,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       float uf = rowref(z[k], t) + d;
       if (nonneg) uf = fmaxf(uf, 0.f);
       const int sj = (rg * CRPT + t) * CW + j;
-      TO xo = sx[sj];
+      const TO xo = sx[sj];  // x after the skips (prologue)
       const TO bo = sb[sj], ho = sh[sj];
-      for (int s = 0; s < m; ++s) xo = skip_update(xo, bo, ho, g);
       const TO xhat = skip_update(xo, bo, ho, g);
       const TO xn = (TO)uf;
       sh[sj] = A::add(ho, A::mul(a.pg, A::sub(xn, xhat)));
@@ -674,12 +753,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     for (int t = 0; t < CRPT; ++t) {
       const int sj = (rg * CRPT + t) * CW + j0 + k;
       const int64_t o = (int64_t)(row0 + t) * CW + j0 + k;
-      TO xo = sx[sj];
-      const TO bo = sb[sj], ho = sh[sj];
-      for (int s = 0; s < m; ++s) {
-        xo = skip_update(xo, bo, ho, g);
-        if (!finite(xo)) kbad = min(kbad, kprev + 1 + s);
-      }
+      const TO ho = sh[sj];
+      const TO xo = skip_chain_px(sx[sj], sb[sj], ho, g, m, kprev + 1, &kbad);
       xp[o] = xo;
       if (e1 > e0) {
         hp[o] = ho;

@@ -137,12 +137,8 @@ __global__ void skip_chain_kernel(TO* __restrict__ x, const TO* __restrict__ b,
   int kbad = 0x7fffffff;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
-    TO xo = x[i];
     const TO bo = b[i], ho = h[i];
-    for (int s = 0; s < pend; ++s) {
-      xo = A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(gamma, ho));
-      if (!finite(xo)) kbad = min(kbad, kfirst + s);
-    }
+    const TO xo = skip_chain_px(x[i], bo, ho, gamma, pend, kfirst, &kbad);
     if (z)
       z[i] = (TF)A::add(A::sub(xo, A::mul(gamma, A::sub(xo, bo))), A::mul(hcoef, ho));
     else
