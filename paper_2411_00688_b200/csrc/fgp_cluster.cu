@@ -443,21 +443,28 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
     z_ex[1] = rx_z[j0 + 1];
   }
   ++zph;
-  const unsigned round0 = round;  // this call's warm-start round
+  // After the first call of a problem the warm start is the previous call's
+  // q_n, whose boundary rows arrived in that call's final round: the first
+  // inner iteration reads them from there (and forms y_0 itself) instead of
+  // exchanging them again -- one DSMEM round trip less per prox call.
+  const bool reuse = e > e0;
+  const unsigned round0 = reuse ? round - 1 : round;  // this call's warm-start round
   // Halo rows travel as MOMENTUM iterates y (the receiver uses them as they
   // are): the warm-start round carries y_0 = fma(0, q_0 - q_0, q_0), round
   // it + 1 (it + 1 < n) carries y_{it+1} = fma(beta_{it+1}, q_{it+1} - q_it,
   // q_{it+1}) -- the values the owner computes for its own pixels, bit for bit
   // -- and the last round q_n itself (the finalize reads q_n).
-  {
+  if (!reuse) {
     float v[6];
     const float y0s[6] = {qky[0][0].x, qkx[0][0].x, qky[1][0].x, qkx[1][0].x, qky[0][1].y,
                           qky[1][1].y};
 #pragma unroll
     for (int i = 0; i < 6; ++i) v[i] = fmaf(0.f, fmaf(y0s[i], -1.f, y0s[i]), y0s[i]);
     push_rows(v[0], v[1], v[2], v[3], v[4], v[5]);
+    ++round;
   }
-  ++round;
+  // y_0 of a halo value q (beta_0 = 0), exactly as the owner forms it
+  auto y0_of = [](float q) { return fmaf(0.f, fmaf(q, -1.f, q), q); };
 
   // One inner iteration; reads (QK, QM), writes the new iterate into QM.
   // Each pixel's arithmetic is the scalar FGP step (each f32x2 lane an IEEE
@@ -506,16 +513,24 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
       if constexpr (TOP) {
         if (has_up) {
-          const unsigned par = recv_up(round0 + it);
+          const bool warm = reuse && it == 0;  // (already received: final round)
+          const unsigned par = warm ? (round0 & 1u) : recv_up(round0 + it);
           yyA = *reinterpret_cast<const float2*>(&rx_up[par][j0]);
+          if (warm) yyA = make_float2(y0_of(yyA.x), y0_of(yyA.y));
         }
       }
       if constexpr (BOT) {
         if (has_dn) {
-          const unsigned par = recv_dn(round0 + it);
+          const bool warm = reuse && it == 0;  // (already received: final round)
+          const unsigned par = warm ? (round0 & 1u) : recv_dn(round0 + it);
           const float4 v = *reinterpret_cast<const float4*>(&rx_dn[par][j0][0]);
           ex_y[0] = v.x, ex_x[0] = v.y, ex_y[1] = v.z, ex_x[1] = v.w;
           if (j0 > 0) ledge_x = rx_dn[par][j0 - 1][1];
+          if (warm) {
+            ex_y[0] = y0_of(ex_y[0]), ex_x[0] = y0_of(ex_x[0]);
+            ex_y[1] = y0_of(ex_y[1]), ex_x[1] = y0_of(ex_x[1]);
+            ledge_x = y0_of(ledge_x);
+          }
         }
       }
       GWAIT(&gE1[rg], ph);
