@@ -287,6 +287,16 @@ int psb_proxskip_denoise_run_streamed(int dtype_outer, int dtype_fgp, void* x, c
 int psb_stream_memops_supported(int* out);
 int psb_stream_write_u32(void* stream, void* dptr, uint32_t value);
 int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value);
+/* psb_chunked_h2d / psb_chunked_d2h: the streamed batch's copies, enqueued in
+ * one call each (items of item_bytes, chunks of `chunk` items).  H2D: copy
+ * chunk c from page-locked host memory, then ready[c] = 1 (fenced stream
+ * write).  D2H: wait until done[c] >= unit * (items in chunk c) (stream wait),
+ * then copy chunk c to page-locked host memory.  Replaces the per-chunk copy
+ * loop of run_proxskip_batched's streamed path. */
+int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_bytes, int64_t n_items,
+                    int64_t chunk, int32_t* ready, void* stream);
+int psb_chunked_d2h(void* dst_host, const void* src, int64_t item_bytes, int64_t n_items,
+                    int64_t chunk, const int32_t* done, uint32_t unit, void* stream);
 
 /* Peer memory for the config-5 z-slab exchange (the reference has
  * no multi-GPU path -- this replaces the halo transfer of the decomposed

@@ -150,7 +150,7 @@ def _memops():
 
 
 def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.0,
-                         precision="fp32", use_graph=False, chunk=256, out=None):
+                         precision="fp32", use_graph=False, chunk=None, out=None):
     """Config-4 entry point: returns (x, prox_counts) as the input currency.
 
     ``out`` (optional, host input only): a contiguous float32 CPU tensor of
@@ -165,6 +165,8 @@ def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.
     chunks still compute.  Same arithmetic and results as the resident run."""
     seeds = np.asarray(seeds).reshape(-1)
     n = int(seeds.size)
+    if chunk is None:  # small chunks: the first input and the last result move fast
+        chunk = max(8, min(256, n // 128))
     shape = tuple(b.shape) if hasattr(b, "shape") else np.shape(b)
     # (streamed only for float32 host data: a dtype conversion would need a
     # kernel on the copy stream, which cannot run while the waiting run
@@ -208,28 +210,25 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
     flags = torch.zeros(2 * nc + 1, dtype=torch.int32, device="cuda")  # ready[nc + 1], done[nc]
     ready, done = flags[:nc + 1], flags[nc + 1:]
     main = torch.cuda.current_stream()
-    start = torch.cuda.Event()
+    start = torch.cuda.Event(enable_timing=dbg)
     start.record(main)  # buffers allocated and zeroed
-    copy = torch.cuda.Stream()
-    copy.wait_event(start)
-    cs = L.C.c_void_p(copy.cuda_stream)
-    pinned = out.is_pinned()
-    evs = []  # debug timeline (PSB_DEBUG_E2E=1): chunk arrivals / completions
-    with torch.cuda.stream(copy):
-        if dbg:
-            evs.append(("start", torch.cuda.Event(enable_timing=True)))
-            evs[-1][1].record(copy)
-        # 1) inputs, chunk by chunk, each announced to the run kernels -- all
-        #    enqueued BEFORE the run, so the copies never depend on the run
-        #    kernels making progress (serialised execution under
-        #    CUDA_LAUNCH_BLOCKING=1, compute-sanitizer or ncu stays correct)
-        for c, (lo, hi) in enumerate(bounds):
-            part = src[lo:hi]  # float32 H2D: a DMA, no kernel on this stream
-            solver.b[lo:hi].copy_(part, non_blocking=part.is_pinned())
-            L.call("psb_stream_write_u32", cs, L.C.c_void_p(ready.data_ptr() + 4 * c), 1)
-            if dbg:
-                evs.append((f"in{c}", torch.cuda.Event(enable_timing=True)))
-                evs[-1][1].record(copy)
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    h2d.wait_event(start)
+    d2h.wait_event(start)
+    item = H * W * 4
+    # 1) inputs, chunk by chunk, each announced to the run kernels by a fenced
+    #    stream write -- all enqueued BEFORE the run, so the copies never depend
+    #    on the run kernels making progress (serialised execution under
+    #    CUDA_LAUNCH_BLOCKING=1, compute-sanitizer or ncu stays correct)
+    if src.is_pinned():  # one native call enqueues every chunk (DMA, no kernels)
+        L.call("psb_chunked_h2d", L.ptr(solver.b), L.C.c_void_p(src.data_ptr()), item, n, chunk,
+               L.ptr(ready), L.C.c_void_p(h2d.cuda_stream))
+    else:
+        cs = L.C.c_void_p(h2d.cuda_stream)
+        with torch.cuda.stream(h2d):
+            for c, (lo, hi) in enumerate(bounds):
+                solver.b[lo:hi].copy_(src[lo:hi])  # float32 H2D: a DMA, no kernel on this stream
+                L.call("psb_stream_write_u32", cs, L.C.c_void_p(ready.data_ptr() + 4 * c), 1)
     # 2) the run: its kernels wait per problem for the chunk flags above
     L.call("psb_proxskip_denoise_run_streamed", L.dcode(solver.dto), L.dcode(solver.dtf),
            L.ptr(solver.x), L.ptr(solver.b), L.ptr(solver.h), L.ptr(solver.z),
@@ -238,35 +237,33 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
            solver.last_weight.ctypes.data_as(L.C.c_void_p),
            solver.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(solver.bad), L.ptr(ready),
            L.ptr(done), chunk, nc, L.stream())
-    with torch.cuda.stream(copy):
-        # 3) results, chunk by chunk, as soon as the chunk's problems are done
-        for c, (lo, hi) in enumerate(bounds):
-            L.call("psb_stream_wait_geq_u32", cs, L.C.c_void_p(done.data_ptr() + 4 * c),
-                   16 * (hi - lo))
-            if dbg:
-                evs.append((f"done{c}", torch.cuda.Event(enable_timing=True)))
-                evs[-1][1].record(copy)
-            if pinned:  # DMA straight into the caller's page-locked buffer
-                out[lo:hi].copy_(solver.x[lo:hi], non_blocking=True)
-            else:
-                AR.download_into(out[lo:hi], solver.x[lo:hi])
-        if dbg:
-            evs.append(("end", torch.cuda.Event(enable_timing=True)))
-            evs[-1][1].record(copy)
-            main_end = torch.cuda.Event(enable_timing=True)
-            main_end.record(main)
-    t2 = time.perf_counter() if dbg else 0.0
-    main.wait_stream(copy)
+    # 3) results on their own stream, chunk by chunk, as soon as the chunk's
+    #    problems are done (stream wait on the device counter): they leave
+    #    while later inputs still arrive
+    pinned = out.is_pinned()
     if pinned:
-        copy.synchronize()
+        L.call("psb_chunked_d2h", L.C.c_void_p(out.data_ptr()), L.ptr(solver.x), item, n, chunk,
+               L.ptr(done), 16, L.C.c_void_p(d2h.cuda_stream))
+    else:
+        cs = L.C.c_void_p(d2h.cuda_stream)
+        with torch.cuda.stream(d2h):
+            for c, (lo, hi) in enumerate(bounds):
+                L.call("psb_stream_wait_geq_u32", cs, L.C.c_void_p(done.data_ptr() + 4 * c),
+                       16 * (hi - lo))
+                AR.download_into(out[lo:hi], solver.x[lo:hi])
+    t2 = time.perf_counter() if dbg else 0.0
+    main.wait_stream(h2d)
+    main.wait_stream(d2h)
+    if pinned:
+        d2h.synchronize()
     if dbg:
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(main)
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         print(f"[psb e2e] setup {1e3 * (t1 - t0):.1f} ms, enqueue {1e3 * (t2 - t1):.1f} ms, "
-              f"run {1e3 * (t3 - t2):.1f} ms; timeline " +
-              " ".join(f"{k}={evs[0][1].elapsed_time(e):.1f}" for k, e in evs[1:]) +
-              f" main_end={evs[0][1].elapsed_time(main_end):.1f} host_after_enqueue="
-              f"{1e3 * (t2 - t1):.1f}", flush=True)
+              f"run {1e3 * (t3 - t2):.1f} ms, device {start.elapsed_time(end):.1f} ms "
+              f"({nc} chunks of {chunk})", flush=True)
     if int(ready[nc].item()) != 0:
         raise RuntimeError("streamed run: an input chunk never arrived (device wait timed out)")
     solver.check_finite()

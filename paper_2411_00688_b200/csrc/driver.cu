@@ -525,6 +525,46 @@ extern "C" int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value)
   return PSB_OK;
 }
 
+// Chunked host<->device streaming of a batch (the e2e path of
+// run_proxskip_batched): one call enqueues every chunk's copy and its stream
+// memory operation, so the host spends microseconds, not a Python round trip,
+// per chunk.  H2D: copy chunk c, then ready[c] = 1 (fenced write).  D2H (on
+// its own stream, so results leave while later inputs still arrive): wait
+// until done[c] >= unit * (items in chunk c), then copy chunk c back.
+extern "C" int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_bytes, int64_t n_items,
+                               int64_t chunk, int32_t* ready, void* stream) {
+  PSB_REQUIRE(item_bytes > 0 && n_items >= 0 && chunk > 0, "chunked h2d: bad sizes");
+  static StreamValueFn wr = stream_fn("cuStreamWriteValue32");
+  if (!wr) return psb::fail(PSB_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  auto st = psb::as_stream(stream);
+  for (int64_t c = 0, lo = 0; lo < n_items; ++c, lo += chunk) {
+    const int64_t k = std::min(chunk, n_items - lo);
+    PSB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + lo * item_bytes,
+                             static_cast<const char*>(src_host) + lo * item_bytes,
+                             (size_t)(k * item_bytes), cudaMemcpyHostToDevice, st));
+    if (wr(stream, reinterpret_cast<unsigned long long>(ready + c), 1u, 0) != 0)
+      return psb::fail(PSB_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+  return PSB_OK;
+}
+
+extern "C" int psb_chunked_d2h(void* dst_host, const void* src, int64_t item_bytes, int64_t n_items,
+                               int64_t chunk, const int32_t* done, uint32_t unit, void* stream) {
+  PSB_REQUIRE(item_bytes > 0 && n_items >= 0 && chunk > 0, "chunked d2h: bad sizes");
+  static StreamValueFn wt = stream_fn("cuStreamWaitValue32");
+  if (!wt) return psb::fail(PSB_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  auto st = psb::as_stream(stream);
+  for (int64_t c = 0, lo = 0; lo < n_items; ++c, lo += chunk) {
+    const int64_t k = std::min(chunk, n_items - lo);
+    if (wt(stream, reinterpret_cast<unsigned long long>(done + c), unit * (uint32_t)k, 0x0) != 0)
+      return psb::fail(PSB_ERR_CUDA, "cuStreamWaitValue32 failed");
+    PSB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst_host) + lo * item_bytes,
+                             static_cast<const char*>(src) + lo * item_bytes,
+                             (size_t)(k * item_bytes), cudaMemcpyDeviceToHost, st));
+  }
+  return PSB_OK;
+}
+
 // Peer memory for the config-5 slab exchange: a rank exports
 // its receive rings / flags with a CUDA IPC handle, its z-neighbours map them
 // and deposit halo planes there directly (kernel stores or copies over
