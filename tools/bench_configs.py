@@ -210,27 +210,8 @@ def cfg8f():
 
 
 def config5_volume(side=1024):
-    """Config-5 input on the device (seeded): 50 ellipsoids U[0,1] + noise 0.1."""
-    torch.manual_seed(0)
-    g = torch.Generator(device="cuda").manual_seed(0)
-    # setup on the device (seeded torch generator): ellipsoid phantom + noise
-    D = H = W = side
-    vol = torch.zeros((D, H, W), dtype=torch.float32, device="cuda")
-    rng = np.random.default_rng(0)
-    zz = (torch.arange(D, device="cuda", dtype=torch.float32) + 0.5) / D
-    for _ in range(50):
-        c = rng.uniform(0.15, 0.85, size=3)
-        r = rng.uniform(0.04, 0.25, size=3)
-        val = float(rng.uniform(0, 1))
-        z0, z1 = max(0, int((c[0] - r[0]) * D) - 1), min(D, int((c[0] + r[0]) * D) + 2)
-        yy = ((zz - float(c[1])) / float(r[1])) ** 2
-        xx = ((zz - float(c[2])) / float(r[2])) ** 2
-        for z in range(z0, z1):
-            m = ((zz[z] - float(c[0])) / float(r[0])) ** 2 + yy[:, None] + xx[None, :] <= 1.0
-            vol[z][m] = val
-    b = vol + 0.1 * torch.randn((D, H, W), generator=g, device="cuda")
-    del vol
-    return b
+    """Config-5 input on the device (seeded): phantoms.config5_volume."""
+    return phantoms.config5_volume(side, 0)
 
 
 def cfg5(side=1024, K=200, inner=20):

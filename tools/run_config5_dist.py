@@ -35,9 +35,7 @@ def volume(side, seed=0):
     if side <= 128:
         vol = phantoms.random_ellipsoids((side, side, side), 50, np.random.default_rng(seed))
         return torch.from_numpy(phantoms.add_noise(vol, 0.1, seed).astype(np.float32)).cuda()
-    sys.path.insert(0, os.path.join(ROOT, "tools"))
-    from bench_configs import config5_volume
-    return config5_volume(side)
+    return phantoms.config5_volume(side, seed)
 
 
 def main():
