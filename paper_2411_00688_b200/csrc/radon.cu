@@ -344,17 +344,21 @@ __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* _
       ds[j] = ok ? fmaf((float)j, dsf, es) : 8.f;
     }
     const float* yrow = y + (int64_t)ia * G.nb;
+    // (dx, dy) of a candidate as one packed pair: FFMA2 for the offsets,
+    // FADD2 with the |.| operand modifier for 1 - |d| -- the scalar ops'
+    // IEEE results lane by lane (ds * (-s) == (-ds) * s exactly)
+    const float2 sc2 = make_float2(-sf, cf), one2 = make_float2(1.f, 1.f);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const bool ok = (unsigned)(b0 + i) < (unsigned)G.nb;
       const float db = fmaf((float)i, spf, eb);
-      const float bx = ok ? db * cf : 8.f, by = ok ? db * sf : 8.f;
+      const float2 bxy = ok ? make_float2(db * cf, db * sf) : make_float2(8.f, 8.f);
       float wsum = 0.f;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        const float dx = fmaf(-ds[j], sf, bx), dy = fmaf(ds[j], cf, by);
-        const float wx = fmaxf(0.f, 1.f - fabsf(dx)), wy = fmaxf(0.f, 1.f - fabsf(dy));
-        wsum = fmaf(wx, wy, wsum);
+        const float2 d2 = __ffma2_rn(make_float2(ds[j], ds[j]), sc2, bxy);
+        const float2 t2 = __fadd2_rn(one2, make_float2(-fabsf(d2.x), -fabsf(d2.y)));
+        wsum = fmaf(fmaxf(0.f, t2.x), fmaxf(0.f, t2.y), wsum);
       }
       acc = fmaf(wsum, yrow[ok ? b0 + i : 0], acc);
     }

@@ -349,3 +349,31 @@ def test_deblur_fused_pre_is_bitwise_the_two_kernel_form(monkeypatch, precision,
         out.append(res)
     for a, c in zip(*out):
         np.testing.assert_array_equal(a, c)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_dual_gap_rof_matches_reference_value(golden, dtype):
+    """dual_gap_rof (tv.py:92-105) on the device: the reference's own value
+    for its 200-iteration prox state (golden `tv_gap`, fp64 state: 1e-13
+    absolute, i.e. ~1e-14 of the primal / dual terms it is the difference of: the gap
+    itself is ~1e-6 and the device's reduction order differs from numpy's),
+    and on fp32 states the oracle's value for the same q (the
+    fp32 state passes the reference's feasibility test, common.cuh
+    kBallShrink)."""
+    g = golden
+    x = g["tv_x"]
+    if dtype == "fp64":
+        st = psb.TvProxState.cold(x.shape, 200, dtype=torch.float64)
+        psb.tv_prox(x, 0.25, st)
+        gap = psb.dual_gap_rof(x, st.q_warm, 0.25)
+        assert gap == pytest.approx(float(g["tv_gap"]), rel=0, abs=1e-13)
+    else:
+        rng = np.random.default_rng(11)
+        xs = rng.standard_normal((40, 52))
+        st = psb.TvProxState.cold(xs.shape, 60)
+        psb.tv_prox(torch.from_numpy(xs).float().cuda(), 0.3, st)
+        q = st.q_warm.astype(np.float64)  # the fp32 state, exactly
+        gap = psb.dual_gap_rof(xs, st.slots[0], 0.3)
+        ref = oc.rof_gap(xs, q, 0.3)
+        assert gap == pytest.approx(ref, rel=1e-6, abs=1e-11)
+        assert gap >= -1e-9
