@@ -316,19 +316,22 @@ __global__ void fgp2d_finalize_kernel(const T* __restrict__ x, int64_t xps, T* q
 //
 // A single 512 x 512 problem (configs 2 and 3i) runs one streaming launch per
 // inner iteration at ~6 us each: latency-bound, the grid is small.  Here a
-// 512-thread CTA loads a 64 x 64 window (a 48 x 48 output tile plus an
-// 8-pixel halo) of z, q_k and q_{k-1} into REGISTERS -- thread (warp row wr,
+// 512-thread CTA loads a 64 x 64 window (a 44 x 44 output tile plus a
+// 10-pixel halo) of z, q_k and q_{k-1} into REGISTERS -- thread (warp row wr,
 // warp column wc, lane) owns column 32 wc + lane, rows 8 wr .. 8 wr + 7, as
-// in the cluster kernel -- and runs TBI = 8 inner iterations on it: the
+// in the cluster kernel -- and runs TBI = 10 inner iterations on it: the
 // stencil has radius 1, so the exact region shrinks by one pixel per
-// iteration and the 48 x 48 interior is exact after 8.  Column neighbours
-// come from shuffles (plus shared memory between the two warp columns), row
-// neighbours from registers (plus shared memory between warp rows); two CTA
-// barriers per iteration; global image boundaries by per-pixel rules on the
-// global index.  8x fewer launches and ~(20 + 16) / 8 B of L2/HBM traffic per
-// pixel-iteration, for (64/48)^2 = 1.78x redundant halo arithmetic.  Per-pixel
-// arithmetic is fgp2d_item's (same expressions), so results equal the
-// streaming kernel's.
+// iteration and the 44 x 44 interior is exact after 10 (12 x 12 = 144 CTAs
+// at 512^2: one wave on 148 SMs).  Column neighbours come from shuffles (plus
+// shared memory between the two warp columns), row neighbours from registers
+// (plus shared memory between warp rows); two CTA barriers per iteration;
+// global image boundaries by per-pixel rules on the global index.  10x fewer
+// launches and ~(20 + 16) / 10 B of L2/HBM traffic per pixel-iteration, for
+// (64/44)^2 = 2.1x redundant halo arithmetic.  The per-pixel formulas are
+// fgp2d_item's; the compiled instruction sequences differ (FMA contraction
+// of the momentum / projection), so the results agree with the streaming
+// kernel to ~1e-6 absolute (tests/test_gpu_tb.py), both well inside the
+// oracle tolerance.
 constexpr int TBI = 10;                   // inner iterations per launch (halo width)
 constexpr int TBS = 64;                   // window side
 constexpr int TBT = TBS - 2 * TBI;        // output tile side (44: 12 x 12 = 144 CTAs at 512^2, one wave)
