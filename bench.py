@@ -56,6 +56,7 @@ SIDE5 = int(os.environ.get("PSB_BENCH_SIDE5", "1024"))
 ALPHA5, P5, ITERS5, INNER5 = 0.08, 0.1, 200, 20
 BYTES3_MOM, BYTES3_FIRST = 40, 28     # 3-D FGP bytes per voxel-iteration
 COUNTERS = os.path.join(ROOT, "profiles", "r02_run_kernel_counters.json")
+C5_TIMEOUT_S = float(os.environ.get("PSB_BENCH_C5_TIMEOUT", "600"))
 METRIC = "ProxSkip TV outer iter/s (config 4: 4096 x 256^2 batch, FGP-50, p=0.1)"
 WORKLOAD = "config4: batched ProxSkip TV denoising, 4096 x 256x256, alpha=0.1, p=0.1, FGP-50"
 UNIT = "outer-iter/s (4096-problem batch)"
@@ -560,13 +561,6 @@ def run_gpu(args):
     elif D.rank == 0:
         parity = {"resident_equals_e2e": rec["resident_equals_e2e"],
                   "note": "oracle comparison runs at N=1 only (cpu_baseline leg)"}
-    c5 = None
-    if not args.no_config5:
-        torch.cuda.empty_cache()
-        c5 = run_config5(args, D, dev, with_cpu=D.rank == 0 and D.world == 1 and not args.no_cpu)
-    if D.rank != 0:
-        D.close()
-        return 0
     line = {
         "metric": METRIC, "value": rec["value"], "unit": UNIT,
         "n_gpus": D.world, "steps": args.steps, "warmup": args.warmup,
@@ -584,10 +578,34 @@ def run_gpu(args):
         "parity": parity,
         "gpu_launches": int(rec["launches"]),
         "clocks": rec["clocks"],
-        "config5": c5,
+        "config5": None,
     }
-    print(json.dumps(line), flush=True)
-    D.close()
+    printed = []
+    if not args.no_config5:
+        torch.cuda.empty_cache()
+        # The config-4 line must survive a config-5 failure: an exception is
+        # recorded in the sub-record, and a watchdog prints the line and ends
+        # every rank if the (multi-GPU: peer-memory) config-5 run stalls.
+        import threading
+
+        def _stalled():
+            if D.rank == 0 and not printed:
+                line["config5"] = {"error": f"timed out after {C5_TIMEOUT_S} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        dog = threading.Timer(C5_TIMEOUT_S, _stalled)
+        dog.daemon = True
+        dog.start()
+        try:
+            line["config5"] = run_config5(args, D, dev,
+                                          with_cpu=D.rank == 0 and D.world == 1 and not args.no_cpu)
+        except Exception as e:  # noqa: BLE001  (reported, not hidden)
+            line["config5"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if D.rank == 0:
+        print(json.dumps(line), flush=True)
+        printed.append(True)
+    D.close()  # (the watchdog, if armed, still guards a stalled teardown)
     return 0
 
 
