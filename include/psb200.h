@@ -273,7 +273,9 @@ int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void
  *   problem to done[p / chunk] (device int32[n_chunks], zeroed) so the copy
  *   stream can psb_stream_wait_geq_u32 for 16 * (problems in the chunk)
  *   before the chunk's D2H copy.  ready[n_chunks] becomes 1 if a wait timed
- *   out (20 s).  Same results as psb_proxskip_denoise_run (bit-identical). */
+ *   out (20 s).  The run starts COLD: x = h = 0 and a zero warm start are
+ *   implied (x, h, q need not be initialised; the kernels write them).  Same
+ *   results as psb_proxskip_denoise_run from zeroed buffers (bit-identical). */
 int psb_proxskip_denoise_run_streamed(int dtype_outer, int dtype_fgp, void* x, const void* b,
                                       void* h, void* z, void* q, int64_t n, int H, int W,
                                       const uint8_t* coins_host, int K, double gamma, double p,

@@ -60,7 +60,7 @@ class BatchedTvDenoise:
     """N independent 0.5||u - b_i||^2 + alpha TV(u) problems on one GPU."""
 
     def __init__(self, b, alpha, inner_budget=50, *, precision="fp32", accelerated=True,
-                 nonneg=False):
+                 nonneg=False, cold_buffers=True):
         if alpha <= 0:
             raise ValueError("alpha must be positive")
         if inner_budget < 1:
@@ -75,10 +75,13 @@ class BatchedTvDenoise:
         self.accelerated = accelerated
         self.nonneg = nonneg
         self.dto, self.dtf = dto, dtf
-        self.x = torch.zeros_like(self.b)
-        self.h = torch.zeros_like(self.b)
+        # cold_buffers=False leaves x, h and the dual slots uninitialised (only
+        # for the streamed run, whose kernels imply a cold start)
+        alloc = torch.zeros if cold_buffers else torch.empty
+        self.x = alloc(self.b.shape, dtype=self.b.dtype, device="cuda")
+        self.h = alloc(self.b.shape, dtype=self.b.dtype, device="cuda")
         self.z = torch.empty((self.n, self.H, self.W), dtype=dtf, device="cuda")
-        self.slots = torch.zeros((self.n, 3, 2, self.H, self.W), dtype=dtf, device="cuda")
+        self.slots = alloc((self.n, 3, 2, self.H, self.W), dtype=dtf, device="cuda")
         self.last_weight = np.full(self.n, np.nan)
         self.prox_count = np.zeros(self.n, dtype=np.int64)
         self.bad = torch.full((self.n,), INT32_MAX, dtype=torch.int32, device="cuda")
@@ -201,8 +204,10 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
                          "of b's shape")
     dbg = os.environ.get("PSB_DEBUG_E2E") == "1"
     t0 = time.perf_counter() if dbg else 0.0
+    # the streamed run starts cold (the kernels imply x = h = 0 and a zero warm
+    # start): no 10 GB of zero-fills inside the call
     solver = BatchedTvDenoise(torch.empty((n, H, W), dtype=torch.float32, device="cuda"), alpha,
-                              inner_budget, precision="fp32")
+                              inner_budget, precision="fp32", cold_buffers=False)
     coins = coin_table(p, seeds, iters)
     t1 = time.perf_counter() if dbg else 0.0
     bounds = [(lo, min(n, lo + chunk)) for lo in range(0, n, chunk)]

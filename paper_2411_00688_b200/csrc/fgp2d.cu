@@ -717,6 +717,16 @@ __global__ void __launch_bounds__(SM_THREADS, 1) fgp_sm_run_kernel(SmRunArgs a) 
       if (tid == 0) chunk_wait(a.cs, p);
       __syncthreads();
     }
+    if (a.cs.ready) {  // a streamed run starts cold: x = h = 0, q_warm = 0 (not initialised)
+      const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int v = tid; v < NV; v += SM_THREADS) {
+        __stcg(reinterpret_cast<float4*>(xp) + v, zero);
+        __stcg(reinterpret_cast<float4*>(hp) + v, zero);
+        __stcg(reinterpret_cast<float4*>(q0) + v, zero);
+        __stcg(reinterpret_cast<float4*>(q0 + HW) + v, zero);
+      }
+      __syncthreads();
+    }
     const uint64_t t_claim = gtimer_ns();
     int kbad = 0x7fffffff;
     int kprev = -1;

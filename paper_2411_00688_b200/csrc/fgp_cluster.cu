@@ -367,15 +367,18 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   if (cr == 0 && tid == 0) t_claim = gtimer_ns();
   // stage this CTA's rows of x, b, h (each thread its own elements; the CTA
   // above reads row 0 after the next cluster barrier)
+  // (a streamed run starts cold: x = h = 0 and q_warm = 0 are implied and
+  // the device buffers are not initialised -- psb_proxskip_denoise_run_streamed)
+  const bool cold = a.cs.ready != nullptr;
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
     const int lr = rg * CRPT + t;
     const int64_t o = (int64_t)(row0 + t) * CW + j0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      sx[lr * CW + j0 + k] = xp[o + k];
+      sx[lr * CW + j0 + k] = cold ? TO(0) : xp[o + k];
       sb[lr * CW + j0 + k] = bp[o + k];
-      sh[lr * CW + j0 + k] = hp[o + k];
+      sh[lr * CW + j0 + k] = cold ? TO(0) : hp[o + k];
     }
   }
   // per column k: z, q_k, q_{k-1} as row pairs
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       rowref(z[k], t) = prox_input(sj);
       if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
         const int64_t o = (int64_t)(row0 + t) * CW + j0 + k;
-        float vy = q0[o], vx = q0[HW + o];
+        float vy = cold ? 0.f : q0[o], vx = cold ? 0.f : q0[HW + o];
         if (a.rep[p]) {
           const float sc = F::ball_scale(vy, vx, w);
           vy *= sc;
@@ -771,8 +774,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       const TO ho = sh[sj];
       const TO xo = skip_chain_px(sx[sj], sb[sj], ho, g, m, kprev + 1, &kbad);
       xp[o] = xo;
+      if (e1 > e0 || cold) hp[o] = ho;
       if (e1 > e0) {
-        hp[o] = ho;
         q0[o] = rowref(qky[k], t);
         q0[HW + o] = rowref(qkx[k], t);
       }
