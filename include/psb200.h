@@ -266,8 +266,9 @@ int psb_proxskip_denoise_run(int dtype_outer, int dtype_fgp, void* x, const void
 
 /* psb_proxskip_denoise_run_streamed: psb_proxskip_denoise_run (fp32 FGP,
  *   256x256, no graph, no log) whose kernels start before their inputs have
- *   arrived.  Problems form chunks of `chunk` (n_chunks * chunk >= n); the
- *   run kernels wait, per problem, until ready[p / chunk] != 0 (device
+ *   arrived.  Problems form chunks c = [bounds_host[c], bounds_host[c+1])
+ *   (host int64[n_chunks + 1], 0 .. n); the run kernels wait, per problem,
+ *   until ready[c] != 0 (device
  *   int32[n_chunks + 1], zeroed; the caller's copy stream writes 1 after the
  *   chunk's H2D copy with psb_stream_write_u32), and add 16 per finished
  *   problem to done[p / chunk] (device int32[n_chunks], zeroed) so the copy
@@ -282,7 +283,7 @@ int psb_proxskip_denoise_run_streamed(int dtype_outer, int dtype_fgp, void* x, c
                                       double alpha, int n_inner, int accelerated, int nonneg,
                                       double* last_weight_host, int64_t* prox_count_host,
                                       int32_t* bad_iter, const int32_t* ready, int32_t* done,
-                                      int chunk, int n_chunks, void* stream);
+                                      const int64_t* bounds_host, int n_chunks, void* stream);
 /* Stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32 with
  * GEQ), used to order copies against the streamed run without a host
  * round trip; psb_stream_memops_supported reports whether the driver has them. */
@@ -290,15 +291,16 @@ int psb_stream_memops_supported(int* out);
 int psb_stream_write_u32(void* stream, void* dptr, uint32_t value);
 int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value);
 /* psb_chunked_h2d / psb_chunked_d2h: the streamed batch's copies, enqueued in
- * one call each (items of item_bytes, chunks of `chunk` items).  H2D: copy
+ * one call each (items of item_bytes; chunk c = items [bounds[c], bounds[c+1]),
+ * bounds a host int64 array of n_chunks + 1).  H2D: copy
  * chunk c from page-locked host memory, then ready[c] = 1 (fenced stream
  * write).  D2H: wait until done[c] >= unit * (items in chunk c) (stream wait),
  * then copy chunk c to page-locked host memory.  Replaces the per-chunk copy
  * loop of run_proxskip_batched's streamed path. */
-int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_bytes, int64_t n_items,
-                    int64_t chunk, int32_t* ready, void* stream);
-int psb_chunked_d2h(void* dst_host, const void* src, int64_t item_bytes, int64_t n_items,
-                    int64_t chunk, const int32_t* done, uint32_t unit, void* stream);
+int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_bytes, const int64_t* bounds,
+                    int n_chunks, int32_t* ready, void* stream);
+int psb_chunked_d2h(void* dst_host, const void* src, int64_t item_bytes, const int64_t* bounds,
+                    int n_chunks, const int32_t* done, uint32_t unit, void* stream);
 
 /* Peer memory for the config-5 z-slab exchange (the reference has
  * no multi-GPU path -- this replaces the halo transfer of the decomposed

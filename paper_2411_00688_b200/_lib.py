@@ -88,12 +88,12 @@ SIGNATURES = {
                                  _vp, _vp, _vp, _i32, _vp, _vp],
     "psb_proxskip_denoise_run_streamed": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32,
                                           _vp, _i32, _dbl, _dbl, _dbl, _i32, _i32, _i32, _vp,
-                                          _vp, _vp, _vp, _vp, _i32, _i32, _vp],
+                                          _vp, _vp, _vp, _vp, _vp, _i32, _vp],
     "psb_stream_memops_supported": [_vp],
     "psb_stream_write_u32": [_vp, _vp, C.c_uint32],
     "psb_stream_wait_geq_u32": [_vp, _vp, C.c_uint32],
-    "psb_chunked_h2d": [_vp, _vp, _i64, _i64, _i64, _vp, _vp],
-    "psb_chunked_d2h": [_vp, _vp, _i64, _i64, _i64, _vp, C.c_uint32, _vp],
+    "psb_chunked_h2d": [_vp, _vp, _i64, _vp, _i32, _vp, _vp],
+    "psb_chunked_d2h": [_vp, _vp, _i64, _vp, _i32, _vp, C.c_uint32, _vp],
     "psb_cluster_max_active": [_vp],
     "psb_copy_async": [_vp, _vp, _i64, _vp],
     "psb_ipc_handle_size": [],

@@ -168,8 +168,8 @@ def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.
     chunks still compute.  Same arithmetic and results as the resident run."""
     seeds = np.asarray(seeds).reshape(-1)
     n = int(seeds.size)
-    if chunk is None:  # small chunks: the first input and the last result move fast
-        chunk = max(8, min(256, n // 128))
+    if chunk is None:
+        chunk = 256  # the middle chunks; the streamed path ramps up to and down from it
     shape = tuple(b.shape) if hasattr(b, "shape") else np.shape(b)
     # (streamed only for float32 host data: a dtype conversion would need a
     # kernel on the copy stream, which cannot run while the waiting run
@@ -187,6 +187,29 @@ def run_proxskip_batched(b, alpha, p, seeds, iters, inner_budget=50, *, gamma=1.
         AR.download_into(out, solver.x.to(out.dtype))
         return (out if isinstance(b, torch.Tensor) else out.numpy()), solver.prox_count.copy()
     return AR.like(solver.x, b), solver.prox_count.copy()
+
+
+def _chunk_edges(n, chunk):
+    """Chunk boundaries of a streamed batch: sizes ramp up 16, 32, ... to
+    ``chunk`` and back down at the end, so the first input arrives and the
+    last result leaves in a fraction of a millisecond while the middle of the
+    batch moves in few large copies."""
+    ramp = []
+    c = 16
+    while c < chunk:
+        ramp.append(c)
+        c *= 2
+    sizes_lo, sizes_hi, total = [], [], 0
+    for c in ramp:  # leading and trailing ramps, while the batch allows
+        if total + 2 * c > n:
+            break
+        sizes_lo.append(c)
+        sizes_hi.append(c)
+        total += 2 * c
+    mid = n - total
+    sizes = sizes_lo + [chunk] * (mid // chunk) + ([mid % chunk] if mid % chunk else []) \
+        + sizes_hi[::-1]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
 
 
 def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=None):
@@ -210,8 +233,10 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
                               inner_budget, precision="fp32", cold_buffers=False)
     coins = coin_table(p, seeds, iters)
     t1 = time.perf_counter() if dbg else 0.0
-    bounds = [(lo, min(n, lo + chunk)) for lo in range(0, n, chunk)]
+    edges = _chunk_edges(n, chunk)
+    bounds = list(zip(edges[:-1], edges[1:]))
     nc = len(bounds)
+    edges_h = np.ascontiguousarray(edges, dtype=np.int64)
     flags = torch.zeros(2 * nc + 1, dtype=torch.int32, device="cuda")  # ready[nc + 1], done[nc]
     ready, done = flags[:nc + 1], flags[nc + 1:]
     main = torch.cuda.current_stream()
@@ -226,8 +251,8 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
     #    on the run kernels making progress (serialised execution under
     #    CUDA_LAUNCH_BLOCKING=1, compute-sanitizer or ncu stays correct)
     if src.is_pinned():  # one native call enqueues every chunk (DMA, no kernels)
-        L.call("psb_chunked_h2d", L.ptr(solver.b), L.C.c_void_p(src.data_ptr()), item, n, chunk,
-               L.ptr(ready), L.C.c_void_p(h2d.cuda_stream))
+        L.call("psb_chunked_h2d", L.ptr(solver.b), L.C.c_void_p(src.data_ptr()), item,
+               edges_h.ctypes.data_as(L.C.c_void_p), nc, L.ptr(ready), L.C.c_void_p(h2d.cuda_stream))
     else:
         cs = L.C.c_void_p(h2d.cuda_stream)
         with torch.cuda.stream(h2d):
@@ -241,14 +266,15 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
            float(gamma), float(p), float(alpha), inner_budget, 1, 0,
            solver.last_weight.ctypes.data_as(L.C.c_void_p),
            solver.prox_count.ctypes.data_as(L.C.c_void_p), L.ptr(solver.bad), L.ptr(ready),
-           L.ptr(done), chunk, nc, L.stream())
+           L.ptr(done), edges_h.ctypes.data_as(L.C.c_void_p), nc, L.stream())
     # 3) results on their own stream, chunk by chunk, as soon as the chunk's
     #    problems are done (stream wait on the device counter): they leave
     #    while later inputs still arrive
     pinned = out.is_pinned()
     if pinned:
-        L.call("psb_chunked_d2h", L.C.c_void_p(out.data_ptr()), L.ptr(solver.x), item, n, chunk,
-               L.ptr(done), 16, L.C.c_void_p(d2h.cuda_stream))
+        L.call("psb_chunked_d2h", L.C.c_void_p(out.data_ptr()), L.ptr(solver.x), item,
+               edges_h.ctypes.data_as(L.C.c_void_p), nc, L.ptr(done), 16,
+               L.C.c_void_p(d2h.cuda_stream))
     else:
         cs = L.C.c_void_p(d2h.cuda_stream)
         with torch.cuda.stream(d2h):
@@ -268,7 +294,7 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
         t3 = time.perf_counter()
         print(f"[psb e2e] setup {1e3 * (t1 - t0):.1f} ms, enqueue {1e3 * (t2 - t1):.1f} ms, "
               f"run {1e3 * (t3 - t2):.1f} ms, device {start.elapsed_time(end):.1f} ms "
-              f"({nc} chunks of {chunk})", flush=True)
+              f"({nc} chunks, sizes {np.diff(edges).tolist()})", flush=True)
     if int(ready[nc].item()) != 0:
         raise RuntimeError("streamed run: an input chunk never arrived (device wait timed out)")
     solver.check_finite()

@@ -215,13 +215,14 @@ __device__ __forceinline__ T skip_chain_px(T x, T b, T h, T g, int m, int kfirst
 struct ChunkSync {
   const int32_t* ready = nullptr;  // null: inputs already resident
   int32_t* done = nullptr;
-  int chunk = 0;
+  const int32_t* chunk_of = nullptr;  // [n] chunk index of each problem (device)
+  const int64_t* bounds = nullptr;    // [n_chunks + 1] chunk starts (HOST, driver only)
   int n_chunks = 0;
 };
 
 __device__ __forceinline__ void chunk_wait(const ChunkSync& cs, int p) {
   if (cs.ready == nullptr) return;
-  const int32_t* f = cs.ready + p / cs.chunk;
+  const int32_t* f = cs.ready + cs.chunk_of[p];
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   const int32_t* err = cs.ready + cs.n_chunks;
@@ -247,7 +248,7 @@ __device__ __forceinline__ void chunk_done(const ChunkSync& cs, int p, int add, 
   if (cs.done == nullptr) return;
   __threadfence();
   __syncthreads();
-  if (leader) atomicAdd(cs.done + p / cs.chunk, add);
+  if (leader) atomicAdd(cs.done + cs.chunk_of[p], add);
 }
 
 // ---- dynamic problem queue (run drivers, configs 1 / 4) ----------------------

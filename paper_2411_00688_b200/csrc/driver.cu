@@ -162,11 +162,20 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                            n_inner <= 1024 && !(no_cluster && no_cluster[0] == '1') &&
                            x_hist == nullptr && !fid.fista;
   PSB_REQUIRE(!fid.fista || (fid.xprev && fid.xbar), "fista: x_prev / xbar buffers missing");
-  const ChunkSync cs = chunks ? *chunks : ChunkSync{};
-  PSB_REQUIRE(cs.ready == nullptr || (use_cluster && !use_graph && cs.chunk > 0 && cs.done &&
-                                      (int64_t)cs.n_chunks * cs.chunk >= n),
+  ChunkSync cs = chunks ? *chunks : ChunkSync{};
+  PSB_REQUIRE(cs.ready == nullptr ||
+                  (use_cluster && !use_graph && cs.done && cs.bounds && cs.n_chunks > 0 &&
+                   cs.bounds[0] == 0 && cs.bounds[cs.n_chunks] == n),
               "streamed run: needs the cluster path (256x256, fp32 FGP, no graph) and a "
               "chunking that covers the batch");
+  std::vector<int32_t> chunk_of;  // problem -> input chunk (streamed runs)
+  if (cs.ready) {
+    chunk_of.resize(n);
+    for (int c = 0; c < cs.n_chunks; ++c) {
+      PSB_REQUIRE(cs.bounds[c] <= cs.bounds[c + 1], "streamed run: chunk bounds not ascending");
+      for (int64_t i = cs.bounds[c]; i < cs.bounds[c + 1]; ++i) chunk_of[i] = c;
+    }
+  }
   // FISTA's outer momentum (solvers.py:156-160): beta_k = (t_k - 1)/t_{k+1}, t_0 = 1
   std::vector<double> fbeta;
   if (fid.fista) {
@@ -215,9 +224,9 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
     order.resize(n);
     for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
-    const int64_t chunk = cs.ready ? cs.chunk : n;
+    auto chunk_id = [&](int32_t i) { return cs.ready ? chunk_of[i] : 0; };
     std::stable_sort(order.begin(), order.end(), [&](int32_t u, int32_t v) {
-      if (u / chunk != v / chunk) return u / chunk < v / chunk;
+      if (chunk_id(u) != chunk_id(v)) return chunk_id(u) < chunk_id(v);
       return cost(u) > cost(v);
     });
     qcost.resize(n);
@@ -255,6 +264,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     o_cost = put(qcost.data(), qcost.size() * sizeof(float));
     o_suffix = put(qsuffix.data(), qsuffix.size() * sizeof(float));
   }
+  const size_t o_chunkof = chunk_of.empty() ? 0 : put(chunk_of.data(), chunk_of.size() * sizeof(int32_t));
   DevBuf d_sched;
   d_sched.st = user_stream;
   PSB_CUDA(cudaMallocAsync(&d_sched.p, std::max<size_t>(pack.size(), 16), user_stream));
@@ -262,6 +272,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                            user_stream));
   // (pageable source: cudaMemcpyAsync stages `pack` before it returns)
   unsigned char* dev = static_cast<unsigned char*>(d_sched.p);
+  if (!chunk_of.empty()) cs.chunk_of = reinterpret_cast<const int32_t*>(dev + o_chunkof);
   const uint8_t* coins_d = dev + o_coins;
   const int32_t* act_d = reinterpret_cast<const int32_t*>(dev + o_act);
   const uint8_t* rep_d = dev + o_rep;
@@ -466,13 +477,13 @@ extern "C" int psb_proxskip_denoise_run_streamed(
     int dtype_outer, int dtype_fgp, void* x, const void* b, void* h, void* z, void* q, int64_t n,
     int H, int W, const uint8_t* coins_host, int K, double gamma, double p, double alpha,
     int n_inner, int accelerated, int nonneg, double* last_weight_host, int64_t* prox_count_host,
-    int32_t* bad_iter, const int32_t* ready, int32_t* done, int chunk, int n_chunks,
-    void* stream) {
+    int32_t* bad_iter, const int32_t* ready, int32_t* done, const int64_t* bounds_host,
+    int n_chunks, void* stream) {
   psb::Fidelity fid;
   psb::ChunkSync cs;
   cs.ready = ready;
   cs.done = done;
-  cs.chunk = chunk;
+  cs.bounds = bounds_host;
   cs.n_chunks = n_chunks;
   return psb::proxskip_tv_run(fid, dtype_outer, dtype_fgp, x, b, h, z, q, n, H, W, coins_host, K,
                               gamma, p, alpha, n_inner, accelerated, nonneg, last_weight_host,
@@ -531,14 +542,15 @@ extern "C" int psb_stream_wait_geq_u32(void* stream, void* dptr, uint32_t value)
 // per chunk.  H2D: copy chunk c, then ready[c] = 1 (fenced write).  D2H (on
 // its own stream, so results leave while later inputs still arrive): wait
 // until done[c] >= unit * (items in chunk c), then copy chunk c back.
-extern "C" int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_bytes, int64_t n_items,
-                               int64_t chunk, int32_t* ready, void* stream) {
-  PSB_REQUIRE(item_bytes > 0 && n_items >= 0 && chunk > 0, "chunked h2d: bad sizes");
+extern "C" int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_bytes,
+                               const int64_t* bounds, int n_chunks, int32_t* ready, void* stream) {
+  PSB_REQUIRE(item_bytes > 0 && n_chunks >= 0 && bounds, "chunked h2d: bad sizes");
   static StreamValueFn wr = stream_fn("cuStreamWriteValue32");
   if (!wr) return psb::fail(PSB_ERR_CUDA, "cuStreamWriteValue32 unavailable");
   auto st = psb::as_stream(stream);
-  for (int64_t c = 0, lo = 0; lo < n_items; ++c, lo += chunk) {
-    const int64_t k = std::min(chunk, n_items - lo);
+  for (int c = 0; c < n_chunks; ++c) {
+    const int64_t lo = bounds[c], k = bounds[c + 1] - bounds[c];
+    PSB_REQUIRE(k >= 0, "chunked h2d: bounds not ascending");
     PSB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + lo * item_bytes,
                              static_cast<const char*>(src_host) + lo * item_bytes,
                              (size_t)(k * item_bytes), cudaMemcpyHostToDevice, st));
@@ -548,14 +560,16 @@ extern "C" int psb_chunked_h2d(void* dst, const void* src_host, int64_t item_byt
   return PSB_OK;
 }
 
-extern "C" int psb_chunked_d2h(void* dst_host, const void* src, int64_t item_bytes, int64_t n_items,
-                               int64_t chunk, const int32_t* done, uint32_t unit, void* stream) {
-  PSB_REQUIRE(item_bytes > 0 && n_items >= 0 && chunk > 0, "chunked d2h: bad sizes");
+extern "C" int psb_chunked_d2h(void* dst_host, const void* src, int64_t item_bytes,
+                               const int64_t* bounds, int n_chunks, const int32_t* done,
+                               uint32_t unit, void* stream) {
+  PSB_REQUIRE(item_bytes > 0 && n_chunks >= 0 && bounds, "chunked d2h: bad sizes");
   static StreamValueFn wt = stream_fn("cuStreamWaitValue32");
   if (!wt) return psb::fail(PSB_ERR_CUDA, "cuStreamWaitValue32 unavailable");
   auto st = psb::as_stream(stream);
-  for (int64_t c = 0, lo = 0; lo < n_items; ++c, lo += chunk) {
-    const int64_t k = std::min(chunk, n_items - lo);
+  for (int c = 0; c < n_chunks; ++c) {
+    const int64_t lo = bounds[c], k = bounds[c + 1] - bounds[c];
+    PSB_REQUIRE(k >= 0, "chunked d2h: bounds not ascending");
     if (wt(stream, reinterpret_cast<unsigned long long>(done + c), unit * (uint32_t)k, 0x0) != 0)
       return psb::fail(PSB_ERR_CUDA, "cuStreamWaitValue32 failed");
     PSB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst_host) + lo * item_bytes,
