@@ -109,6 +109,16 @@ __device__ __forceinline__ void store_xbar_copies(void* xT, float* xpad, int n, 
   }
 }
 
+// fp32 bilinear tap sum of one sample: (1-fy)((1-fx) a + fx b) + fy((1-fx) c + fx d)
+// -- the reference's four tap weights (operators.py:247-252) in nested form:
+// 6 flops, and the per-lane accumulator sees one add per sample (independent
+// samples overlap).  A tap of weight 0 or outside the image adds 0.
+__device__ __forceinline__ float bilerp(float fx, float fy, float a, float b, float c, float d) {
+  const float gx = 1.f - fx, gy = 1.f - fy;
+  const float r0 = fmaf(fx, b, gx * a), r1 = fmaf(fx, d, gx * c);
+  return fmaf(fy, r1, gy * r0);
+}
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T acc) {
 #pragma unroll
@@ -182,12 +192,8 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
         const double fx0 = floor(px), fy0 = floor(py);
         const int x0 = (int)fx0, y0 = (int)fy0;
         const float fx = (float)(px - fx0), fy = (float)(py - fy0);
-        const float gx = 1.f - fx, gy = 1.f - fy;
         const float* ur = srcp + y0 * ayp + x0 * axp;
-        acc = fmaf(gy * gx, ur[0], acc);
-        acc = fmaf(gy * fx, ur[axp], acc);
-        acc = fmaf(fy * gx, ur[ayp], acc);
-        acc = fmaf(fy * fx, ur[axp + ayp], acc);
+        acc += bilerp(fx, fy, ur[0], ur[axp], ur[ayp], ur[axp + ayp]);
       }
       return warp_sum(acc);
     }
@@ -206,13 +212,11 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
       const int x0 = (int)fx0, y0 = (int)fy0;
       if (x0 < -1 || x0 >= n || y0 < -1 || y0 >= n) continue;
       const float fx = (float)(px - fx0), fy = (float)(py - fy0);
-      const float gx = 1.f - fx, gy = 1.f - fy;
       const bool xa = x0 >= 0, xb = x0 + 1 < n, ya = y0 >= 0, yb = y0 + 1 < n;
       const float* ur = src + y0 * ay + x0 * ax;
-      if (ya && xa) acc = fmaf(gy * gx, ur[0], acc);
-      if (ya && xb && fx > 0.f) acc = fmaf(gy * fx, ur[ax], acc);
-      if (yb && xa && fy > 0.f) acc = fmaf(fy * gx, ur[ay], acc);
-      if (yb && xb && fx > 0.f && fy > 0.f) acc = fmaf(fy * fx, ur[ax + ay], acc);
+      // taps outside the image contribute 0 (the padded path reads zeros)
+      acc += bilerp(fx, fy, (ya && xa) ? ur[0] : 0.f, (ya && xb) ? ur[ax] : 0.f,
+                    (yb && xa) ? ur[ay] : 0.f, (yb && xb) ? ur[ax + ay] : 0.f);
     }
     return warp_sum(acc);
   }
