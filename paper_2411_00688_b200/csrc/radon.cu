@@ -480,7 +480,7 @@ __global__ void pdhg1_primal_kernel(Geo G, T* __restrict__ x, const T* __restric
 
 // dual, fidelity block: y_A <- ((y_A + tau A xbar) - tau b) / (1 + tau)   (problems.py:143-144)
 template <class T>
-__global__ void pdhg_dual_fid_kernel(Geo G, const T* __restrict__ xbar, T* __restrict__ y,
+__global__ void __launch_bounds__(256, 6) pdhg_dual_fid_kernel(Geo G, const T* __restrict__ xbar, T* __restrict__ y,
                                      const T* __restrict__ b, T tau0, const T* __restrict__ tau_arr) {
   const int ray = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
