@@ -539,12 +539,14 @@ def run_proxskip_slabs(slabs, coins, *, gamma=1.0, p=0.1, exchange=None, fgp_eve
 
 
 def proxskip_denoise3d(b, alpha, p, seed, iters, inner_budget=20, *, n_slabs=1, precision="fp32",
-                       step=STEP_3D, defer_skips=True, exchange="direct"):
+                       step=STEP_3D, defer_skips=True, exchange="direct", out=None):
     """Single-process config-5 entry point (``n_slabs`` > 1 emulates the slab
     decomposition on one GPU).  ``exchange``: "direct" (edge kernels store
     into the neighbours' rings, one stream), "copy" (send buffers + copies:
     the NCCL data path), "peer" (one stream per slab, flags in device memory:
-    the multi-GPU peer-memory protocol).  Returns x in the input's currency."""
+    the multi-GPU peer-memory protocol).  Returns x in the input's currency;
+    ``out`` (optional, CPU input only): a contiguous CPU tensor of b's shape
+    and the state dtype that receives x (page-locked: one DMA)."""
     t = AR.to_dev(b, PRECISIONS[precision][0])
     Dg = t.shape[0]
     slabs = []
@@ -559,7 +561,14 @@ def proxskip_denoise3d(b, alpha, p, seed, iters, inner_budget=20, *, n_slabs=1, 
         raise ValueError(f"proxskip_denoise3d: unknown exchange {exchange!r}")
     xs = run_proxskip_slabs(slabs, SkipConfig(p, seed).coins(iters), gamma=1.0, p=p,
                             defer_skips=defer_skips, exchange=ex)
-    return AR.like(torch.cat(xs, dim=0), b), slabs
+    x = xs[0] if len(xs) == 1 else torch.cat(xs, dim=0)
+    if out is not None:
+        if (not isinstance(out, torch.Tensor) or out.is_cuda or tuple(out.shape) != tuple(x.shape)
+                or out.dtype != x.dtype or not out.is_contiguous()):
+            raise ValueError("proxskip_denoise3d: out must be a contiguous CPU tensor of b's shape "
+                             "and the state dtype")
+        return AR.download_into(out, x), slabs
+    return AR.like(x, b), slabs
 
 
 class TvProxState3D:

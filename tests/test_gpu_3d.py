@@ -150,3 +150,17 @@ def test_peer_exchange_across_processes(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"bitwise_equal_whole_volume": true' in r.stdout
+
+
+def test_proxskip_denoise3d_into_caller_buffer():
+    """out=: x lands in the caller's (page-locked) CPU buffer -- the same bits
+    as the default return; a wrong buffer is a ValueError."""
+    vol = phantoms.random_ellipsoids((24, 20, 36), 5, np.random.default_rng(8))
+    b = torch.from_numpy(phantoms.add_noise(vol, 0.1, 8).astype(np.float32)).pin_memory()
+    x_ref, _ = v3.proxskip_denoise3d(b, 0.08, 0.3, 0, 9, 4)
+    out = torch.full(b.shape, float("nan"), dtype=torch.float32).pin_memory()
+    x, _ = v3.proxskip_denoise3d(b, 0.08, 0.3, 0, 9, 4, out=out)
+    assert x is out
+    assert torch.equal(out, x_ref)
+    with pytest.raises(ValueError):
+        v3.proxskip_denoise3d(b, 0.08, 0.3, 0, 9, 4, out=torch.empty((3, 3, 3)))
