@@ -39,6 +39,20 @@ namespace cg = cooperative_groups;
 
 namespace psb {
 
+#ifdef PSB_DBG_PHASES  // timing experiment: per-phase ns of one thread per role
+__device__ unsigned long long g_phase_ns[16];
+#define PHASE_MARK(v) uint64_t v = gtimer_ns()
+#define PHASE_ADD(slot, t0, t1)                                                 \
+  do {                                                                         \
+    if (blockIdx.x == 0 && (tid == 0 || tid == 128 || tid == 384))             \
+      atomicAdd(&g_phase_ns[(slot) * 4 + (tid == 0 ? 0 : tid == 128 ? 1 : 2)], \
+                (unsigned long long)((t1) - (t0)));                            \
+  } while (0)
+#else
+#define PHASE_MARK(v)
+#define PHASE_ADD(slot, t0, t1)
+#endif
+
 namespace {
 
 constexpr int CW = 256;    // image width
@@ -360,6 +374,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   TO* hp = a.h + (int64_t)p * HW;
   float* q0 = a.q + (int64_t)p * a.qps;
   const int e0 = a.ev_off[p], e1 = a.ev_off[p + 1];
+  const bool rep = a.rep[p];
   if (a.cs.ready) {  // this problem's input chunk has arrived
     if (tid == 0) chunk_wait(a.cs, p);
     __syncthreads();
@@ -370,6 +385,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   // (a streamed run starts cold: x = h = 0 and q_warm = 0 are implied and
   // the device buffers are not initialised -- psb_proxskip_denoise_run_streamed)
   const bool cold = a.cs.ready != nullptr;
+  // per column k: z, q_k, q_{k-1} as row pairs
+  float2 z[2][NP], qky[2][NP], qkx[2][NP], qmy[2][NP], qmx[2][NP];
+  // the warm-start duals (slot 0) are loaded here with x, b, h so the first
+  // prox call does not pay a second HBM round trip
 #pragma unroll
   for (int t = 0; t < CRPT; ++t) {
     const int lr = rg * CRPT + t;
@@ -379,10 +398,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       sx[lr * CW + j0 + k] = cold ? TO(0) : xp[o + k];
       sb[lr * CW + j0 + k] = bp[o + k];
       sh[lr * CW + j0 + k] = cold ? TO(0) : hp[o + k];
+      rowref(qky[k], t) = cold || e1 == e0 ? 0.f : q0[o + k];
+      rowref(qkx[k], t) = cold || e1 == e0 ? 0.f : q0[HW + o + k];
     }
   }
-  // per column k: z, q_k, q_{k-1} as row pairs
-  float2 z[2][NP], qky[2][NP], qkx[2][NP], qmy[2][NP], qmx[2][NP];
   int kbad = 0x7fffffff;
   int kprev = -1;
   for (int e = e0; e < e1; ++e) {
@@ -392,6 +411,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   // (no cluster-wide barrier per prox call: the only data crossing CTAs are
   // the halo rows and the z row, each tracked by the receiver's mbarrier)
   __syncthreads();
+  PHASE_MARK(ph_a);
   // ---- prologue: skips, prox input, warm start ------------------------------
   // The m skipped iterations since the last prox call (skip.py:68), executed
   // in the reference's op order; x after them goes back to shared memory for
@@ -410,10 +430,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
       const int lr = rg * CRPT + t;
       const int sj = lr * CW + j0 + k;
       rowref(z[k], t) = prox_input(sj);
-      if (e == e0) {  // warm start from HBM (slot 0), re-projected if the weight changed
-        const int64_t o = (int64_t)(row0 + t) * CW + j0 + k;
-        float vy = cold ? 0.f : q0[o], vx = cold ? 0.f : q0[HW + o];
-        if (a.rep[p]) {
+      if (e == e0) {  // warm start (staged above), re-projected if the weight changed
+        float vy = rowref(qky[k], t), vx = rowref(qkx[k], t);
+        if (rep) {
           const float sc = F::ball_scale(vy, vx, w);
           vy *= sc;
           vx *= sc;
@@ -699,6 +718,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
         }
     }
   };
+  PHASE_MARK(ph_b);
   if (rg_top)
     run_inner(std::integral_constant<int, 0>{});
   else if (rg_bot)
@@ -706,6 +726,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   else
     run_inner(std::integral_constant<int, 1>{});
 
+  PHASE_MARK(ph_c);
   // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -------------
   __syncthreads();  // every group is past its last inner iteration's reads
   const unsigned pe = recv_rows(round0 + a.n_inner);
@@ -761,6 +782,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster_run_kernel(RunArgs<TO
   }
   if (!ok) kbad = min(kbad, kk);
   kprev = kk;
+  PHASE_MARK(ph_d);
+  PHASE_ADD(0, ph_a, ph_b);
+  PHASE_ADD(1, ph_b, ph_c);
+  PHASE_ADD(2, ph_c, ph_d);
   }  // prox calls
 
   // ---- trailing skips, write-back -------------------------------------------
@@ -855,6 +880,15 @@ int cluster_run(int dto, void* x, const void* b, void* h, void* q, int64_t qps,
 }
 
 }  // namespace psb
+
+#ifdef PSB_DBG_PHASES
+extern "C" int psb_debug_phases(double* out16) {
+  unsigned long long h[16];
+  cudaMemcpyFromSymbol(h, psb::g_phase_ns, sizeof(h));
+  for (int i = 0; i < 16; ++i) out16[i] = (double)h[i];
+  return 0;
+}
+#endif
 
 extern "C" int psb_cluster_max_active(int* out) {
   using namespace psb;
