@@ -119,18 +119,81 @@ __device__ __forceinline__ float bilerp(float fx, float fy, float a, float b, fl
   return fmaf(fy, r1, gy * r0);
 }
 
+// Rays per warp of the forward gathers at angle (c, s).  A warp serves RG
+// adjacent bins of one angle with L = 32 / RG lanes each (lane q of a group
+// takes the ray's samples q, q + L, ...).  Lanes along one ray (RG = 1) load
+// from one memory row when the ray runs along the row direction of the copy
+// it reads (xbar or its transpose), but a diagonal ray's 32 consecutive
+// samples cross ~23 rows -- ~23 L1 wavefronts per tap load.  A 4 x 8 or 8 x 4
+// patch of (bin, step) lattice points spans ~9 rows at any angle.  RG by the
+// tangent of the ray's angle to the nearest axis: the thresholds minimise the
+// distinct 128-B lines per tap load of config 3's 60 angles in a host model
+// of these addresses (12.2 -> 7.0 lines on average; 21 -> 8.7 at 45 deg).
+// fp64 (the exact parity path) keeps RG = 1.
+__device__ __forceinline__ int fwd_lg_rays_per_warp(double c, double s) {  // log2 RG
+  const double ac = fabs(c), as = fabs(s);
+  const double mn = fmin(ac, as), mx = fmax(ac, as);
+  return mn < 0.0787 * mx ? 0 : mn < 0.240 * mx ? 1 : mn < 0.854 * mx ? 2 : 3;
+}
+
+// sum over the 2^lgL lanes of each aligned lane segment (valid in its first lane)
 template <class T>
-__device__ __forceinline__ T warp_sum(T acc) {
+__device__ __forceinline__ T seg_sum(T acc, int lgL) {
+  const int L = 1 << lgL;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  for (int o = 16; o > 0; o >>= 1)
+    if (o < L) acc += __shfl_down_sync(0xffffffffu, acc, o, L);
   return acc;
 }
 
-// Forward projection of one ray; the result is valid in lane 0 and is a
-// deterministic shuffle reduction.
+// Sample range [is_lo, is_hi] of ray (c, s, ib) that can deposit into the
+// image: px, py in [-1, n) with px = A - st*s, py = B + st*c is an interval
+// of st, widened by a 2-sample margin (the exact per-sample test of the
+// unpadded paths stays the arbiter; reciprocals instead of divisions move
+// the ends by an ulp at most).  Empty: is_hi < is_lo.
+__device__ __forceinline__ int2 ray_range(const Geo& G, double c, double s, int ib) {
+  const int n = G.n;
+  double lo = -G.half_span, hi = G.half_span;
+  const double o = G.off[ib];
+  const double av[2] = {o * c + G.center, o * s + G.center}, kv[2] = {-s, c};
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const double a = av[d], k = kv[d];
+    if (fabs(k) < 1e-9) {
+      if (a < -2.0 || a > n + 1.0) hi = lo - 1.0;
+      continue;
+    }
+    const double ik = __drcp_rn(k);
+    double t0 = (-1.0 - a) * ik, t1 = ((double)n - a) * ik;
+    if (t0 > t1) {
+      const double tt = t0;
+      t0 = t1;
+      t1 = tt;
+    }
+    lo = fmax(lo, t0);
+    hi = fmin(hi, t1);
+  }
+  int2 rg = make_int2(0, -1);
+  if (lo <= hi) {
+    const double ids = __drcp_rn(G.dstep);
+    rg.x = max(0, (int)floor((lo + G.half_span) * ids) - 2);
+    rg.y = min(G.ns - 1, (int)ceil((hi + G.half_span) * ids) + 2);
+  }
+  return rg;
+}
+
+// Forward projection of ray (ia, ib) (samples is_lo..is_hi, ray_range) by
+// the L lanes of its group (lane q), part r of RG (the lane's sample chain
+// j = 0, 1, ... cut into RG contiguous pieces): returns this lane's partial
+// sum; seg_sum over the group and the sum over the RG parts in order
+// (fwd_block_sum) complete it in a fixed order -- deterministic, no atomics.
+// The chain starts at a multiple of L, so every lane visits the same
+// samples as a loop over [0, ns) minus some that deposit nothing.
 template <class T>
 __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int ia, int ib,
-                                     int lane, const T* __restrict__ uT = nullptr) {
+                                     int is_lo, int is_hi, int q, int lgL, int r, int lgR,
+                                     const T* __restrict__ uT = nullptr) {
+  const int L = 1 << lgL;
   const double c = G.cs[ia], s = G.sn[ia];
   const int n = G.n;
   // tap addresses: u(y, x) = u[y n + x], or uT[x n + y] for steep rays
@@ -138,39 +201,18 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
   const T* src = tr ? uT : u;
   const int ax = tr ? n : 1, ay = tr ? 1 : n;  // address strides of x, y
   T acc = T(0);
-  // Samples that can deposit into the image have px, py in [-1, n).  With
-  // px = A - st*s, py = B + st*c that is an interval of st, computed here with
-  // a 2-sample margin (the exact per-sample test below stays the arbiter).
-  // The loop starts at a multiple of 32, so every lane visits the same
-  // samples as a loop over [0, ns) minus some that deposit nothing: the
-  // per-lane sums, and therefore the result, are bit-identical.
-  double lo = -G.half_span, hi = G.half_span;
-  {
-    const double o = G.off[ib];
-    const double av[2] = {o * c + G.center, o * s + G.center}, kv[2] = {-s, c};
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const double a = av[d], k = kv[d];
-      if (fabs(k) < 1e-9) {
-        if (a < -2.0 || a > n + 1.0) hi = lo - 1.0;
-        continue;
-      }
-      double t0 = (-1.0 - a) / k, t1 = ((double)n - a) / k;
-      if (t0 > t1) {
-        const double tt = t0;
-        t0 = t1;
-        t1 = tt;
-      }
-      lo = fmax(lo, t0);
-      hi = fmin(hi, t1);
-    }
-  }
-  int is_lo = 0, is_hi = -1;
-  if (lo <= hi) {
-    is_lo = max(0, (int)floor((lo + G.half_span) / G.dstep) - 2);
-    is_hi = min(G.ns - 1, (int)ceil((hi + G.half_span) / G.dstep) + 2);
-  }
+  const int base = is_lo & ~(L - 1), is0 = base + q;
+  const int chunk = ((base <= is_hi ? ((is_hi - base) >> lgL) + 1 : 0) + (1 << lgR) - 1) >> lgR;
+  const int jb = r * chunk;
+  const int nj = min(is0 <= is_hi ? ((is_hi - is0) >> lgL) + 1 : 0, jb + chunk);
   if constexpr (sizeof(T) == 4) {
+    double px0, py0;
+    sample_pos(G, c, s, ib, min(is0, G.ns - 1), px0, py0);
+    // each lane's first sample position exactly as the reference computes
+    // it, then the lattice step along the ray (L samples per lane step) as
+    // one fp64 FMA per coordinate; the fractional offsets and the bilinear
+    // weights in fp32 (weights agree with the fp64 path to ~1e-7)
+    const double sx = -(double)L * G.dstep * s, sy = (double)L * G.dstep * c;
     if (G.xpad != nullptr) {
       // padded copies: the same positions, weights and FMA order as below,
       // without the per-sample / per-tap tests
@@ -178,15 +220,10 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
       const bool trp = fabs(c) > fabs(s);
       const float* srcp = G.xpad + (trp ? (size_t)wp * wp : 0) + PADB * wp + PADB;
       const int axp = trp ? wp : 1, ayp = trp ? 1 : wp;
-      const int is0 = (is_lo & ~31) + lane;
-      const int nj = is0 <= is_hi ? (is_hi - is0) / 32 + 1 : 0;
-      // (a lane's samples before is_lo lie up to 31 steps outside the image
-      // and deposit nothing: start at the first one >= is_lo, whose taps --
-      // like every sample up to is_hi -- fall inside the zero border)
-      const int js = is0 < is_lo ? (is_lo - is0 + 31) / 32 : 0;
-      double px0, py0;
-      sample_pos(G, c, s, ib, min(is0, G.ns - 1), px0, py0);
-      const double sx = -32.0 * G.dstep * s, sy = 32.0 * G.dstep * c;
+      // (a lane's samples before is_lo lie up to L - 1 steps outside the
+      // image and deposit nothing: start at the first one >= is_lo, whose
+      // taps -- like every sample up to is_hi -- fall inside the zero border)
+      const int js = max(jb, is0 < is_lo ? (is_lo - is0 + L - 1) >> lgL : 0);
       for (int j = js; j < nj; ++j) {
         const double px = fma((double)j, sx, px0), py = fma((double)j, sy, py0);
         const double fx0 = floor(px), fy0 = floor(py);
@@ -195,18 +232,9 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
         const float* ur = srcp + y0 * ayp + x0 * axp;
         acc += bilerp(fx, fy, ur[0], ur[axp], ur[ayp], ur[axp + ayp]);
       }
-      return warp_sum(acc);
+      return acc;
     }
-    // fp32 state: each lane's first sample position exactly as the reference
-    // computes it, then the lattice step along the ray (32 samples per lane
-    // step) as one fp64 FMA per coordinate; the fractional offsets and the
-    // bilinear weights in fp32 (weights agree with the fp64 path to ~1e-7)
-    const int is0 = (is_lo & ~31) + lane;
-    const int nj = is0 <= is_hi ? (is_hi - is0) / 32 + 1 : 0;
-    double px0, py0;
-    sample_pos(G, c, s, ib, min(is0, G.ns - 1), px0, py0);
-    const double sx = -32.0 * G.dstep * s, sy = 32.0 * G.dstep * c;
-    for (int j = 0; j < nj; ++j) {
+    for (int j = jb; j < nj; ++j) {
       const double px = fma((double)j, sx, px0), py = fma((double)j, sy, py0);
       const double fx0 = floor(px), fy0 = floor(py);
       const int x0 = (int)fx0, y0 = (int)fy0;
@@ -218,9 +246,10 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
       acc += bilerp(fx, fy, (ya && xa) ? ur[0] : 0.f, (ya && xb) ? ur[ax] : 0.f,
                     (yb && xa) ? ur[ay] : 0.f, (yb && xb) ? ur[ax + ay] : 0.f);
     }
-    return warp_sum(acc);
+    return acc;
   }
-  for (int is = (is_lo & ~31) + lane; is <= is_hi; is += 32) {
+  for (int j = jb; j < nj; ++j) {
+    const int is = is0 + j * L;
     double px, py;
     sample_pos(G, c, s, ib, is, px, py);
     const double fx0 = floor(px), fy0 = floor(py);
@@ -236,8 +265,45 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
     if (yb && xa && w10 > 0) acc += (T)w10 * ur[ay];
     if (yb && xb && w11 > 0) acc += (T)w11 * ur[ax + ay];
   }
-  return warp_sum(acc);
+  return acc;
 }
+
+// One block of 8 warps projects 8 adjacent rays (bins 8 blockIdx.x ..
+// + 7 of angle blockIdx.y): the rays form 8 / RG groups of RG rays; each
+// group is served by RG warps, warp r covering part r of every ray's samples
+// with L = 32 / RG lanes per ray -- so a warp's loads hit a compact
+// RG x L patch of the (bin, step) lattice, and every block does the same
+// work whatever RG is.  Returns the sum of ray 8 blockIdx.x + threadIdx.x in
+// threads 0..7 (T(0) elsewhere, and for bins past the last).
+template <class T>
+__device__ __forceinline__ T fwd_block_sum(const Geo& G, const T* __restrict__ u,
+                                           const T* __restrict__ uT, T (&part)[8][8]) {
+  const int ia = blockIdx.y, b0 = blockIdx.x * 8;
+  __shared__ int2 s_rng[8];  // the block's ray ranges, computed once
+  if (threadIdx.x < 8)
+    s_rng[threadIdx.x] = b0 + (int)threadIdx.x < G.nb
+                             ? ray_range(G, G.cs[ia], G.sn[ia], b0 + threadIdx.x)
+                             : make_int2(0, -1);
+  __syncthreads();
+  const int lgR = sizeof(T) == 4 ? fwd_lg_rays_per_warp(G.cs[ia], G.sn[ia]) : 0;
+  const int lgL = 5 - lgR, RG = 1 << lgR;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> lgL, q = lane & ((1 << lgL) - 1), r = w & (RG - 1);
+  const int ib = b0 + (w & ~(RG - 1)) + g;
+  const bool live = ib < G.nb;
+  const int2 rg = s_rng[ib - b0];
+  const T v = seg_sum(live ? ray_sum(G, u, ia, ib, rg.x, rg.y, q, lgL, r, lgR, uT) : T(0), lgL);
+  if (q == 0) part[w][g] = v;
+  __syncthreads();
+  T sum = T(0);
+  if (threadIdx.x < 8) {
+    const int t = threadIdx.x, w0 = t & ~(RG - 1), gt = t & (RG - 1);
+    sum = part[w0][gt];
+    for (int k = 1; k < RG; ++k) sum += part[w0 + k][gt];
+  }
+  return sum;
+}
+inline dim3 fwd_grid(const Geo& G) { return dim3((G.nb + 7) / 8, G.na); }
 
 // Adjoint at pixel (r, c): sum over angles and the lattice samples that
 // deposit into it of w * y(angle, bin).  Exact path (double): positions and
@@ -382,11 +448,10 @@ __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y,
 
 template <class T>
 __global__ void radon_fwd_kernel(Geo G, const T* __restrict__ u, T* __restrict__ out) {
-  const int ray = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (ray >= G.na * G.nb) return;
-  const T v = ray_sum(G, u, ray / G.nb, ray % G.nb, lane);
-  if (lane == 0) out[ray] = v;
+  __shared__ T part[8][8];
+  const T v = fwd_block_sum<T>(G, u, nullptr, part);
+  const int ib = blockIdx.x * 8 + threadIdx.x;
+  if (threadIdx.x < 8 && ib < G.nb) out[(int64_t)blockIdx.y * G.nb + ib] = v;
 }
 
 template <class T>
@@ -482,11 +547,11 @@ __global__ void pdhg1_primal_kernel(Geo G, T* __restrict__ x, const T* __restric
 template <class T>
 __global__ void __launch_bounds__(256, 6) pdhg_dual_fid_kernel(Geo G, const T* __restrict__ xbar, T* __restrict__ y,
                                      const T* __restrict__ b, T tau0, const T* __restrict__ tau_arr) {
-  const int ray = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (ray >= G.na * G.nb) return;
-  const T ax = ray_sum(G, xbar, ray / G.nb, ray % G.nb, lane, static_cast<const T*>(G.xT));
-  if (lane == 0) {
+  __shared__ T part[8][8];
+  const T ax = fwd_block_sum<T>(G, xbar, static_cast<const T*>(G.xT), part);
+  const int ib = blockIdx.x * 8 + threadIdx.x;
+  if (threadIdx.x < 8 && ib < G.nb) {
+    const int64_t ray = (int64_t)blockIdx.y * G.nb + ib;
     const T tau = tau_arr ? tau_arr[ray] : tau0;
     const T v = y[ray] + tau * ax;
     y[ray] = (v - tau * b[ray]) / (T(1) + tau);
@@ -580,6 +645,7 @@ inline int check_geo(const psb_radon_geom* g) {
   PSB_REQUIRE(g->n >= 2 && g->n_angles >= 1 && g->n_bins >= g->n && g->n_steps >= 2,
               "RadonGeometry: need image_side >= 2, n_angles >= 1, n_bins >= image_side");
   PSB_REQUIRE(g->bin_spacing > 0 && g->step_spacing > 0, "radon: spacings must be positive");
+  PSB_REQUIRE(g->n_angles <= 65535, "radon: at most 65535 angles (forward grid y)");
   return PSB_OK;
 }
 
@@ -588,8 +654,7 @@ inline int check_geo(const psb_radon_geom* g) {
 int radon_fwd(int dtype, const psb_radon_geom* g, const void* u, void* out, cudaStream_t st) {
   if (int rc = check_geo(g)) return rc;
   Geo G = make_geo(g);
-  const int rays = G.na * G.nb;
-  dim3 grid((rays + 7) / 8);
+  const dim3 grid = fwd_grid(G);
   if (dtype == PSB_F32)
     radon_fwd_kernel<float><<<grid, 256, 0, st>>>(G, (const float*)u, (float*)out);
   else if (dtype == PSB_F64)
@@ -623,7 +688,7 @@ int pdhg_step_t(const Geo& G, T* x, T* y, T* h, T* xbar, const T* b, int32_t* ba
   pdhg_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(G, x, y, h, xbar, coin, (T)sigma, sig,
                                                           (T)hc, (T)ps, nonneg, bad, k);
   PSB_LAUNCHED("pdhg_primal");
-  pdhg_dual_fid_kernel<T><<<(G.na * G.nb + 7) / 8, 256, 0, st>>>(G, xbar, y, b, (T)tau, tau_arr);
+  pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, xbar, y, b, (T)tau, tau_arr);
   PSB_LAUNCHED("pdhg_dual_fid");
   pdhg_dual_tv_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(
       G.n, xbar, y + nfid, (T)tau, tau_arr ? tau_arr + nfid : nullptr, (T)alpha);
@@ -662,7 +727,7 @@ int pdhg1_step(int dtype, const psb_radon_geom* g, void* x, void* y, void* xbar,
     pdhg1_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(G, (T*)x, (const T*)y, (T*)xbar, coin,
                                                              (T)sigma, (T)p, (T)opw, nonneg, bad, k);
     PSB_LAUNCHED("pdhg1_primal");
-    pdhg_dual_fid_kernel<T><<<(G.na * G.nb + 7) / 8, 256, 0, st>>>(G, (const T*)xbar, (T*)y,
+    pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, (const T*)xbar, (T*)y,
                                                                   (const T*)b, (T)tau, nullptr);
     PSB_LAUNCHED("pdhg_dual_fid");
     pdhg_dual_tv_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(G.n, (const T*)xbar, (T*)y + nfid,
@@ -699,7 +764,7 @@ int ct_implicit_step(const Geo& G, T* x, T* y, T* h, T* xbar, TF* z, TF* q, cons
         G.n, x, h, xbar, z, q, n_inner, nonneg, (T)ps, bad, k, static_cast<T*>(G.xT), G.xpad);
     PSB_LAUNCHED("ct_implicit_post");
   }
-  pdhg_dual_fid_kernel<T><<<(G.na * G.nb + 7) / 8, 256, 0, st>>>(G, xbar, y, b, (T)tau, nullptr);
+  pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, xbar, y, b, (T)tau, nullptr);
   PSB_LAUNCHED("pdhg_dual_fid");
   return PSB_OK;
 }
