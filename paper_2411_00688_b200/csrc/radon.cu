@@ -385,10 +385,17 @@ __device__ __forceinline__ float pixel_gather_tent(const Geo& G, const float* __
 
 // The same tent gather over a FIXED 3 x 3 lattice window per angle, for
 // lattices whose spacings exceed 2 sqrt(2) / 3 (a window of half-width sqrt 2
-// then holds at most 3 bins and 3 steps; config 3: 1 and 0.9987).  Candidates
-// outside the window's true range, and bins / steps outside the sinogram, get
-// weight exactly 0 (pushed > 1 away), which leaves every fmaf sum unchanged:
-// no data-dependent trip counts, no divergence, ~half the instructions.
+// then holds at most 3 bins and 3 steps; config 3: 1 and 0.9987), and at
+// least 3 bins and steps.  The window starts at the first bin / step in
+// reach, clamped into the sinogram: it still covers every in-reach lattice
+// point, and a point out of reach (|lattice offset| > sqrt 2, so one image-
+// axis offset exceeds 1) gets tent weight exactly 0 -- which leaves every
+// fmaf sum unchanged.  No bounds tests, no data-dependent trip counts, and
+// the window's three y values load from one base address.
+// Tent weights in doubled form: t + |t| = 2 max(0, t) exactly (one packed
+// FADD2 for both axes instead of two FMNMX), so the weight sums and the
+// accumulator carry an exact factor 4, removed at the end (power-of-two
+// scaling commutes with rounding for normal numbers).
 __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* __restrict__ y,
                                                     int r, int cc) {
   const double dxp = (double)cc - G.center, dyp = (double)r - G.center;
@@ -397,49 +404,47 @@ __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* _
   const double rs = 1.41421356237309515 / G.dstep + 1e-9;
   const double isp = 1.0 / G.spacing, ids = 1.0 / G.dstep;
   const float spf = (float)G.spacing, dsf = (float)G.dstep;
-  float acc = 0.f;
+  const int bmax = G.nb - 3, smax = G.ns - 3;
+  float acc4 = 0.f;
 #pragma unroll 2
   for (int ia = 0; ia < G.na; ++ia) {
     const double c = G.cs[ia], s = G.sn[ia];
     const double ob = (dxp * c + dyp * s) * isp + mid;
     const double os = (-dxp * s + dyp * c + G.half_span) * ids;
-    const int b0 = (int)ceil(ob - rb), s0 = (int)ceil(os - rs);
+    const int b0 = min(max((int)ceil(ob - rb), 0), bmax);
+    const int s0 = min(max((int)ceil(os - rs), 0), smax);
     const float cf = (float)c, sf = (float)s;
     const float eb = (float)((double)b0 - ob) * spf;
     const float es = (float)((double)s0 - os) * dsf;
-    float ds[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const bool ok = (unsigned)(s0 + j) < (unsigned)G.ns;
-      ds[j] = ok ? fmaf((float)j, dsf, es) : 8.f;
-    }
-    const float* yrow = y + (int64_t)ia * G.nb;
+    const float* yw = y + (int64_t)ia * G.nb + b0;
     // (dx, dy) of a candidate as one packed pair: FFMA2 for the offsets,
-    // FADD2 with the |.| operand modifier for 1 - |d| -- the scalar ops'
-    // IEEE results lane by lane (ds * (-s) == (-ds) * s exactly)
+    // FADD2 with the |.| operand modifier for 1 - |d| and for t + |t| --
+    // the scalar ops' IEEE results lane by lane (ds * (-s) == (-ds) * s)
     const float2 sc2 = make_float2(-sf, cf), one2 = make_float2(1.f, 1.f);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const bool ok = (unsigned)(b0 + i) < (unsigned)G.nb;
       const float db = fmaf((float)i, spf, eb);
-      const float2 bxy = ok ? make_float2(db * cf, db * sf) : make_float2(8.f, 8.f);
-      float wsum = 0.f;
+      const float2 bxy = make_float2(db * cf, db * sf);
+      float wsum4 = 0.f;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        const float2 d2 = __ffma2_rn(make_float2(ds[j], ds[j]), sc2, bxy);
+        const float ds = fmaf((float)j, dsf, es);
+        const float2 d2 = __ffma2_rn(make_float2(ds, ds), sc2, bxy);
         const float2 t2 = __fadd2_rn(one2, make_float2(-fabsf(d2.x), -fabsf(d2.y)));
-        wsum = fmaf(fmaxf(0.f, t2.x), fmaxf(0.f, t2.y), wsum);
+        const float2 w2 = __fadd2_rn(t2, make_float2(fabsf(t2.x), fabsf(t2.y)));
+        wsum4 = fmaf(w2.x, w2.y, wsum4);
       }
-      acc = fmaf(wsum, yrow[ok ? b0 + i : 0], acc);
+      acc4 = fmaf(wsum4, yw[i], acc4);
     }
   }
-  return acc;
+  return acc4 * 0.25f;
 }
 
 template <class T>
 __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y, int r, int cc) {
   if constexpr (sizeof(T) == 4) {
-    if (G.spacing > 0.9429 && G.dstep > 0.9429) return pixel_gather_tent3(G, y, r, cc);
+    if (G.spacing > 0.9429 && G.dstep > 0.9429 && G.nb >= 3 && G.ns >= 3)
+      return pixel_gather_tent3(G, y, r, cc);
     return pixel_gather_tent(G, y, r, cc);
   } else {
     return pixel_gather_exact(G, y, r, cc);
