@@ -22,6 +22,8 @@
 // the host with numpy and uploaded, so positions match the reference bitwise.
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace psb {
 
 namespace {
@@ -119,6 +121,26 @@ __device__ __forceinline__ float bilerp(float fx, float fy, float a, float b, fl
   return fmaf(fy, r1, gy * r0);
 }
 
+// 32.32 fixed-point lattice coordinate: (hi, lo) += (shi, slo) as one
+// add-with-carry pair (kept opaque so the compiler does not rebuild the walk
+// from 64-bit multiplies of the trip count)
+struct Fix32 {
+  int hi;
+  unsigned lo;
+};
+__device__ __forceinline__ Fix32 fix_from(double v) {
+  const long long f = __double2ll_rn(v * 4294967296.0);
+  return Fix32{(int)(f >> 32), (unsigned)f};
+}
+__device__ __forceinline__ void fix_add(Fix32& a, const Fix32& b) {
+  asm("add.cc.u32 %0, %0, %2;\n\taddc.s32 %1, %1, %3;"
+      : "+r"(a.lo), "+r"(a.hi)
+      : "r"(b.lo), "r"(b.hi));
+}
+__device__ __forceinline__ float fix_frac(const Fix32& a) {
+  return __uint2float_rn(a.lo) * 2.3283064365386963e-10f;  // lo * 2^-32
+}
+
 // Rays per warp of the forward gathers at angle (c, s).  A warp serves RG
 // adjacent bins of one angle with L = 32 / RG lanes each (lane q of a group
 // takes the ray's samples q, q + L, ...).  Lanes along one ray (RG = 1) load
@@ -208,38 +230,57 @@ __device__ __forceinline__ T ray_sum(const Geo& G, const T* __restrict__ u, int 
   if constexpr (sizeof(T) == 4) {
     double px0, py0;
     sample_pos(G, c, s, ib, min(is0, G.ns - 1), px0, py0);
-    // each lane's first sample position exactly as the reference computes
-    // it, then the lattice step along the ray (L samples per lane step) as
-    // one fp64 FMA per coordinate; the fractional offsets and the bilinear
-    // weights in fp32 (weights agree with the fp64 path to ~1e-7)
-    const double sx = -(double)L * G.dstep * s, sy = (double)L * G.dstep * c;
+    // Each lane's first sample position exactly as the reference computes
+    // it; from there the lane walks its lattice points (L samples apart) in
+    // 32.32 fixed point: floor = the high word, the fractional offset = the
+    // low word, the step one 64-bit add per coordinate (position error
+    // <= (j + 1) 2^-33 pixel after j steps, i.e. < 1e-8 here; the bilinear
+    // weights in fp32 agree with the fp64 path to ~1e-7).
+    const Fix32 sxf = fix_from(-(double)L * G.dstep * s), syf = fix_from((double)L * G.dstep * c);
+    const long long sx64 = ((long long)sxf.hi << 32) | sxf.lo, sy64 = ((long long)syf.hi << 32) | syf.lo;
+    const long long px64 = __double2ll_rn(px0 * 4294967296.0), py64 = __double2ll_rn(py0 * 4294967296.0);
+    auto start = [&](long long p, long long st, int j) {  // position of step j
+      const long long v = p + (long long)j * st;
+      return Fix32{(int)(v >> 32), (unsigned)v};
+    };
     if (G.xpad != nullptr) {
       // padded copies: the same positions, weights and FMA order as below,
-      // without the per-sample / per-tap tests
+      // without the per-sample / per-tap tests.  (A lane's samples before
+      // is_lo lie up to L - 1 steps outside the image and deposit nothing:
+      // start at the first one >= is_lo, whose taps -- like every sample up
+      // to is_hi -- fall inside the zero border.)
       const int wp = n + 2 * PADB;
-      const bool trp = fabs(c) > fabs(s);
-      const float* srcp = G.xpad + (trp ? (size_t)wp * wp : 0) + PADB * wp + PADB;
-      const int axp = trp ? wp : 1, ayp = trp ? 1 : wp;
-      // (a lane's samples before is_lo lie up to L - 1 steps outside the
-      // image and deposit nothing: start at the first one >= is_lo, whose
-      // taps -- like every sample up to is_hi -- fall inside the zero border)
       const int js = max(jb, is0 < is_lo ? (is_lo - is0 + L - 1) >> lgL : 0);
-      for (int j = js; j < nj; ++j) {
-        const double px = fma((double)j, sx, px0), py = fma((double)j, sy, py0);
-        const double fx0 = floor(px), fy0 = floor(py);
-        const int x0 = (int)fx0, y0 = (int)fy0;
-        const float fx = (float)(px - fx0), fy = (float)(py - fy0);
-        const float* ur = srcp + y0 * ayp + x0 * axp;
-        acc += bilerp(fx, fy, ur[0], ur[axp], ur[ayp], ur[axp + ayp]);
-      }
+      Fix32 pxf = start(px64, sx64, js), pyf = start(py64, sy64, js);
+      // the copy whose rows run along the ray's major axis: memory rows
+      // (slow, fast) = (y, x) in xbar, (x, y) in its transpose; the four taps
+      // are two adjacent floats in each of two adjacent rows
+      auto walk = [&](auto trp_tag) {
+        constexpr bool TRP = decltype(trp_tag)::value;
+        const float* srcp = G.xpad + (TRP ? (size_t)wp * wp : 0) + PADB * wp + PADB;
+        for (int j = js; j < nj; ++j) {
+          const int x0 = pxf.hi, y0 = pyf.hi;
+          const float fx = fix_frac(pxf), fy = fix_frac(pyf);
+          const float* p0 = srcp + ((TRP ? x0 : y0) * wp + (TRP ? y0 : x0));
+          const float* p1 = p0 + wp;
+          const float t00 = p0[0], t01 = p0[1], t10 = p1[0], t11 = p1[1];
+          // bilerp(fx, fy, u(x0, y0), u(x0+1, y0), u(x0, y0+1), u(x0+1, y0+1))
+          acc += TRP ? bilerp(fx, fy, t00, t10, t01, t11) : bilerp(fx, fy, t00, t01, t10, t11);
+          fix_add(pxf, sxf);
+          fix_add(pyf, syf);
+        }
+      };
+      if (fabs(c) > fabs(s))
+        walk(std::true_type{});
+      else
+        walk(std::false_type{});
       return acc;
     }
-    for (int j = jb; j < nj; ++j) {
-      const double px = fma((double)j, sx, px0), py = fma((double)j, sy, py0);
-      const double fx0 = floor(px), fy0 = floor(py);
-      const int x0 = (int)fx0, y0 = (int)fy0;
+    Fix32 pxf = start(px64, sx64, jb), pyf = start(py64, sy64, jb);
+    for (int j = jb; j < nj; ++j, fix_add(pxf, sxf), fix_add(pyf, syf)) {
+      const int x0 = pxf.hi, y0 = pyf.hi;
       if (x0 < -1 || x0 >= n || y0 < -1 || y0 >= n) continue;
-      const float fx = (float)(px - fx0), fy = (float)(py - fy0);
+      const float fx = fix_frac(pxf), fy = fix_frac(pyf);
       const bool xa = x0 >= 0, xb = x0 + 1 < n, ya = y0 >= 0, yb = y0 + 1 < n;
       const float* ur = src + y0 * ay + x0 * ax;
       // taps outside the image contribute 0 (the padded path reads zeros)
