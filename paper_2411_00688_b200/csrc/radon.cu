@@ -437,9 +437,11 @@ __device__ __forceinline__ float pixel_gather_tent(const Geo& G, const float* __
 // FADD2 for both axes instead of two FMNMX), so the weight sums and the
 // accumulator carry an exact factor 4, removed at the end (power-of-two
 // scaling commutes with rounding for normal numbers).
+// One pixel (r, cc); the pair form below does the same IEEE operations for
+// each of its two pixels, lane by lane.
 __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* __restrict__ y,
                                                     int r, int cc) {
-  const double dxp = (double)cc - G.center, dyp = (double)r - G.center;
+  const double dyp = (double)r - G.center, dxp = (double)cc - G.center;
   const double mid = 0.5 * (G.nb - 1);
   const double rb = 1.41421356237309515 / G.spacing + 1e-9;
   const double rs = 1.41421356237309515 / G.dstep + 1e-9;
@@ -450,8 +452,11 @@ __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* _
 #pragma unroll 2
   for (int ia = 0; ia < G.na; ++ia) {
     const double c = G.cs[ia], s = G.sn[ia];
-    const double ob = (dxp * c + dyp * s) * isp + mid;
-    const double os = (-dxp * s + dyp * c + G.half_span) * ids;
+    // lattice coordinates of the pixel centre (inverse rotation):
+    // ob = (dx c + dy s) / spacing + mid, os = (-dx s + (dy c + half_span)) / dstep
+    const double ys = __dmul_rn(dyp, s), yc = __fma_rn(dyp, c, G.half_span);
+    const double ob = __fma_rn(__fma_rn(dxp, c, ys), isp, mid);
+    const double os = __dmul_rn(__fma_rn(-dxp, s, yc), ids);
     const int b0 = min(max((int)ceil(ob - rb), 0), bmax);
     const int s0 = min(max((int)ceil(os - rs), 0), smax);
     const float cf = (float)c, sf = (float)s;
@@ -481,11 +486,74 @@ __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* _
   return acc4 * 0.25f;
 }
 
+// Two horizontally adjacent pixels (r, c0), (r, c0 + 1): each angle's loads
+// and the row's part of the inverse rotation are shared, and every fp32 op
+// is a packed pair over the two pixels (lane k = pixel k: the same IEEE
+// results as pixel_gather_tent3 on each, ~35 % fewer instructions).
+__device__ __forceinline__ float2 pixel_gather_tent3_pair(const Geo& G, const float* __restrict__ y,
+                                                          int r, int c0) {
+  const double dyp = (double)r - G.center;
+  const double dx0 = (double)c0 - G.center, dx1 = (double)(c0 + 1) - G.center;
+  const double mid = 0.5 * (G.nb - 1);
+  const double rb = 1.41421356237309515 / G.spacing + 1e-9;
+  const double rs = 1.41421356237309515 / G.dstep + 1e-9;
+  const double isp = 1.0 / G.spacing, ids = 1.0 / G.dstep;
+  const float spf = (float)G.spacing, dsf = (float)G.dstep;
+  const float2 sp2 = make_float2(spf, spf), ds2 = make_float2(dsf, dsf);
+  const int bmax = G.nb - 3, smax = G.ns - 3;
+  float2 acc4 = make_float2(0.f, 0.f);
+  const float2 one2 = make_float2(1.f, 1.f);
+#pragma unroll 2
+  for (int ia = 0; ia < G.na; ++ia) {
+    const double c = G.cs[ia], s = G.sn[ia];
+    const double ys = __dmul_rn(dyp, s), yc = __fma_rn(dyp, c, G.half_span);
+    const double ob0 = __fma_rn(__fma_rn(dx0, c, ys), isp, mid);
+    const double ob1 = __fma_rn(__fma_rn(dx1, c, ys), isp, mid);
+    const double os0 = __dmul_rn(__fma_rn(-dx0, s, yc), ids);
+    const double os1 = __dmul_rn(__fma_rn(-dx1, s, yc), ids);
+    const int b00 = min(max((int)ceil(ob0 - rb), 0), bmax);
+    const int b01 = min(max((int)ceil(ob1 - rb), 0), bmax);
+    const int s00 = min(max((int)ceil(os0 - rs), 0), smax);
+    const int s01 = min(max((int)ceil(os1 - rs), 0), smax);
+    const float cf = (float)c, sf = (float)s;
+    const float2 cf2 = make_float2(cf, cf), sf2 = make_float2(sf, sf);
+    const float2 msf2 = make_float2(-sf, -sf);
+    const float2 eb2 = __fmul2_rn(make_float2((float)((double)b00 - ob0), (float)((double)b01 - ob1)), sp2);
+    const float2 es2 = __fmul2_rn(make_float2((float)((double)s00 - os0), (float)((double)s01 - os1)), ds2);
+    const float* yrow = y + (int64_t)ia * G.nb;
+    const float* yw0 = yrow + b00;
+    const float* yw1 = yrow + b01;
+    float2 dsj[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dsj[j] = __ffma2_rn(make_float2((float)j, (float)j), ds2, es2);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const float2 db = __ffma2_rn(make_float2((float)i, (float)i), sp2, eb2);
+      const float2 bx = __fmul2_rn(db, cf2), by = __fmul2_rn(db, sf2);
+      float2 wsum4 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float2 dx = __ffma2_rn(dsj[j], msf2, bx), dy = __ffma2_rn(dsj[j], cf2, by);
+        const float2 tx = __fadd2_rn(one2, make_float2(-fabsf(dx.x), -fabsf(dx.y)));
+        const float2 ty = __fadd2_rn(one2, make_float2(-fabsf(dy.x), -fabsf(dy.y)));
+        const float2 wx = __fadd2_rn(tx, make_float2(fabsf(tx.x), fabsf(tx.y)));
+        const float2 wy = __fadd2_rn(ty, make_float2(fabsf(ty.x), fabsf(ty.y)));
+        wsum4 = __ffma2_rn(wx, wy, wsum4);
+      }
+      acc4 = __ffma2_rn(wsum4, make_float2(yw0[i], yw1[i]), acc4);
+    }
+  }
+  return __fmul2_rn(acc4, make_float2(0.25f, 0.25f));
+}
+
+__host__ __device__ __forceinline__ bool tent3_ok(const Geo& G) {
+  return G.spacing > 0.9429 && G.dstep > 0.9429 && G.nb >= 3 && G.ns >= 3;
+}
+
 template <class T>
 __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y, int r, int cc) {
   if constexpr (sizeof(T) == 4) {
-    if (G.spacing > 0.9429 && G.dstep > 0.9429 && G.nb >= 3 && G.ns >= 3)
-      return pixel_gather_tent3(G, y, r, cc);
+    if (tent3_ok(G)) return pixel_gather_tent3(G, y, r, cc);
     return pixel_gather_tent(G, y, r, cc);
   } else {
     return pixel_gather_exact(G, y, r, cc);
@@ -515,45 +583,62 @@ __global__ void radon_adj_kernel(Geo G, const T* __restrict__ y, T* __restrict__
 //   PDHGSkip-2: xhat = t + sigma h ; x' = coin ? prox_g(t + hc h) : xhat ;
 //               h += ps (x' - xhat)                             (skip.py:134-145)
 //   both      : xbar = 2 x' - x                                 (skip.py:143)
-template <class T>
+// NP = 2 (fp32 tent gather): two horizontally adjacent pixels per thread,
+// sharing each angle's setup of the adjoint gather.
+template <class T, int NP>
 __global__ void pdhg_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
                                    T* __restrict__ h, T* __restrict__ xbar, int coin, T sigma,
                                    const T* __restrict__ sig, T hc, T ps, int nonneg, int32_t* bad,
                                    int k) {
-  const int n = G.n;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * n) return;
-  const int r = idx / n, c = idx % n;
+  const int n = G.n, per_row = (n + NP - 1) / NP;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n * per_row) return;
+  const int r = tid / per_row, c0 = (tid % per_row) * NP;
   const T* yA = y;
   const T* yy = y + (int64_t)G.na * G.nb;
   const T* yx = yy + (int64_t)n * n;
-  T d = T(0);  // divergence of y_D (operators.py:66-70 order)
-  if (r < n - 1) d += yy[idx];
-  if (r > 0) d -= yy[idx - n];
-  if (c < n - 1) d += yx[idx];
-  if (c > 0) d -= yx[idx - 1];
-  const T kty = pixel_gather(G, yA, r, c) + (-d);  // block_stack adjoint: A^T y_A + (-div y_D)
-  const T xo = x[idx];
-  const T t = xo - (sig ? sig[idx] : sigma) * kty;  // diagonal steps: solvers.py:212-234
-  T xn;
-  if (h) {
-    const T ho = h[idx];
-    const T xhat = t + sigma * ho;
-    if (coin) {
-      xn = t + hc * ho;
-      if (nonneg) xn = xn > T(0) ? xn : T(0);
-    } else {
-      xn = xhat;
-    }
-    h[idx] = ho + ps * (xn - xhat);
+  T aty[NP];
+  if constexpr (NP == 2) {
+    static_assert(sizeof(T) == 4, "paired pixels: fp32 tent gather only");
+    const float2 v = pixel_gather_tent3_pair(G, yA, r, c0);
+    aty[0] = v.x;
+    aty[1] = v.y;
   } else {
-    xn = nonneg ? (t > T(0) ? t : T(0)) : t;
+    aty[0] = pixel_gather(G, yA, r, c0);
   }
-  x[idx] = xn;
-  const T xb = T(2) * xn - xo;
-  xbar[idx] = xb;
-  store_xbar_copies(G.xT, G.xpad, n, r, c, xb);
-  if (bad && !isfinite(xn)) atomicMin(bad, k);
+#pragma unroll
+  for (int kk = 0; kk < NP; ++kk) {
+    const int c = c0 + kk;
+    if (c >= n) break;
+    const int idx = r * n + c;
+    T d = T(0);  // divergence of y_D (operators.py:66-70 order)
+    if (r < n - 1) d += yy[idx];
+    if (r > 0) d -= yy[idx - n];
+    if (c < n - 1) d += yx[idx];
+    if (c > 0) d -= yx[idx - 1];
+    const T kty = aty[kk] + (-d);  // block_stack adjoint: A^T y_A + (-div y_D)
+    const T xo = x[idx];
+    const T t = xo - (sig ? sig[idx] : sigma) * kty;  // diagonal steps: solvers.py:212-234
+    T xn;
+    if (h) {
+      const T ho = h[idx];
+      const T xhat = t + sigma * ho;
+      if (coin) {
+        xn = t + hc * ho;
+        if (nonneg) xn = xn > T(0) ? xn : T(0);
+      } else {
+        xn = xhat;
+      }
+      h[idx] = ho + ps * (xn - xhat);
+    } else {
+      xn = nonneg ? (t > T(0) ? t : T(0)) : t;
+    }
+    x[idx] = xn;
+    const T xb = T(2) * xn - xo;
+    xbar[idx] = xb;
+    store_xbar_copies(G.xT, G.xpad, n, r, c, xb);
+    if (bad && !isfinite(xn)) atomicMin(bad, k);
+  }
 }
 
 // PDHGSkip-1 primal (skip.py:82-114), explicit splitting: on a success draw
@@ -731,8 +816,14 @@ int pdhg_step_t(const Geo& G, T* x, T* y, T* h, T* xbar, const T* b, int32_t* ba
                 const T* sig = nullptr, const T* tau_arr = nullptr) {
   const int npx = G.n * G.n;
   const int64_t nfid = (int64_t)G.na * G.nb;
-  pdhg_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(G, x, y, h, xbar, coin, (T)sigma, sig,
-                                                          (T)hc, (T)ps, nonneg, bad, k);
+  if (sizeof(T) == 4 && tent3_ok(G)) {
+    const int nt = G.n * ((G.n + 1) / 2);
+    pdhg_primal_kernel<T, sizeof(T) == 4 ? 2 : 1><<<(nt + 127) / 128, 128, 0, st>>>(
+        G, x, y, h, xbar, coin, (T)sigma, sig, (T)hc, (T)ps, nonneg, bad, k);
+  } else {
+    pdhg_primal_kernel<T, 1><<<(npx + 255) / 256, 256, 0, st>>>(
+        G, x, y, h, xbar, coin, (T)sigma, sig, (T)hc, (T)ps, nonneg, bad, k);
+  }
   PSB_LAUNCHED("pdhg_primal");
   pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, xbar, y, b, (T)tau, tau_arr);
   PSB_LAUNCHED("pdhg_dual_fid");
