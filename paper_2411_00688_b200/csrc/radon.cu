@@ -491,7 +491,7 @@ __device__ __forceinline__ float pixel_gather_tent3(const Geo& G, const float* _
 // is a packed pair over the two pixels (lane k = pixel k: the same IEEE
 // results as pixel_gather_tent3 on each, ~35 % fewer instructions).
 __device__ __forceinline__ float2 pixel_gather_tent3_pair(const Geo& G, const float* __restrict__ y,
-                                                          int r, int c0) {
+                                                          int r, int c0, int ia0, int ia1) {
   const double dyp = (double)r - G.center;
   const double dx0 = (double)c0 - G.center, dx1 = (double)(c0 + 1) - G.center;
   const double mid = 0.5 * (G.nb - 1);
@@ -504,7 +504,7 @@ __device__ __forceinline__ float2 pixel_gather_tent3_pair(const Geo& G, const fl
   float2 acc4 = make_float2(0.f, 0.f);
   const float2 one2 = make_float2(1.f, 1.f);
 #pragma unroll 2
-  for (int ia = 0; ia < G.na; ++ia) {
+  for (int ia = ia0; ia < ia1; ++ia) {
     const double c = G.cs[ia], s = G.sn[ia];
     const double ys = __dmul_rn(dyp, s), yc = __fma_rn(dyp, c, G.half_span);
     const double ob0 = __fma_rn(__fma_rn(dx0, c, ys), isp, mid);
@@ -583,62 +583,80 @@ __global__ void radon_adj_kernel(Geo G, const T* __restrict__ y, T* __restrict__
 //   PDHGSkip-2: xhat = t + sigma h ; x' = coin ? prox_g(t + hc h) : xhat ;
 //               h += ps (x' - xhat)                             (skip.py:134-145)
 //   both      : xbar = 2 x' - x                                 (skip.py:143)
-// NP = 2 (fp32 tent gather): two horizontally adjacent pixels per thread,
-// sharing each angle's setup of the adjoint gather.
-template <class T, int NP>
+// One pixel's primal update given its A^T y_A.
+template <class T>
+__device__ __forceinline__ void pdhg_primal_px(const Geo& G, T* __restrict__ x, const T* __restrict__ y,
+                                               T* __restrict__ h, T* __restrict__ xbar, int coin,
+                                               T sigma, const T* __restrict__ sig, T hc, T ps,
+                                               int nonneg, int32_t* bad, int k, int r, int c, T aty) {
+  const int n = G.n;
+  const T* yy = y + (int64_t)G.na * G.nb;
+  const T* yx = yy + (int64_t)n * n;
+  const int idx = r * n + c;
+  T d = T(0);  // divergence of y_D (operators.py:66-70 order)
+  if (r < n - 1) d += yy[idx];
+  if (r > 0) d -= yy[idx - n];
+  if (c < n - 1) d += yx[idx];
+  if (c > 0) d -= yx[idx - 1];
+  const T kty = aty + (-d);  // block_stack adjoint: A^T y_A + (-div y_D)
+  const T xo = x[idx];
+  const T t = xo - (sig ? sig[idx] : sigma) * kty;  // diagonal steps: solvers.py:212-234
+  T xn;
+  if (h) {
+    const T ho = h[idx];
+    const T xhat = t + sigma * ho;
+    if (coin) {
+      xn = t + hc * ho;
+      if (nonneg) xn = xn > T(0) ? xn : T(0);
+    } else {
+      xn = xhat;
+    }
+    h[idx] = ho + ps * (xn - xhat);
+  } else {
+    xn = nonneg ? (t > T(0) ? t : T(0)) : t;
+  }
+  x[idx] = xn;
+  const T xb = T(2) * xn - xo;
+  xbar[idx] = xb;
+  store_xbar_copies(G.xT, G.xpad, n, r, c, xb);
+  if (bad && !isfinite(xn)) atomicMin(bad, k);
+}
+
+template <class T>
 __global__ void pdhg_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
                                    T* __restrict__ h, T* __restrict__ xbar, int coin, T sigma,
                                    const T* __restrict__ sig, T hc, T ps, int nonneg, int32_t* bad,
                                    int k) {
-  const int n = G.n, per_row = (n + NP - 1) / NP;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= n * per_row) return;
-  const int r = tid / per_row, c0 = (tid % per_row) * NP;
-  const T* yA = y;
-  const T* yy = y + (int64_t)G.na * G.nb;
-  const T* yx = yy + (int64_t)n * n;
-  T aty[NP];
-  if constexpr (NP == 2) {
-    static_assert(sizeof(T) == 4, "paired pixels: fp32 tent gather only");
-    const float2 v = pixel_gather_tent3_pair(G, yA, r, c0);
-    aty[0] = v.x;
-    aty[1] = v.y;
-  } else {
-    aty[0] = pixel_gather(G, yA, r, c0);
-  }
-#pragma unroll
-  for (int kk = 0; kk < NP; ++kk) {
-    const int c = c0 + kk;
-    if (c >= n) break;
-    const int idx = r * n + c;
-    T d = T(0);  // divergence of y_D (operators.py:66-70 order)
-    if (r < n - 1) d += yy[idx];
-    if (r > 0) d -= yy[idx - n];
-    if (c < n - 1) d += yx[idx];
-    if (c > 0) d -= yx[idx - 1];
-    const T kty = aty[kk] + (-d);  // block_stack adjoint: A^T y_A + (-div y_D)
-    const T xo = x[idx];
-    const T t = xo - (sig ? sig[idx] : sigma) * kty;  // diagonal steps: solvers.py:212-234
-    T xn;
-    if (h) {
-      const T ho = h[idx];
-      const T xhat = t + sigma * ho;
-      if (coin) {
-        xn = t + hc * ho;
-        if (nonneg) xn = xn > T(0) ? xn : T(0);
-      } else {
-        xn = xhat;
-      }
-      h[idx] = ho + ps * (xn - xhat);
-    } else {
-      xn = nonneg ? (t > T(0) ? t : T(0)) : t;
-    }
-    x[idx] = xn;
-    const T xb = T(2) * xn - xo;
-    xbar[idx] = xb;
-    store_xbar_copies(G.xT, G.xpad, n, r, c, xb);
-    if (bad && !isfinite(xn)) atomicMin(bad, k);
-  }
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= G.n * G.n) return;
+  const int r = idx / G.n, c = idx % G.n;
+  pdhg_primal_px(G, x, y, h, xbar, coin, sigma, sig, hc, ps, nonneg, bad, k, r, c,
+                 pixel_gather(G, y, r, c));
+}
+
+// fp32 tent gather: a pair of lanes serves two horizontally adjacent pixels
+// -- each gathers both pixels over half of the angles
+// (pixel_gather_tent3_pair), the halves are added in a fixed order (first +
+// second) and each lane then updates one of the two pixels.  A warp serves 16
+// pixel pairs of a row.
+__global__ void pdhg_primal_pair_kernel(Geo G, float* __restrict__ x, const float* __restrict__ y,
+                                        float* __restrict__ h, float* __restrict__ xbar, int coin,
+                                        float sigma, const float* __restrict__ sig, float hc,
+                                        float ps, int nonneg, int32_t* bad, int k) {
+  const int n = G.n, per_row = (n + 1) / 2, pairs = n * per_row;
+  const int lane = threadIdx.x & 31, half = lane & 1, mid = G.na >> 1;
+  const int pq = ((blockIdx.x * blockDim.x + threadIdx.x) >> 1);
+  if ((pq & ~15) >= pairs) return;  // whole warps only (the shuffles below)
+  const int pr = min(pq, pairs - 1);  // (past the end: recomputed, not stored)
+  const int r = pr / per_row, c0 = (pr % per_row) * 2;
+  const float2 v = pixel_gather_tent3_pair(G, y, r, c0, half ? mid : 0, half ? G.na : mid);
+  const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1),
+                               __shfl_xor_sync(0xffffffffu, v.y, 1));
+  const float2 sum = half ? __fadd2_rn(o, v) : __fadd2_rn(v, o);
+  const int c = c0 + half;
+  if (pq < pairs && c < n)
+    pdhg_primal_px(G, x, y, h, xbar, coin, sigma, sig, hc, ps, nonneg, bad, k, r, c,
+                   half ? sum.y : sum.x);
 }
 
 // PDHGSkip-1 primal (skip.py:82-114), explicit splitting: on a success draw
@@ -817,11 +835,13 @@ int pdhg_step_t(const Geo& G, T* x, T* y, T* h, T* xbar, const T* b, int32_t* ba
   const int npx = G.n * G.n;
   const int64_t nfid = (int64_t)G.na * G.nb;
   if (sizeof(T) == 4 && tent3_ok(G)) {
-    const int nt = G.n * ((G.n + 1) / 2);
-    pdhg_primal_kernel<T, sizeof(T) == 4 ? 2 : 1><<<(nt + 127) / 128, 128, 0, st>>>(
-        G, x, y, h, xbar, coin, (T)sigma, sig, (T)hc, (T)ps, nonneg, bad, k);
+    const int lanes = 2 * G.n * ((G.n + 1) / 2);
+    pdhg_primal_pair_kernel<<<(lanes + 127) / 128, 128, 0, st>>>(G, (float*)x, (const float*)y, (float*)h,
+                                                    (float*)xbar, coin, (float)sigma,
+                                                    (const float*)sig, (float)hc, (float)ps,
+                                                    nonneg, bad, k);
   } else {
-    pdhg_primal_kernel<T, 1><<<(npx + 255) / 256, 256, 0, st>>>(
+    pdhg_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(
         G, x, y, h, xbar, coin, (T)sigma, sig, (T)hc, (T)ps, nonneg, bad, k);
   }
   PSB_LAUNCHED("pdhg_primal");
