@@ -550,6 +550,37 @@ __host__ __device__ __forceinline__ bool tent3_ok(const Geo& G) {
   return G.spacing > 0.9429 && G.dstep > 0.9429 && G.nb >= 3 && G.ns >= 3;
 }
 
+// Pixel-pair lanes for the fp32 tent-gather kernels (grid: pair_lanes(G)
+// threads): lanes 2m, 2m+1 of a warp gather pixels (r, c0), (r, c0 + 1) over
+// the first / second half of the angles (pixel_gather_tent3_pair) and add
+// the halves in a fixed order; lane 2m + h then owns pixel (r, c0 + h).
+// `live` is false for a lane with no pixel (past the image); whole warps past
+// the end return before the gather (its shuffles need every lane).
+struct PairLane {
+  int r, c;
+  float aty;
+  bool live;
+};
+inline int pair_lanes(const Geo& G) { return 2 * G.n * ((G.n + 1) / 2); }
+__device__ __forceinline__ bool pair_gather_lane(const Geo& G, const float* __restrict__ y,
+                                                 PairLane& L) {
+  const int n = G.n, per_row = (n + 1) / 2, pairs = n * per_row;
+  const int half = threadIdx.x & 1, mid = G.na >> 1;
+  const int pq = (blockIdx.x * blockDim.x + threadIdx.x) >> 1;
+  if ((pq & ~15) >= pairs) return false;
+  const int pr = min(pq, pairs - 1);  // (past the end: recomputed, not stored)
+  L.r = pr / per_row;
+  const int c0 = (pr % per_row) * 2;
+  const float2 v = pixel_gather_tent3_pair(G, y, L.r, c0, half ? mid : 0, half ? G.na : mid);
+  const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1),
+                               __shfl_xor_sync(0xffffffffu, v.y, 1));
+  const float2 sum = half ? __fadd2_rn(o, v) : __fadd2_rn(v, o);
+  L.c = c0 + half;
+  L.aty = half ? sum.y : sum.x;
+  L.live = pq < pairs && L.c < n;
+  return true;
+}
+
 template <class T>
 __device__ __forceinline__ T pixel_gather(const Geo& G, const T* __restrict__ y, int r, int cc) {
   if constexpr (sizeof(T) == 4) {
@@ -566,6 +597,11 @@ __global__ void radon_fwd_kernel(Geo G, const T* __restrict__ u, T* __restrict__
   const T v = fwd_block_sum<T>(G, u, nullptr, part);
   const int ib = blockIdx.x * 8 + threadIdx.x;
   if (threadIdx.x < 8 && ib < G.nb) out[(int64_t)blockIdx.y * G.nb + ib] = v;
+}
+
+__global__ void radon_adj_pair_kernel(Geo G, const float* __restrict__ y, float* __restrict__ out) {
+  PairLane L;
+  if (pair_gather_lane(G, y, L) && L.live) out[L.r * G.n + L.c] = L.aty;
 }
 
 template <class T>
@@ -643,36 +679,22 @@ __global__ void pdhg_primal_pair_kernel(Geo G, float* __restrict__ x, const floa
                                         float* __restrict__ h, float* __restrict__ xbar, int coin,
                                         float sigma, const float* __restrict__ sig, float hc,
                                         float ps, int nonneg, int32_t* bad, int k) {
-  const int n = G.n, per_row = (n + 1) / 2, pairs = n * per_row;
-  const int lane = threadIdx.x & 31, half = lane & 1, mid = G.na >> 1;
-  const int pq = ((blockIdx.x * blockDim.x + threadIdx.x) >> 1);
-  if ((pq & ~15) >= pairs) return;  // whole warps only (the shuffles below)
-  const int pr = min(pq, pairs - 1);  // (past the end: recomputed, not stored)
-  const int r = pr / per_row, c0 = (pr % per_row) * 2;
-  const float2 v = pixel_gather_tent3_pair(G, y, r, c0, half ? mid : 0, half ? G.na : mid);
-  const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1),
-                               __shfl_xor_sync(0xffffffffu, v.y, 1));
-  const float2 sum = half ? __fadd2_rn(o, v) : __fadd2_rn(v, o);
-  const int c = c0 + half;
-  if (pq < pairs && c < n)
-    pdhg_primal_px(G, x, y, h, xbar, coin, sigma, sig, hc, ps, nonneg, bad, k, r, c,
-                   half ? sum.y : sum.x);
+  PairLane L;
+  if (pair_gather_lane(G, y, L) && L.live)
+    pdhg_primal_px(G, x, y, h, xbar, coin, sigma, sig, hc, ps, nonneg, bad, k, L.r, L.c, L.aty);
 }
 
 // PDHGSkip-1 primal (skip.py:82-114), explicit splitting: on a success draw
 // xhat = (prox_g(x - sigma K^T y) - x) / p, else xhat = 0 (no K^T, no prox);
 // x' = x + xhat / (1 + omega); xbar = x' + xhat feeds the dual step.
 template <class T>
-__global__ void pdhg1_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
-                                    T* __restrict__ xbar, int coin, T sigma, T p, T opw,
-                                    int nonneg, int32_t* bad, int k) {
-  const int n = G.n;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * n) return;
+__device__ __forceinline__ void pdhg1_px(const Geo& G, T* __restrict__ x, const T* __restrict__ y,
+                                         T* __restrict__ xbar, int coin, T sigma, T p, T opw,
+                                         int nonneg, int32_t* bad, int k, int r, int c, T aty) {
+  const int n = G.n, idx = r * n + c;
   const T xo = x[idx];
   T xhat = T(0);
   if (coin) {
-    const int r = idx / n, c = idx % n;
     const T* yy = y + (int64_t)G.na * G.nb;
     const T* yx = yy + (int64_t)n * n;
     T d = T(0);
@@ -680,7 +702,7 @@ __global__ void pdhg1_primal_kernel(Geo G, T* __restrict__ x, const T* __restric
     if (r > 0) d -= yy[idx - n];
     if (c < n - 1) d += yx[idx];
     if (c > 0) d -= yx[idx - 1];
-    const T kty = pixel_gather(G, y, r, c) + (-d);
+    const T kty = aty + (-d);
     T px = xo - sigma * kty;
     if (nonneg) px = px > T(0) ? px : T(0);
     xhat = (px - xo) / p;
@@ -688,8 +710,28 @@ __global__ void pdhg1_primal_kernel(Geo G, T* __restrict__ x, const T* __restric
   const T xn = xo + xhat / opw;
   x[idx] = xn;
   xbar[idx] = xn + xhat;
-  store_xbar_copies(G.xT, G.xpad, n, idx / n, idx % n, xn + xhat);
+  store_xbar_copies(G.xT, G.xpad, n, r, c, xn + xhat);
   if (bad && !isfinite(xn)) atomicMin(bad, k);
+}
+
+template <class T>
+__global__ void pdhg1_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
+                                    T* __restrict__ xbar, int coin, T sigma, T p, T opw,
+                                    int nonneg, int32_t* bad, int k) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= G.n * G.n) return;
+  const int r = idx / G.n, c = idx % G.n;
+  pdhg1_px(G, x, y, xbar, coin, sigma, p, opw, nonneg, bad, k, r, c,
+           coin ? pixel_gather(G, y, r, c) : T(0));
+}
+
+// success draws, fp32 tent gather: pixel-pair lanes (pair_gather_lane)
+__global__ void pdhg1_primal_pair_kernel(Geo G, float* __restrict__ x, const float* __restrict__ y,
+                                         float* __restrict__ xbar, float sigma, float p, float opw,
+                                         int nonneg, int32_t* bad, int k) {
+  PairLane L;
+  if (pair_gather_lane(G, y, L) && L.live)
+    pdhg1_px(G, x, y, xbar, 1, sigma, p, opw, nonneg, bad, k, L.r, L.c, L.aty);
 }
 
 // dual, fidelity block: y_A <- ((y_A + tau A xbar) - tau b) / (1 + tau)   (problems.py:143-144)
@@ -734,14 +776,11 @@ __global__ void pdhg_dual_tv_kernel(int n, const T* __restrict__ xbar, T* __rest
 //   post: x' = u ; h += ps (x' - xhat) ; xbar = 2 x' - x ; x = x'
 // Skipped iterations do pre + post in one pass with x' = xhat.
 template <class T, class TF>
-__global__ void ct_implicit_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
-                                          T* __restrict__ h, T* __restrict__ xbar,
-                                          TF* __restrict__ z, int coin, T sigma, T hc, T ps,
-                                          int32_t* bad, int k) {
-  const int n = G.n;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * n) return;
-  const T kty = pixel_gather(G, y, idx / n, idx % n);
+__device__ __forceinline__ void ct_implicit_pre_px(const Geo& G, T* __restrict__ x, T* __restrict__ h,
+                                                   T* __restrict__ xbar, TF* __restrict__ z,
+                                                   int coin, T sigma, T hc, T ps, int32_t* bad,
+                                                   int k, int r, int c, T kty) {
+  const int n = G.n, idx = r * n + c;
   const T xo = x[idx], ho = h[idx];
   const T t = xo - sigma * kty;
   const T xhat = t + sigma * ho;
@@ -754,8 +793,31 @@ __global__ void ct_implicit_primal_kernel(Geo G, T* __restrict__ x, const T* __r
   h[idx] = ho + ps * (xn - xhat);
   x[idx] = xn;
   xbar[idx] = T(2) * xn - xo;
-  store_xbar_copies(G.xT, G.xpad, n, idx / n, idx % n, T(2) * xn - xo);
+  store_xbar_copies(G.xT, G.xpad, n, r, c, T(2) * xn - xo);
   if (bad && !isfinite(xn)) atomicMin(bad, k);
+}
+
+template <class T, class TF>
+__global__ void ct_implicit_primal_kernel(Geo G, T* __restrict__ x, const T* __restrict__ y,
+                                          T* __restrict__ h, T* __restrict__ xbar,
+                                          TF* __restrict__ z, int coin, T sigma, T hc, T ps,
+                                          int32_t* bad, int k) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= G.n * G.n) return;
+  const int r = idx / G.n, c = idx % G.n;
+  ct_implicit_pre_px<T, TF>(G, x, h, xbar, z, coin, sigma, hc, ps, bad, k, r, c,
+                            pixel_gather(G, y, r, c));
+}
+
+// fp32 tent gather: pixel-pair lanes (pair_gather_lane)
+template <class TF>
+__global__ void ct_implicit_primal_pair_kernel(Geo G, float* __restrict__ x, const float* __restrict__ y,
+                                               float* __restrict__ h, float* __restrict__ xbar,
+                                               TF* __restrict__ z, int coin, float sigma, float hc,
+                                               float ps, int32_t* bad, int k) {
+  PairLane L;
+  if (pair_gather_lane(G, y, L) && L.live)
+    ct_implicit_pre_px<float, TF>(G, x, h, xbar, z, coin, sigma, hc, ps, bad, k, L.r, L.c, L.aty);
 }
 
 template <class T, class TF>
@@ -819,7 +881,11 @@ int radon_adj(int dtype, const psb_radon_geom* g, const void* y, void* out, cuda
   Geo G = make_geo(g);
   dim3 grid((G.n * G.n + 255) / 256);
   if (dtype == PSB_F32)
-    radon_adj_kernel<float><<<grid, 256, 0, st>>>(G, (const float*)y, (float*)out);
+    if (tent3_ok(G))
+      radon_adj_pair_kernel<<<(pair_lanes(G) + 127) / 128, 128, 0, st>>>(G, (const float*)y,
+                                                                          (float*)out);
+    else
+      radon_adj_kernel<float><<<grid, 256, 0, st>>>(G, (const float*)y, (float*)out);
   else if (dtype == PSB_F64)
     radon_adj_kernel<double><<<grid, 256, 0, st>>>(G, (const double*)y, (double*)out);
   else
@@ -835,8 +901,7 @@ int pdhg_step_t(const Geo& G, T* x, T* y, T* h, T* xbar, const T* b, int32_t* ba
   const int npx = G.n * G.n;
   const int64_t nfid = (int64_t)G.na * G.nb;
   if (sizeof(T) == 4 && tent3_ok(G)) {
-    const int lanes = 2 * G.n * ((G.n + 1) / 2);
-    pdhg_primal_pair_kernel<<<(lanes + 127) / 128, 128, 0, st>>>(G, (float*)x, (const float*)y, (float*)h,
+    pdhg_primal_pair_kernel<<<(pair_lanes(G) + 127) / 128, 128, 0, st>>>(G, (float*)x, (const float*)y, (float*)h,
                                                     (float*)xbar, coin, (float)sigma,
                                                     (const float*)sig, (float)hc, (float)ps,
                                                     nonneg, bad, k);
@@ -881,8 +946,13 @@ int pdhg1_step(int dtype, const psb_radon_geom* g, void* x, void* y, void* xbar,
   const int64_t nfid = (int64_t)G.na * G.nb;
   auto go = [&](auto tag) -> int {
     using T = decltype(tag);
-    pdhg1_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(G, (T*)x, (const T*)y, (T*)xbar, coin,
-                                                             (T)sigma, (T)p, (T)opw, nonneg, bad, k);
+    if (sizeof(T) == 4 && coin && tent3_ok(G))
+      pdhg1_primal_pair_kernel<<<(pair_lanes(G) + 127) / 128, 128, 0, st>>>(
+          G, (float*)x, (const float*)y, (float*)xbar, (float)sigma, (float)p, (float)opw, nonneg,
+          bad, k);
+    else
+      pdhg1_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(
+          G, (T*)x, (const T*)y, (T*)xbar, coin, (T)sigma, (T)p, (T)opw, nonneg, bad, k);
     PSB_LAUNCHED("pdhg1_primal");
     pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, (const T*)xbar, (T*)y,
                                                                   (const T*)b, (T)tau, nullptr);
@@ -910,8 +980,17 @@ int ct_implicit_step(const Geo& G, T* x, T* y, T* h, T* xbar, TF* z, TF* q, cons
                      const double* betas, int32_t* bad, int k, cudaStream_t st) {
   const int npx = G.n * G.n;
   const int dtf = sizeof(TF) == 4 ? PSB_F32 : PSB_F64;
-  ct_implicit_primal_kernel<T, TF><<<(npx + 255) / 256, 256, 0, st>>>(
-      G, x, y, h, xbar, z, coin, (T)sigma, (T)hc, (T)ps, bad, k);
+  if constexpr (sizeof(T) == 4) {
+    if (tent3_ok(G))
+      ct_implicit_primal_pair_kernel<TF><<<(pair_lanes(G) + 127) / 128, 128, 0, st>>>(
+          G, x, y, h, xbar, z, coin, (T)sigma, (T)hc, (T)ps, bad, k);
+    else
+      ct_implicit_primal_kernel<T, TF><<<(npx + 255) / 256, 256, 0, st>>>(
+          G, x, y, h, xbar, z, coin, (T)sigma, (T)hc, (T)ps, bad, k);
+  } else {
+    ct_implicit_primal_kernel<T, TF><<<(npx + 255) / 256, 256, 0, st>>>(
+        G, x, y, h, xbar, z, coin, (T)sigma, (T)hc, (T)ps, bad, k);
+  }
   PSB_LAUNCHED("ct_implicit_primal");
   if (coin) {
     if (int rc = fgp2d_run(dtf, z, npx, q, 6LL * npx, one_d, 1, weight, nullptr, 0, rep_d, G.n, G.n,
