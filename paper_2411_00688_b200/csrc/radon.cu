@@ -751,10 +751,9 @@ __global__ void __launch_bounds__(256, 6) pdhg_dual_fid_kernel(Geo G, const T* _
 
 // dual, TV block: y_D <- P_alpha(y_D + tau grad xbar)   (problems.py:145)
 template <class T>
-__global__ void pdhg_dual_tv_kernel(int n, const T* __restrict__ xbar, T* __restrict__ yD, T tau,
-                                    const T* __restrict__ tauD, T alpha) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * n) return;
+__device__ __forceinline__ void pdhg_dual_tv_px(int n, int idx, const T* __restrict__ xbar,
+                                                T* __restrict__ yD, T tau,
+                                                const T* __restrict__ tauD, T alpha) {
   const int r = idx / n, c = idx % n;
   const T v = xbar[idx];
   const T gy = r < n - 1 ? xbar[idx + n] - v : T(0);
@@ -765,6 +764,38 @@ __global__ void pdhg_dual_tv_kernel(int n, const T* __restrict__ xbar, T* __rest
   const T sc = alpha / (alpha > m ? alpha : m);
   yD[idx] = a * sc;
   yD[(int64_t)n * n + idx] = bb * sc;
+}
+
+// Both dual blocks in one launch: blocks (x, y < na) project rays (the
+// fidelity block), blocks of the extra rows y >= na update 256 pixels of the
+// TV block each -- they fill the SMs the ray blocks leave idle, and one launch
+// less per iteration.
+template <class T>
+__global__ void __launch_bounds__(256, 6)
+    pdhg_dual_kernel(Geo G, const T* __restrict__ xbar, T* __restrict__ y, const T* __restrict__ b,
+                     T tau0, const T* __restrict__ tau_arr, T alpha) {
+  if ((int)blockIdx.y < G.na) {
+    __shared__ T part[8][8];
+    const T ax = fwd_block_sum<T>(G, xbar, static_cast<const T*>(G.xT), part);
+    const int ib = blockIdx.x * 8 + threadIdx.x;
+    if (threadIdx.x < 8 && ib < G.nb) {
+      const int64_t ray = (int64_t)blockIdx.y * G.nb + ib;
+      const T tau = tau_arr ? tau_arr[ray] : tau0;
+      const T v = y[ray] + tau * ax;
+      y[ray] = (v - tau * b[ray]) / (T(1) + tau);
+    }
+    return;
+  }
+  const int idx = (((int)blockIdx.y - G.na) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= G.n * G.n) return;
+  const int64_t nfid = (int64_t)G.na * G.nb;
+  pdhg_dual_tv_px(G.n, idx, xbar, y + nfid, tau0, tau_arr ? tau_arr + nfid : nullptr, alpha);
+}
+inline dim3 dual_grid(const Geo& G) {
+  dim3 g = fwd_grid(G);
+  const int tv_blocks = (G.n * G.n + 255) / 256;
+  g.y += (tv_blocks + g.x - 1) / g.x;
+  return g;
 }
 
 // ---- implicit splitting K = A, TV inside the warm-started FGP prox --------
@@ -910,11 +941,8 @@ int pdhg_step_t(const Geo& G, T* x, T* y, T* h, T* xbar, const T* b, int32_t* ba
         G, x, y, h, xbar, coin, (T)sigma, sig, (T)hc, (T)ps, nonneg, bad, k);
   }
   PSB_LAUNCHED("pdhg_primal");
-  pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, xbar, y, b, (T)tau, tau_arr);
-  PSB_LAUNCHED("pdhg_dual_fid");
-  pdhg_dual_tv_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(
-      G.n, xbar, y + nfid, (T)tau, tau_arr ? tau_arr + nfid : nullptr, (T)alpha);
-  PSB_LAUNCHED("pdhg_dual_tv");
+  pdhg_dual_kernel<T><<<dual_grid(G), 256, 0, st>>>(G, xbar, y, b, (T)tau, tau_arr, (T)alpha);
+  PSB_LAUNCHED("pdhg_dual");
   return PSB_OK;
 }
 
@@ -954,12 +982,9 @@ int pdhg1_step(int dtype, const psb_radon_geom* g, void* x, void* y, void* xbar,
       pdhg1_primal_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(
           G, (T*)x, (const T*)y, (T*)xbar, coin, (T)sigma, (T)p, (T)opw, nonneg, bad, k);
     PSB_LAUNCHED("pdhg1_primal");
-    pdhg_dual_fid_kernel<T><<<fwd_grid(G), 256, 0, st>>>(G, (const T*)xbar, (T*)y,
-                                                                  (const T*)b, (T)tau, nullptr);
-    PSB_LAUNCHED("pdhg_dual_fid");
-    pdhg_dual_tv_kernel<T><<<(npx + 255) / 256, 256, 0, st>>>(G.n, (const T*)xbar, (T*)y + nfid,
-                                                              (T)tau, nullptr, (T)alpha);
-    PSB_LAUNCHED("pdhg_dual_tv");
+    pdhg_dual_kernel<T><<<dual_grid(G), 256, 0, st>>>(G, (const T*)xbar, (T*)y, (const T*)b,
+                                                      (T)tau, nullptr, (T)alpha);
+    PSB_LAUNCHED("pdhg_dual");
     return PSB_OK;
   };
   if (dtype == PSB_F32) return go(float{});
