@@ -1,0 +1,109 @@
+// Cluster / DSMEM / mbarrier PTX helpers shared by the cluster-resident run
+// kernels (fgp_cluster.cu: 16 CTAs x 4 rows per thread, fgp_cluster8.cu:
+// 8 CTAs x 8 rows per thread).
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace psb {
+
+template <class TO>
+__device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
+  using A = Ar<TO>;
+  return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
+}
+
+// 32-bit shared::cluster address of `p` in CTA `rank` of this cluster, and a load from it
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
+  uint32_t local = (uint32_t)__cvta_generic_to_shared(p), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  return remote;
+}
+template <class T>
+__device__ __forceinline__ T dsmem_ld(uint32_t addr) {
+  if constexpr (std::is_same<T, int>::value) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+  } else if constexpr (sizeof(T) == 8) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+  } else {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+  }
+}
+
+// ---- point-to-point halo rows: st.async into the neighbour's shared memory,
+// completion counted in bytes on the neighbour's mbarrier (no cluster-wide
+// barrier, no memory fence on the critical path) -----------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+#ifdef PSB_DBG_NOGSYNC  // timing experiment only: row-group waits skipped (results invalid)
+#define GWAIT(m, ph) ((void)0)
+#else
+#define GWAIT(m, ph) mbar_wait(m, ph)
+#endif
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(raddr),
+               "r"(__float_as_uint(v)), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, float v0, float v1, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(rmbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float v0, float v1, float v2, float v3,
+                                            uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(raddr),
+               "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(__float_as_uint(v2)),
+               "r"(__float_as_uint(v3)), "r"(rmbar)
+               : "memory");
+}
+
+// MUFU.RSQ without the denormal rescaling rsqrtf() wraps around it (|a|^2 of a
+// dual vector is never denormal in a way that matters: the ball test is
+// min(1, w / |a|)); 1 instruction instead of ~6 per pixel.
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+}  // namespace psb

@@ -33,6 +33,12 @@ int blur_grad2d(int dtype, const void* u, const void* b, void* g, int H, int W,
                 cudaStream_t st);
 bool cluster_shape_ok(int H, int W);
 int cluster_count();
+int cluster8_count();
+int cluster8_run(void* x, const void* b, void* h, void* q, int64_t qps, const WorkQueue& wq, int G,
+                 const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K, int n_inner,
+                 int accelerated, int nonneg, double weight, double gamma, double hc, double pg,
+                 double step, const float* betas, int32_t* bad, const ChunkSync& cs,
+                 cudaStream_t st);
 int sm_prepare();
 int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const WorkQueue& wq,
            int n_workers, const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K,
@@ -192,6 +198,14 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   std::vector<uint8_t> rep_p;
   std::vector<float> beta_f;
   int G = 0, NW = 0;
+  // PSB_CLUSTER8=1 (fp32 outer state): the 8-CTA cluster kernel
+  // (fgp_cluster8.cu: 16 px per thread, q_{k-1} and z in shared memory) --
+  // bit-identical, measured equal per SM to the 16-CTA kernel (shared-memory
+  // bound instead of synchronisation bound); kept for comparisons and for
+  // devices whose GPCs cannot host seven 16-CTA clusters
+  const char* c8 = std::getenv("PSB_CLUSTER8");
+  const bool use8 = dto == PSB_F32 && c8 && c8[0] == '1';
+  const int ccl = use8 ? 8 : 16;
   if (use_cluster) {
     ev_off.assign(n + 1, 0);
     for (size_t e = 0; e < act.size(); ++e) ev_off[act[e] + 1] += 1;
@@ -213,14 +227,14 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     const char* no_sm = std::getenv("PSB_NO_SMWORK");
     const char* sm_only = std::getenv("PSB_SM_ONLY");
     const bool only_sm = sm_only && sm_only[0] == '1' && dto == PSB_F32 && !use_graph;
-    G = only_sm ? 0 : (int)std::min<int64_t>(n, cluster_count());
+    G = only_sm ? 0 : (int)std::min<int64_t>(n, use8 ? cluster8_count() : cluster_count());
     if (only_sm) {  // PSB_SM_WORKERS caps the worker count (profiling the 36-SM share)
       const char* nws = std::getenv("PSB_SM_WORKERS");
       const int cap = nws ? std::max(1, std::atoi(nws)) : sm_count();
       NW = (int)std::min<int64_t>(n, std::min(cap, sm_count()));
     }
     else if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1'))
-      NW = std::max(0, sm_count() - G * 16);
+      NW = std::max(0, sm_count() - G * ccl);
     auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
     order.resize(n);
     for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
@@ -331,9 +345,12 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       cudaEventRecord(d0, st);
     }
     if (rc == PSB_OK)
-      rc = cluster_run(dto, x, b, h, q, qps, wq, G, i32(o_evo), i32(o_evk), dev + o_repp, K,
-                       n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d, bad,
-                       cs, st);
+      rc = use8 ? cluster8_run(x, b, h, q, qps, wq, G, i32(o_evo), i32(o_evk), dev + o_repp, K,
+                               n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
+                               beta_d, bad, cs, st)
+                : cluster_run(dto, x, b, h, q, qps, wq, G, i32(o_evo), i32(o_evk), dev + o_repp, K,
+                              n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d,
+                              bad, cs, st);
     // The SM workers follow in the same stream as a programmatic dependent:
     // they are placed once every cluster CTA has started (griddepcontrol.
     // launch_dependents at the top of the cluster kernel), so they can never

@@ -1,0 +1,770 @@
+// Cluster-resident ProxSkip runs for 256 x 256 problems, fp32 outer state
+// (BASELINE config 4), on 8-CTA clusters: the same run segment, schedule and
+// per-pixel arithmetic as fgp_cluster.cu (skip.py:46-79, tv.py:53-89 -- see
+// the header comment there), with twice the pixels per SM.
+//
+//   cluster = 8 CTAs x 32 rows; CTA = 512 threads = 4 row groups of 8 rows;
+//   thread  = 2 columns x 8 rows, held as row pairs (t, t + 4) in float2
+//             registers (packed FFMA2 / FADD2 / FMUL2 on aligned pairs; only
+//             one pair per column strip end is built from two halves).
+//
+// 16 pixels per thread do not fit the register file with z, q_k and q_{k-1}
+// all resident (80 state registers + temporaries > 128), so only q_k lives in
+// registers: the prox input z and the previous dual iterate q_{k-1} are
+// thread-private float4 columns in shared memory ([slot][tid]: conflict-free
+// LDS / STS), read once and written once per inner iteration
+// (20 B/px: ~1280 shared-memory cycles per 8192-px iteration, under the
+// ~1000 issue cycles it overlaps with).  What this buys over the 16-CTA form:
+// every synchronisation of the inner loop (warp-edge columns, row-group rows,
+// the DSMEM halo round trip) is paid once per 16 pixels of a thread instead
+// of once per 8, eight independent pair chains per thread instead of four,
+// and 8-CTA clusters tile the GPCs without leaving a quarter of the SMs to
+// the slower one-SM workers.
+//
+// Every pixel's arithmetic is the scalar FGP step of the other kernels
+// (each f32x2 lane an IEEE fp32 op), so results are bit-identical to
+// fgp_cluster_run_kernel, fgp_sm_run_kernel and the streaming path.
+#include <cooperative_groups.h>
+
+#include <type_traits>
+
+#include "cluster_ptx.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace psb {
+
+namespace {
+
+constexpr int CW = 256;                  // image width
+constexpr int CRPT = 8;                  // rows per thread
+constexpr int NP = CRPT / 2;             // row pairs (t, t + NP) per column strip
+constexpr int CTPR = CW / 2;             // threads per row group (2 columns each)
+constexpr int CRG = 4;                   // row groups per CTA
+constexpr int CCL = 8;                   // CTAs per cluster
+constexpr int SR = CRG * CRPT;           // rows per CTA (32)
+constexpr int CH = CCL * SR;             // image height = 256
+constexpr int CTHREADS = CTPR * CRG;     // 512
+constexpr int CWARPS_ROW = CTPR / 32;    // 4 warps across a row group
+constexpr int kMaxBetas = 1024;
+static_assert(CH == 256 && CTHREADS == 512, "256 x 256 problems on 8 x 512 threads");
+
+struct Run8Args {
+  float* x;
+  const float* b;
+  float* h;
+  float* q;  // warm-start slot 0 of problem p: q + p*qps (channel stride CH*CW)
+  int64_t qps;
+  WorkQueue wq;
+  const int32_t* ev_off;  // [n + 1]: problem p's coin-fired iterations ev_k[ev_off[p] ..]
+  const int32_t* ev_k;    // ascending, 0 .. K-1 (this run segment)
+  const uint8_t* rep;     // [n]: re-project the warm start at the first prox call (tv.py:68-69)
+  int K;
+  int n_inner;
+  int accelerated;
+  float weight;
+  float gamma, hc, pg;
+  float step;
+  int32_t* bad;        // [n]: first non-finite iteration (atomicMin)
+  const float* betas;  // device table beta[0..n_inner-1]
+  ChunkSync cs;
+};
+
+// Packed fp32 pairs as 64-bit registers (fma/add/mul.rn.f32x2 operate on .b64):
+// lo = row t, hi = row t + NP of a column strip.  No mul is ever followed by
+// an add of its result here (ptxas would contract that pair into an FFMA2).
+using P2 = unsigned long long;
+__device__ __forceinline__ P2 pk(float lo, float hi) {
+  P2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float plo(P2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float phi(P2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ P2 pfma(P2 a, P2 b, P2 c) {
+  P2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ P2 padd(P2 a, P2 b) {
+  P2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ P2 pmul(P2 a, P2 b) {
+  P2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// row t of a column strip held as pairs (t, t + NP)
+__device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
+  return t < NP ? v[t].x : v[t - NP].y;
+}
+
+constexpr size_t kStageBytes = (size_t)3 * SR * CW * sizeof(float);           // x, b, h rows
+constexpr size_t kQmBytes = (size_t)2 * NP * CTHREADS * sizeof(float4);       // q_{k-1}
+constexpr size_t kZBytes = (size_t)NP * CTHREADS * sizeof(float4);            // z
+constexpr size_t kDynBytes = kStageBytes + kQmBytes + kZBytes;
+
+template <bool NONNEG>
+__global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args a) {
+  using F = Ar<float>;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const int jt = tid % CTPR, rg = tid / CTPR;  // column pair, row group
+  const int j0 = 2 * jt;                        // columns j0, j0 + 1
+  const int lane = tid & 31, wc = jt >> 5;
+  const int row0 = cr * SR + rg * CRPT;
+  const bool rg_top = rg == 0, rg_bot = rg == CRG - 1;
+  const bool has_up = cr > 0, has_dn = cr < CCL - 1;
+  constexpr int64_t HW = (int64_t)CH * CW;
+
+  // halo rows received from the neighbour CTAs, double-buffered by round parity
+  __shared__ __align__(16) float rx_dn[2][CW][2];  // CTA below's first row of y (y, x)
+  __shared__ __align__(8) float rx_up[2][CW];      // CTA above's last row of y (y)
+  __shared__ __align__(8) uint64_t mb_dn[2], mb_up[2];
+  __shared__ __align__(16) float rx_z[CW];  // CTA below's first row of z, once per prox call
+  __shared__ __align__(8) uint64_t mb_z;
+  // row-group mbarriers, one phase per inner iteration (see fgp_cluster.cu)
+  __shared__ __align__(8) uint64_t gE1[CRG], gE2[CRG], gYY[CRG], gU[CRG];
+  __shared__ __align__(8) float s_rg_yy[CRG][CW];  // each row group's last-row y_y
+  __shared__ __align__(8) float s_rg_u[CRG][CW];   // each row group's first-row u
+  // warp-edge columns as row pairs: s_edge_yx[rg][P][w + 1] = last column of
+  // warp w (slot 0 stays zero), s_edge_u[rg][P][w] = first column of warp w
+  __shared__ __align__(16) P2 s_edge_yx[CRG][NP][CWARPS_ROW + 1];
+  __shared__ __align__(16) P2 s_edge_u[CRG][NP][CWARPS_ROW];
+  __shared__ float s_beta[kMaxBetas];
+  __shared__ int s_next[2];
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  float* sx = reinterpret_cast<float*>(dyn_raw);  // [SR][CW]
+  float* sb = sx + SR * CW;
+  float* sh = sb + SR * CW;
+  // thread-private columns: s_qmy / s_qmx[k * NP + P][tid] = the row pair P of
+  // column k of q_{k-1} (float2 slots: the packed results go straight from
+  // their register pairs to STS.64, no quad assembly);
+  // s_z[P][tid] = (z col 0 pair P, z col 1 pair P)
+  P2* s_qmy = reinterpret_cast<P2*>(dyn_raw + kStageBytes);
+  P2* s_qmx = s_qmy + 2 * NP * CTHREADS;
+  ulonglong2* s_z = reinterpret_cast<ulonglong2*>(dyn_raw + kStageBytes + kQmBytes);
+
+  const float g = a.gamma;
+  const float w = a.weight;
+  constexpr bool nonneg = NONNEG;
+  for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
+  if (tid < CRG * NP) s_edge_yx[tid / NP][tid % NP][0] = pk(0.f, 0.f);
+  if (tid == 0) {
+    mbar_init(&mb_dn[0], 1);
+    mbar_init(&mb_dn[1], 1);
+    mbar_init(&mb_up[0], 1);
+    mbar_init(&mb_up[1], 1);
+    mbar_init(&mb_z, 1);
+    for (int gi = 0; gi < CRG; ++gi) {
+      mbar_init(&gE1[gi], CTPR);
+      mbar_init(&gE2[gi], CTPR);
+      mbar_init(&gYY[gi], CTPR);
+      mbar_init(&gU[gi], CTPR);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // every CTA of this grid is resident: the SM-worker kernel (a programmatic
+  // dependent) may now be placed on the SMs the clusters left
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  cluster_arrive();  // every CTA's mbarriers exist before anyone pushes
+  cluster_wait();
+  constexpr unsigned BYTES_DN = CW * 2 * 4, BYTES_UP = CW * 4;
+  const uint32_t up_rx_remote = dsmem_addr(&rx_dn[0][0][0], has_up ? cr - 1 : cr);  // my top row -> CTA above
+  const uint32_t up_mb_remote = dsmem_addr(&mb_dn[0], has_up ? cr - 1 : cr);
+  const uint32_t dn_rx_remote = dsmem_addr(&rx_up[0][0], has_dn ? cr + 1 : cr);  // my bottom row -> CTA below
+  const uint32_t dn_mb_remote = dsmem_addr(&mb_up[0], has_dn ? cr + 1 : cr);
+  const uint32_t z_rx_remote = dsmem_addr(&rx_z[0], has_up ? cr - 1 : cr);
+  const uint32_t z_mb_remote = dsmem_addr(&mb_z, has_up ? cr - 1 : cr);
+  unsigned zph = 0;    // prox calls so far (mb_z phases)
+  unsigned round = 0;  // halo rounds so far (round r lands in buffer r & 1)
+  unsigned gph = 0;    // inner iterations so far (row-group mbarrier phases)
+  const bool arm = lane == 0 && wc == 0;
+  auto push_up = [&](float ty0, float tx0, float ty1, float tx1) {  // top group, has_up
+#ifdef PSB_DBG_NOHALO
+    return;
+#endif
+    const unsigned b = round & 1;
+    st_async_v4(up_rx_remote + 4u * (b * CW * 2 + j0 * 2), ty0, tx0, ty1, tx1, up_mb_remote + 8u * b);
+  };
+  auto push_dn = [&](float by0, float by1) {  // bottom group, has_dn
+#ifdef PSB_DBG_NOHALO
+    return;
+#endif
+    const unsigned b = round & 1;
+    st_async_v2(dn_rx_remote + 4u * (b * CW + j0), by0, by1, dn_mb_remote + 8u * b);
+  };
+  auto recv_up = [&](unsigned r) {  // top group, has_up
+    const unsigned b = r & 1, ph = (r >> 1) & 1;
+#ifdef PSB_DBG_NOHALO
+    return b;
+#endif
+    if (arm) mbar_expect_tx(&mb_up[b], BYTES_UP);
+    mbar_wait(&mb_up[b], ph);
+    return b;
+  };
+  auto recv_dn = [&](unsigned r) {  // bottom group, has_dn
+    const unsigned b = r & 1, ph = (r >> 1) & 1;
+#ifdef PSB_DBG_NOHALO
+    return b;
+#endif
+    if (arm) mbar_expect_tx(&mb_dn[b], BYTES_DN);
+    mbar_wait(&mb_dn[b], ph);
+    return b;
+  };
+  const bool right_fetch = lane == 31 && wc < CWARPS_ROW - 1;
+  const bool last_col = lane == 31 && wc == CWARPS_ROW - 1;  // owns global column W-1
+
+  const uint32_t next_remote = dsmem_addr(&s_next[0], 0);
+  uint64_t t_claim = 0;
+  for (unsigned pj = 0;; ++pj) {
+    // rank 0 claims the next problem; everyone reads it after the barrier
+    if (cr == 0 && tid == 0) s_next[pj & 1] = wq_claim(a.wq);
+    cluster_arrive();
+    cluster_wait();
+    const int pos = dsmem_ld<int>(next_remote + 4u * (pj & 1));
+    if (pos < 0) break;
+    const int p = a.wq.order[pos];
+    float* xp = a.x + (int64_t)p * HW;
+    const float* bp = a.b + (int64_t)p * HW;
+    float* hp = a.h + (int64_t)p * HW;
+    float* q0 = a.q + (int64_t)p * a.qps;
+    const int e0 = a.ev_off[p], e1 = a.ev_off[p + 1];
+    const bool rep = a.rep[p];
+    if (a.cs.ready) {  // this problem's input chunk has arrived
+      if (tid == 0) chunk_wait(a.cs, p);
+      __syncthreads();
+    }
+    if (cr == 0 && tid == 0) t_claim = gtimer_ns();
+    // stage this CTA's rows of x, b, h (each thread its own elements) and the
+    // warm-start duals; a streamed run starts cold (x = h = 0, q_warm = 0
+    // implied, device buffers uninitialised)
+    const bool cold = a.cs.ready != nullptr;
+    float2 qky[2][NP], qkx[2][NP];  // q_k: per column k, row pairs
+    {
+      const bool ldq = !(cold || e1 == e0);
+#pragma unroll
+      for (int t = 0; t < CRPT; ++t) {
+        const int lr = rg * CRPT + t;
+        const int64_t o = (int64_t)(row0 + t) * CW + j0;
+        const float2 zero2 = make_float2(0.f, 0.f);
+        const float2 xv = cold ? zero2 : *reinterpret_cast<const float2*>(xp + o);
+        const float2 bv = *reinterpret_cast<const float2*>(bp + o);
+        const float2 hv = cold ? zero2 : *reinterpret_cast<const float2*>(hp + o);
+        const float2 qy = ldq ? *reinterpret_cast<const float2*>(q0 + o) : zero2;
+        const float2 qx = ldq ? *reinterpret_cast<const float2*>(q0 + HW + o) : zero2;
+        *reinterpret_cast<float2*>(&sx[lr * CW + j0]) = xv;
+        *reinterpret_cast<float2*>(&sb[lr * CW + j0]) = bv;
+        *reinterpret_cast<float2*>(&sh[lr * CW + j0]) = hv;
+        rowref(qky[0], t) = qy.x;
+        rowref(qky[1], t) = qy.y;
+        rowref(qkx[0], t) = qx.x;
+        rowref(qkx[1], t) = qx.y;
+      }
+    }
+    int kbad = 0x7fffffff;
+    int kprev = -1;
+    for (int e = e0; e < e1; ++e) {
+      const int kk = a.ev_k[e];
+      const int m = kk - kprev - 1;  // skip iterations kprev+1 .. kk-1 before this prox call
+      const int kf = kprev + 1;
+      __syncthreads();
+      // ---- prologue: skips, prox input, warm start ----------------------------
+      float z_top[2] = {0.f, 0.f};  // row 0 of this thread's z (top group: pushed up)
+      {
+        float2 z[2][NP];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+#pragma unroll
+          for (int t = 0; t < CRPT; ++t) {
+            const int sj = (rg * CRPT + t) * CW + j0 + k;
+            const float bo = sb[sj], ho = sh[sj];
+            const float xo = skip_chain_px(sx[sj], bo, ho, g, m, kf, &kbad);
+            if (m > 0) sx[sj] = xo;
+            rowref(z[k], t) = F::add(F::sub(xo, F::mul(g, F::sub(xo, bo))), F::mul(a.hc, ho));
+            if (e == e0) {  // warm start (staged above), re-projected if the weight changed
+              float vy = rowref(qky[k], t), vx = rowref(qkx[k], t);
+              if (rep) {
+                const float sc = F::ball_scale(vy, vx, w);
+                vy *= sc;
+                vx *= sc;
+              }
+              // q_y on the last row and q_x on the last column stay 0
+              // (operators.py:66-70): zero padding instead of boundary masks
+              if (row0 + t == CH - 1) vy = 0.f;
+              if (j0 + k == CW - 1) vx = 0.f;
+              rowref(qky[k], t) = vy;
+              rowref(qkx[k], t) = vx;
+            }
+          }
+        }
+#pragma unroll
+        for (int P = 0; P < NP; ++P)
+          s_z[P * CTHREADS + tid] = make_ulonglong2(pk(z[0][P].x, z[0][P].y), pk(z[1][P].x, z[1][P].y));
+        z_top[0] = z[0][0].x;
+        z_top[1] = z[1][0].x;
+      }
+      // the bottom row group also owns the CTA-below's first row for u: its z
+      // arrives from that CTA (st.async on mb_z); mine goes to the CTA above
+      if (rg_top && has_up) st_async_v2(z_rx_remote + 4u * j0, z_top[0], z_top[1], z_mb_remote);
+      float z_ex[2] = {0.f, 0.f};
+      if (rg_bot && has_dn) {
+        if (arm) mbar_expect_tx(&mb_z, CW * 4);
+        mbar_wait(&mb_z, zph & 1u);
+        z_ex[0] = rx_z[j0];
+        z_ex[1] = rx_z[j0 + 1];
+      }
+      ++zph;
+      // After the first call of a problem the warm start's boundary rows are
+      // the previous call's final round (no exchange); halo rows travel as
+      // momentum iterates y (fgp_cluster.cu)
+      const bool reuse = e > e0;
+      const unsigned round0 = reuse ? round - 1 : round;  // this call's warm-start round
+      auto y0_of = [](float q) { return fmaf(0.f, fmaf(q, -1.f, q), q); };
+      if (!reuse) {
+#ifndef PSB_DBG_NOHALO
+        if (rg_top && has_up)
+          push_up(y0_of(qky[0][0].x), y0_of(qkx[0][0].x), y0_of(qky[1][0].x), y0_of(qkx[1][0].x));
+        if (rg_bot && has_dn) push_dn(y0_of(qky[0][NP - 1].y), y0_of(qky[1][NP - 1].y));
+#endif
+        ++round;
+      }
+
+      // One inner iteration: y from (q_k registers, q_{k-1} shared memory),
+      // q_k -> shared memory (the next q_{k-1}), the new iterate -> q_k
+      // registers.  ROLE (warp-uniform): 0 top / 1 middle / 2 bottom group.
+      auto run_inner = [&](auto role_tag) {
+        constexpr int ROLE = decltype(role_tag)::value;
+        constexpr bool TOP = ROLE == 0, BOT = ROLE == 2;
+        // the loop-carried iterate as 64-bit register pairs (P2), so the values
+        // cross the back-edge as pairs and need no re-pairing moves
+        P2 QY[2][NP], QX[2][NP];
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int P = 0; P < NP; ++P) {
+            QY[k][P] = pk(qky[k][P].x, qky[k][P].y);
+            QX[k][P] = pk(qkx[k][P].x, qkx[k][P].y);
+          }
+        const P2 m1 = pk(-1.f, -1.f);
+        const float wr = w * kBallShrink;
+        const P2 st2 = pk(a.step, a.step), w2 = pk(wr, wr);
+        auto inner = [&](int it, auto first_tag) {
+          constexpr bool FIRST = decltype(first_tag)::value;
+          const unsigned ph = gph & 1u;
+          const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
+          const P2 b2 = pk(beta, beta);
+          P2 yy[2][NP], yx[2][NP];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int P = 0; P < NP; ++P) {
+              P2 my = QY[k][P], mx = QX[k][P];  // (the momentum restarts with every call)
+              if constexpr (!FIRST) {
+                my = s_qmy[(k * NP + P) * CTHREADS + tid];
+                mx = s_qmx[(k * NP + P) * CTHREADS + tid];
+              }
+              yy[k][P] = pfma(b2, pfma(my, m1, QY[k][P]), QY[k][P]);
+              yx[k][P] = pfma(b2, pfma(mx, m1, QX[k][P]), QX[k][P]);
+            }
+          // q_k becomes q_{k-1} (its halo entries for the y pushed below are kept)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int P = 0; P < NP; ++P) {
+              s_qmy[(k * NP + P) * CTHREADS + tid] = QY[k][P];
+              s_qmx[(k * NP + P) * CTHREADS + tid] = QX[k][P];
+            }
+          float old_e[4];
+          if constexpr (TOP) {
+            old_e[0] = plo(QY[0][0]), old_e[1] = plo(QX[0][0]), old_e[2] = plo(QY[1][0]), old_e[3] = plo(QX[1][0]);
+          }
+          if constexpr (BOT) {
+            old_e[0] = phi(QY[0][NP - 1]), old_e[1] = phi(QY[1][NP - 1]);
+          }
+          if constexpr (!BOT) {  // last-row y_y for the group below
+            *reinterpret_cast<float2*>(&s_rg_yy[rg][j0]) = make_float2(phi(yy[0][NP - 1]), phi(yy[1][NP - 1]));
+            mbar_arrive(&gYY[rg]);
+          }
+          if (lane == 31) {
+#pragma unroll
+            for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
+          }
+          mbar_arrive(&gE1[rg]);
+          float2 yyA = make_float2(0.f, 0.f);  // TOP: y row above (zeros at row 0)
+          float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
+          if constexpr (TOP) {
+            if (has_up) {
+              const bool warm = reuse && it == 0;  // (already received: final round)
+              const unsigned par = warm ? (round0 & 1u) : recv_up(round0 + it);
+              yyA = *reinterpret_cast<const float2*>(&rx_up[par][j0]);
+              if (warm) yyA = make_float2(y0_of(yyA.x), y0_of(yyA.y));
+            }
+          }
+          if constexpr (BOT) {
+            if (has_dn) {
+              const bool warm = reuse && it == 0;
+              const unsigned par = warm ? (round0 & 1u) : recv_dn(round0 + it);
+              const float4 v = *reinterpret_cast<const float4*>(&rx_dn[par][j0][0]);
+              ex_y[0] = v.x, ex_x[0] = v.y, ex_y[1] = v.z, ex_x[1] = v.w;
+              if (j0 > 0) ledge_x = rx_dn[par][j0 - 1][1];
+              if (warm) {
+                ex_y[0] = y0_of(ex_y[0]), ex_x[0] = y0_of(ex_x[0]);
+                ex_y[1] = y0_of(ex_y[1]), ex_x[1] = y0_of(ex_x[1]);
+                ledge_x = y0_of(ledge_x);
+              }
+            }
+          }
+          GWAIT(&gE1[rg], ph);
+          // left neighbours of column 0: shuffles inside the warp, the warp to
+          // the left's last column from shared memory (zeros left of column 0)
+          P2 left[NP];
+#pragma unroll
+          for (int P = 0; P < NP; ++P)
+            left[P] = pk(__shfl_up_sync(0xffffffffu, plo(yx[1][P]), 1),
+                         __shfl_up_sync(0xffffffffu, phi(yx[1][P]), 1));
+          if (lane == 0) {
+#pragma unroll
+            for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
+          }
+          float yy_above[2] = {yyA.x, yyA.y};
+          P2 u[2][NP];
+          // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
+          auto u_pairs = [&](int P) {  // both columns of pair P
+            const ulonglong2 zv = s_z[P * CTHREADS + tid];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const P2 ab2 = P == 0 ? pk(yy_above[k], plo(yy[k][NP - 1])) : yy[k][P > 0 ? P - 1 : 0];
+              const P2 l2 = k == 0 ? left[P] : yx[0][P];
+              const P2 d1 = padd(pfma(ab2, m1, yy[k][P]), yx[k][P]);
+              const P2 d2 = pfma(l2, m1, d1);
+              const P2 v = padd(k == 0 ? zv.x : zv.y, d2);
+              u[k][P] = nonneg ? pk(fmaxf(plo(v), 0.f), fmaxf(phi(v), 0.f)) : v;
+            }
+          };
+          if constexpr (BOT) {  // pairs 1.. need no row of another group
+#pragma unroll
+            for (int P = 1; P < NP; ++P) u_pairs(P);
+          }
+          if constexpr (!TOP) {
+            GWAIT(&gYY[rg - 1], ph);
+            const float2 ya2 = *reinterpret_cast<const float2*>(&s_rg_yy[rg - 1][j0]);
+            yy_above[0] = ya2.x;
+            yy_above[1] = ya2.y;
+          }
+          u_pairs(0);
+          if constexpr (!BOT) {
+#pragma unroll
+            for (int P = 1; P < NP; ++P) u_pairs(P);
+          }
+          float u_below[2] = {0.f, 0.f};
+          if constexpr (BOT) {
+            if (has_dn) {  // u of the CTA-below's first row, from its y row
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const float d = ((ex_y[k] - phi(yy[k][NP - 1])) + ex_x[k]) - (k == 0 ? ledge_x : ex_x[0]);
+                const float v = z_ex[k] + d;
+                u_below[k] = nonneg ? fmaxf(v, 0.f) : v;
+              }
+            } else {  // the global last row: gy = 0 (below := u)
+              u_below[0] = phi(u[0][NP - 1]);
+              u_below[1] = phi(u[1][NP - 1]);
+            }
+          }
+          if constexpr (!TOP) {  // first-row u for the group above
+            *reinterpret_cast<float2*>(&s_rg_u[rg][j0]) = make_float2(plo(u[0][0]), plo(u[1][0]));
+            mbar_arrive(&gU[rg]);
+          }
+          if (lane == 0) {
+#pragma unroll
+            for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[0][P];
+          }
+          mbar_arrive(&gE2[rg]);
+          GWAIT(&gE2[rg], ph);
+          // right neighbour of column 1: shuffles (lane 31 keeps its own column 1
+          // at the global last column: gx = 0), the warp to the right's first
+          // column from shared memory
+          P2 right[NP];
+#pragma unroll
+          for (int P = 0; P < NP; ++P)
+            right[P] = pk(__shfl_down_sync(0xffffffffu, plo(u[0][P]), 1),
+                          __shfl_down_sync(0xffffffffu, phi(u[0][P]), 1));
+          if (right_fetch) {
+#pragma unroll
+            for (int P = 0; P < NP; ++P) right[P] = s_edge_u[rg][P][wc + 1];
+          }
+          if (last_col) {
+#pragma unroll
+            for (int P = 0; P < NP; ++P) right[P] = u[1][P];
+          }
+          auto q_pair = [&](int k, int P) {
+            const P2 bl2 = P == NP - 1 ? pk(phi(u[k][0]), u_below[k]) : u[k][P < NP - 1 ? P + 1 : 0];
+            const P2 rt = k == 0 ? u[1][P] : right[P];
+            const P2 gy = pfma(u[k][P], m1, bl2);
+            const P2 gx = pfma(u[k][P], m1, rt);
+            const P2 ay = pfma(st2, gy, yy[k][P]);
+            const P2 ax = pfma(st2, gx, yx[k][P]);
+            const P2 m2 = pfma(ay, ay, pmul(ax, ax));
+            const P2 rs = pk(rsqrt_approx(plo(m2)), rsqrt_approx(phi(m2)));
+            const P2 s0 = pmul(w2, rs);
+            const P2 sc = pk(fminf(1.f, plo(s0)), fminf(1.f, phi(s0)));  // w / max(w, |a|)
+            QY[k][P] = pmul(ay, sc);
+            QX[k][P] = pmul(ax, sc);
+          };
+          // halo rows of the new iterate: y_{it+1} (or q_n after the last iteration)
+          const float b1 = (a.accelerated && it + 1 < a.n_inner) ? s_beta[it] : 0.f;
+          if constexpr (TOP) {  // pair 0 holds row 0: compute it, push, then the rest
+            q_pair(0, 0);
+            q_pair(1, 0);
+            if (has_up) {
+              float v[4] = {plo(QY[0][0]), plo(QX[0][0]), plo(QY[1][0]), plo(QX[1][0])};
+              if (it + 1 < a.n_inner) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = fmaf(b1, fmaf(old_e[i], -1.f, v[i]), v[i]);
+              }
+              push_up(v[0], v[1], v[2], v[3]);
+            }
+#pragma unroll
+            for (int P = 1; P < NP - 1; ++P) {
+              q_pair(0, P);
+              q_pair(1, P);
+            }
+            GWAIT(&gU[rg + 1], ph);
+            const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+            u_below[0] = ub.x;
+            u_below[1] = ub.y;
+            q_pair(0, NP - 1);
+            q_pair(1, NP - 1);
+          } else if constexpr (BOT) {  // pair NP-1 holds the last row: compute it, push, then the rest
+            q_pair(0, NP - 1);
+            q_pair(1, NP - 1);
+            if (has_dn) {
+              float v[2] = {phi(QY[0][NP - 1]), phi(QY[1][NP - 1])};
+              if (it + 1 < a.n_inner) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) v[i] = fmaf(b1, fmaf(old_e[i], -1.f, v[i]), v[i]);
+              }
+              push_dn(v[0], v[1]);
+            }
+#pragma unroll
+            for (int P = 0; P < NP - 1; ++P) {
+              q_pair(0, P);
+              q_pair(1, P);
+            }
+          } else {
+#pragma unroll
+            for (int P = 0; P < NP - 1; ++P) {
+              q_pair(0, P);
+              q_pair(1, P);
+            }
+            GWAIT(&gU[rg + 1], ph);
+            const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+            u_below[0] = ub.x;
+            u_below[1] = ub.y;
+            q_pair(0, NP - 1);
+            q_pair(1, NP - 1);
+          }
+          ++round;
+          ++gph;
+        };
+        inner(0, std::true_type{});
+        for (int it = 1; it < a.n_inner; ++it) inner(it, std::false_type{});
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int P = 0; P < NP; ++P) {
+            qky[k][P] = make_float2(plo(QY[k][P]), phi(QY[k][P]));
+            qkx[k][P] = make_float2(plo(QX[k][P]), phi(QX[k][P]));
+          }
+      };
+      if (rg_top)
+        run_inner(std::integral_constant<int, 0>{});
+      else if (rg_bot)
+        run_inner(std::integral_constant<int, 2>{});
+      else
+        run_inner(std::integral_constant<int, 1>{});
+
+      // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -----------
+      __syncthreads();  // every group is past its last inner iteration's reads
+      float yy_above[2] = {0.f, 0.f};
+      {
+        const unsigned r = round0 + a.n_inner;
+        const unsigned pe = r & 1, ph = (r >> 1) & 1;
+#ifndef PSB_DBG_NOHALO
+        if (rg_bot && has_dn) {
+          if (arm) mbar_expect_tx(&mb_dn[pe], BYTES_DN);
+          mbar_wait(&mb_dn[pe], ph);
+        }
+        if (rg_top && has_up) {
+          if (arm) mbar_expect_tx(&mb_up[pe], BYTES_UP);
+          mbar_wait(&mb_up[pe], ph);
+        }
+#endif
+        if (rg_top && has_up) {
+          yy_above[0] = rx_up[pe][j0];
+          yy_above[1] = rx_up[pe][j0 + 1];
+        }
+      }
+      s_rg_yy[rg][j0] = rowref(qky[0], CRPT - 1);
+      s_rg_yy[rg][j0 + 1] = rowref(qky[1], CRPT - 1);
+      if (lane == 31) {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = pk(qkx[1][P].x, qkx[1][P].y);
+      }
+      __syncthreads();
+      float2 qleft[NP];
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        qleft[P].x = __shfl_up_sync(0xffffffffu, qkx[1][P].x, 1);
+        qleft[P].y = __shfl_up_sync(0xffffffffu, qkx[1][P].y, 1);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) {
+          const P2 e2 = s_edge_yx[rg][P][wc];
+          qleft[P] = make_float2(plo(e2), phi(e2));
+        }
+      }
+      if (!rg_top) {
+        yy_above[0] = s_rg_yy[rg - 1][j0];
+        yy_above[1] = s_rg_yy[rg - 1][j0 + 1];
+      }
+      bool ok = true;
+      float2 zf[2][NP];
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        const ulonglong2 zv = s_z[P * CTHREADS + tid];
+        zf[0][P] = make_float2(plo(zv.x), phi(zv.x));
+        zf[1][P] = make_float2(plo(zv.y), phi(zv.y));
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+#pragma unroll
+        for (int t = 0; t < CRPT; ++t) {
+          const float left = k == 0 ? rowref(qleft, t) : rowref(qkx[0], t);
+          const int r = row0 + t, j = j0 + k;
+          float d = 0.f;
+          if (r < CH - 1) d += rowref(qky[k], t);
+          if (r > 0) d -= (t > 0 ? rowref(qky[k], t > 0 ? t - 1 : 0) : yy_above[k]);
+          if (j < CW - 1) d += rowref(qkx[k], t);
+          if (j > 0) d -= left;
+          float uf = rowref(zf[k], t) + d;
+          if (nonneg) uf = fmaxf(uf, 0.f);
+          const int sj = (rg * CRPT + t) * CW + j;
+          const float xo = sx[sj];  // x after the skips (prologue)
+          const float bo = sb[sj], ho = sh[sj];
+          const float xhat = skip_update(xo, bo, ho, g);
+          const float xn = uf;
+          sh[sj] = F::add(ho, F::mul(a.pg, F::sub(xn, xhat)));
+          sx[sj] = xn;
+          ok &= finite(xn);
+        }
+      }
+      if (!ok) kbad = min(kbad, kk);
+      kprev = kk;
+    }  // prox calls
+
+    // ---- trailing skips, write-back -------------------------------------------
+    const int m = a.K - 1 - kprev;
+#pragma unroll
+    for (int t = 0; t < CRPT; ++t) {
+      const int sj = (rg * CRPT + t) * CW + j0;
+      const int64_t o = (int64_t)(row0 + t) * CW + j0;
+      const float2 hv = *reinterpret_cast<const float2*>(&sh[sj]);
+      const float2 xv = *reinterpret_cast<const float2*>(&sx[sj]);
+      const float2 bv = *reinterpret_cast<const float2*>(&sb[sj]);
+      float2 xo;
+      xo.x = skip_chain_px(xv.x, bv.x, hv.x, g, m, kprev + 1, &kbad);
+      xo.y = skip_chain_px(xv.y, bv.y, hv.y, g, m, kprev + 1, &kbad);
+      *reinterpret_cast<float2*>(xp + o) = xo;
+      if (e1 > e0 || cold) *reinterpret_cast<float2*>(hp + o) = hv;
+      if (e1 > e0) {
+        *reinterpret_cast<float2*>(q0 + o) = make_float2(rowref(qky[0], t), rowref(qky[1], t));
+        *reinterpret_cast<float2*>(q0 + HW + o) = make_float2(rowref(qkx[0], t), rowref(qkx[1], t));
+      }
+    }
+    if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
+    chunk_done(a.cs, p, 16 / CCL, tid == 0);  // this CTA's rows of the problem are written
+    if (cr == 0 && tid == 0) wq_record(a.wq, 0, pos, t_claim);
+  }  // problems
+  cluster_arrive();  // no CTA leaves while a neighbour may still push into it
+  cluster_wait();
+}
+
+}  // namespace
+
+int cluster8_ctas() { return CCL; }
+
+// 8-CTA clusters of the run kernel resident on this device at once (cached)
+int cluster8_count() {
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    int mc = 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CCL * 64);
+    cfg.blockDim = dim3(CTHREADS);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CCL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.dynamicSmemBytes = kDynBytes;
+    auto kern = fgp_cluster8_run_kernel<false>;
+    if (func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynBytes) != PSB_OK ||
+        cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc <= 0) {
+      (void)cudaGetLastError();
+      mc = 1;
+    }
+    max_clusters = mc;
+  }
+  return max_clusters;
+}
+
+template <bool NN>
+static int launch_run8(const Run8Args& a, int G, cudaStream_t st) {
+  auto kern = fgp_cluster8_run_kernel<NN>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)G * CCL);
+  cfg.blockDim = dim3(CTHREADS);
+  cfg.dynamicSmemBytes = kDynBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CCL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynBytes));
+  PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  PSB_LAUNCHED("fgp_cluster8_run");
+  return PSB_OK;
+}
+
+// fp32 outer state only (the fp64 instantiation stays on the 16-CTA kernel)
+int cluster8_run(void* x, const void* b, void* h, void* q, int64_t qps, const WorkQueue& wq, int G,
+                 const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K, int n_inner,
+                 int accelerated, int nonneg, double weight, double gamma, double hc, double pg,
+                 double step, const float* betas, int32_t* bad, const ChunkSync& cs,
+                 cudaStream_t st) {
+  if (G <= 0) return PSB_OK;
+  Run8Args a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, wq, ev_off, ev_k, rep, K, n_inner,
+             accelerated, (float)weight, (float)gamma, (float)hc, (float)pg, (float)step, bad, betas, cs};
+  return nonneg ? launch_run8<true>(a, G, st) : launch_run8<false>(a, G, st);
+}
+
+}  // namespace psb

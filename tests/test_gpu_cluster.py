@@ -215,6 +215,44 @@ def test_sm_worker_and_cluster_kernels_bitwise_equal(monkeypatch):
     assert torch.equal(xq, xc)
 
 
+def test_cluster8_kernel_bitwise_equals_cluster16(monkeypatch):
+    """The 8-CTA cluster kernel (csrc/fgp_cluster8.cu: 16 px per thread, z and
+    q_{k-1} in shared memory; PSB_CLUSTER8=1) gives the 16-CTA kernel's bits:
+    warm restarts with re-projection, odd / even inner budgets, nonneg off,
+    the streamed (cold, host input) path, and a diverging problem's iteration."""
+    idx = np.arange(40) * 53 % 4096
+    b = _batch(idx).astype(np.float32)
+    for K, inner, p in ((25, 7, 0.3), (12, 50, 0.2), (9, 1, 0.5)):
+        outs = []
+        for c8 in ("0", "1"):
+            monkeypatch.setenv("PSB_CLUSTER8", c8)
+            monkeypatch.setenv("PSB_NO_SMWORK", "1")
+            s = psb.BatchedTvDenoise(torch.from_numpy(b).cuda(), 0.1, inner, precision="fp32")
+            from paper_2411_00688_b200 import batched
+            coins = batched.coin_table(p, idx, 2 * K)
+            s.run_proxskip(coins[:K], 1.0, p)
+            s.run_proxskip(coins[K:], 1.0, 0.5 * p + 0.1)  # weight changes: re-projection
+            outs.append((s.x.clone(), s.h.clone(), s.slots[:, 0].clone(), s.prox_count.copy()))
+            monkeypatch.delenv("PSB_NO_SMWORK")
+            xh, ch = psb.run_proxskip_batched(b, 0.1, p, idx, K, inner)  # streamed host run
+            outs[-1] += (torch.as_tensor(xh).clone(), np.asarray(ch).copy())
+        a16, a8 = outs
+        for u, v in zip(a16, a8):
+            if isinstance(u, torch.Tensor):
+                assert torch.equal(u, v)
+            else:
+                np.testing.assert_array_equal(u, v)
+    bad = b[:3].copy()
+    bad[1, 100, 100] = np.inf
+    ks = []
+    for c8 in ("0", "1"):
+        monkeypatch.setenv("PSB_CLUSTER8", c8)
+        with pytest.raises(psb.DivergenceError) as ei:
+            psb.run_proxskip_batched(torch.from_numpy(bad).cuda(), 0.1, 0.3, idx[:3], 20, 5)
+        ks.append(ei.value.iteration)
+    assert ks[0] == ks[1]
+
+
 @pytest.mark.parametrize("host", ["numpy", "numpy64", "pinned", "pageable"])
 def test_streamed_host_run_equals_resident_run(host):
     """Host input streams in chunks (kernels wait on per-chunk ready flags,
