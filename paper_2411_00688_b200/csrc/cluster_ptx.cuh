@@ -15,6 +15,41 @@ __device__ __forceinline__ TO skip_update(TO xo, TO bo, TO ho, TO g) {
   return A::add(A::sub(xo, A::mul(g, A::sub(xo, bo))), A::mul(g, ho));  // skip.py:68
 }
 
+// Packed fp32 pairs as 64-bit registers (fma/add/mul.rn.f32x2 operate on .b64):
+// lo / hi = the two rows of a row pair of a column strip.  No mul is ever followed by
+// an add of its result here (ptxas would contract that pair into an FFMA2).
+using P2 = unsigned long long;
+__device__ __forceinline__ P2 pk(float lo, float hi) {
+  P2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float plo(P2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float phi(P2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ P2 pfma(P2 a, P2 b, P2 c) {
+  P2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ P2 padd(P2 a, P2 b) {
+  P2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ P2 pmul(P2 a, P2 b) {
+  P2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 // 32-bit shared::cluster address of `p` in CTA `rank` of this cluster, and a load from it
 __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
   uint32_t local = (uint32_t)__cvta_generic_to_shared(p), remote;

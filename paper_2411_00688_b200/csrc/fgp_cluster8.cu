@@ -70,41 +70,6 @@ struct Run8Args {
   ChunkSync cs;
 };
 
-// Packed fp32 pairs as 64-bit registers (fma/add/mul.rn.f32x2 operate on .b64):
-// lo = row t, hi = row t + NP of a column strip.  No mul is ever followed by
-// an add of its result here (ptxas would contract that pair into an FFMA2).
-using P2 = unsigned long long;
-__device__ __forceinline__ P2 pk(float lo, float hi) {
-  P2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float plo(P2 v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-  return lo;
-}
-__device__ __forceinline__ float phi(P2 v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-  return hi;
-}
-__device__ __forceinline__ P2 pfma(P2 a, P2 b, P2 c) {
-  P2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ P2 padd(P2 a, P2 b) {
-  P2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ P2 pmul(P2 a, P2 b) {
-  P2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
 // row t of a column strip held as pairs (t, t + NP)
 __device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
   return t < NP ? v[t].x : v[t - NP].y;
