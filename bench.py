@@ -44,7 +44,10 @@ SIDE = 256
 ALPHA = 0.1
 P = 0.1
 INNER = 50
-E2E_REPS = 5
+RESIDENT_REPS = 3   # timed resident segments (median)
+E2E_REPS = 5        # at least; short calls repeat up to E2E_MAX_REPS within E2E_BUDGET_S
+E2E_MAX_REPS = 15   # (host stalls under the nvidia-smi sampler come in bursts of several calls)
+E2E_BUDGET_S = 1.5
 RUN_LEN = 300
 HW = SIDE * SIDE
 U_TOL, OBJ_TOL = 1e-4, 1e-5          # BASELINE.json north_star parity tolerance
@@ -326,8 +329,9 @@ def _roofline4(units, t, n_pxit, sm_mhz, sms):
     model_gbs = n_pxit * BYTES_FGP_MOM / t / 1e9
     out = {"bound": "issue", "unit": "Gwarp-inst/s", "achieved": None, "peak": sms * 4 * f_ghz,
            "frac": None, "traffic": None,
-           "kernel": "fgp_cluster_run_kernel<float> + fgp_sm_run_kernel (one launch each for the "
-                     "K timed steps, problems claimed from one device work queue)",
+           "kernel": "fgp_cluster_run_kernel<float> + fgp_cluster8_run_kernel + fgp_sm_run_kernel "
+                     "(one launch each for the K timed steps, problems claimed from one device "
+                     "work queue)",
            "fp32": {"achieved_tflops": fp32, "peak_tflops": fp32_peak, "frac": fp32 / fp32_peak,
                     "flops_per_unit": f"{FLOPS_PER_PXIT} per pixel-iteration (FMA = 2)"},
            "hbm_model": {"achieved_gbs": model_gbs, "peak_gbs": hbm_peak,
@@ -339,14 +343,17 @@ def _roofline4(units, t, n_pxit, sm_mhz, sms):
            "peak_source": f"4 warp-inst/cycle/SM x {sms} SMs x {f_ghz * 1000:.0f} MHz "
                           "(median SM clock under load)"}
     if cnt is not None:
-        inst = units[0] * cnt["cluster"]["inst_per_unit"] + units[1] * cnt["sm_worker"]["inst_per_unit"]
+        c8 = cnt.get("cluster8", cnt["cluster"])
+        inst = units[0] * cnt["cluster"]["inst_per_unit"] + units[1] * cnt["sm_worker"]["inst_per_unit"] + \
+            units[2] * c8["inst_per_unit"]
         dram = units[0] * cnt["cluster"]["dram_bytes_per_unit"] + \
-            units[1] * cnt["sm_worker"]["dram_bytes_per_unit"]
+            units[1] * cnt["sm_worker"]["dram_bytes_per_unit"] + units[2] * c8["dram_bytes_per_unit"]
         out["achieved"] = inst / t / 1e9
         out["frac"] = out["achieved"] / out["peak"]
         out["traffic"] = dram
         out["counters"] = {"source": os.path.relpath(COUNTERS, ROOT),
                            "cluster_units": units[0], "sm_worker_units": units[1],
+                           "cluster8_units": units[2],
                            "issue_active_pct_ncu": cnt.get("issue_active_pct")}
     return out
 
@@ -376,28 +383,38 @@ def run_config4(args, D, dev):
     solver = psb.BatchedTvDenoise(b_host, ALPHA, INNER, precision="fp32")
 
     # ---- device-resident throughput: warm-up steps, then K timed steps ----
-    solver.reset()
-    solver.run_proxskip(coins[:args.warmup], 1.0, P)
-    fgp_t = np.zeros(args.steps)
-    D.barrier()
+    # The segment (cold reset, W warm-up steps, K timed steps) is run
+    # RESIDENT_REPS times and the median taken: one 36 ms segment (K = 20) is
+    # hit by 1-20 ms box-side stalls about one time in ten (with or without
+    # the clock sampler); every sample is in the line (t_samples_s).
     stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    solver.run_proxskip(coins[args.warmup:], 1.0, P, fgp_time=fgp_t)
-    e1.record(stream)
-    D.barrier()
-    solver.check_finite()
-    t_local = e0.elapsed_time(e1) / 1000.0
-    qs = (L.C.c_double * 4)()
-    L.call("psb_queue_stats", qs)
-    units = (float(qs[1]), float(qs[3]))
+    runs = []
+    for _ in range(RESIDENT_REPS):
+        solver.reset()
+        solver.run_proxskip(coins[:args.warmup], 1.0, P)
+        fgp_t = np.zeros(args.steps)
+        D.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        solver.run_proxskip(coins[args.warmup:], 1.0, P, fgp_time=fgp_t)
+        e1.record(stream)
+        D.barrier()
+        solver.check_finite()
+        qs = (L.C.c_double * 6)()
+        L.call("psb_queue_stats", qs)
+        # 16-CTA clusters, SM workers, 8-CTA clusters
+        runs.append((e0.elapsed_time(e1) / 1000.0, (float(qs[1]), float(qs[3]), float(qs[5]))))
+    t_samples = [r[0] for r in runs]
+    t_local, units = sorted(runs, key=lambda r: r[0])[len(runs) // 2]
     timed = coins[args.warmup:]
     active = timed.sum(axis=1)                       # coin-fired problems per step
     n_pxit = float(active.sum()) * INNER * HW
     if CLUSTER:
-        # one fgp_cluster_run_kernel launch for the K timed steps, plus one
-        # fgp_sm_run_kernel launch on the SMs the clusters leave
-        launches = 1 + (os.environ.get("PSB_NO_SMWORK", "0") != "1")
+        # one fgp_cluster_run_kernel launch for the K timed steps, one
+        # fgp_cluster8_run_kernel launch (the 8-CTA clusters in the GPC space the
+        # 16-CTA clusters cannot use) and one fgp_sm_run_kernel launch on the
+        # SMs both leave
+        launches = 1 + int(units[1] > 0) + int(units[2] > 0)
     else:
         launches = args.steps + int(np.count_nonzero(active)) * (INNER + 1)
     t_job, = D.reduce([t_local], "max")
@@ -409,7 +426,12 @@ def run_config4(args, D, dev):
     # ---- e2e: the public API with host buffers, copies inside the region ----
     del solver
     e2e_samples = []
-    for _ in range(E2E_REPS):
+    n_reps = E2E_REPS
+    if D.world == 1:  # (ranks must agree on the call count: fixed under torchrun)
+        n_reps = E2E_MAX_REPS
+    for rep in range(n_reps):
+        if rep >= E2E_REPS and sum(e2e_samples) > E2E_BUDGET_S:
+            break
         D.barrier()
         t0 = time.perf_counter()
         x_e2e, counts = psb.run_proxskip_batched(b_pin, ALPHA, P, idx, args.warmup + args.steps,
@@ -428,13 +450,15 @@ def run_config4(args, D, dev):
     same = bool(np.array_equal(x_e2e, x_resident))
 
     rec = {
-        "value": value, "t_job": t_job, "inner_rate": inner_rate, "roofline": roof,
+        "value": value, "t_job": t_job, "t_samples_s": [round(t, 6) for t in t_samples],
+        "inner_rate": inner_rate, "roofline": roof,
         "launches": launches, "clocks": clocks,
         "e2e": {"value": n_e2e / t_e2e, "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "paper_2411_00688_b200.run_proxskip_batched (pinned host in, pinned "
                         "host out; W+K outer iterations from a cold start per call)",
-                "timing": f"host wall clock per call, median of {E2E_REPS} calls (max over ranks)",
+                "timing": f"host wall clock per call, median of {len(e2e_samples)} calls (max over "
+                          "ranks)",
                 "samples_s": [round(t, 5) for t in e2e_samples]},
         "idx": idx, "x_e2e": x_e2e, "counts": counts, "resident_equals_e2e": same,
     }
@@ -566,6 +590,9 @@ def run_gpu(args):
         "metric": METRIC, "value": rec["value"], "unit": UNIT,
         "n_gpus": D.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * rec["t_job"] / args.steps, "higher_is_better": True,
+        "timing": f"CUDA events around the K timed steps (after a cold reset and W warm-up steps), "
+                  f"median of {RESIDENT_REPS} such segments, max over ranks",
+        "t_samples_s": rec["t_samples_s"],
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded random-shape phantoms, SURVEY D3; no public dataset)",
         "config": {"workload": WORKLOAD, "problems": N_PROBLEMS, "side": SIDE, "inner": INNER,

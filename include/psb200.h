@@ -415,11 +415,11 @@ int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, 
 int psb_cluster_max_active(int* out);
 
 /* psb_queue_stats: work-queue statistics of the last cluster-path run
- * (psb_proxskip_denoise_run[_streamed]) -- out4 = {cluster ns, cluster cost
- * units, SM-worker ns, SM-worker cost units}, summed over finished problems
- * (cost unit = one FGP inner iteration of one 256x256 problem; +2 per
- * problem).  Valid once the run's stream has been synchronised. */
-int psb_queue_stats(double* out4);
+ * (psb_proxskip_denoise_run[_streamed]) -- out6 = {ns, cost units} of the
+ * 16-CTA clusters, of the SM workers and of the 8-CTA clusters, summed over
+ * finished problems (cost unit = one FGP inner iteration of one 256x256
+ * problem; +2 per problem).  Valid once the run's stream has been synchronised. */
+int psb_queue_stats(double* out6);
 
 /* psb_proxskip_deblur_run: the same native driver for the implicit TV
  *   deblurring problem (BASELINE config 2): A = periodic blur, one problem,

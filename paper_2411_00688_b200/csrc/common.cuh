@@ -264,7 +264,7 @@ __device__ __forceinline__ void chunk_done(const ChunkSync& cs, int p, int add, 
 // runs a problem never changes a result (the two kernels are bit-identical).
 struct WorkQueue {
   unsigned int* head = nullptr;         // next position of `order` to claim (zero at run start)
-  unsigned long long* stats = nullptr;  // [4]: cluster ns, cluster cost, worker ns, worker cost
+  unsigned long long* stats = nullptr;  // [6]: ns, cost of the 16-CTA clusters, the SM workers, the 8-CTA clusters
   const int32_t* order = nullptr;       // [n] problem indices in claim order
   const float* cost = nullptr;          // [n] cost units of order[i]
   const float* suffix = nullptr;        // [n + 1] sum of cost[i .. n)
@@ -291,10 +291,14 @@ __device__ __forceinline__ int wq_claim_worker(const WorkQueue& q) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(i) : "l"(q.head) : "memory");
     if (i >= (unsigned)q.n) return -1;
     if (q.clusters > 0) {
-      unsigned long long s[4];
+      unsigned long long s[6];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 6; ++k)
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(s[k]) : "l"(q.stats + k) : "memory");
+      if (s[1] == 0) {  // no 16-CTA cluster has finished a problem: 8-CTA rate, two per `clusters`
+        s[0] = s[4] / 2;
+        s[1] = s[5];
+      }
       if (s[1] > 0 && s[3] > 0) {
         const double t_worker = (double)s[2] / (double)s[3] * (double)q.cost[i];
         const double t_rest = (double)s[0] / (double)s[1] * (double)q.suffix[i + 1] / q.clusters;
@@ -305,7 +309,7 @@ __device__ __forceinline__ int wq_claim_worker(const WorkQueue& q) {
   }
 }
 
-// a finished problem's time and cost (role 0: cluster, 1: SM worker)
+// a finished problem's time and cost (role 0: 16-CTA cluster, 1: SM worker, 2: 8-CTA cluster)
 __device__ __forceinline__ void wq_record(const WorkQueue& q, int role, int pos, uint64_t t0) {
   atomicAdd(q.stats + 2 * role, (unsigned long long)(gtimer_ns() - t0));
   atomicAdd(q.stats + 2 * role + 1, (unsigned long long)q.cost[pos]);

@@ -37,7 +37,7 @@ int cluster8_count();
 int cluster8_run(void* x, const void* b, void* h, void* q, int64_t qps, const WorkQueue& wq, int G,
                  const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K, int n_inner,
                  int accelerated, int nonneg, double weight, double gamma, double hc, double pg,
-                 double step, const float* betas, int32_t* bad, const ChunkSync& cs,
+                 double step, const float* betas, int32_t* bad, const ChunkSync& cs, bool dependent,
                  cudaStream_t st);
 int sm_prepare();
 int sm_run(void* x, const void* b, void* h, void* q, int64_t qps, void* z, const WorkQueue& wq,
@@ -102,10 +102,10 @@ static unsigned long long* queue_stats_host() {
   static unsigned long long* p = nullptr;
   if (p == nullptr) {
     void* h = nullptr;
-    if (cudaHostAlloc(&h, 4 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
+    if (cudaHostAlloc(&h, 6 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
       return nullptr;
     p = static_cast<unsigned long long*>(h);
-    for (int i = 0; i < 4; ++i) p[i] = 0;
+    for (int i = 0; i < 6; ++i) p[i] = 0;
   }
   return p;
 }
@@ -198,13 +198,17 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   std::vector<uint8_t> rep_p;
   std::vector<float> beta_f;
   int G = 0, NW = 0;
-  // PSB_CLUSTER8=1 (fp32 outer state): the 8-CTA cluster kernel
-  // (fgp_cluster8.cu: 16 px per thread, q_{k-1} and z in shared memory) --
-  // bit-identical, measured equal per SM to the 16-CTA kernel (shared-memory
-  // bound instead of synchronisation bound); kept for comparisons and for
-  // devices whose GPCs cannot host seven 16-CTA clusters
+  // The 8-CTA cluster kernel (fgp_cluster8.cu: 16 px per thread, q_{k-1} and z
+  // in shared memory; fp32 outer state) is bit-identical to the 16-CTA kernel
+  // and measured equal per SM.  By default it fills the GPC space the 16-CTA
+  // clusters cannot use: G8 extra 8-CTA clusters (8-CTA capacity minus two per
+  // 16-CTA cluster; 1 on a 148-SM B200) run beside them and take those SMs from
+  // the slower one-SM workers.  PSB_CLUSTER8=1: 8-CTA clusters only;
+  // PSB_CLUSTER8=0: none.
   const char* c8 = std::getenv("PSB_CLUSTER8");
   const bool use8 = dto == PSB_F32 && c8 && c8[0] == '1';
+  const bool no8 = c8 && c8[0] == '0';
+  int G8 = 0;
   const int ccl = use8 ? 8 : 16;
   if (use_cluster) {
     ev_off.assign(n + 1, 0);
@@ -233,8 +237,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       const int cap = nws ? std::max(1, std::atoi(nws)) : sm_count();
       NW = (int)std::min<int64_t>(n, std::min(cap, sm_count()));
     }
-    else if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1'))
-      NW = std::max(0, sm_count() - G * ccl);
+    else if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1')) {
+      if (!use8 && !no8) G8 = (int)std::min<int64_t>(n - G, std::max(0, cluster8_count() - 2 * G));
+      NW = std::max(0, sm_count() - G * ccl - G8 * 8);
+    }
     auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
     order.resize(n);
     for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
@@ -271,9 +277,9 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     o_evk = put(ev_k.data(), ev_k.size() * sizeof(int32_t));
     o_repp = put(rep_p.data(), rep_p.size());
     o_beta = put(beta_f.data(), beta_f.size() * sizeof(float));
-    const uint64_t zeros[5] = {0, 0, 0, 0, 0};  // queue head + rate statistics start at 0
+    const uint64_t zeros[7] = {0, 0, 0, 0, 0, 0, 0};  // queue head + rate statistics start at 0
     o_head = put(zeros, sizeof(uint32_t));
-    o_stats = put(zeros, 4 * sizeof(uint64_t));
+    o_stats = put(zeros, 6 * sizeof(uint64_t));
     o_order = put(order.data(), order.size() * sizeof(int32_t));
     o_cost = put(qcost.data(), qcost.size() * sizeof(float));
     o_suffix = put(qsuffix.data(), qsuffix.size() * sizeof(float));
@@ -333,7 +339,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     wq.cost = reinterpret_cast<const float*>(dev + o_cost);
     wq.suffix = reinterpret_cast<const float*>(dev + o_suffix);
     wq.n = (int)n;
-    wq.clusters = G;
+    // (an 8-CTA cluster runs at half a 16-CTA cluster's rate)
+    wq.clusters = use8 ? (G + 1) / 2 : G + (G8 + 1) / 2;
     if (NW > 0) rc = sm_prepare();  // module loaded before the clusters launch
     // (never in a streamed run: the synchronisation below would wait for
     // kernels that wait for copies the caller has not enqueued yet)
@@ -347,7 +354,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     if (rc == PSB_OK)
       rc = use8 ? cluster8_run(x, b, h, q, qps, wq, G, i32(o_evo), i32(o_evk), dev + o_repp, K,
                                n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125,
-                               beta_d, bad, cs, st)
+                               beta_d, bad, cs, false, st)
                 : cluster_run(dto, x, b, h, q, qps, wq, G, i32(o_evo), i32(o_evk), dev + o_repp, K,
                               n_inner, accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d,
                               bad, cs, st);
@@ -357,6 +364,12 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     // take GPC space a 16-CTA cluster needs, and they finish only after the
     // clusters (griddepcontrol.wait at their end) -- no host gate, no second
     // stream.
+    // mixed run: the extra 8-CTA clusters follow as a programmatic dependent
+    // (placed after every 16-CTA cluster, before the SM workers)
+    if (G8 > 0 && rc == PSB_OK)
+      rc = cluster8_run(x, b, h, q, qps, wq, G8, i32(o_evo), i32(o_evk), dev + o_repp, K, n_inner,
+                        accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d, bad, cs,
+                        G > 0, st);
     if (NW > 0 && rc == PSB_OK)
       rc = sm_run(x, b, h, q, qps, z, wq, NW, i32(o_evo), i32(o_evk), dev + o_repp, K, n_inner,
                   accelerated, nonneg, weight, gamma, hcoef, pg, 0.125, beta_d, bad, cs, G > 0, st);
@@ -364,7 +377,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     // valid once the stream has drained)
     if (rc == PSB_OK && !use_graph) {
       unsigned long long* hs = queue_stats_host();
-      if (hs && cudaMemcpyAsync(hs, wq.stats, 4 * sizeof(unsigned long long),
+      if (hs && cudaMemcpyAsync(hs, wq.stats, 6 * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, st) != cudaSuccess)
         rc = fail(PSB_ERR_CUDA, "queue statistics copy failed");
     }
@@ -373,13 +386,15 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       cudaDeviceSynchronize();
       float a = 0;
       cudaEventElapsedTime(&a, d0, d1);
-      uint64_t stt[4] = {0, 0, 0, 0};
+      uint64_t stt[6] = {0, 0, 0, 0, 0, 0};
       cudaMemcpy(stt, wq.stats, sizeof(stt), cudaMemcpyDeviceToHost);
       fprintf(stderr,
-              "[psb] %d clusters + %d sm workers: %.3f ms; cluster %.1f ns/unit over %llu units, "
-              "worker %.1f ns/unit over %llu units\n",
-              G, NW, a, stt[1] ? (double)stt[0] / stt[1] : 0.0, (unsigned long long)stt[1],
-              stt[3] ? (double)stt[2] / stt[3] : 0.0, (unsigned long long)stt[3]);
+              "[psb] %d 16-CTA clusters + %d 8-CTA clusters + %d sm workers: %.3f ms; cluster16 "
+              "%.1f ns/unit over %llu units, cluster8 %.1f over %llu, worker %.1f over %llu\n",
+              use8 ? 0 : G, use8 ? G : G8, NW, a, stt[1] ? (double)stt[0] / stt[1] : 0.0,
+              (unsigned long long)stt[1], stt[5] ? (double)stt[4] / stt[5] : 0.0,
+              (unsigned long long)stt[5], stt[3] ? (double)stt[2] / stt[3] : 0.0,
+              (unsigned long long)stt[3]);
       cudaEventDestroy(d0);
       cudaEventDestroy(d1);
     }
@@ -464,10 +479,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
 
 }  // namespace psb
 
-extern "C" int psb_queue_stats(double* out4) {
-  PSB_REQUIRE(out4 != nullptr, "queue_stats: output missing");
+extern "C" int psb_queue_stats(double* out6) {
+  PSB_REQUIRE(out6 != nullptr, "queue_stats: output missing");
   const unsigned long long* hs = psb::queue_stats_host();
-  for (int i = 0; i < 4; ++i) out4[i] = hs ? (double)hs[i] : 0.0;
+  for (int i = 0; i < 6; ++i) out6[i] = hs ? (double)hs[i] : 0.0;
   return PSB_OK;
 }
 

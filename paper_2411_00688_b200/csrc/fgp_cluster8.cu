@@ -662,10 +662,13 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
     }
     if (kbad != 0x7fffffff && a.bad) atomicMin(a.bad + p, kbad);
     chunk_done(a.cs, p, 16 / CCL, tid == 0);  // this CTA's rows of the problem are written
-    if (cr == 0 && tid == 0) wq_record(a.wq, 0, pos, t_claim);
+    if (cr == 0 && tid == 0) wq_record(a.wq, 2, pos, t_claim);
   }  // problems
   cluster_arrive();  // no CTA leaves while a neighbour may still push into it
   cluster_wait();
+  // launched as a programmatic dependent of the 16-CTA cluster kernel (mixed
+  // run): this grid completes only after that one (a no-op otherwise)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 }  // namespace
@@ -700,20 +703,23 @@ int cluster8_count() {
 }
 
 template <bool NN>
-static int launch_run8(const Run8Args& a, int G, cudaStream_t st) {
+static int launch_run8(const Run8Args& a, int G, bool dependent, cudaStream_t st) {
   auto kern = fgp_cluster8_run_kernel<NN>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)G * CCL);
   cfg.blockDim = dim3(CTHREADS);
   cfg.dynamicSmemBytes = kDynBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CCL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // placed once every CTA of the preceding (16-CTA cluster) kernel is resident
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = dependent ? 2 : 1;
   PSB_CHECK(func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynBytes));
   PSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   PSB_LAUNCHED("fgp_cluster8_run");
@@ -724,12 +730,12 @@ static int launch_run8(const Run8Args& a, int G, cudaStream_t st) {
 int cluster8_run(void* x, const void* b, void* h, void* q, int64_t qps, const WorkQueue& wq, int G,
                  const int32_t* ev_off, const int32_t* ev_k, const uint8_t* rep, int K, int n_inner,
                  int accelerated, int nonneg, double weight, double gamma, double hc, double pg,
-                 double step, const float* betas, int32_t* bad, const ChunkSync& cs,
+                 double step, const float* betas, int32_t* bad, const ChunkSync& cs, bool dependent,
                  cudaStream_t st) {
   if (G <= 0) return PSB_OK;
   Run8Args a{(float*)x, (const float*)b, (float*)h, (float*)q, qps, wq, ev_off, ev_k, rep, K, n_inner,
              accelerated, (float)weight, (float)gamma, (float)hc, (float)pg, (float)step, bad, betas, cs};
-  return nonneg ? launch_run8<true>(a, G, st) : launch_run8<false>(a, G, st);
+  return nonneg ? launch_run8<true>(a, G, dependent, st) : launch_run8<false>(a, G, dependent, st);
 }
 
 }  // namespace psb

@@ -131,6 +131,6 @@ def test_run_kernels_deterministic_over_repeats():
         else:
             assert torch.equal(x, ref[0])
             np.testing.assert_array_equal(c, ref[1])
-    qs = (L.C.c_double * 4)()
+    qs = (L.C.c_double * 6)()
     L.call("psb_queue_stats", qs)
     assert qs[1] + qs[3] > 0  # both roles reported their work

@@ -10,11 +10,12 @@ live run (psb_queue_stats) and divides by the live CUDA-event time.
 
 Workload: the bench's config-4 timed segment on a subset of the problems
 (W = 5 warm-up outer iterations, then K = 20), once with the clusters only
-(PSB_NO_SMWORK=1) and once with the SM workers only (PSB_SM_ONLY=1).
+(PSB_NO_SMWORK=1), once with the SM workers only (PSB_SM_ONLY=1) and once
+with 8-CTA clusters only (PSB_CLUSTER8=1 PSB_NO_SMWORK=1).
 
 On the GPU box:
 
-  for m in cluster sm; do
+  for m in cluster sm cluster8; do
     ncu --metrics smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,\
 gpu__time_duration.sum,sm__inst_issued.avg.pct_of_peak_sustained_active,\
 sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active \
@@ -39,7 +40,10 @@ N, W, K = 1184, 5, 20  # 1184 = 8 x 148 problems
 
 
 def run(mode):
-    os.environ["PSB_NO_SMWORK" if mode == "cluster" else "PSB_SM_ONLY"] = "1"
+    os.environ["PSB_SM_ONLY" if mode == "sm" else "PSB_NO_SMWORK"] = "1"
+    os.environ["PSB_CLUSTER8"] = "1" if mode == "cluster8" else "0"
+    if mode == "sm":  # the workers' share of the SMs in the bench's run (L2-resident working sets)
+        os.environ.setdefault("PSB_SM_WORKERS", "28")
     import torch
     import paper_2411_00688_b200 as psb
     from paper_2411_00688_b200 import _lib as L
@@ -51,9 +55,9 @@ def run(mode):
     s.run_proxskip(coins[:W], 1.0, 0.1)          # launch 1 (warm-up)
     s.run_proxskip(coins[W:], 1.0, 0.1)          # launch 2 (the measured one)
     torch.cuda.synchronize()
-    qs = (L.C.c_double * 4)()
+    qs = (L.C.c_double * 6)()
     L.call("psb_queue_stats", qs)
-    units = qs[1] if mode == "cluster" else qs[3]
+    units = {"cluster": qs[1], "sm": qs[3], "cluster8": qs[5]}[mode]
     print(json.dumps({"mode": mode, "problems": N, "warmup": W, "steps": K, "units": units,
                       "prox_calls": int(coins[W:].sum())}))
 
@@ -69,7 +73,10 @@ def emit(d):
     out = {"source": "ncu --metrics (tools/run_kernel_counters.py), second launch of each kernel",
            "unit": "one FGP inner iteration of one 256x256 problem (+2 per problem)"}
     for mode, key, kname in (("cluster", "cluster", "fgp_cluster_run_kernel"),
-                             ("sm", "sm_worker", "fgp_sm_run_kernel")):
+                             ("sm", "sm_worker", "fgp_sm_run_kernel"),
+                             ("cluster8", "cluster8", "fgp_cluster8_run_kernel")):
+        if not os.path.exists(os.path.join(d, f"ctr_{mode}.json")):
+            continue
         meta = json.loads(open(os.path.join(d, f"ctr_{mode}.json")).read().strip().splitlines()[-1])
         rows = [r for r in _ncu_rows(os.path.join(d, f"ctr_{mode}.csv"))
                 if kname in r["Kernel Name"]]
@@ -93,7 +100,7 @@ def emit(d):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", choices=["cluster", "sm"])
+    ap.add_argument("--mode", choices=["cluster", "sm", "cluster8"])
     ap.add_argument("--emit")
     a = ap.parse_args()
     if a.emit:

@@ -24,10 +24,10 @@ for inner in [int(a) for a in sys.argv[1:]] or [50]:
     s.run_proxskip(coins[5:], 1.0, 0.1)
     e1.record()
     torch.cuda.synchronize()
-    qs = (L.C.c_double * 4)()
+    qs = (L.C.c_double * 6)()
     L.call("psb_queue_stats", qs)
     calls = int(coins[5:].sum())
     print(f"inner {inner}: {e0.elapsed_time(e1):.2f} ms, {calls} prox calls, cluster "
-          f"{qs[0] / max(qs[1], 1):.1f} ns/unit, worker {qs[2] / max(qs[3], 1):.1f} ns/unit, "
+          f"{qs[0] / max(qs[1], 1):.1f} ns/unit, cluster8 {qs[4] / max(qs[5], 1):.1f}, worker {qs[2] / max(qs[3], 1):.1f} ns/unit, "
           f"{1e6 * e0.elapsed_time(e1) / (calls * inner):.1f} ns per problem-iteration overall",
           flush=True)
