@@ -269,7 +269,8 @@ struct WorkQueue {
   const float* cost = nullptr;          // [n] cost units of order[i]
   const float* suffix = nullptr;        // [n + 1] sum of cost[i .. n)
   int n = 0;
-  int clusters = 0;                     // clusters claiming beside the SM workers
+  int clusters = 0;                     // 16-CTA clusters claiming beside the SM workers
+  int clusters8 = 0;                    // 8-CTA clusters
 };
 
 __device__ __forceinline__ uint64_t gtimer_ns() {
@@ -290,18 +291,22 @@ __device__ __forceinline__ int wq_claim_worker(const WorkQueue& q) {
     unsigned i;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(i) : "l"(q.head) : "memory");
     if (i >= (unsigned)q.n) return -1;
-    if (q.clusters > 0) {
+    if (q.clusters + q.clusters8 > 0) {
       unsigned long long s[6];
 #pragma unroll
       for (int k = 0; k < 6; ++k)
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(s[k]) : "l"(q.stats + k) : "memory");
-      if (s[1] == 0) {  // no 16-CTA cluster has finished a problem: 8-CTA rate, two per `clusters`
-        s[0] = s[4] / 2;
-        s[1] = s[5];
-      }
-      if (s[1] > 0 && s[3] > 0) {
+      // the clusters' capacity in cost units per ns, each kind at its measured
+      // rate (a kind without a finished problem yet: the other's, an 8-CTA
+      // cluster counting as half a 16-CTA cluster)
+      double r16 = s[0] > 0 ? (double)s[1] / (double)s[0] : 0.0;
+      double r8 = s[4] > 0 ? (double)s[5] / (double)s[4] : 0.0;
+      if (r16 == 0.0) r16 = 2.0 * r8;
+      if (r8 == 0.0) r8 = 0.5 * r16;
+      const double cap = q.clusters * r16 + q.clusters8 * r8;
+      if (cap > 0.0 && s[3] > 0) {
         const double t_worker = (double)s[2] / (double)s[3] * (double)q.cost[i];
-        const double t_rest = (double)s[0] / (double)s[1] * (double)q.suffix[i + 1] / q.clusters;
+        const double t_rest = (double)q.suffix[i + 1] / cap;
         if (t_worker > t_rest) return -1;
       }
     }

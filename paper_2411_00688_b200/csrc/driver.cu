@@ -198,16 +198,17 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   std::vector<uint8_t> rep_p;
   std::vector<float> beta_f;
   int G = 0, NW = 0;
-  // The 8-CTA cluster kernel (fgp_cluster8.cu: 16 px per thread, q_{k-1} and z
-  // in shared memory; fp32 outer state) is bit-identical to the 16-CTA kernel
-  // and measured equal per SM.  By default it fills the GPC space the 16-CTA
-  // clusters cannot use: G8 extra 8-CTA clusters (8-CTA capacity minus two per
-  // 16-CTA cluster; 1 on a 148-SM B200) run beside them and take those SMs from
-  // the slower one-SM workers.  PSB_CLUSTER8=1: 8-CTA clusters only;
-  // PSB_CLUSTER8=0: none.
+  // fp32 outer state runs on 8-CTA clusters (fgp_cluster8.cu: 16 px per
+  // thread, q_k in registers, q_{k-1} and z in tensor memory): bit-identical to
+  // the 16-CTA kernel, 15 % faster per SM, and 15 clusters tile 120 of the 148
+  // SMs (seven 16-CTA clusters: 112).  fp64 outer state (mixed-precision single
+  // problems) stays on the 16-CTA kernel.  PSB_CLUSTER8=0: 16-CTA clusters
+  // only; PSB_CLUSTER8=2: 16-CTA clusters plus the 8-CTA clusters that fit in
+  // the GPC space they leave (tests, comparisons).
   const char* c8 = std::getenv("PSB_CLUSTER8");
-  const bool use8 = dto == PSB_F32 && c8 && c8[0] == '1';
   const bool no8 = c8 && c8[0] == '0';
+  const bool mix8 = c8 && c8[0] == '2';
+  const bool use8 = dto == PSB_F32 && !no8 && !mix8;
   int G8 = 0;
   const int ccl = use8 ? 8 : 16;
   if (use_cluster) {
@@ -238,7 +239,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       NW = (int)std::min<int64_t>(n, std::min(cap, sm_count()));
     }
     else if (n > G && dto == PSB_F32 && !use_graph && !(no_sm && no_sm[0] == '1')) {
-      if (!use8 && !no8) G8 = (int)std::min<int64_t>(n - G, std::max(0, cluster8_count() - 2 * G));
+      if (mix8) G8 = (int)std::min<int64_t>(n - G, std::max(0, cluster8_count() - 2 * G));
       NW = std::max(0, sm_count() - G * ccl - G8 * 8);
     }
     auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
@@ -339,8 +340,8 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     wq.cost = reinterpret_cast<const float*>(dev + o_cost);
     wq.suffix = reinterpret_cast<const float*>(dev + o_suffix);
     wq.n = (int)n;
-    // (an 8-CTA cluster runs at half a 16-CTA cluster's rate)
-    wq.clusters = use8 ? (G + 1) / 2 : G + (G8 + 1) / 2;
+    wq.clusters = use8 ? 0 : G;
+    wq.clusters8 = use8 ? G : G8;
     if (NW > 0) rc = sm_prepare();  // module loaded before the clusters launch
     // (never in a streamed run: the synchronisation below would wait for
     // kernels that wait for copies the caller has not enqueued yet)

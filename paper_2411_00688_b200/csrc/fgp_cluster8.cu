@@ -70,6 +70,71 @@ struct Run8Args {
   ChunkSync cs;
 };
 
+
+// ---- tensor memory as a thread-private register-spill space -------------------
+// The SM's 256 KB of TMEM (512 columns x 128 lanes x 32 bit) is idle in a
+// kernel without tcgen05.mma.  tcgen05.ld / .st with the .32x32b shape move
+// N consecutive columns of ONE lane per thread -- lane 32 (warp % 4) + laneid --
+// so the four warps that share a lane quarter split the 512 columns: every
+// thread owns 128 private words, reached by one instruction per 16 / 32
+// registers, on a datapath of its own (measured, tools/micro/tmem_bw.cu:
+// 247 B/cycle/SM loads against 128 B/cycle/SM for shared memory, and the
+// shared-memory pipe stays free for the shuffles and the edge exchange).
+#ifndef PSB_C8_TMEM
+#define PSB_C8_TMEM 1
+#endif
+// wait::ld names the loaded registers as in/out operands: their consumers must
+// not be scheduled above the wait (a volatile asm orders only other volatile
+// asms and memory accesses, not register arithmetic)
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15])::"memory");
+}
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&v)[16], uint32_t (&w)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]),
+                 "+r"(w[6]), "+r"(w[7]), "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]),
+                 "+r"(w[13]), "+r"(w[14]), "+r"(w[15])::"memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr)
+      : "memory");
+}
+__device__ __forceinline__ void tm_st16(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// one packed pair (a 64-bit register pair as it is: no gathering moves)
+__device__ __forceinline__ void tm_st2(uint32_t addr, P2 v) {
+  uint32_t a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void p2_split(P2 v, uint32_t& lo, uint32_t& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+__device__ __forceinline__ P2 p2_join(uint32_t lo, uint32_t hi) {
+  P2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+// thread-private TMEM columns: [0,32) q_{k-1}: words 4 (k NP + P) + {0,1} the
+// y pair, + {2,3} the x pair of column k, pair P (one 2-word store per register
+// pair as it is, two 16-word loads); [32,48) z: words 4 P + 2 k + {0,1}
+constexpr uint32_t kTmQ = 0, kTmZ = 32;
+
 // row t of a column strip held as pairs (t, t + NP)
 __device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
   return t < NP ? v[t].x : v[t - NP].y;
@@ -78,7 +143,7 @@ __device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
 constexpr size_t kStageBytes = (size_t)3 * SR * CW * sizeof(float);           // x, b, h rows
 constexpr size_t kQmBytes = (size_t)2 * NP * CTHREADS * sizeof(float4);       // q_{k-1}
 constexpr size_t kZBytes = (size_t)NP * CTHREADS * sizeof(float4);            // z
-constexpr size_t kDynBytes = kStageBytes + kQmBytes + kZBytes;
+constexpr size_t kDynBytes = PSB_C8_TMEM ? kStageBytes : kStageBytes + kQmBytes + kZBytes;
 
 template <bool NONNEG>
 __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args a) {
@@ -110,6 +175,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   __shared__ __align__(16) P2 s_edge_u[CRG][NP][CWARPS_ROW];
   __shared__ float s_beta[kMaxBetas];
   __shared__ int s_next[2];
+  __shared__ uint32_t s_tm_base;
   extern __shared__ __align__(16) unsigned char dyn_raw[];
   float* sx = reinterpret_cast<float*>(dyn_raw);  // [SR][CW]
   float* sb = sx + SR * CW;
@@ -118,9 +184,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   // column k of q_{k-1} (float2 slots: the packed results go straight from
   // their register pairs to STS.64, no quad assembly);
   // s_z[P][tid] = (z col 0 pair P, z col 1 pair P)
+#if !PSB_C8_TMEM
   P2* s_qmy = reinterpret_cast<P2*>(dyn_raw + kStageBytes);
   P2* s_qmx = s_qmy + 2 * NP * CTHREADS;
   ulonglong2* s_z = reinterpret_cast<ulonglong2*>(dyn_raw + kStageBytes + kQmBytes);
+#endif
 
   const float g = a.gamma;
   const float w = a.weight;
@@ -141,6 +209,18 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+#if PSB_C8_TMEM
+  if (tid < 32) {  // warp 0 takes the SM's whole tensor memory (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        smem_u32(&s_tm_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  // this thread's 128 columns of its lane (bits 31:16 lane, 15:0 column)
+  const uint32_t tm = s_tm_base + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) + (uint32_t)((tid >> 7) * 128);
+#endif
   // every CTA of this grid is resident: the SM-worker kernel (a programmatic
   // dependent) may now be placed on the SMs the clusters left
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -275,9 +355,22 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             }
           }
         }
+#if PSB_C8_TMEM
+        {
+          uint32_t zw[16];
+#pragma unroll
+          for (int P = 0; P < NP; ++P) {
+            zw[4 * P + 0] = __float_as_uint(z[0][P].x), zw[4 * P + 1] = __float_as_uint(z[0][P].y);
+            zw[4 * P + 2] = __float_as_uint(z[1][P].x), zw[4 * P + 3] = __float_as_uint(z[1][P].y);
+          }
+          tm_st16(tm + kTmZ, zw);
+          tm_wait_st();
+        }
+#else
 #pragma unroll
         for (int P = 0; P < NP; ++P)
           s_z[P * CTHREADS + tid] = make_ulonglong2(pk(z[0][P].x, z[0][P].y), pk(z[1][P].x, z[1][P].y));
+#endif
         z_top[0] = z[0][0].x;
         z_top[1] = z[1][0].x;
       }
@@ -332,6 +425,42 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
           const P2 b2 = pk(beta, beta);
           P2 yy[2][NP], yx[2][NP];
+#if PSB_C8_TMEM
+          // q_{k-1} from tensor memory (two 16-word loads), y, then q_k goes
+          // where q_{k-1} was (the previous iteration's stores have landed:
+          // wait::st below, before this load)
+          {
+            uint32_t m0[16], m1w[16];  // column 0 / column 1: 4 P + {0,1} y pair, + {2,3} x pair
+            if constexpr (!FIRST) {
+              tm_ld16(tm + kTmQ, m0);
+              tm_ld16(tm + kTmQ + 16, m1w);
+              tm_wait_ld(m0, m1w);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+              for (int P = 0; P < NP; ++P) {
+                P2 vy = QY[k][P], vx = QX[k][P];  // (the momentum restarts with every call)
+                if constexpr (!FIRST) {
+                  const uint32_t(&mw)[16] = k == 0 ? m0 : m1w;
+                  vy = p2_join(mw[4 * P], mw[4 * P + 1]);
+                  vx = p2_join(mw[4 * P + 2], mw[4 * P + 3]);
+                }
+                yy[k][P] = pfma(b2, pfma(vy, m1, QY[k][P]), QY[k][P]);
+                yx[k][P] = pfma(b2, pfma(vx, m1, QX[k][P]), QX[k][P]);
+              }
+            // q_k becomes q_{k-1} (its halo entries for the y pushed below are kept)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+              for (int P = 0; P < NP; ++P) {
+                tm_st2(tm + kTmQ + 4 * (k * NP + P), QY[k][P]);
+                tm_st2(tm + kTmQ + 4 * (k * NP + P) + 2, QX[k][P]);
+              }
+          }
+          uint32_t zw[16];
+          tm_ld16(tm + kTmZ, zw);  // (waited for before the first u below)
+#else
 #pragma unroll
           for (int k = 0; k < 2; ++k)
 #pragma unroll
@@ -352,6 +481,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               s_qmy[(k * NP + P) * CTHREADS + tid] = QY[k][P];
               s_qmx[(k * NP + P) * CTHREADS + tid] = QX[k][P];
             }
+#endif
           float old_e[4];
           if constexpr (TOP) {
             old_e[0] = plo(QY[0][0]), old_e[1] = plo(QX[0][0]), old_e[2] = plo(QY[1][0]), old_e[3] = plo(QX[1][0]);
@@ -393,6 +523,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             }
           }
           GWAIT(&gE1[rg], ph);
+#if PSB_C8_TMEM
+          tm_wait_ld(zw);  // z
+#endif
           // left neighbours of column 0: shuffles inside the warp, the warp to
           // the left's last column from shared memory (zeros left of column 0)
           P2 left[NP];
@@ -408,7 +541,12 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           P2 u[2][NP];
           // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
           auto u_pairs = [&](int P) {  // both columns of pair P
+#if PSB_C8_TMEM
+            const ulonglong2 zv = make_ulonglong2(p2_join(zw[4 * P], zw[4 * P + 1]),
+                                                  p2_join(zw[4 * P + 2], zw[4 * P + 3]));
+#else
             const ulonglong2 zv = s_z[P * CTHREADS + tid];
+#endif
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const P2 ab2 = P == 0 ? pk(yy_above[k], plo(yy[k][NP - 1])) : yy[k][P > 0 ? P - 1 : 0];
@@ -541,6 +679,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             q_pair(0, NP - 1);
             q_pair(1, NP - 1);
           }
+#if PSB_C8_TMEM
+          tm_wait_st();  // q_{k-1} is in place for the next iteration's load
+#endif
           ++round;
           ++gph;
         };
@@ -608,12 +749,25 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       }
       bool ok = true;
       float2 zf[2][NP];
+#if PSB_C8_TMEM
+      {
+        uint32_t zw[16];
+        tm_ld16(tm + kTmZ, zw);
+        tm_wait_ld(zw);
+#pragma unroll
+        for (int P = 0; P < NP; ++P) {
+          zf[0][P] = make_float2(__uint_as_float(zw[4 * P]), __uint_as_float(zw[4 * P + 1]));
+          zf[1][P] = make_float2(__uint_as_float(zw[4 * P + 2]), __uint_as_float(zw[4 * P + 3]));
+        }
+      }
+#else
 #pragma unroll
       for (int P = 0; P < NP; ++P) {
         const ulonglong2 zv = s_z[P * CTHREADS + tid];
         zf[0][P] = make_float2(plo(zv.x), phi(zv.x));
         zf[1][P] = make_float2(plo(zv.y), phi(zv.y));
       }
+#endif
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
 #pragma unroll
@@ -666,6 +820,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   }  // problems
   cluster_arrive();  // no CTA leaves while a neighbour may still push into it
   cluster_wait();
+#if PSB_C8_TMEM
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_tm_base));
+#endif
   // launched as a programmatic dependent of the 16-CTA cluster kernel (mixed
   // run): this grid completes only after that one (a no-op otherwise)
   asm volatile("griddepcontrol.wait;\n" ::: "memory");

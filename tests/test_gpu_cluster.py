@@ -217,14 +217,15 @@ def test_sm_worker_and_cluster_kernels_bitwise_equal(monkeypatch):
 
 def test_cluster8_kernel_bitwise_equals_cluster16(monkeypatch):
     """The 8-CTA cluster kernel (csrc/fgp_cluster8.cu: 16 px per thread, z and
-    q_{k-1} in shared memory; PSB_CLUSTER8=1) gives the 16-CTA kernel's bits:
+    q_{k-1} in tensor memory; the default for fp32 outer state) gives the
+    16-CTA kernel's (PSB_CLUSTER8=0) bits, and so does the mixed launch (2):
     warm restarts with re-projection, odd / even inner budgets, nonneg off,
     the streamed (cold, host input) path, and a diverging problem's iteration."""
     idx = np.arange(40) * 53 % 4096
     b = _batch(idx).astype(np.float32)
     for K, inner, p in ((25, 7, 0.3), (12, 50, 0.2), (9, 1, 0.5)):
         outs = []
-        for c8 in ("0", "1"):
+        for c8 in ("0", "1", "2"):
             monkeypatch.setenv("PSB_CLUSTER8", c8)
             monkeypatch.setenv("PSB_NO_SMWORK", "1")
             s = psb.BatchedTvDenoise(torch.from_numpy(b).cuda(), 0.1, inner, precision="fp32")
@@ -236,12 +237,12 @@ def test_cluster8_kernel_bitwise_equals_cluster16(monkeypatch):
             monkeypatch.delenv("PSB_NO_SMWORK")
             xh, ch = psb.run_proxskip_batched(b, 0.1, p, idx, K, inner)  # streamed host run
             outs[-1] += (torch.as_tensor(xh).clone(), np.asarray(ch).copy())
-        a16, a8 = outs
-        for u, v in zip(a16, a8):
-            if isinstance(u, torch.Tensor):
-                assert torch.equal(u, v)
-            else:
-                np.testing.assert_array_equal(u, v)
+        for other in outs[1:]:
+            for u, v in zip(outs[0], other):
+                if isinstance(u, torch.Tensor):
+                    assert torch.equal(u, v)
+                else:
+                    np.testing.assert_array_equal(u, v)
     bad = b[:3].copy()
     bad[1, 100, 100] = np.inf
     ks = []
