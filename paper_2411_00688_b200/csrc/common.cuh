@@ -174,6 +174,13 @@ __device__ __forceinline__ bool same_bits(double a, double b) {
   return __double_as_longlong(a) == __double_as_longlong(b);
 }
 
+// one skipped ProxSkip iteration of the identity fidelity (skip.py:68)
+template <class T>
+__device__ __forceinline__ T skip_step(T x, T b, T h, T g) {
+  using A = Ar<T>;
+  return A::add(A::sub(x, A::mul(g, A::sub(x, b))), A::mul(g, h));
+}
+
 // m skipped ProxSkip iterations of the identity fidelity,
 // x <- (x - g (x - b)) + g h (skip.py:68), with the reference's roundings.
 // The update is a fixed map of x (b, h, g do not change across a run of

@@ -39,20 +39,6 @@ namespace cg = cooperative_groups;
 
 namespace psb {
 
-#ifdef PSB_DBG_PHASES  // timing experiment: per-phase ns of one thread per role
-__device__ unsigned long long g_phase_ns[16];
-#define PHASE_MARK(v) uint64_t v = gtimer_ns()
-#define PHASE_ADD(slot, t0, t1)                                                 \
-  do {                                                                         \
-    if (blockIdx.x == 0 && (tid == 0 || tid == 128 || tid == 384))             \
-      atomicAdd(&g_phase_ns[(slot) * 4 + (tid == 0 ? 0 : tid == 128 ? 1 : 2)], \
-                (unsigned long long)((t1) - (t0)));                            \
-  } while (0)
-#else
-#define PHASE_MARK(v)
-#define PHASE_ADD(slot, t0, t1)
-#endif
-
 namespace {
 
 constexpr int CW = 256;    // image width

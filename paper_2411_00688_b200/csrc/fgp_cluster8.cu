@@ -173,6 +173,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   // warp w (slot 0 stays zero), s_edge_u[rg][P][w] = first column of warp w
   __shared__ __align__(16) P2 s_edge_yx[CRG][NP][CWARPS_ROW + 1];
   __shared__ __align__(16) P2 s_edge_u[CRG][NP][CWARPS_ROW];
+  // the finalize's own exchange rows (q_n's last row per group, q_n's warp-edge
+  // columns): separate from the inner loop's, so no barrier is needed between
+  // the last inner iteration and these writes
+  __shared__ __align__(8) float s_fin_yy[CRG][CW];
+  __shared__ __align__(16) P2 s_fin_edge[CRG][NP][CWARPS_ROW + 1];
   __shared__ float s_beta[kMaxBetas];
   __shared__ int s_next[2];
   __shared__ uint32_t s_tm_base;
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   const float w = a.weight;
   constexpr bool nonneg = NONNEG;
   for (int e = tid; e < a.n_inner && e < kMaxBetas; e += CTHREADS) s_beta[e] = a.betas[e];
-  if (tid < CRG * NP) s_edge_yx[tid / NP][tid % NP][0] = pk(0.f, 0.f);
+  if (tid < CRG * NP) s_edge_yx[tid / NP][tid % NP][0] = s_fin_edge[tid / NP][tid % NP][0] = pk(0.f, 0.f);
   if (tid == 0) {
     mbar_init(&mb_dn[0], 1);
     mbar_init(&mb_dn[1], 1);
@@ -325,21 +330,67 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       const int kk = a.ev_k[e];
       const int m = kk - kprev - 1;  // skip iterations kprev+1 .. kk-1 before this prox call
       const int kf = kprev + 1;
-      __syncthreads();
+      // (no barrier here: x, b, h and the spill columns are thread-private, the
+      // inner loop's exchange buffers were last read before the previous
+      // call's finalize barrier, and rx_z is rewritten only after this CTA's
+      // final-round push of that call)
+      PHASE_MARK(ph_a);
       // ---- prologue: skips, prox input, warm start ----------------------------
-      float z_top[2] = {0.f, 0.f};  // row 0 of this thread's z (top group: pushed up)
       {
+        // this thread's 2 columns x CRPT rows of x, b, h
+        float2 xv[CRPT], bv[CRPT], hv[CRPT];
+#pragma unroll
+        for (int t = 0; t < CRPT; ++t) {
+          const int sj = (rg * CRPT + t) * CW + j0;
+          xv[t] = *reinterpret_cast<const float2*>(&sx[sj]);
+          bv[t] = *reinterpret_cast<const float2*>(&sb[sj]);
+          hv[t] = *reinterpret_cast<const float2*>(&sh[sj]);
+        }
+        if (m > 0) {
+          // the m skipped iterations (skip.py:68) of all 16 pixels side by side;
+          // the update is a fixed map of x, so once no pixel changes any more
+          // the remaining steps change nothing either (skip_chain_px, common.cuh)
+          for (int sk = 0; sk < m; ++sk) {
+            bool changed = false;
+#pragma unroll
+            for (int t = 0; t < CRPT; ++t) {
+              const float nx = skip_step(xv[t].x, bv[t].x, hv[t].x, g);
+              const float ny = skip_step(xv[t].y, bv[t].y, hv[t].y, g);
+              changed |= !same_bits(nx, xv[t].x) | !same_bits(ny, xv[t].y);
+              xv[t] = make_float2(nx, ny);
+            }
+            if (!changed) break;
+          }
+          bool fin = true;
+#pragma unroll
+          for (int t = 0; t < CRPT; ++t) fin &= finite(xv[t].x) & finite(xv[t].y);
+          if (!fin) {  // slow path: the first non-finite step, from the x still in shared memory
+#pragma unroll
+            for (int t = 0; t < CRPT; ++t) {
+              const int sj = (rg * CRPT + t) * CW + j0;
+              (void)skip_chain_px(sx[sj], bv[t].x, hv[t].x, g, m, kf, &kbad);
+              (void)skip_chain_px(sx[sj + 1], bv[t].y, hv[t].y, g, m, kf, &kbad);
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < CRPT; ++t)
+            *reinterpret_cast<float2*>(&sx[(rg * CRPT + t) * CW + j0]) = xv[t];
+        }
         float2 z[2][NP];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int t = 0; t < CRPT; ++t) {
+          rowref(z[0], t) = F::add(F::sub(xv[t].x, F::mul(g, F::sub(xv[t].x, bv[t].x))), F::mul(a.hc, hv[t].x));
+          rowref(z[1], t) = F::add(F::sub(xv[t].y, F::mul(g, F::sub(xv[t].y, bv[t].y))), F::mul(a.hc, hv[t].y));
+        }
+        // my first row of z goes to the CTA above (its bottom group computes u
+        // of that row itself); the row from the CTA below is awaited in the
+        // first inner iteration, where it is first used
+        if (rg_top && has_up) st_async_v2(z_rx_remote + 4u * j0, z[0][0].x, z[1][0].x, z_mb_remote);
+        if (e == e0) {  // warm start (staged above), re-projected if the weight changed
 #pragma unroll
-          for (int t = 0; t < CRPT; ++t) {
-            const int sj = (rg * CRPT + t) * CW + j0 + k;
-            const float bo = sb[sj], ho = sh[sj];
-            const float xo = skip_chain_px(sx[sj], bo, ho, g, m, kf, &kbad);
-            if (m > 0) sx[sj] = xo;
-            rowref(z[k], t) = F::add(F::sub(xo, F::mul(g, F::sub(xo, bo))), F::mul(a.hc, ho));
-            if (e == e0) {  // warm start (staged above), re-projected if the weight changed
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int t = 0; t < CRPT; ++t) {
               float vy = rowref(qky[k], t), vx = rowref(qkx[k], t);
               if (rep) {
                 const float sc = F::ball_scale(vy, vx, w);
@@ -353,7 +404,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               rowref(qky[k], t) = vy;
               rowref(qkx[k], t) = vx;
             }
-          }
         }
 #if PSB_C8_TMEM
         {
@@ -371,19 +421,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
         for (int P = 0; P < NP; ++P)
           s_z[P * CTHREADS + tid] = make_ulonglong2(pk(z[0][P].x, z[0][P].y), pk(z[1][P].x, z[1][P].y));
 #endif
-        z_top[0] = z[0][0].x;
-        z_top[1] = z[1][0].x;
       }
-      // the bottom row group also owns the CTA-below's first row for u: its z
-      // arrives from that CTA (st.async on mb_z); mine goes to the CTA above
-      if (rg_top && has_up) st_async_v2(z_rx_remote + 4u * j0, z_top[0], z_top[1], z_mb_remote);
-      float z_ex[2] = {0.f, 0.f};
-      if (rg_bot && has_dn) {
-        if (arm) mbar_expect_tx(&mb_z, CW * 4);
-        mbar_wait(&mb_z, zph & 1u);
-        z_ex[0] = rx_z[j0];
-        z_ex[1] = rx_z[j0 + 1];
-      }
+      float z_ex[2] = {0.f, 0.f};  // the CTA-below's first row of z (bottom group, first iteration)
+      const unsigned zpar = zph & 1u;
       ++zph;
       // After the first call of a problem the warm start's boundary rows are
       // the previous call's final round (no exchange); halo rows travel as
@@ -573,6 +613,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             for (int P = 1; P < NP; ++P) u_pairs(P);
           }
           float u_below[2] = {0.f, 0.f};
+          if constexpr (BOT && FIRST) {
+            if (has_dn) {  // the z row pushed by the CTA below in its prologue
+              if (arm) mbar_expect_tx(&mb_z, CW * 4);
+              mbar_wait(&mb_z, zpar);
+              const float2 zr = *reinterpret_cast<const float2*>(&rx_z[j0]);
+              z_ex[0] = zr.x;
+              z_ex[1] = zr.y;
+            }
+          }
           if constexpr (BOT) {
             if (has_dn) {  // u of the CTA-below's first row, from its y row
 #pragma unroll
@@ -695,6 +744,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             qkx[k][P] = make_float2(plo(QX[k][P]), phi(QX[k][P]));
           }
       };
+      PHASE_MARK(ph_b);
       if (rg_top)
         run_inner(std::integral_constant<int, 0>{});
       else if (rg_bot)
@@ -702,8 +752,21 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       else
         run_inner(std::integral_constant<int, 1>{});
 
+      PHASE_MARK(ph_c);
       // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -----------
-      __syncthreads();  // every group is past its last inner iteration's reads
+      // q_n's row / column halos inside the CTA go through the finalize's own
+      // buffers (no barrier before these writes), z comes back from tensor
+      // memory while the barrier is pending
+      *reinterpret_cast<float2*>(&s_fin_yy[rg][j0]) =
+          make_float2(rowref(qky[0], CRPT - 1), rowref(qky[1], CRPT - 1));
+      if (lane == 31) {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) s_fin_edge[rg][P][wc + 1] = pk(qkx[1][P].x, qkx[1][P].y);
+      }
+#if PSB_C8_TMEM
+      uint32_t zw[16];
+      tm_ld16(tm + kTmZ, zw);
+#endif
       float yy_above[2] = {0.f, 0.f};
       {
         const unsigned r = round0 + a.n_inner;
@@ -723,12 +786,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           yy_above[1] = rx_up[pe][j0 + 1];
         }
       }
-      s_rg_yy[rg][j0] = rowref(qky[0], CRPT - 1);
-      s_rg_yy[rg][j0 + 1] = rowref(qky[1], CRPT - 1);
-      if (lane == 31) {
-#pragma unroll
-        for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = pk(qkx[1][P].x, qkx[1][P].y);
-      }
       __syncthreads();
       float2 qleft[NP];
 #pragma unroll
@@ -739,26 +796,23 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       if (lane == 0) {
 #pragma unroll
         for (int P = 0; P < NP; ++P) {
-          const P2 e2 = s_edge_yx[rg][P][wc];
+          const P2 e2 = s_fin_edge[rg][P][wc];
           qleft[P] = make_float2(plo(e2), phi(e2));
         }
       }
       if (!rg_top) {
-        yy_above[0] = s_rg_yy[rg - 1][j0];
-        yy_above[1] = s_rg_yy[rg - 1][j0 + 1];
+        const float2 ya = *reinterpret_cast<const float2*>(&s_fin_yy[rg - 1][j0]);
+        yy_above[0] = ya.x;
+        yy_above[1] = ya.y;
       }
       bool ok = true;
       float2 zf[2][NP];
 #if PSB_C8_TMEM
-      {
-        uint32_t zw[16];
-        tm_ld16(tm + kTmZ, zw);
-        tm_wait_ld(zw);
+      tm_wait_ld(zw);
 #pragma unroll
-        for (int P = 0; P < NP; ++P) {
-          zf[0][P] = make_float2(__uint_as_float(zw[4 * P]), __uint_as_float(zw[4 * P + 1]));
-          zf[1][P] = make_float2(__uint_as_float(zw[4 * P + 2]), __uint_as_float(zw[4 * P + 3]));
-        }
+      for (int P = 0; P < NP; ++P) {
+        zf[0][P] = make_float2(__uint_as_float(zw[4 * P]), __uint_as_float(zw[4 * P + 1]));
+        zf[1][P] = make_float2(__uint_as_float(zw[4 * P + 2]), __uint_as_float(zw[4 * P + 3]));
       }
 #else
 #pragma unroll
@@ -769,9 +823,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       }
 #endif
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int t = 0; t < CRPT; ++t) {
+        const int sj = (rg * CRPT + t) * CW + j0;
+        const float2 xo = *reinterpret_cast<const float2*>(&sx[sj]);  // x after the skips (prologue)
+        const float2 bo = *reinterpret_cast<const float2*>(&sb[sj]);
+        const float2 ho = *reinterpret_cast<const float2*>(&sh[sj]);
+        float xn[2], hn[2];
 #pragma unroll
-        for (int t = 0; t < CRPT; ++t) {
+        for (int k = 0; k < 2; ++k) {
           const float left = k == 0 ? rowref(qleft, t) : rowref(qkx[0], t);
           const int r = row0 + t, j = j0 + k;
           float d = 0.f;
@@ -781,18 +840,21 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           if (j > 0) d -= left;
           float uf = rowref(zf[k], t) + d;
           if (nonneg) uf = fmaxf(uf, 0.f);
-          const int sj = (rg * CRPT + t) * CW + j;
-          const float xo = sx[sj];  // x after the skips (prologue)
-          const float bo = sb[sj], ho = sh[sj];
-          const float xhat = skip_update(xo, bo, ho, g);
-          const float xn = uf;
-          sh[sj] = F::add(ho, F::mul(a.pg, F::sub(xn, xhat)));
-          sx[sj] = xn;
-          ok &= finite(xn);
+          const float xok = k == 0 ? xo.x : xo.y, bok = k == 0 ? bo.x : bo.y, hok = k == 0 ? ho.x : ho.y;
+          const float xhat = skip_update(xok, bok, hok, g);
+          xn[k] = uf;
+          hn[k] = F::add(hok, F::mul(a.pg, F::sub(uf, xhat)));
+          ok &= finite(uf);
         }
+        *reinterpret_cast<float2*>(&sh[sj]) = make_float2(hn[0], hn[1]);
+        *reinterpret_cast<float2*>(&sx[sj]) = make_float2(xn[0], xn[1]);
       }
       if (!ok) kbad = min(kbad, kk);
       kprev = kk;
+      PHASE_MARK(ph_d);
+      PHASE_ADD(0, ph_a, ph_b);
+      PHASE_ADD(1, ph_b, ph_c);
+      PHASE_ADD(2, ph_c, ph_d);
     }  // prox calls
 
     // ---- trailing skips, write-back -------------------------------------------
@@ -896,3 +958,12 @@ int cluster8_run(void* x, const void* b, void* h, void* q, int64_t qps, const Wo
 }
 
 }  // namespace psb
+
+#ifdef PSB_DBG_PHASES
+extern "C" int psb_debug_phases8(double* out16) {
+  unsigned long long h[16];
+  cudaMemcpyFromSymbol(h, psb::g_phase_ns, sizeof(h));
+  for (int i = 0; i < 16; ++i) out16[i] = (double)h[i];
+  return 0;
+}
+#endif

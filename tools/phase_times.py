@@ -10,8 +10,9 @@ for inner in (10, 50, 200):
     coins = batched.coin_table(0.1, idx, 25)
     lib = L.LIB
     z = (C.c_double * 16)()
-    lib.psb_debug_phases(z); base = np.array(z[:])
+    dbg = lib.psb_debug_phases if os.environ.get('PSB_CLUSTER8') == '0' else lib.psb_debug_phases8
+    dbg(z); base = np.array(z[:])
     s.run_proxskip(coins, 1.0, 0.1); torch.cuda.synchronize()
-    lib.psb_debug_phases(z); v = (np.array(z[:]) - base)
+    dbg(z); v = (np.array(z[:]) - base)
     # cluster 0 did some number of calls; print ns per call-phase ratios
     print(inner, "prologue", v[0:3], "inner", v[4:7], "epilogue", v[8:11])
