@@ -9,7 +9,8 @@ library raises.
 """
 
 from . import _lib  # noqa: F401  (fails loudly when libpsb200.so is missing)
-from .batched import BatchedTvDenoise, coin_table, run_proxskip_batched, shard_indices
+from .batched import (BatchedTvDenoise, coin_table, run_proxskip_batched, shard_balanced,
+                      shard_indices)
 from .devlog import CSV_HEADER, DeviceObjective, device_objective, emit_csv
 from .errors import DivergenceError, ReferenceRejectedError
 from .operators import (BlurKernel, LinearMap, RadonGeometry, blur_adjoint, blur_forward, blur_map,

@@ -42,6 +42,21 @@ def shard_indices(n_total, rank, world):
     return np.arange(lo, min(n_total, lo + per))
 
 
+def shard_balanced(costs, rank, world):
+    """Problem indices owned by ``rank`` when the per-problem work is known up
+    front (config 4: the prox calls of each problem's coin stream): problems
+    sorted by cost, longest first, and dealt to the ranks in snake order, so
+    every rank gets the same count (+-1) and nearly the same total work.  Every
+    rank computes the same partition on its own -- still no exchange.  Returns
+    ascending indices."""
+    costs = np.asarray(costs).reshape(-1)
+    order = np.argsort(-costs, kind="stable")
+    pos = np.arange(order.size)
+    lap, slot = pos // world, pos % world
+    owner = np.where(lap % 2 == 0, slot, world - 1 - slot)
+    return np.sort(order[owner == rank])
+
+
 def coin_table(p, seeds, iters):
     """(iters, N) uint8: column i is SkipConfig(p, seeds[i]).coins(iters), i.e.
     Generator(Philox(seed)).random() < p per draw (skip.py:27-28) -- generated

@@ -66,6 +66,22 @@ def test_skip_config_validation():
         SkipConfig(1.5, 0)
 
 
+def test_shard_balanced_partition_and_balance():
+    from paper_2411_00688_b200 import shard_balanced
+    rng = np.random.default_rng(0)
+    costs = rng.binomial(300, 0.1, size=4096)
+    for world in (1, 2, 3, 8):
+        parts = [shard_balanced(costs, r, world) for r in range(world)]
+        allp = np.sort(np.concatenate(parts))
+        np.testing.assert_array_equal(allp, np.arange(4096))  # every problem exactly once
+        sizes = [len(q) for q in parts]
+        assert max(sizes) - min(sizes) <= 1
+        work = [int(costs[q].sum()) for q in parts]
+        assert max(work) - min(work) <= costs.max()  # within one problem of each other
+        for q in parts:
+            assert np.all(np.diff(q) > 0)
+
+
 def test_shard_indices_partition():
     from paper_2411_00688_b200 import shard_indices
     for world in (1, 2, 3, 8):

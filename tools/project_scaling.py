@@ -1,5 +1,5 @@
 """Config-4 strong scaling projected from one GPU: the per-rank workload at
-N ranks is shard_indices(4096, r, N) with no collective on the data path, so
+N ranks is shard_balanced(prox-call counts, r, N) with no collective on the data path, so
 each rank's device time can be measured alone.  Prints T_1 / (N * T_N) for
 the slowest shard (all shards of N are timed)."""
 import json
@@ -21,9 +21,10 @@ b_all = bench.make_inputs(np.arange(4096))
 for n in (1, 2, 4, 8):
     worst = 0.0
     per = []
+    all_coins = batched.coin_table(0.1, np.arange(4096), W + K)
     for r in range(n):
-        idx = batched.shard_indices(4096, r, n)
-        coins = batched.coin_table(0.1, idx, W + K)
+        idx = batched.shard_balanced(all_coins.sum(axis=0), r, n) if n > 1 else np.arange(4096)
+        coins = all_coins[:, idx]
         s = psb.BatchedTvDenoise(b_all[idx], 0.1, 50, precision="fp32")
         best = None
         for rep in range(2):  # best of two cold runs (host-side one-offs excluded)
