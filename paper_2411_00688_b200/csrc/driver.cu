@@ -208,7 +208,10 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   const char* c8 = std::getenv("PSB_CLUSTER8");
   const bool no8 = c8 && c8[0] == '0';
   const bool mix8 = c8 && c8[0] == '2';
-  const bool use8 = dto == PSB_F32 && !no8 && !mix8;
+  // (a batch smaller than the 16-CTA capacity runs on 16-CTA clusters: 16 SMs
+  // per problem finish a problem 1.7x sooner than 8, and nothing waits)
+  const bool use8 = dto == PSB_F32 && !no8 && !mix8 &&
+                    (n > cluster_count() || (c8 && c8[0] == '1'));
   int G8 = 0;
   const int ccl = use8 ? 8 : 16;
   if (use_cluster) {
