@@ -3,12 +3,13 @@
 Config 4 -- 4096 independent 256x256 problems (seeded random-ellipse/rectangle
 phantoms, noise sigma_i ~ U[0.05, 0.15], alpha = 0.1, gamma = 1, p = 0.1
 per-problem Philox coin streams, FGP-50 inner iterations), sharded over N
-GPUs (one process per GPU, contiguous problem blocks, no collective on the
-data path).  A "step" is one outer ProxSkip iteration over the whole batch.
-The native driver runs the K timed steps as ONE segment: fgp_cluster_run_kernel
-(16-CTA clusters, one problem at a time, all of its coin-fired prox calls back
-to back with the FGP state in registers) plus fgp_sm_run_kernel on the SMs the
-clusters leave, both claiming problems from one device work queue; each problem
+GPUs (one process per GPU, problems dealt by their known work, no collective
+on the data path).  A "step" is one outer ProxSkip iteration over the whole
+batch.  The native driver runs the K timed steps as ONE segment:
+fgp_cluster8_run_kernel (fifteen 8-CTA clusters, one problem at a time, all of
+its coin-fired prox calls back to back with the FGP state in registers and
+tensor memory) plus fgp_sm_run_kernel on the 28 SMs the clusters leave, both
+claiming problems from one device work queue; each problem
 is advanced by exactly K outer iterations.  W warm-up steps are outer
 iterations 0..W-1 of the run; the K timed steps are iterations W..W+K-1
 (default W+K = 300, the full config-4 run).

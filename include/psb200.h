@@ -410,8 +410,9 @@ int psb_proxskip_post3d(int dtype_outer, int dtype_fgp, void* x, const void* b, 
                         int pend, int32_t* bad_iter, int k, void* stream);
 
 /* psb_cluster_max_active: how many 16-CTA clusters of the cluster-resident
- * 256x256 ProxSkip kernel (csrc/fgp_cluster.cu, used by
- * psb_proxskip_denoise_run for 256x256 fp32-FGP problems) fit on the device. */
+ * 256x256 ProxSkip kernel (csrc/fgp_cluster.cu: fp64 outer state and small
+ * batches; fp32 batches run on the 8-CTA kernel, csrc/fgp_cluster8.cu) fit
+ * on the device. */
 int psb_cluster_max_active(int* out);
 
 /* psb_queue_stats: work-queue statistics of the last cluster-path run

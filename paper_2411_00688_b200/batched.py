@@ -6,9 +6,10 @@ The reference has no batch API: config 4 is 4096 independent
 one set of device buffers -- x, h, b, z: (N, H, W); dual slots (N, 3, 2, H, W).
 For 256 x 256 problems with an fp32 FGP (config 4) one native call runs the
 whole K-iteration segment of every problem in ONE launch of the cluster run
-kernel (csrc/fgp_cluster.cu: a 16-CTA cluster takes one problem at a time and
-executes all of its coin-fired prox calls back to back, FGP state in
-registers) plus the SM-worker kernel on the SMs the clusters leave
+kernel (csrc/fgp_cluster8.cu: an 8-CTA cluster takes one problem at a time
+and executes all of its coin-fired prox calls back to back, FGP state in
+registers and tensor memory; fp64 outer state: the 16-CTA form,
+csrc/fgp_cluster.cu) plus the SM-worker kernel on the SMs the clusters leave
 (csrc/fgp2d.cu), both claiming problems from one device work queue.  Other
 shapes / precisions advance all problems together per outer iteration: one
 fused pre kernel over the batch, the FGP inner iterations over the compacted
@@ -17,7 +18,8 @@ Per-problem semantics (own Philox coin stream, warm starts, last_weight
 re-projection, inner-iteration counters) equal N separate reference runs;
 tests/test_gpu_fullsize.py checks 32 config-4 problems at the full 300 x 50
 schedule against fixtures produced by the reference.  Multi-GPU: problems are
-sharded across ranks with no collective (``shard_indices``).
+sharded across ranks with no collective (``shard_balanced`` by known work,
+``shard_indices`` contiguous).
 """
 
 from __future__ import annotations

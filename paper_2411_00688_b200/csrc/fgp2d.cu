@@ -490,17 +490,18 @@ __global__ void __launch_bounds__(TB_THREADS, 1) fgp2d_tb_kernel(TbArgs a) {
 
 // ---- SM-resident ProxSkip worker (config 4, the SMs the clusters leave) ----
 //
-// The 16-CTA clusters of fgp_cluster.cu fit only 7 times on a B200 (one per
-// GPC with >= 16 free SMs); the remaining SMs run this kernel concurrently,
+// The clusters of the run kernels do not tile the whole device (8-CTA
+// clusters: 15 x 8 = 120 of 148 SMs; 16-CTA clusters: 7 x 16 = 112 -- a
+// cluster needs its SMs in one GPC); the remaining SMs run this kernel concurrently,
 // one 512-thread CTA per SM, each working through its own list of whole
 // problems: for every coin-fired iteration of a problem the CTA runs the skip
 // chain + prox input, the n_inner FGP iterations (the streaming item above
 // with L2-coherent loads and a CTA barrier between iterations: the problem's
 // ~2 MB working set stays L2-resident), finalize + control variate, then the
 // trailing skips.  Same arithmetic as the streaming driver (proxskip_pre /
-// fgp2d_iter / fgp2d_finalize / proxskip_post).  The host splits the problems
-// between clusters and these workers by a static cost model, so which kernel
-// runs a problem does not depend on timing.
+// fgp2d_iter / fgp2d_finalize / proxskip_post).  Clusters and workers claim
+// problems from one device work queue (common.cuh); the kernels are
+// bit-identical, so which one runs a problem never changes a result.
 struct SmRunArgs {
   float* x;
   const float* b;
