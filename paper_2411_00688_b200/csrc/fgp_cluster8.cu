@@ -441,9 +441,12 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       // One inner iteration: y from (q_k registers, q_{k-1} shared memory),
       // q_k -> shared memory (the next q_{k-1}), the new iterate -> q_k
       // registers.  ROLE (warp-uniform): 0 top / 1 middle / 2 bottom group.
-      auto run_inner = [&](auto role_tag) {
-        constexpr int ROLE = decltype(role_tag)::value;
-        constexpr bool TOP = ROLE == 0, BOT = ROLE == 2;
+      auto run_inner = [&](auto rg_tag) {
+        // one copy per row group: the group index is a compile-time constant,
+        // so every shared-memory exchange address below is the CTA's window
+        // base plus an immediate
+        constexpr int RG = decltype(rg_tag)::value;
+        constexpr bool TOP = RG == 0, BOT = RG == CRG - 1;
         // the loop-carried iterate as 64-bit register pairs (P2), so the values
         // cross the back-edge as pairs and need no re-pairing moves
         P2 QY[2][NP], QX[2][NP];
@@ -528,14 +531,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             old_e[0] = phi(QY[0][NP - 1]), old_e[1] = phi(QY[1][NP - 1]);
           }
           if constexpr (!BOT) {  // last-row y_y for the group below
-            *reinterpret_cast<float2*>(&s_rg_yy[rg][j0]) = make_float2(phi(yy[0][NP - 1]), phi(yy[1][NP - 1]));
-            mbar_arrive(&gYY[rg]);
+            *reinterpret_cast<float2*>(&s_rg_yy[RG][j0]) = make_float2(phi(yy[0][NP - 1]), phi(yy[1][NP - 1]));
+            mbar_arrive(&gYY[RG]);
           }
           if (lane == 31) {
 #pragma unroll
-            for (int P = 0; P < NP; ++P) s_edge_yx[rg][P][wc + 1] = yx[1][P];
+            for (int P = 0; P < NP; ++P) s_edge_yx[RG][P][wc + 1] = yx[1][P];
           }
-          mbar_arrive(&gE1[rg]);
+          mbar_arrive(&gE1[RG]);
           float2 yyA = make_float2(0.f, 0.f);  // TOP: y row above (zeros at row 0)
           float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
           if constexpr (TOP) {
@@ -560,7 +563,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               }
             }
           }
-          GWAIT(&gE1[rg], ph);
+          GWAIT(&gE1[RG], ph);
 #if PSB_C8_TMEM
           tm_wait_ld(zw);  // z
 #endif
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
                          __shfl_up_sync(0xffffffffu, phi(yx[1][P]), 1));
           if (lane == 0) {
 #pragma unroll
-            for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[rg][P][wc];
+            for (int P = 0; P < NP; ++P) left[P] = s_edge_yx[RG][P][wc];
           }
           float yy_above[2] = {yyA.x, yyA.y};
           P2 u[2][NP];
@@ -600,8 +603,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             for (int P = 1; P < NP; ++P) u_pairs(P);
           }
           if constexpr (!TOP) {
-            GWAIT(&gYY[rg - 1], ph);
-            const float2 ya2 = *reinterpret_cast<const float2*>(&s_rg_yy[rg - 1][j0]);
+            GWAIT(&gYY[RG - 1], ph);
+            const float2 ya2 = *reinterpret_cast<const float2*>(&s_rg_yy[RG - 1][j0]);
             yy_above[0] = ya2.x;
             yy_above[1] = ya2.y;
           }
@@ -634,15 +637,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             }
           }
           if constexpr (!TOP) {  // first-row u for the group above
-            *reinterpret_cast<float2*>(&s_rg_u[rg][j0]) = make_float2(plo(u[0][0]), plo(u[1][0]));
-            mbar_arrive(&gU[rg]);
+            *reinterpret_cast<float2*>(&s_rg_u[RG][j0]) = make_float2(plo(u[0][0]), plo(u[1][0]));
+            mbar_arrive(&gU[RG]);
           }
           if (lane == 0) {
 #pragma unroll
-            for (int P = 0; P < NP; ++P) s_edge_u[rg][P][wc] = u[0][P];
+            for (int P = 0; P < NP; ++P) s_edge_u[RG][P][wc] = u[0][P];
           }
-          mbar_arrive(&gE2[rg]);
-          GWAIT(&gE2[rg], ph);
+          mbar_arrive(&gE2[RG]);
+          GWAIT(&gE2[RG], ph);
           // right neighbour of column 1: shuffles (lane 31 keeps its own column 1
           // at the global last column: gx = 0), the warp to the right's first
           // column from shared memory
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
                           __shfl_down_sync(0xffffffffu, phi(u[0][P]), 1));
           if (right_fetch) {
 #pragma unroll
-            for (int P = 0; P < NP; ++P) right[P] = s_edge_u[rg][P][wc + 1];
+            for (int P = 0; P < NP; ++P) right[P] = s_edge_u[RG][P][wc + 1];
           }
           if (last_col) {
 #pragma unroll
@@ -691,8 +694,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               q_pair(0, P);
               q_pair(1, P);
             }
-            GWAIT(&gU[rg + 1], ph);
-            const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+            GWAIT(&gU[RG + 1], ph);
+            const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[RG + 1][j0]);
             u_below[0] = ub.x;
             u_below[1] = ub.y;
             q_pair(0, NP - 1);
@@ -719,8 +722,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               q_pair(0, P);
               q_pair(1, P);
             }
-            GWAIT(&gU[rg + 1], ph);
-            const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[rg + 1][j0]);
+            GWAIT(&gU[RG + 1], ph);
+            const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[RG + 1][j0]);
             u_below[0] = ub.x;
             u_below[1] = ub.y;
             q_pair(0, NP - 1);
@@ -743,12 +746,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           }
       };
       PHASE_MARK(ph_b);
-      if (rg_top)
+      if (rg == 0)
         run_inner(std::integral_constant<int, 0>{});
-      else if (rg_bot)
+      else if (rg == 1)
+        run_inner(std::integral_constant<int, 1>{});
+      else if (rg == 2)
         run_inner(std::integral_constant<int, 2>{});
       else
-        run_inner(std::integral_constant<int, 1>{});
+        run_inner(std::integral_constant<int, 3>{});
+      static_assert(CRG == 4, "one inner-loop copy per row group");
 
       PHASE_MARK(ph_c);
       // ---- epilogue: finalize u = clamp(z + div q_n) + ProxSkip post -----------
