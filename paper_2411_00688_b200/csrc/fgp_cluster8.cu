@@ -151,7 +151,11 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   const int tid = threadIdx.x;
   const int jt = tid % CTPR, rg = tid / CTPR;  // column pair, row group
   const int j0 = 2 * jt;                        // columns j0, j0 + 1
-  const int lane = tid & 31, wc = jt >> 5;
+  // the warp index broadcast from lane 0: the compiler then knows it is
+  // warp-uniform and keeps what derives from it (tensor-memory addresses,
+  // warp-edge slots) on the uniform datapath
+  const int warp_u = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int lane = tid & 31, wc = warp_u & (CWARPS_ROW - 1);
   const int row0 = cr * SR + rg * CRPT;
   const bool rg_top = rg == 0, rg_bot = rg == CRG - 1;
   const bool has_up = cr > 0, has_dn = cr < CCL - 1;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   // this thread's 128 columns of its lane (bits 31:16 lane, 15:0 column)
-  const uint32_t tm = s_tm_base + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) + (uint32_t)((tid >> 7) * 128);
+  const uint32_t tm = s_tm_base + ((uint32_t)((warp_u & 3) * 32) << 16) + (uint32_t)((warp_u >> 2) * 128);
 #endif
   // every CTA of this grid is resident: the SM-worker kernel (a programmatic
   // dependent) may now be placed on the SMs the clusters left
