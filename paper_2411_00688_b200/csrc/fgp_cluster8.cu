@@ -133,6 +133,29 @@ __device__ __forceinline__ P2 p2_join(uint32_t lo, uint32_t hi) {
 // pair as it is, two 16-word loads); [32,48) z: words 4 P + 2 k + {0,1}
 constexpr uint32_t kTmQ = 0, kTmZ = 32;
 
+// row-group mbarriers addressed as one base register + immediate byte offset
+template <int OFF>
+__device__ __forceinline__ void gb_arrive(uint32_t base) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0+%1];\n" ::"r"(base), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void gb_wait(uint32_t base, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0+%1], %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(base),
+      "n"(OFF), "r"(parity)
+      : "memory");
+}
+#ifdef PSB_DBG_NOGSYNC
+#define GBWAIT(off, ph) ((void)0)
+#else
+#define GBWAIT(off, ph) gb_wait<(off)>(gb, ph)
+#endif
+
 // row t of a column strip held as pairs (t, t + NP)
 __device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
   return t < NP ? v[t].x : v[t - NP].y;
@@ -168,7 +191,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   __shared__ __align__(16) float rx_z[CW];  // CTA below's first row of z, once per prox call
   __shared__ __align__(8) uint64_t mb_z;
   // row-group mbarriers, one phase per inner iteration (see fgp_cluster.cu)
-  __shared__ __align__(8) uint64_t gE1[CRG], gE2[CRG], gYY[CRG], gU[CRG];
+  // (one array: every barrier is the base register plus an immediate)
+  __shared__ __align__(8) uint64_t gbar[4 * CRG];
+  constexpr int kE1 = 0, kE2 = CRG, kYY = 2 * CRG, kU = 3 * CRG;  // + row group
   __shared__ __align__(8) float s_rg_yy[CRG][CW];  // each row group's last-row y_y
   __shared__ __align__(8) float s_rg_u[CRG][CW];   // each row group's first-row u
   // warp-edge columns as row pairs: s_edge_yx[rg][P][w + 1] = last column of
@@ -209,10 +234,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
     mbar_init(&mb_up[1], 1);
     mbar_init(&mb_z, 1);
     for (int gi = 0; gi < CRG; ++gi) {
-      mbar_init(&gE1[gi], CTPR);
-      mbar_init(&gE2[gi], CTPR);
-      mbar_init(&gYY[gi], CTPR);
-      mbar_init(&gU[gi], CTPR);
+      mbar_init(&gbar[kE1 + gi], CTPR);
+      mbar_init(&gbar[kE2 + gi], CTPR);
+      mbar_init(&gbar[kYY + gi], CTPR);
+      mbar_init(&gbar[kU + gi], CTPR);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -240,6 +265,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   const uint32_t dn_mb_remote = dsmem_addr(&mb_up[0], has_dn ? cr + 1 : cr);
   const uint32_t z_rx_remote = dsmem_addr(&rx_z[0], has_up ? cr - 1 : cr);
   const uint32_t z_mb_remote = dsmem_addr(&mb_z, has_up ? cr - 1 : cr);
+  const uint32_t gb = smem_u32(&gbar[0]);
   unsigned zph = 0;    // prox calls so far (mb_z phases)
   unsigned round = 0;  // halo rounds so far (round r lands in buffer r & 1)
   unsigned gph = 0;    // inner iterations so far (row-group mbarrier phases)
@@ -536,13 +562,13 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           }
           if constexpr (!BOT) {  // last-row y_y for the group below
             *reinterpret_cast<float2*>(&s_rg_yy[RG][j0]) = make_float2(phi(yy[0][NP - 1]), phi(yy[1][NP - 1]));
-            mbar_arrive(&gYY[RG]);
+            gb_arrive<8 * (kYY + RG)>(gb);
           }
           if (lane == 31) {
 #pragma unroll
             for (int P = 0; P < NP; ++P) s_edge_yx[RG][P][wc + 1] = yx[1][P];
           }
-          mbar_arrive(&gE1[RG]);
+          gb_arrive<8 * (kE1 + RG)>(gb);
           float2 yyA = make_float2(0.f, 0.f);  // TOP: y row above (zeros at row 0)
           float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
           if constexpr (TOP) {
@@ -567,7 +593,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               }
             }
           }
-          GWAIT(&gE1[RG], ph);
+          GBWAIT(8 * (kE1 + RG), ph);
 #if PSB_C8_TMEM
           tm_wait_ld(zw);  // z
 #endif
@@ -607,7 +633,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             for (int P = 1; P < NP; ++P) u_pairs(P);
           }
           if constexpr (!TOP) {
-            GWAIT(&gYY[RG - 1], ph);
+            GBWAIT(8 * (kYY + RG - 1), ph);
             const float2 ya2 = *reinterpret_cast<const float2*>(&s_rg_yy[RG - 1][j0]);
             yy_above[0] = ya2.x;
             yy_above[1] = ya2.y;
@@ -642,14 +668,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           }
           if constexpr (!TOP) {  // first-row u for the group above
             *reinterpret_cast<float2*>(&s_rg_u[RG][j0]) = make_float2(plo(u[0][0]), plo(u[1][0]));
-            mbar_arrive(&gU[RG]);
+            gb_arrive<8 * (kU + RG)>(gb);
           }
           if (lane == 0) {
 #pragma unroll
             for (int P = 0; P < NP; ++P) s_edge_u[RG][P][wc] = u[0][P];
           }
-          mbar_arrive(&gE2[RG]);
-          GWAIT(&gE2[RG], ph);
+          gb_arrive<8 * (kE2 + RG)>(gb);
+          GBWAIT(8 * (kE2 + RG), ph);
           // right neighbour of column 1: shuffles (lane 31 keeps its own column 1
           // at the global last column: gx = 0), the warp to the right's first
           // column from shared memory
@@ -662,9 +688,9 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
 #pragma unroll
             for (int P = 0; P < NP; ++P) right[P] = s_edge_u[RG][P][wc + 1];
           }
-          if (last_col) {
+          if (wc == CWARPS_ROW - 1) {  // (warp-uniform: only the last warp column pays the selects)
 #pragma unroll
-            for (int P = 0; P < NP; ++P) right[P] = u[1][P];
+            for (int P = 0; P < NP; ++P) right[P] = lane == 31 ? u[1][P] : right[P];
           }
           auto q_pair = [&](int k, int P) {
             const P2 bl2 = P == NP - 1 ? pk(phi(u[k][0]), u_below[k]) : u[k][P < NP - 1 ? P + 1 : 0];
@@ -698,7 +724,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               q_pair(0, P);
               q_pair(1, P);
             }
-            GWAIT(&gU[RG + 1], ph);
+            GBWAIT(8 * (kU + RG + 1), ph);
             const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[RG + 1][j0]);
             u_below[0] = ub.x;
             u_below[1] = ub.y;
@@ -726,7 +752,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               q_pair(0, P);
               q_pair(1, P);
             }
-            GWAIT(&gU[RG + 1], ph);
+            GBWAIT(8 * (kU + RG + 1), ph);
             const float2 ub = *reinterpret_cast<const float2*>(&s_rg_u[RG + 1][j0]);
             u_below[0] = ub.x;
             u_below[1] = ub.y;
