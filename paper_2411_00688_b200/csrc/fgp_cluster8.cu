@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           float ex_y[2] = {0.f, 0.f}, ex_x[2] = {0.f, 0.f}, ledge_x = 0.f;  // BOT: row below
           if constexpr (TOP) {
             if (has_up) {
-              const bool warm = reuse && it == 0;  // (already received: final round)
+              const bool warm = FIRST && reuse;  // (already received: the previous call's final round)
               const unsigned par = warm ? (round0 & 1u) : recv_up(round0 + it);
               yyA = *reinterpret_cast<const float2*>(&rx_up[par][j0]);
               if (warm) yyA = make_float2(y0_of(yyA.x), y0_of(yyA.y));
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           }
           if constexpr (BOT) {
             if (has_dn) {
-              const bool warm = reuse && it == 0;
+              const bool warm = FIRST && reuse;
               const unsigned par = warm ? (round0 & 1u) : recv_dn(round0 + it);
               const float4 v = *reinterpret_cast<const float4*>(&rx_dn[par][j0][0]);
               ex_y[0] = v.x, ex_x[0] = v.y, ex_y[1] = v.z, ex_x[1] = v.w;
