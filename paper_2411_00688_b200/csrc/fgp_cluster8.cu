@@ -11,15 +11,14 @@
 // 16 pixels per thread do not fit the register file with z, q_k and q_{k-1}
 // all resident (80 state registers + temporaries > 128), so only q_k lives in
 // registers: the prox input z and the previous dual iterate q_{k-1} are
-// thread-private float4 columns in shared memory ([slot][tid]: conflict-free
-// LDS / STS), read once and written once per inner iteration
-// (20 B/px: ~1280 shared-memory cycles per 8192-px iteration, under the
-// ~1000 issue cycles it overlaps with).  What this buys over the 16-CTA form:
-// every synchronisation of the inner loop (warp-edge columns, row-group rows,
-// the DSMEM halo round trip) is paid once per 16 pixels of a thread instead
-// of once per 8, eight independent pair chains per thread instead of four,
-// and 8-CTA clusters tile the GPCs without leaving a quarter of the SMs to
-// the slower one-SM workers.
+// thread-private columns of the SM's TENSOR MEMORY (tcgen05.ld / .st, below),
+// read once and written once per inner iteration.  What this buys over the
+// 16-CTA form: every synchronisation of the inner loop (warp-edge columns,
+// row-group rows, the DSMEM halo round trip) is paid once per 16 pixels of a
+// thread instead of once per 8, eight independent pair chains per thread
+// instead of four, and 8-CTA clusters tile 120 of the 148 SMs (16-CTA: 112).
+// The inner loop is compiled once per row group (exchange addresses become
+// immediates) on 64-bit register pairs (P2, cluster_ptx.cuh).
 //
 // Every pixel's arithmetic is the scalar FGP step of the other kernels
 // (each f32x2 lane an IEEE fp32 op), so results are bit-identical to
@@ -80,9 +79,6 @@ struct Run8Args {
 // registers, on a datapath of its own (measured, tools/micro/tmem_bw.cu:
 // 247 B/cycle/SM loads against 128 B/cycle/SM for shared memory, and the
 // shared-memory pipe stays free for the shuffles and the edge exchange).
-#ifndef PSB_C8_TMEM
-#define PSB_C8_TMEM 1
-#endif
 // wait::ld names the loaded registers as in/out operands: their consumers must
 // not be scheduled above the wait (a volatile asm orders only other volatile
 // asms and memory accesses, not register arithmetic)
@@ -162,9 +158,7 @@ __device__ __forceinline__ float& rowref(float2 (&v)[NP], int t) {
 }
 
 constexpr size_t kStageBytes = (size_t)3 * SR * CW * sizeof(float);           // x, b, h rows
-constexpr size_t kQmBytes = (size_t)2 * NP * CTHREADS * sizeof(float4);       // q_{k-1}
-constexpr size_t kZBytes = (size_t)NP * CTHREADS * sizeof(float4);            // z
-constexpr size_t kDynBytes = PSB_C8_TMEM ? kStageBytes : kStageBytes + kQmBytes + kZBytes;
+constexpr size_t kDynBytes = kStageBytes;
 
 template <bool NONNEG>
 __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args a) {
@@ -212,15 +206,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   float* sx = reinterpret_cast<float*>(dyn_raw);  // [SR][CW]
   float* sb = sx + SR * CW;
   float* sh = sb + SR * CW;
-  // thread-private columns: s_qmy / s_qmx[k * NP + P][tid] = the row pair P of
-  // column k of q_{k-1} (float2 slots: the packed results go straight from
-  // their register pairs to STS.64, no quad assembly);
-  // s_z[P][tid] = (z col 0 pair P, z col 1 pair P)
-#if !PSB_C8_TMEM
-  P2* s_qmy = reinterpret_cast<P2*>(dyn_raw + kStageBytes);
-  P2* s_qmx = s_qmy + 2 * NP * CTHREADS;
-  ulonglong2* s_z = reinterpret_cast<ulonglong2*>(dyn_raw + kStageBytes + kQmBytes);
-#endif
 
   const float g = a.gamma;
   const float w = a.weight;
@@ -241,7 +226,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-#if PSB_C8_TMEM
   if (tid < 32) {  // warp 0 takes the SM's whole tensor memory (one CTA per SM)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
         smem_u32(&s_tm_base)));
@@ -252,7 +236,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   // this thread's 128 columns of its lane (bits 31:16 lane, 15:0 column)
   const uint32_t tm = s_tm_base + ((uint32_t)((warp_u & 3) * 32) << 16) + (uint32_t)((warp_u >> 2) * 128);
-#endif
   // every CTA of this grid is resident: the SM-worker kernel (a programmatic
   // dependent) may now be placed on the SMs the clusters left
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -433,7 +416,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
               rowref(qkx[k], t) = vx;
             }
         }
-#if PSB_C8_TMEM
         {
           uint32_t zw[16];
 #pragma unroll
@@ -444,11 +426,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           tm_st16(tm + kTmZ, zw);
           tm_wait_st();
         }
-#else
-#pragma unroll
-        for (int P = 0; P < NP; ++P)
-          s_z[P * CTHREADS + tid] = make_ulonglong2(pk(z[0][P].x, z[0][P].y), pk(z[1][P].x, z[1][P].y));
-#endif
       }
       float z_ex[2] = {0.f, 0.f};  // the CTA-below's first row of z (bottom group, first iteration)
       const unsigned zpar = zph & 1u;
@@ -468,9 +445,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
         ++round;
       }
 
-      // One inner iteration: y from (q_k registers, q_{k-1} shared memory),
-      // q_k -> shared memory (the next q_{k-1}), the new iterate -> q_k
-      // registers.  ROLE (warp-uniform): 0 top / 1 middle / 2 bottom group.
+      // One inner iteration: y from (q_k registers, q_{k-1} tensor memory),
+      // q_k -> tensor memory (the next q_{k-1}), the new iterate -> q_k
+      // registers.  Row group 0 is the top group (halo from the CTA above),
+      // CRG - 1 the bottom group, the others carry no halo code.
       auto run_inner = [&](auto rg_tag) {
         // one copy per row group: the group index is a compile-time constant,
         // so every shared-memory exchange address below is the CTA's window
@@ -496,7 +474,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           const float beta = (a.accelerated && it > 0) ? s_beta[it - 1] : 0.f;
           const P2 b2 = pk(beta, beta);
           P2 yy[2][NP], yx[2][NP];
-#if PSB_C8_TMEM
           // q_{k-1} from tensor memory (two 16-word loads), y, then q_k goes
           // where q_{k-1} was (the previous iteration's stores have landed:
           // wait::st below, before this load)
@@ -531,28 +508,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           }
           uint32_t zw[16];
           tm_ld16(tm + kTmZ, zw);  // (waited for before the first u below)
-#else
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int P = 0; P < NP; ++P) {
-              P2 my = QY[k][P], mx = QX[k][P];  // (the momentum restarts with every call)
-              if constexpr (!FIRST) {
-                my = s_qmy[(k * NP + P) * CTHREADS + tid];
-                mx = s_qmx[(k * NP + P) * CTHREADS + tid];
-              }
-              yy[k][P] = pfma(b2, pfma(my, m1, QY[k][P]), QY[k][P]);
-              yx[k][P] = pfma(b2, pfma(mx, m1, QX[k][P]), QX[k][P]);
-            }
-          // q_k becomes q_{k-1} (its halo entries for the y pushed below are kept)
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int P = 0; P < NP; ++P) {
-              s_qmy[(k * NP + P) * CTHREADS + tid] = QY[k][P];
-              s_qmx[(k * NP + P) * CTHREADS + tid] = QX[k][P];
-            }
-#endif
           float old_e[4];
           if constexpr (TOP) {
             old_e[0] = plo(QY[0][0]), old_e[1] = plo(QX[0][0]), old_e[2] = plo(QY[1][0]), old_e[3] = plo(QX[1][0]);
@@ -594,9 +549,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             }
           }
           GBWAIT(8 * (kE1 + RG), ph);
-#if PSB_C8_TMEM
           tm_wait_ld(zw);  // z
-#endif
           // left neighbours of column 0: shuffles inside the warp, the warp to
           // the left's last column from shared memory (zeros left of column 0)
           P2 left[NP];
@@ -612,12 +565,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
           P2 u[2][NP];
           // ((0 + yy) - yy_up) + yx - yx_left, boundary terms zero-padded; u = z + d
           auto u_pairs = [&](int P) {  // both columns of pair P
-#if PSB_C8_TMEM
             const ulonglong2 zv = make_ulonglong2(p2_join(zw[4 * P], zw[4 * P + 1]),
                                                   p2_join(zw[4 * P + 2], zw[4 * P + 3]));
-#else
-            const ulonglong2 zv = s_z[P * CTHREADS + tid];
-#endif
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const P2 ab2 = P == 0 ? pk(yy_above[k], plo(yy[k][NP - 1])) : yy[k][P > 0 ? P - 1 : 0];
@@ -759,9 +708,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
             q_pair(0, NP - 1);
             q_pair(1, NP - 1);
           }
-#if PSB_C8_TMEM
           tm_wait_st();  // q_{k-1} is in place for the next iteration's load
-#endif
           ++round;
           ++gph;
         };
@@ -797,10 +744,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
 #pragma unroll
         for (int P = 0; P < NP; ++P) s_fin_edge[rg][P][wc + 1] = pk(qkx[1][P].x, qkx[1][P].y);
       }
-#if PSB_C8_TMEM
       uint32_t zw[16];
       tm_ld16(tm + kTmZ, zw);
-#endif
       float yy_above[2] = {0.f, 0.f};
       {
         const unsigned r = round0 + a.n_inner;
@@ -841,21 +786,12 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
       }
       bool ok = true;
       float2 zf[2][NP];
-#if PSB_C8_TMEM
       tm_wait_ld(zw);
 #pragma unroll
       for (int P = 0; P < NP; ++P) {
         zf[0][P] = make_float2(__uint_as_float(zw[4 * P]), __uint_as_float(zw[4 * P + 1]));
         zf[1][P] = make_float2(__uint_as_float(zw[4 * P + 2]), __uint_as_float(zw[4 * P + 3]));
       }
-#else
-#pragma unroll
-      for (int P = 0; P < NP; ++P) {
-        const ulonglong2 zv = s_z[P * CTHREADS + tid];
-        zf[0][P] = make_float2(plo(zv.x), phi(zv.x));
-        zf[1][P] = make_float2(plo(zv.y), phi(zv.y));
-      }
-#endif
 #pragma unroll
       for (int t = 0; t < CRPT; ++t) {
         const int sj = (rg * CRPT + t) * CW + j0;
@@ -916,9 +852,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) fgp_cluster8_run_kernel(Run8Args 
   }  // problems
   cluster_arrive();  // no CTA leaves while a neighbour may still push into it
   cluster_wait();
-#if PSB_C8_TMEM
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_tm_base));
-#endif
   // launched as a programmatic dependent of the 16-CTA cluster kernel (mixed
   // run): this grid completes only after that one (a no-op otherwise)
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
