@@ -135,3 +135,42 @@ def test_device_loggable_rules():
     assert not device_loggable(IterationLog(reference=ref, callback=lambda r, x: None))
     assert not device_loggable(IterationLog(reference=ref, transform=lambda x: x))
     assert not device_loggable(IterationLog(objective_fn=lambda u: 0.0))
+
+
+def test_cluster8_inner_loop_sass_budget():
+    """Regression guard for the config-4 kernel's code generation.  ptxas'
+    register allocation of fgp_cluster8_run_kernel's inner loop is fragile:
+    unrelated edits elsewhere in the kernel have taken it from ~14-27 to
+    46-90 register moves per iteration (10-25 % slower, DESIGN.md 'Tried and
+    reverted').  The four per-row-group copies of the loop (16 MUFU.RSQ each)
+    must stay within their instruction budget."""
+    import re
+    import shutil
+    import subprocess
+    lib = os.path.join(ROOT, "paper_2411_00688_b200", "libpsb200.so")
+    if shutil.which("cuobjdump") is None or not os.path.exists(lib):
+        pytest.skip("needs cuobjdump and the built library")
+    sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
+    funcs = [f for f in re.split(r"\n\s*Function : ", sass)[1:]
+             if "fgp_cluster8_run_kernel" in f.split("\n")[0]]
+    assert len(funcs) == 2  # nonneg on / off
+    for f in funcs:
+        ins = []
+        for line in f.split("\n"):
+            m = re.search(r"/\*([0-9a-f]{4,5})\*/\s+(.*?);", line)
+            if m:
+                ins.append((int(m.group(1), 16), m.group(2).strip()))
+        at = {a: i for i, (a, _) in enumerate(ins)}
+        loops = []
+        for i, (a, t) in enumerate(ins):
+            m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\d,\s*)?(?:P\d,\s*)?(0x[0-9a-f]+)", t)
+            if m and int(m.group(1), 16) < a and int(m.group(1), 16) in at:
+                body = [x for _, x in ins[at[int(m.group(1), 16)]:i + 1]]
+                if len(body) < 600 and sum("MUFU.RSQ" in x for x in body) == 16:
+                    movs = sum(1 for x in body if re.match(r"(@!?U?P\d\s+)?(MOV|IMAD\.MOV)", x))
+                    loops.append((len(body), movs))
+        assert len(loops) == 4, loops          # one copy per row group
+        # 280 + 335 + 338 + 280 = 1233 (308 + 352 + 372 + 308 = 1340 with the nonneg clamp)
+        budget = 1400 if "ILb1E" in f.split("\n")[0] else 1300
+        assert sum(n for n, _ in loops) <= budget, loops
+        assert max(m for _, m in loops) <= 40, loops
