@@ -433,6 +433,12 @@ def run_config4(args, D, dev):
 
     # ---- e2e: the public API with host buffers, copies inside the region ----
     del solver
+    # one untimed full-size call first: on a fresh box the first full-size calls
+    # pay the 10 GB device allocation (0.1-0.2 s) and run 5-15 % slow for a few
+    # calls; short calls get two such warm-up calls
+    for _ in range(2 if args.steps + args.warmup <= 60 else 1):
+        psb.run_proxskip_batched(b_pin, ALPHA, P, idx, args.warmup + args.steps, INNER,
+                                 precision="fp32", out=x_pin)
     e2e_samples = []
     n_reps = E2E_REPS
     if D.world == 1:  # (ranks must agree on the call count: fixed under torchrun)
