@@ -46,7 +46,7 @@ ALPHA = 0.1
 P = 0.1
 INNER = 50
 RESIDENT_REPS = 3   # timed resident segments (median)
-E2E_REPS = 5        # at least; short calls repeat up to E2E_MAX_REPS within E2E_BUDGET_S
+E2E_REPS = 7        # at least; short calls repeat up to E2E_MAX_REPS within E2E_BUDGET_S
 E2E_MAX_REPS = 15   # (host stalls under the nvidia-smi sampler come in bursts of several calls)
 E2E_BUDGET_S = 1.5
 RUN_LEN = 300
