@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <chrono>
 
 #include "common.cuh"
 
@@ -124,6 +125,15 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   PSB_REQUIRE(H >= 2 && W >= 2, "grad_forward: need a 2-D grid with both sides >= 2");
   PSB_REQUIRE(n >= 1 && n <= 65535, "proxskip run: batch size out of range");
   if (K <= 0) return PSB_OK;
+  // PSB_DEBUG_HOST=1: host microseconds of this call's phases on stderr
+  const char* dbg_host = std::getenv("PSB_DEBUG_HOST");
+  const bool dbg_h = dbg_host && dbg_host[0] == '1';
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double th0 = dbg_h ? now_us() : 0.0;
+  double th1 = 0, th2 = 0, th3 = 0, th4 = 0;
   const int64_t HW = (int64_t)H * W;
   const int64_t qps = 6 * HW;
   // skip.py:64,70,74 -- scalars formed in double exactly as the reference does
@@ -138,19 +148,32 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
   std::vector<int64_t> off(K + 1, 0);
   std::vector<uint8_t> seen(n, 0);
   act.reserve((size_t)(K * n * p * 1.2) + 16);
-  for (int k = 0; k < K; ++k) {
-    for (int64_t i = 0; i < n; ++i) {
-      if (!coins_host[(int64_t)k * n + i]) continue;
-      act.push_back((int32_t)i);
-      const double lw = last_weight[i];
-      uint8_t r = 0;
-      if (!seen[i]) {
-        r = (!std::isnan(lw) && lw != weight) ? 1 : 0;
-        seen[i] = 1;
-      }
-      rep.push_back(r);
-      prox_count[i] += 1;
+  rep.reserve((size_t)(K * n * p * 1.2) + 16);
+  auto fired = [&](int64_t i) {
+    act.push_back((int32_t)i);
+    const double lw = last_weight[i];
+    uint8_t r = 0;
+    if (!seen[i]) {
+      r = (!std::isnan(lw) && lw != weight) ? 1 : 0;
+      seen[i] = 1;
     }
+    rep.push_back(r);
+    prox_count[i] += 1;
+  };
+  for (int k = 0; k < K; ++k) {  // (coins are sparse: eight at a time, zero words skipped)
+    const uint8_t* row = coins_host + (int64_t)k * n;
+    int64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w8;
+      std::memcpy(&w8, row + i, 8);
+      while (w8) {  // (little-endian: byte j of the word is coin i + j)
+        const int j = __builtin_ctzll(w8) >> 3;
+        fired(i + j);
+        w8 &= ~(0xFFull << (8 * j));
+      }
+    }
+    for (; i < n; ++i)
+      if (row[i]) fired(i);
     off[k + 1] = (int64_t)act.size();
   }
   for (int64_t i = 0; i < n; ++i)
@@ -158,6 +181,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
 
   std::vector<double> beta(n_inner, 0.0);
   if (accelerated) fista_betas(n_inner, beta.data());
+  if (dbg_h) th1 = now_us();
 
   // Cluster-resident path (csrc/fgp_cluster.cu): 256 x 256 identity-fidelity
   // problems with an fp32 FGP.  Skipped iterations are deferred per problem
@@ -246,13 +270,20 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
       NW = std::max(0, sm_count() - G * ccl - G8 * 8);
     }
     auto cost = [&](int32_t i) { return (float)(ev_off[i + 1] - ev_off[i]) * n_inner + 2.0f; };
-    order.resize(n);
-    for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
-    auto chunk_id = [&](int32_t i) { return cs.ready ? chunk_of[i] : 0; };
-    std::stable_sort(order.begin(), order.end(), [&](int32_t u, int32_t v) {
-      if (chunk_id(u) != chunk_id(v)) return chunk_id(u) < chunk_id(v);
-      return cost(u) > cost(v);
-    });
+    // claim order: by input chunk, then longest first, ties in index order --
+    // a counting sort over (chunk, K - prox calls)
+    {
+      const int nch = cs.ready ? cs.n_chunks : 1;
+      std::vector<int32_t> start((size_t)nch * (K + 1) + 1, 0);
+      auto bucket = [&](int64_t i) {
+        const int c = cs.ready ? chunk_of[i] : 0;
+        return (size_t)c * (K + 1) + (size_t)(K - (ev_off[i + 1] - ev_off[i]));
+      };
+      for (int64_t i = 0; i < n; ++i) start[bucket(i) + 1] += 1;
+      for (size_t bkt = 1; bkt < start.size(); ++bkt) start[bkt] += start[bkt - 1];
+      order.resize(n);
+      for (int64_t i = 0; i < n; ++i) order[start[bucket(i)]++] = (int32_t)i;
+    }
     qcost.resize(n);
     qsuffix.assign(n + 1, 0.0f);
     for (int64_t i = 0; i < n; ++i) qcost[i] = cost(order[i]);
@@ -289,12 +320,42 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     o_suffix = put(qsuffix.data(), qsuffix.size() * sizeof(float));
   }
   const size_t o_chunkof = chunk_of.empty() ? 0 : put(chunk_of.data(), chunk_of.size() * sizeof(int32_t));
+  if (dbg_h) th2 = now_us();
   DevBuf d_sched;
   d_sched.st = user_stream;
+  keep_pool_cached();
   PSB_CUDA(cudaMallocAsync(&d_sched.p, std::max<size_t>(pack.size(), 16), user_stream));
-  PSB_CUDA(cudaMemcpyAsync(d_sched.p, pack.data(), pack.size(), cudaMemcpyHostToDevice,
-                           user_stream));
-  // (pageable source: cudaMemcpyAsync stages `pack` before it returns)
+  // through a page-locked staging buffer kept across calls (a pageable source
+  // makes cudaMemcpyAsync stage and wait, ~0.2 ms per call); an event guards
+  // its reuse
+  {
+    static std::mutex mu;
+    static void* stage = nullptr;
+    static size_t stage_cap = 0;
+    static cudaEvent_t stage_free = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (stage_free == nullptr) PSB_CUDA(cudaEventCreateWithFlags(&stage_free, cudaEventDisableTiming));
+    else PSB_CUDA(cudaEventSynchronize(stage_free));
+    if (pack.size() > stage_cap) {
+      if (stage) cudaFreeHost(stage);
+      stage = nullptr;
+      stage_cap = 0;
+      const size_t want = std::max<size_t>(2 * pack.size(), (size_t)1 << 20);
+      if (cudaHostAlloc(&stage, want, cudaHostAllocDefault) == cudaSuccess) stage_cap = want;
+      else (void)cudaGetLastError();
+    }
+    cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+    (void)cudaStreamIsCapturing(user_stream, &cap_status);
+    if (stage_cap >= pack.size() && cap_status == cudaStreamCaptureStatusNone) {
+      std::memcpy(stage, pack.data(), pack.size());
+      PSB_CUDA(cudaMemcpyAsync(d_sched.p, stage, pack.size(), cudaMemcpyHostToDevice, user_stream));
+      PSB_CUDA(cudaEventRecord(stage_free, user_stream));
+    } else {
+      // (pageable source: cudaMemcpyAsync stages `pack` before it returns)
+      PSB_CUDA(cudaMemcpyAsync(d_sched.p, pack.data(), pack.size(), cudaMemcpyHostToDevice,
+                               user_stream));
+    }
+  }
   unsigned char* dev = static_cast<unsigned char*>(d_sched.p);
   if (!chunk_of.empty()) cs.chunk_of = reinterpret_cast<const int32_t*>(dev + o_chunkof);
   const uint8_t* coins_d = dev + o_coins;
@@ -317,6 +378,7 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
     xalt = d_xalt.p;
   }
 
+  if (dbg_h) th3 = now_us();
   CapturedRun cap;
   if (int rc0 = cap.begin(user_stream, use_graph != 0)) return rc0;
   cudaStream_t st = cap.st;
@@ -445,6 +507,11 @@ int proxskip_tv_run(const Fidelity& fid, int dto, int dtf, void* x, const void* 
                          act_d + off[k], na, H, W, n_inner, nonneg, gamma, pg, bad, k, st);
   }
 
+  if (dbg_h) {
+    th4 = now_us();
+    fprintf(stderr, "[psb host] active lists %.0f us, schedule %.0f us, pack + copy %.0f us, launches %.0f us\n",
+            th1 - th0, th2 - th1, th3 - th2, th4 - th3);
+  }
   if (x_hist && rc == PSB_OK)
     if (cudaMemcpyAsync(static_cast<char*>(x_hist) + (size_t)(K - 1) * x_bytes, xcur, x_bytes,
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
