@@ -229,6 +229,18 @@ def _chunk_edges(n, chunk):
     return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
 
 
+_COPY_STREAMS = {}
+
+
+def _copy_streams():
+    """The two copy streams of the streamed run, one pair per device (kept
+    across calls: creating a stream costs tens of microseconds)."""
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return _COPY_STREAMS[dev]
+
+
 def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=None):
     tensor_in = isinstance(b, torch.Tensor)
     src = b.detach().contiguous() if tensor_in else torch.from_numpy(np.ascontiguousarray(b))
@@ -248,7 +260,6 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
     # start): no 10 GB of zero-fills inside the call
     solver = BatchedTvDenoise(torch.empty((n, H, W), dtype=torch.float32, device="cuda"), alpha,
                               inner_budget, precision="fp32", cold_buffers=False)
-    coins = coin_table(p, seeds, iters)
     t1 = time.perf_counter() if dbg else 0.0
     edges = _chunk_edges(n, chunk)
     bounds = list(zip(edges[:-1], edges[1:]))
@@ -259,7 +270,7 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
     main = torch.cuda.current_stream()
     start = torch.cuda.Event(enable_timing=dbg)
     start.record(main)  # buffers allocated and zeroed
-    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    h2d, d2h = _copy_streams()
     h2d.wait_event(start)
     d2h.wait_event(start)
     item = H * W * 4
@@ -276,6 +287,8 @@ def _run_streamed(b, alpha, p, seeds, iters, inner_budget, gamma, chunk, out=Non
             for c, (lo, hi) in enumerate(bounds):
                 solver.b[lo:hi].copy_(src[lo:hi])  # float32 H2D: a DMA, no kernel on this stream
                 L.call("psb_stream_write_u32", cs, L.C.c_void_p(ready.data_ptr() + 4 * c), 1)
+    # (the coin streams are drawn while the first chunks are already on their way)
+    coins = coin_table(p, seeds, iters)
     # 2) the run: its kernels wait per problem for the chunk flags above
     L.call("psb_proxskip_denoise_run_streamed", L.dcode(solver.dto), L.dcode(solver.dtf),
            L.ptr(solver.x), L.ptr(solver.b), L.ptr(solver.h), L.ptr(solver.z),
