@@ -425,11 +425,11 @@ def run_config4(args, D, dev):
     active = timed.sum(axis=1)                       # coin-fired problems per step
     n_pxit = float(active.sum()) * INNER * HW
     if CLUSTER:
-        # one fgp_cluster_run_kernel launch for the K timed steps, one
-        # fgp_cluster8_run_kernel launch (the 8-CTA clusters in the GPC space the
-        # 16-CTA clusters cannot use) and one fgp_sm_run_kernel launch on the
-        # SMs both leave
-        launches = 1 + int(units[1] > 0) + int(units[2] > 0)
+        # per timed segment: one fgp_cluster8_run_kernel launch (fp32 batches; the
+        # 16-CTA fgp_cluster_run_kernel only with PSB_CLUSTER8=0 / 2) and one
+        # fgp_sm_run_kernel launch on the SMs the clusters leave -- counted from
+        # the kernels that reported work
+        launches = int(units[0] > 0) + int(units[1] > 0) + int(units[2] > 0)
     else:
         launches = args.steps + int(np.count_nonzero(active)) * (INNER + 1)
     t_job, = D.reduce([t_local], "max")
