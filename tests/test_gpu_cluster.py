@@ -53,6 +53,23 @@ def test_cluster_matches_streaming_and_oracle(graph):
         assert rel(xc[j], xr) < 1e-5
 
 
+def test_cluster8_in_a_captured_graph_matches_stream_launch():
+    """More problems than 16-CTA clusters fit: the batch runs on the 8-CTA
+    tensor-memory kernel; its launch inside a captured CUDA graph gives the
+    stream launch's bits and the streaming kernels' values."""
+    idx = np.arange(20) * 101 % 4096
+    b = _batch(idx)
+    K, inner, p = 30, 9, 0.3
+    xg, cg = _run(b, idx, K, inner, p, stream_only=False, graph=True)
+    xc, cc = _run(b, idx, K, inner, p, stream_only=False, graph=False)
+    xs, cs = _run(b, idx, K, inner, p, stream_only=True)
+    np.testing.assert_array_equal(cg, cc)
+    np.testing.assert_array_equal(cg, cs)
+    np.testing.assert_array_equal(np.asarray(xg), np.asarray(xc))
+    for j in range(len(idx)):
+        assert rel(xg[j], xs[j]) < 2e-6
+
+
 def test_cluster_warm_restart_reprojection_and_state():
     """Two runs on the same solver: the second uses a different p, so the prox
     weight changes and the warm start is re-projected (tv.py:68-69); x and h
