@@ -70,6 +70,43 @@ def test_cluster8_in_a_captured_graph_matches_stream_launch():
         assert rel(xg[j], xs[j]) < 2e-6
 
 
+def test_cluster_kernels_nonneg_instantiation(monkeypatch):
+    """The nonneg = True instantiations (u clamped at 0 inside every FGP
+    iteration and in the finalize, tv.py:77,89): 8-CTA kernel, 16-CTA kernel, SM
+    workers and the streaming kernels agree, and match the oracle with a
+    nonnegativity-constrained TV prox."""
+    from paper_2411_00688_b200 import batched
+    idx = np.arange(20) * 37 % 4096
+    b = _batch(idx).astype(np.float32) - 0.35   # data with negative parts: the clamp is active
+    K, inner, p = 24, 11, 0.3
+    coins = batched.coin_table(p, idx, K)
+    outs = {}
+    for name, env in (("c8", {"PSB_CLUSTER8": "1", "PSB_NO_SMWORK": "1"}),
+                      ("c16", {"PSB_CLUSTER8": "0", "PSB_NO_SMWORK": "1"}),
+                      ("sm", {"PSB_SM_ONLY": "1"}),
+                      ("stream", {"PSB_NO_CLUSTER": "1"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = psb.BatchedTvDenoise(torch.from_numpy(b).cuda(), 0.1, inner, precision="fp32", nonneg=True)
+        s.run_proxskip(coins, 1.0, p)
+        outs[name] = (s.x.clone(), s.prox_count.copy())
+        for k in env:
+            monkeypatch.delenv(k)
+    for name in ("c16", "sm"):
+        assert torch.equal(outs["c8"][0], outs[name][0]), name
+        np.testing.assert_array_equal(outs["c8"][1], outs[name][1])
+    xs = outs["stream"][0].cpu().numpy()
+    xc = outs["c8"][0].cpu().numpy()
+    for j in (0, 7, 19):
+        assert rel(xc[j], xs[j]) < 2e-6
+        pr = oc.make_recon(oc.identity_op(b[j].shape), b[j].astype(np.float64), 0.1,
+                           splitting="implicit", inner=inner, nonneg=True)
+        xr, _, n_prox, _ = oc.proxskip(pr.grad, pr.prox, np.zeros(b[j].shape), None, 1.0 / pr.L, p,
+                                       int(idx[j]), K)
+        assert outs["c8"][1][j] == n_prox
+        assert rel(xc[j], xr) < 1e-5
+
+
 def test_cluster_warm_restart_reprojection_and_state():
     """Two runs on the same solver: the second uses a different p, so the prox
     weight changes and the warm start is re-projected (tv.py:68-69); x and h
