@@ -107,6 +107,35 @@ def test_cluster_kernels_nonneg_instantiation(monkeypatch):
         assert rel(xc[j], xr) < 1e-5
 
 
+def test_cluster_kernels_plain_fgp(monkeypatch):
+    """accelerated = False (the plain projected-gradient inner loop, beta = 0
+    in every iteration, tv.py:79-81): the run kernels agree bit for bit and
+    match the streaming kernels."""
+    from paper_2411_00688_b200 import batched
+    idx = np.arange(18) * 41 % 4096
+    b = _batch(idx).astype(np.float32)
+    K, inner, p = 20, 8, 0.35
+    coins = batched.coin_table(p, idx, K)
+    outs = {}
+    for name, env in (("c8", {"PSB_CLUSTER8": "1", "PSB_NO_SMWORK": "1"}),
+                      ("c16", {"PSB_CLUSTER8": "0", "PSB_NO_SMWORK": "1"}),
+                      ("sm", {"PSB_SM_ONLY": "1"}),
+                      ("stream", {"PSB_NO_CLUSTER": "1"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = psb.BatchedTvDenoise(torch.from_numpy(b).cuda(), 0.1, inner, precision="fp32",
+                                 accelerated=False)
+        s.run_proxskip(coins, 1.0, p)
+        outs[name] = s.x.clone()
+        for k in env:
+            monkeypatch.delenv(k)
+    assert torch.equal(outs["c8"], outs["c16"])
+    assert torch.equal(outs["c8"], outs["sm"])
+    xs, xc = outs["stream"].cpu().numpy(), outs["c8"].cpu().numpy()
+    for j in range(len(idx)):
+        assert rel(xc[j], xs[j]) < 2e-6
+
+
 def test_cluster_warm_restart_reprojection_and_state():
     """Two runs on the same solver: the second uses a different p, so the prox
     weight changes and the warm start is re-projected (tv.py:68-69); x and h
